@@ -1,0 +1,172 @@
+"""Plan cache and evaluator around the C ABI's hs_plan (csrc/plan.cu).
+
+An :class:`Evaluator` owns one device plan for a fixed (kind, geometry, grid,
+rc, n, n_targets) configuration and evaluates it for new strengths/positions.
+Inputs may be NumPy arrays (host; copied by the library on its stream) or
+torch CUDA tensors (device-resident; zero copies).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+import threading
+
+import numpy as np
+
+from . import _lib
+from .errors import ParameterError
+
+TIME_KEYS = ("gridding", "fft", "scale", "ifft", "gather", "real", "fourier", "prep", "total", "io")
+
+
+def _is_torch(a) -> bool:
+    return type(a).__module__.startswith("torch")
+
+
+def _host_f64(a, shape_cols=3):
+    arr = np.ascontiguousarray(np.asarray(a, dtype=np.float64))
+    if arr.ndim != 2 or arr.shape[1] != shape_cols:
+        raise ParameterError(f"expected (n,{shape_cols}) float64 array, got {arr.shape}")
+    return arr
+
+
+class Evaluator:
+    """Device plan for one configuration (grid from a GridSpec-like object)."""
+
+    def __init__(self, kind, geometry, L, xi, rc, grid, n, n_targets, targets_are_sources, device=None):
+        self.ctx = _lib.Context.get(device)
+        self.lib = self.ctx.lib
+        self.kind, self.geometry = kind, geometry
+        self.n, self.n_targets = int(n), int(n_targets)
+        self.targets_are_sources = bool(targets_are_sources)
+        self.grid = grid
+        p = _lib.HsParams()
+        p.kind = _lib.KIND_ID[kind]
+        p.geometry = _lib.GEOM_ID[geometry]
+        p.L = float(L)
+        p.xi = float(xi)
+        p.rc = float(rc)
+        p.M = int(grid.M)
+        p.P = int(grid.P)
+        p.h = float(grid.h)
+        p.eta = float(grid.eta)
+        p.origin = _lib.vec3([float(v) for v in grid.origin])
+        p.dims = _lib.vec3([int(v) for v in grid.dims], C.c_int64)
+        p.padded = _lib.vec3([int(v) for v in grid.padded_dims], C.c_int64)
+        p.n = self.n
+        p.n_targets = self.n_targets
+        p.targets_are_sources = 1 if self.targets_are_sources else 0
+        self.params = p
+        h = C.c_void_p()
+        _lib.check(self.lib.hs_plan_create(self.ctx.handle, C.byref(p), C.byref(h)))
+        self.handle = h
+        self._table_ids = {}
+        self.tables_ready = False
+
+    def __del__(self):
+        try:
+            if getattr(self, "handle", None):
+                self.lib.hs_plan_destroy(self.handle)
+                self.handle = None
+        except Exception:
+            pass
+
+    @property
+    def device_bytes(self) -> int:
+        return int(self.lib.hs_plan_bytes(self.handle))
+
+    def fft_counts(self):
+        a, b = C.c_int(), C.c_int()
+        _lib.check(self.lib.hs_plan_fft_counts(self.handle, C.byref(a), C.byref(b)))
+        return a.value, b.value
+
+    # ---- tables
+    def build_tables(self):
+        """GPU precompute_greens for every table this kind/geometry needs (ewald_fourier.py:207-244)."""
+        from .ewald_fourier import _oversampling_big
+        big = np.asarray(_oversampling_big(self.grid), dtype=np.int64)
+        guards = np.asarray(self.grid.guards, dtype=np.int64)
+        _lib.check(self.lib.hs_plan_build_tables(self.handle, _lib.i64ptr(big), float(self.grid.R),
+                                                 _lib.i64ptr(guards)))
+        self.tables_ready = True
+        self._table_ids = {"built": True}
+
+    def set_tables(self, tables: dict):
+        """Load reference-layout GreensTable samples (host or torch CUDA)."""
+        for name, tab in tables.items():
+            key = (id(tab), id(getattr(tab, "samples", None)))
+            if self._table_ids.get(name) == key:
+                continue
+            s = tab.samples
+            if _is_torch(s):
+                s = s.contiguous()
+                _lib.check(self.lib.hs_plan_set_table(self.handle, _lib.TABLE_ID[name], C.c_void_p(s.data_ptr()),
+                                                      _lib.HS_MEM_DEVICE))
+            else:
+                arr = np.ascontiguousarray(s, dtype=np.float64)
+                _lib.check(self.lib.hs_plan_set_table(self.handle, _lib.TABLE_ID[name],
+                                                      arr.ctypes.data_as(C.c_void_p), _lib.HS_MEM_HOST))
+            self._table_ids[name] = key
+        self.tables_ready = True
+
+    # ---- evaluation
+    def execute(self, positions, sa, sb=None, targets=None, tcols=None, what=3, out=None):
+        """Run the plan.  Host (NumPy) inputs -> NumPy outputs; torch CUDA inputs -> torch outputs.
+
+        Returns (u, u_real, u_fourier, times_ms dict)."""
+        times = (C.c_double * 10)()
+        if _is_torch(positions):
+            return self._execute_torch(positions, sa, sb, targets, tcols, what, times, out)
+        pos = _host_f64(positions)
+        a = _host_f64(sa)
+        b = _host_f64(sb) if sb is not None else None
+        nt = self.n_targets
+        tg = _host_f64(targets) if targets is not None else None
+        tc = np.ascontiguousarray(np.asarray(tcols, dtype=np.int64)) if tcols is not None else None
+        u = np.empty((nt, 3))
+        ur = np.empty((nt, 3))
+        uf = np.empty((nt, 3))
+        vp = lambda x: x.ctypes.data_as(C.c_void_p) if x is not None else None  # noqa: E731
+        self.ctx.bind_stream(None)
+        st = self.lib.hs_plan_execute(self.handle, vp(pos), vp(a), vp(b), vp(tg), vp(tc), vp(u), vp(ur), vp(uf),
+                                      _lib.HS_MEM_HOST, int(what), times)
+        _lib.check(st)
+        return u, ur, uf, dict(zip(TIME_KEYS, list(times)))
+
+    def _execute_torch(self, positions, sa, sb, targets, tcols, what, times, out):
+        import torch
+        dev = positions.device
+        nt = self.n_targets
+        if out is None:
+            out = torch.empty((3, nt, 3), dtype=torch.float64, device=dev)
+        u, ur, uf = out[0], out[1], out[2]
+        vp = lambda x: C.c_void_p(x.data_ptr()) if x is not None else None  # noqa: E731
+        self.ctx.bind_torch_stream()
+        st = self.lib.hs_plan_execute(self.handle, vp(positions), vp(sa), vp(sb), vp(targets), vp(tcols), vp(u),
+                                      vp(ur), vp(uf), _lib.HS_MEM_DEVICE, int(what), times)
+        _lib.check(st)
+        return u, ur, uf, dict(zip(TIME_KEYS, list(times)))
+
+
+_cache: dict = {}
+_cache_lock = threading.Lock()
+_CACHE_MAX = 4
+
+
+def get_evaluator(kind, geometry, L, xi, rc, grid, n, n_targets, targets_are_sources) -> Evaluator:
+    key = (kind, geometry, float(L), float(xi), float(rc), int(grid.M), int(grid.P), tuple(grid.padded_dims),
+           int(n), int(n_targets), bool(targets_are_sources))
+    with _cache_lock:
+        ev = _cache.get(key)
+        if ev is None:
+            while len(_cache) >= _CACHE_MAX:
+                _cache.pop(next(iter(_cache)))
+            ev = Evaluator(kind, geometry, L, xi, rc, grid, n, n_targets, targets_are_sources)
+            _cache[key] = ev
+        return ev
+
+
+def clear_cache():
+    with _cache_lock:
+        _cache.clear()

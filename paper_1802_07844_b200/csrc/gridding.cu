@@ -1,0 +1,324 @@
+// gridding.cu -- Gaussian spreading and gathering on the extended grid
+// (reference: _gridding.py:21-89, ewald_fourier.py:319-346,626-630).
+//
+// Spreading is owner-computes and atomic-free: one CTA owns a 16x16x8 tile of
+// grid nodes, each thread one (x,y) column of 8 z-nodes for every channel in
+// registers.  The CTA streams the sources whose P^3 support can reach the
+// tile (sources are bin-sorted by the tile of their window-centre cell, so
+// the candidates are 3x3 (x,y) runs of 5 z-bins), stages per-source window
+// slices restricted to the tile in shared memory, and every warp (a 4x8
+// (x,y) patch) skips sources whose support misses its patch (warp-uniform
+// branch).  Each grid value is written exactly once, deterministically,
+// without FP64 shared-memory atomics (a CAS loop on sm_100a).
+//
+// Gathering: one warp per target, lanes over the P z-nodes of one (x,y)
+// support column (coalesced 8*P-byte reads), loop over the P*P columns,
+// shuffle reduction over lanes.
+#include <cmath>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace hs {
+
+__global__ void k_grid_keys(const double* __restrict__ pos, int n_src, int n, int mode, GridGeom g, int nbx,
+                            int nby, int nbz, int* __restrict__ keys, unsigned* __restrict__ flags) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int s = (mode == 1 && i >= n_src) ? i - n_src : i;
+    const bool mir = (mode == 2) || (mode == 1 && i >= n_src);
+    const double pc[3] = {pos[3 * s], pos[3 * s + 1], mir ? -pos[3 * s + 2] : pos[3 * s + 2]};
+    int b[3];
+    const int tsz[3] = {SP_TX, SP_TY, SP_TZ};
+    const int nb[3] = {nbx, nby, nbz};
+    bool bad = false;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const int64_t lo = window_lo(pc[k], g.origin[k], g.h, g.P);
+      bad |= (lo < 0) || (lo + g.P > g.dims[k]);
+      int64_t c = lo + g.P / 2 - 1;  // window-centre cell i0
+      c = c < 0 ? 0 : (c >= g.dims[k] ? g.dims[k] - 1 : c);
+      int bb = (int)(c / tsz[k]);
+      b[k] = bb >= nb[k] ? nb[k] - 1 : bb;
+    }
+    if (bad) atomicOr(flags, FLAG_OUT_OF_GRID);
+    keys[i] = (b[0] * nby + b[1]) * nbz + b[2];
+  }
+}
+
+hs_status launch_grid_keys(hs_ctx* ctx, const double* pos, int n_src, int n, int mode, const GridGeom& g,
+                           int* keys) {
+  if (n == 0) return HS_OK;
+  const int gs = (int)std::min<int64_t>(ceil_div(n, 256), ctx->sm_count * 8);
+  k_grid_keys<<<gs, 256, 0, ctx->stream>>>(pos, n_src, n, mode, g, sp_nbins(g, 0), sp_nbins(g, 1), sp_nbins(g, 2),
+                                           keys, ctx->d_flags);
+  HS_LAUNCHED(ctx);
+  return HS_OK;
+}
+
+// ---------------------------------------------------------------------------
+constexpr int SP_CHUNK = 64;   // sources staged per round
+constexpr int SP_MAXCH = 8;
+
+template <int NCH>
+__global__ void __launch_bounds__(256) k_spread(const double4* __restrict__ pts, const double* __restrict__ w,
+                                                const int* __restrict__ bin_start, GridGeom g, int nbx, int nby,
+                                                int nbz, double* __restrict__ grids) {
+  __shared__ double s_wx[SP_CHUNK][SP_TX];
+  __shared__ double s_wy[SP_CHUNK][SP_TY];
+  __shared__ double s_wz[SP_CHUNK][SP_TZ];
+  __shared__ double s_q[SP_CHUNK][NCH];
+  __shared__ int s_lo[SP_CHUNK][3];
+  __shared__ int run_beg[9], run_pre[10];
+  __shared__ int s_nrun;
+
+  const int tz = blockIdx.x % nbz;
+  const int ty = (blockIdx.x / nbz) % nby;
+  const int tx = blockIdx.x / (nbz * nby);
+  const int x0 = tx * SP_TX, y0 = ty * SP_TY, z0 = tz * SP_TZ;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // warp patch: 4 (x) x 8 (y); 8 warps tile 16 x 16
+  const int px0 = (warp & 3) * 4, py0 = (warp >> 2) * 8;
+  const int xo = px0 + (lane & 3), yo = py0 + (lane >> 2);
+  const int P = g.P;
+
+  if (threadIdx.x == 0) {
+    int nr = 0, tot = 0;
+    const int zlo = max(tz - 2, 0), zhi = min(tz + 2, nbz - 1);
+    for (int bx = max(tx - 1, 0); bx <= min(tx + 1, nbx - 1); ++bx)
+      for (int by = max(ty - 1, 0); by <= min(ty + 1, nby - 1); ++by) {
+        const int f = (bx * nby + by) * nbz;
+        const int b = bin_start[f + zlo], e = bin_start[f + zhi + 1];
+        if (e > b) {
+          run_beg[nr] = b;
+          run_pre[nr] = tot;
+          tot += e - b;
+          ++nr;
+        }
+      }
+    run_pre[nr] = tot;
+    s_nrun = nr;
+  }
+  __syncthreads();
+  const int nrun = s_nrun, ncand = run_pre[nrun];
+
+  double acc[NCH][SP_TZ];
+#pragma unroll
+  for (int c = 0; c < NCH; ++c)
+#pragma unroll
+    for (int j = 0; j < SP_TZ; ++j) acc[c][j] = 0.0;
+
+  for (int c0 = 0; c0 < ncand; c0 += SP_CHUNK) {
+    const int nc = min(SP_CHUNK, ncand - c0);
+    __syncthreads();
+    // stage: 4 threads per source
+    {
+      const int s = threadIdx.x >> 2, part = threadIdx.x & 3;
+      if (s < nc) {
+        const int v = c0 + s;
+        int r = 0;
+        while (r + 1 < nrun && run_pre[r + 1] <= v) ++r;
+        const int row = run_beg[r] + (v - run_pre[r]);
+        const double4 p = pts[row];
+        if (part == 0) {
+          const int64_t lx = window_lo(p.x, g.origin[0], g.h, P);
+          s_lo[s][0] = (int)lx;
+#pragma unroll 4
+          for (int i = 0; i < SP_TX; ++i) {
+            const int64_t node = x0 + i;
+            double val = 0.0;
+            if (node >= lx && node < lx + P) {
+              const double d = window_d(p.x, g.origin[0], g.h, node);
+              val = exp(-g.alpha * d * d);
+            }
+            s_wx[s][i] = val;
+          }
+        } else if (part == 1) {
+          const int64_t ly = window_lo(p.y, g.origin[1], g.h, P);
+          s_lo[s][1] = (int)ly;
+#pragma unroll 4
+          for (int i = 0; i < SP_TY; ++i) {
+            const int64_t node = y0 + i;
+            double val = 0.0;
+            if (node >= ly && node < ly + P) {
+              const double d = window_d(p.y, g.origin[1], g.h, node);
+              val = exp(-g.alpha * d * d);
+            }
+            s_wy[s][i] = val;
+          }
+        } else if (part == 2) {
+          const int64_t lz = window_lo(p.z, g.origin[2], g.h, P);
+          s_lo[s][2] = (int)lz;
+#pragma unroll
+          for (int i = 0; i < SP_TZ; ++i) {
+            const int64_t node = z0 + i;
+            double val = 0.0;
+            if (node >= lz && node < lz + P) {
+              const double d = window_d(p.z, g.origin[2], g.h, node);
+              val = exp(-g.alpha * d * d);
+            }
+            s_wz[s][i] = val;
+          }
+        } else {
+#pragma unroll
+          for (int c = 0; c < NCH; ++c) s_q[s][c] = g.pref * w[(size_t)row * NCH + c];
+        }
+      }
+    }
+    __syncthreads();
+    for (int s = 0; s < nc; ++s) {
+      const int lx = s_lo[s][0], ly = s_lo[s][1], lz = s_lo[s][2];
+      // warp-uniform overlap test of the support with this warp's patch and the tile's z-range
+      const bool hit = (lx < x0 + px0 + 4) && (lx + P > x0 + px0) && (ly < y0 + py0 + 8) && (ly + P > y0 + py0) &&
+                       (lz < z0 + SP_TZ) && (lz + P > z0);
+      if (!hit) continue;
+      const double cxy = s_wx[s][xo] * s_wy[s][yo];
+      double wz[SP_TZ];
+#pragma unroll
+      for (int j = 0; j < SP_TZ; ++j) wz[j] = s_wz[s][j];
+#pragma unroll
+      for (int c = 0; c < NCH; ++c) {
+        const double q = s_q[s][c] * cxy;
+#pragma unroll
+        for (int j = 0; j < SP_TZ; ++j) acc[c][j] = fma(q, wz[j], acc[c][j]);
+      }
+    }
+  }
+  const int x = x0 + xo, y = y0 + yo;
+  if (x < g.dims[0] && y < g.dims[1]) {
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) {
+      double* dst = grids + c * g.ch_stride + x * g.stride[0] + y * g.stride[1];
+#pragma unroll
+      for (int j = 0; j < SP_TZ; ++j) {
+        const int z = z0 + j;
+        if (z < g.dims[2]) dst[z * g.stride[2]] = acc[c][j];
+      }
+    }
+  }
+}
+
+hs_status launch_spread(hs_ctx* ctx, const double4* pts, const double* w, int n, int nch, const int* bin_start,
+                        const GridGeom& g, double* grids) {
+  const int nbx = sp_nbins(g, 0), nby = sp_nbins(g, 1), nbz = sp_nbins(g, 2);
+  dim3 grid(nbx * nby * nbz), block(256);
+  (void)n;
+  switch (nch) {
+#define HS_SP(N) \
+  case N: k_spread<N><<<grid, block, 0, ctx->stream>>>(pts, w, bin_start, g, nbx, nby, nbz, grids); break;
+    HS_SP(1) HS_SP(2) HS_SP(3) HS_SP(4) HS_SP(5) HS_SP(6) HS_SP(7) HS_SP(8)
+#undef HS_SP
+    default:
+      return fail(HS_ERR_PARAMETER, "spread supports 1..8 channels per launch");
+  }
+  HS_LAUNCHED(ctx);
+  return HS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Gather: warp per point, lanes over z.  MODE 0: generic channels -> out[perm[i]*ldo + c]
+// (ewald_fourier.gather); MODE 1: half/free Fourier velocity with T1 (3) and T2 (3).
+template <int NCH, int MODE>
+__global__ void __launch_bounds__(256) k_gather(const double4* __restrict__ pts, const int* __restrict__ perm,
+                                                int n, GridGeom g, const double* __restrict__ grids,
+                                                double* __restrict__ out, int ldo, double scale,
+                                                double* __restrict__ u_total, const double* __restrict__ u_real,
+                                                unsigned* __restrict__ flags) {
+  __shared__ double s_w[8][2][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int P = g.P;
+  for (int i = blockIdx.x * 8 + warp; i < n; i += gridDim.x * 8) {
+    const double4 p = pts[i];
+    const int64_t lx = window_lo(p.x, g.origin[0], g.h, P);
+    const int64_t ly = window_lo(p.y, g.origin[1], g.h, P);
+    const int64_t lz = window_lo(p.z, g.origin[2], g.h, P);
+    const bool bad = lx < 0 || ly < 0 || lz < 0 || lx + P > g.dims[0] || ly + P > g.dims[1] || lz + P > g.dims[2];
+    double acc[NCH];
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) acc[c] = 0.0;
+    if (!bad) {
+      __syncwarp();
+      if (lane < P) {
+        const double dx = window_d(p.x, g.origin[0], g.h, lx + lane);
+        const double dy = window_d(p.y, g.origin[1], g.h, ly + lane);
+        s_w[warp][0][lane] = exp(-g.alpha * dx * dx);
+        s_w[warp][1][lane] = exp(-g.alpha * dy * dy);
+      }
+      double wz = 0.0;
+      if (lane < P) {
+        const double dz = window_d(p.z, g.origin[2], g.h, lz + lane);
+        wz = exp(-g.alpha * dz * dz);
+      }
+      __syncwarp();
+      const int zi = lane < P ? lane : 0;
+      const double* base = grids + lx * g.stride[0] + ly * g.stride[1] + (lz + zi) * g.stride[2];
+      for (int a = 0; a < P; ++a) {
+        const double wxa = g.pref * s_w[warp][0][a];
+        for (int b = 0; b < P; ++b) {
+          const double wv = (wxa * s_w[warp][1][b]) * wz;
+          const double* q = base + a * g.stride[0] + b * g.stride[1];
+#pragma unroll
+          for (int c = 0; c < NCH; ++c) acc[c] = fma(__ldg(q + c * g.ch_stride), wv, acc[c]);
+        }
+      }
+    } else if (lane == 0) {
+      atomicOr(flags, FLAG_OUT_OF_GRID);
+    }
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) acc[c] = warp_sum(acc[c]);
+    if (lane == 0) {
+      const int o = perm ? perm[i] : i;
+      const double h3 = g.h * g.h * g.h;
+      if (MODE == 0) {
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) out[(size_t)o * ldo + c] = acc[c] * h3 * scale;
+      } else {
+        // u_F = h^3 sum w T1 - x3 h^3 sum w T2   (ewald_fourier.py:626-630)
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+          double v = acc[q] * h3;
+          if (NCH == 6) v -= p.z * (acc[3 + q] * h3);
+          if (out) out[3 * (size_t)o + q] = v;
+          if (u_total) u_total[3 * (size_t)o + q] = (u_real ? u_real[3 * (size_t)o + q] : 0.0) + v;
+        }
+      }
+    }
+  }
+}
+
+hs_status launch_gather(hs_ctx* ctx, const double4* pts, const int* perm, int n, int nch, const GridGeom& g,
+                        const double* grids, double* out, int ldo, double scale) {
+  if (n == 0) return HS_OK;
+  if (g.P > 32) return fail(HS_ERR_PARAMETER, "gather supports window support P <= 32");
+  const int gs = (int)std::min<int64_t>(ceil_div(n, 8), ctx->sm_count * 64);
+  switch (nch) {
+#define HS_GA(N)                                                                                               \
+  case N:                                                                                                      \
+    k_gather<N, 0><<<gs, 256, 0, ctx->stream>>>(pts, perm, n, g, grids, out, ldo, scale, nullptr, nullptr,   \
+                                                ctx->d_flags);                                               \
+    break;
+    HS_GA(1) HS_GA(2) HS_GA(3) HS_GA(4) HS_GA(5) HS_GA(6) HS_GA(7) HS_GA(8)
+#undef HS_GA
+    default:
+      return fail(HS_ERR_PARAMETER, "gather supports 1..8 channels per launch");
+  }
+  HS_LAUNCHED(ctx);
+  return HS_OK;
+}
+
+hs_status launch_gather_fourier(hs_ctx* ctx, const double4* pts, const int* orig, int n, int half,
+                                const GridGeom& g, const double* T, double* u_fourier, double* u_total,
+                                const double* u_real) {
+  if (n == 0) return HS_OK;
+  if (g.P > 32) return fail(HS_ERR_PARAMETER, "gather supports window support P <= 32");
+  const int gs = (int)std::min<int64_t>(ceil_div(n, 8), ctx->sm_count * 64);
+  if (half)
+    k_gather<6, 1><<<gs, 256, 0, ctx->stream>>>(pts, orig, n, g, T, u_fourier, 3, 1.0, u_total, u_real,
+                                                ctx->d_flags);
+  else
+    k_gather<3, 1><<<gs, 256, 0, ctx->stream>>>(pts, orig, n, g, T, u_fourier, 3, 1.0, u_total, u_real,
+                                                ctx->d_flags);
+  HS_LAUNCHED(ctx);
+  return HS_OK;
+}
+
+}  // namespace hs

@@ -1,0 +1,113 @@
+// kernels.cuh -- internal launcher interfaces shared by the .cu translation units.
+#pragma once
+#include "common.cuh"
+
+namespace hs {
+
+// sort.cu
+hs_status counting_sort(hs_ctx* ctx, const int* keys, int n, int nb, int* order, int* start, int* work);
+inline size_t counting_sort_work_ints(int n, int nb) { return (size_t)2 * nb + 4 + (size_t)n; }
+
+// ---------------------------------------------------------------------------
+// cell lists (cell_list.cu)
+struct CellGeom {
+  double lo[3], hi[3], edge[3];
+  int64_t dims[3];
+  int64_t ncell() const { return dims[0] * dims[1] * dims[2]; }
+};
+// dims/edge exactly as numpy computes them (ewald_real.py:241-243)
+hs_status cell_geometry(double rc, const double lo[3], const double hi[3], CellGeom* g);
+// keys for n_total points: point i < n_src is pos[i]; i >= n_src is pos[i-n_src]
+// mirrored through z=0 when `mirror` (ImageSystem.combined_positions, system.py:164-191).
+hs_status launch_cell_keys(hs_ctx* ctx, const double* pos, int n_src, int n_total, int mirror,
+                           const CellGeom& g, int check_bounds, int* keys);
+
+// ---------------------------------------------------------------------------
+// spreading / gathering (gridding.cu)
+struct GridGeom {
+  double origin[3];
+  double h, alpha, pref;   // alpha = 2 xi^2/eta, pref = (2 xi^2/(pi eta))^{3/2}
+  int dims[3];             // nx, ny, nz (region holding data)
+  int P;
+  int64_t stride[3];       // element strides of the storage layout (x, y, z)
+  int64_t ch_stride;       // element stride between channels
+};
+constexpr int SP_TX = 16, SP_TY = 16, SP_TZ = 8;  // spread tile / bin shape
+inline int sp_nbins(const GridGeom& g, int k) {
+  const int t[3] = {SP_TX, SP_TY, SP_TZ};
+  return (int)ceil_div(g.dims[k], t[k]);
+}
+// Bin keys of spreading/gathering points by the grid tile holding their window
+// centre cell; flags FLAG_OUT_OF_GRID if a window leaves the grid (_gridding.py:50-52).
+// point i of a set: mode 0 -> pos[i]; mode 1 -> combined [y; y^I] (n_total = 2 n_src);
+// mode 2 -> images y^I only (n_total = n_src).
+hs_status launch_grid_keys(hs_ctx* ctx, const double* pos, int n_src, int n_total, int mode, const GridGeom& g,
+                           int* keys);
+// sorted spread: pts/weights already in bin order; bin_start[nbins+1]
+hs_status launch_spread(hs_ctx* ctx, const double4* pts, const double* w, int n, int nch,
+                        const int* bin_start, const GridGeom& g, double* grids);
+// gather: nch channels (<= 8) at n points (any order); out[i*ldo + ch] (times h^3 * scale)
+hs_status launch_gather(hs_ctx* ctx, const double4* pts, const int* perm, int n, int nch,
+                        const GridGeom& g, const double* grids, double* out, int ldo, double scale);
+// half-space Fourier gather: u[orig] (+)= h^3 (T1 . w - x3 T2 . w) (ewald_fourier.py:626-630)
+hs_status launch_gather_fourier(hs_ctx* ctx, const double4* pts, const int* orig, int n, int half,
+                                const GridGeom& g, const double* T, double* u_fourier, double* u_total,
+                                const double* u_real);
+
+// ---------------------------------------------------------------------------
+// real space (pair.cu)
+struct PairArgs {
+  const double4* P;   // cell-sorted combined sources: x, y, z, original combined index
+  const double4* A;   // strength a: f (stokeslet), g (stresslet), sign*(g x q) (rotlet)
+  const double4* B;   // strength b: q (stresslet), image wall channel v1,v2 (rotlet)
+  const int* start;   // src cell start, ncell+1
+  const double4* TP;  // cell-sorted targets: x, y, z, tcol
+  const int* torig;   // output row of each sorted target
+  const int* t_start; // target cell start, ncell+1
+  const int* cells;   // non-empty target cells
+  int n_cells;        // launch bound (>= actual count)
+  const int* n_cells_d;  // actual count (device)
+  int dims[3];
+  double xi, rc2;
+  int n_real;         // combined index >= n_real -> image
+  int kind;
+  const double* self_f;  // stokeslet self term strengths (original f) or null
+  double* u;          // (nt,3) real-space velocity (normalised)
+  double* uk;         // optional (nt,3) kernel part
+  double* uc;         // optional (nt,3) correction part
+  unsigned* flags;
+};
+hs_status launch_pair(hs_ctx* ctx, const PairArgs& a);
+hs_status launch_direct(hs_ctx* ctx, int kind, int half, int n_real, int n_src, const double4* P,
+                        const double4* A, const double4* B, int nt, const double4* TP, double* u);
+
+// ---------------------------------------------------------------------------
+// k-space (kspace.cu)
+struct KGeom {
+  int p[3];          // padded dims
+  int nzh;           // p[2]/2 + 1 (half spectrum)
+  double kscale[3];  // 1/(p_i h) (numpy fftfreq spacing)
+  double a, b;       // (1-eta)/4xi^2, 1/4xi^2
+  double inv_n;      // 1/(px py pz) (scipy ifftn normalisation)
+};
+// channel layout per kind (see plan.cu); spectra: (nch, px, py, nzh) complex
+hs_status launch_kscale(hs_ctx* ctx, int kind, int half, const KGeom& k, const double* tabB,
+                        const double* tabH, double2* spec, int64_t ch_stride);
+// Green's table precompute (ewald_fourier.py:154-174,207-244)
+hs_status launch_greens_hat(hs_ctx* ctx, int kind, double R, double h, const int64_t big[3],
+                            double2* out);
+hs_status launch_crop(hs_ctx* ctx, const double* field, const int64_t big[3], const int64_t keep[3], double scale,
+                      double* crop);
+hs_status launch_real_part(hs_ctx* ctx, const double2* spec, int64_t n, double* out);
+hs_status launch_expand_half(hs_ctx* ctx, const double2* half_spec, const int64_t p[3], double* full);
+hs_status launch_take_half(hs_ctx* ctx, const double* full, const int64_t p[3], double* half);
+
+// plan.cu helpers reused by the stand-alone API
+hs_status greens_half_table(hs_ctx* ctx, int kind, double R, double h, const int64_t big[3], const int64_t dims[3],
+                            const int64_t guards[3], const int64_t pd[3], double* half_out);
+hs_status build_pair_records(hs_ctx* ctx, int kind, int half, const int* order, int n_comb, int n, const double* pos,
+                             const double* sa, const double* sb, double4* P, double4* A, double4* B);
+hs_status build_target_records(hs_ctx* ctx, const int* order, int nt, const double* tpos, const long long* tcols,
+                               int tcol_identity, double4* TP, int* torig);
+
+}  // namespace hs

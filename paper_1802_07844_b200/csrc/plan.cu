@@ -1,0 +1,739 @@
+// plan.cu -- one evaluation of ewald.ewald_sum (reference: ewald.py:46-80) on the GPU.
+//
+// The plan owns all device buffers of one configuration and runs, stream-ordered:
+//   real space:  cell keys of [y; y^I] -> stable counting sort -> cell-sorted
+//                source records (reflect + wall channels fused) -> target cell
+//                sort -> pair kernel (+ normalisation + stokeslet self term)
+//   Fourier:     bin-sort kernel sources [y; y^I] and images y^I -> spread into
+//                zero-padded real grids -> batched cuFFT D2Z -> fused k-space
+//                scale (one pass, in place) -> batched cuFFT Z2D -> gather at
+//                targets, adding the real-space part.
+// Phase times are CUDA events on the plan's stream.
+#include <cufft.h>
+
+#include <cmath>
+#include <vector>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace hs {
+
+#define HS_CUFFT(expr)                                                                  \
+  do {                                                                                  \
+    cufftResult _r = (expr);                                                            \
+    if (_r != CUFFT_SUCCESS)                                                            \
+      return ::hs::fail(HS_ERR_RESOURCE, std::string(#expr) + ": cuFFT error " + std::to_string((int)_r)); \
+  } while (0)
+
+// ---------------------------------------------------------------------------
+// record builders
+
+// pair records in cell order: order[k] = combined index i (i >= n -> image of i-n)
+__global__ void k_pair_records(int kind, int half, const int* __restrict__ order, int n_comb, int n,
+                               const double* __restrict__ pos, const double* __restrict__ sa,
+                               const double* __restrict__ sb, double4* __restrict__ P, double4* __restrict__ A,
+                               double4* __restrict__ B) {
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n_comb; k += gridDim.x * blockDim.x) {
+    const int i = order[k];
+    const bool img = half && i >= n;
+    const int s = img ? i - n : i;
+    const double m = img ? -1.0 : 1.0;  // MIRROR z
+    P[k] = make_double4(pos[3 * s], pos[3 * s + 1], m * pos[3 * s + 2], (double)i);
+    const double a0 = sa[3 * s], a1 = sa[3 * s + 1], a2 = sa[3 * s + 2];
+    if (kind == HS_STOKESLET) {
+      // combined_f = [f; -f^I], f^I = f * (1,1,-1)  (system.py:171-177)
+      A[k] = img ? make_double4(-a0, -a1, a2, 0.0) : make_double4(a0, a1, a2, 0.0);
+    } else {
+      const double b0 = sb[3 * s], b1 = sb[3 * s + 1], b2 = sb[3 * s + 2];
+      const double g0 = a0, g1 = a1, g2 = m * a2;  // g or g^I
+      const double q0 = b0, q1 = b1, q2 = m * b2;  // q or q^I
+      if (kind == HS_STRESSLET) {
+        A[k] = make_double4(g0, g1, g2, 0.0);
+        B[k] = make_double4(q0, q1, q2, 0.0);
+      } else {
+        const double sg = img ? -1.0 : 1.0;
+        A[k] = make_double4(sg * (g1 * q2 - g2 * q1), sg * (g2 * q0 - g0 * q2), sg * (g0 * q1 - g1 * q0), 0.0);
+        // image wall channel v = 4 (q3 g^I - g3 q^I), v3 = 0 (kernels_direct.py:123-127)
+        if (img) B[k] = make_double4(4.0 * (b2 * g0 - a2 * q0), 4.0 * (b2 * g1 - a2 * q1), 0.0, 0.0);
+        else B[k] = make_double4(0.0, 0.0, 0.0, 0.0);
+      }
+    }
+  }
+}
+
+// target records in cell order: order[k] = target t
+__global__ void k_target_records(const int* __restrict__ order, int nt, const double* __restrict__ tpos,
+                                 const long long* __restrict__ tcols, int tcol_identity, double4* __restrict__ TP,
+                                 int* __restrict__ torig) {
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < nt; k += gridDim.x * blockDim.x) {
+    const int t = order ? order[k] : k;
+    const double tc = tcol_identity ? (double)t : (tcols ? (double)tcols[t] : -1.0);
+    TP[k] = make_double4(tpos[3 * t], tpos[3 * t + 1], tpos[3 * t + 2], tc);
+    torig[k] = t;
+  }
+}
+
+__global__ void k_nonempty_cells(const int* __restrict__ t_start, int ncell, int* __restrict__ cells,
+                                 int* __restrict__ count) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < ncell; c += gridDim.x * blockDim.x)
+    if (t_start[c + 1] > t_start[c]) cells[atomicAdd(count, 1)] = c;
+}
+
+// spread source records in bin order.  set 0: kernel sources [y; y^I]; set 1: images y^I
+// with wall channels.  W has nch doubles per row (see kspace.cu channel layout).
+__global__ void k_spread_records(int kind, int half, int set, const int* __restrict__ order, int n_rows, int n,
+                                 const double* __restrict__ pos, const double* __restrict__ sa,
+                                 const double* __restrict__ sb, int nch, double4* __restrict__ P,
+                                 double* __restrict__ W) {
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n_rows; k += gridDim.x * blockDim.x) {
+    const int i = order[k];
+    const bool img = (set == 1) || (half && i >= n);
+    const int s = (set == 0 && half && i >= n) ? i - n : i;
+    const double m = img ? -1.0 : 1.0;
+    const double y3 = pos[3 * s + 2];
+    P[k] = make_double4(pos[3 * s], pos[3 * s + 1], m * y3, 0.0);
+    double* w = W + (size_t)k * nch;
+    const double a0 = sa[3 * s], a1 = sa[3 * s + 1], a2 = sa[3 * s + 2];
+    double b0 = 0, b1 = 0, b2 = 0;
+    if (kind != HS_STOKESLET) {
+      b0 = sb[3 * s];
+      b1 = sb[3 * s + 1];
+      b2 = sb[3 * s + 2];
+    }
+    if (set == 0) {
+      if (kind == HS_STOKESLET) {  // _kernel_weights: combined_f (ewald_fourier.py:357-359)
+        w[0] = img ? -a0 : a0;
+        w[1] = img ? -a1 : a1;
+        w[2] = a2;  // -(f^I)_3 = f_3
+      } else {
+        const double g0 = a0, g1 = a1, g2 = m * a2, q0 = b0, q1 = b1, q2 = m * b2;
+        const double sg = img ? -1.0 : 1.0;
+        if (kind == HS_STRESSLET) {  // symmetric part of sign * g (x) q
+          w[0] = sg * g0 * q0;
+          w[1] = sg * 0.5 * (g0 * q1 + g1 * q0);
+          w[2] = sg * 0.5 * (g0 * q2 + g2 * q0);
+          w[3] = sg * g1 * q1;
+          w[4] = sg * 0.5 * (g1 * q2 + g2 * q1);
+          w[5] = sg * g2 * q2;
+        } else {  // sign * (g x q)
+          w[0] = sg * (g1 * q2 - g2 * q1);
+          w[1] = sg * (g2 * q0 - g0 * q2);
+          w[2] = sg * (g0 * q1 - g1 * q0);
+        }
+      }
+    } else {
+      // _correction_weights (ewald_fourier.py:373-382) with phi_channels (kernels_direct.py:93-127)
+      if (kind == HS_STOKESLET) {
+        w[0] = -a2;        // s = -f3
+        w[1] = -y3 * a0;   // v = -y3 f^I
+        w[2] = -y3 * a1;
+        w[3] = y3 * a2;
+      } else if (kind == HS_STRESSLET) {
+        const double g0 = a0, g1 = a1, g2 = -a2, q0 = b0, q1 = b1, q2 = -b2;  // g^I, q^I
+        w[0] = 2.0 * (g0 * q0 + g1 * q1 + g2 * q2);  // v3
+        w[1] = -y3 * 2.0 * g0 * q0;                   // M00
+        w[2] = -y3 * (g0 * q1 + q0 * g1);             // M01
+        w[3] = -y3 * (g0 * q2 + q0 * g2);             // M02
+        w[4] = -y3 * 2.0 * g1 * q1;                   // M11
+        w[5] = -y3 * (g1 * q2 + q1 * g2);             // M12
+        w[6] = -y3 * 2.0 * g2 * q2;                   // M22
+      } else {
+        const double g0 = a0, g1 = a1, q0 = b0, q1 = b1;  // (g^I)_{0,1} = g_{0,1}
+        w[0] = 4.0 * (b2 * g0 - a2 * q0);
+        w[1] = 4.0 * (b2 * g1 - a2 * q1);
+      }
+    }
+  }
+}
+
+// stokeslet self term only (rc = 0 path): u[t] = -(4 xi/sqrt(pi)) f[tcol] / (8 pi)
+__global__ void k_self_term(int nt, const double* __restrict__ tpos, const long long* __restrict__ tcols,
+                            int tcol_identity, int n, double xi, const double* __restrict__ f, double* __restrict__ u) {
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < nt; t += gridDim.x * blockDim.x) {
+    const long long c = tcol_identity ? t : (tcols ? tcols[t] : -1);
+    if (c >= 0 && c < n) {
+      const double sc = -(4.0 * xi / kSqrtPi);
+      for (int q = 0; q < 3; ++q) u[3 * t + q] = sc * f[3 * c + q] / (8.0 * kPi);
+    }
+  }
+}
+
+// targets for the Fourier gather, in bin order
+__global__ void k_gather_records(const int* __restrict__ order, int nt, const double* __restrict__ tpos,
+                                 double4* __restrict__ TG, int* __restrict__ tg_orig) {
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < nt; k += gridDim.x * blockDim.x) {
+    const int t = order[k];
+    TG[k] = make_double4(tpos[3 * t], tpos[3 * t + 1], tpos[3 * t + 2], 0.0);
+    tg_orig[k] = t;
+  }
+}
+
+inline int grid_size(hs_ctx* ctx, int64_t n) {
+  return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 256), (int64_t)ctx->sm_count * 8));
+}
+
+hs_status build_pair_records(hs_ctx* ctx, int kind, int half, const int* order, int n_comb, int n, const double* pos,
+                             const double* sa, const double* sb, double4* P, double4* A, double4* B) {
+  if (n_comb == 0) return HS_OK;
+  k_pair_records<<<grid_size(ctx, n_comb), 256, 0, ctx->stream>>>(kind, half, order, n_comb, n, pos, sa, sb, P, A, B);
+  HS_LAUNCHED(ctx);
+  return HS_OK;
+}
+
+hs_status build_target_records(hs_ctx* ctx, const int* order, int nt, const double* tpos, const long long* tcols,
+                               int tcol_identity, double4* TP, int* torig) {
+  if (nt == 0) return HS_OK;
+  k_target_records<<<grid_size(ctx, nt), 256, 0, ctx->stream>>>(order, nt, tpos, tcols, tcol_identity, TP, torig);
+  HS_LAUNCHED(ctx);
+  return HS_OK;
+}
+
+}  // namespace hs
+
+using namespace hs;
+
+struct DeviceBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+};
+
+struct hs_plan {
+  hs_ctx* ctx = nullptr;
+  hs_params prm{};
+  bool half = true;
+  int n_comb = 0;       // sources in the real-space / kernel spread set
+  int nk = 0, nc = 0;   // kernel / correction channels
+  int n_in = 0, n_out = 0;
+  CellGeom cg{};
+  GridGeom gg{};        // padded real grids
+  KGeom kg{};
+  int64_t n_real_grid = 0, n_half = 0;
+  int nbins = 0;
+  std::vector<DeviceBuf> bufs;
+  int64_t bytes = 0;
+  // inputs (staging for host memory)
+  double *d_pos = nullptr, *d_sa = nullptr, *d_sb = nullptr, *d_tgt = nullptr;
+  long long* d_tcols = nullptr;
+  // real space
+  int *keys = nullptr, *order = nullptr, *start = nullptr, *work = nullptr;
+  int *t_order = nullptr, *t_start = nullptr, *cells = nullptr, *n_cells_d = nullptr;
+  double4 *P = nullptr, *A = nullptr, *B = nullptr, *TP = nullptr;
+  int* torig = nullptr;
+  // Fourier
+  int *bk_order = nullptr, *bk_start = nullptr, *bc_order = nullptr, *bc_start = nullptr;
+  int *bt_order = nullptr, *bt_start = nullptr;
+  double4 *SPk = nullptr, *SPc = nullptr, *TG = nullptr;
+  double *SWk = nullptr, *SWc = nullptr;
+  int* tg_orig = nullptr;
+  double* grid_in = nullptr;    // n_in * n_real_grid
+  double2* spec = nullptr;      // max(n_in,n_out) * n_half
+  double* grid_out = nullptr;   // n_out * n_real_grid
+  double* tabB = nullptr;       // n_half (real)
+  double* tabH = nullptr;
+  bool have_B = false, have_H = false;
+  cufftHandle fwd = 0, inv = 0;
+  void* fft_work = nullptr;
+  // outputs
+  double *u = nullptr, *u_real = nullptr, *u_four = nullptr, *uk = nullptr, *uc = nullptr;
+  cudaEvent_t ev[12] = {};
+};
+
+namespace {
+
+template <typename T>
+hs_status palloc(hs_plan* p, size_t count, T** out, bool zero = false) {
+  size_t bytes = std::max<size_t>(count, 1) * sizeof(T);
+  void* ptr = nullptr;
+  cudaError_t e = cudaMalloc(&ptr, bytes);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(HS_ERR_RESOURCE, "device allocation of " + std::to_string(bytes) + " bytes failed: " +
+                                     cudaGetErrorString(e));
+  }
+  if (zero) HS_CUDA(cudaMemset(ptr, 0, bytes));
+  p->bufs.push_back({ptr, bytes});
+  p->bytes += (int64_t)bytes;
+  *out = (T*)ptr;
+  return HS_OK;
+}
+
+int table_needs(int kind, int half, int table_kind) {
+  // table_kinds_for (ewald_fourier.py:281-290)
+  if (table_kind == HS_BIHARMONIC) return kind != HS_ROTLET;
+  return kind == HS_ROTLET || half;
+}
+
+}  // namespace
+
+namespace hs {
+hs_status plan_channels(int kind, int half, int* nk, int* nc) {
+  if (kind == HS_STOKESLET) { *nk = 3; *nc = half ? 4 : 0; }
+  else if (kind == HS_STRESSLET) { *nk = 6; *nc = half ? 7 : 0; }
+  else if (kind == HS_ROTLET) { *nk = 3; *nc = half ? 2 : 0; }
+  else return fail(HS_ERR_PARAMETER, "unknown kernel kind");
+  return HS_OK;
+}
+}  // namespace hs
+
+extern "C" hs_status hs_plan_create(hs_ctx* ctx, const hs_params* prm, hs_plan** out) {
+  if (!ctx || !prm || !out) return fail(HS_ERR_PARAMETER, "null argument");
+  HS_CUDA(cudaSetDevice(ctx->device));
+  hs_plan* p = new hs_plan();
+  p->ctx = ctx;
+  p->prm = *prm;
+  p->half = prm->geometry == HS_HALF;
+  hs_status st = HS_OK;
+  auto bail = [&](hs_status s) {
+    hs_plan_destroy(p);
+    return s;
+  };
+  if (prm->n < 1 || prm->n_targets < 0 || prm->n > (1 << 29) || prm->n_targets > (1 << 30))
+    return bail(fail(HS_ERR_PARAMETER, "unsupported source/target count"));
+  if ((st = plan_channels(prm->kind, p->half, &p->nk, &p->nc)) != HS_OK) return bail(st);
+  const int n = (int)prm->n, nt = (int)prm->n_targets;
+  p->n_comb = p->half ? 2 * n : n;
+  p->n_in = p->nk + p->nc;
+  p->n_out = p->half ? 6 : 3;
+  // ---- real-space cell geometry: build_cell_list(src, 0.5*rc, (lo, hi))  (ewald_real.py:415-430)
+  const double L = prm->L;
+  double lo[3] = {0.0, 0.0, p->half ? -L : 0.0}, hi[3] = {L, L, L};
+  const bool do_real = prm->rc > 0;
+  if (do_real) {
+    if ((st = cell_geometry(0.5 * prm->rc, lo, hi, &p->cg)) != HS_OK) return bail(st);
+  } else {
+    p->cg.dims[0] = p->cg.dims[1] = p->cg.dims[2] = 1;
+  }
+  const int ncell = (int)p->cg.ncell();
+  // ---- grid geometry
+  GridGeom& g = p->gg;
+  for (int k = 0; k < 3; ++k) {
+    g.origin[k] = prm->origin[k];
+    g.dims[k] = (int)prm->dims[k];
+  }
+  g.h = prm->h;
+  g.P = (int)prm->P;
+  g.alpha = 2.0 * prm->xi * prm->xi / prm->eta;
+  g.pref = std::pow(2.0 * prm->xi * prm->xi / (kPi * prm->eta), 1.5);
+  const int64_t px = prm->padded[0], py = prm->padded[1], pz = prm->padded[2];
+  g.stride[0] = py * pz;
+  g.stride[1] = pz;
+  g.stride[2] = 1;
+  g.ch_stride = px * py * pz;
+  p->n_real_grid = px * py * pz;
+  p->n_half = px * py * (pz / 2 + 1);
+  KGeom& kg = p->kg;
+  kg.p[0] = (int)px;
+  kg.p[1] = (int)py;
+  kg.p[2] = (int)pz;
+  kg.nzh = (int)(pz / 2 + 1);
+  for (int k = 0; k < 3; ++k) kg.kscale[k] = 1.0 / ((double)prm->padded[k] * prm->h);
+  kg.a = (1.0 - prm->eta) / (4.0 * prm->xi * prm->xi);
+  kg.b = 1.0 / (4.0 * prm->xi * prm->xi);
+  kg.inv_n = 1.0 / ((double)px * (double)py * (double)pz);
+  p->nbins = sp_nbins(g, 0) * sp_nbins(g, 1) * sp_nbins(g, 2);
+  const int nb = p->nbins;
+
+  // ---- buffers
+  const int maxn = std::max(p->n_comb, std::max(nt, n));
+  const int maxb = std::max(ncell, nb);
+#define A_(cnt, ptr, ...) if ((st = palloc(p, (size_t)(cnt), &(ptr), ##__VA_ARGS__)) != HS_OK) return bail(st)
+  A_(3 * (size_t)n, p->d_pos);
+  A_(3 * (size_t)n, p->d_sa);
+  if (prm->kind != HS_STOKESLET) A_(3 * (size_t)n, p->d_sb);
+  if (!prm->targets_are_sources) {
+    A_(3 * (size_t)std::max(nt, 1), p->d_tgt);
+    A_((size_t)std::max(nt, 1), p->d_tcols);
+  }
+  A_(maxn, p->keys);
+  A_(maxn, p->order);
+  A_(counting_sort_work_ints(maxn, maxb), p->work);
+  A_(ncell + 1, p->start);
+  A_(nt + 1, p->t_order);
+  A_(ncell + 1, p->t_start);
+  A_(ncell, p->cells);
+  A_(1, p->n_cells_d);
+  A_(p->n_comb, p->P);
+  A_(p->n_comb, p->A);
+  A_(p->n_comb, p->B);
+  A_(std::max(nt, 1), p->TP);
+  A_(std::max(nt, 1), p->torig);
+  A_(p->n_comb, p->bk_order);
+  A_(nb + 1, p->bk_start);
+  A_(n, p->bc_order);
+  A_(nb + 1, p->bc_start);
+  A_(std::max(nt, 1), p->bt_order);
+  A_(nb + 1, p->bt_start);
+  A_(p->n_comb, p->SPk);
+  A_((size_t)p->n_comb * p->nk, p->SWk);
+  if (p->nc) {
+    A_(n, p->SPc);
+    A_((size_t)n * p->nc, p->SWc);
+  }
+  A_(std::max(nt, 1), p->TG);
+  A_(std::max(nt, 1), p->tg_orig);
+  A_((size_t)p->n_in * p->n_real_grid, p->grid_in, true);  // zero padding persists (D2Z is out of place)
+  A_((size_t)std::max(p->n_in, p->n_out) * p->n_half, p->spec);
+  A_((size_t)p->n_out * p->n_real_grid, p->grid_out);
+  if (table_needs(prm->kind, p->half, HS_BIHARMONIC)) A_(p->n_half, p->tabB);
+  if (table_needs(prm->kind, p->half, HS_HARMONIC)) A_(p->n_half, p->tabH);
+  A_(3 * (size_t)std::max(nt, 1), p->u);
+  A_(3 * (size_t)std::max(nt, 1), p->u_real, true);
+  A_(3 * (size_t)std::max(nt, 1), p->u_four, true);
+  A_(3 * (size_t)std::max(nt, 1), p->uk, true);
+  A_(3 * (size_t)std::max(nt, 1), p->uc, true);
+#undef A_
+  // ---- cuFFT plans (batched over channels, shared work area)
+  {
+    long long nn[3] = {px, py, pz};
+    size_t ws1 = 0, ws2 = 0;
+    if (cufftCreate(&p->fwd) != CUFFT_SUCCESS || cufftCreate(&p->inv) != CUFFT_SUCCESS)
+      return bail(fail(HS_ERR_RESOURCE, "cufftCreate failed"));
+    cufftSetAutoAllocation(p->fwd, 0);
+    cufftSetAutoAllocation(p->inv, 0);
+    if (cufftMakePlanMany64(p->fwd, 3, nn, nullptr, 1, p->n_real_grid, nullptr, 1, p->n_half, CUFFT_D2Z, p->n_in,
+                            &ws1) != CUFFT_SUCCESS)
+      return bail(fail(HS_ERR_RESOURCE, "cuFFT D2Z plan failed"));
+    if (cufftMakePlanMany64(p->inv, 3, nn, nullptr, 1, p->n_half, nullptr, 1, p->n_real_grid, CUFFT_Z2D, p->n_out,
+                            &ws2) != CUFFT_SUCCESS)
+      return bail(fail(HS_ERR_RESOURCE, "cuFFT Z2D plan failed"));
+    const size_t ws = std::max(ws1, ws2);
+    char* wsp = nullptr;
+    if ((st = palloc(p, std::max<size_t>(ws, 16), &wsp)) != HS_OK) return bail(st);
+    p->fft_work = wsp;
+    cufftSetWorkArea(p->fwd, wsp);
+    cufftSetWorkArea(p->inv, wsp);
+    cufftSetStream(p->fwd, ctx->stream);
+    cufftSetStream(p->inv, ctx->stream);
+  }
+  for (auto& e : p->ev) HS_CUDA(cudaEventCreate(&e));
+  *out = p;
+  return HS_OK;
+}
+
+extern "C" hs_status hs_plan_destroy(hs_plan* p) {
+  if (!p) return HS_OK;
+  if (p->fwd) cufftDestroy(p->fwd);
+  if (p->inv) cufftDestroy(p->inv);
+  for (auto& e : p->ev)
+    if (e) cudaEventDestroy(e);
+  for (auto& b : p->bufs) cudaFree(b.p);
+  delete p;
+  return HS_OK;
+}
+
+extern "C" int64_t hs_plan_bytes(const hs_plan* p) { return p ? p->bytes : 0; }
+
+extern "C" hs_status hs_plan_fft_counts(const hs_plan* p, int* n_fft, int* n_ifft) {
+  if (!p) return fail(HS_ERR_PARAMETER, "null plan");
+  if (n_fft) *n_fft = p->n_in;
+  if (n_ifft) *n_ifft = p->n_out;
+  return HS_OK;
+}
+
+extern "C" hs_status hs_plan_real_parts(hs_plan* p, double* kernel_part, double* correction_part, int mem) {
+  if (!p) return fail(HS_ERR_PARAMETER, "null plan");
+  const size_t bytes = 24 * (size_t)p->prm.n_targets;
+  const cudaMemcpyKind k = mem == HS_MEM_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+  if (bytes && kernel_part) HS_CUDA(cudaMemcpyAsync(kernel_part, p->uk, bytes, k, p->ctx->stream));
+  if (bytes && correction_part) HS_CUDA(cudaMemcpyAsync(correction_part, p->uc, bytes, k, p->ctx->stream));
+  HS_CUDA(cudaStreamSynchronize(p->ctx->stream));
+  return HS_OK;
+}
+
+extern "C" hs_status hs_plan_set_table(hs_plan* p, int table_kind, const double* samples, int mem) {
+  if (!p || !samples) return fail(HS_ERR_PARAMETER, "null argument");
+  double* dst = table_kind == HS_BIHARMONIC ? p->tabB : p->tabH;
+  if (!dst) return HS_OK;  // not needed by this kind/geometry
+  hs_ctx* ctx = p->ctx;
+  const int64_t pd[3] = {p->prm.padded[0], p->prm.padded[1], p->prm.padded[2]};
+  const size_t full = (size_t)pd[0] * pd[1] * pd[2];
+  const double* src = samples;
+  double* tmp = nullptr;
+  if (mem == HS_MEM_HOST) {
+    HS_CUDA(cudaMallocAsync(&tmp, full * sizeof(double), ctx->stream));
+    HS_CUDA(cudaMemcpyAsync(tmp, samples, full * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    src = tmp;
+  }
+  hs_status st = launch_take_half(ctx, src, pd, dst);
+  if (tmp) cudaFreeAsync(tmp, ctx->stream);
+  HS_TRY(st);
+  HS_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (table_kind == HS_BIHARMONIC) p->have_B = true;
+  else p->have_H = true;
+  return HS_OK;
+}
+
+namespace hs {
+// precompute_greens into a half-spectrum real table (ewald_fourier.py:207-244)
+hs_status greens_half_table(hs_ctx* ctx, int kind, double R, double h, const int64_t big[3], const int64_t dims[3],
+                            const int64_t guards[3], const int64_t pd[3], double* half_out) {
+  cudaStream_t st = ctx->stream;
+  const int64_t nzb = big[2] / 2 + 1;
+  const size_t nbh = (size_t)big[0] * big[1] * nzb, nbr = (size_t)big[0] * big[1] * big[2];
+  const size_t ncrop = (size_t)pd[0] * pd[1] * pd[2], nch = (size_t)pd[0] * pd[1] * (pd[2] / 2 + 1);
+  double2* hat = nullptr;
+  double* field = nullptr;
+  void* ws = nullptr;
+  cufftHandle pb = 0, pf = 0;
+  hs_status rs = HS_OK;
+  auto cleanup = [&]() {
+    if (pb) cufftDestroy(pb);
+    if (pf) cufftDestroy(pf);
+    if (hat) cudaFree(hat);
+    if (field) cudaFree(field);
+    if (ws) cudaFree(ws);
+  };
+  do {
+    if (cudaMalloc(&hat, std::max(nbh * sizeof(double2), ncrop * sizeof(double))) != cudaSuccess ||
+        cudaMalloc(&field, std::max(nbr, nch * 2) * sizeof(double)) != cudaSuccess) {
+      cudaGetLastError();
+      rs = fail(HS_ERR_RESOURCE, "precompute: big-grid allocation failed");
+      break;
+    }
+    if ((rs = launch_greens_hat(ctx, kind, R, h, big, hat)) != HS_OK) break;
+    long long nb[3] = {big[0], big[1], big[2]};
+    size_t w1 = 0, w2 = 0;
+    cufftCreate(&pb);
+    cufftSetAutoAllocation(pb, 0);
+    if (cufftMakePlanMany64(pb, 3, nb, nullptr, 1, 0, nullptr, 1, 0, CUFFT_Z2D, 1, &w1) != CUFFT_SUCCESS) {
+      rs = fail(HS_ERR_RESOURCE, "precompute: cuFFT Z2D plan failed");
+      break;
+    }
+    long long np[3] = {pd[0], pd[1], pd[2]};
+    cufftCreate(&pf);
+    cufftSetAutoAllocation(pf, 0);
+    if (cufftMakePlanMany64(pf, 3, np, nullptr, 1, 0, nullptr, 1, 0, CUFFT_D2Z, 1, &w2) != CUFFT_SUCCESS) {
+      rs = fail(HS_ERR_RESOURCE, "precompute: cuFFT D2Z plan failed");
+      break;
+    }
+    if (cudaMalloc(&ws, std::max<size_t>(std::max(w1, w2), 16)) != cudaSuccess) {
+      cudaGetLastError();
+      rs = fail(HS_ERR_RESOURCE, "precompute: cuFFT work area allocation failed");
+      break;
+    }
+    cufftSetWorkArea(pb, ws);
+    cufftSetWorkArea(pf, ws);
+    cufftSetStream(pb, st);
+    cufftSetStream(pf, st);
+    if (cufftExecZ2D(pb, (cufftDoubleComplex*)hat, field) != CUFFT_SUCCESS) {
+      rs = fail(HS_ERR_RESOURCE, "precompute: Z2D failed");
+      break;
+    }
+    // irfftn normalisation 1/prod(big); crop to the guarded torus (keep d+g per side)
+    int64_t keep[3];
+    for (int k = 0; k < 3; ++k) keep[k] = dims[k] + guards[k];
+    const double scale = 1.0 / ((double)big[0] * (double)big[1] * (double)big[2]);
+    double* crop = (double*)hat;  // reuse
+    if ((rs = launch_crop(ctx, field, big, keep, scale, crop)) != HS_OK) break;
+    double2* cs = (double2*)field;
+    if (cufftExecD2Z(pf, crop, (cufftDoubleComplex*)cs) != CUFFT_SUCCESS) {
+      rs = fail(HS_ERR_RESOURCE, "precompute: D2Z failed");
+      break;
+    }
+    if ((rs = launch_real_part(ctx, cs, (int64_t)nch, half_out)) != HS_OK) break;
+    if (cudaStreamSynchronize(st) != cudaSuccess) {
+      rs = fail(HS_ERR_CUDA, "precompute: stream sync failed");
+      break;
+    }
+  } while (false);
+  cleanup();
+  return rs;
+}
+}  // namespace hs
+
+extern "C" hs_status hs_plan_build_tables(hs_plan* p, const int64_t big[3], double R, const int64_t guards[3]) {
+  if (!p) return fail(HS_ERR_PARAMETER, "null plan");
+  const int64_t pd[3] = {p->prm.padded[0], p->prm.padded[1], p->prm.padded[2]};
+  if (p->tabB) {
+    HS_TRY(greens_half_table(p->ctx, HS_BIHARMONIC, R, p->prm.h, big, p->prm.dims, guards, pd, p->tabB));
+    p->have_B = true;
+  }
+  if (p->tabH) {
+    HS_TRY(greens_half_table(p->ctx, HS_HARMONIC, R, p->prm.h, big, p->prm.dims, guards, pd, p->tabH));
+    p->have_H = true;
+  }
+  return HS_OK;
+}
+
+namespace {
+
+hs_status sort_points_by_cell(hs_plan* p, const double* pos, int n_src, int n_total, int mirror, int check,
+                              int* order, int* start) {
+  hs_ctx* ctx = p->ctx;
+  HS_TRY(launch_cell_keys(ctx, pos, n_src, n_total, mirror, p->cg, check, p->keys));
+  return counting_sort(ctx, p->keys, n_total, (int)p->cg.ncell(), order, start, p->work);
+}
+
+hs_status sort_points_by_bin(hs_plan* p, const double* pos, int n_src, int n_total, int mode, int* order,
+                             int* start) {
+  hs_ctx* ctx = p->ctx;
+  HS_TRY(launch_grid_keys(ctx, pos, n_src, n_total, mode, p->gg, p->keys));
+  return counting_sort(ctx, p->keys, n_total, p->nbins, order, start, p->work);
+}
+
+}  // namespace
+
+extern "C" hs_status hs_plan_execute(hs_plan* p, const double* positions, const double* sa, const double* sb,
+                                     const double* targets, const int64_t* tcols, double* u, double* u_real,
+                                     double* u_fourier, int mem, int what, double* times) {
+  if (!p || !positions || !sa || !u) return fail(HS_ERR_PARAMETER, "null argument");
+  hs_ctx* ctx = p->ctx;
+  cudaStream_t st = ctx->stream;
+  const hs_params& prm = p->prm;
+  const int n = (int)prm.n, nt = (int)prm.n_targets;
+  const int kind = prm.kind;
+  if (kind != HS_STOKESLET && !sb) return fail(HS_ERR_PARAMETER, "stresslet/rotlet need q");
+  if (!prm.targets_are_sources && nt > 0 && !targets) return fail(HS_ERR_PARAMETER, "targets required");
+  if ((what & 2) && (p->tabB && !p->have_B)) return fail(HS_ERR_CONFIG, "missing biharmonic table");
+  if ((what & 2) && (p->tabH && !p->have_H)) return fail(HS_ERR_CONFIG, "missing harmonic table");
+  HS_CUDA(cudaSetDevice(ctx->device));
+  HS_TRY(ctx_reset_flags(ctx));
+  cudaEvent_t* ev = p->ev;
+  HS_CUDA(cudaEventRecord(ev[0], st));
+  // ---- inputs
+  const double *pos = positions, *fa = sa, *fb = sb, *tp = targets;
+  const long long* tc = (const long long*)tcols;
+  if (mem == HS_MEM_HOST) {
+    HS_CUDA(cudaMemcpyAsync(p->d_pos, positions, 24 * (size_t)n, cudaMemcpyHostToDevice, st));
+    HS_CUDA(cudaMemcpyAsync(p->d_sa, sa, 24 * (size_t)n, cudaMemcpyHostToDevice, st));
+    pos = p->d_pos;
+    fa = p->d_sa;
+    if (kind != HS_STOKESLET) {
+      HS_CUDA(cudaMemcpyAsync(p->d_sb, sb, 24 * (size_t)n, cudaMemcpyHostToDevice, st));
+      fb = p->d_sb;
+    }
+    if (!prm.targets_are_sources && nt > 0) {
+      HS_CUDA(cudaMemcpyAsync(p->d_tgt, targets, 24 * (size_t)nt, cudaMemcpyHostToDevice, st));
+      tp = p->d_tgt;
+      if (tcols) {
+        HS_CUDA(cudaMemcpyAsync(p->d_tcols, tcols, 8 * (size_t)nt, cudaMemcpyHostToDevice, st));
+        tc = p->d_tcols;
+      }
+    }
+  }
+  if (prm.targets_are_sources) tp = pos;
+  const int tcol_identity = prm.targets_are_sources ? 1 : 0;
+  HS_CUDA(cudaEventRecord(ev[1], st));
+  // ---- real space
+  const bool do_real = (what & 1) && prm.rc > 0;
+  if (do_real) {
+    HS_TRY(sort_points_by_cell(p, pos, n, p->n_comb, p->half ? 1 : 0, 1, p->order, p->start));
+    k_pair_records<<<grid_size(ctx, p->n_comb), 256, 0, st>>>(kind, p->half, p->order, p->n_comb, n, pos, fa, fb,
+                                                              p->P, p->A, p->B);
+    HS_LAUNCHED(ctx);
+    if (nt > 0) {
+      HS_TRY(sort_points_by_cell(p, tp, nt, nt, 0, 0, p->t_order, p->t_start));
+      k_target_records<<<grid_size(ctx, nt), 256, 0, st>>>(p->t_order, nt, tp, tc, tcol_identity, p->TP, p->torig);
+      HS_LAUNCHED(ctx);
+      HS_CUDA(cudaMemsetAsync(p->n_cells_d, 0, sizeof(int), st));
+      const int ncell = (int)p->cg.ncell();
+      k_nonempty_cells<<<grid_size(ctx, ncell), 256, 0, st>>>(p->t_start, ncell, p->cells, p->n_cells_d);
+      HS_LAUNCHED(ctx);
+      PairArgs a{};
+      a.P = p->P;
+      a.A = p->A;
+      a.B = p->B;
+      a.start = p->start;
+      a.TP = p->TP;
+      a.torig = p->torig;
+      a.t_start = p->t_start;
+      a.cells = p->cells;
+      a.n_cells = std::min(ncell, nt);
+      a.n_cells_d = p->n_cells_d;
+      for (int k = 0; k < 3; ++k) a.dims[k] = (int)p->cg.dims[k];
+      a.xi = prm.xi;
+      a.rc2 = prm.rc * prm.rc;
+      a.n_real = n;
+      a.kind = kind | (p->half ? 16 : 0);
+      a.self_f = kind == HS_STOKESLET ? fa : nullptr;
+      a.u = p->u_real;
+      a.uk = p->uk;
+      a.uc = p->uc;
+      a.flags = ctx->d_flags;
+      HS_TRY(launch_pair(ctx, a));
+    }
+  } else if (nt > 0) {
+    HS_CUDA(cudaMemsetAsync(p->u_real, 0, 24 * (size_t)nt, st));
+    HS_CUDA(cudaMemsetAsync(p->uk, 0, 24 * (size_t)nt, st));
+    HS_CUDA(cudaMemsetAsync(p->uc, 0, 24 * (size_t)nt, st));
+    if ((what & 1) && kind == HS_STOKESLET) {
+      // rc = 0: no pairs, but the self term is still added (ewald_real.py:444-449)
+      k_self_term<<<grid_size(ctx, nt), 256, 0, st>>>(nt, tp, tc, tcol_identity, n, prm.xi, fa, p->u_real);
+      HS_LAUNCHED(ctx);
+    }
+  }
+  HS_CUDA(cudaEventRecord(ev[2], st));
+  // ---- Fourier space
+  const bool do_four = (what & 2) != 0;
+  if (do_four) {
+    // kernel sources [y; y^I] (or y) and wall-correction sources y^I
+    HS_TRY(sort_points_by_bin(p, pos, n, p->n_comb, p->half ? 1 : 0, p->bk_order, p->bk_start));
+    k_spread_records<<<grid_size(ctx, p->n_comb), 256, 0, st>>>(kind, p->half, 0, p->bk_order, p->n_comb, n, pos,
+                                                                fa, fb, p->nk, p->SPk, p->SWk);
+    HS_LAUNCHED(ctx);
+    if (p->nc) {
+      HS_TRY(sort_points_by_bin(p, pos, n, n, 2, p->bc_order, p->bc_start));
+      k_spread_records<<<grid_size(ctx, n), 256, 0, st>>>(kind, p->half, 1, p->bc_order, n, n, pos, fa, fb, p->nc,
+                                                          p->SPc, p->SWc);
+      HS_LAUNCHED(ctx);
+    }
+    HS_TRY(launch_spread(ctx, p->SPk, p->SWk, p->n_comb, p->nk, p->bk_start, p->gg, p->grid_in));
+    if (p->nc)
+      HS_TRY(launch_spread(ctx, p->SPc, p->SWc, n, p->nc, p->bc_start, p->gg,
+                           p->grid_in + (size_t)p->nk * p->n_real_grid));
+    HS_CUDA(cudaEventRecord(ev[3], st));
+    if (cufftExecD2Z(p->fwd, p->grid_in, (cufftDoubleComplex*)p->spec) != CUFFT_SUCCESS)
+      return fail(HS_ERR_CUDA, "cuFFT D2Z failed");
+    HS_CUDA(cudaEventRecord(ev[4], st));
+    HS_TRY(launch_kscale(ctx, kind, p->half, p->kg, p->tabB, p->tabH, p->spec, p->n_half));
+    HS_CUDA(cudaEventRecord(ev[5], st));
+    if (cufftExecZ2D(p->inv, (cufftDoubleComplex*)p->spec, p->grid_out) != CUFFT_SUCCESS)
+      return fail(HS_ERR_CUDA, "cuFFT Z2D failed");
+    HS_CUDA(cudaEventRecord(ev[6], st));
+    if (nt > 0) {
+      HS_TRY(sort_points_by_bin(p, tp, nt, nt, 0, p->bt_order, p->bt_start));
+      k_gather_records<<<grid_size(ctx, nt), 256, 0, st>>>(p->bt_order, nt, tp, p->TG, p->tg_orig);
+      HS_LAUNCHED(ctx);
+      HS_TRY(launch_gather_fourier(ctx, p->TG, p->tg_orig, nt, p->half ? 1 : 0, p->gg, p->grid_out, p->u_four, p->u,
+                                   p->u_real));
+    }
+  } else {
+    for (int k = 3; k <= 6; ++k) HS_CUDA(cudaEventRecord(ev[k], st));
+    if (nt > 0) {
+      HS_CUDA(cudaMemsetAsync(p->u_four, 0, 24 * (size_t)nt, st));
+      HS_CUDA(cudaMemcpyAsync(p->u, p->u_real, 24 * (size_t)nt, cudaMemcpyDeviceToDevice, st));
+    }
+  }
+  HS_CUDA(cudaEventRecord(ev[7], st));
+  // ---- outputs
+  const cudaMemcpyKind ok = mem == HS_MEM_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+  if (nt > 0) {
+    HS_CUDA(cudaMemcpyAsync(u, p->u, 24 * (size_t)nt, ok, st));
+    if (u_real) HS_CUDA(cudaMemcpyAsync(u_real, p->u_real, 24 * (size_t)nt, ok, st));
+    if (u_fourier) HS_CUDA(cudaMemcpyAsync(u_fourier, p->u_four, 24 * (size_t)nt, ok, st));
+  }
+  HS_CUDA(cudaEventRecord(ev[8], st));
+  HS_CUDA(cudaStreamSynchronize(st));
+  HS_TRY(ctx_check_flags(ctx, "hs_plan_execute"));
+  if (times) {
+    float ms[9] = {0};
+    for (int k = 0; k < 8; ++k) cudaEventElapsedTime(&ms[k], ev[k], ev[k + 1]);
+    float tot = 0;
+    cudaEventElapsedTime(&tot, ev[0], ev[8]);
+    float fourier = 0;
+    cudaEventElapsedTime(&fourier, ev[2], ev[7]);
+    // [gridding, fft, scale, ifft, gather, real, fourier, prep, total, io]
+    times[0] = ms[2];
+    times[1] = ms[3];
+    times[2] = ms[4];
+    times[3] = ms[5];
+    times[4] = ms[6];
+    times[5] = ms[1];
+    times[6] = fourier;
+    times[7] = ms[0];
+    times[8] = tot;
+    times[9] = ms[7] + ms[0];
+  }
+  return HS_OK;
+}
