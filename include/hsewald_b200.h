@@ -123,8 +123,9 @@ hs_status hs_plan_build_tables(hs_plan* plan, const int64_t big[3], double R, co
  *   targets (n_targets,3) or NULL when targets_are_sources;
  *   tcols int64[n_targets] = target_indices (or NULL: -1 for all, no self term);
  *   u (n_targets,3) = real + fourier; u_real / u_fourier optional (NULL).
- *   times (optional, 10 doubles, milliseconds, CUDA events):
- *     [gridding, fft, scale, ifft, gather, real, fourier, prep, total, unused]
+ *   times (optional, 16 doubles, milliseconds, CUDA events):
+ *     [gridding, fft, scale, ifft, gather, real, fourier, h2d, total, io,
+ *      k_pair, k_spread, k_gather, k_scale (kernel-only), accepted pairs, accepted image pairs]
  *   what: bit 0 = real part, bit 1 = Fourier part (3 = full sum). */
 hs_status hs_plan_execute(hs_plan* plan, const double* positions, const double* sa, const double* sb,
                           const double* targets, const int64_t* tcols, double* u, double* u_real,

@@ -17,7 +17,8 @@ import numpy as np
 from . import _lib
 from .errors import ParameterError
 
-TIME_KEYS = ("gridding", "fft", "scale", "ifft", "gather", "real", "fourier", "prep", "total", "io")
+TIME_KEYS = ("gridding", "fft", "scale", "ifft", "gather", "real", "fourier", "prep", "total", "io",
+             "k_pair", "k_spread", "k_gather", "k_scale", "pairs", "image_pairs")
 
 
 def _is_torch(a) -> bool:
@@ -115,7 +116,7 @@ class Evaluator:
         """Run the plan.  Host (NumPy) inputs -> NumPy outputs; torch CUDA inputs -> torch outputs.
 
         Returns (u, u_real, u_fourier, times_ms dict)."""
-        times = (C.c_double * 10)()
+        times = (C.c_double * 16)()
         if _is_torch(positions):
             return self._execute_torch(positions, sa, sb, targets, tcols, what, times, out)
         pos = _host_f64(positions)

@@ -76,6 +76,7 @@ struct PairArgs {
   double* uk;         // optional (nt,3) kernel part
   double* uc;         // optional (nt,3) correction part
   unsigned* flags;
+  unsigned long long* counts;  // [accepted pairs, accepted image pairs] (optional)
 };
 hs_status launch_pair(hs_ctx* ctx, const PairArgs& a);
 hs_status launch_direct(hs_ctx* ctx, int kind, int half, int n_real, int n_src, const double4* P,

@@ -195,6 +195,7 @@ __global__ void __launch_bounds__(PT_WARPS * 32) k_pair(const PairArgs a) {
         for (int q = 0; q < 6; ++q) acc[g][q] = 0.0;
       }
       bool singular = false;
+      unsigned long long n_acc = 0, n_img = 0;
 
       for (int c0 = 0; c0 < ncand; c0 += PT_K) {
         __syncthreads();
@@ -231,6 +232,8 @@ __global__ void __launch_bounds__(PT_WARPS * 32) k_pair(const PairArgs a) {
             const unsigned m = __ballot_sync(0xffffffffu, ok);
             if (ok) sq[warp][g][qlen[g] + __popc(m & lt_mask)] = (unsigned short)j;
             qlen[g] += __popc(m);
+            n_acc += __popc(m);
+            if (HALF) n_img += __popc(m & __ballot_sync(0xffffffffu, ok && sid >= a.n_real));
             if (qlen[g] >= 32) {
               __syncwarp();
               const int jj = sq[warp][g][qlen[g] - 32 + lane];
@@ -264,6 +267,10 @@ __global__ void __launch_bounds__(PT_WARPS * 32) k_pair(const PairArgs a) {
         }
       }
       if (singular) atomicOr(a.flags, FLAG_SINGULAR);
+      if (a.counts && lane == 0) {
+        atomicAdd(&a.counts[0], n_acc);
+        atomicAdd(&a.counts[1], n_img);
+      }
 #pragma unroll
       for (int g = 0; g < PT_G; ++g) {
         double r[6];

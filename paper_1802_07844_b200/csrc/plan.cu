@@ -236,7 +236,8 @@ struct hs_plan {
   void* fft_work = nullptr;
   // outputs
   double *u = nullptr, *u_real = nullptr, *u_four = nullptr, *uk = nullptr, *uc = nullptr;
-  cudaEvent_t ev[12] = {};
+  unsigned long long* pair_counts = nullptr;
+  cudaEvent_t ev[16] = {};
 };
 
 namespace {
@@ -381,6 +382,7 @@ extern "C" hs_status hs_plan_create(hs_ctx* ctx, const hs_params* prm, hs_plan**
   A_(3 * (size_t)std::max(nt, 1), p->u_real, true);
   A_(3 * (size_t)std::max(nt, 1), p->u_four, true);
   A_(3 * (size_t)std::max(nt, 1), p->uk, true);
+  A_(2, p->pair_counts, true);
   A_(3 * (size_t)std::max(nt, 1), p->uc, true);
 #undef A_
   // ---- cuFFT plans (batched over channels, shared work area)
@@ -617,6 +619,7 @@ extern "C" hs_status hs_plan_execute(hs_plan* p, const double* positions, const 
   HS_CUDA(cudaEventRecord(ev[1], st));
   // ---- real space
   const bool do_real = (what & 1) && prm.rc > 0;
+  bool pair_timed = false, spread_timed = false, gather_timed = false;
   if (do_real) {
     HS_TRY(sort_points_by_cell(p, pos, n, p->n_comb, p->half ? 1 : 0, 1, p->order, p->start));
     k_pair_records<<<grid_size(ctx, p->n_comb), 256, 0, st>>>(kind, p->half, p->order, p->n_comb, n, pos, fa, fb,
@@ -651,7 +654,12 @@ extern "C" hs_status hs_plan_execute(hs_plan* p, const double* positions, const 
       a.uk = p->uk;
       a.uc = p->uc;
       a.flags = ctx->d_flags;
+      a.counts = p->pair_counts;
+      HS_CUDA(cudaMemsetAsync(p->pair_counts, 0, 2 * sizeof(unsigned long long), st));
+      HS_CUDA(cudaEventRecord(ev[9], st));
       HS_TRY(launch_pair(ctx, a));
+      HS_CUDA(cudaEventRecord(ev[10], st));
+      pair_timed = true;
     }
   } else if (nt > 0) {
     HS_CUDA(cudaMemsetAsync(p->u_real, 0, 24 * (size_t)nt, st));
@@ -678,10 +686,13 @@ extern "C" hs_status hs_plan_execute(hs_plan* p, const double* positions, const 
                                                           p->SPc, p->SWc);
       HS_LAUNCHED(ctx);
     }
+    HS_CUDA(cudaEventRecord(ev[11], st));
     HS_TRY(launch_spread(ctx, p->SPk, p->SWk, p->n_comb, p->nk, p->bk_start, p->gg, p->grid_in));
     if (p->nc)
       HS_TRY(launch_spread(ctx, p->SPc, p->SWc, n, p->nc, p->bc_start, p->gg,
                            p->grid_in + (size_t)p->nk * p->n_real_grid));
+    HS_CUDA(cudaEventRecord(ev[12], st));
+    spread_timed = true;
     HS_CUDA(cudaEventRecord(ev[3], st));
     if (cufftExecD2Z(p->fwd, p->grid_in, (cufftDoubleComplex*)p->spec) != CUFFT_SUCCESS)
       return fail(HS_ERR_CUDA, "cuFFT D2Z failed");
@@ -695,8 +706,11 @@ extern "C" hs_status hs_plan_execute(hs_plan* p, const double* positions, const 
       HS_TRY(sort_points_by_bin(p, tp, nt, nt, 0, p->bt_order, p->bt_start));
       k_gather_records<<<grid_size(ctx, nt), 256, 0, st>>>(p->bt_order, nt, tp, p->TG, p->tg_orig);
       HS_LAUNCHED(ctx);
+      HS_CUDA(cudaEventRecord(ev[13], st));
       HS_TRY(launch_gather_fourier(ctx, p->TG, p->tg_orig, nt, p->half ? 1 : 0, p->gg, p->grid_out, p->u_four, p->u,
                                    p->u_real));
+      HS_CUDA(cudaEventRecord(ev[14], st));
+      gather_timed = true;
     }
   } else {
     for (int k = 3; k <= 6; ++k) HS_CUDA(cudaEventRecord(ev[k], st));
@@ -734,6 +748,19 @@ extern "C" hs_status hs_plan_execute(hs_plan* p, const double* positions, const 
     times[7] = ms[0];
     times[8] = tot;
     times[9] = ms[7] + ms[0];
+    float kp = 0, ks = 0, kg = 0;
+    if (pair_timed) cudaEventElapsedTime(&kp, ev[9], ev[10]);
+    if (spread_timed) cudaEventElapsedTime(&ks, ev[11], ev[12]);
+    if (gather_timed) cudaEventElapsedTime(&kg, ev[13], ev[14]);
+    // kernel-only times: [10] pair, [11] spread, [12] gather, [13] scale
+    times[10] = kp;
+    times[11] = ks;
+    times[12] = kg;
+    times[13] = ms[4];
+    unsigned long long cnt[2] = {0, 0};
+    if (pair_timed) cudaMemcpy(cnt, p->pair_counts, sizeof(cnt), cudaMemcpyDeviceToHost);
+    times[14] = (double)cnt[0];  // accepted pairs
+    times[15] = (double)cnt[1];  // accepted image pairs
   }
   return HS_OK;
 }

@@ -1,0 +1,248 @@
+"""Parity of the CUDA path (through the C ABI) against the reference's golden
+vectors and the CPU oracle.  Tolerances: bit-exact for cell lists (integer
+work); relative L2 <= 1e-10 for FP64 velocities (BASELINE.json north star)."""
+
+import numpy as np
+import pytest
+
+from conftest import golden, rel_l2
+
+pytestmark = pytest.mark.gpu
+KINDS = ("stokeslet", "stresslet", "rotlet")
+TOL = 1e-10
+
+
+def _system(hs, d, key, L, geom="half"):
+    kw = dict(kind=None, geometry=geom, box_length=L, positions=d[f"{key}_pos"])
+    if f"{key}_f" in d:
+        kw.update(kind="stokeslet", f=d[f"{key}_f"])
+    else:
+        kw.update(g=d[f"{key}_g"], q=d[f"{key}_q"])
+    return kw
+
+
+def _mk(hs, kind, d, key, L, geom="half"):
+    kw = _system(hs, d, key, L, geom)
+    kw["kind"] = kind
+    return hs.PointSystem(**kw)
+
+
+def test_cell_lists_bit_exact(gpu):
+    d = golden("cell_lists")
+    for name in d["names"]:
+        c = gpu.build_cell_list(d[f"{name}_pts"], float(d[f"{name}_rc"]), (d[f"{name}_lo"], d[f"{name}_hi"]))
+        np.testing.assert_array_equal(c.dims, d[f"{name}_dims"])
+        np.testing.assert_array_equal(c.edge, d[f"{name}_edge"])
+        np.testing.assert_array_equal(c.order, d[f"{name}_order"], err_msg=name)
+        np.testing.assert_array_equal(c.start, d[f"{name}_start"], err_msg=name)
+
+
+def test_cell_list_large_vs_oracle(gpu, oracle):
+    from paper_1802_07844_b200.configs import make_system
+    s, _ = make_system("cfg4", n=200_000)     # wall-clustered: long segments
+    zz = np.vstack([s.positions, s.positions * [1, 1, -1]])
+    for rc in (0.0466, 0.02, 0.3):
+        c = gpu.build_cell_list(zz, 0.5 * rc, (np.array([0, 0, -1.0]), np.ones(3)))
+        dims, edge, order, start = oracle.build_cell_list(zz, 0.5 * rc, np.array([0, 0, -1.0]), np.ones(3))
+        np.testing.assert_array_equal(c.order, order)
+        np.testing.assert_array_equal(c.start, start)
+
+
+def test_cell_list_bounds_error(gpu):
+    with pytest.raises(gpu.GeometryError):
+        gpu.build_cell_list(np.array([[0.5, 0.5, 1.5]]), 0.2, (np.zeros(3), np.ones(3)))
+
+
+@pytest.mark.parametrize("kind", KINDS)
+@pytest.mark.parametrize("geom", ("half", "free"))
+def test_real_space_golden(gpu, kind, geom):
+    d = golden("real_space")
+    key = f"{kind}_{geom}"
+    s = _mk(gpu, kind, d, key, 2.0, geom)
+    r = gpu.real_space_sum(s, gpu.RealSpaceParams(xi=3.0, rc=0.9))
+    assert rel_l2(r.velocities, d[f"{key}_u"]) < 1e-12
+    assert rel_l2(r.parts["kernel"], d[f"{key}_uk"]) < 1e-12
+    if geom == "half":
+        assert rel_l2(r.parts["correction"], d[f"{key}_uc"]) < 1e-11
+
+
+@pytest.mark.parametrize("kind", KINDS)
+def test_real_space_separate_targets(gpu, kind):
+    d = golden("real_space")
+    s = _mk(gpu, kind, d, f"{kind}_half", 2.0)
+    r = gpu.real_space_sum(s, gpu.RealSpaceParams(xi=3.0, rc=0.9), targets=d[f"{kind}_targets_tg"])
+    assert rel_l2(r.velocities, d[f"{kind}_targets_u"]) < 1e-12
+
+
+@pytest.mark.parametrize("kind", KINDS)
+def test_real_space_vs_oracle_cfg_scale(gpu, oracle, kind):
+    from paper_1802_07844_b200.configs import make_system
+    name = {"stokeslet": "cfg2", "stresslet": "cfg3", "rotlet": "cfg4"}[kind]
+    s, _ = make_system(name, n=20_000)
+    xi, rc = 20.0, 0.2
+    r = gpu.real_space_sum(s, gpu.RealSpaceParams(xi=xi, rc=rc))
+    kw = {"f": s.f} if kind == "stokeslet" else {"g": s.g, "q": s.q}
+    u, uk, uc = oracle.real_space_sum(kind, "half", 1.0, s.positions, xi, rc, **kw)
+    assert rel_l2(r.velocities, u) < 1e-11
+    assert rel_l2(r.parts["correction"], uc) < 1e-10
+
+
+def test_real_space_singular(gpu):
+    pos = np.array([[0.5, 0.5, 0.5], [0.5, 0.5, 0.5], [0.2, 0.3, 0.4]])
+    s = gpu.PointSystem(kind="stokeslet", geometry="half", box_length=1.0, positions=pos, f=np.ones((3, 3)))
+    with pytest.raises(gpu.SingularityError):
+        gpu.real_space_sum(s, gpu.RealSpaceParams(xi=3.0, rc=0.4))
+
+
+def test_real_space_rc_zero_self_term(gpu):
+    d = golden("real_space")
+    s = _mk(gpu, "stokeslet", d, "stokeslet_half", 2.0)
+    r = gpu.real_space_sum(s, gpu.RealSpaceParams(xi=3.0, rc=0.0))
+    expect = -(4.0 * 3.0 / np.sqrt(np.pi)) * s.f / (8 * np.pi)
+    np.testing.assert_allclose(r.velocities, expect, rtol=1e-14)
+
+
+@pytest.mark.parametrize("geom", ("half", "free"))
+def test_spread_gather_golden(gpu, geom):
+    d = golden("gridding")
+    L, M, P, xi = d[f"{geom}_grid"]
+    g = gpu.GridSpec(L=L, M=int(M), P=int(P), xi=xi, geometry=geom)
+    grids = gpu.spread(d[f"{geom}_pts"], d[f"{geom}_w"], g)
+    assert rel_l2(grids, d[f"{geom}_grids"]) < 1e-13
+    out = gpu.gather(d[f"{geom}_F"], d[f"{geom}_pts"], g)
+    assert rel_l2(out, d[f"{geom}_gather"]) < 1e-13
+
+
+def test_spread_gather_adjoint_and_mass(gpu):
+    rng = np.random.default_rng(5)
+    g = gpu.GridSpec(L=2.0, M=40, P=24, xi=8.0, geometry="half")
+    pts = rng.uniform([0.2, 0.2, -1.8], [1.8, 1.8, 1.8], (500, 3))
+    w = rng.normal(size=(500, 3))
+    grids = gpu.spread(pts, w, g)
+    np.testing.assert_allclose(grids.sum(axis=(1, 2, 3)) * g.h**3, w.sum(axis=0), rtol=1e-7)
+    F = rng.normal(size=(3,) + g.dims)
+    lhs = np.sum(grids * F) * g.h**3
+    rhs = np.sum(w * gpu.gather(F, pts, g))
+    np.testing.assert_allclose(lhs, rhs, rtol=1e-12)
+
+
+def test_spread_out_of_grid(gpu):
+    g = gpu.GridSpec(L=1.0, M=16, P=8, xi=4.0, geometry="free")
+    with pytest.raises(gpu.GeometryError):
+        gpu.spread(np.array([[2.5, 0.5, 0.5]]), np.ones((1, 1)), g)
+
+
+@pytest.mark.parametrize("geom", ("half", "free"))
+@pytest.mark.parametrize("kind", ("harmonic", "biharmonic"))
+def test_tables_golden(gpu, geom, kind):
+    d = golden("tables")
+    g = gpu.GridSpec(L=1.0, M=6, P=6, xi=4.0, geometry=geom)
+    s = gpu.precompute_greens(kind, g).samples
+    np.testing.assert_array_equal(s.shape, d[f"{geom}_{kind}_shape"])
+    assert rel_l2(s[::3, ::3, ::3], d[f"{geom}_{kind}_sub"]) < 1e-12
+    np.testing.assert_allclose([s.sum(), (s * s).sum(), np.abs(s).max()], d[f"{geom}_{kind}_sum"], rtol=1e-11)
+
+
+def test_tables_vs_oracle_cfg1(gpu, oracle):
+    g = gpu.GridSpec(L=1.0, M=64, P=24, xi=12.0)
+    og = oracle.Grid(1.0, 64, 24, 12.0)
+    for kind in ("harmonic", "biharmonic"):
+        s = gpu.precompute_greens(kind, g, max_bytes=None).samples
+        assert rel_l2(s, oracle.precompute_greens(kind, og, workers=8)) < 1e-12
+
+
+@pytest.mark.parametrize("kind", KINDS)
+@pytest.mark.parametrize("geom", ("half", "free"))
+def test_fourier_golden(gpu, kind, geom):
+    d = golden("fourier")
+    key = f"{kind}_{geom}"
+    s = _mk(gpu, kind, d, key, 2.0, geom)
+    g = gpu.GridSpec(L=2.0, M=12, P=8, xi=3.0, geometry=geom)
+    r = gpu.fourier_space_sum(s, g)
+    assert rel_l2(r.velocities, d[f"{key}_u"]) < TOL
+    assert tuple(r.meta["fft_count_reference"]) == tuple(d[f"{key}_counts"])
+
+
+def test_ewald_cfg1_golden(gpu):
+    """BASELINE configs[0] through ewald_sum vs the reference's own output (rel L2 <= 1e-10)."""
+    d = golden("ewald")
+    s = gpu.PointSystem(kind="stokeslet", geometry="half", box_length=1.0, positions=d["cfg1_pos"], f=d["cfg1_f"])
+    r = gpu.ewald_sum(s, gpu.EwaldParams(xi=12.0, rc=0.35, M=64, P=24))
+    assert rel_l2(r.parts["real"], d["cfg1_ureal"]) < 1e-12
+    assert rel_l2(r.parts["fourier"], d["cfg1_ufourier"]) < TOL
+    assert rel_l2(r.velocities, d["cfg1_u"]) < TOL
+
+
+@pytest.mark.parametrize("kind", ("stresslet", "rotlet"))
+def test_ewald_kinds_golden(gpu, kind):
+    d = golden("ewald")
+    s = _mk(gpu, kind, d, kind, 1.0)
+    r = gpu.ewald_sum(s, gpu.EwaldParams(xi=8.0, rc=0.45, M=24, P=16))
+    assert rel_l2(r.velocities, d[f"{kind}_u"]) < TOL
+
+
+def test_ewald_mixed_targets_golden(gpu):
+    d = golden("ewald")
+    s = gpu.PointSystem(kind="stokeslet", geometry="half", box_length=1.0, positions=d["mixed_pos"], f=d["mixed_f"])
+    r = gpu.ewald_sum(s, gpu.EwaldParams(xi=8.0, rc=0.45, M=24, P=16), targets=d["mixed_tg"],
+                      target_indices=d["mixed_ti"])
+    assert rel_l2(r.velocities, d["mixed_u"]) < TOL
+
+
+@pytest.mark.parametrize("kind", KINDS)
+def test_direct_golden(gpu, kind):
+    d = golden("direct")
+    s = _mk(gpu, kind, d, kind, 2.0)
+    assert rel_l2(gpu.direct_sum_half(s).velocities, d[f"{kind}_u"]) < 1e-13
+    uw = gpu.direct_sum_half(s, targets=d[f"{kind}_wall"]).velocities
+    assert np.abs(uw).max() <= 1e-12 * np.abs(d[f"{kind}_u"]).max()   # no-slip at the wall
+    sf = _mk(gpu, kind, d, f"{kind}_free", 2.0, "free")
+    assert rel_l2(gpu.direct_sum_free(sf).velocities, d[f"{kind}_free_u"]) < 1e-13
+
+
+@pytest.mark.parametrize("kind", KINDS)
+def test_ewald_vs_direct_and_oracle_2e4(gpu, oracle, kind):
+    """Moderate size: GPU ewald vs CPU oracle (same algorithm) and vs direct sum."""
+    from paper_1802_07844_b200.configs import make_system
+    name = {"stokeslet": "cfg2", "stresslet": "cfg3", "rotlet": "cfg4"}[kind]
+    s, _ = make_system(name, n=20_000)
+    xi, rc, M, P = 20.8, 0.17, 80, 24
+    r = gpu.ewald_sum(s, gpu.EwaldParams(xi=xi, rc=rc, M=M, P=P))
+    g = oracle.Grid(1.0, M, P, xi)
+    tabs = {t: oracle.precompute_greens(t, g, workers=8) for t in oracle.table_kinds_for(kind, "half")}
+    kw = {"f": s.f} if kind == "stokeslet" else {"g": s.g, "q": s.q}
+    sub = np.arange(0, s.n, 97)
+    u_or, _, _ = oracle.ewald_sum(kind, "half", 1.0, s.positions, xi, rc, M, P, tabs, targets=s.positions[sub],
+                                  target_indices=sub, workers=8, **kw)
+    assert rel_l2(r.velocities[sub], u_or) < TOL
+    ud = gpu.direct_sum_half(s, targets=s.positions[sub], target_indices=sub).velocities
+    assert rel_l2(r.velocities[sub], ud) < 2e-5   # truncation error at xi*rc = 3.5
+
+
+def test_fourier_linearity_full_size(gpu):
+    """Size-independent property at the headline grid: Fourier part is linear in the strengths."""
+    from paper_1802_07844_b200.configs import make_system
+    s, _ = make_system("HL", n=200_000)
+    g = gpu.GridSpec(L=1.0, M=192, P=24, xi=49.92)
+    u1 = gpu.fourier_space_sum(s, g).velocities
+    u3 = gpu.fourier_space_sum(s.scaled(-3.0), g).velocities
+    assert rel_l2(u3, -3.0 * u1) < 1e-13
+
+
+def test_ewald_deterministic(gpu):
+    from paper_1802_07844_b200.configs import make_system
+    s, _ = make_system("cfg2", n=30_000)
+    p = gpu.EwaldParams(xi=20.8, rc=0.17, M=80, P=24)
+    a = gpu.ewald_sum(s, p).velocities
+    b = gpu.ewald_sum(s, p).velocities
+    np.testing.assert_array_equal(a, b)
+
+
+def test_missing_table_rejected(gpu):
+    d = golden("fourier")
+    s = _mk(gpu, "rotlet", d, "rotlet_half", 2.0)
+    g1 = gpu.GridSpec(L=2.0, M=12, P=8, xi=3.0)
+    g2 = gpu.GridSpec(L=2.0, M=16, P=8, xi=3.0)
+    tabs = gpu.get_tables("rotlet", g1)
+    with pytest.raises(gpu.ConfigError):
+        gpu.fourier_space_sum(s, g2, tables=tabs)
