@@ -125,9 +125,10 @@ class Evaluator:
         nt = self.n_targets
         tg = _host_f64(targets) if targets is not None else None
         tc = np.ascontiguousarray(np.asarray(tcols, dtype=np.int64)) if tcols is not None else None
-        u = np.empty((nt, 3))
-        ur = np.empty((nt, 3))
-        uf = np.empty((nt, 3))
+        if out is not None:   # caller-provided (e.g. pinned) host buffers; parts may be None
+            u, ur, uf = out
+        else:
+            u, ur, uf = np.empty((nt, 3)), np.empty((nt, 3)), np.empty((nt, 3))
         vp = lambda x: x.ctypes.data_as(C.c_void_p) if x is not None else None  # noqa: E731
         self.ctx.bind_stream(None)
         st = self.lib.hs_plan_execute(self.handle, vp(pos), vp(a), vp(b), vp(tg), vp(tc), vp(u), vp(ur), vp(uf),
