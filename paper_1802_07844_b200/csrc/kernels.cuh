@@ -7,6 +7,8 @@ namespace hs {
 // sort.cu
 hs_status counting_sort(hs_ctx* ctx, const int* keys, int n, int nb, int* order, int* start, int* work);
 inline size_t counting_sort_work_ints(int n, int nb) { return (size_t)2 * nb + 4 + (size_t)n; }
+// exclusive scan of in[0..n) into out[0..n] (out[n] = total); scratch: n + 2 ints
+hs_status exclusive_scan(hs_ctx* ctx, const int* in, int n, int* out, int* scratch);
 
 // ---------------------------------------------------------------------------
 // cell lists (cell_list.cu)
@@ -64,10 +66,16 @@ struct PairArgs {
   const double4* TP;  // cell-sorted targets: x, y, z, tcol
   const int* torig;   // output row of each sorted target
   const int* t_start; // target cell start, ncell+1
-  const int* cells;   // non-empty target cells
-  int n_cells;        // launch bound (>= actual count)
-  const int* n_cells_d;  // actual count (device)
+  const int2* items;  // work items (cell column, first sorted target)
+  int max_items;      // launch bound (>= actual count)
+  const int* n_items_d;  // actual count (device)
   int dims[3];
+  double cz_lo, cz_edge;  // z cell geometry: cz = clamp(trunc((z - cz_lo)/cz_edge))
+  __device__ __forceinline__ int cell_z(double z) const {
+    long long c = (long long)__ddiv_rn(__dsub_rn(z, cz_lo), cz_edge);
+    c = c < 0 ? 0 : c;
+    return (int)(c > dims[2] - 1 ? dims[2] - 1 : c);
+  }
   double xi, rc2;
   int n_real;         // combined index >= n_real -> image
   int kind;
@@ -79,6 +87,8 @@ struct PairArgs {
   unsigned long long* counts;  // [accepted pairs, accepted image pairs] (optional)
 };
 hs_status launch_pair(hs_ctx* ctx, const PairArgs& a);
+hs_status build_pair_items(hs_ctx* ctx, const int* t_start, int ncol, int nz, int* work, int2* items,
+                           const int** n_items_d);
 hs_status launch_direct(hs_ctx* ctx, int kind, int half, int n_real, int n_src, const double4* P,
                         const double4* A, const double4* B, int nt, const double4* TP, double* u);
 

@@ -25,11 +25,7 @@
 
 namespace hs {
 
-constexpr int PT_WARPS = 8;
-constexpr int PT_G = 4;      // targets per warp per pass
-constexpr int PT_K = 256;    // candidates staged per chunk
-constexpr int PT_Q = 64;     // queue capacity per (warp, target)
-constexpr int PT_MAXRUN = 25;
+constexpr int PT_MAXRUN = 25;  // 5 x 5 (x, y) cell columns
 
 struct PairConst {
   double xi, xi2, c2xs;  // xi, xi^2, 2 xi / sqrt(pi)
@@ -126,19 +122,34 @@ __device__ __forceinline__ double exact_r2(double d0, double d1, double d2) {
   return __dadd_rn(__dadd_rn(__dmul_rn(d0, d0), __dmul_rn(d1, d1)), __dmul_rn(d2, d2));
 }
 
+// ---------------------------------------------------------------------------
+// Queue design (used by launch_pair): one thread per target.  A CTA owns up to
+// PC_TG consecutive cell-sorted targets of ONE (ix,iy) cell column, so all its
+// targets share a compact candidate region: 25 z-runs over
+// [cz_first-2, cz_last+2].  Candidates are staged in shared memory and scanned
+// in lock-step with broadcast reads (one smem wavefront per candidate per
+// warp); each lane pushes the candidates IT accepts (exact reference test)
+// into a lane-private queue, and the warp evaluates queued pairs in rounds
+// whenever >= 3/4 of its lanes have work, so the erfc/exp-heavy evaluation
+// runs with nearly full SIMT utilisation while every thread accumulates only
+// its own target (no cross-lane reductions, no atomics, deterministic order).
+constexpr int PC_WARPS = 4;
+constexpr int PC_TG = PC_WARPS * 32;  // targets per work item
+constexpr int PC_K = 256;             // candidates per staged chunk
+constexpr int PC_Q = 64;              // per-lane queue capacity
+
 template <int KIND, bool HALF>
-__global__ void __launch_bounds__(PT_WARPS * 32) k_pair(const PairArgs a) {
-  __shared__ double4 sP[PT_K];
-  __shared__ double4 sA[PT_K];
-  __shared__ double4 sB[PT_K];
-  __shared__ unsigned short sq[PT_WARPS][PT_G][PT_Q];
+__global__ void __launch_bounds__(PC_TG) k_pair_q(const PairArgs a) {
+  __shared__ double4 sP[PC_K];
+  __shared__ double4 sA[PC_K];
+  constexpr bool kNeedB = (KIND == HS_STRESSLET) || (KIND == HS_ROTLET && HALF);
+  __shared__ double4 sB[kNeedB ? PC_K : 1];
+  __shared__ unsigned short sq[PC_WARPS][PC_Q][32];
   __shared__ int run_beg[PT_MAXRUN];
   __shared__ int run_pre[PT_MAXRUN + 1];
   __shared__ int s_nrun;
-  constexpr bool kNeedB = (KIND == HS_STRESSLET) || (KIND == HS_ROTLET && HALF);
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const unsigned lt_mask = (1u << lane) - 1u;
   const int nx = a.dims[0], ny = a.dims[1], nz = a.dims[2];
   PairConst pc;
   pc.xi = a.xi;
@@ -146,18 +157,22 @@ __global__ void __launch_bounds__(PT_WARPS * 32) k_pair(const PairArgs a) {
   pc.c2xs = 2.0 * a.xi / kSqrtPi;
   const double norm_k = (KIND == HS_ROTLET) ? 1.0 / (4.0 * kPi) : 1.0 / (8.0 * kPi);
   const double norm_c = 1.0 / (4.0 * kPi);
+  unsigned short(*q)[32] = sq[warp];
 
-  const int n_cells = *a.n_cells_d;
-  for (int cb = blockIdx.x; cb < n_cells; cb += gridDim.x) {
-    const int cell = a.cells[cb];
-    const int cz = cell % nz, cy = (cell / nz) % ny, cx = cell / (ny * nz);
+  const int n_items = *a.n_items_d;
+  for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+    const int2 item = a.items[it];
+    const int col = item.x, t0 = item.y;
+    const int t1 = min(t0 + PC_TG, a.t_start[(col + 1) * nz]);
+    const int ix = col / ny, iy = col % ny;
     __syncthreads();
     if (threadIdx.x == 0) {
+      const int cz0 = a.cell_z(a.TP[t0].z), cz1 = a.cell_z(a.TP[t1 - 1].z);
       int nr = 0, tot = 0;
-      const int zlo = max(cz - 2, 0), zhi = min(cz + 2, nz - 1);
-      for (int ix = max(cx - 2, 0); ix <= min(cx + 2, nx - 1); ++ix)
-        for (int iy = max(cy - 2, 0); iy <= min(cy + 2, ny - 1); ++iy) {
-          const int f = (ix * ny + iy) * nz;
+      const int zlo = max(cz0 - 2, 0), zhi = min(cz1 + 2, nz - 1);
+      for (int jx = max(ix - 2, 0); jx <= min(ix + 2, nx - 1); ++jx)
+        for (int jy = max(iy - 2, 0); jy <= min(iy + 2, ny - 1); ++jy) {
+          const int f = (jx * ny + jy) * nz;
           const int b = a.start[f + zlo], e = a.start[f + zhi + 1];
           if (e > b) {
             run_beg[nr] = b;
@@ -172,147 +187,150 @@ __global__ void __launch_bounds__(PT_WARPS * 32) k_pair(const PairArgs a) {
     __syncthreads();
     const int nrun = s_nrun;
     const int ncand = run_pre[nrun];
-    const int t_beg = a.t_start[cell];
-    const int t_cnt = a.t_start[cell + 1] - t_beg;
+    const int t = t0 + threadIdx.x;
+    const bool tvalid = t < t1;
+    const double4 T = a.TP[tvalid ? t : t0];
+    const long long tcol = tvalid ? (long long)T.w : -2;  // -2 never matches a source id
+    double acc[6] = {0, 0, 0, 0, 0, 0};
+    int qlen = 0;
+    bool singular = false;
+    unsigned long long n_acc = 0, n_img = 0;
 
-    for (int tb = 0; tb < t_cnt; tb += PT_WARPS * PT_G) {
-      double tx[PT_G], ty[PT_G], tz[PT_G];
-      long long tcol[PT_G];
-      bool tvalid[PT_G];
-      double acc[PT_G][6];
-      int qlen[PT_G];
-#pragma unroll
-      for (int g = 0; g < PT_G; ++g) {
-        const int ti = tb + warp * PT_G + g;
-        tvalid[g] = ti < t_cnt;
-        const double4 t = a.TP[t_beg + (tvalid[g] ? ti : 0)];
-        tx[g] = t.x;
-        ty[g] = t.y;
-        tz[g] = t.z;
-        tcol[g] = (long long)t.w;
-        qlen[g] = 0;
-#pragma unroll
-        for (int q = 0; q < 6; ++q) acc[g][q] = 0.0;
-      }
-      bool singular = false;
-      unsigned long long n_acc = 0, n_img = 0;
+    auto eval_one = [&](int jj) {
+      const double4 S = sP[jj];
+      const double4 A = sA[jj];
+      const double4 B = kNeedB ? sB[jj] : make_double4(0, 0, 0, 0);
+      const double e0 = T.x - S.x, e1 = T.y - S.y, e2 = T.z - S.z;
+      const double rr = exact_r2(e0, e1, e2);
+      const bool img = HALF && ((long long)S.w >= a.n_real);
+      if (img) ++n_img;
+      eval_pair<KIND, true>(pc, e0, e1, e2, rr, T.z, S, A, B, img, &acc[0], &acc[3]);
+    };
 
-      for (int c0 = 0; c0 < ncand; c0 += PT_K) {
-        __syncthreads();
-        {
-          const int j = threadIdx.x;
-          const int v = c0 + j;
-          if (j < PT_K) {
-            if (v < ncand) {
-              int r = 0;
-              while (r + 1 < nrun && run_pre[r + 1] <= v) ++r;
-              const int row = run_beg[r] + (v - run_pre[r]);
-              sP[j] = a.P[row];
-              sA[j] = a.A[row];
-              if (kNeedB) sB[j] = a.B[row];
-            }
-          }
+    for (int c0 = 0; c0 < ncand; c0 += PC_K) {
+      __syncthreads();
+      for (int j = threadIdx.x; j < PC_K; j += PC_TG) {
+        const int v = c0 + j;
+        if (v < ncand) {
+          int r = 0;
+          while (r + 1 < nrun && run_pre[r + 1] <= v) ++r;
+          const int row = run_beg[r] + (v - run_pre[r]);
+          sP[j] = a.P[row];
+          sA[j] = a.A[row];
+          if (kNeedB) sB[j] = a.B[row];
         }
-        __syncthreads();
-        const int nc = min(PT_K, ncand - c0);
-        for (int j0 = 0; j0 < nc; j0 += 32) {
-          const int j = j0 + lane;
-          const bool have = j < nc;
-          const double4 s = sP[have ? j : 0];
-          const long long sid = (long long)s.w;
-#pragma unroll
-          for (int g = 0; g < PT_G; ++g) {
-            const double d0 = __dsub_rn(tx[g], s.x), d1 = __dsub_rn(ty[g], s.y), d2 = __dsub_rn(tz[g], s.z);
-            const double r2 = exact_r2(d0, d1, d2);
-            bool ok = have && tvalid[g] && sid != tcol[g] && r2 <= a.rc2;
-            if (ok && r2 == 0.0) {
+      }
+      __syncthreads();
+      const int nc = min(PC_K, ncand - c0);
+      for (int j0 = 0; j0 < nc; j0 += 32) {
+        const int jn = min(32, nc - j0);
+#pragma unroll 4
+        for (int jj = 0; jj < jn; ++jj) {
+          const int j = j0 + jj;
+          const double4 S = sP[j];  // broadcast
+          const double d0 = __dsub_rn(T.x, S.x), d1 = __dsub_rn(T.y, S.y), d2 = __dsub_rn(T.z, S.z);
+          const double r2 = exact_r2(d0, d1, d2);
+          if (r2 <= a.rc2 && (long long)S.w != tcol && tvalid) {
+            if (r2 == 0.0) {
               singular = true;
-              ok = false;
-            }
-            const unsigned m = __ballot_sync(0xffffffffu, ok);
-            if (ok) sq[warp][g][qlen[g] + __popc(m & lt_mask)] = (unsigned short)j;
-            qlen[g] += __popc(m);
-            n_acc += __popc(m);
-            if (HALF) n_img += __popc(m & __ballot_sync(0xffffffffu, ok && sid >= a.n_real));
-            if (qlen[g] >= 32) {
-              __syncwarp();
-              const int jj = sq[warp][g][qlen[g] - 32 + lane];
-              const double4 S = sP[jj];
-              const double4 A = sA[jj];
-              const double4 B = kNeedB ? sB[jj] : make_double4(0, 0, 0, 0);
-              const double e0 = tx[g] - S.x, e1 = ty[g] - S.y, e2 = tz[g] - S.z;
-              const double rr = exact_r2(e0, e1, e2);
-              const bool img = HALF && ((long long)S.w >= a.n_real);
-              eval_pair<KIND, true>(pc, e0, e1, e2, rr, tz[g], S, A, B, img, &acc[g][0], &acc[g][3]);
-              qlen[g] -= 32;
-              __syncwarp();
+            } else {
+              q[qlen][lane] = (unsigned short)j;
+              ++qlen;
             }
           }
         }
-        // flush the partial queues before the chunk is overwritten
-#pragma unroll
-        for (int g = 0; g < PT_G; ++g) {
-          __syncwarp();
-          if (lane < qlen[g]) {
-            const int jj = sq[warp][g][lane];
-            const double4 S = sP[jj];
-            const double4 A = sA[jj];
-            const double4 B = kNeedB ? sB[jj] : make_double4(0, 0, 0, 0);
-            const double e0 = tx[g] - S.x, e1 = ty[g] - S.y, e2 = tz[g] - S.z;
-            const double rr = exact_r2(e0, e1, e2);
-            const bool img = HALF && ((long long)S.w >= a.n_real);
-            eval_pair<KIND, true>(pc, e0, e1, e2, rr, tz[g], S, A, B, img, &acc[g][0], &acc[g][3]);
+        // evaluate while most lanes have queued work (or a queue is close to full)
+        while (true) {
+          const unsigned busy = __ballot_sync(0xffffffffu, qlen > 0);
+          const unsigned mx = __reduce_max_sync(0xffffffffu, (unsigned)qlen);
+          if (__popc(busy) < 24 && mx <= PC_Q - 32) break;
+          if (qlen > 0) {
+            --qlen;
+            ++n_acc;
+            eval_one(q[qlen][lane]);
           }
-          qlen[g] = 0;
         }
       }
-      if (singular) atomicOr(a.flags, FLAG_SINGULAR);
-      if (a.counts && lane == 0) {
+      // drain before the chunk is overwritten
+      while (__any_sync(0xffffffffu, qlen > 0)) {
+        if (qlen > 0) {
+          --qlen;
+          ++n_acc;
+          eval_one(q[qlen][lane]);
+        }
+      }
+    }
+    if (singular) atomicOr(a.flags, FLAG_SINGULAR);
+    if (a.counts) {
+      n_acc = __reduce_add_sync(0xffffffffu, (unsigned)n_acc);
+      n_img = __reduce_add_sync(0xffffffffu, (unsigned)n_img);
+      if (lane == 0) {
         atomicAdd(&a.counts[0], n_acc);
         atomicAdd(&a.counts[1], n_img);
       }
+    }
+    if (tvalid) {
+      const int o = a.torig[t];
+      double u[3];
 #pragma unroll
-      for (int g = 0; g < PT_G; ++g) {
-        double r[6];
+      for (int k = 0; k < 3; ++k) u[k] = acc[k] * norm_k + acc[3 + k] * norm_c;
+      if (KIND == HS_STOKESLET && a.self_f != nullptr && tcol >= 0 && tcol < a.n_real) {
+        const double sc = -(4.0 * a.xi / kSqrtPi);
 #pragma unroll
-        for (int q = 0; q < 6; ++q) r[q] = warp_sum(acc[g][q]);
-        if (lane == 0 && tvalid[g]) {
-          const int ti = t_beg + tb + warp * PT_G + g;
-          const int o = a.torig[ti];
-          double u[3];
+        for (int k = 0; k < 3; ++k) u[k] += sc * a.self_f[3 * tcol + k] / (8.0 * kPi);
+      }
 #pragma unroll
-          for (int q = 0; q < 3; ++q) u[q] = r[q] * norm_k + r[3 + q] * norm_c;
-          if (KIND == HS_STOKESLET && a.self_f != nullptr && tcol[g] >= 0 && tcol[g] < a.n_real) {
-            // self term -(4 xi/sqrt(pi)) f / (8 pi)   (ewald_real.py:446-449)
-            const double sc = -(4.0 * a.xi / kSqrtPi);
+      for (int k = 0; k < 3; ++k) a.u[3 * o + k] = u[k];
+      if (a.uk) {
 #pragma unroll
-            for (int q = 0; q < 3; ++q) u[q] += sc * a.self_f[3 * tcol[g] + q] / (8.0 * kPi);
-          }
+        for (int k = 0; k < 3; ++k) a.uk[3 * o + k] = acc[k] * norm_k;
+      }
+      if (a.uc) {
 #pragma unroll
-          for (int q = 0; q < 3; ++q) a.u[3 * o + q] = u[q];
-          if (a.uk) {
-#pragma unroll
-            for (int q = 0; q < 3; ++q) a.uk[3 * o + q] = r[q] * norm_k;
-          }
-          if (a.uc) {
-#pragma unroll
-            for (int q = 0; q < 3; ++q) a.uc[3 * o + q] = r[3 + q] * norm_c;
-          }
-        }
+        for (int k = 0; k < 3; ++k) a.uc[3 * o + k] = acc[3 + k] * norm_c;
       }
     }
   }
 }
 
+// work items: (column, first target) for every group of PC_TG targets of a cell column
+__global__ void k_count_groups(const int* __restrict__ t_start, int ncol, int nz, int* __restrict__ cnt) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < ncol; c += gridDim.x * blockDim.x) {
+    const int n = t_start[(c + 1) * nz] - t_start[c * nz];
+    cnt[c] = (n + PC_TG - 1) / PC_TG;
+  }
+}
+
+__global__ void k_fill_items(const int* __restrict__ t_start, const int* __restrict__ gstart, int ncol, int nz,
+                             int2* __restrict__ items) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < ncol; c += gridDim.x * blockDim.x) {
+    const int b = t_start[c * nz];
+    for (int g = gstart[c]; g < gstart[c + 1]; ++g) items[g] = make_int2(c, b + (g - gstart[c]) * PC_TG);
+  }
+}
+
+hs_status build_pair_items(hs_ctx* ctx, const int* t_start, int ncol, int nz, int* work, int2* items,
+                           const int** n_items_d) {
+  int* cnt = work;             // ncol
+  int* gstart = work + ncol;   // ncol + 1
+  int* scratch = work + 2 * ncol + 1;
+  const int gs = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(ncol, 256), ctx->sm_count * 4));
+  k_count_groups<<<gs, 256, 0, ctx->stream>>>(t_start, ncol, nz, cnt);
+  HS_LAUNCHED(ctx);
+  HS_TRY(exclusive_scan(ctx, cnt, ncol, gstart, scratch));
+  k_fill_items<<<gs, 256, 0, ctx->stream>>>(t_start, gstart, ncol, nz, items);
+  HS_LAUNCHED(ctx);
+  *n_items_d = gstart + ncol;
+  return HS_OK;
+}
+
 hs_status launch_pair(hs_ctx* ctx, const PairArgs& a) {
-  if (a.n_cells == 0) return HS_OK;
-  const bool half = a.n_real >= 0;  // always true; geometry decided by B/P content
-  (void)half;
-  dim3 grid(a.n_cells), block(PT_WARPS * 32);
-  // HALF is encoded by the caller through a.kind >= 16
+  if (a.max_items == 0) return HS_OK;
   const int kind = a.kind & 15;
   const bool is_half = (a.kind & 16) != 0;
-#define HS_PAIR_CASE(K, H) k_pair<K, H><<<grid, block, 0, ctx->stream>>>(a)
+  // persistent-style grid: enough CTAs to fill the machine, looping over the device-side item count
+  const int grid = std::max(1, std::min(a.max_items, ctx->sm_count * 16));
+#define HS_PAIR_CASE(K, H) k_pair_q<K, H><<<grid, PC_TG, 0, ctx->stream>>>(a)
   if (is_half) {
     if (kind == HS_STOKESLET) HS_PAIR_CASE(HS_STOKESLET, true);
     else if (kind == HS_STRESSLET) HS_PAIR_CASE(HS_STRESSLET, true);

@@ -74,12 +74,6 @@ __global__ void k_target_records(const int* __restrict__ order, int nt, const do
   }
 }
 
-__global__ void k_nonempty_cells(const int* __restrict__ t_start, int ncell, int* __restrict__ cells,
-                                 int* __restrict__ count) {
-  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < ncell; c += gridDim.x * blockDim.x)
-    if (t_start[c + 1] > t_start[c]) cells[atomicAdd(count, 1)] = c;
-}
-
 // spread source records in bin order.  set 0: kernel sources [y; y^I]; set 1: images y^I
 // with wall channels.  W has nch doubles per row (see kspace.cu channel layout).
 __global__ void k_spread_records(int kind, int half, int set, const int* __restrict__ order, int n_rows, int n,
@@ -217,7 +211,8 @@ struct hs_plan {
   long long* d_tcols = nullptr;
   // real space
   int *keys = nullptr, *order = nullptr, *start = nullptr, *work = nullptr;
-  int *t_order = nullptr, *t_start = nullptr, *cells = nullptr, *n_cells_d = nullptr;
+  int *t_order = nullptr, *t_start = nullptr;
+  int2* items = nullptr;
   double4 *P = nullptr, *A = nullptr, *B = nullptr, *TP = nullptr;
   int* torig = nullptr;
   // Fourier
@@ -352,8 +347,7 @@ extern "C" hs_status hs_plan_create(hs_ctx* ctx, const hs_params* prm, hs_plan**
   A_(ncell + 1, p->start);
   A_(nt + 1, p->t_order);
   A_(ncell + 1, p->t_start);
-  A_(ncell, p->cells);
-  A_(1, p->n_cells_d);
+  A_((size_t)nt / 128 + (size_t)p->cg.dims[0] * p->cg.dims[1] + 2, p->items);
   A_(p->n_comb, p->P);
   A_(p->n_comb, p->A);
   A_(p->n_comb, p->B);
@@ -629,10 +623,9 @@ extern "C" hs_status hs_plan_execute(hs_plan* p, const double* positions, const 
       HS_TRY(sort_points_by_cell(p, tp, nt, nt, 0, 0, p->t_order, p->t_start));
       k_target_records<<<grid_size(ctx, nt), 256, 0, st>>>(p->t_order, nt, tp, tc, tcol_identity, p->TP, p->torig);
       HS_LAUNCHED(ctx);
-      HS_CUDA(cudaMemsetAsync(p->n_cells_d, 0, sizeof(int), st));
-      const int ncell = (int)p->cg.ncell();
-      k_nonempty_cells<<<grid_size(ctx, ncell), 256, 0, st>>>(p->t_start, ncell, p->cells, p->n_cells_d);
-      HS_LAUNCHED(ctx);
+      const int ncol = (int)(p->cg.dims[0] * p->cg.dims[1]);
+      const int* n_items_d = nullptr;
+      HS_TRY(build_pair_items(ctx, p->t_start, ncol, (int)p->cg.dims[2], p->work, p->items, &n_items_d));
       PairArgs a{};
       a.P = p->P;
       a.A = p->A;
@@ -641,10 +634,12 @@ extern "C" hs_status hs_plan_execute(hs_plan* p, const double* positions, const 
       a.TP = p->TP;
       a.torig = p->torig;
       a.t_start = p->t_start;
-      a.cells = p->cells;
-      a.n_cells = std::min(ncell, nt);
-      a.n_cells_d = p->n_cells_d;
+      a.items = p->items;
+      a.max_items = nt / 128 + ncol + 1;
+      a.n_items_d = n_items_d;
       for (int k = 0; k < 3; ++k) a.dims[k] = (int)p->cg.dims[k];
+      a.cz_lo = p->cg.lo[2];
+      a.cz_edge = p->cg.edge[2];
       a.xi = prm.xi;
       a.rc2 = prm.rc * prm.rc;
       a.n_real = n;

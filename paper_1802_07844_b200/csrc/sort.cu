@@ -160,4 +160,11 @@ hs_status counting_sort(hs_ctx* ctx, const int* keys, int n, int nb, int* order,
   return HS_OK;
 }
 
+hs_status exclusive_scan(hs_ctx* ctx, const int* in, int n, int* out, int* scratch) {
+  HS_CUDA(cudaMemsetAsync(scratch + n, 0, sizeof(int), ctx->stream));
+  k_scan<<<1, 1024, 0, ctx->stream>>>(in, n, out, scratch, scratch + n);
+  HS_LAUNCHED(ctx);
+  return HS_OK;
+}
+
 }  // namespace hs
