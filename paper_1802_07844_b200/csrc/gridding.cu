@@ -56,18 +56,76 @@ hs_status launch_grid_keys(hs_ctx* ctx, const double* pos, int n_src, int n, int
 }
 
 // ---------------------------------------------------------------------------
+// Spreading.  Per source, the window along each axis is
+//   w[a] = exp(-alpha (d0 - a h)^2) = E1 * E2^a * E3[a],
+//   E1 = exp(-alpha d0^2), E2 = exp(2 alpha d0 h), E3[a] = exp(-alpha h^2 a^2)
+// (d0 = distance to the first support node, _gridding.py:24-29), so a tile's
+// window slice costs two multiplies per node instead of one exp; E1/E2 are
+// computed once per source (k_spread_windows).
 constexpr int SP_CHUNK = 64;   // sources staged per round
-constexpr int SP_MAXCH = 8;
+constexpr int SP_MAXCH = 4;    // channels per launch (register budget)
+constexpr int SP_MAXP = 64;
+
+struct WinConst {
+  double e3[SP_MAXP];
+};
+
+__global__ void k_spread_windows(const double4* __restrict__ pts, int n, GridGeom g, int4* __restrict__ lo,
+                                 double4* __restrict__ wxy, double2* __restrict__ wz) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const double4 p = pts[i];
+    const double pc[3] = {p.x, p.y, p.z};
+    int l[3];
+    double e1[3], e2[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const int64_t lk = window_lo(pc[k], g.origin[k], g.h, g.P);
+      l[k] = (int)lk;
+      const double d0 = window_d(pc[k], g.origin[k], g.h, lk);
+      e1[k] = exp(-g.alpha * d0 * d0);
+      e2[k] = exp(2.0 * g.alpha * d0 * g.h);
+    }
+    lo[i] = make_int4(l[0], l[1], l[2], 0);
+    wxy[i] = make_double4(e1[0] * g.pref, e2[0], e1[1], e2[1]);  // pref folded into the x factor
+    wz[i] = make_double2(e1[2], e2[2]);
+  }
+}
+
+// window slice of length L starting at grid node `node0`, support start lo
+template <int L>
+__device__ __forceinline__ void window_slice(int node0, int lo, int P, double e1, double e2, const double* e3,
+                                             double* out) {
+  int a = node0 - lo;
+  // e2^max(a,0) by binary exponentiation
+  double pw = 1.0, b = e2;
+  int m = a > 0 ? a : 0;
+  while (m) {
+    if (m & 1) pw *= b;
+    b *= b;
+    m >>= 1;
+  }
+#pragma unroll
+  for (int i = 0; i < L; ++i, ++a) {
+    double v = 0.0;
+    if (a >= 0 && a < P) {
+      v = e1 * pw * e3[a];
+      pw *= e2;
+    }
+    out[i] = v;
+  }
+}
 
 template <int NCH>
-__global__ void __launch_bounds__(256) k_spread(const double4* __restrict__ pts, const double* __restrict__ w,
-                                                const int* __restrict__ bin_start, GridGeom g, int nbx, int nby,
-                                                int nbz, double* __restrict__ grids) {
+__global__ void __launch_bounds__(256) k_spread(const int4* __restrict__ lo4, const double4* __restrict__ wxy,
+                                                const double2* __restrict__ wzp, const double* __restrict__ w,
+                                                int ldw, const int* __restrict__ bin_start, GridGeom g,
+                                                WinConst wc, int nbx, int nby, int nbz, double* __restrict__ grids) {
   __shared__ double s_wx[SP_CHUNK][SP_TX];
   __shared__ double s_wy[SP_CHUNK][SP_TY];
   __shared__ double s_wz[SP_CHUNK][SP_TZ];
   __shared__ double s_q[SP_CHUNK][NCH];
-  __shared__ int s_lo[SP_CHUNK][3];
+  __shared__ unsigned s_mask[SP_CHUNK];
+  __shared__ double s_e3[SP_MAXP];
   __shared__ int run_beg[9], run_pre[10];
   __shared__ int s_nrun;
 
@@ -77,10 +135,10 @@ __global__ void __launch_bounds__(256) k_spread(const double4* __restrict__ pts,
   const int x0 = tx * SP_TX, y0 = ty * SP_TY, z0 = tz * SP_TZ;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   // warp patch: 4 (x) x 8 (y); 8 warps tile 16 x 16
-  const int px0 = (warp & 3) * 4, py0 = (warp >> 2) * 8;
-  const int xo = px0 + (lane & 3), yo = py0 + (lane >> 2);
+  const int xo = (warp & 3) * 4 + (lane & 3), yo = (warp >> 2) * 8 + (lane >> 2);
   const int P = g.P;
 
+  for (int i = threadIdx.x; i < P; i += blockDim.x) s_e3[i] = wc.e3[i];
   if (threadIdx.x == 0) {
     int nr = 0, tot = 0;
     const int zlo = max(tz - 2, 0), zhi = min(tz + 2, nbz - 1);
@@ -110,7 +168,6 @@ __global__ void __launch_bounds__(256) k_spread(const double4* __restrict__ pts,
   for (int c0 = 0; c0 < ncand; c0 += SP_CHUNK) {
     const int nc = min(SP_CHUNK, ncand - c0);
     __syncthreads();
-    // stage: 4 threads per source
     {
       const int s = threadIdx.x >> 2, part = threadIdx.x & 3;
       if (s < nc) {
@@ -118,68 +175,48 @@ __global__ void __launch_bounds__(256) k_spread(const double4* __restrict__ pts,
         int r = 0;
         while (r + 1 < nrun && run_pre[r + 1] <= v) ++r;
         const int row = run_beg[r] + (v - run_pre[r]);
-        const double4 p = pts[row];
+        const int4 l = lo4[row];
         if (part == 0) {
-          const int64_t lx = window_lo(p.x, g.origin[0], g.h, P);
-          s_lo[s][0] = (int)lx;
-#pragma unroll 4
-          for (int i = 0; i < SP_TX; ++i) {
-            const int64_t node = x0 + i;
-            double val = 0.0;
-            if (node >= lx && node < lx + P) {
-              const double d = window_d(p.x, g.origin[0], g.h, node);
-              val = exp(-g.alpha * d * d);
-            }
-            s_wx[s][i] = val;
-          }
+          const double4 e = wxy[row];
+          window_slice<SP_TX>(x0, l.x, P, e.x, e.y, s_e3, s_wx[s]);
         } else if (part == 1) {
-          const int64_t ly = window_lo(p.y, g.origin[1], g.h, P);
-          s_lo[s][1] = (int)ly;
-#pragma unroll 4
-          for (int i = 0; i < SP_TY; ++i) {
-            const int64_t node = y0 + i;
-            double val = 0.0;
-            if (node >= ly && node < ly + P) {
-              const double d = window_d(p.y, g.origin[1], g.h, node);
-              val = exp(-g.alpha * d * d);
-            }
-            s_wy[s][i] = val;
-          }
+          const double4 e = wxy[row];
+          window_slice<SP_TY>(y0, l.y, P, e.z, e.w, s_e3, s_wy[s]);
         } else if (part == 2) {
-          const int64_t lz = window_lo(p.z, g.origin[2], g.h, P);
-          s_lo[s][2] = (int)lz;
+          const double2 e = wzp[row];
+          window_slice<SP_TZ>(z0, l.z, P, e.x, e.y, s_e3, s_wz[s]);
+          // which warps' 4x8 (x,y) patches does the support reach? (z overlap is CTA-wide)
+          unsigned m = 0;
+          if (l.z < z0 + SP_TZ && l.z + P > z0) {
 #pragma unroll
-          for (int i = 0; i < SP_TZ; ++i) {
-            const int64_t node = z0 + i;
-            double val = 0.0;
-            if (node >= lz && node < lz + P) {
-              const double d = window_d(p.z, g.origin[2], g.h, node);
-              val = exp(-g.alpha * d * d);
+            for (int wq = 0; wq < 8; ++wq) {
+              const int px = x0 + (wq & 3) * 4, py = y0 + (wq >> 2) * 8;
+              if (l.x < px + 4 && l.x + P > px && l.y < py + 8 && l.y + P > py) m |= 1u << wq;
             }
-            s_wz[s][i] = val;
           }
+          s_mask[s] = m;
         } else {
 #pragma unroll
-          for (int c = 0; c < NCH; ++c) s_q[s][c] = g.pref * w[(size_t)row * NCH + c];
+          for (int c = 0; c < NCH; ++c) s_q[s][c] = w[(size_t)row * ldw + c];
         }
       }
     }
     __syncthreads();
-    for (int s = 0; s < nc; ++s) {
-      const int lx = s_lo[s][0], ly = s_lo[s][1], lz = s_lo[s][2];
-      // warp-uniform overlap test of the support with this warp's patch and the tile's z-range
-      const bool hit = (lx < x0 + px0 + 4) && (lx + P > x0 + px0) && (ly < y0 + py0 + 8) && (ly + P > y0 + py0) &&
-                       (lz < z0 + SP_TZ) && (lz + P > z0);
-      if (!hit) continue;
-      const double cxy = s_wx[s][xo] * s_wy[s][yo];
-      double wz[SP_TZ];
+    for (int base = 0; base < nc; base += 32) {
+      unsigned m = __ballot_sync(0xffffffffu, base + lane < nc && ((s_mask[base + lane] >> warp) & 1u));
+      while (m) {
+        const int s = base + __ffs(m) - 1;
+        m &= m - 1;
+        const double cxy = s_wx[s][xo] * s_wy[s][yo];
+        double wz[SP_TZ];
 #pragma unroll
-      for (int j = 0; j < SP_TZ; ++j) wz[j] = s_wz[s][j];
+        for (int j = 0; j < SP_TZ; ++j) wz[j] = s_wz[s][j];
 #pragma unroll
-      for (int c = 0; c < NCH; ++c) {
-        const double q = s_q[s][c] * cxy;
+        for (int c = 0; c < NCH; ++c) {
+          const double q = s_q[s][c] * cxy;
 #pragma unroll
-        for (int j = 0; j < SP_TZ; ++j) acc[c][j] = fma(q, wz[j], acc[c][j]);
+          for (int j = 0; j < SP_TZ; ++j) acc[c][j] = fma(q, wz[j], acc[c][j]);
+        }
       }
     }
   }
@@ -199,18 +236,36 @@ __global__ void __launch_bounds__(256) k_spread(const double4* __restrict__ pts,
 
 hs_status launch_spread(hs_ctx* ctx, const double4* pts, const double* w, int n, int nch, const int* bin_start,
                         const GridGeom& g, double* grids) {
+  if (g.P > SP_MAXP) return fail(HS_ERR_PARAMETER, "spread supports window support P <= 64");
   const int nbx = sp_nbins(g, 0), nby = sp_nbins(g, 1), nbz = sp_nbins(g, 2);
-  dim3 grid(nbx * nby * nbz), block(256);
-  (void)n;
-  switch (nch) {
-#define HS_SP(N) \
-  case N: k_spread<N><<<grid, block, 0, ctx->stream>>>(pts, w, bin_start, g, nbx, nby, nbz, grids); break;
-    HS_SP(1) HS_SP(2) HS_SP(3) HS_SP(4) HS_SP(5) HS_SP(6) HS_SP(7) HS_SP(8)
-#undef HS_SP
-    default:
-      return fail(HS_ERR_PARAMETER, "spread supports 1..8 channels per launch");
+  void* scr = nullptr;
+  const size_t per = sizeof(int4) + sizeof(double4) + sizeof(double2);
+  HS_TRY(ctx_scratch(ctx, per * (size_t)std::max(n, 1), &scr));
+  int4* lo = (int4*)scr;
+  double4* wxy = (double4*)(lo + std::max(n, 1));
+  double2* wz = (double2*)(wxy + std::max(n, 1));
+  if (n > 0) {
+    const int gs = (int)std::min<int64_t>(ceil_div(n, 256), ctx->sm_count * 8);
+    k_spread_windows<<<gs, 256, 0, ctx->stream>>>(pts, n, g, lo, wxy, wz);
+    HS_LAUNCHED(ctx);
   }
-  HS_LAUNCHED(ctx);
+  WinConst wc{};
+  for (int a = 0; a < g.P; ++a) wc.e3[a] = std::exp(-g.alpha * (g.h * a) * (g.h * a));
+  dim3 grid(nbx * nby * nbz), block(256);
+  for (int c0 = 0; c0 < nch; c0 += SP_MAXCH) {
+    const int cn = std::min(SP_MAXCH, nch - c0);
+    double* gout = grids + (size_t)c0 * g.ch_stride;
+    const double* wc0 = w + c0;
+    switch (cn) {
+#define HS_SP(N)                                                                                             \
+  case N:                                                                                                    \
+    k_spread<N><<<grid, block, 0, ctx->stream>>>(lo, wxy, wz, wc0, nch, bin_start, g, wc, nbx, nby, nbz, gout); \
+    break;
+      HS_SP(1) HS_SP(2) HS_SP(3) HS_SP(4)
+#undef HS_SP
+    }
+    HS_LAUNCHED(ctx);
+  }
   return HS_OK;
 }
 

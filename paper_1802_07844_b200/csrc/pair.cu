@@ -25,6 +25,26 @@
 
 namespace hs {
 
+namespace {
+#include "erfcx_table.inc"
+}
+__device__ double g_erfcx_coef[HS_ERFCX_NINT * (HS_ERFCX_DEG + 1)];
+static bool g_erfcx_ready = false;
+
+// erfc(x) = exp(-x^2) erfcx(x); E = exp(-x^2) is already computed by the caller.
+// Piecewise degree-13 polynomials on [0, 8) (tools/gen_erfcx.py, max rel. error ~1.1e-15).
+__device__ __forceinline__ double erfc_from_E(double x, double E, const double* __restrict__ tab) {
+  if (x < HS_ERFCX_W * HS_ERFCX_NINT) {
+    const int k = (int)(x * (1.0 / HS_ERFCX_W));
+    const double t = (x - (HS_ERFCX_W * k + 0.5 * HS_ERFCX_W)) * (2.0 / HS_ERFCX_W);
+    double p = tab[HS_ERFCX_DEG * HS_ERFCX_NINT + k];
+#pragma unroll
+    for (int j = HS_ERFCX_DEG - 1; j >= 0; --j) p = fma(p, t, tab[j * HS_ERFCX_NINT + k]);
+    return E * p;
+  }
+  return erfc(x);
+}
+
 constexpr int PT_MAXRUN = 25;  // 5 x 5 (x, y) cell columns
 
 struct PairConst {
@@ -36,14 +56,14 @@ struct PairConst {
 template <int KIND, bool SCREENED>
 __device__ __forceinline__ void eval_pair(const PairConst& pc, double d0, double d1, double d2, double r2,
                                           double x2, const double4& S, const double4& A, const double4& B,
-                                          bool image, double* k, double* c) {
-  const double rn = sqrt(r2);
-  const double ri = 1.0 / rn;
+                                          bool image, double* k, double* c, const double* __restrict__ etab) {
+  const double ri = rsqrt(r2);
   const double ri2 = ri * ri;
   double C = 1.0, e = 0.0;
   if (SCREENED) {
+    const double rn = r2 * ri;
     const double E = exp(-pc.xi2 * r2);
-    C = erfc(pc.xi * rn);
+    C = erfc_from_E(pc.xi * rn, E, etab);
     e = pc.c2xs * E;
   }
   const double c0 = C * ri;
@@ -148,6 +168,8 @@ __global__ void __launch_bounds__(PC_TG) k_pair_q(const PairArgs a) {
   __shared__ int run_beg[PT_MAXRUN];
   __shared__ int run_pre[PT_MAXRUN + 1];
   __shared__ int s_nrun;
+  __shared__ double s_erfcx[HS_ERFCX_NINT * (HS_ERFCX_DEG + 1)];
+  for (int i = threadIdx.x; i < HS_ERFCX_NINT * (HS_ERFCX_DEG + 1); i += blockDim.x) s_erfcx[i] = g_erfcx_coef[i];
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nx = a.dims[0], ny = a.dims[1], nz = a.dims[2];
@@ -204,7 +226,7 @@ __global__ void __launch_bounds__(PC_TG) k_pair_q(const PairArgs a) {
       const double rr = exact_r2(e0, e1, e2);
       const bool img = HALF && ((long long)S.w >= a.n_real);
       if (img) ++n_img;
-      eval_pair<KIND, true>(pc, e0, e1, e2, rr, T.z, S, A, B, img, &acc[0], &acc[3]);
+      eval_pair<KIND, true>(pc, e0, e1, e2, rr, T.z, S, A, B, img, &acc[0], &acc[3], s_erfcx);
     };
 
     for (int c0 = 0; c0 < ncand; c0 += PC_K) {
@@ -326,6 +348,10 @@ hs_status build_pair_items(hs_ctx* ctx, const int* t_start, int ncol, int nz, in
 
 hs_status launch_pair(hs_ctx* ctx, const PairArgs& a) {
   if (a.max_items == 0) return HS_OK;
+  if (!g_erfcx_ready) {
+    HS_CUDA(cudaMemcpyToSymbol(g_erfcx_coef, hs_erfcx_coef, sizeof(hs_erfcx_coef)));
+    g_erfcx_ready = true;
+  }
   const int kind = a.kind & 15;
   const bool is_half = (a.kind & 16) != 0;
   // persistent-style grid: enough CTAs to fill the machine, looping over the device-side item count
@@ -380,7 +406,7 @@ __global__ void __launch_bounds__(256) k_direct(int half, int n_real, int n_src,
         continue;
       }
       const bool img = half && ((long long)S.w >= n_real);
-      eval_pair<KIND, false>(pc, d0, d1, d2, r2, T.z, S, sA[i], sB[i], img, k, c);
+      eval_pair<KIND, false>(pc, d0, d1, d2, r2, T.z, S, sA[i], sB[i], img, k, c, nullptr);
     }
   }
   if (bad && tv) atomicOr(flags, FLAG_SINGULAR);
