@@ -1,0 +1,394 @@
+// fft.cu -- the x-direction stage of the pruned 3-D FFT, fused with the k-space scaling.
+//
+// Pipeline per evaluation (plan.cu), with data (nx,ny,nz) zero-padded to (px,py,pz):
+//   Z  : cuFFT D2Z along z on the ny*nx nonzero lines          -> A[y][x][kz]
+//   Y  : cuFFT Z2Z along y (input rows y >= ny are zero)         -> B_c[ky][x][kz]
+//   X  : THIS KERNEL, one CTA per (ky, kz..kz+KB-1) column group:
+//          load the nx nonzero x-values of every source channel (zero-extend to px),
+//          forward FFT along x (warp-per-line Stockham in shared memory),
+//          k-space multipliers + wall channels + Nyquist symmetrisation (kmult.cuh),
+//          inverse FFT along x of the 6 (or 3) output channels,
+//          store only the x < nx outputs (output pruning)          -> B_o[ky][x][kz]
+//   Y^-1, Z^-1: cuFFT Z2Z inverse along y, Z2D along z (only the y < ny lines)
+// The full (px,py,pz/2+1) spectrum of a channel therefore never exists in HBM;
+// the x-stage replaces 13 full-spectrum passes + the scale pass of a 3-D cuFFT
+// pipeline with one read of the sources and one write of the outputs.
+#include <cmath>
+#include <vector>
+
+#include "common.cuh"
+#include "kernels.cuh"
+#include "kmult.cuh"
+
+namespace hs {
+
+// ---- warp-cooperative in-place Stockham FFT of one line in shared memory -------------
+__device__ __forceinline__ double2 cm(double2 a, double2 b) {
+  return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+__device__ __forceinline__ double2 ad(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 sb(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 mi(double2 a) { return make_double2(a.y, -a.x); }  // -i a
+
+template <int R>
+__device__ __forceinline__ void dft(double2* a) {
+  if (R == 2) {
+    const double2 t = a[0];
+    a[0] = ad(t, a[1]);
+    a[1] = sb(t, a[1]);
+  } else if (R == 3) {
+    const double c = 0.86602540378443864676;  // sin(2 pi/3)
+    const double2 s = ad(a[1], a[2]), d = sb(a[1], a[2]);
+    const double2 m = make_double2(a[0].x - 0.5 * s.x, a[0].y - 0.5 * s.y);
+    a[0] = ad(a[0], s);
+    const double2 t = make_double2(c * d.y, -c * d.x);  // -i c d
+    a[1] = ad(m, t);
+    a[2] = sb(m, t);
+  } else if (R == 4) {
+    const double2 t0 = ad(a[0], a[2]), t1 = sb(a[0], a[2]), t2 = ad(a[1], a[3]), t3 = mi(sb(a[1], a[3]));
+    a[0] = ad(t0, t2);
+    a[2] = sb(t0, t2);
+    a[1] = ad(t1, t3);
+    a[3] = sb(t1, t3);
+  } else if (R == 5) {
+    const double c1 = 0.30901699437494742410, c2 = -0.80901699437494742410;
+    const double s1 = 0.95105651629515357212, s2 = 0.58778525229247312917;
+    const double2 p1 = ad(a[1], a[4]), d1 = sb(a[1], a[4]), p2 = ad(a[2], a[3]), d2 = sb(a[2], a[3]);
+    const double2 a0 = a[0];
+    a[0] = ad(a0, ad(p1, p2));
+    const double2 t1 = make_double2(a0.x + c1 * p1.x + c2 * p2.x, a0.y + c1 * p1.y + c2 * p2.y);
+    const double2 t2 = make_double2(a0.x + c2 * p1.x + c1 * p2.x, a0.y + c2 * p1.y + c1 * p2.y);
+    const double2 u1 = make_double2(s1 * d1.x + s2 * d2.x, s1 * d1.y + s2 * d2.y);
+    const double2 u2 = make_double2(s2 * d1.x - s1 * d2.x, s2 * d1.y - s1 * d2.y);
+    a[1] = ad(t1, mi(u1));
+    a[4] = sb(t1, mi(u1));
+    a[2] = ad(t2, mi(u2));
+    a[3] = sb(t2, mi(u2));
+  } else if (R == 8) {
+    double2 e[4] = {a[0], a[2], a[4], a[6]}, o[4] = {a[1], a[3], a[5], a[7]};
+    dft<4>(e);
+    dft<4>(o);
+    const double h = 0.70710678118654752440;
+    const double2 w1 = make_double2(h, -h), w3 = make_double2(-h, -h);
+    o[1] = cm(o[1], w1);
+    o[2] = mi(o[2]);
+    o[3] = cm(o[3], w3);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      a[k] = ad(e[k], o[k]);
+      a[k + 4] = sb(e[k], o[k]);
+    }
+  } else {
+    // generic small prime (7, 11): direct DFT with exact-angle twiddles
+    double2 y[R];
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      double2 s = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int m = 0; m < R; ++m) {
+        double sn, cs;
+        sincospi(-2.0 * ((m * k) % R) / R, &sn, &cs);
+        s = ad(s, cm(a[m], make_double2(cs, sn)));
+      }
+      y[k] = s;
+    }
+#pragma unroll
+    for (int k = 0; k < R; ++k) a[k] = y[k];
+  }
+}
+
+// One radix-R pass of a length-N line (current sub-transform length L) by one warp:
+// each lane loads its butterflies' inputs into registers, __syncwarp, writes them back
+// (in-place Stockham autosort).
+template <int R, int MAXB>
+__device__ __forceinline__ void warp_pass(double2* line, int N, int L, const double2* tw, int lane) {
+  const int nb = N / R;
+  const int tstep = N / (L * R);
+  double2 v[MAXB][R];
+#pragma unroll
+  for (int q = 0; q < MAXB; ++q) {
+    const int b = lane + 32 * q;
+    if (b < nb) {
+      const int k = b % L;
+#pragma unroll
+      for (int m = 0; m < R; ++m) {
+        double2 x = line[b + m * nb];
+        if (m > 0 && k > 0) x = cm(x, tw[m * k * tstep]);
+        v[q][m] = x;
+      }
+      dft<R>(v[q]);
+    }
+  }
+  __syncwarp();
+#pragma unroll
+  for (int q = 0; q < MAXB; ++q) {
+    const int b = lane + 32 * q;
+    if (b < nb) {
+      const int k = b % L;
+      const int base = (b / L) * L * R + k;
+#pragma unroll
+      for (int m = 0; m < R; ++m) line[base + m * L] = v[q][m];
+    }
+  }
+  __syncwarp();
+}
+
+// Compile-time radix plan: FFT length N = product of Rs (natural-order output).
+template <int N, int L, int R, int... Rest>
+__device__ __forceinline__ void fft_passes(double2* line, const double2* tw, int lane) {
+  warp_pass<R, (N / R + 31) / 32>(line, N, L, tw, lane);
+  if constexpr (sizeof...(Rest) > 0) fft_passes<N, L * R, Rest...>(line, tw, lane);
+}
+
+template <int... Rs>
+struct FixedFFT {
+  static constexpr int N = (Rs * ...);
+  __device__ __forceinline__ static void run(double2* line, const FftPlan&, const double2* tw, int lane) {
+    fft_passes<N, 1, Rs...>(line, tw, lane);
+  }
+};
+
+// Runtime radix plan (any 11-smooth N <= 1024): one non-inlined function per
+// (radix, butterflies-per-lane) variant.
+template <int R, int MAXB>
+__device__ __noinline__ void warp_pass_v(double2* line, int N, int L, const double2* tw, int lane) {
+  warp_pass<R, MAXB>(line, N, L, tw, lane);
+}
+
+template <int R, int M0, int... Ms>
+__device__ __forceinline__ void warp_pass_pick(int need, double2* line, int N, int L, const double2* tw, int lane) {
+  if constexpr (sizeof...(Ms) == 0) {
+    warp_pass_v<R, M0>(line, N, L, tw, lane);
+  } else {
+    if (need <= M0) warp_pass_v<R, M0>(line, N, L, tw, lane);
+    else warp_pass_pick<R, Ms...>(need, line, N, L, tw, lane);
+  }
+}
+
+struct AnyFFT {
+  static constexpr int N = 0;
+  __device__ __forceinline__ static void run(double2* line, const FftPlan& pl, const double2* tw, int lane) {
+    int L = 1;
+    const int n = pl.n;
+    for (int s = 0; s < pl.npass; ++s) {
+      const int R = pl.radix[s];
+      const int need = (n / R + 31) / 32;
+      switch (R) {
+        case 2: warp_pass_pick<2, 1, 2, 4, 8, 16>(need, line, n, L, tw, lane); break;
+        case 3: warp_pass_pick<3, 1, 2, 3, 4, 6, 11>(need, line, n, L, tw, lane); break;
+        case 4: warp_pass_pick<4, 1, 2, 4, 8>(need, line, n, L, tw, lane); break;
+        case 5: warp_pass_pick<5, 1, 2, 4, 7>(need, line, n, L, tw, lane); break;
+        case 7: warp_pass_pick<7, 1, 2, 5>(need, line, n, L, tw, lane); break;
+        case 8: warp_pass_pick<8, 1, 2, 4>(need, line, n, L, tw, lane); break;
+        default: warp_pass_pick<11, 1, 3>(need, line, n, L, tw, lane); break;
+      }
+      L *= R;
+    }
+  }
+};
+
+hs_status make_fft_plan(int n, FftPlan* pl) {
+  pl->n = n;
+  pl->npass = 0;
+  int m = n;
+  const int order[] = {8, 4, 2, 3, 5, 7, 11};
+  while (m > 1) {
+    bool found = false;
+    for (int r : order) {
+      if (m % r == 0) {
+        if (pl->npass >= FftPlan::kMaxPass) return fail(HS_ERR_PARAMETER, "FFT length has too many factors");
+        pl->radix[pl->npass++] = r;
+        m /= r;
+        found = true;
+        break;
+      }
+    }
+    if (!found) return fail(HS_ERR_PARAMETER, "padded FFT length must be 11-smooth");
+  }
+  if (n > 1024) return fail(HS_ERR_PARAMETER, "padded FFT length > 1024 is not supported by the x-stage");
+  return HS_OK;
+}
+
+// ---- fused x-stage ----------------------------------------------------------------------
+// Nyquist planes (rare): full scale_point with the Hermitian symmetrisation, kept out of line so
+// its register footprint does not limit the main kernel.
+template <int KIND, bool HALF>
+__device__ __noinline__ void scale_nyquist(double2* col, int cstride, int kx, int ky, int kz, const int* p,
+                                           const double* kscale, double ka, double kb, double inv_n, double tB,
+                                           double tH) {
+  constexpr int NIN = KChan<KIND, HALF>::NIN, NOUT = KChan<KIND, HALF>::NOUT;
+  cplx C[NIN], out[6];
+#pragma unroll
+  for (int c = 0; c < NIN; ++c) {
+    const double2 v = col[c * cstride];
+    C[c] = {v.x, v.y};
+  }
+  scale_point<KIND, HALF>(kx, ky, kz, p, kscale, ka, kb, inv_n, tB, tH, C, out);
+#pragma unroll
+  for (int o = 0; o < NOUT; ++o) col[o * cstride] = make_double2(out[o].re, -out[o].im);
+}
+
+template <int KIND, bool HALF, int KB, class FFT>
+__global__ void __launch_bounds__(256, 2) k_xfused(const XArgs a) {
+  constexpr int NIN = KChan<KIND, HALF>::NIN, NOUT = KChan<KIND, HALF>::NOUT;
+  extern __shared__ double2 smem[];
+  const int px = a.plan.n;
+  double2* lines = smem;                    // [NIN][KB][px]
+  double2* tw = smem + NIN * KB * px;       // [px]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int i = tid; i < px; i += blockDim.x) tw[i] = a.tw[i];
+  const int nkb = (a.nzh + KB - 1) / KB;
+  const int n_items = a.py * nkb;
+  const int p[3] = {a.px, a.py, a.pz};
+  for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+    const int ky = item / nkb;
+    const int kz0 = (item % nkb) * KB;
+    const int kbn = min(KB, a.nzh - kz0);
+    __syncthreads();
+    // load the nx nonzero x-values of every channel, zero-extend to px
+    for (int i = tid; i < NIN * px; i += blockDim.x) {
+      const int c = i / px, x = i - c * px;
+      double2 v[KB];
+#pragma unroll
+      for (int kb = 0; kb < KB; ++kb) v[kb] = make_double2(0.0, 0.0);
+      if (x < a.nx) {
+        const double2* src = a.B + c * a.ch_stride + ((int64_t)ky * a.nx + x) * a.nzh + kz0;
+        if (KB == 2 && kbn == 2) {
+          const double4 w = *reinterpret_cast<const double4*>(src);
+          v[0] = make_double2(w.x, w.y);
+          v[KB - 1] = make_double2(w.z, w.w);
+        } else {
+#pragma unroll
+          for (int kb = 0; kb < KB; ++kb)
+            if (kb < kbn) v[kb] = src[kb];
+        }
+      }
+#pragma unroll
+      for (int kb = 0; kb < KB; ++kb) lines[(c * KB + kb) * px + x] = v[kb];
+    }
+    __syncthreads();
+    for (int l = warp; l < NIN * KB; l += blockDim.x / 32) FFT::run(lines + l * px, a.plan, tw, lane);
+    __syncthreads();
+    // k-space scaling at every (kx, ky, kz) of the group
+    for (int i = tid; i < KB * px; i += blockDim.x) {
+      const int kb = i / px, kx = i - kb * px;
+      if (kb >= kbn) continue;
+      const int kz = kz0 + kb;
+      const int64_t ti = ((int64_t)ky * a.nzh + kz) * px + kx;
+      const double tB = (KIND == HS_ROTLET) ? 0.0 : a.tabB[ti];
+      const double tH = (KIND == HS_ROTLET || HALF) ? a.tabH[ti] : 0.0;
+      double2* col = lines + kb * px + kx;  // channel c at col[c * KB * px]
+      if (2 * kx == px || 2 * ky == a.py || 2 * kz == a.pz) {
+        scale_nyquist<KIND, HALF>(col, KB * px, kx, ky, kz, p, a.kscale, a.ka, a.kb, a.inv_n, tB, tH);
+        continue;
+      }
+      cplx C[NIN], out[6];
+#pragma unroll
+      for (int c = 0; c < NIN; ++c) {
+        const double2 v = col[c * KB * px];
+        C[c] = {v.x, v.y};
+      }
+      const double s8 = 1.0 / (8.0 * kPi), s4 = 1.0 / (4.0 * kPi);
+      const double kxv = kval(kx, px, a.kscale[0]), kyv = kval(ky, a.py, a.kscale[1]),
+                   kzv = kval(kz, a.pz, a.kscale[2]);
+      const double k2 = kxv * kxv + kyv * kyv + kzv * kzv;
+      const double E = exp(-a.ka * k2);
+      const double G = (KIND == HS_ROTLET) ? tH * E * s4 * a.inv_n : tB * E * (1.0 + a.kb * k2) * s8 * a.inv_n;
+      const double Fc = HALF ? tH * E * s4 * a.inv_n : 0.0;
+      apply_multiplier<KIND, HALF>(kxv, kyv, kzv, G, Fc, C, out);
+      // inverse transform by conjugation: IFFT(y) = conj(FFT(conj(y))) (normalisation already in inv_n)
+#pragma unroll
+      for (int o = 0; o < NOUT; ++o) col[o * KB * px] = make_double2(out[o].re, -out[o].im);
+    }
+    __syncthreads();
+    for (int l = warp; l < NOUT * KB; l += blockDim.x / 32) FFT::run(lines + l * px, a.plan, tw, lane);
+    __syncthreads();
+    // store the x < nx outputs (conjugated back)
+    for (int i = tid; i < NOUT * a.nx; i += blockDim.x) {
+      const int o = i / a.nx, x = i - o * a.nx;
+      double2* dst = a.B + o * a.ch_stride + ((int64_t)ky * a.nx + x) * a.nzh + kz0;
+#pragma unroll
+      for (int kb = 0; kb < KB; ++kb) {
+        if (kb < kbn) {
+          const double2 v = lines[(o * KB + kb) * px + x];
+          dst[kb] = make_double2(v.x, -v.y);
+        }
+      }
+    }
+  }
+}
+
+template <int KIND, bool HALF, int KB, class FFT>
+static hs_status launch_xfused_t(hs_ctx* ctx, const XArgs& a) {
+  constexpr int NIN = KChan<KIND, HALF>::NIN;
+  const size_t smem = sizeof(double2) * ((size_t)NIN * KB * a.plan.n + a.plan.n);
+  if (smem > 227 * 1024) return fail(HS_ERR_PARAMETER, "x-stage shared memory exceeds 227 KB");
+  auto kern = k_xfused<KIND, HALF, KB, FFT>;
+  HS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per_sm = 0;
+  HS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem));
+  const int nkb = (a.nzh + KB - 1) / KB;
+  const int items = a.py * nkb;
+  const int grid = std::max(1, std::min(items, ctx->sm_count * std::max(per_sm, 1) * 8));
+  kern<<<grid, 256, smem, ctx->stream>>>(a);
+  HS_LAUNCHED(ctx);
+  return HS_OK;
+}
+
+// FFT-length specialisations for the BASELINE configurations (cfg1 240, cfg2/3 352,
+// HL 480, cfg4 750, cfg5 864); any other 11-smooth length <= 1024 uses AnyFFT.
+template <int KIND, int KB>
+static hs_status launch_xfused_half(hs_ctx* ctx, const XArgs& a) {
+  switch (a.plan.n) {
+    case 240: return launch_xfused_t<KIND, true, KB, FixedFFT<8, 2, 3, 5>>(ctx, a);
+    case 352: return launch_xfused_t<KIND, true, KB, FixedFFT<8, 4, 11>>(ctx, a);
+    case 480: return launch_xfused_t<KIND, true, KB, FixedFFT<8, 4, 3, 5>>(ctx, a);
+    case 750: return launch_xfused_t<KIND, true, KB, FixedFFT<2, 3, 5, 5, 5>>(ctx, a);
+    case 864: return launch_xfused_t<KIND, true, KB, FixedFFT<8, 4, 3, 3, 3>>(ctx, a);
+    default: return launch_xfused_t<KIND, true, KB, AnyFFT>(ctx, a);
+  }
+}
+
+hs_status launch_xfused(hs_ctx* ctx, int kind, int half, const XArgs& a) {
+  if (half) {
+    if (kind == HS_STOKESLET) return launch_xfused_half<HS_STOKESLET, 2>(ctx, a);
+    if (kind == HS_STRESSLET) return launch_xfused_half<HS_STRESSLET, 1>(ctx, a);
+    return launch_xfused_half<HS_ROTLET, 2>(ctx, a);
+  }
+  if (kind == HS_STOKESLET) return launch_xfused_t<HS_STOKESLET, false, 2, AnyFFT>(ctx, a);
+  if (kind == HS_STRESSLET) return launch_xfused_t<HS_STRESSLET, false, 2, AnyFFT>(ctx, a);
+  return launch_xfused_t<HS_ROTLET, false, 2, AnyFFT>(ctx, a);
+}
+
+// twiddles exp(-2 pi i j / n), computed in long double on the host
+hs_status make_twiddles(int n, double2* d_tw, cudaStream_t st) {
+  std::vector<double2> tw(n);
+  for (int j = 0; j < n; ++j) {
+    const long double ang = -2.0L * 3.141592653589793238462643383279502884L * (long double)j / (long double)n;
+    tw[j] = make_double2((double)std::cos(ang), (double)std::sin(ang));
+  }
+  HS_CUDA(cudaMemcpyAsync(d_tw, tw.data(), sizeof(double2) * n, cudaMemcpyHostToDevice, st));
+  HS_CUDA(cudaStreamSynchronize(st));
+  return HS_OK;
+}
+
+// half-spectrum table [kx][ky][kz] -> x-stage layout [ky][kz][kx]
+__global__ void k_table_to_xmajor(const double* __restrict__ in, int px, int py, int nzh, double* __restrict__ out) {
+  const int64_t n = (int64_t)px * py * nzh;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int kx = (int)(i % px);
+    const int64_t r = i / px;
+    const int kz = (int)(r % nzh), ky = (int)(r / nzh);
+    out[i] = in[((int64_t)kx * py + ky) * nzh + kz];
+  }
+}
+
+hs_status launch_table_to_xmajor(hs_ctx* ctx, const double* in, int px, int py, int nzh, double* out) {
+  const int64_t n = (int64_t)px * py * nzh;
+  const int gs = (int)std::min<int64_t>(ceil_div(n, 256), (int64_t)ctx->sm_count * 16);
+  k_table_to_xmajor<<<gs, 256, 0, ctx->stream>>>(in, px, py, nzh, out);
+  HS_LAUNCHED(ctx);
+  return HS_OK;
+}
+
+}  // namespace hs

@@ -113,6 +113,30 @@ hs_status launch_real_part(hs_ctx* ctx, const double2* spec, int64_t n, double* 
 hs_status launch_expand_half(hs_ctx* ctx, const double2* half_spec, const int64_t p[3], double* full);
 hs_status launch_take_half(hs_ctx* ctx, const double* full, const int64_t p[3], double* half);
 
+// ---------------------------------------------------------------------------
+// fused x-stage of the pruned FFT pipeline (fft.cu)
+struct FftPlan {
+  static constexpr int kMaxPass = 12;
+  int n, npass;
+  int radix[kMaxPass];
+};
+struct XArgs {
+  double2* B;            // channel-major spectra, each [ky < py][x < nx][kz < nzh]
+  int64_t ch_stride;     // complex elements between channels
+  const double* tabB;    // biharmonic table, x-stage layout [ky][kz][kx] (or null)
+  const double* tabH;    // harmonic table, same layout (or null)
+  const double2* tw;     // px twiddles exp(-2 pi i j/px)
+  FftPlan plan;          // radix plan of px
+  int px, py, pz, nzh, nx;
+  double kscale[3];      // 1/(p_i h)
+  double ka, kb;         // (1-eta)/4xi^2, 1/4xi^2
+  double inv_n;          // 1/(px py pz)
+};
+hs_status make_fft_plan(int n, FftPlan* pl);
+hs_status make_twiddles(int n, double2* d_tw, cudaStream_t st);
+hs_status launch_xfused(hs_ctx* ctx, int kind, int half, const XArgs& a);
+hs_status launch_table_to_xmajor(hs_ctx* ctx, const double* in, int px, int py, int nzh, double* out);
+
 // plan.cu helpers reused by the stand-alone API
 hs_status greens_half_table(hs_ctx* ctx, int kind, double R, double h, const int64_t big[3], const int64_t dims[3],
                             const int64_t guards[3], const int64_t pd[3], double* half_out);

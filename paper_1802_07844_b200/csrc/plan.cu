@@ -221,13 +221,19 @@ struct hs_plan {
   double4 *SPk = nullptr, *SPc = nullptr, *TG = nullptr;
   double *SWk = nullptr, *SWc = nullptr;
   int* tg_orig = nullptr;
-  double* grid_in = nullptr;    // n_in * n_real_grid
-  double2* spec = nullptr;      // max(n_in,n_out) * n_half
-  double* grid_out = nullptr;   // n_out * n_real_grid
-  double* tabB = nullptr;       // n_half (real)
+  // pruned FFT pipeline (fft.cu): grid_in/out [y][x][pz] real per channel, A/spec [y|ky][x][kz] complex
+  int64_t n_grid = 0;           // ny * nx * pz
+  int64_t n_mixed = 0;          // py * nx * nzh
+  double* grid_in = nullptr;    // n_in * n_grid (z-padding stays zero: the z-transform is out of place)
+  double2* Amix = nullptr;      // n_mixed (rows y >= ny stay zero: the y-transform is out of place)
+  double2* spec = nullptr;      // max(n_in, n_out) * n_mixed
+  double* grid_out = nullptr;   // n_out * n_grid
+  double* tabB = nullptr;       // x-stage layout [ky][kz][kx]
   double* tabH = nullptr;
+  double2* tw = nullptr;        // px twiddles
+  FftPlan xplan{};
   bool have_B = false, have_H = false;
-  cufftHandle fwd = 0, inv = 0;
+  cufftHandle zf = 0, yf = 0, zi = 0;
   void* fft_work = nullptr;
   // outputs
   double *u = nullptr, *u_real = nullptr, *u_four = nullptr, *uk = nullptr, *uc = nullptr;
@@ -312,12 +318,18 @@ extern "C" hs_status hs_plan_create(hs_ctx* ctx, const hs_params* prm, hs_plan**
   g.alpha = 2.0 * prm->xi * prm->xi / prm->eta;
   g.pref = std::pow(2.0 * prm->xi * prm->xi / (kPi * prm->eta), 1.5);
   const int64_t px = prm->padded[0], py = prm->padded[1], pz = prm->padded[2];
-  g.stride[0] = py * pz;
-  g.stride[1] = pz;
+  const int64_t nxd = prm->dims[0], nyd = prm->dims[1], nzh = pz / 2 + 1;
+  // grids are stored [y][x][z] with z-pitch pz (see fft.cu)
+  g.stride[0] = pz;
+  g.stride[1] = nxd * pz;
   g.stride[2] = 1;
-  g.ch_stride = px * py * pz;
+  g.ch_stride = nyd * nxd * pz;
+  p->n_grid = nyd * nxd * pz;
+  p->n_mixed = py * nxd * nzh;
   p->n_real_grid = px * py * pz;
-  p->n_half = px * py * (pz / 2 + 1);
+  p->n_half = px * py * nzh;
+  if (px != py) return bail(fail(HS_ERR_PARAMETER, "padded x and y lengths must agree"));
+  if ((st = make_fft_plan((int)px, &p->xplan)) != HS_OK) return bail(st);
   KGeom& kg = p->kg;
   kg.p[0] = (int)px;
   kg.p[1] = (int)py;
@@ -367,11 +379,14 @@ extern "C" hs_status hs_plan_create(hs_ctx* ctx, const hs_params* prm, hs_plan**
   }
   A_(std::max(nt, 1), p->TG);
   A_(std::max(nt, 1), p->tg_orig);
-  A_((size_t)p->n_in * p->n_real_grid, p->grid_in, true);  // zero padding persists (D2Z is out of place)
-  A_((size_t)std::max(p->n_in, p->n_out) * p->n_half, p->spec);
-  A_((size_t)p->n_out * p->n_real_grid, p->grid_out);
+  A_((size_t)p->n_in * p->n_grid, p->grid_in, true);
+  A_((size_t)p->n_mixed, p->Amix, true);
+  A_((size_t)std::max(p->n_in, p->n_out) * p->n_mixed, p->spec);
+  A_((size_t)p->n_out * p->n_grid, p->grid_out);
   if (table_needs(prm->kind, p->half, HS_BIHARMONIC)) A_(p->n_half, p->tabB);
   if (table_needs(prm->kind, p->half, HS_HARMONIC)) A_(p->n_half, p->tabH);
+  A_(px, p->tw);
+  if ((st = make_twiddles((int)px, p->tw, ctx->stream)) != HS_OK) return bail(st);
   A_(3 * (size_t)std::max(nt, 1), p->u);
   A_(3 * (size_t)std::max(nt, 1), p->u_real, true);
   A_(3 * (size_t)std::max(nt, 1), p->u_four, true);
@@ -381,26 +396,29 @@ extern "C" hs_status hs_plan_create(hs_ctx* ctx, const hs_params* prm, hs_plan**
 #undef A_
   // ---- cuFFT plans (batched over channels, shared work area)
   {
-    long long nn[3] = {px, py, pz};
-    size_t ws1 = 0, ws2 = 0;
-    if (cufftCreate(&p->fwd) != CUFFT_SUCCESS || cufftCreate(&p->inv) != CUFFT_SUCCESS)
+    // 1-D batched cuFFT plans for the z and y stages (x is fused with the scaling, fft.cu)
+    size_t w1 = 0, w2 = 0, w3 = 0;
+    if (cufftCreate(&p->zf) != CUFFT_SUCCESS || cufftCreate(&p->yf) != CUFFT_SUCCESS ||
+        cufftCreate(&p->zi) != CUFFT_SUCCESS)
       return bail(fail(HS_ERR_RESOURCE, "cufftCreate failed"));
-    cufftSetAutoAllocation(p->fwd, 0);
-    cufftSetAutoAllocation(p->inv, 0);
-    if (cufftMakePlanMany64(p->fwd, 3, nn, nullptr, 1, p->n_real_grid, nullptr, 1, p->n_half, CUFFT_D2Z, p->n_in,
-                            &ws1) != CUFFT_SUCCESS)
-      return bail(fail(HS_ERR_RESOURCE, "cuFFT D2Z plan failed"));
-    if (cufftMakePlanMany64(p->inv, 3, nn, nullptr, 1, p->n_half, nullptr, 1, p->n_real_grid, CUFFT_Z2D, p->n_out,
-                            &ws2) != CUFFT_SUCCESS)
-      return bail(fail(HS_ERR_RESOURCE, "cuFFT Z2D plan failed"));
-    const size_t ws = std::max(ws1, ws2);
+    cufftSetAutoAllocation(p->zf, 0);
+    cufftSetAutoAllocation(p->yf, 0);
+    cufftSetAutoAllocation(p->zi, 0);
+    long long nz1[1] = {pz}, nzh1[1] = {nzh}, ny1[1] = {py};
+    if (cufftMakePlanMany64(p->zf, 1, nz1, nz1, 1, pz, nzh1, 1, nzh, CUFFT_D2Z, nyd * nxd, &w1) != CUFFT_SUCCESS)
+      return bail(fail(HS_ERR_RESOURCE, "cuFFT z D2Z plan failed"));
+    if (cufftMakePlanMany64(p->yf, 1, ny1, ny1, nxd * nzh, 1, ny1, nxd * nzh, 1, CUFFT_Z2Z, nxd * nzh, &w2) !=
+        CUFFT_SUCCESS)
+      return bail(fail(HS_ERR_RESOURCE, "cuFFT y Z2Z plan failed"));
+    if (cufftMakePlanMany64(p->zi, 1, nz1, nzh1, 1, nzh, nz1, 1, pz, CUFFT_Z2D, nyd * nxd, &w3) != CUFFT_SUCCESS)
+      return bail(fail(HS_ERR_RESOURCE, "cuFFT z Z2D plan failed"));
+    const size_t ws = std::max(w1, std::max(w2, w3));
     char* wsp = nullptr;
     if ((st = palloc(p, std::max<size_t>(ws, 16), &wsp)) != HS_OK) return bail(st);
     p->fft_work = wsp;
-    cufftSetWorkArea(p->fwd, wsp);
-    cufftSetWorkArea(p->inv, wsp);
-    cufftSetStream(p->fwd, ctx->stream);
-    cufftSetStream(p->inv, ctx->stream);
+    cufftSetWorkArea(p->zf, wsp);
+    cufftSetWorkArea(p->yf, wsp);
+    cufftSetWorkArea(p->zi, wsp);
   }
   for (auto& e : p->ev) HS_CUDA(cudaEventCreate(&e));
   *out = p;
@@ -409,8 +427,9 @@ extern "C" hs_status hs_plan_create(hs_ctx* ctx, const hs_params* prm, hs_plan**
 
 extern "C" hs_status hs_plan_destroy(hs_plan* p) {
   if (!p) return HS_OK;
-  if (p->fwd) cufftDestroy(p->fwd);
-  if (p->inv) cufftDestroy(p->inv);
+  if (p->zf) cufftDestroy(p->zf);
+  if (p->yf) cufftDestroy(p->yf);
+  if (p->zi) cufftDestroy(p->zi);
   for (auto& e : p->ev)
     if (e) cudaEventDestroy(e);
   for (auto& b : p->bufs) cudaFree(b.p);
@@ -451,7 +470,11 @@ extern "C" hs_status hs_plan_set_table(hs_plan* p, int table_kind, const double*
     HS_CUDA(cudaMemcpyAsync(tmp, samples, full * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
     src = tmp;
   }
-  hs_status st = launch_take_half(ctx, src, pd, dst);
+  double* half = nullptr;
+  HS_CUDA(cudaMallocAsync(&half, (size_t)p->n_half * sizeof(double), ctx->stream));
+  hs_status st = launch_take_half(ctx, src, pd, half);
+  if (st == HS_OK) st = launch_table_to_xmajor(ctx, half, (int)pd[0], (int)pd[1], (int)(pd[2] / 2 + 1), dst);
+  cudaFreeAsync(half, ctx->stream);
   if (tmp) cudaFreeAsync(tmp, ctx->stream);
   HS_TRY(st);
   HS_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -541,15 +564,20 @@ hs_status greens_half_table(hs_ctx* ctx, int kind, double R, double h, const int
 extern "C" hs_status hs_plan_build_tables(hs_plan* p, const int64_t big[3], double R, const int64_t guards[3]) {
   if (!p) return fail(HS_ERR_PARAMETER, "null plan");
   const int64_t pd[3] = {p->prm.padded[0], p->prm.padded[1], p->prm.padded[2]};
-  if (p->tabB) {
-    HS_TRY(greens_half_table(p->ctx, HS_BIHARMONIC, R, p->prm.h, big, p->prm.dims, guards, pd, p->tabB));
-    p->have_B = true;
+  hs_ctx* ctx = p->ctx;
+  double* half = nullptr;
+  HS_CUDA(cudaMalloc(&half, (size_t)p->n_half * sizeof(double)));
+  hs_status st = HS_OK;
+  for (int kind = 0; kind < 2 && st == HS_OK; ++kind) {
+    double* dst = kind == HS_BIHARMONIC ? p->tabB : p->tabH;
+    if (!dst) continue;
+    st = greens_half_table(ctx, kind, R, p->prm.h, big, p->prm.dims, guards, pd, half);
+    if (st == HS_OK) st = launch_table_to_xmajor(ctx, half, (int)pd[0], (int)pd[1], (int)(pd[2] / 2 + 1), dst);
+    if (st == HS_OK && cudaStreamSynchronize(ctx->stream) != cudaSuccess) st = fail(HS_ERR_CUDA, "table build");
+    if (st == HS_OK) (kind == HS_BIHARMONIC ? p->have_B : p->have_H) = true;
   }
-  if (p->tabH) {
-    HS_TRY(greens_half_table(p->ctx, HS_HARMONIC, R, p->prm.h, big, p->prm.dims, guards, pd, p->tabH));
-    p->have_H = true;
-  }
-  return HS_OK;
+  cudaFree(half);
+  return st;
 }
 
 namespace {
@@ -685,17 +713,48 @@ extern "C" hs_status hs_plan_execute(hs_plan* p, const double* positions, const 
     HS_TRY(launch_spread(ctx, p->SPk, p->SWk, p->n_comb, p->nk, p->bk_start, p->gg, p->grid_in));
     if (p->nc)
       HS_TRY(launch_spread(ctx, p->SPc, p->SWc, n, p->nc, p->bc_start, p->gg,
-                           p->grid_in + (size_t)p->nk * p->n_real_grid));
+                           p->grid_in + (size_t)p->nk * p->n_grid));
     HS_CUDA(cudaEventRecord(ev[12], st));
     spread_timed = true;
     HS_CUDA(cudaEventRecord(ev[3], st));
-    if (cufftExecD2Z(p->fwd, p->grid_in, (cufftDoubleComplex*)p->spec) != CUFFT_SUCCESS)
-      return fail(HS_ERR_CUDA, "cuFFT D2Z failed");
+    cufftSetStream(p->zf, st);
+    cufftSetStream(p->yf, st);
+    cufftSetStream(p->zi, st);
+    // forward z (D2Z) and y (Z2Z) stages, one source channel at a time through the shared A buffer
+    for (int c = 0; c < p->n_in; ++c) {
+      if (cufftExecD2Z(p->zf, p->grid_in + (size_t)c * p->n_grid, (cufftDoubleComplex*)p->Amix) != CUFFT_SUCCESS)
+        return fail(HS_ERR_CUDA, "cuFFT z D2Z failed");
+      if (cufftExecZ2Z(p->yf, (cufftDoubleComplex*)p->Amix, (cufftDoubleComplex*)(p->spec + (size_t)c * p->n_mixed),
+                       CUFFT_FORWARD) != CUFFT_SUCCESS)
+        return fail(HS_ERR_CUDA, "cuFFT y Z2Z failed");
+    }
     HS_CUDA(cudaEventRecord(ev[4], st));
-    HS_TRY(launch_kscale(ctx, kind, p->half, p->kg, p->tabB, p->tabH, p->spec, p->n_half));
+    {
+      XArgs xa{};
+      xa.B = p->spec;
+      xa.ch_stride = p->n_mixed;
+      xa.tabB = p->tabB;
+      xa.tabH = p->tabH;
+      xa.tw = p->tw;
+      xa.plan = p->xplan;
+      xa.px = p->kg.p[0];
+      xa.py = p->kg.p[1];
+      xa.pz = p->kg.p[2];
+      xa.nzh = p->kg.nzh;
+      xa.nx = p->gg.dims[0];
+      for (int k = 0; k < 3; ++k) xa.kscale[k] = p->kg.kscale[k];
+      xa.ka = p->kg.a;
+      xa.kb = p->kg.b;
+      xa.inv_n = p->kg.inv_n;
+      HS_TRY(launch_xfused(ctx, kind, p->half, xa));
+    }
     HS_CUDA(cudaEventRecord(ev[5], st));
-    if (cufftExecZ2D(p->inv, (cufftDoubleComplex*)p->spec, p->grid_out) != CUFFT_SUCCESS)
-      return fail(HS_ERR_CUDA, "cuFFT Z2D failed");
+    for (int o = 0; o < p->n_out; ++o) {
+      cufftDoubleComplex* so = (cufftDoubleComplex*)(p->spec + (size_t)o * p->n_mixed);
+      if (cufftExecZ2Z(p->yf, so, so, CUFFT_INVERSE) != CUFFT_SUCCESS) return fail(HS_ERR_CUDA, "cuFFT y^-1 failed");
+      if (cufftExecZ2D(p->zi, so, p->grid_out + (size_t)o * p->n_grid) != CUFFT_SUCCESS)
+        return fail(HS_ERR_CUDA, "cuFFT z Z2D failed");
+    }
     HS_CUDA(cudaEventRecord(ev[6], st));
     if (nt > 0) {
       HS_TRY(sort_points_by_bin(p, tp, nt, nt, 0, p->bt_order, p->bt_start));
