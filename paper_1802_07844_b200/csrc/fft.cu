@@ -231,10 +231,11 @@ __device__ __noinline__ void scale_nyquist(double2* col, int cstride, int kx, in
 template <int KIND, bool HALF, int KB, class FFT>
 __global__ void __launch_bounds__(256, 2) k_xfused(const XArgs a) {
   constexpr int NIN = KChan<KIND, HALF>::NIN, NOUT = KChan<KIND, HALF>::NOUT;
+  constexpr int NL = NIN > NOUT ? NIN : NOUT;
   extern __shared__ double2 smem[];
   const int px = a.plan.n;
-  double2* lines = smem;                    // [NIN][KB][px]
-  double2* tw = smem + NIN * KB * px;       // [px]
+  double2* lines = smem;                    // [max(NIN,NOUT)][KB][px]
+  double2* tw = smem + NL * KB * px;        // [px]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int i = tid; i < px; i += blockDim.x) tw[i] = a.tw[i];
   const int nkb = (a.nzh + KB - 1) / KB;
@@ -320,8 +321,9 @@ __global__ void __launch_bounds__(256, 2) k_xfused(const XArgs a) {
 
 template <int KIND, bool HALF, int KB, class FFT>
 static hs_status launch_xfused_t(hs_ctx* ctx, const XArgs& a) {
-  constexpr int NIN = KChan<KIND, HALF>::NIN;
-  const size_t smem = sizeof(double2) * ((size_t)NIN * KB * a.plan.n + a.plan.n);
+  constexpr int NL = KChan<KIND, HALF>::NIN > KChan<KIND, HALF>::NOUT ? KChan<KIND, HALF>::NIN
+                                                                       : KChan<KIND, HALF>::NOUT;
+  const size_t smem = sizeof(double2) * ((size_t)NL * KB * a.plan.n + a.plan.n);
   if (smem > 227 * 1024) return fail(HS_ERR_PARAMETER, "x-stage shared memory exceeds 227 KB");
   auto kern = k_xfused<KIND, HALF, KB, FFT>;
   HS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
