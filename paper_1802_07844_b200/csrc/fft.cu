@@ -23,6 +23,10 @@
 namespace hs {
 
 // ---- warp-cooperative in-place Stockham FFT of one line in shared memory -------------
+// Lines are stored padded (one spare element per 8) so that the strided butterfly
+// writes of the early passes hit 8 distinct 16-byte bank groups per quarter-warp.
+__device__ __forceinline__ int pd8(int i) { return i + (i >> 3); }
+__host__ __device__ __forceinline__ int padded_line(int n) { return n + (n >> 3) + 1; }
 __device__ __forceinline__ double2 cm(double2 a, double2 b) {
   return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
 }
@@ -112,7 +116,7 @@ __device__ __forceinline__ void warp_pass(double2* line, int N, int L, const dou
       const int k = b % L;
 #pragma unroll
       for (int m = 0; m < R; ++m) {
-        double2 x = line[b + m * nb];
+        double2 x = line[pd8(b + m * nb)];
         if (m > 0 && k > 0) x = cm(x, tw[m * k * tstep]);
         v[q][m] = x;
       }
@@ -127,7 +131,7 @@ __device__ __forceinline__ void warp_pass(double2* line, int N, int L, const dou
       const int k = b % L;
       const int base = (b / L) * L * R + k;
 #pragma unroll
-      for (int m = 0; m < R; ++m) line[base + m * L] = v[q][m];
+      for (int m = 0; m < R; ++m) line[pd8(base + m * L)] = v[q][m];
     }
   }
   __syncwarp();
@@ -228,14 +232,17 @@ __device__ __noinline__ void scale_nyquist(double2* col, int cstride, int kx, in
   for (int o = 0; o < NOUT; ++o) col[o * cstride] = make_double2(out[o].re, -out[o].im);
 }
 
+constexpr int XF_THREADS = 512;
+
 template <int KIND, bool HALF, int KB, class FFT>
-__global__ void __launch_bounds__(256, 2) k_xfused(const XArgs a) {
+__global__ void __launch_bounds__(XF_THREADS, 1) k_xfused(const XArgs a) {
   constexpr int NIN = KChan<KIND, HALF>::NIN, NOUT = KChan<KIND, HALF>::NOUT;
   constexpr int NL = NIN > NOUT ? NIN : NOUT;
   extern __shared__ double2 smem[];
   const int px = a.plan.n;
-  double2* lines = smem;                    // [max(NIN,NOUT)][KB][px]
-  double2* tw = smem + NL * KB * px;        // [px]
+  const int LS = padded_line(px);
+  double2* lines = smem;                    // [max(NIN,NOUT)][KB][LS]
+  double2* tw = smem + NL * KB * LS;        // [px]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int i = tid; i < px; i += blockDim.x) tw[i] = a.tw[i];
   const int nkb = (a.nzh + KB - 1) / KB;
@@ -265,10 +272,10 @@ __global__ void __launch_bounds__(256, 2) k_xfused(const XArgs a) {
         }
       }
 #pragma unroll
-      for (int kb = 0; kb < KB; ++kb) lines[(c * KB + kb) * px + x] = v[kb];
+      for (int kb = 0; kb < KB; ++kb) lines[(c * KB + kb) * LS + pd8(x)] = v[kb];
     }
     __syncthreads();
-    for (int l = warp; l < NIN * KB; l += blockDim.x / 32) FFT::run(lines + l * px, a.plan, tw, lane);
+    for (int l = warp; l < NIN * KB; l += blockDim.x / 32) FFT::run(lines + l * LS, a.plan, tw, lane);
     __syncthreads();
     // k-space scaling at every (kx, ky, kz) of the group
     for (int i = tid; i < KB * px; i += blockDim.x) {
@@ -278,15 +285,15 @@ __global__ void __launch_bounds__(256, 2) k_xfused(const XArgs a) {
       const int64_t ti = ((int64_t)ky * a.nzh + kz) * px + kx;
       const double tB = (KIND == HS_ROTLET) ? 0.0 : a.tabB[ti];
       const double tH = (KIND == HS_ROTLET || HALF) ? a.tabH[ti] : 0.0;
-      double2* col = lines + kb * px + kx;  // channel c at col[c * KB * px]
+      double2* col = lines + kb * LS + pd8(kx);  // channel c at col[c * KB * LS]
       if (2 * kx == px || 2 * ky == a.py || 2 * kz == a.pz) {
-        scale_nyquist<KIND, HALF>(col, KB * px, kx, ky, kz, p, a.kscale, a.ka, a.kb, a.inv_n, tB, tH);
+        scale_nyquist<KIND, HALF>(col, KB * LS, kx, ky, kz, p, a.kscale, a.ka, a.kb, a.inv_n, tB, tH);
         continue;
       }
       cplx C[NIN], out[6];
 #pragma unroll
       for (int c = 0; c < NIN; ++c) {
-        const double2 v = col[c * KB * px];
+        const double2 v = col[c * KB * LS];
         C[c] = {v.x, v.y};
       }
       const double s8 = 1.0 / (8.0 * kPi), s4 = 1.0 / (4.0 * kPi);
@@ -299,10 +306,10 @@ __global__ void __launch_bounds__(256, 2) k_xfused(const XArgs a) {
       apply_multiplier<KIND, HALF>(kxv, kyv, kzv, G, Fc, C, out);
       // inverse transform by conjugation: IFFT(y) = conj(FFT(conj(y))) (normalisation already in inv_n)
 #pragma unroll
-      for (int o = 0; o < NOUT; ++o) col[o * KB * px] = make_double2(out[o].re, -out[o].im);
+      for (int o = 0; o < NOUT; ++o) col[o * KB * LS] = make_double2(out[o].re, -out[o].im);
     }
     __syncthreads();
-    for (int l = warp; l < NOUT * KB; l += blockDim.x / 32) FFT::run(lines + l * px, a.plan, tw, lane);
+    for (int l = warp; l < NOUT * KB; l += blockDim.x / 32) FFT::run(lines + l * LS, a.plan, tw, lane);
     __syncthreads();
     // store the x < nx outputs (conjugated back)
     for (int i = tid; i < NOUT * a.nx; i += blockDim.x) {
@@ -311,7 +318,7 @@ __global__ void __launch_bounds__(256, 2) k_xfused(const XArgs a) {
 #pragma unroll
       for (int kb = 0; kb < KB; ++kb) {
         if (kb < kbn) {
-          const double2 v = lines[(o * KB + kb) * px + x];
+          const double2 v = lines[(o * KB + kb) * LS + pd8(x)];
           dst[kb] = make_double2(v.x, -v.y);
         }
       }
@@ -323,16 +330,16 @@ template <int KIND, bool HALF, int KB, class FFT>
 static hs_status launch_xfused_t(hs_ctx* ctx, const XArgs& a) {
   constexpr int NL = KChan<KIND, HALF>::NIN > KChan<KIND, HALF>::NOUT ? KChan<KIND, HALF>::NIN
                                                                        : KChan<KIND, HALF>::NOUT;
-  const size_t smem = sizeof(double2) * ((size_t)NL * KB * a.plan.n + a.plan.n);
+  const size_t smem = sizeof(double2) * ((size_t)NL * KB * padded_line(a.plan.n) + a.plan.n);
   if (smem > 227 * 1024) return fail(HS_ERR_PARAMETER, "x-stage shared memory exceeds 227 KB");
   auto kern = k_xfused<KIND, HALF, KB, FFT>;
   HS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0;
-  HS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem));
+  HS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, XF_THREADS, smem));
   const int nkb = (a.nzh + KB - 1) / KB;
   const int items = a.py * nkb;
   const int grid = std::max(1, std::min(items, ctx->sm_count * std::max(per_sm, 1) * 8));
-  kern<<<grid, 256, smem, ctx->stream>>>(a);
+  kern<<<grid, XF_THREADS, smem, ctx->stream>>>(a);
   HS_LAUNCHED(ctx);
   return HS_OK;
 }

@@ -23,11 +23,13 @@ namespace hs {
 
 __global__ void k_grid_keys(const double* __restrict__ pos, int n_src, int n, int mode, GridGeom g, int nbx,
                             int nby, int nbz, int* __restrict__ keys, unsigned* __restrict__ flags) {
+  const bool fine = (mode & 8) != 0;  // gather targets: sub-bins of 4x4x4 cells inside each tile
+  mode &= 7;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const int s = (mode == 1 && i >= n_src) ? i - n_src : i;
     const bool mir = (mode == 2) || (mode == 1 && i >= n_src);
     const double pc[3] = {pos[3 * s], pos[3 * s + 1], mir ? -pos[3 * s + 2] : pos[3 * s + 2]};
-    int b[3];
+    int b[3], sub[3];
     const int tsz[3] = {SP_TX, SP_TY, SP_TZ};
     const int nb[3] = {nbx, nby, nbz};
     bool bad = false;
@@ -39,9 +41,11 @@ __global__ void k_grid_keys(const double* __restrict__ pos, int n_src, int n, in
       c = c < 0 ? 0 : (c >= g.dims[k] ? g.dims[k] - 1 : c);
       int bb = (int)(c / tsz[k]);
       b[k] = bb >= nb[k] ? nb[k] - 1 : bb;
+      sub[k] = (int)(c - (int64_t)b[k] * tsz[k]) / 4;
     }
     if (bad) atomicOr(flags, FLAG_OUT_OF_GRID);
-    keys[i] = (b[0] * nby + b[1]) * nbz + b[2];
+    const int key = (b[0] * nby + b[1]) * nbz + b[2];
+    keys[i] = fine ? key * SP_NSUB + (sub[0] * (SP_TY / 4) + sub[1]) * (SP_TZ / 4) + sub[2] : key;
   }
 }
 
@@ -116,14 +120,15 @@ __device__ __forceinline__ void window_slice(int node0, int lo, int P, double e1
 }
 
 template <int NCH>
-__global__ void __launch_bounds__(256) k_spread(const int4* __restrict__ lo4, const double4* __restrict__ wxy,
+__global__ void __launch_bounds__(256, 2) k_spread(const int4* __restrict__ lo4, const double4* __restrict__ wxy,
                                                 const double2* __restrict__ wzp, const double* __restrict__ w,
                                                 int ldw, const int* __restrict__ bin_start, GridGeom g,
                                                 WinConst wc, int nbx, int nby, int nbz, double* __restrict__ grids) {
-  __shared__ double s_wx[SP_CHUNK][SP_TX];
-  __shared__ double s_wy[SP_CHUNK][SP_TY];
-  __shared__ double s_wz[SP_CHUNK][SP_TZ];
-  __shared__ double s_q[SP_CHUNK][NCH];
+  // rows padded by one double so the per-source staging writes do not share banks
+  __shared__ double s_wx[SP_CHUNK][SP_TX + 1];
+  __shared__ double s_wy[SP_CHUNK][SP_TY + 1];
+  __shared__ double s_wz[SP_CHUNK][SP_TZ + 1];
+  __shared__ double s_q[SP_CHUNK][NCH | 1];
   __shared__ unsigned s_mask[SP_CHUNK];
   __shared__ double s_e3[SP_MAXP];
   __shared__ int run_beg[9], run_pre[10];
@@ -360,18 +365,114 @@ hs_status launch_gather(hs_ctx* ctx, const double4* pts, const int* perm, int n,
   return HS_OK;
 }
 
-hs_status launch_gather_fourier(hs_ctx* ctx, const double4* pts, const int* orig, int n, int half,
-                                const GridGeom& g, const double* T, double* u_fourier, double* u_total,
-                                const double* u_real) {
+// ---------------------------------------------------------------------------
+// Fourier gather of the half-space pipeline (ewald_fourier.py:626-630):
+//   u_F(t) = h^3 [ sum_p w_t(p) T1(p) - x3_t sum_p w_t(p) T2(p) ]
+// Lanes = 32 targets that are close in space (sorted by 4x4x4 sub-tiles); the warp
+// walks the union of their P^3 supports and every grid value is a single broadcast
+// load shared by all 32 lanes (output grids are channel-interleaved by the inverse
+// z-transform, so one point's channels are 2-3 128-bit loads).  Window factors come
+// from the Gaussian recurrence w(n+1) = w(n) r(n), r(n+1) = r(n) q (q = e^{-2 alpha h^2})
+// started once per lane at the union origin; nodes outside a lane's support are
+// masked to exactly zero (the reference truncates the window at P nodes).
+template <int NCH, int PITCH>
+__global__ void __launch_bounds__(256) k_gather2(const double4* __restrict__ pts, const int* __restrict__ orig, int n,
+                                                 GridGeom g, const double* __restrict__ T, double* __restrict__ u_four,
+                                                 double* __restrict__ u_tot, const double* __restrict__ u_real,
+                                                 unsigned* __restrict__ flags) {
+  const int lane = threadIdx.x & 31;
+  const int nwarps = gridDim.x * (blockDim.x >> 5);
+  const int P = g.P;
+  const double q = exp(-2.0 * g.alpha * g.h * g.h);
+  for (int wbase = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; wbase < n; wbase += nwarps * 32) {
+    const int t = wbase + lane;
+    const bool valid = t < n;
+    const double4 pt = pts[valid ? t : wbase];
+    const double pc[3] = {pt.x, pt.y, pt.z};
+    int lo[3];
+    bool bad = false;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const int64_t l = window_lo(pc[k], g.origin[k], g.h, P);
+      bad |= (l < 0) || (l + P > g.dims[k]);
+      lo[k] = (int)l;
+    }
+    if (valid && bad) atomicOr(flags, FLAG_OUT_OF_GRID);
+    const bool act = valid && !bad;
+    int U0[3], U1[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      U0[k] = (int)__reduce_min_sync(0xffffffffu, (unsigned)(act ? lo[k] : 0x7fffffff));
+      U1[k] = (int)__reduce_max_sync(0xffffffffu, (unsigned)(act ? lo[k] : 0)) + P;
+    }
+    double acc[NCH];
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) acc[c] = 0.0;
+    if (U0[0] <= U1[0] - P) {  // at least one active lane
+      // per-lane recurrence starts at the union origin
+      double w0[3], r0[3];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        const double d = window_d(pc[k], g.origin[k], g.h, U0[k]);
+        w0[k] = act ? exp(-g.alpha * d * d) : 0.0;
+        r0[k] = exp(g.alpha * (2.0 * d * g.h - g.h * g.h));
+      }
+      w0[2] *= g.pref;
+      double wx = w0[0], rx = r0[0];
+      for (int x = U0[0]; x < U1[0]; ++x) {
+        const double wxe = (x >= lo[0] && x < lo[0] + P) ? wx : 0.0;
+        wx *= rx;
+        rx *= q;
+        if (!__any_sync(0xffffffffu, wxe != 0.0)) continue;
+        double wy = w0[1], ry = r0[1];
+        for (int y = U0[1]; y < U1[1]; ++y) {
+          const double wye = (y >= lo[1] && y < lo[1] + P) ? wy : 0.0;
+          wy *= ry;
+          ry *= q;
+          const double cxy = wxe * wye;
+          if (!__any_sync(0xffffffffu, cxy != 0.0)) continue;
+          double wz = w0[2] * cxy, rz = r0[2];
+          const double* src = T + (int64_t)x * g.stride[0] + (int64_t)y * g.stride[1] + (int64_t)U0[2] * PITCH;
+#pragma unroll 4
+          for (int z = U0[2]; z < U1[2]; ++z, src += PITCH) {
+            const double we = (z >= lo[2] && z < lo[2] + P) ? wz : 0.0;
+            wz *= rz;
+            rz *= q;
+            double v[PITCH];
+#pragma unroll
+            for (int c = 0; c < PITCH; c += 2) {
+              const double2 vv = __ldg(reinterpret_cast<const double2*>(src + c));
+              v[c] = vv.x;
+              v[c + 1] = vv.y;
+            }
+#pragma unroll
+            for (int c = 0; c < NCH; ++c) acc[c] = fma(we, v[c], acc[c]);
+          }
+        }
+      }
+    }
+    if (act) {
+      const int o = orig[t];
+      const double h3 = g.h * g.h * g.h;
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        double v = acc[k] * h3;
+        if (NCH == 6) v -= pt.z * (acc[3 + k] * h3);
+        if (u_four) u_four[3 * (size_t)o + k] = v;
+        if (u_tot) u_tot[3 * (size_t)o + k] = (u_real ? u_real[3 * (size_t)o + k] : 0.0) + v;
+      }
+    }
+  }
+}
+
+hs_status launch_gather_fourier(hs_ctx* ctx, const double4* pts, const int* orig, int n, int half, const GridGeom& g,
+                                const double* T, double* u_fourier, double* u_total, const double* u_real) {
   if (n == 0) return HS_OK;
-  if (g.P > 32) return fail(HS_ERR_PARAMETER, "gather supports window support P <= 32");
-  const int gs = (int)std::min<int64_t>(ceil_div(n, 8), ctx->sm_count * 64);
+  const int gs = (int)std::min<int64_t>(ceil_div(n, 256), (int64_t)ctx->sm_count * 32);
   if (half)
-    k_gather<6, 1><<<gs, 256, 0, ctx->stream>>>(pts, orig, n, g, T, u_fourier, 3, 1.0, u_total, u_real,
-                                                ctx->d_flags);
+    k_gather2<6, 6><<<gs, 256, 0, ctx->stream>>>(pts, orig, n, g, T, u_fourier, u_total, u_real, ctx->d_flags);
   else
-    k_gather<3, 1><<<gs, 256, 0, ctx->stream>>>(pts, orig, n, g, T, u_fourier, 3, 1.0, u_total, u_real,
-                                                ctx->d_flags);
+    k_gather2<3, 4><<<gs, 256, 0, ctx->stream>>>(pts, orig, n, g, T, u_fourier, u_total, u_real, ctx->d_flags);
   HS_LAUNCHED(ctx);
   return HS_OK;
 }

@@ -35,6 +35,7 @@ struct GridGeom {
   int64_t ch_stride;       // element stride between channels
 };
 constexpr int SP_TX = 16, SP_TY = 16, SP_TZ = 8;  // spread tile / bin shape
+constexpr int SP_NSUB = (SP_TX / 4) * (SP_TY / 4) * (SP_TZ / 4);  // 4x4x4 sub-bins per tile (gather order)
 inline int sp_nbins(const GridGeom& g, int k) {
   const int t[3] = {SP_TX, SP_TY, SP_TZ};
   return (int)ceil_div(g.dims[k], t[k]);

@@ -227,7 +227,9 @@ struct hs_plan {
   double* grid_in = nullptr;    // n_in * n_grid (z-padding stays zero: the z-transform is out of place)
   double2* Amix = nullptr;      // n_mixed (rows y >= ny stay zero: the y-transform is out of place)
   double2* spec = nullptr;      // max(n_in, n_out) * n_mixed
-  double* grid_out = nullptr;   // n_out * n_grid
+  double* grid_out = nullptr;   // [y][x][z][out_pitch] (channel-interleaved)
+  int out_pitch = 6;
+  GridGeom go{};                // geometry of grid_out
   double* tabB = nullptr;       // x-stage layout [ky][kz][kx]
   double* tabH = nullptr;
   double2* tw = nullptr;        // px twiddles
@@ -344,7 +346,7 @@ extern "C" hs_status hs_plan_create(hs_ctx* ctx, const hs_params* prm, hs_plan**
 
   // ---- buffers
   const int maxn = std::max(p->n_comb, std::max(nt, n));
-  const int maxb = std::max(ncell, nb);
+  const int maxb = std::max(ncell, nb * SP_NSUB);
 #define A_(cnt, ptr, ...) if ((st = palloc(p, (size_t)(cnt), &(ptr), ##__VA_ARGS__)) != HS_OK) return bail(st)
   A_(3 * (size_t)n, p->d_pos);
   A_(3 * (size_t)n, p->d_sa);
@@ -370,7 +372,7 @@ extern "C" hs_status hs_plan_create(hs_ctx* ctx, const hs_params* prm, hs_plan**
   A_(n, p->bc_order);
   A_(nb + 1, p->bc_start);
   A_(std::max(nt, 1), p->bt_order);
-  A_(nb + 1, p->bt_start);
+  A_((size_t)nb * SP_NSUB + 1, p->bt_start);
   A_(p->n_comb, p->SPk);
   A_((size_t)p->n_comb * p->nk, p->SWk);
   if (p->nc) {
@@ -382,7 +384,13 @@ extern "C" hs_status hs_plan_create(hs_ctx* ctx, const hs_params* prm, hs_plan**
   A_((size_t)p->n_in * p->n_grid, p->grid_in, true);
   A_((size_t)p->n_mixed, p->Amix, true);
   A_((size_t)std::max(p->n_in, p->n_out) * p->n_mixed, p->spec);
-  A_((size_t)p->n_out * p->n_grid, p->grid_out);
+  p->out_pitch = p->half ? 6 : 4;
+  A_((size_t)p->out_pitch * p->n_grid, p->grid_out, true);
+  p->go = p->gg;
+  p->go.stride[0] = (int64_t)p->out_pitch * pz;
+  p->go.stride[1] = (int64_t)p->out_pitch * nxd * pz;
+  p->go.stride[2] = p->out_pitch;
+  p->go.ch_stride = 1;
   if (table_needs(prm->kind, p->half, HS_BIHARMONIC)) A_(p->n_half, p->tabB);
   if (table_needs(prm->kind, p->half, HS_HARMONIC)) A_(p->n_half, p->tabH);
   A_(px, p->tw);
@@ -410,7 +418,9 @@ extern "C" hs_status hs_plan_create(hs_ctx* ctx, const hs_params* prm, hs_plan**
     if (cufftMakePlanMany64(p->yf, 1, ny1, ny1, nxd * nzh, 1, ny1, nxd * nzh, 1, CUFFT_Z2Z, nxd * nzh, &w2) !=
         CUFFT_SUCCESS)
       return bail(fail(HS_ERR_RESOURCE, "cuFFT y Z2Z plan failed"));
-    if (cufftMakePlanMany64(p->zi, 1, nz1, nzh1, 1, nzh, nz1, 1, pz, CUFFT_Z2D, nyd * nxd, &w3) != CUFFT_SUCCESS)
+    // inverse z writes the output channels interleaved (pitch = out_pitch) for the gather
+    if (cufftMakePlanMany64(p->zi, 1, nz1, nzh1, 1, nzh, nz1, p->out_pitch, (long long)p->out_pitch * pz, CUFFT_Z2D,
+                            nyd * nxd, &w3) != CUFFT_SUCCESS)
       return bail(fail(HS_ERR_RESOURCE, "cuFFT z Z2D plan failed"));
     const size_t ws = std::max(w1, std::max(w2, w3));
     char* wsp = nullptr;
@@ -593,7 +603,8 @@ hs_status sort_points_by_bin(hs_plan* p, const double* pos, int n_src, int n_tot
                              int* start) {
   hs_ctx* ctx = p->ctx;
   HS_TRY(launch_grid_keys(ctx, pos, n_src, n_total, mode, p->gg, p->keys));
-  return counting_sort(ctx, p->keys, n_total, p->nbins, order, start, p->work);
+  const int nb = (mode & 8) ? p->nbins * SP_NSUB : p->nbins;
+  return counting_sort(ctx, p->keys, n_total, nb, order, start, p->work);
 }
 
 }  // namespace
@@ -752,16 +763,16 @@ extern "C" hs_status hs_plan_execute(hs_plan* p, const double* positions, const 
     for (int o = 0; o < p->n_out; ++o) {
       cufftDoubleComplex* so = (cufftDoubleComplex*)(p->spec + (size_t)o * p->n_mixed);
       if (cufftExecZ2Z(p->yf, so, so, CUFFT_INVERSE) != CUFFT_SUCCESS) return fail(HS_ERR_CUDA, "cuFFT y^-1 failed");
-      if (cufftExecZ2D(p->zi, so, p->grid_out + (size_t)o * p->n_grid) != CUFFT_SUCCESS)
+      if (cufftExecZ2D(p->zi, so, p->grid_out + o) != CUFFT_SUCCESS)
         return fail(HS_ERR_CUDA, "cuFFT z Z2D failed");
     }
     HS_CUDA(cudaEventRecord(ev[6], st));
     if (nt > 0) {
-      HS_TRY(sort_points_by_bin(p, tp, nt, nt, 0, p->bt_order, p->bt_start));
+      HS_TRY(sort_points_by_bin(p, tp, nt, nt, 8, p->bt_order, p->bt_start));
       k_gather_records<<<grid_size(ctx, nt), 256, 0, st>>>(p->bt_order, nt, tp, p->TG, p->tg_orig);
       HS_LAUNCHED(ctx);
       HS_CUDA(cudaEventRecord(ev[13], st));
-      HS_TRY(launch_gather_fourier(ctx, p->TG, p->tg_orig, nt, p->half ? 1 : 0, p->gg, p->grid_out, p->u_four, p->u,
+      HS_TRY(launch_gather_fourier(ctx, p->TG, p->tg_orig, nt, p->half ? 1 : 0, p->go, p->grid_out, p->u_four, p->u,
                                    p->u_real));
       HS_CUDA(cudaEventRecord(ev[14], st));
       gather_timed = true;
