@@ -34,12 +34,13 @@ struct KeyGeom {
 };
 
 __global__ void k_cell_keys(const double* __restrict__ pos, int n_src, int n_total, int mirror, KeyGeom g,
-                            int check_bounds, int* __restrict__ keys, unsigned* __restrict__ flags) {
+                            int check_bounds, int* __restrict__ keys, unsigned* __restrict__ flags, int sub) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_total; i += gridDim.x * blockDim.x) {
     const int s = i < n_src ? i : i - n_src;
     double p[3] = {pos[3 * s], pos[3 * s + 1], pos[3 * s + 2]};
     if (mirror && i >= n_src) p[2] = -p[2];  // y * MIRROR (system.py:168-169)
     int64_t c[3];
+    double vz = 0.0;
     bool bad = false;
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
@@ -49,14 +50,22 @@ __global__ void k_cell_keys(const double* __restrict__ pos, int n_src, int n_tot
       ci = ci < 0 ? 0 : ci;
       ci = ci > g.dims[k] - 1 ? g.dims[k] - 1 : ci;
       c[k] = ci;
+      if (k == 2) vz = v;
     }
     if (check_bounds && bad) atomicOr(flags, FLAG_GEOMETRY);
-    keys[i] = (int)((c[0] * g.dims[1] + c[1]) * g.dims[2] + c[2]);
+    const int flat = (int)((c[0] * g.dims[1] + c[1]) * g.dims[2] + c[2]);
+    if (sub > 1) {
+      int sl = (int)((vz - (double)c[2]) * sub);
+      sl = sl < 0 ? 0 : (sl > sub - 1 ? sub - 1 : sl);
+      keys[i] = flat * sub + sl;
+    } else {
+      keys[i] = flat;
+    }
   }
 }
 
 hs_status launch_cell_keys(hs_ctx* ctx, const double* pos, int n_src, int n_total, int mirror,
-                           const CellGeom& cg, int check_bounds, int* keys) {
+                           const CellGeom& cg, int check_bounds, int* keys, int sub) {
   KeyGeom g;
   for (int k = 0; k < 3; ++k) {
     g.lo[k] = cg.lo[k];
@@ -67,7 +76,8 @@ hs_status launch_cell_keys(hs_ctx* ctx, const double* pos, int n_src, int n_tota
   }
   if (n_total == 0) return HS_OK;
   int gs = (int)std::min<int64_t>(ceil_div(n_total, 256), ctx->sm_count * 8);
-  k_cell_keys<<<gs, 256, 0, ctx->stream>>>(pos, n_src, n_total, mirror, g, check_bounds, keys, ctx->d_flags);
+  k_cell_keys<<<gs, 256, 0, ctx->stream>>>(pos, n_src, n_total, mirror, g, check_bounds, keys, ctx->d_flags,
+                                           sub);
   HS_LAUNCHED(ctx);
   return HS_OK;
 }

@@ -21,8 +21,9 @@ struct CellGeom {
 hs_status cell_geometry(double rc, const double lo[3], const double hi[3], CellGeom* g);
 // keys for n_total points: point i < n_src is pos[i]; i >= n_src is pos[i-n_src]
 // mirrored through z=0 when `mirror` (ImageSystem.combined_positions, system.py:164-191).
+// sub > 1: key = flat * sub + z sub-slab (ordering only; the cell itself is reference-exact)
 hs_status launch_cell_keys(hs_ctx* ctx, const double* pos, int n_src, int n_total, int mirror,
-                           const CellGeom& g, int check_bounds, int* keys);
+                           const CellGeom& g, int check_bounds, int* keys, int sub = 1);
 
 // ---------------------------------------------------------------------------
 // spreading / gathering (gridding.cu)
@@ -66,7 +67,8 @@ struct PairArgs {
   const int* start;   // src cell start, ncell+1
   const double4* TP;  // cell-sorted targets: x, y, z, tcol
   const int* torig;   // output row of each sorted target
-  const int* t_start; // target cell start, ncell+1
+  const int* t_start; // target (cell, z sub-slab) start, ncell*t_sub+1
+  int t_sub;          // z sub-slabs per cell in the target order
   const int2* items;  // work items (cell column, first sorted target)
   int max_items;      // launch bound (>= actual count)
   const int* n_items_d;  // actual count (device)
@@ -78,6 +80,7 @@ struct PairArgs {
     return (int)(c > dims[2] - 1 ? dims[2] - 1 : c);
   }
   double xi, rc2;
+  float rc2_hi;       // FP32 prefilter bound: (rc (1+1e-4) + 2^-20 box)^2, conservative
   int n_real;         // combined index >= n_real -> image
   int kind;
   const double* self_f;  // stokeslet self term strengths (original f) or null

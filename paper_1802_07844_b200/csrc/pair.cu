@@ -161,6 +161,7 @@ constexpr int PC_Q = 64;              // per-lane queue capacity
 template <int KIND, bool HALF>
 __global__ void __launch_bounds__(PC_TG) k_pair_q(const PairArgs a) {
   __shared__ double4 sP[PC_K];
+  __shared__ float4 sF[PC_K];   // candidate position relative to the item's first target (FP32 prefilter)
   __shared__ double4 sA[PC_K];
   constexpr bool kNeedB = (KIND == HS_STRESSLET) || (KIND == HS_ROTLET && HALF);
   __shared__ double4 sB[kNeedB ? PC_K : 1];
@@ -185,7 +186,7 @@ __global__ void __launch_bounds__(PC_TG) k_pair_q(const PairArgs a) {
   for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
     const int2 item = a.items[it];
     const int col = item.x, t0 = item.y;
-    const int t1 = min(t0 + PC_TG, a.t_start[(col + 1) * nz]);
+    const int t1 = min(t0 + PC_TG, a.t_start[(col + 1) * nz * a.t_sub]);
     const int ix = col / ny, iy = col % ny;
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -213,6 +214,22 @@ __global__ void __launch_bounds__(PC_TG) k_pair_q(const PairArgs a) {
     const bool tvalid = t < t1;
     const double4 T = a.TP[tvalid ? t : t0];
     const long long tcol = tvalid ? (long long)T.w : -2;  // -2 never matches a source id
+    // FP32 view relative to the item's first target, and this warp's target bounding box
+    const double4 R0 = a.TP[t0];
+    const float tfx = (float)(T.x - R0.x), tfy = (float)(T.y - R0.y), tfz = (float)(T.z - R0.z);
+    float bmin[3] = {tfx, tfy, tfz}, bmax[3] = {tfx, tfy, tfz};
+    if (!tvalid) {
+      bmin[0] = bmin[1] = bmin[2] = 3.0e38f;
+      bmax[0] = bmax[1] = bmax[2] = -3.0e38f;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        bmin[k] = fminf(bmin[k], __shfl_xor_sync(0xffffffffu, bmin[k], o));
+        bmax[k] = fmaxf(bmax[k], __shfl_xor_sync(0xffffffffu, bmax[k], o));
+      }
+    }
     double acc[6] = {0, 0, 0, 0, 0, 0};
     int qlen = 0;
     bool singular = false;
@@ -237,7 +254,9 @@ __global__ void __launch_bounds__(PC_TG) k_pair_q(const PairArgs a) {
           int r = 0;
           while (r + 1 < nrun && run_pre[r + 1] <= v) ++r;
           const int row = run_beg[r] + (v - run_pre[r]);
-          sP[j] = a.P[row];
+          const double4 S = a.P[row];
+          sP[j] = S;
+          sF[j] = make_float4((float)(S.x - R0.x), (float)(S.y - R0.y), (float)(S.z - R0.z), 0.0f);
           sA[j] = a.A[row];
           if (kNeedB) sB[j] = a.B[row];
         }
@@ -245,19 +264,37 @@ __global__ void __launch_bounds__(PC_TG) k_pair_q(const PairArgs a) {
       __syncthreads();
       const int nc = min(PC_K, ncand - c0);
       for (int j0 = 0; j0 < nc; j0 += 32) {
-        const int jn = min(32, nc - j0);
-#pragma unroll 4
-        for (int jj = 0; jj < jn; ++jj) {
-          const int j = j0 + jj;
-          const double4 S = sP[j];  // broadcast
-          const double d0 = __dsub_rn(T.x, S.x), d1 = __dsub_rn(T.y, S.y), d2 = __dsub_rn(T.z, S.z);
-          const double r2 = exact_r2(d0, d1, d2);
-          if (r2 <= a.rc2 && (long long)S.w != tcol && tvalid) {
-            if (r2 == 0.0) {
-              singular = true;
-            } else {
-              q[qlen][lane] = (unsigned short)j;
-              ++qlen;
+        // warp-level culling: candidates farther than rc (+margin) from the warp's target box
+        unsigned near;
+        {
+          const int j = j0 + lane;
+          bool keep = false;
+          if (j < nc) {
+            const float4 F = sF[j];
+            const float dx = fmaxf(fmaxf(bmin[0] - F.x, F.x - bmax[0]), 0.0f);
+            const float dy = fmaxf(fmaxf(bmin[1] - F.y, F.y - bmax[1]), 0.0f);
+            const float dz = fmaxf(fmaxf(bmin[2] - F.z, F.z - bmax[2]), 0.0f);
+            keep = dx * dx + dy * dy + dz * dz <= a.rc2_hi;
+          }
+          near = __ballot_sync(0xffffffffu, keep);
+        }
+        while (near) {
+          const int j = j0 + __ffs(near) - 1;
+          near &= near - 1;
+          const float4 F = sF[j];  // broadcast
+          const float fx = tfx - F.x, fy = tfy - F.y, fz = tfz - F.z;
+          if (fx * fx + fy * fy + fz * fz <= a.rc2_hi) {
+            // exact reference test (bit-identical neighbour sets)
+            const double4 S = sP[j];
+            const double d0 = __dsub_rn(T.x, S.x), d1 = __dsub_rn(T.y, S.y), d2 = __dsub_rn(T.z, S.z);
+            const double r2 = exact_r2(d0, d1, d2);
+            if (r2 <= a.rc2 && (long long)S.w != tcol && tvalid) {
+              if (r2 == 0.0) {
+                singular = true;
+              } else {
+                q[qlen][lane] = (unsigned short)j;
+                ++qlen;
+              }
             }
           }
         }
@@ -318,7 +355,7 @@ __global__ void __launch_bounds__(PC_TG) k_pair_q(const PairArgs a) {
 // work items: (column, first target) for every group of PC_TG targets of a cell column
 __global__ void k_count_groups(const int* __restrict__ t_start, int ncol, int nz, int* __restrict__ cnt) {
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < ncol; c += gridDim.x * blockDim.x) {
-    const int n = t_start[(c + 1) * nz] - t_start[c * nz];
+    const int n = t_start[(c + 1) * nz] - t_start[c * nz];  // nz here = cells per column * sub-slabs
     cnt[c] = (n + PC_TG - 1) / PC_TG;
   }
 }

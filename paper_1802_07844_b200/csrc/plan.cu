@@ -153,6 +153,17 @@ __global__ void k_self_term(int nt, const double* __restrict__ tpos, const long 
   }
 }
 
+// grid_out[i * pitch + c] = tmp[c][i]
+__global__ void k_interleave(const double* __restrict__ tmp, int nch, int64_t n, int pitch, double* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    double v[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) v[c] = c < nch ? tmp[(int64_t)c * n + i] : 0.0;
+    double2* o = reinterpret_cast<double2*>(out + i * pitch);
+    for (int c = 0; c < pitch; c += 2) o[c / 2] = make_double2(v[c], v[c + 1]);
+  }
+}
+
 // targets for the Fourier gather, in bin order
 __global__ void k_gather_records(const int* __restrict__ order, int nt, const double* __restrict__ tpos,
                                  double4* __restrict__ TG, int* __restrict__ tg_orig) {
@@ -229,6 +240,7 @@ struct hs_plan {
   double2* spec = nullptr;      // max(n_in, n_out) * n_mixed
   double* grid_out = nullptr;   // [y][x][z][out_pitch] (channel-interleaved)
   int out_pitch = 6;
+  double* grid_tmp = nullptr;   // n_out * n_grid: inverse-z outputs before interleaving
   GridGeom go{};                // geometry of grid_out
   double* tabB = nullptr;       // x-stage layout [ky][kz][kx]
   double* tabH = nullptr;
@@ -244,6 +256,8 @@ struct hs_plan {
 };
 
 namespace {
+
+constexpr int kTargetSub = 8;  // z sub-slabs per cell in the pair-kernel target order
 
 template <typename T>
 hs_status palloc(hs_plan* p, size_t count, T** out, bool zero = false) {
@@ -346,7 +360,7 @@ extern "C" hs_status hs_plan_create(hs_ctx* ctx, const hs_params* prm, hs_plan**
 
   // ---- buffers
   const int maxn = std::max(p->n_comb, std::max(nt, n));
-  const int maxb = std::max(ncell, nb * SP_NSUB);
+  const int maxb = std::max(ncell * kTargetSub, nb * SP_NSUB);
 #define A_(cnt, ptr, ...) if ((st = palloc(p, (size_t)(cnt), &(ptr), ##__VA_ARGS__)) != HS_OK) return bail(st)
   A_(3 * (size_t)n, p->d_pos);
   A_(3 * (size_t)n, p->d_sa);
@@ -360,7 +374,7 @@ extern "C" hs_status hs_plan_create(hs_ctx* ctx, const hs_params* prm, hs_plan**
   A_(counting_sort_work_ints(maxn, maxb), p->work);
   A_(ncell + 1, p->start);
   A_(nt + 1, p->t_order);
-  A_(ncell + 1, p->t_start);
+  A_((size_t)ncell * kTargetSub + 1, p->t_start);
   A_((size_t)nt / 128 + (size_t)p->cg.dims[0] * p->cg.dims[1] + 2, p->items);
   A_(p->n_comb, p->P);
   A_(p->n_comb, p->A);
@@ -386,6 +400,7 @@ extern "C" hs_status hs_plan_create(hs_ctx* ctx, const hs_params* prm, hs_plan**
   A_((size_t)std::max(p->n_in, p->n_out) * p->n_mixed, p->spec);
   p->out_pitch = p->half ? 6 : 4;
   A_((size_t)p->out_pitch * p->n_grid, p->grid_out, true);
+  A_((size_t)p->n_out * p->n_grid, p->grid_tmp);
   p->go = p->gg;
   p->go.stride[0] = (int64_t)p->out_pitch * pz;
   p->go.stride[1] = (int64_t)p->out_pitch * nxd * pz;
@@ -418,9 +433,7 @@ extern "C" hs_status hs_plan_create(hs_ctx* ctx, const hs_params* prm, hs_plan**
     if (cufftMakePlanMany64(p->yf, 1, ny1, ny1, nxd * nzh, 1, ny1, nxd * nzh, 1, CUFFT_Z2Z, nxd * nzh, &w2) !=
         CUFFT_SUCCESS)
       return bail(fail(HS_ERR_RESOURCE, "cuFFT y Z2Z plan failed"));
-    // inverse z writes the output channels interleaved (pitch = out_pitch) for the gather
-    if (cufftMakePlanMany64(p->zi, 1, nz1, nzh1, 1, nzh, nz1, p->out_pitch, (long long)p->out_pitch * pz, CUFFT_Z2D,
-                            nyd * nxd, &w3) != CUFFT_SUCCESS)
+    if (cufftMakePlanMany64(p->zi, 1, nz1, nzh1, 1, nzh, nz1, 1, pz, CUFFT_Z2D, nyd * nxd, &w3) != CUFFT_SUCCESS)
       return bail(fail(HS_ERR_RESOURCE, "cuFFT z Z2D plan failed"));
     const size_t ws = std::max(w1, std::max(w2, w3));
     char* wsp = nullptr;
@@ -593,10 +606,10 @@ extern "C" hs_status hs_plan_build_tables(hs_plan* p, const int64_t big[3], doub
 namespace {
 
 hs_status sort_points_by_cell(hs_plan* p, const double* pos, int n_src, int n_total, int mirror, int check,
-                              int* order, int* start) {
+                              int* order, int* start, int sub = 1) {
   hs_ctx* ctx = p->ctx;
-  HS_TRY(launch_cell_keys(ctx, pos, n_src, n_total, mirror, p->cg, check, p->keys));
-  return counting_sort(ctx, p->keys, n_total, (int)p->cg.ncell(), order, start, p->work);
+  HS_TRY(launch_cell_keys(ctx, pos, n_src, n_total, mirror, p->cg, check, p->keys, sub));
+  return counting_sort(ctx, p->keys, n_total, (int)p->cg.ncell() * sub, order, start, p->work);
 }
 
 hs_status sort_points_by_bin(hs_plan* p, const double* pos, int n_src, int n_total, int mode, int* order,
@@ -659,12 +672,14 @@ extern "C" hs_status hs_plan_execute(hs_plan* p, const double* positions, const 
                                                               p->P, p->A, p->B);
     HS_LAUNCHED(ctx);
     if (nt > 0) {
-      HS_TRY(sort_points_by_cell(p, tp, nt, nt, 0, 0, p->t_order, p->t_start));
+      // targets: reference cells, ordered by z sub-slab inside each cell (compact warps)
+      HS_TRY(sort_points_by_cell(p, tp, nt, nt, 0, 0, p->t_order, p->t_start, kTargetSub));
       k_target_records<<<grid_size(ctx, nt), 256, 0, st>>>(p->t_order, nt, tp, tc, tcol_identity, p->TP, p->torig);
       HS_LAUNCHED(ctx);
       const int ncol = (int)(p->cg.dims[0] * p->cg.dims[1]);
       const int* n_items_d = nullptr;
-      HS_TRY(build_pair_items(ctx, p->t_start, ncol, (int)p->cg.dims[2], p->work, p->items, &n_items_d));
+      HS_TRY(build_pair_items(ctx, p->t_start, ncol, (int)p->cg.dims[2] * kTargetSub, p->work, p->items,
+                              &n_items_d));
       PairArgs a{};
       a.P = p->P;
       a.A = p->A;
@@ -673,6 +688,7 @@ extern "C" hs_status hs_plan_execute(hs_plan* p, const double* positions, const 
       a.TP = p->TP;
       a.torig = p->torig;
       a.t_start = p->t_start;
+      a.t_sub = kTargetSub;
       a.items = p->items;
       a.max_items = nt / 128 + ncol + 1;
       a.n_items_d = n_items_d;
@@ -681,6 +697,12 @@ extern "C" hs_status hs_plan_execute(hs_plan* p, const double* positions, const 
       a.cz_edge = p->cg.edge[2];
       a.xi = prm.xi;
       a.rc2 = prm.rc * prm.rc;
+      {
+        // FP32 prefilter bound: relative FP32 coordinates err by < 2^-22 * (box size); keep a wide margin
+        const double box = 3.0 * prm.L;
+        const double rch = prm.rc * (1.0 + 1e-4) + box * std::ldexp(1.0, -20);
+        a.rc2_hi = (float)(rch * rch) * (1.0f + 1e-6f);
+      }
       a.n_real = n;
       a.kind = kind | (p->half ? 16 : 0);
       a.self_f = kind == HS_STOKESLET ? fa : nullptr;
@@ -763,9 +785,13 @@ extern "C" hs_status hs_plan_execute(hs_plan* p, const double* positions, const 
     for (int o = 0; o < p->n_out; ++o) {
       cufftDoubleComplex* so = (cufftDoubleComplex*)(p->spec + (size_t)o * p->n_mixed);
       if (cufftExecZ2Z(p->yf, so, so, CUFFT_INVERSE) != CUFFT_SUCCESS) return fail(HS_ERR_CUDA, "cuFFT y^-1 failed");
-      if (cufftExecZ2D(p->zi, so, p->grid_out + o) != CUFFT_SUCCESS)
+      if (cufftExecZ2D(p->zi, so, p->grid_tmp + (size_t)o * p->n_grid) != CUFFT_SUCCESS)
         return fail(HS_ERR_CUDA, "cuFFT z Z2D failed");
     }
+    // channel-interleave the (y < ny, x < nx, z < nz) outputs for the broadcast gather
+    k_interleave<<<grid_size(ctx, p->n_grid / 2), 256, 0, st>>>(p->grid_tmp, p->n_out, p->n_grid, p->out_pitch,
+                                                                p->grid_out);
+    HS_LAUNCHED(ctx);
     HS_CUDA(cudaEventRecord(ev[6], st));
     if (nt > 0) {
       HS_TRY(sort_points_by_bin(p, tp, nt, nt, 8, p->bt_order, p->bt_start));
