@@ -15,6 +15,7 @@
 // support column (coalesced 8*P-byte reads), loop over the P*P columns,
 // shuffle reduction over lanes.
 #include <cmath>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -409,35 +410,45 @@ __global__ void __launch_bounds__(256) k_gather2(const double4* __restrict__ pts
 #pragma unroll
     for (int c = 0; c < NCH; ++c) acc[c] = 0.0;
     if (U0[0] <= U1[0] - P) {  // at least one active lane
-      // per-lane recurrence starts at the union origin
+      // per-lane recurrence starts at the lane's own first support node (values stay O(1):
+      // starting at the union origin could underflow for widely spread warps)
       double w0[3], r0[3];
 #pragma unroll
       for (int k = 0; k < 3; ++k) {
-        const double d = window_d(pc[k], g.origin[k], g.h, U0[k]);
+        const double d = window_d(pc[k], g.origin[k], g.h, lo[k]);
         w0[k] = act ? exp(-g.alpha * d * d) : 0.0;
         r0[k] = exp(g.alpha * (2.0 * d * g.h - g.h * g.h));
       }
       w0[2] *= g.pref;
       double wx = w0[0], rx = r0[0];
       for (int x = U0[0]; x < U1[0]; ++x) {
-        const double wxe = (x >= lo[0] && x < lo[0] + P) ? wx : 0.0;
-        wx *= rx;
-        rx *= q;
+        const bool inx = x >= lo[0] && x < lo[0] + P;
+        const double wxe = inx ? wx : 0.0;
+        if (inx) {
+          wx *= rx;
+          rx *= q;
+        }
         if (!__any_sync(0xffffffffu, wxe != 0.0)) continue;
         double wy = w0[1], ry = r0[1];
         for (int y = U0[1]; y < U1[1]; ++y) {
-          const double wye = (y >= lo[1] && y < lo[1] + P) ? wy : 0.0;
-          wy *= ry;
-          ry *= q;
+          const bool iny = y >= lo[1] && y < lo[1] + P;
+          const double wye = iny ? wy : 0.0;
+          if (iny) {
+            wy *= ry;
+            ry *= q;
+          }
           const double cxy = wxe * wye;
           if (!__any_sync(0xffffffffu, cxy != 0.0)) continue;
           double wz = w0[2] * cxy, rz = r0[2];
           const double* src = T + (int64_t)x * g.stride[0] + (int64_t)y * g.stride[1] + (int64_t)U0[2] * PITCH;
 #pragma unroll 4
           for (int z = U0[2]; z < U1[2]; ++z, src += PITCH) {
-            const double we = (z >= lo[2] && z < lo[2] + P) ? wz : 0.0;
-            wz *= rz;
-            rz *= q;
+            const bool inz = z >= lo[2] && z < lo[2] + P;
+            const double we = inz ? wz : 0.0;
+            if (inz) {
+              wz *= rz;
+              rz *= q;
+            }
             double v[PITCH];
 #pragma unroll
             for (int c = 0; c < PITCH; c += 2) {
@@ -468,6 +479,18 @@ __global__ void __launch_bounds__(256) k_gather2(const double4* __restrict__ pts
 hs_status launch_gather_fourier(hs_ctx* ctx, const double4* pts, const int* orig, int n, int half, const GridGeom& g,
                                 const double* T, double* u_fourier, double* u_total, const double* u_real) {
   if (n == 0) return HS_OK;
+  static const bool v1 = getenv("HS_GATHER_V1") != nullptr;  // debugging aid: warp-per-target gather
+  if (v1) {
+    const int gs1 = (int)std::min<int64_t>(ceil_div(n, 8), ctx->sm_count * 64);
+    if (half)
+      k_gather<6, 1><<<gs1, 256, 0, ctx->stream>>>(pts, orig, n, g, T, u_fourier, 3, 1.0, u_total, u_real,
+                                                   ctx->d_flags);
+    else
+      k_gather<3, 1><<<gs1, 256, 0, ctx->stream>>>(pts, orig, n, g, T, u_fourier, 3, 1.0, u_total, u_real,
+                                                   ctx->d_flags);
+    HS_LAUNCHED(ctx);
+    return HS_OK;
+  }
   const int gs = (int)std::min<int64_t>(ceil_div(n, 256), (int64_t)ctx->sm_count * 32);
   if (half)
     k_gather2<6, 6><<<gs, 256, 0, ctx->stream>>>(pts, orig, n, g, T, u_fourier, u_total, u_real, ctx->d_flags);
