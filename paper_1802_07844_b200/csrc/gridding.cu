@@ -369,26 +369,30 @@ hs_status launch_gather(hs_ctx* ctx, const double4* pts, const int* perm, int n,
 // ---------------------------------------------------------------------------
 // Fourier gather of the half-space pipeline (ewald_fourier.py:626-630):
 //   u_F(t) = h^3 [ sum_p w_t(p) T1(p) - x3_t sum_p w_t(p) T2(p) ]
-// Lanes = 32 targets that are close in space (sorted by 4x4x4 sub-tiles); the warp
-// walks the union of their P^3 supports and every grid value is a single broadcast
-// load shared by all 32 lanes (output grids are channel-interleaved by the inverse
-// z-transform, so one point's channels are 2-3 128-bit loads).  Window factors come
-// from the Gaussian recurrence w(n+1) = w(n) r(n), r(n+1) = r(n) q (q = e^{-2 alpha h^2})
-// started once per lane at the union origin; nodes outside a lane's support are
-// masked to exactly zero (the reference truncates the window at P nodes).
+// A CTA owns GA_T consecutive targets of the 4x4x4-sub-tile order (spatially compact).
+// It walks the x-planes of the union of their supports; each plane slab
+// (y-range x z-range x channels) is staged in shared memory by the whole CTA
+// (coalesced rows of the channel-interleaved output grid), then every warp
+// (lanes = 32 targets) accumulates its targets from broadcast shared-memory reads.
+// Window factors come from the Gaussian recurrence w(n+1) = w(n) r(n),
+// r(n+1) = r(n) q (q = e^{-2 alpha h^2}) started at each lane's first support node.
+constexpr int GA_T = 256;                 // targets (threads) per CTA
+constexpr int GA_SMEM_DOUBLES = 9216;     // 72 KB plane slab
+
 template <int NCH, int PITCH>
-__global__ void __launch_bounds__(256) k_gather2(const double4* __restrict__ pts, const int* __restrict__ orig, int n,
-                                                 GridGeom g, const double* __restrict__ T, double* __restrict__ u_four,
-                                                 double* __restrict__ u_tot, const double* __restrict__ u_real,
-                                                 unsigned* __restrict__ flags) {
+__global__ void __launch_bounds__(GA_T, 2) k_gather3(const double4* __restrict__ pts, const int* __restrict__ orig,
+                                                    int n, GridGeom g, const double* __restrict__ T,
+                                                    double* __restrict__ u_four, double* __restrict__ u_tot,
+                                                    const double* __restrict__ u_real, unsigned* __restrict__ flags) {
+  extern __shared__ __align__(16) double slab[];  // GA_SMEM_DOUBLES
+  __shared__ int s_box[6];
   const int lane = threadIdx.x & 31;
-  const int nwarps = gridDim.x * (blockDim.x >> 5);
   const int P = g.P;
   const double q = exp(-2.0 * g.alpha * g.h * g.h);
-  for (int wbase = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; wbase < n; wbase += nwarps * 32) {
-    const int t = wbase + lane;
+  for (int base = blockIdx.x * GA_T; base < n; base += gridDim.x * GA_T) {
+    const int t = base + threadIdx.x;
     const bool valid = t < n;
-    const double4 pt = pts[valid ? t : wbase];
+    const double4 pt = pts[valid ? t : base];
     const double pc[3] = {pt.x, pt.y, pt.z};
     int lo[3];
     bool bad = false;
@@ -400,18 +404,32 @@ __global__ void __launch_bounds__(256) k_gather2(const double4* __restrict__ pts
     }
     if (valid && bad) atomicOr(flags, FLAG_OUT_OF_GRID);
     const bool act = valid && !bad;
-    int U0[3], U1[3];
+    // warp and CTA union boxes
+    int W0[3], W1[3];
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-      U0[k] = (int)__reduce_min_sync(0xffffffffu, (unsigned)(act ? lo[k] : 0x7fffffff));
-      U1[k] = (int)__reduce_max_sync(0xffffffffu, (unsigned)(act ? lo[k] : 0)) + P;
+      W0[k] = (int)__reduce_min_sync(0xffffffffu, (unsigned)(act ? lo[k] : 0x7fffffff));
+      W1[k] = (int)__reduce_max_sync(0xffffffffu, (unsigned)(act ? lo[k] + P : 0));
     }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      s_box[0] = s_box[1] = s_box[2] = 0x7fffffff;
+      s_box[3] = s_box[4] = s_box[5] = 0;
+    }
+    __syncthreads();
+    if (lane == 0 && W1[0] > 0) {
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        atomicMin(&s_box[k], W0[k]);
+        atomicMax(&s_box[3 + k], W1[k]);
+      }
+    }
+    __syncthreads();
+    const int X0 = s_box[0], Y0 = s_box[1], Z0 = s_box[2], X1 = s_box[3], Y1 = s_box[4], Z1 = s_box[5];
     double acc[NCH];
 #pragma unroll
     for (int c = 0; c < NCH; ++c) acc[c] = 0.0;
-    if (U0[0] <= U1[0] - P) {  // at least one active lane
-      // per-lane recurrence starts at the lane's own first support node (values stay O(1):
-      // starting at the union origin could underflow for widely spread warps)
+    if (X1 > X0) {
       double w0[3], r0[3];
 #pragma unroll
       for (int k = 0; k < 3; ++k) {
@@ -420,44 +438,76 @@ __global__ void __launch_bounds__(256) k_gather2(const double4* __restrict__ pts
         r0[k] = exp(g.alpha * (2.0 * d * g.h - g.h * g.h));
       }
       w0[2] *= g.pref;
+      const int nzu = Z1 - Z0;
+      const int rowlen = nzu * PITCH;                       // doubles per staged row
+      const int ychunk = max(1, min(Y1 - Y0, GA_SMEM_DOUBLES / rowlen));
       double wx = w0[0], rx = r0[0];
-      for (int x = U0[0]; x < U1[0]; ++x) {
+      for (int x = X0; x < X1; ++x) {
         const bool inx = x >= lo[0] && x < lo[0] + P;
         const double wxe = inx ? wx : 0.0;
         if (inx) {
           wx *= rx;
           rx *= q;
         }
-        if (!__any_sync(0xffffffffu, wxe != 0.0)) continue;
+        const bool warp_x = __any_sync(0xffffffffu, wxe != 0.0);
         double wy = w0[1], ry = r0[1];
-        for (int y = U0[1]; y < U1[1]; ++y) {
-          const bool iny = y >= lo[1] && y < lo[1] + P;
-          const double wye = iny ? wy : 0.0;
-          if (iny) {
-            wy *= ry;
-            ry *= q;
+        for (int yc = Y0; yc < Y1; yc += ychunk) {
+          const int yn = min(ychunk, Y1 - yc);
+          __syncthreads();
+          // stage rows y in [yc, yc+yn) of plane x: contiguous (z, channel) runs
+          {
+            const int nvec = rowlen / 2;  // double2 per row
+            for (int i = threadIdx.x; i < yn * nvec; i += GA_T) {
+              const int r = i / nvec, v = i - r * nvec;
+              const double* src = T + (int64_t)x * g.stride[0] + (int64_t)(yc + r) * g.stride[1] +
+                                  (int64_t)Z0 * PITCH + 2 * v;
+              reinterpret_cast<double2*>(slab)[r * nvec + v] = __ldg(reinterpret_cast<const double2*>(src));
+            }
           }
-          const double cxy = wxe * wye;
-          if (!__any_sync(0xffffffffu, cxy != 0.0)) continue;
-          double wz = w0[2] * cxy, rz = r0[2];
-          const double* src = T + (int64_t)x * g.stride[0] + (int64_t)y * g.stride[1] + (int64_t)U0[2] * PITCH;
-#pragma unroll 4
-          for (int z = U0[2]; z < U1[2]; ++z, src += PITCH) {
-            const bool inz = z >= lo[2] && z < lo[2] + P;
-            const double we = inz ? wz : 0.0;
-            if (inz) {
-              wz *= rz;
-              rz *= q;
+          __syncthreads();
+          if (!warp_x) continue;
+          const int ya = max(yc, W0[1]), yb = min(yc + yn, W1[1]);
+          for (int y = yc; y < ya; ++y) {  // advance the y recurrence through rows before this warp's range
+            if (y >= lo[1] && y < lo[1] + P) {
+              wy *= ry;
+              ry *= q;
             }
-            double v[PITCH];
-#pragma unroll
-            for (int c = 0; c < PITCH; c += 2) {
-              const double2 vv = __ldg(reinterpret_cast<const double2*>(src + c));
-              v[c] = vv.x;
-              v[c + 1] = vv.y;
+          }
+          for (int y = ya; y < yb; ++y) {
+            const bool iny = y >= lo[1] && y < lo[1] + P;
+            const double wye = iny ? wy : 0.0;
+            if (iny) {
+              wy *= ry;
+              ry *= q;
             }
+            const double cxy = wxe * wye;
+            if (!__any_sync(0xffffffffu, cxy != 0.0)) continue;
+            double wz = w0[2] * cxy, rz = r0[2];
+            const double* row = slab + (y - yc) * rowlen;
+            for (int z = W0[2]; z < W1[2]; ++z) {
+              const bool inz = z >= lo[2] && z < lo[2] + P;
+              const double we = inz ? wz : 0.0;
+              if (inz) {
+                wz *= rz;
+                rz *= q;
+              }
+              const double* pz = row + (z - Z0) * PITCH;
+              double v[PITCH];
 #pragma unroll
-            for (int c = 0; c < NCH; ++c) acc[c] = fma(we, v[c], acc[c]);
+              for (int c = 0; c < PITCH; c += 2) {
+                const double2 vv = *reinterpret_cast<const double2*>(pz + c);
+                v[c] = vv.x;
+                v[c + 1] = vv.y;
+              }
+#pragma unroll
+              for (int c = 0; c < NCH; ++c) acc[c] = fma(we, v[c], acc[c]);
+            }
+          }
+          for (int y = yb; y < yc + yn; ++y) {  // rows after this warp's range (keep the recurrence in step)
+            if (y >= lo[1] && y < lo[1] + P) {
+              wy *= ry;
+              ry *= q;
+            }
           }
         }
       }
@@ -491,11 +541,15 @@ hs_status launch_gather_fourier(hs_ctx* ctx, const double4* pts, const int* orig
     HS_LAUNCHED(ctx);
     return HS_OK;
   }
-  const int gs = (int)std::min<int64_t>(ceil_div(n, 256), (int64_t)ctx->sm_count * 32);
-  if (half)
-    k_gather2<6, 6><<<gs, 256, 0, ctx->stream>>>(pts, orig, n, g, T, u_fourier, u_total, u_real, ctx->d_flags);
-  else
-    k_gather2<3, 4><<<gs, 256, 0, ctx->stream>>>(pts, orig, n, g, T, u_fourier, u_total, u_real, ctx->d_flags);
+  const int gs = (int)std::min<int64_t>(ceil_div(n, GA_T), (int64_t)ctx->sm_count * 32);
+  const size_t smem = sizeof(double) * GA_SMEM_DOUBLES;
+  if (half) {
+    HS_CUDA(cudaFuncSetAttribute(k_gather3<6, 6>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_gather3<6, 6><<<gs, GA_T, smem, ctx->stream>>>(pts, orig, n, g, T, u_fourier, u_total, u_real, ctx->d_flags);
+  } else {
+    HS_CUDA(cudaFuncSetAttribute(k_gather3<3, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_gather3<3, 4><<<gs, GA_T, smem, ctx->stream>>>(pts, orig, n, g, T, u_fourier, u_total, u_real, ctx->d_flags);
+  }
   HS_LAUNCHED(ctx);
   return HS_OK;
 }

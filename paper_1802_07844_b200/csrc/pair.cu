@@ -159,7 +159,7 @@ constexpr int PC_K = 256;             // candidates per staged chunk
 constexpr int PC_Q = 64;              // per-lane queue capacity
 
 template <int KIND, bool HALF>
-__global__ void __launch_bounds__(PC_TG) k_pair_q(const PairArgs a) {
+__global__ void __launch_bounds__(PC_TG, 5) k_pair_q(const PairArgs a) {
   __shared__ double4 sP[PC_K];
   __shared__ float4 sF[PC_K];   // candidate position relative to the item's first target (FP32 prefilter)
   __shared__ double4 sA[PC_K];
