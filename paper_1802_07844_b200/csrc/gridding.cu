@@ -67,7 +67,7 @@ hs_status launch_grid_keys(hs_ctx* ctx, const double* pos, int n_src, int n, int
 // (d0 = distance to the first support node, _gridding.py:24-29), so a tile's
 // window slice costs two multiplies per node instead of one exp; E1/E2 are
 // computed once per source (k_spread_windows).
-constexpr int SP_CHUNK = 64;   // sources staged per round
+constexpr int SP_CHUNK = 96;   // sources staged per round
 constexpr int SP_MAXCH = 4;    // channels per launch (register budget)
 constexpr int SP_MAXP = 64;
 
@@ -175,20 +175,22 @@ __global__ void __launch_bounds__(256, 2) k_spread(const int4* __restrict__ lo4,
     const int nc = min(SP_CHUNK, ncand - c0);
     __syncthreads();
     {
-      const int s = threadIdx.x >> 2, part = threadIdx.x & 3;
-      if (s < nc) {
+      // staging roles are warp-uniform (no intra-warp divergence): warps 0-1 x windows,
+      // 2-3 y windows, 4-5 z windows + warp masks, 6-7 channel weights; 2 sources per thread
+      const int role = warp >> 1;
+      for (int s = (warp & 1) * 32 + lane; s < nc; s += 64) {  // nc <= SP_CHUNK
         const int v = c0 + s;
         int r = 0;
         while (r + 1 < nrun && run_pre[r + 1] <= v) ++r;
         const int row = run_beg[r] + (v - run_pre[r]);
-        const int4 l = lo4[row];
-        if (part == 0) {
+        if (role == 0) {
           const double4 e = wxy[row];
-          window_slice<SP_TX>(x0, l.x, P, e.x, e.y, s_e3, s_wx[s]);
-        } else if (part == 1) {
+          window_slice<SP_TX>(x0, lo4[row].x, P, e.x, e.y, s_e3, s_wx[s]);
+        } else if (role == 1) {
           const double4 e = wxy[row];
-          window_slice<SP_TY>(y0, l.y, P, e.z, e.w, s_e3, s_wy[s]);
-        } else if (part == 2) {
+          window_slice<SP_TY>(y0, lo4[row].y, P, e.z, e.w, s_e3, s_wy[s]);
+        } else if (role == 2) {
+          const int4 l = lo4[row];
           const double2 e = wzp[row];
           window_slice<SP_TZ>(z0, l.z, P, e.x, e.y, s_e3, s_wz[s]);
           // which warps' 4x8 (x,y) patches does the support reach? (z overlap is CTA-wide)
