@@ -232,10 +232,10 @@ __device__ __noinline__ void scale_nyquist(double2* col, int cstride, int kx, in
   for (int o = 0; o < NOUT; ++o) col[o * cstride] = make_double2(out[o].re, -out[o].im);
 }
 
-constexpr int XF_THREADS = 512;
+constexpr int XF_THREADS = 256;  // 2 CTAs per SM: one CTA's loads overlap the other's FFTs
 
 template <int KIND, bool HALF, int KB, class FFT>
-__global__ void __launch_bounds__(XF_THREADS, 1) k_xfused(const XArgs a) {
+__global__ void __launch_bounds__(XF_THREADS, 2) k_xfused(const XArgs a) {
   constexpr int NIN = KChan<KIND, HALF>::NIN, NOUT = KChan<KIND, HALF>::NOUT;
   constexpr int NL = NIN > NOUT ? NIN : NOUT;
   extern __shared__ double2 smem[];
@@ -360,9 +360,9 @@ static hs_status launch_xfused_half(hs_ctx* ctx, const XArgs& a) {
 
 hs_status launch_xfused(hs_ctx* ctx, int kind, int half, const XArgs& a) {
   if (half) {
-    if (kind == HS_STOKESLET) return launch_xfused_half<HS_STOKESLET, 2>(ctx, a);
+    if (kind == HS_STOKESLET) return launch_xfused_half<HS_STOKESLET, 1>(ctx, a);
     if (kind == HS_STRESSLET) return launch_xfused_half<HS_STRESSLET, 1>(ctx, a);
-    return launch_xfused_half<HS_ROTLET, 2>(ctx, a);
+    return launch_xfused_half<HS_ROTLET, 1>(ctx, a);
   }
   if (kind == HS_STOKESLET) return launch_xfused_t<HS_STOKESLET, false, 2, AnyFFT>(ctx, a);
   if (kind == HS_STRESSLET) return launch_xfused_t<HS_STRESSLET, false, 2, AnyFFT>(ctx, a);

@@ -380,6 +380,7 @@ hs_status launch_gather(hs_ctx* ctx, const double4* pts, const int* perm, int n,
 // r(n+1) = r(n) q (q = e^{-2 alpha h^2}) started at each lane's first support node.
 constexpr int GA_T = 256;                 // targets (threads) per CTA
 constexpr int GA_SMEM_DOUBLES = 9216;     // 72 KB plane slab
+constexpr int GA_ZM = 32;                 // register z-window length (fast path)
 
 template <int NCH, int PITCH>
 __global__ void __launch_bounds__(GA_T, 2) k_gather3(const double4* __restrict__ pts, const int* __restrict__ orig,
@@ -440,6 +441,23 @@ __global__ void __launch_bounds__(GA_T, 2) k_gather3(const double4* __restrict__
         r0[k] = exp(g.alpha * (2.0 * d * g.h - g.h * g.h));
       }
       w0[2] *= g.pref;
+      // per-lane z window over this warp's z range, zero outside the lane's support
+      const int nzw = W1[2] - W0[2];
+      const bool zfast = nzw <= GA_ZM;
+      double wzv[GA_ZM];
+      {
+        double wz = w0[2], rz = r0[2];
+#pragma unroll
+        for (int i = 0; i < GA_ZM; ++i) {
+          const int z = W0[2] + i;
+          const bool inz = z >= lo[2] && z < lo[2] + P;
+          wzv[i] = inz ? wz : 0.0;
+          if (inz) {
+            wz *= rz;
+            rz *= q;
+          }
+        }
+      }
       const int nzu = Z1 - Z0;
       const int rowlen = nzu * PITCH;                       // doubles per staged row
       const int ychunk = max(1, min(Y1 - Y0, GA_SMEM_DOUBLES / rowlen));
@@ -484,8 +502,32 @@ __global__ void __launch_bounds__(GA_T, 2) k_gather3(const double4* __restrict__
             }
             const double cxy = wxe * wye;
             if (!__any_sync(0xffffffffu, cxy != 0.0)) continue;
-            double wz = w0[2] * cxy, rz = r0[2];
             const double* row = slab + (y - yc) * rowlen;
+            if (zfast) {
+              // fast path: per-lane z window in registers, 6 FMAs + broadcast loads per node
+              double S[NCH];
+#pragma unroll
+              for (int c = 0; c < NCH; ++c) S[c] = 0.0;
+              const double* pz0 = row + (W0[2] - Z0) * PITCH;
+#pragma unroll
+              for (int i = 0; i < GA_ZM; ++i) {
+                if (i < nzw) {
+                  double v[PITCH];
+#pragma unroll
+                  for (int c = 0; c < PITCH; c += 2) {
+                    const double2 vv = *reinterpret_cast<const double2*>(pz0 + i * PITCH + c);
+                    v[c] = vv.x;
+                    v[c + 1] = vv.y;
+                  }
+#pragma unroll
+                  for (int c = 0; c < NCH; ++c) S[c] = fma(wzv[i], v[c], S[c]);
+                }
+              }
+#pragma unroll
+              for (int c = 0; c < NCH; ++c) acc[c] = fma(cxy, S[c], acc[c]);
+              continue;
+            }
+            double wz = w0[2] * cxy, rz = r0[2];
             for (int z = W0[2]; z < W1[2]; ++z) {
               const bool inz = z >= lo[2] && z < lo[2] + P;
               const double we = inz ? wz : 0.0;

@@ -214,6 +214,7 @@ __global__ void __launch_bounds__(PC_TG, 5) k_pair_q(const PairArgs a) {
     const bool tvalid = t < t1;
     const double4 T = a.TP[tvalid ? t : t0];
     const long long tcol = tvalid ? (long long)T.w : -2;  // -2 never matches a source id
+    const int tcol_i = (int)tcol;
     // FP32 view relative to the item's first target, and this warp's target bounding box
     const double4 R0 = a.TP[t0];
     const float tfx = (float)(T.x - R0.x), tfy = (float)(T.y - R0.y), tfz = (float)(T.z - R0.z);
@@ -241,7 +242,7 @@ __global__ void __launch_bounds__(PC_TG, 5) k_pair_q(const PairArgs a) {
       const double4 B = kNeedB ? sB[jj] : make_double4(0, 0, 0, 0);
       const double e0 = T.x - S.x, e1 = T.y - S.y, e2 = T.z - S.z;
       const double rr = exact_r2(e0, e1, e2);
-      const bool img = HALF && ((long long)S.w >= a.n_real);
+      const bool img = HALF && (__float_as_int(sF[jj].w) >= a.n_real);
       if (img) ++n_img;
       eval_pair<KIND, true>(pc, e0, e1, e2, rr, T.z, S, A, B, img, &acc[0], &acc[3], s_erfcx);
     };
@@ -256,7 +257,9 @@ __global__ void __launch_bounds__(PC_TG, 5) k_pair_q(const PairArgs a) {
           const int row = run_beg[r] + (v - run_pre[r]);
           const double4 S = a.P[row];
           sP[j] = S;
-          sF[j] = make_float4((float)(S.x - R0.x), (float)(S.y - R0.y), (float)(S.z - R0.z), 0.0f);
+          // .w carries the combined source index as int bits (no per-pair FP64->int conversions)
+          sF[j] = make_float4((float)(S.x - R0.x), (float)(S.y - R0.y), (float)(S.z - R0.z),
+                              __int_as_float((int)S.w));
           sA[j] = a.A[row];
           if (kNeedB) sB[j] = a.B[row];
         }
@@ -288,7 +291,7 @@ __global__ void __launch_bounds__(PC_TG, 5) k_pair_q(const PairArgs a) {
             const double4 S = sP[j];
             const double d0 = __dsub_rn(T.x, S.x), d1 = __dsub_rn(T.y, S.y), d2 = __dsub_rn(T.z, S.z);
             const double r2 = exact_r2(d0, d1, d2);
-            if (r2 <= a.rc2 && (long long)S.w != tcol && tvalid) {
+            if (r2 <= a.rc2 && __float_as_int(F.w) != tcol_i && tvalid) {
               if (r2 == 0.0) {
                 singular = true;
               } else {
