@@ -24,13 +24,13 @@ namespace hs {
 
 __global__ void k_grid_keys(const double* __restrict__ pos, int n_src, int n, int mode, GridGeom g, int nbx,
                             int nby, int nbz, int* __restrict__ keys, unsigned* __restrict__ flags) {
-  const bool fine = (mode & 8) != 0;  // gather targets: sub-bins of 4x4x4 cells inside each tile
+  const bool fine = (mode & 8) != 0;  // gather targets: (8x8 column, z cell) order
   mode &= 7;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const int s = (mode == 1 && i >= n_src) ? i - n_src : i;
     const bool mir = (mode == 2) || (mode == 1 && i >= n_src);
     const double pc[3] = {pos[3 * s], pos[3 * s + 1], mir ? -pos[3 * s + 2] : pos[3 * s + 2]};
-    int b[3], sub[3];
+    int b[3], cc[3];
     const int tsz[3] = {SP_TX, SP_TY, SP_TZ};
     const int nb[3] = {nbx, nby, nbz};
     bool bad = false;
@@ -42,11 +42,17 @@ __global__ void k_grid_keys(const double* __restrict__ pos, int n_src, int n, in
       c = c < 0 ? 0 : (c >= g.dims[k] ? g.dims[k] - 1 : c);
       int bb = (int)(c / tsz[k]);
       b[k] = bb >= nb[k] ? nb[k] - 1 : bb;
-      sub[k] = (int)(c - (int64_t)b[k] * tsz[k]) / 4;
+      cc[k] = (int)c;
     }
     if (bad) atomicOr(flags, FLAG_OUT_OF_GRID);
-    const int key = (b[0] * nby + b[1]) * nbz + b[2];
-    keys[i] = fine ? key * SP_NSUB + (sub[0] * (SP_TY / 4) + sub[1]) * (SP_TZ / 4) + sub[2] : key;
+    if (fine) {
+      // warps of 32 consecutive targets then share one 8x8 (x,y) column and a few z cells:
+      // a narrow z range (register z-window in the gather) and an (8+P-1)^2 column union
+      const int n8y = (g.dims[1] + 7) / 8;
+      keys[i] = ((cc[0] >> 3) * n8y + (cc[1] >> 3)) * g.dims[2] + cc[2];
+    } else {
+      keys[i] = (b[0] * nby + b[1]) * nbz + b[2];
+    }
   }
 }
 

@@ -36,7 +36,8 @@ struct GridGeom {
   int64_t ch_stride;       // element stride between channels
 };
 constexpr int SP_TX = 16, SP_TY = 16, SP_TZ = 8;  // spread tile / bin shape
-constexpr int SP_NSUB = (SP_TX / 4) * (SP_TY / 4) * (SP_TZ / 4);  // 4x4x4 sub-bins per tile (gather order)
+// gather target order: (8x8 (x,y) column, z cell) of the window-centre cell
+inline int gather_keys(const GridGeom& g) { return ((g.dims[0] + 7) / 8) * ((g.dims[1] + 7) / 8) * g.dims[2]; }
 inline int sp_nbins(const GridGeom& g, int k) {
   const int t[3] = {SP_TX, SP_TY, SP_TZ};
   return (int)ceil_div(g.dims[k], t[k]);

@@ -360,7 +360,7 @@ extern "C" hs_status hs_plan_create(hs_ctx* ctx, const hs_params* prm, hs_plan**
 
   // ---- buffers
   const int maxn = std::max(p->n_comb, std::max(nt, n));
-  const int maxb = std::max(ncell * kTargetSub, nb * SP_NSUB);
+  const int maxb = std::max(std::max(ncell * kTargetSub, nb), gather_keys(g));
 #define A_(cnt, ptr, ...) if ((st = palloc(p, (size_t)(cnt), &(ptr), ##__VA_ARGS__)) != HS_OK) return bail(st)
   A_(3 * (size_t)n, p->d_pos);
   A_(3 * (size_t)n, p->d_sa);
@@ -386,7 +386,7 @@ extern "C" hs_status hs_plan_create(hs_ctx* ctx, const hs_params* prm, hs_plan**
   A_(n, p->bc_order);
   A_(nb + 1, p->bc_start);
   A_(std::max(nt, 1), p->bt_order);
-  A_((size_t)nb * SP_NSUB + 1, p->bt_start);
+  A_((size_t)gather_keys(g) + 1, p->bt_start);
   A_(p->n_comb, p->SPk);
   A_((size_t)p->n_comb * p->nk, p->SWk);
   if (p->nc) {
@@ -616,7 +616,7 @@ hs_status sort_points_by_bin(hs_plan* p, const double* pos, int n_src, int n_tot
                              int* start) {
   hs_ctx* ctx = p->ctx;
   HS_TRY(launch_grid_keys(ctx, pos, n_src, n_total, mode, p->gg, p->keys));
-  const int nb = (mode & 8) ? p->nbins * SP_NSUB : p->nbins;
+  const int nb = (mode & 8) ? gather_keys(p->gg) : p->nbins;
   return counting_sort(ctx, p->keys, n_total, nb, order, start, p->work);
 }
 
