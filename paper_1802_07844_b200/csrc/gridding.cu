@@ -517,17 +517,16 @@ __global__ void __launch_bounds__(GA_T, 2) k_gather3(const double4* __restrict__
               const double* pz0 = row + (W0[2] - Z0) * PITCH;
 #pragma unroll
               for (int i = 0; i < GA_ZM; ++i) {
-                if (i < nzw) {
-                  double v[PITCH];
+                const int ii = min(i, nzw - 1);
+                double v[PITCH];
 #pragma unroll
-                  for (int c = 0; c < PITCH; c += 2) {
-                    const double2 vv = *reinterpret_cast<const double2*>(pz0 + i * PITCH + c);
-                    v[c] = vv.x;
-                    v[c + 1] = vv.y;
-                  }
-#pragma unroll
-                  for (int c = 0; c < NCH; ++c) S[c] = fma(wzv[i], v[c], S[c]);
+                for (int c = 0; c < PITCH; c += 2) {
+                  const double2 vv = *reinterpret_cast<const double2*>(pz0 + ii * PITCH + c);
+                  v[c] = vv.x;
+                  v[c + 1] = vv.y;
                 }
+#pragma unroll
+                for (int c = 0; c < NCH; ++c) S[c] = fma(wzv[i], v[c], S[c]);
               }
 #pragma unroll
               for (int c = 0; c < NCH; ++c) acc[c] = fma(cxy, S[c], acc[c]);
@@ -576,142 +575,6 @@ __global__ void __launch_bounds__(GA_T, 2) k_gather3(const double4* __restrict__
   }
 }
 
-// Barrier-free variant: no shared-memory staging; every grid node is one broadcast
-// 128-bit read per channel pair straight from L1/L2, with the z-loop fully unrolled
-// (<= 3*GA_ZM independent loads in flight per warp hide the L2 latency).
-template <int NCH, int PITCH>
-__global__ void __launch_bounds__(256, 2) k_gather4(const double4* __restrict__ pts, const int* __restrict__ orig,
-                                                   int n, GridGeom g, const double* __restrict__ T,
-                                                   double* __restrict__ u_four, double* __restrict__ u_tot,
-                                                   const double* __restrict__ u_real, unsigned* __restrict__ flags) {
-  const int lane = threadIdx.x & 31;
-  const int nwarps = gridDim.x * (blockDim.x >> 5);
-  const int P = g.P;
-  const double q = exp(-2.0 * g.alpha * g.h * g.h);
-  for (int wbase = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; wbase < n; wbase += nwarps * 32) {
-    const int t = wbase + lane;
-    const bool valid = t < n;
-    const double4 pt = pts[valid ? t : wbase];
-    const double pc[3] = {pt.x, pt.y, pt.z};
-    int lo[3];
-    bool bad = false;
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      const int64_t l = window_lo(pc[k], g.origin[k], g.h, P);
-      bad |= (l < 0) || (l + P > g.dims[k]);
-      lo[k] = (int)l;
-    }
-    if (valid && bad) atomicOr(flags, FLAG_OUT_OF_GRID);
-    const bool act = valid && !bad;
-    int W0[3], W1[3];
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      W0[k] = (int)__reduce_min_sync(0xffffffffu, (unsigned)(act ? lo[k] : 0x7fffffff));
-      W1[k] = (int)__reduce_max_sync(0xffffffffu, (unsigned)(act ? lo[k] + P : 0));
-    }
-    double acc[NCH];
-#pragma unroll
-    for (int c = 0; c < NCH; ++c) acc[c] = 0.0;
-    if (W1[0] > W0[0]) {
-      double w0[3], r0[3];
-#pragma unroll
-      for (int k = 0; k < 3; ++k) {
-        const double d = window_d(pc[k], g.origin[k], g.h, lo[k]);
-        w0[k] = act ? exp(-g.alpha * d * d) : 0.0;
-        r0[k] = exp(g.alpha * (2.0 * d * g.h - g.h * g.h));
-      }
-      w0[2] *= g.pref;
-      const int nzw = W1[2] - W0[2];
-      const bool zfast = nzw <= GA_ZM;
-      double wzv[GA_ZM];
-      {
-        double wz = w0[2], rz = r0[2];
-#pragma unroll
-        for (int i = 0; i < GA_ZM; ++i) {
-          const int z = W0[2] + i;
-          const bool inz = z >= lo[2] && z < lo[2] + P;
-          wzv[i] = inz ? wz : 0.0;
-          if (inz) {
-            wz *= rz;
-            rz *= q;
-          }
-        }
-      }
-      double wx = w0[0], rx = r0[0];
-      for (int x = W0[0]; x < W1[0]; ++x) {
-        const bool inx = x >= lo[0] && x < lo[0] + P;
-        const double wxe = inx ? wx : 0.0;
-        if (inx) {
-          wx *= rx;
-          rx *= q;
-        }
-        if (!__any_sync(0xffffffffu, wxe != 0.0)) continue;
-        double wy = w0[1], ry = r0[1];
-        for (int y = W0[1]; y < W1[1]; ++y) {
-          const bool iny = y >= lo[1] && y < lo[1] + P;
-          const double wye = iny ? wy : 0.0;
-          if (iny) {
-            wy *= ry;
-            ry *= q;
-          }
-          const double cxy = wxe * wye;
-          if (!__any_sync(0xffffffffu, cxy != 0.0)) continue;
-          const double* col = T + (int64_t)x * g.stride[0] + (int64_t)y * g.stride[1] + (int64_t)W0[2] * PITCH;
-          if (zfast) {
-            double S[NCH];
-#pragma unroll
-            for (int c = 0; c < NCH; ++c) S[c] = 0.0;
-#pragma unroll
-            for (int i = 0; i < GA_ZM; ++i) {
-              if (i < nzw) {
-                double v[PITCH];
-#pragma unroll
-                for (int c = 0; c < PITCH; c += 2) {
-                  const double2 vv = __ldg(reinterpret_cast<const double2*>(col + i * PITCH + c));
-                  v[c] = vv.x;
-                  v[c + 1] = vv.y;
-                }
-#pragma unroll
-                for (int c = 0; c < NCH; ++c) S[c] = fma(wzv[i], v[c], S[c]);
-              }
-            }
-#pragma unroll
-            for (int c = 0; c < NCH; ++c) acc[c] = fma(cxy, S[c], acc[c]);
-          } else {
-            double wz = w0[2] * cxy, rz = r0[2];
-            for (int z = W0[2]; z < W1[2]; ++z) {
-              const bool inz = z >= lo[2] && z < lo[2] + P;
-              const double we = inz ? wz : 0.0;
-              if (inz) {
-                wz *= rz;
-                rz *= q;
-              }
-              const double* pz = col + (z - W0[2]) * PITCH;
-#pragma unroll
-              for (int c = 0; c < PITCH; c += 2) {
-                const double2 vv = __ldg(reinterpret_cast<const double2*>(pz + c));
-                if (c < NCH) acc[c] = fma(we, vv.x, acc[c]);
-                if (c + 1 < NCH) acc[c + 1] = fma(we, vv.y, acc[c + 1]);
-              }
-            }
-          }
-        }
-      }
-    }
-    if (act) {
-      const int o = orig[t];
-      const double h3 = g.h * g.h * g.h;
-#pragma unroll
-      for (int k = 0; k < 3; ++k) {
-        double v = acc[k] * h3;
-        if (NCH == 6) v -= pt.z * (acc[3 + k] * h3);
-        if (u_four) u_four[3 * (size_t)o + k] = v;
-        if (u_tot) u_tot[3 * (size_t)o + k] = (u_real ? u_real[3 * (size_t)o + k] : 0.0) + v;
-      }
-    }
-  }
-}
-
 hs_status launch_gather_fourier(hs_ctx* ctx, const double4* pts, const int* orig, int n, int half, const GridGeom& g,
                                 const double* T, double* u_fourier, double* u_total, const double* u_real) {
   if (n == 0) return HS_OK;
@@ -724,16 +587,6 @@ hs_status launch_gather_fourier(hs_ctx* ctx, const double4* pts, const int* orig
     else
       k_gather<3, 1><<<gs1, 256, 0, ctx->stream>>>(pts, orig, n, g, T, u_fourier, 3, 1.0, u_total, u_real,
                                                    ctx->d_flags);
-    HS_LAUNCHED(ctx);
-    return HS_OK;
-  }
-  static const bool v3 = getenv("HS_GATHER_V3") != nullptr;  // smem-staged variant (comparison)
-  if (!v3) {
-    const int gs4 = (int)std::min<int64_t>(ceil_div(n, 256), (int64_t)ctx->sm_count * 32);
-    if (half)
-      k_gather4<6, 6><<<gs4, 256, 0, ctx->stream>>>(pts, orig, n, g, T, u_fourier, u_total, u_real, ctx->d_flags);
-    else
-      k_gather4<3, 4><<<gs4, 256, 0, ctx->stream>>>(pts, orig, n, g, T, u_fourier, u_total, u_real, ctx->d_flags);
     HS_LAUNCHED(ctx);
     return HS_OK;
   }
