@@ -155,7 +155,8 @@ __device__ __forceinline__ double exact_r2(double d0, double d1, double d2) {
 // its own target (no cross-lane reductions, no atomics, deterministic order).
 constexpr int PC_WARPS = 4;
 constexpr int PC_TG = PC_WARPS * 32;  // targets per work item
-constexpr int PC_K = 256;             // candidates per staged chunk
+constexpr int PC_K = 256;             // staged candidates (two halves of PC_H)
+constexpr int PC_H = PC_K / 2;        // candidates per chunk
 constexpr int PC_Q = 64;              // per-lane queue capacity
 
 template <int KIND, bool HALF>
@@ -232,7 +233,6 @@ __global__ void __launch_bounds__(PC_TG, 5) k_pair_q(const PairArgs a) {
       }
     }
     double acc[6] = {0, 0, 0, 0, 0, 0};
-    int qlen = 0;
     bool singular = false;
     unsigned long long n_acc = 0, n_img = 0;
 
@@ -247,25 +247,55 @@ __global__ void __launch_bounds__(PC_TG, 5) k_pair_q(const PairArgs a) {
       eval_pair<KIND, true>(pc, e0, e1, e2, rr, T.z, S, A, B, img, &acc[0], &acc[3], s_erfcx);
     };
 
-    for (int c0 = 0; c0 < ncand; c0 += PC_K) {
+    // Two-half ring of staged candidates + per-lane FIFO queues: entries of chunk c may be
+    // evaluated while chunk c+1 is scanned, so queues never have to be drained at every
+    // chunk boundary (only the leftovers of chunk c-2 before its half is restaged).
+    int head = 0, tail = 0;
+    // stride coprime with ncand (a few primes larger than any realistic candidate count)
+    int pstride = 1;
+    {
+      const int primes[4] = {1000003, 999983, 1000033, 1000037};
+      for (int k = 0; k < 4; ++k)
+        if (ncand % primes[k] != 0) {
+          pstride = primes[k] % max(ncand, 1);
+          if (pstride == 0) pstride = 1;
+          break;
+        }
+    }
+    auto pop_eval = [&]() {
+      const int jj = q[head & (PC_Q - 1)][lane];
+      ++head;
+      ++n_acc;
+      eval_one(jj);
+    };
+    for (int c = 0, c0 = 0; c0 < ncand; ++c, c0 += PC_H) {
+      const int h = c & 1, hb = h * PC_H;
+      // drain the (oldest) entries that still reference half h
+      while (__any_sync(0xffffffffu, tail > head && (q[head & (PC_Q - 1)][lane] >> 7) == h)) {
+        if (tail > head && (q[head & (PC_Q - 1)][lane] >> 7) == h) pop_eval();
+      }
       __syncthreads();
-      for (int j = threadIdx.x; j < PC_K; j += PC_TG) {
-        const int v = c0 + j;
-        if (v < ncand) {
+      for (int j = threadIdx.x; j < PC_H; j += PC_TG) {
+        const int v0 = c0 + j;
+        if (v0 < ncand) {
+          // stride permutation of the candidate list: every chunk samples the whole
+          // neighbourhood, so each lane's acceptance rate per chunk is about its average
+          // and the full-round evaluation below keeps all lanes busy
+          const int v = (int)(((long long)v0 * pstride) % ncand);
           int r = 0;
           while (r + 1 < nrun && run_pre[r + 1] <= v) ++r;
           const int row = run_beg[r] + (v - run_pre[r]);
           const double4 S = a.P[row];
-          sP[j] = S;
+          sP[hb + j] = S;
           // .w carries the combined source index as int bits (no per-pair FP64->int conversions)
-          sF[j] = make_float4((float)(S.x - R0.x), (float)(S.y - R0.y), (float)(S.z - R0.z),
-                              __int_as_float((int)S.w));
-          sA[j] = a.A[row];
-          if (kNeedB) sB[j] = a.B[row];
+          sF[hb + j] = make_float4((float)(S.x - R0.x), (float)(S.y - R0.y), (float)(S.z - R0.z),
+                                   __int_as_float((int)S.w));
+          sA[hb + j] = a.A[row];
+          if (kNeedB) sB[hb + j] = a.B[row];
         }
       }
       __syncthreads();
-      const int nc = min(PC_K, ncand - c0);
+      const int nc = min(PC_H, ncand - c0);
       for (int j0 = 0; j0 < nc; j0 += 32) {
         // warp-level culling: candidates farther than rc (+margin) from the warp's target box
         unsigned near;
@@ -273,7 +303,7 @@ __global__ void __launch_bounds__(PC_TG, 5) k_pair_q(const PairArgs a) {
           const int j = j0 + lane;
           bool keep = false;
           if (j < nc) {
-            const float4 F = sF[j];
+            const float4 F = sF[hb + j];
             const float dx = fmaxf(fmaxf(bmin[0] - F.x, F.x - bmax[0]), 0.0f);
             const float dy = fmaxf(fmaxf(bmin[1] - F.y, F.y - bmax[1]), 0.0f);
             const float dz = fmaxf(fmaxf(bmin[2] - F.z, F.z - bmax[2]), 0.0f);
@@ -282,7 +312,7 @@ __global__ void __launch_bounds__(PC_TG, 5) k_pair_q(const PairArgs a) {
           near = __ballot_sync(0xffffffffu, keep);
         }
         while (near) {
-          const int j = j0 + __ffs(near) - 1;
+          const int j = hb + j0 + __ffs(near) - 1;
           near &= near - 1;
           const float4 F = sF[j];  // broadcast
           const float fx = tfx - F.x, fy = tfy - F.y, fz = tfz - F.z;
@@ -295,32 +325,24 @@ __global__ void __launch_bounds__(PC_TG, 5) k_pair_q(const PairArgs a) {
               if (r2 == 0.0) {
                 singular = true;
               } else {
-                q[qlen][lane] = (unsigned short)j;
-                ++qlen;
+                q[tail & (PC_Q - 1)][lane] = (unsigned short)j;
+                ++tail;
               }
             }
           }
         }
-        // evaluate while most lanes have queued work (or a queue is close to full)
-        while (true) {
-          const unsigned busy = __ballot_sync(0xffffffffu, qlen > 0);
-          const unsigned mx = __reduce_max_sync(0xffffffffu, (unsigned)qlen);
-          if (__popc(busy) < 24 && mx <= PC_Q - 32) break;
-          if (qlen > 0) {
-            --qlen;
-            ++n_acc;
-            eval_one(q[qlen][lane]);
-          }
+        // full rounds while every valid lane has work; partial rounds only against overflow
+        unsigned mn = __reduce_min_sync(0xffffffffu, (unsigned)(tvalid ? tail - head : 0x7fffffff));
+        if (mn == 0x7fffffffu) mn = 0;
+        if (tvalid)
+          for (unsigned r = 0; r < mn; ++r) pop_eval();
+        while ((int)__reduce_max_sync(0xffffffffu, (unsigned)(tail - head)) > PC_Q - 32) {
+          if (tail > head) pop_eval();
         }
       }
-      // drain before the chunk is overwritten
-      while (__any_sync(0xffffffffu, qlen > 0)) {
-        if (qlen > 0) {
-          --qlen;
-          ++n_acc;
-          eval_one(q[qlen][lane]);
-        }
-      }
+    }
+    while (__any_sync(0xffffffffu, tail > head)) {
+      if (tail > head) pop_eval();
     }
     if (singular) atomicOr(a.flags, FLAG_SINGULAR);
     if (a.counts) {
