@@ -106,23 +106,27 @@ __global__ void k_spread_windows(const double4* __restrict__ pts, int n, GridGeo
 template <int L>
 __device__ __forceinline__ void window_slice(int node0, int lo, int P, double e1, double e2, const double* e3,
                                              double* out) {
-  int a = node0 - lo;
-  // e2^max(a,0) by binary exponentiation
+#pragma unroll
+  for (int i = 0; i < L; ++i) out[i] = 0.0;
+  const int i0 = max(0, lo - node0);   // first slice index inside the support
+  const int a0 = node0 + i0 - lo;      // its support offset (>= 0)
+  if (i0 >= L || a0 >= P) return;
+  // e2^a0 by binary exponentiation, then 4 independent chains with step e2^4
   double pw = 1.0, b = e2;
-  int m = a > 0 ? a : 0;
-  while (m) {
+  for (int m = a0; m; m >>= 1) {
     if (m & 1) pw *= b;
     b *= b;
-    m >>= 1;
   }
+  const double e22 = e2 * e2, e24 = e22 * e22;
+  double p[4] = {e1 * pw, e1 * pw * e2, e1 * pw * e22, e1 * pw * e22 * e2};
 #pragma unroll
-  for (int i = 0; i < L; ++i, ++a) {
-    double v = 0.0;
-    if (a >= 0 && a < P) {
-      v = e1 * pw * e3[a];
-      pw *= e2;
+  for (int j = 0; j < (L + 3) / 4; ++j) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int i = i0 + 4 * j + k, aa = a0 + 4 * j + k;
+      if (i < L && aa < P) out[i] = p[k] * e3[aa];
+      p[k] *= e24;
     }
-    out[i] = v;
   }
 }
 
@@ -177,28 +181,50 @@ __global__ void __launch_bounds__(256, 2) k_spread(const int4* __restrict__ lo4,
 #pragma unroll
     for (int j = 0; j < SP_TZ; ++j) acc[c][j] = 0.0;
 
-  for (int c0 = 0; c0 < ncand; c0 += SP_CHUNK) {
-    const int nc = min(SP_CHUNK, ncand - c0);
-    __syncthreads();
-    {
-      // staging roles are warp-uniform (no intra-warp divergence): warps 0-1 x windows,
-      // 2-3 y windows, 4-5 z windows + warp masks, 6-7 channel weights; 2 sources per thread
-      const int role = warp >> 1;
-      for (int s = (warp & 1) * 32 + lane; s < nc; s += 64) {  // nc <= SP_CHUNK
-        const int v = c0 + s;
+  // staging roles are warp-uniform (no intra-warp divergence): warps 0-1 x windows,
+  // 2-3 y windows, 4-5 z windows + warp masks, 6-7 channel weights; 2 sources per thread.
+  // The global records of chunk c+1 are loaded into registers while chunk c is computed.
+  const int role = warp >> 1;
+  int4 pl[2];
+  double4 pe[2];
+  double pq[2][NCH];
+  auto prefetch = [&](int cbase) {
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const int sidx = (warp & 1) * 32 + lane + 64 * k;
+      const int v = cbase + sidx;
+      if (sidx < SP_CHUNK && v < ncand) {
         int r = 0;
         while (r + 1 < nrun && run_pre[r + 1] <= v) ++r;
         const int row = run_beg[r] + (v - run_pre[r]);
-        if (role == 0) {
-          const double4 e = wxy[row];
-          window_slice<SP_TX>(x0, lo4[row].x, P, e.x, e.y, s_e3, s_wx[s]);
-        } else if (role == 1) {
-          const double4 e = wxy[row];
-          window_slice<SP_TY>(y0, lo4[row].y, P, e.z, e.w, s_e3, s_wy[s]);
-        } else if (role == 2) {
-          const int4 l = lo4[row];
+        if (role <= 2) pl[k] = lo4[row];
+        if (role <= 1) pe[k] = wxy[row];
+        if (role == 2) {
           const double2 e = wzp[row];
-          window_slice<SP_TZ>(z0, l.z, P, e.x, e.y, s_e3, s_wz[s]);
+          pe[k] = make_double4(e.x, e.y, 0.0, 0.0);
+        }
+        if (role == 3) {
+#pragma unroll
+          for (int c = 0; c < NCH; ++c) pq[k][c] = w[(size_t)row * ldw + c];
+        }
+      }
+    }
+  };
+  if (ncand > 0) prefetch(0);
+  for (int c0 = 0; c0 < ncand; c0 += SP_CHUNK) {
+    const int nc = min(SP_CHUNK, ncand - c0);
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const int s = (warp & 1) * 32 + lane + 64 * k;
+      if (s < nc) {
+        const int4 l = pl[k];
+        if (role == 0) {
+          window_slice<SP_TX>(x0, l.x, P, pe[k].x, pe[k].y, s_e3, s_wx[s]);
+        } else if (role == 1) {
+          window_slice<SP_TY>(y0, l.y, P, pe[k].z, pe[k].w, s_e3, s_wy[s]);
+        } else if (role == 2) {
+          window_slice<SP_TZ>(z0, l.z, P, pe[k].x, pe[k].y, s_e3, s_wz[s]);
           // which warps' 4x8 (x,y) patches does the support reach? (z overlap is CTA-wide)
           unsigned m = 0;
           if (l.z < z0 + SP_TZ && l.z + P > z0) {
@@ -211,11 +237,12 @@ __global__ void __launch_bounds__(256, 2) k_spread(const int4* __restrict__ lo4,
           s_mask[s] = m;
         } else {
 #pragma unroll
-          for (int c = 0; c < NCH; ++c) s_q[s][c] = w[(size_t)row * ldw + c];
+          for (int c = 0; c < NCH; ++c) s_q[s][c] = pq[k][c];
         }
       }
     }
     __syncthreads();
+    if (c0 + SP_CHUNK < ncand) prefetch(c0 + SP_CHUNK);
     for (int base = 0; base < nc; base += 32) {
       unsigned m = __ballot_sync(0xffffffffu, base + lane < nc && ((s_mask[base + lane] >> warp) & 1u));
       while (m) {
@@ -235,6 +262,123 @@ __global__ void __launch_bounds__(256, 2) k_spread(const int4* __restrict__ lo4,
     }
   }
   const int x = x0 + xo, y = y0 + yo;
+  if (x < g.dims[0] && y < g.dims[1]) {
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) {
+      double* dst = grids + c * g.ch_stride + x * g.stride[0] + y * g.stride[1];
+#pragma unroll
+      for (int j = 0; j < SP_TZ; ++j) {
+        const int z = z0 + j;
+        if (z < g.dims[2]) dst[z * g.stride[2]] = acc[c][j];
+      }
+    }
+  }
+}
+
+// Warp-independent variant (no CTA barriers): every warp streams the tile's candidate
+// list itself, 32 sources at a time (lane = source), keeps the sources whose support
+// reaches its own 4x8 (x,y) patch and the tile's z-range (ballot), builds their window
+// slices for ITS 4 x-nodes, 8 y-nodes and 8 z-nodes in warp-private shared memory and
+// accumulates them.  The z-slices are recomputed per warp (cheap: a few multiplies per
+// node); in exchange no warp ever waits for another.
+constexpr int SW_STRIDE = 4 + 8 + 8 + 1;  // wx[4] wy[8] wz[8] + pad (odd stride: conflict-free)
+
+template <int NCH>
+__global__ void __launch_bounds__(256, 2) k_spread2(const int4* __restrict__ lo4, const double4* __restrict__ wxy,
+                                                   const double2* __restrict__ wzp, const double* __restrict__ w,
+                                                   int ldw, const int* __restrict__ bin_start, GridGeom g,
+                                                   WinConst wc, int nbx, int nby, int nbz,
+                                                   double* __restrict__ grids) {
+  extern __shared__ double sw_dyn[];  // [8 warps][32 * SW_STRIDE] windows, then [8][32 * (NCH|1)] weights
+  __shared__ double s_e3[SP_MAXP];
+  __shared__ int run_beg[9], run_pre[10];
+  __shared__ int s_nrun;
+
+  const int tz = blockIdx.x % nbz;
+  const int ty = (blockIdx.x / nbz) % nby;
+  const int tx = blockIdx.x / (nbz * nby);
+  const int x0 = tx * SP_TX, y0 = ty * SP_TY, z0 = tz * SP_TZ;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int px0 = x0 + (warp & 3) * 4, py0 = y0 + (warp >> 2) * 8;  // this warp's patch
+  const int xi = lane & 3, yi = lane >> 2;
+  const int P = g.P;
+  constexpr int QS = NCH | 1;
+  double* win = sw_dyn + warp * 32 * SW_STRIDE;
+  double* qw = sw_dyn + 8 * 32 * SW_STRIDE + warp * 32 * QS;
+
+  for (int i = threadIdx.x; i < P; i += blockDim.x) s_e3[i] = wc.e3[i];
+  if (threadIdx.x == 0) {
+    int nr = 0, tot = 0;
+    const int zlo = max(tz - 2, 0), zhi = min(tz + 2, nbz - 1);
+    for (int bx = max(tx - 1, 0); bx <= min(tx + 1, nbx - 1); ++bx)
+      for (int by = max(ty - 1, 0); by <= min(ty + 1, nby - 1); ++by) {
+        const int f = (bx * nby + by) * nbz;
+        const int b = bin_start[f + zlo], e = bin_start[f + zhi + 1];
+        if (e > b) {
+          run_beg[nr] = b;
+          run_pre[nr] = tot;
+          tot += e - b;
+          ++nr;
+        }
+      }
+    run_pre[nr] = tot;
+    s_nrun = nr;
+  }
+  __syncthreads();
+  const int nrun = s_nrun, ncand = run_pre[nrun];
+
+  double acc[NCH][SP_TZ];
+#pragma unroll
+  for (int c = 0; c < NCH; ++c)
+#pragma unroll
+    for (int j = 0; j < SP_TZ; ++j) acc[c][j] = 0.0;
+
+  int r = 0;  // current run (candidates are visited in increasing order)
+  for (int c0 = 0; c0 < ncand; c0 += 32) {
+    const int v = c0 + lane;
+    bool hit = false;
+    int4 l = make_int4(0, 0, 0, 0);
+    int row = 0;
+    if (v < ncand) {
+      while (r + 1 < nrun && run_pre[r + 1] <= c0) ++r;
+      int rr = r;
+      while (rr + 1 < nrun && run_pre[rr + 1] <= v) ++rr;
+      row = run_beg[rr] + (v - run_pre[rr]);
+      l = lo4[row];
+      hit = (l.x < px0 + 4) && (l.x + P > px0) && (l.y < py0 + 8) && (l.y + P > py0) && (l.z < z0 + SP_TZ) &&
+            (l.z + P > z0);
+    }
+    unsigned m = __ballot_sync(0xffffffffu, hit);
+    if (!m) continue;
+    if (hit) {
+      const double4 e = wxy[row];
+      const double2 ez = wzp[row];
+      double* ws = win + lane * SW_STRIDE;
+      window_slice<4>(px0, l.x, P, e.x, e.y, s_e3, ws);
+      window_slice<8>(py0, l.y, P, e.z, e.w, s_e3, ws + 4);
+      window_slice<SP_TZ>(z0, l.z, P, ez.x, ez.y, s_e3, ws + 12);
+#pragma unroll
+      for (int c = 0; c < NCH; ++c) qw[lane * QS + c] = w[(size_t)row * ldw + c];
+    }
+    __syncwarp();
+    while (m) {
+      const int sl = __ffs(m) - 1;
+      m &= m - 1;
+      const double* ws = win + sl * SW_STRIDE;
+      const double cxy = ws[xi] * ws[4 + yi];
+      double wz[SP_TZ];
+#pragma unroll
+      for (int j = 0; j < SP_TZ; ++j) wz[j] = ws[12 + j];
+#pragma unroll
+      for (int c = 0; c < NCH; ++c) {
+        const double q = qw[sl * QS + c] * cxy;
+#pragma unroll
+        for (int j = 0; j < SP_TZ; ++j) acc[c][j] = fma(q, wz[j], acc[c][j]);
+      }
+    }
+    __syncwarp();
+  }
+  const int x = px0 + xi, y = py0 + yi;
   if (x < g.dims[0] && y < g.dims[1]) {
 #pragma unroll
     for (int c = 0; c < NCH; ++c) {
@@ -270,10 +414,17 @@ hs_status launch_spread(hs_ctx* ctx, const double4* pts, const double* w, int n,
     const int cn = std::min(SP_MAXCH, nch - c0);
     double* gout = grids + (size_t)c0 * g.ch_stride;
     const double* wc0 = w + c0;
+    static const bool v1 = getenv("HS_SPREAD_V1") != nullptr;  // CTA-staged variant (comparison)
     switch (cn) {
-#define HS_SP(N)                                                                                             \
-  case N:                                                                                                    \
-    k_spread<N><<<grid, block, 0, ctx->stream>>>(lo, wxy, wz, wc0, nch, bin_start, g, wc, nbx, nby, nbz, gout); \
+#define HS_SP(N)                                                                                              \
+  case N:                                                                                                     \
+    if (v1)                                                                                                   \
+      k_spread<N><<<grid, block, 0, ctx->stream>>>(lo, wxy, wz, wc0, nch, bin_start, g, wc, nbx, nby, nbz, gout); \
+    else {                                                                                                    \
+      const size_t sm2 = sizeof(double) * 8 * 32 * (SW_STRIDE + (N | 1));                                     \
+      HS_CUDA(cudaFuncSetAttribute(k_spread2<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2));     \
+      k_spread2<N><<<grid, block, sm2, ctx->stream>>>(lo, wxy, wz, wc0, nch, bin_start, g, wc, nbx, nby, nbz, gout); \
+    }                                                                                                         \
     break;
       HS_SP(1) HS_SP(2) HS_SP(3) HS_SP(4)
 #undef HS_SP
