@@ -275,6 +275,173 @@ __global__ void __launch_bounds__(256, 2) k_spread(const int4* __restrict__ lo4,
   }
 }
 
+// Tensor-core variant: the per-warp accumulation is the small GEMM
+//   C[(x,y) position p][z node n] += sum_s A[p][s] B[s][n],
+//   A[p][s] = q_s wx_s(x_p) wy_s(y_p),  B[s][n] = wz_s(z_n),
+// evaluated with FP64 DMMA (mma.sync m8n8k4; there is no FP64 tcgen05 kind) over groups
+// of 4 hitting sources: the warp's 32 (x,y) positions are 4 row blocks of 8, the tile's
+// 8 z nodes are the 8 columns.  One DMMA replaces 8 warp-wide DFMAs plus their operand
+// traffic; the staging and hit masks are those of k_spread.
+__device__ __forceinline__ void dmma_884(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+template <int NCH>
+__global__ void __launch_bounds__(256, 2) k_spread_mma(const int4* __restrict__ lo4, const double4* __restrict__ wxy,
+                                                      const double2* __restrict__ wzp, const double* __restrict__ w,
+                                                      int ldw, const int* __restrict__ bin_start, GridGeom g,
+                                                      WinConst wc, int nbx, int nby, int nbz,
+                                                      double* __restrict__ grids) {
+  __shared__ double s_wx[SP_CHUNK][SP_TX + 1];
+  __shared__ double s_wy[SP_CHUNK][SP_TY + 1];
+  __shared__ double s_wz[SP_CHUNK][SP_TZ + 1];
+  __shared__ double s_q[SP_CHUNK][NCH | 1];
+  __shared__ unsigned s_mask[SP_CHUNK];
+  __shared__ double s_e3[SP_MAXP];
+  __shared__ int run_beg[9], run_pre[10];
+  __shared__ int s_nrun;
+
+  const int tz = blockIdx.x % nbz;
+  const int ty = (blockIdx.x / nbz) % nby;
+  const int tx = blockIdx.x / (nbz * nby);
+  const int x0 = tx * SP_TX, y0 = ty * SP_TY, z0 = tz * SP_TZ;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int wx0 = (warp & 3) * 4, wy0 = (warp >> 2) * 8;  // warp patch origin inside the tile
+  const int P = g.P;
+  const int kq = lane & 3;   // k index (source slot) of this lane's A and B fragments
+  const int rq = lane >> 2;  // A row / B column / C row of this lane
+
+  for (int i = threadIdx.x; i < P; i += blockDim.x) s_e3[i] = wc.e3[i];
+  if (threadIdx.x == 0) {
+    int nr = 0, tot = 0;
+    const int zlo = max(tz - 2, 0), zhi = min(tz + 2, nbz - 1);
+    for (int bx = max(tx - 1, 0); bx <= min(tx + 1, nbx - 1); ++bx)
+      for (int by = max(ty - 1, 0); by <= min(ty + 1, nby - 1); ++by) {
+        const int f = (bx * nby + by) * nbz;
+        const int b = bin_start[f + zlo], e = bin_start[f + zhi + 1];
+        if (e > b) {
+          run_beg[nr] = b;
+          run_pre[nr] = tot;
+          tot += e - b;
+          ++nr;
+        }
+      }
+    run_pre[nr] = tot;
+    s_nrun = nr;
+  }
+  __syncthreads();
+  const int nrun = s_nrun, ncand = run_pre[nrun];
+
+  double acc[4][NCH][2];
+#pragma unroll
+  for (int rb = 0; rb < 4; ++rb)
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) acc[rb][c][0] = acc[rb][c][1] = 0.0;
+
+  const int role = warp >> 1;
+  int4 pl[2];
+  double4 pe[2];
+  double pq[2][NCH];
+  auto prefetch = [&](int cbase) {
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const int sidx = (warp & 1) * 32 + lane + 64 * k;
+      const int v = cbase + sidx;
+      if (sidx < SP_CHUNK && v < ncand) {
+        int r = 0;
+        while (r + 1 < nrun && run_pre[r + 1] <= v) ++r;
+        const int row = run_beg[r] + (v - run_pre[r]);
+        if (role <= 2) pl[k] = lo4[row];
+        if (role <= 1) pe[k] = wxy[row];
+        if (role == 2) {
+          const double2 e = wzp[row];
+          pe[k] = make_double4(e.x, e.y, 0.0, 0.0);
+        }
+        if (role == 3) {
+#pragma unroll
+          for (int c = 0; c < NCH; ++c) pq[k][c] = w[(size_t)row * ldw + c];
+        }
+      }
+    }
+  };
+  if (ncand > 0) prefetch(0);
+  for (int c0 = 0; c0 < ncand; c0 += SP_CHUNK) {
+    const int nc = min(SP_CHUNK, ncand - c0);
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const int s = (warp & 1) * 32 + lane + 64 * k;
+      if (s < nc) {
+        const int4 l = pl[k];
+        if (role == 0) {
+          window_slice<SP_TX>(x0, l.x, P, pe[k].x, pe[k].y, s_e3, s_wx[s]);
+        } else if (role == 1) {
+          window_slice<SP_TY>(y0, l.y, P, pe[k].z, pe[k].w, s_e3, s_wy[s]);
+        } else if (role == 2) {
+          window_slice<SP_TZ>(z0, l.z, P, pe[k].x, pe[k].y, s_e3, s_wz[s]);
+          unsigned m = 0;
+          if (l.z < z0 + SP_TZ && l.z + P > z0) {
+#pragma unroll
+            for (int wq = 0; wq < 8; ++wq) {
+              const int px = x0 + (wq & 3) * 4, py = y0 + (wq >> 2) * 8;
+              if (l.x < px + 4 && l.x + P > px && l.y < py + 8 && l.y + P > py) m |= 1u << wq;
+            }
+          }
+          s_mask[s] = m;
+        } else {
+#pragma unroll
+          for (int c = 0; c < NCH; ++c) s_q[s][c] = pq[k][c];
+        }
+      }
+    }
+    __syncthreads();
+    if (c0 + SP_CHUNK < ncand) prefetch(c0 + SP_CHUNK);
+    for (int base = 0; base < nc; base += 32) {
+      unsigned m = __ballot_sync(0xffffffffu, base + lane < nc && ((s_mask[base + lane] >> warp) & 1u));
+      while (m) {
+        // next group of up to 4 hitting sources; this lane's slot kq
+        int sk = -1;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int sb = m ? base + __ffs(m) - 1 : -1;
+          if (m) m &= m - 1;
+          if (k == kq) sk = sb;
+        }
+        const double bz = sk >= 0 ? s_wz[sk][rq] : 0.0;  // B[k][n] = wz_{s_k}(z_n), n = rq
+        double q[NCH];
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) q[c] = sk >= 0 ? s_q[sk][c] : 0.0;
+#pragma unroll
+        for (int rb = 0; rb < 4; ++rb) {
+          const int p = rb * 8 + rq;  // position of A row rq in row block rb
+          const double cxy = sk >= 0 ? s_wx[sk][wx0 + (p & 3)] * s_wy[sk][wy0 + (p >> 2)] : 0.0;
+#pragma unroll
+          for (int c = 0; c < NCH; ++c) dmma_884(acc[rb][c][0], acc[rb][c][1], cxy * q[c], bz);
+        }
+      }
+    }
+  }
+  // C fragment: row rq of row block rb = position p, columns z = 2 kq, 2 kq + 1
+#pragma unroll
+  for (int rb = 0; rb < 4; ++rb) {
+    const int p = rb * 8 + rq;
+    const int x = x0 + wx0 + (p & 3), y = y0 + wy0 + (p >> 2);
+    if (x < g.dims[0] && y < g.dims[1]) {
+#pragma unroll
+      for (int c = 0; c < NCH; ++c) {
+        double* dst = grids + c * g.ch_stride + x * g.stride[0] + y * g.stride[1];
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const int z = z0 + 2 * kq + i;
+          if (z < g.dims[2]) dst[z * g.stride[2]] = acc[rb][c][i];
+        }
+      }
+    }
+  }
+}
+
 // Warp-independent variant (no CTA barriers): every warp streams the tile's candidate
 // list itself, 32 sources at a time (lane = source), keeps the sources whose support
 // reaches its own 4x8 (x,y) patch and the tile's z-range (ballot), builds their window
@@ -414,11 +581,14 @@ hs_status launch_spread(hs_ctx* ctx, const double4* pts, const double* w, int n,
     const int cn = std::min(SP_MAXCH, nch - c0);
     double* gout = grids + (size_t)c0 * g.ch_stride;
     const double* wc0 = w + c0;
-    static const bool v1 = getenv("HS_SPREAD_V1") != nullptr;  // CTA-staged variant (comparison)
+    // default: DMMA tensor-core accumulation; HS_SPREAD_V1 = scalar DFMA, HS_SPREAD_V2 = warp-independent
+    static const int variant = getenv("HS_SPREAD_V1") ? 1 : (getenv("HS_SPREAD_V2") ? 2 : 0);
     switch (cn) {
 #define HS_SP(N)                                                                                              \
   case N:                                                                                                     \
-    if (v1)                                                                                                   \
+    if (variant == 0)                                                                                         \
+      k_spread_mma<N><<<grid, block, 0, ctx->stream>>>(lo, wxy, wz, wc0, nch, bin_start, g, wc, nbx, nby, nbz, gout); \
+    else if (variant == 1)                                                                                    \
       k_spread<N><<<grid, block, 0, ctx->stream>>>(lo, wxy, wz, wc0, nch, bin_start, g, wc, nbx, nby, nbz, gout); \
     else {                                                                                                    \
       const size_t sm2 = sizeof(double) * 8 * 32 * (SW_STRIDE + (N | 1));                                     \
