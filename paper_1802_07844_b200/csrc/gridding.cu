@@ -288,17 +288,18 @@ __device__ __forceinline__ void dmma_884(double& c0, double& c1, double a, doubl
                : "d"(a), "d"(b));
 }
 
-template <int NCH>
+template <int NCH, int CH>
 __global__ void __launch_bounds__(256, 2) k_spread_mma(const int4* __restrict__ lo4, const double4* __restrict__ wxy,
                                                       const double2* __restrict__ wzp, const double* __restrict__ w,
                                                       int ldw, const int* __restrict__ bin_start, GridGeom g,
                                                       WinConst wc, int nbx, int nby, int nbz,
                                                       double* __restrict__ grids) {
-  __shared__ double s_wx[SP_CHUNK][SP_TX + 1];
-  __shared__ double s_wy[SP_CHUNK][SP_TY + 1];
-  __shared__ double s_wz[SP_CHUNK][SP_TZ + 1];
-  __shared__ double s_q[SP_CHUNK][NCH | 1];
-  __shared__ unsigned s_mask[SP_CHUNK];
+  extern __shared__ double sm_dyn[];  // CH-source staging (dynamic: CH * ~50 doubles)
+  double(*s_wx)[SP_TX + 1] = reinterpret_cast<double(*)[SP_TX + 1]>(sm_dyn);
+  double(*s_wy)[SP_TY + 1] = reinterpret_cast<double(*)[SP_TY + 1]>(sm_dyn + CH * (SP_TX + 1));
+  double(*s_wz)[SP_TZ + 1] = reinterpret_cast<double(*)[SP_TZ + 1]>(sm_dyn + CH * (SP_TX + SP_TY + 2));
+  double(*s_q)[NCH | 1] = reinterpret_cast<double(*)[NCH | 1]>(sm_dyn + CH * (SP_TX + SP_TY + SP_TZ + 3));
+  unsigned* s_mask = reinterpret_cast<unsigned*>(sm_dyn + CH * (SP_TX + SP_TY + SP_TZ + 3 + (NCH | 1)));
   __shared__ double s_e3[SP_MAXP];
   __shared__ int run_beg[9], run_pre[10];
   __shared__ int s_nrun;
@@ -341,15 +342,16 @@ __global__ void __launch_bounds__(256, 2) k_spread_mma(const int4* __restrict__ 
     for (int c = 0; c < NCH; ++c) acc[rb][c][0] = acc[rb][c][1] = 0.0;
 
   const int role = warp >> 1;
-  int4 pl[2];
-  double4 pe[2];
-  double pq[2][NCH];
+  constexpr int KPT = CH / 64;  // sources per staging thread
+  int4 pl[KPT];
+  double4 pe[KPT];
+  double pq[KPT][NCH];
   auto prefetch = [&](int cbase) {
 #pragma unroll
-    for (int k = 0; k < 2; ++k) {
+    for (int k = 0; k < KPT; ++k) {
       const int sidx = (warp & 1) * 32 + lane + 64 * k;
       const int v = cbase + sidx;
-      if (sidx < SP_CHUNK && v < ncand) {
+      if (v < ncand) {
         int r = 0;
         while (r + 1 < nrun && run_pre[r + 1] <= v) ++r;
         const int row = run_beg[r] + (v - run_pre[r]);
@@ -367,11 +369,11 @@ __global__ void __launch_bounds__(256, 2) k_spread_mma(const int4* __restrict__ 
     }
   };
   if (ncand > 0) prefetch(0);
-  for (int c0 = 0; c0 < ncand; c0 += SP_CHUNK) {
-    const int nc = min(SP_CHUNK, ncand - c0);
+  for (int c0 = 0; c0 < ncand; c0 += CH) {
+    const int nc = min(CH, ncand - c0);
     __syncthreads();
 #pragma unroll
-    for (int k = 0; k < 2; ++k) {
+    for (int k = 0; k < KPT; ++k) {
       const int s = (warp & 1) * 32 + lane + 64 * k;
       if (s < nc) {
         const int4 l = pl[k];
@@ -397,7 +399,7 @@ __global__ void __launch_bounds__(256, 2) k_spread_mma(const int4* __restrict__ 
       }
     }
     __syncthreads();
-    if (c0 + SP_CHUNK < ncand) prefetch(c0 + SP_CHUNK);
+    if (c0 + CH < ncand) prefetch(c0 + CH);
     for (int base = 0; base < nc; base += 32) {
       unsigned m = __ballot_sync(0xffffffffu, base + lane < nc && ((s_mask[base + lane] >> warp) & 1u));
       while (m) {
@@ -586,9 +588,13 @@ hs_status launch_spread(hs_ctx* ctx, const double4* pts, const double* w, int n,
     switch (cn) {
 #define HS_SP(N)                                                                                              \
   case N:                                                                                                     \
-    if (variant == 0)                                                                                         \
-      k_spread_mma<N><<<grid, block, 0, ctx->stream>>>(lo, wxy, wz, wc0, nch, bin_start, g, wc, nbx, nby, nbz, gout); \
-    else if (variant == 1)                                                                                    \
+    if (variant == 0) {                                                                                       \
+      constexpr int CHM = 64;                                                                                 \
+      const size_t smm = sizeof(double) * CHM * (SP_TX + SP_TY + SP_TZ + 3 + (N | 1)) + sizeof(unsigned) * CHM; \
+      HS_CUDA(cudaFuncSetAttribute(k_spread_mma<N, CHM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smm)); \
+      k_spread_mma<N, CHM><<<grid, block, smm, ctx->stream>>>(lo, wxy, wz, wc0, nch, bin_start, g, wc, nbx, nby, nbz, \
+                                                              gout);                                          \
+    } else if (variant == 1)                                                                                  \
       k_spread<N><<<grid, block, 0, ctx->stream>>>(lo, wxy, wz, wc0, nch, bin_start, g, wc, nbx, nby, nbz, gout); \
     else {                                                                                                    \
       const size_t sm2 = sizeof(double) * 8 * 32 * (SW_STRIDE + (N | 1));                                     \
