@@ -33,10 +33,11 @@ class Workload:
 WORKLOADS = {
     # BASELINE configs[0]: the reference's CPU-runnable case
     "cfg1": Workload("cfg1", "stokeslet", 1000, 1.0, 12.0, 0.35, 64, 24, 1001),
-    # SURVEY App. B balanced rule xi = 0.26 M / L, rc from the reference estimator
+    # SURVEY App. B balanced rule xi = 0.26 M / L; rc = estimates.select_rc(kind, 1e-10 * rms(u), xi, L, Q)
+    # (reference estimator, ref:estimates.py:105-125; rms(u) from SURVEY App. B)
     "cfg2": Workload("cfg2", "stokeslet", 100_000, 1.0, 33.28, 0.151, 128, 24, 1002),
     "cfg3": Workload("cfg3", "stresslet", 100_000, 1.0, 33.28, 0.163, 128, 24, 1003, zdist="uniform0"),
-    "cfg4": Workload("cfg4", "rotlet", 1_000_000, 1.0, 83.2, 0.0466, 320, 24, 1004, zdist="wall_exp"),
+    "cfg4": Workload("cfg4", "rotlet", 1_000_000, 1.0, 83.2, 0.0555, 320, 24, 1004, zdist="wall_exp"),
     # the metric's configuration: half-space stokeslet, N = 1e6
     "HL": Workload("HL", "stokeslet", 1_000_000, 1.0, 49.92, 0.101, 192, 24, 1000),
     "cfg5": Workload("cfg5", "stokeslet", 4_000_000, 2.0, 49.92, 0.10, 384, 24, 1005, separate_targets=True),
