@@ -902,6 +902,165 @@ __global__ void __launch_bounds__(GA_T, 2) k_gather3(const double4* __restrict__
   }
 }
 
+// Barrier-free gather: lanes = 32 nearby targets (one warp is independent of the others).
+// The warp walks the (x,y) columns of its targets' union; each column's z-range (<= GA_ZM
+// nodes x 6 channels, 1.5 KB) is loaded cooperatively (one 48-byte node per lane, fully
+// coalesced) into a warp-private, double-buffered shared-memory slot one column ahead, and
+// consumed with broadcast 128-bit reads against the per-lane register z-window.
+template <int NCH, int PITCH>
+__global__ void __launch_bounds__(256, 2) k_gather5(const double4* __restrict__ pts, const int* __restrict__ orig,
+                                                   int n, GridGeom g, const double* __restrict__ T,
+                                                   double* __restrict__ u_four, double* __restrict__ u_tot,
+                                                   const double* __restrict__ u_real, unsigned* __restrict__ flags) {
+  __shared__ __align__(16) double s_col[8][2][GA_ZM * PITCH];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nwarps = gridDim.x * (blockDim.x >> 5);
+  const int P = g.P;
+  const double q = exp(-2.0 * g.alpha * g.h * g.h);
+  for (int wbase = (blockIdx.x * (blockDim.x >> 5) + warp) * 32; wbase < n; wbase += nwarps * 32) {
+    const int t = wbase + lane;
+    const bool valid = t < n;
+    const double4 pt = pts[valid ? t : wbase];
+    const double pc[3] = {pt.x, pt.y, pt.z};
+    int lo[3];
+    bool bad = false;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const int64_t l = window_lo(pc[k], g.origin[k], g.h, P);
+      bad |= (l < 0) || (l + P > g.dims[k]);
+      lo[k] = (int)l;
+    }
+    if (valid && bad) atomicOr(flags, FLAG_OUT_OF_GRID);
+    const bool act = valid && !bad;
+    int W0[3], W1[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      W0[k] = (int)__reduce_min_sync(0xffffffffu, (unsigned)(act ? lo[k] : 0x7fffffff));
+      W1[k] = (int)__reduce_max_sync(0xffffffffu, (unsigned)(act ? lo[k] + P : 0));
+    }
+    double acc[NCH];
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) acc[c] = 0.0;
+    const int nzw = W1[2] - W0[2];
+    if (W1[0] > W0[0] && nzw <= GA_ZM) {
+      double w0[3], r0[3];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        const double d = window_d(pc[k], g.origin[k], g.h, lo[k]);
+        w0[k] = act ? exp(-g.alpha * d * d) : 0.0;
+        r0[k] = exp(g.alpha * (2.0 * d * g.h - g.h * g.h));
+      }
+      w0[2] *= g.pref;
+      double wzv[GA_ZM];
+      {
+        double wz = w0[2], rz = r0[2];
+#pragma unroll
+        for (int i = 0; i < GA_ZM; ++i) {
+          const int z = W0[2] + i;
+          const bool inz = z >= lo[2] && z < lo[2] + P;
+          wzv[i] = inz ? wz : 0.0;
+          if (inz) {
+            wz *= rz;
+            rz *= q;
+          }
+        }
+      }
+      const int ny_u = W1[1] - W0[1];
+      const int ncol = (W1[0] - W0[0]) * ny_u;
+      const int zl = min(lane, nzw - 1);  // node this lane loads (clamped; wzv is 0 beyond nzw)
+      auto load_col = [&](int ci, double2* r) {
+        const int x = W0[0] + ci / ny_u, y = W0[1] + ci % ny_u;
+        const double* src = T + (int64_t)x * g.stride[0] + (int64_t)y * g.stride[1] + (int64_t)(W0[2] + zl) * PITCH;
+#pragma unroll
+        for (int c = 0; c < PITCH / 2; ++c) r[c] = __ldg(reinterpret_cast<const double2*>(src) + c);
+      };
+      double2 nxt[PITCH / 2];
+      load_col(0, nxt);
+      double wx = w0[0], rx = r0[0], wy = w0[1], ry = r0[1], wxe = 0.0;
+      for (int ci = 0; ci < ncol; ++ci) {
+        const int buf = ci & 1;
+        double2* dst = reinterpret_cast<double2*>(s_col[warp][buf]) + lane * (PITCH / 2);
+#pragma unroll
+        for (int c = 0; c < PITCH / 2; ++c) dst[c] = nxt[c];
+        __syncwarp();
+        if (ci + 1 < ncol) load_col(ci + 1, nxt);
+        // window factors of column (x, y) (x-major, y-minor traversal)
+        const int yy = ci % ny_u;
+        if (yy == 0) {
+          const int x = W0[0] + ci / ny_u;
+          const bool inx = x >= lo[0] && x < lo[0] + P;
+          wxe = inx ? wx : 0.0;
+          if (inx) {
+            wx *= rx;
+            rx *= q;
+          }
+          wy = w0[1];
+          ry = r0[1];
+        }
+        const int y = W0[1] + yy;
+        const bool iny = y >= lo[1] && y < lo[1] + P;
+        const double cxy = wxe * (iny ? wy : 0.0);
+        if (iny) {
+          wy *= ry;
+          ry *= q;
+        }
+        if (__any_sync(0xffffffffu, cxy != 0.0)) {
+          const double* colp = s_col[warp][buf];
+          double S[NCH];
+#pragma unroll
+          for (int c = 0; c < NCH; ++c) S[c] = 0.0;
+#pragma unroll
+          for (int i = 0; i < GA_ZM; ++i) {
+            double v[PITCH];
+#pragma unroll
+            for (int c = 0; c < PITCH; c += 2) {
+              const double2 vv = *reinterpret_cast<const double2*>(colp + i * PITCH + c);
+              v[c] = vv.x;
+              v[c + 1] = vv.y;
+            }
+#pragma unroll
+            for (int c = 0; c < NCH; ++c) S[c] = fma(wzv[i], v[c], S[c]);
+          }
+#pragma unroll
+          for (int c = 0; c < NCH; ++c) acc[c] = fma(cxy, S[c], acc[c]);
+        }
+      }
+    } else if (W1[0] > W0[0]) {
+      // sparse warp (z range wider than the register window): each lane sums its own support
+      if (act) {
+        double ws[3][GA_ZM];
+        for (int k = 0; k < 3; ++k)
+          for (int a2 = 0; a2 < P; ++a2) {
+            const double d = window_d(pc[k], g.origin[k], g.h, lo[k] + a2);
+            ws[k][a2] = exp(-g.alpha * d * d);
+          }
+        for (int a2 = 0; a2 < P; ++a2)
+          for (int b2 = 0; b2 < P; ++b2) {
+            const double cxy = g.pref * ws[0][a2] * ws[1][b2];
+            const double* src = T + (int64_t)(lo[0] + a2) * g.stride[0] + (int64_t)(lo[1] + b2) * g.stride[1] +
+                                (int64_t)lo[2] * PITCH;
+            for (int c2 = 0; c2 < P; ++c2) {
+              const double wv = cxy * ws[2][c2];
+#pragma unroll
+              for (int c = 0; c < NCH; ++c) acc[c] = fma(wv, __ldg(src + c2 * PITCH + c), acc[c]);
+            }
+          }
+      }
+    }
+    if (act) {
+      const int o = orig[t];
+      const double h3 = g.h * g.h * g.h;
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        double v = acc[k] * h3;
+        if (NCH == 6) v -= pt.z * (acc[3 + k] * h3);
+        if (u_four) u_four[3 * (size_t)o + k] = v;
+        if (u_tot) u_tot[3 * (size_t)o + k] = (u_real ? u_real[3 * (size_t)o + k] : 0.0) + v;
+      }
+    }
+  }
+}
+
 hs_status launch_gather_fourier(hs_ctx* ctx, const double4* pts, const int* orig, int n, int half, const GridGeom& g,
                                 const double* T, double* u_fourier, double* u_total, const double* u_real) {
   if (n == 0) return HS_OK;
@@ -914,6 +1073,17 @@ hs_status launch_gather_fourier(hs_ctx* ctx, const double4* pts, const int* orig
     else
       k_gather<3, 1><<<gs1, 256, 0, ctx->stream>>>(pts, orig, n, g, T, u_fourier, 3, 1.0, u_total, u_real,
                                                    ctx->d_flags);
+    HS_LAUNCHED(ctx);
+    return HS_OK;
+  }
+  if (g.P > GA_ZM) return fail(HS_ERR_PARAMETER, "window support P > 32 is not supported by the gather");
+  static const bool v3 = getenv("HS_GATHER_V3") != nullptr;  // CTA-staged variant (comparison)
+  if (!v3) {
+    const int gs5 = (int)std::min<int64_t>(ceil_div(n, 256), (int64_t)ctx->sm_count * 32);
+    if (half)
+      k_gather5<6, 6><<<gs5, 256, 0, ctx->stream>>>(pts, orig, n, g, T, u_fourier, u_total, u_real, ctx->d_flags);
+    else
+      k_gather5<3, 4><<<gs5, 256, 0, ctx->stream>>>(pts, orig, n, g, T, u_fourier, u_total, u_real, ctx->d_flags);
     HS_LAUNCHED(ctx);
     return HS_OK;
   }
