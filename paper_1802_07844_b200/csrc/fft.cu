@@ -364,9 +364,9 @@ hs_status launch_xfused(hs_ctx* ctx, int kind, int half, const XArgs& a) {
     if (kind == HS_STRESSLET) return launch_xfused_half<HS_STRESSLET, 1>(ctx, a);
     return launch_xfused_half<HS_ROTLET, 1>(ctx, a);
   }
-  if (kind == HS_STOKESLET) return launch_xfused_t<HS_STOKESLET, false, 2, AnyFFT>(ctx, a);
-  if (kind == HS_STRESSLET) return launch_xfused_t<HS_STRESSLET, false, 2, AnyFFT>(ctx, a);
-  return launch_xfused_t<HS_ROTLET, false, 2, AnyFFT>(ctx, a);
+  if (kind == HS_STOKESLET) return launch_xfused_t<HS_STOKESLET, false, 1, AnyFFT>(ctx, a);
+  if (kind == HS_STRESSLET) return launch_xfused_t<HS_STRESSLET, false, 1, AnyFFT>(ctx, a);
+  return launch_xfused_t<HS_ROTLET, false, 1, AnyFFT>(ctx, a);
 }
 
 // twiddles exp(-2 pi i j / n), computed in long double on the host
