@@ -283,3 +283,18 @@ def test_configs_vs_direct_subset(gpu, name):
     s, _ = make_system(w)
     err = _subset_direct_check(gpu, s, None, gpu.EwaldParams(xi=w.xi, rc=w.rc, M=w.M, P=w.P), nsub=300)
     assert err < 1e-8, err
+
+
+def test_target_sharded_matches_unsharded(gpu):
+    """Single-device emulation of the target-sharded multi-GPU evaluation (sharding.py):
+    the shards' slices, evaluated independently, reassemble the unsharded result."""
+    from paper_1802_07844_b200.configs import make_system
+    from paper_1802_07844_b200.sharding import shard_bounds
+    s, _ = make_system("cfg2", n=40_000)
+    p = gpu.EwaldParams(xi=20.8, rc=0.17, M=80, P=24)
+    full = gpu.ewald_sum(s, p).velocities
+    parts = []
+    for r in range(3):
+        lo, hi = shard_bounds(s.n, 3, r)
+        parts.append(gpu.ewald_sum(s, p, targets=s.positions[lo:hi], target_indices=np.arange(lo, hi)).velocities)
+    assert rel_l2(np.concatenate(parts), full) < 1e-13
