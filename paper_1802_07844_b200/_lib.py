@@ -15,7 +15,8 @@ import numpy as np
 
 from .errors import DeviceError, raise_for_status
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libhsewald_b200.so")
+# HSEWALD_LIB: alternative build of the same library (kernel-variant A/B runs in tools/)
+LIB_PATH = os.environ.get("HSEWALD_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libhsewald_b200.so")
 
 HS_MEM_DEVICE, HS_MEM_HOST = 0, 1
 KIND_ID = {"stokeslet": 0, "stresslet": 1, "rotlet": 2}

@@ -33,16 +33,58 @@ static bool g_erfcx_ready = false;
 
 // erfc(x) = exp(-x^2) erfcx(x); E = exp(-x^2) is already computed by the caller.
 // Piecewise degree-13 polynomials on [0, 8) (tools/gen_erfcx.py, max rel. error ~1.1e-15).
+// Branch-free: x >= 8 (only reachable when xi r_c >= 8) clamps to the last interval's end
+// point; there erfc(x) < 1.2e-29 and the pair's contribution is below double resolution
+// of any sum it enters.
 __device__ __forceinline__ double erfc_from_E(double x, double E, const double* __restrict__ tab) {
-  if (x < HS_ERFCX_W * HS_ERFCX_NINT) {
-    const int k = (int)(x * (1.0 / HS_ERFCX_W));
-    const double t = (x - (HS_ERFCX_W * k + 0.5 * HS_ERFCX_W)) * (2.0 / HS_ERFCX_W);
-    double p = tab[HS_ERFCX_DEG * HS_ERFCX_NINT + k];
+  const double xc = fmin(x, HS_ERFCX_W * HS_ERFCX_NINT);
+  const int k = min((int)(xc * (1.0 / HS_ERFCX_W)), HS_ERFCX_NINT - 1);
+  const double t = (xc - (HS_ERFCX_W * k + 0.5 * HS_ERFCX_W)) * (2.0 / HS_ERFCX_W);
+  double p = tab[HS_ERFCX_DEG * HS_ERFCX_NINT + k];
 #pragma unroll
-    for (int j = HS_ERFCX_DEG - 1; j >= 0; --j) p = fma(p, t, tab[j * HS_ERFCX_NINT + k]);
-    return E * p;
+  for (int j = HS_ERFCX_DEG - 1; j >= 0; --j) p = fma(p, t, tab[j * HS_ERFCX_NINT + k]);
+  return E * p;
+}
+
+// exp(x) for x <= 0, branch-free (no special-case slow path, so two pair evaluations
+// interleave freely): x = n ln2 + r, |r| <= ln2/2, Taylor degree 13 (truncation 5e-18),
+// 2^n assembled in the exponent field.  Arguments below -708 clamp (result ~1e-308).
+__device__ __forceinline__ double exp_nonpos(double x) {
+  x = fmax(x, -708.0);
+  const double kShift = 6755399441055744.0;  // 1.5 * 2^52
+  const double t = fma(x, 1.4426950408889634, kShift);
+  const double n = t - kShift;
+  const int ni = __double2loint(t);
+  double r = fma(n, -6.93147180369123816490e-01, x);  // ln2 hi (exact product for |n| < 2^11)
+  r = fma(n, -1.90821492927058770002e-10, r);         // ln2 lo
+  double p = 1.0 / 6227020800.0;
+  p = fma(p, r, 1.0 / 479001600.0);
+  p = fma(p, r, 1.0 / 39916800.0);
+  p = fma(p, r, 1.0 / 3628800.0);
+  p = fma(p, r, 1.0 / 362880.0);
+  p = fma(p, r, 1.0 / 40320.0);
+  p = fma(p, r, 1.0 / 5040.0);
+  p = fma(p, r, 1.0 / 720.0);
+  p = fma(p, r, 1.0 / 120.0);
+  p = fma(p, r, 1.0 / 24.0);
+  p = fma(p, r, 1.0 / 6.0);
+  p = fma(p, r, 0.5);
+  p = fma(p, r, 1.0);
+  p = fma(p, r, 1.0);
+  return p * __hiloint2double((ni + 1023) << 20, 0);
+}
+
+// 1/sqrt(r2) for normal r2 > 0, branch-free: hardware approximation + two Newton steps
+__device__ __forceinline__ double rsqrt_pos(double r2) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(r2));
+#pragma unroll
+  for (int it = 0; it < 2; ++it) {  // ~2^-23 -> 2^-46 -> rounding level
+    const double h = r2 * y;
+    const double e = fma(-h, y, 1.0);
+    y = fma(0.5 * y, e, y);
   }
-  return erfc(x);
+  return y;
 }
 
 constexpr int PT_MAXRUN = 25;  // 5 x 5 (x, y) cell columns
@@ -51,23 +93,37 @@ struct PairConst {
   double xi, xi2, c2xs;  // xi, xi^2, 2 xi / sqrt(pi)
 };
 
+// Radial coefficients of one pair (the transcendental part; branch-free when SCREENED).
+struct PairCoef {
+  double ri, ri2, c0, c1, e;
+};
+template <bool SCREENED>
+__device__ __forceinline__ PairCoef pair_coef(const PairConst& pc, double r2, const double* __restrict__ etab) {
+  PairCoef q;
+  double C = 1.0;
+  q.e = 0.0;
+  if (SCREENED) {
+    q.ri = rsqrt_pos(r2);
+    const double rn = r2 * q.ri;
+    const double E = exp_nonpos(-pc.xi2 * r2);
+    C = erfc_from_E(pc.xi * rn, E, etab);
+    q.e = pc.c2xs * E;
+  } else {
+    q.ri = rsqrt(r2);
+  }
+  q.ri2 = q.ri * q.ri;
+  q.c0 = C * q.ri;
+  q.c1 = (q.c0 + q.e) * q.ri2;
+  return q;
+}
+
 // Accumulate one pair.  d = x - y (target minus source), r2 = |d|^2 (> 0).
 // k[0..2]: kernel part (raw), c[0..2]: wall correction (raw, 4 pi G convention).
-template <int KIND, bool SCREENED>
-__device__ __forceinline__ void eval_pair(const PairConst& pc, double d0, double d1, double d2, double r2,
-                                          double x2, const double4& S, const double4& A, const double4& B,
-                                          bool image, double* k, double* c, const double* __restrict__ etab) {
-  const double ri = rsqrt(r2);
-  const double ri2 = ri * ri;
-  double C = 1.0, e = 0.0;
-  if (SCREENED) {
-    const double rn = r2 * ri;
-    const double E = exp(-pc.xi2 * r2);
-    C = erfc_from_E(pc.xi * rn, E, etab);
-    e = pc.c2xs * E;
-  }
-  const double c0 = C * ri;
-  const double c1 = (c0 + e) * ri2;
+template <int KIND>
+__device__ __forceinline__ void apply_pair(const PairConst& pc, const PairCoef& q, double d0, double d1, double d2,
+                                           double r2, double x2, const double4& S, const double4& A,
+                                           const double4& B, bool image, double* k, double* c) {
+  const double ri = q.ri, ri2 = q.ri2, c0 = q.c0, c1 = q.c1, e = q.e;
   if (KIND == HS_STOKESLET) {
     // a = 2(xi E/sqrt(pi) + C/(2r)) = C/r + e ; a - b = C/r - e   (ewald_real.py:303-309)
     const double a = c0 + e, amb = c0 - e;
@@ -137,6 +193,13 @@ __device__ __forceinline__ void eval_pair(const PairConst& pc, double d0, double
   }
 }
 
+template <int KIND, bool SCREENED>
+__device__ __forceinline__ void eval_pair(const PairConst& pc, double d0, double d1, double d2, double r2,
+                                          double x2, const double4& S, const double4& A, const double4& B,
+                                          bool image, double* k, double* c, const double* __restrict__ etab) {
+  apply_pair<KIND>(pc, pair_coef<SCREENED>(pc, r2, etab), d0, d1, d2, r2, x2, S, A, B, image, k, c);
+}
+
 __device__ __forceinline__ double exact_r2(double d0, double d1, double d2) {
   // numba: r2 = d0 * d0 + d1 * d1 + d2 * d2, each op rounded, left to right
   return __dadd_rn(__dadd_rn(__dmul_rn(d0, d0), __dmul_rn(d1, d1)), __dmul_rn(d2, d2));
@@ -158,9 +221,12 @@ constexpr int PC_TG = PC_WARPS * 32;  // targets per work item
 constexpr int PC_K = 256;             // staged candidates (two halves of PC_H)
 constexpr int PC_H = PC_K / 2;        // candidates per chunk
 constexpr int PC_Q = 64;              // per-lane queue capacity
+#ifndef PC_MINB
+#define PC_MINB 4                     // resident CTAs per SM (register budget 128)
+#endif
 
 template <int KIND, bool HALF>
-__global__ void __launch_bounds__(PC_TG, 5) k_pair_q(const PairArgs a) {
+__global__ void __launch_bounds__(PC_TG, PC_MINB) k_pair_q(const PairArgs a) {
   __shared__ double4 sP[PC_K];
   __shared__ float4 sF[PC_K];   // candidate position relative to the item's first target (FP32 prefilter)
   __shared__ double4 sA[PC_K];
@@ -268,6 +334,33 @@ __global__ void __launch_bounds__(PC_TG, 5) k_pair_q(const PairArgs a) {
       ++n_acc;
       eval_one(jj);
     };
+    // two queued pairs in straight-line code: their exp / erfc / rsqrt chains are
+    // independent and interleave (the evaluation is latency-, not issue-bound)
+    auto pop_eval2 = [&]() {
+      const int j1 = q[head & (PC_Q - 1)][lane];
+      const int j2 = q[(head + 1) & (PC_Q - 1)][lane];
+      head += 2;
+      n_acc += 2;
+      const double4 S1 = sP[j1], S2 = sP[j2];
+      const double f0 = T.x - S1.x, f1 = T.y - S1.y, f2 = T.z - S1.z;
+      const double g0 = T.x - S2.x, g1 = T.y - S2.y, g2 = T.z - S2.z;
+      const double r1 = exact_r2(f0, f1, f2), r2 = exact_r2(g0, g1, g2);
+      const PairCoef q1 = pair_coef<true>(pc, r1, s_erfcx);
+      const PairCoef q2 = pair_coef<true>(pc, r2, s_erfcx);
+      const bool i1 = HALF && (__float_as_int(sF[j1].w) >= a.n_real);
+      const bool i2 = HALF && (__float_as_int(sF[j2].w) >= a.n_real);
+      n_img += (unsigned)i1 + (unsigned)i2;
+      {
+        const double4 A = sA[j1];
+        const double4 B = kNeedB ? sB[j1] : make_double4(0, 0, 0, 0);
+        apply_pair<KIND>(pc, q1, f0, f1, f2, r1, T.z, S1, A, B, i1, &acc[0], &acc[3]);
+      }
+      {
+        const double4 A = sA[j2];
+        const double4 B = kNeedB ? sB[j2] : make_double4(0, 0, 0, 0);
+        apply_pair<KIND>(pc, q2, g0, g1, g2, r2, T.z, S2, A, B, i2, &acc[0], &acc[3]);
+      }
+    };
     for (int c = 0, c0 = 0; c0 < ncand; ++c, c0 += PC_H) {
       const int h = c & 1, hb = h * PC_H;
       // drain the (oldest) entries that still reference half h
@@ -334,15 +427,21 @@ __global__ void __launch_bounds__(PC_TG, 5) k_pair_q(const PairArgs a) {
         // full rounds while every valid lane has work; partial rounds only against overflow
         unsigned mn = __reduce_min_sync(0xffffffffu, (unsigned)(tvalid ? tail - head : 0x7fffffff));
         if (mn == 0x7fffffffu) mn = 0;
-        if (tvalid)
-          for (unsigned r = 0; r < mn; ++r) pop_eval();
+        if (tvalid) {
+          unsigned r = 0;
+          for (; r + 1 < mn; r += 2) pop_eval2();
+          if (r < mn) pop_eval();
+        }
         while ((int)__reduce_max_sync(0xffffffffu, (unsigned)(tail - head)) > PC_Q - 32) {
           if (tail > head) pop_eval();
         }
       }
     }
     while (__any_sync(0xffffffffu, tail > head)) {
-      if (tail > head) pop_eval();
+      if (tail - head >= 2)
+        pop_eval2();
+      else if (tail > head)
+        pop_eval();
     }
     if (singular) atomicOr(a.flags, FLAG_SINGULAR);
     if (a.counts) {
