@@ -50,7 +50,7 @@ hs_status ctx_check_flags(hs_ctx* ctx, const char* where) {
   HS_CUDA(cudaMemcpyAsync(ctx->h_flags, ctx->d_flags, sizeof(unsigned), cudaMemcpyDeviceToHost, ctx->stream));
   HS_CUDA(cudaStreamSynchronize(ctx->stream));
   const unsigned f = *ctx->h_flags;
-  if (f & FLAG_GEOMETRY) return fail(HS_ERR_GEOMETRY, std::string(where) + ": cell-list bounds do not enclose all points");
+  if (f & FLAG_GEOMETRY) return fail(HS_ERR_GEOMETRY, std::string(where) + ": points outside the box (cell-list bounds, or a source below the wall)");
   if (f & FLAG_OUT_OF_GRID) return fail(HS_ERR_OUT_OF_GRID, std::string(where) + ": window support leaves the grid");
   if (f & FLAG_SINGULAR) return fail(HS_ERR_SINGULAR, std::string(where) + ": coincident target and source");
   return HS_OK;

@@ -227,11 +227,15 @@ constexpr int PC_Q = 64;              // per-lane queue capacity
 
 template <int KIND, bool HALF>
 __global__ void __launch_bounds__(PC_TG, PC_MINB) k_pair_q(const PairArgs a) {
-  __shared__ double4 sP[PC_K];
-  __shared__ float4 sF[PC_K];   // candidate position relative to the item's first target (FP32 prefilter)
-  __shared__ double4 sA[PC_K];
+  // Candidate rows as 16-byte columns: the evaluation reads them at lane-random rows, and a
+  // 16-byte array spreads those reads over 8 bank groups (a 32-byte row only over 4).
+  __shared__ double2 sXY[PC_K];  // x, y
+  __shared__ double2 sZA[PC_K];  // z (sign bit = image in the half space), a.x
+  __shared__ double2 sAA[PC_K];  // a.y, a.z
+  __shared__ float4 sF[PC_K];    // candidate position relative to the item's first target (FP32 prefilter)
   constexpr bool kNeedB = (KIND == HS_STRESSLET) || (KIND == HS_ROTLET && HALF);
-  __shared__ double4 sB[kNeedB ? PC_K : 1];
+  __shared__ double2 sB0[kNeedB ? PC_K : 1];  // b.x, b.y
+  __shared__ double sB1[KIND == HS_STRESSLET ? PC_K : 1];  // b.z
   __shared__ unsigned short sq[PC_WARPS][PC_Q][32];
   __shared__ int run_beg[PT_MAXRUN];
   __shared__ int run_pre[PT_MAXRUN + 1];
@@ -302,13 +306,27 @@ __global__ void __launch_bounds__(PC_TG, PC_MINB) k_pair_q(const PairArgs a) {
     bool singular = false;
     unsigned long long n_acc = 0, n_img = 0;
 
+    // candidate row j as (S, A, B); S.w unused; image <=> sign bit of z (k_pair_records)
+    auto load_cand = [&](int jj, double4& S, double4& A, double4& B, bool& img) {
+      const double2 xy = sXY[jj], za = sZA[jj], aa = sAA[jj];
+      S = make_double4(xy.x, xy.y, za.x, 0.0);
+      A = make_double4(za.y, aa.x, aa.y, 0.0);
+      img = HALF && __double_as_longlong(za.x) < 0;
+      B = make_double4(0, 0, 0, 0);
+      if (KIND == HS_STRESSLET) {
+        const double2 b = sB0[jj];
+        B = make_double4(b.x, b.y, sB1[jj], 0.0);
+      } else if (kNeedB && img) {  // rotlet: the wall channel exists for images only
+        const double2 b = sB0[jj];
+        B = make_double4(b.x, b.y, 0.0, 0.0);
+      }
+    };
     auto eval_one = [&](int jj) {
-      const double4 S = sP[jj];
-      const double4 A = sA[jj];
-      const double4 B = kNeedB ? sB[jj] : make_double4(0, 0, 0, 0);
+      double4 S, A, B;
+      bool img;
+      load_cand(jj, S, A, B, img);
       const double e0 = T.x - S.x, e1 = T.y - S.y, e2 = T.z - S.z;
       const double rr = exact_r2(e0, e1, e2);
-      const bool img = HALF && (__float_as_int(sF[jj].w) >= a.n_real);
       if (img) ++n_img;
       eval_pair<KIND, true>(pc, e0, e1, e2, rr, T.z, S, A, B, img, &acc[0], &acc[3], s_erfcx);
     };
@@ -341,25 +359,18 @@ __global__ void __launch_bounds__(PC_TG, PC_MINB) k_pair_q(const PairArgs a) {
       const int j2 = q[(head + 1) & (PC_Q - 1)][lane];
       head += 2;
       n_acc += 2;
-      const double4 S1 = sP[j1], S2 = sP[j2];
+      double4 S1, A1, B1, S2, A2, B2;
+      bool i1, i2;
+      load_cand(j1, S1, A1, B1, i1);
+      load_cand(j2, S2, A2, B2, i2);
       const double f0 = T.x - S1.x, f1 = T.y - S1.y, f2 = T.z - S1.z;
       const double g0 = T.x - S2.x, g1 = T.y - S2.y, g2 = T.z - S2.z;
       const double r1 = exact_r2(f0, f1, f2), r2 = exact_r2(g0, g1, g2);
       const PairCoef q1 = pair_coef<true>(pc, r1, s_erfcx);
       const PairCoef q2 = pair_coef<true>(pc, r2, s_erfcx);
-      const bool i1 = HALF && (__float_as_int(sF[j1].w) >= a.n_real);
-      const bool i2 = HALF && (__float_as_int(sF[j2].w) >= a.n_real);
       n_img += (unsigned)i1 + (unsigned)i2;
-      {
-        const double4 A = sA[j1];
-        const double4 B = kNeedB ? sB[j1] : make_double4(0, 0, 0, 0);
-        apply_pair<KIND>(pc, q1, f0, f1, f2, r1, T.z, S1, A, B, i1, &acc[0], &acc[3]);
-      }
-      {
-        const double4 A = sA[j2];
-        const double4 B = kNeedB ? sB[j2] : make_double4(0, 0, 0, 0);
-        apply_pair<KIND>(pc, q2, g0, g1, g2, r2, T.z, S2, A, B, i2, &acc[0], &acc[3]);
-      }
+      apply_pair<KIND>(pc, q1, f0, f1, f2, r1, T.z, S1, A1, B1, i1, &acc[0], &acc[3]);
+      apply_pair<KIND>(pc, q2, g0, g1, g2, r2, T.z, S2, A2, B2, i2, &acc[0], &acc[3]);
     };
     for (int c = 0, c0 = 0; c0 < ncand; ++c, c0 += PC_H) {
       const int h = c & 1, hb = h * PC_H;
@@ -379,12 +390,18 @@ __global__ void __launch_bounds__(PC_TG, PC_MINB) k_pair_q(const PairArgs a) {
           while (r + 1 < nrun && run_pre[r + 1] <= v) ++r;
           const int row = run_beg[r] + (v - run_pre[r]);
           const double4 S = a.P[row];
-          sP[hb + j] = S;
+          const double4 A = a.A[row];
+          sXY[hb + j] = make_double2(S.x, S.y);
+          sZA[hb + j] = make_double2(S.z, A.x);
+          sAA[hb + j] = make_double2(A.y, A.z);
           // .w carries the combined source index as int bits (no per-pair FP64->int conversions)
           sF[hb + j] = make_float4((float)(S.x - R0.x), (float)(S.y - R0.y), (float)(S.z - R0.z),
                                    __int_as_float((int)S.w));
-          sA[hb + j] = a.A[row];
-          if (kNeedB) sB[hb + j] = a.B[row];
+          if (kNeedB) {
+            const double4 B = a.B[row];
+            sB0[hb + j] = make_double2(B.x, B.y);
+            if (KIND == HS_STRESSLET) sB1[hb + j] = B.z;
+          }
         }
       }
       __syncthreads();
@@ -411,8 +428,9 @@ __global__ void __launch_bounds__(PC_TG, PC_MINB) k_pair_q(const PairArgs a) {
           const float fx = tfx - F.x, fy = tfy - F.y, fz = tfz - F.z;
           if (fx * fx + fy * fy + fz * fz <= a.rc2_hi) {
             // exact reference test (bit-identical neighbour sets)
-            const double4 S = sP[j];
-            const double d0 = __dsub_rn(T.x, S.x), d1 = __dsub_rn(T.y, S.y), d2 = __dsub_rn(T.z, S.z);
+            const double2 xy = sXY[j];
+            const double sz = sZA[j].x;
+            const double d0 = __dsub_rn(T.x, xy.x), d1 = __dsub_rn(T.y, xy.y), d2 = __dsub_rn(T.z, sz);
             const double r2 = exact_r2(d0, d1, d2);
             if (r2 <= a.rc2 && __float_as_int(F.w) != tcol_i && tvalid) {
               if (r2 == 0.0) {

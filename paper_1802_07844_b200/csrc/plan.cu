@@ -33,13 +33,17 @@ namespace hs {
 __global__ void k_pair_records(int kind, int half, const int* __restrict__ order, int n_comb, int n,
                                const double* __restrict__ pos, const double* __restrict__ sa,
                                const double* __restrict__ sb, double4* __restrict__ P, double4* __restrict__ A,
-                               double4* __restrict__ B) {
+                               double4* __restrict__ B, unsigned* __restrict__ flags) {
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n_comb; k += gridDim.x * blockDim.x) {
     const int i = order[k];
     const bool img = half && i >= n;
     const int s = img ? i - n : i;
     const double m = img ? -1.0 : 1.0;  // MIRROR z
-    P[k] = make_double4(pos[3 * s], pos[3 * s + 1], m * pos[3 * s + 2], (double)i);
+    // z + 0.0 maps -0.0 to +0.0: in the half space the sign bit of a record's z then tells
+    // images (z <= -0.0) from sources (z >= +0.0), which k_pair_q uses instead of the index
+    const double z = pos[3 * s + 2];
+    if (half && z < 0.0) atomicOr(flags, FLAG_GEOMETRY);  // sources must lie in x3 >= 0 (system.py:77)
+    P[k] = make_double4(pos[3 * s], pos[3 * s + 1], m * (z + 0.0), (double)i);
     const double a0 = sa[3 * s], a1 = sa[3 * s + 1], a2 = sa[3 * s + 2];
     if (kind == HS_STOKESLET) {
       // combined_f = [f; -f^I], f^I = f * (1,1,-1)  (system.py:171-177)
@@ -181,7 +185,8 @@ inline int grid_size(hs_ctx* ctx, int64_t n) {
 hs_status build_pair_records(hs_ctx* ctx, int kind, int half, const int* order, int n_comb, int n, const double* pos,
                              const double* sa, const double* sb, double4* P, double4* A, double4* B) {
   if (n_comb == 0) return HS_OK;
-  k_pair_records<<<grid_size(ctx, n_comb), 256, 0, ctx->stream>>>(kind, half, order, n_comb, n, pos, sa, sb, P, A, B);
+  k_pair_records<<<grid_size(ctx, n_comb), 256, 0, ctx->stream>>>(kind, half, order, n_comb, n, pos, sa, sb, P, A, B,
+                                                                         ctx->d_flags);
   HS_LAUNCHED(ctx);
   return HS_OK;
 }
@@ -669,7 +674,7 @@ extern "C" hs_status hs_plan_execute(hs_plan* p, const double* positions, const 
   if (do_real) {
     HS_TRY(sort_points_by_cell(p, pos, n, p->n_comb, p->half ? 1 : 0, 1, p->order, p->start));
     k_pair_records<<<grid_size(ctx, p->n_comb), 256, 0, st>>>(kind, p->half, p->order, p->n_comb, n, pos, fa, fb,
-                                                              p->P, p->A, p->B);
+                                                              p->P, p->A, p->B, ctx->d_flags);
     HS_LAUNCHED(ctx);
     if (nt > 0) {
       // targets: reference cells, ordered by z sub-slab inside each cell (compact warps)
