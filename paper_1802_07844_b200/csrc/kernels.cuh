@@ -82,6 +82,7 @@ struct PairArgs {
   }
   double xi, rc2;
   float rc2_hi;       // FP32 prefilter bound: (rc (1+1e-4) + 2^-20 box)^2, conservative
+  float rc2_lo;       // FP32 sure-accept bound: (rc (1-1e-4) - 2^-20 box)^2 (0 if negative)
   int n_real;         // combined index >= n_real -> image
   int kind;
   const double* self_f;  // stokeslet self term strengths (original f) or null

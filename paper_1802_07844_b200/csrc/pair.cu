@@ -28,50 +28,48 @@ namespace hs {
 namespace {
 #include "erfcx_table.inc"
 }
-__device__ double g_erfcx_coef[HS_ERFCX_NINT * (HS_ERFCX_DEG + 1)];
+__device__ double2 g_erfcx_coef[HS_ERFCX_NPAIR * HS_ERFCX_NINT];
 static bool g_erfcx_ready = false;
 
 // erfc(x) = exp(-x^2) erfcx(x); E = exp(-x^2) is already computed by the caller.
-// Piecewise degree-13 polynomials on [0, 8) (tools/gen_erfcx.py, max rel. error ~1.1e-15).
-// Branch-free: x >= 8 (only reachable when xi r_c >= 8) clamps to the last interval's end
-// point; there erfc(x) < 1.2e-29 and the pair's contribution is below double resolution
-// of any sum it enters.
-__device__ __forceinline__ double erfc_from_E(double x, double E, const double* __restrict__ tab) {
-  const double xc = fmin(x, HS_ERFCX_W * HS_ERFCX_NINT);
-  const int k = min((int)(xc * (1.0 / HS_ERFCX_W)), HS_ERFCX_NINT - 1);
-  const double t = (xc - (HS_ERFCX_W * k + 0.5 * HS_ERFCX_W)) * (2.0 / HS_ERFCX_W);
-  double p = tab[HS_ERFCX_DEG * HS_ERFCX_NINT + k];
+// Piecewise degree-10 polynomials on [0, 8) (tools/gen_erfcx.py, max rel. error ~1.3e-15),
+// coefficient pairs read with one 16-byte shared-memory load each.
+// Branch-free: x >= 8 (only reachable when xi r_c >= 8) evaluates the last interval's
+// polynomial outside its interval; there erfc(x) < 1.2e-29, so the pair's contribution is
+// below the double resolution of any sum it enters, and E * p stays finite.
+__device__ __forceinline__ double erfc_from_E(double x, double E, const double2* __restrict__ tab) {
+  const int k = min((int)(x * (1.0 / HS_ERFCX_W)), HS_ERFCX_NINT - 1);
+  const double t = (x - (HS_ERFCX_W * k + 0.5 * HS_ERFCX_W)) * (2.0 / HS_ERFCX_W);
+  const double2 top = tab[(HS_ERFCX_NPAIR - 1) * HS_ERFCX_NINT + k];
+  double p = (HS_ERFCX_DEG & 1) ? fma(top.y, t, top.x) : top.x;
 #pragma unroll
-  for (int j = HS_ERFCX_DEG - 1; j >= 0; --j) p = fma(p, t, tab[j * HS_ERFCX_NINT + k]);
+  for (int j = HS_ERFCX_NPAIR - 2; j >= 0; --j) {
+    const double2 c = tab[j * HS_ERFCX_NINT + k];
+    p = fma(p, t, c.y);
+    p = fma(p, t, c.x);
+  }
   return E * p;
 }
 
 // exp(x) for x <= 0, branch-free (no special-case slow path, so two pair evaluations
 // interleave freely): x = n ln2 + r, |r| <= ln2/2, Taylor degree 13 (truncation 5e-18),
-// 2^n assembled in the exponent field.  Arguments below -708 clamp (result ~1e-308).
+// 2^n assembled in the exponent field; below -708 (2^n subnormal) the result flushes to 0.
+// Coefficients live in constant memory so the DFMAs take them as c[] operands.
+__constant__ double c_exp_taylor[14] = {
+    1.0 / 6227020800.0, 1.0 / 479001600.0, 1.0 / 39916800.0, 1.0 / 3628800.0, 1.0 / 362880.0,
+    1.0 / 40320.0,      1.0 / 5040.0,      1.0 / 720.0,      1.0 / 120.0,     1.0 / 24.0,
+    1.0 / 6.0,          0.5,               1.0,              1.0};
 __device__ __forceinline__ double exp_nonpos(double x) {
-  x = fmax(x, -708.0);
   const double kShift = 6755399441055744.0;  // 1.5 * 2^52
   const double t = fma(x, 1.4426950408889634, kShift);
   const double n = t - kShift;
   const int ni = __double2loint(t);
   double r = fma(n, -6.93147180369123816490e-01, x);  // ln2 hi (exact product for |n| < 2^11)
   r = fma(n, -1.90821492927058770002e-10, r);         // ln2 lo
-  double p = 1.0 / 6227020800.0;
-  p = fma(p, r, 1.0 / 479001600.0);
-  p = fma(p, r, 1.0 / 39916800.0);
-  p = fma(p, r, 1.0 / 3628800.0);
-  p = fma(p, r, 1.0 / 362880.0);
-  p = fma(p, r, 1.0 / 40320.0);
-  p = fma(p, r, 1.0 / 5040.0);
-  p = fma(p, r, 1.0 / 720.0);
-  p = fma(p, r, 1.0 / 120.0);
-  p = fma(p, r, 1.0 / 24.0);
-  p = fma(p, r, 1.0 / 6.0);
-  p = fma(p, r, 0.5);
-  p = fma(p, r, 1.0);
-  p = fma(p, r, 1.0);
-  return p * __hiloint2double((ni + 1023) << 20, 0);
+  double p = c_exp_taylor[0];
+#pragma unroll
+  for (int j = 1; j < 14; ++j) p = fma(p, r, c_exp_taylor[j]);
+  return p * __hiloint2double(max(ni + 1023, 0) << 20, 0);
 }
 
 // 1/sqrt(r2) for normal r2 > 0, branch-free: hardware approximation + two Newton steps
@@ -98,7 +96,7 @@ struct PairCoef {
   double ri, ri2, c0, c1, e;
 };
 template <bool SCREENED>
-__device__ __forceinline__ PairCoef pair_coef(const PairConst& pc, double r2, const double* __restrict__ etab) {
+__device__ __forceinline__ PairCoef pair_coef(const PairConst& pc, double r2, const double2* __restrict__ etab) {
   PairCoef q;
   double C = 1.0;
   q.e = 0.0;
@@ -196,7 +194,7 @@ __device__ __forceinline__ void apply_pair(const PairConst& pc, const PairCoef& 
 template <int KIND, bool SCREENED>
 __device__ __forceinline__ void eval_pair(const PairConst& pc, double d0, double d1, double d2, double r2,
                                           double x2, const double4& S, const double4& A, const double4& B,
-                                          bool image, double* k, double* c, const double* __restrict__ etab) {
+                                          bool image, double* k, double* c, const double2* __restrict__ etab) {
   apply_pair<KIND>(pc, pair_coef<SCREENED>(pc, r2, etab), d0, d1, d2, r2, x2, S, A, B, image, k, c);
 }
 
@@ -240,8 +238,8 @@ __global__ void __launch_bounds__(PC_TG, PC_MINB) k_pair_q(const PairArgs a) {
   __shared__ int run_beg[PT_MAXRUN];
   __shared__ int run_pre[PT_MAXRUN + 1];
   __shared__ int s_nrun;
-  __shared__ double s_erfcx[HS_ERFCX_NINT * (HS_ERFCX_DEG + 1)];
-  for (int i = threadIdx.x; i < HS_ERFCX_NINT * (HS_ERFCX_DEG + 1); i += blockDim.x) s_erfcx[i] = g_erfcx_coef[i];
+  __shared__ double2 s_erfcx[HS_ERFCX_NPAIR * HS_ERFCX_NINT];
+  for (int i = threadIdx.x; i < HS_ERFCX_NPAIR * HS_ERFCX_NINT; i += blockDim.x) s_erfcx[i] = g_erfcx_coef[i];
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nx = a.dims[0], ny = a.dims[1], nz = a.dims[2];
@@ -426,14 +424,21 @@ __global__ void __launch_bounds__(PC_TG, PC_MINB) k_pair_q(const PairArgs a) {
           near &= near - 1;
           const float4 F = sF[j];  // broadcast
           const float fx = tfx - F.x, fy = tfy - F.y, fz = tfz - F.z;
-          if (fx * fx + fy * fy + fz * fz <= a.rc2_hi) {
-            // exact reference test (bit-identical neighbour sets)
-            const double2 xy = sXY[j];
-            const double sz = sZA[j].x;
-            const double d0 = __dsub_rn(T.x, xy.x), d1 = __dsub_rn(T.y, xy.y), d2 = __dsub_rn(T.z, sz);
-            const double r2 = exact_r2(d0, d1, d2);
-            if (r2 <= a.rc2 && __float_as_int(F.w) != tcol_i && tvalid) {
-              if (r2 == 0.0) {
+          const float r2f = fx * fx + fy * fy + fz * fz;
+          if (r2f <= a.rc2_hi) {
+            // FP32 distance inside r_c by a margin far above its rounding error: the exact
+            // reference test would accept too; otherwise run it (bit-identical neighbour sets)
+            bool ok = r2f > 0.0f && r2f <= a.rc2_lo, sing = false;
+            if (!ok) {
+              const double2 xy = sXY[j];
+              const double sz = sZA[j].x;
+              const double d0 = __dsub_rn(T.x, xy.x), d1 = __dsub_rn(T.y, xy.y), d2 = __dsub_rn(T.z, sz);
+              const double r2 = exact_r2(d0, d1, d2);
+              ok = r2 <= a.rc2;
+              sing = r2 == 0.0;
+            }
+            if (ok && __float_as_int(F.w) != tcol_i && tvalid) {
+              if (sing) {
                 singular = true;
               } else {
                 q[tail & (PC_Q - 1)][lane] = (unsigned short)j;

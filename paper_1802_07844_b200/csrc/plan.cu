@@ -707,6 +707,8 @@ extern "C" hs_status hs_plan_execute(hs_plan* p, const double* positions, const 
         const double box = 3.0 * prm.L;
         const double rch = prm.rc * (1.0 + 1e-4) + box * std::ldexp(1.0, -20);
         a.rc2_hi = (float)(rch * rch) * (1.0f + 1e-6f);
+        const double rcl = prm.rc * (1.0 - 1e-4) - box * std::ldexp(1.0, -20);
+        a.rc2_lo = rcl > 0 ? (float)(rcl * rcl) * (1.0f - 1e-6f) : 0.0f;
       }
       a.n_real = n;
       a.kind = kind | (p->half ? 16 : 0);
