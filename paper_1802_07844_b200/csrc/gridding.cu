@@ -23,7 +23,8 @@
 namespace hs {
 
 __global__ void k_grid_keys(const double* __restrict__ pos, int n_src, int n, int mode, GridGeom g, int nbx,
-                            int nby, int nbz, int* __restrict__ keys, unsigned* __restrict__ flags) {
+                            int nby, int nbz, int* __restrict__ keys, unsigned* __restrict__ flags,
+                            bool gather_v5_keys) {
   const bool fine = (mode & 8) != 0;  // gather targets: (8x8 column, z cell) order
   mode &= 7;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
@@ -45,11 +46,15 @@ __global__ void k_grid_keys(const double* __restrict__ pos, int n_src, int n, in
       cc[k] = (int)c;
     }
     if (bad) atomicOr(flags, FLAG_OUT_OF_GRID);
-    if (fine) {
-      // warps of 32 consecutive targets then share one 8x8 (x,y) column and a few z cells:
-      // a narrow z range (register z-window in the gather) and an (8+P-1)^2 column union
+    if (fine && gather_v5_keys) {
+      // gather v5: warps of 32 consecutive targets share one 8x8 (x,y) column and a few z cells
       const int n8y = (g.dims[1] + 7) / 8;
       keys[i] = ((cc[0] >> 3) * n8y + (cc[1] >> 3)) * g.dims[2] + cc[2];
+    } else if (fine) {
+      // gather v7: (4x4 (x,y) column, z node): 8 consecutive targets span a 4x4 footprint
+      // and ~5 z nodes (union ~(P+3)^2 columns x (P+5) nodes)
+      const int n4y = (g.dims[1] + 3) / 4;
+      keys[i] = ((cc[0] >> 2) * n4y + (cc[1] >> 2)) * g.dims[2] + cc[2];
     } else {
       keys[i] = (b[0] * nby + b[1]) * nbz + b[2];
     }
@@ -61,7 +66,7 @@ hs_status launch_grid_keys(hs_ctx* ctx, const double* pos, int n_src, int n, int
   if (n == 0) return HS_OK;
   const int gs = (int)std::min<int64_t>(ceil_div(n, 256), ctx->sm_count * 8);
   k_grid_keys<<<gs, 256, 0, ctx->stream>>>(pos, n_src, n, mode, g, sp_nbins(g, 0), sp_nbins(g, 1), sp_nbins(g, 2),
-                                           keys, ctx->d_flags);
+                                           keys, ctx->d_flags, gather_v5());
   HS_LAUNCHED(ctx);
   return HS_OK;
 }
@@ -1061,8 +1066,267 @@ __global__ void __launch_bounds__(256, 2) k_gather5(const double4* __restrict__ 
   }
 }
 
+// Gather v7 (default).  Targets are sorted by (4x4 (x,y) block, z node) of their window
+// centre and cut into RUNS of <= G7_TG targets of one block whose windows start within
+// 32 - P z nodes of each other, and ITEMS of <= G7_WARPS runs of one block
+// (k_g7_items).  A CTA takes an item, one warp per run; the warp's lanes are 32
+// consecutive z nodes.  The CTA walks the (x,y) columns of the item's union (a (P+3)^2
+// square), staging each column's z-range once through a cp.async ring; every lane takes
+// ITS node of the column (all channels) and accumulates, per target t and channel c,
+//   E_l[t][c] += wx_t(x) wy_t(y) G_c(x, y, z_l)
+// so each shared-memory value feeds G7_TG fused multiply-adds from registers (no
+// broadcast reads).  The z factor is applied once at the end, u_t,c = sum_l wz_t(z_l)
+// E_l[t][c] (warp reduction).  The x/y factors of a run live in warp-private tables.
+// Windows are evaluated directly, exp(-alpha d^2), as in the reference (_gridding.py:21-30).
+constexpr int G7_TG = 8, G7_GW = 32, G7_WARPS = 4, G7_ZC = 96, G7_STEP = 2, G7_R = 3 * G7_STEP;
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+// runs and items of one 4x4 block's targets [b, e) (z-sorted); emit == nullptr: count only
+__device__ int g7_cut(const double4* __restrict__ pts, int b, int e, const GridGeom& g, int4* emit) {
+  int nitem = 0, i = b;
+  while (i < e) {
+    const int ib = i;
+    int nrun = 0;
+    int lens = 0;
+    const int64_t zi0 = window_lo(pts[i].z, g.origin[2], g.h, g.P);
+    while (i < e && nrun < G7_WARPS) {
+      const int64_t zr0 = window_lo(pts[i].z, g.origin[2], g.h, g.P);
+      if (zr0 - zi0 > G7_ZC - g.P) break;
+      int len = 1;
+      ++i;
+      while (i < e && len < G7_TG) {
+        const int64_t z = window_lo(pts[i].z, g.origin[2], g.h, g.P);
+        if (z - zr0 > 32 - g.P || z - zi0 > G7_ZC - g.P) break;
+        ++len;
+        ++i;
+      }
+      lens |= len << (8 * nrun);
+      ++nrun;
+    }
+    if (emit) emit[nitem] = make_int4(ib, i - ib, lens, 0);
+    ++nitem;
+  }
+  return nitem;
+}
+
+__global__ void k_g7_count(const double4* __restrict__ pts, const int* __restrict__ bstart, int nblk, int nz,
+                           GridGeom g, int* __restrict__ cnt) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < nblk; c += gridDim.x * blockDim.x)
+    cnt[c] = g7_cut(pts, bstart[c * nz], bstart[(c + 1) * nz], g, nullptr);
+}
+
+__global__ void k_g7_fill(const double4* __restrict__ pts, const int* __restrict__ bstart, int nblk, int nz,
+                          GridGeom g, const int* __restrict__ istart, int4* __restrict__ items) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < nblk; c += gridDim.x * blockDim.x)
+    g7_cut(pts, bstart[c * nz], bstart[(c + 1) * nz], g, items + istart[c]);
+}
+
+template <int NCH, int PITCH>
+__global__ void __launch_bounds__(G7_WARPS * 32, 2) k_gather7(const double4* __restrict__ pts,
+                                                             const int* __restrict__ orig, const int4* __restrict__ items,
+                                                             const int* __restrict__ n_items_d, GridGeom g,
+                                                             const double* __restrict__ T,
+                                                             double* __restrict__ u_four, double* __restrict__ u_tot,
+                                                             const double* __restrict__ u_real,
+                                                             unsigned* __restrict__ flags) {
+  constexpr int TG = G7_TG, GW = G7_GW, NT = G7_WARPS * 32, CPN = PITCH / 2;  // 16-byte chunks per node
+  __shared__ double s_w[G7_WARPS][2][TG][GW];
+  __shared__ __align__(16) double s_ring[G7_R][G7_ZC * PITCH];
+  __shared__ int s_u[G7_WARPS][6];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int P = g.P;
+  double(*wx_tab)[GW] = s_w[warp][0];
+  double(*wy_tab)[GW] = s_w[warp][1];
+  const int n_items = *n_items_d;
+  for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+    const int4 item = items[it];
+    int rb = item.x;
+#pragma unroll
+    for (int w = 0; w < G7_WARPS; ++w)
+      if (w < warp) rb += (item.z >> (8 * w)) & 0xff;
+    const int rlen = (item.z >> (8 * warp)) & 0xff;
+    const int t = rb + lane;
+    const bool valid = lane < rlen;
+    const double4 pt = pts[valid ? t : item.x];
+    const double pc[3] = {pt.x, pt.y, pt.z};
+    int lo[3];
+    bool bad = false;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const int64_t l = window_lo(pc[k], g.origin[k], g.h, P);
+      bad |= (l < 0) || (l + P > g.dims[k]);
+      lo[k] = (int)l;
+    }
+    if (valid && bad) atomicOr(flags, FLAG_OUT_OF_GRID);
+    const bool act = valid && !bad;
+    const unsigned amask = __ballot_sync(0xffffffffu, act);
+    int W0[3], W1[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      W0[k] = (int)__reduce_min_sync(0xffffffffu, (unsigned)(act ? lo[k] : 0x7fffffff));
+      W1[k] = (int)__reduce_max_sync(0xffffffffu, (unsigned)(act ? lo[k] + P : 0));
+    }
+    __syncthreads();  // previous item done with s_u / ring / tables
+    if (lane == 0) {
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        s_u[warp][k] = amask ? W0[k] : 0x7fffffff;
+        s_u[warp][3 + k] = amask ? W1[k] : (int)0x80000000;
+      }
+    }
+    __syncthreads();
+    int C0[3] = {0x7fffffff, 0x7fffffff, 0x7fffffff}, C1[3] = {(int)0x80000000, (int)0x80000000, (int)0x80000000};
+#pragma unroll
+    for (int w = 0; w < G7_WARPS; ++w)
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        C0[k] = min(C0[k], s_u[w][k]);
+        C1[k] = max(C1[k], s_u[w][3 + k]);
+      }
+    const int nxu = C1[0] - C0[0], nyu = C1[1] - C0[1], nzu = C1[2] - C0[2];
+    // no active target, or (only with out-of-grid targets, an error anyway) limits exceeded
+    if (nxu <= 0 || nxu > GW || nyu > GW || nzu > G7_ZC) continue;
+    double res[NCH];
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) res[c] = 0.0;
+    // x / y window tables of this warp's run (0 outside a target's support)
+#pragma unroll
+    for (int tt = 0; tt < TG; ++tt) {
+      const bool tin = (amask >> tt) & 1u;
+      const double px = __shfl_sync(0xffffffffu, pc[0], tt), py = __shfl_sync(0xffffffffu, pc[1], tt);
+      const int lx = __shfl_sync(0xffffffffu, lo[0], tt), ly = __shfl_sync(0xffffffffu, lo[1], tt);
+      double vx = 0.0, vy = 0.0;
+      const int x = C0[0] + lane, y = C0[1] + lane;
+      if (tin && lane < nxu && x >= lx && x < lx + P) {
+        const double d = window_d(px, g.origin[0], g.h, x);
+        vx = exp(-g.alpha * d * d);
+      }
+      if (tin && lane < nyu && y >= ly && y < ly + P) {
+        const double d = window_d(py, g.origin[1], g.h, y);
+        vy = exp(-g.alpha * d * d);
+      }
+      wx_tab[tt][lane] = vx;
+      wy_tab[tt][lane] = vy;
+    }
+    __syncwarp();
+    const int ncol = nxu * nyu, nchunk = nzu * CPN;
+    // cp.async issue state: this thread's 16-byte chunks k = tid + NT j of every column
+    const double* colp = T + (int64_t)C0[0] * g.stride[0] + (int64_t)C0[1] * g.stride[1] + (int64_t)C0[2] * PITCH +
+                         2 * threadIdx.x;
+    const int64_t row_wrap = g.stride[0] - (int64_t)nyu * g.stride[1];
+    int iy = 0, nissued = 0;
+    auto issue_step = [&](int step) {
+#pragma unroll
+      for (int j = 0; j < G7_STEP; ++j) {
+        if (nissued < ncol) {
+          double* dst = s_ring[(step * G7_STEP + j) % G7_R] + 2 * threadIdx.x;
+#pragma unroll
+          for (int q = 0; q < (G7_ZC * CPN + NT - 1) / NT; ++q)
+            if ((int)threadIdx.x + q * NT < nchunk) cp_async16(dst + 2 * q * NT, colp + 2 * q * NT);
+          ++nissued;
+          colp += g.stride[1];
+          if (++iy == nyu) {
+            iy = 0;
+            colp += row_wrap;
+          }
+        }
+      }
+      cp_async_commit();
+    };
+    issue_step(0);
+    issue_step(1);
+    const int zn = min(W0[2] - C0[2] + lane, nzu - 1);  // this lane's node in the staged column
+    double E[TG][NCH];
+#pragma unroll
+    for (int tt = 0; tt < TG; ++tt)
+#pragma unroll
+      for (int c = 0; c < NCH; ++c) E[tt][c] = 0.0;
+    int cx = 0, cy = 0;
+    const int nstep = (ncol + G7_STEP - 1) / G7_STEP;
+    for (int sidx = 0; sidx < nstep; ++sidx) {
+      cp_async_wait<1>();
+      __syncthreads();
+      issue_step(sidx + 2);
+      if (amask) {
+        // both columns of the step: node values and window factors first, then the FMAs
+        double v[G7_STEP][PITCH], cxy[G7_STEP][TG];
+#pragma unroll
+        for (int j = 0; j < G7_STEP; ++j) {
+          const int ci = sidx * G7_STEP + j;
+          const bool ok = ci < ncol;
+          const double2* src = reinterpret_cast<const double2*>(&s_ring[ci % G7_R][zn * PITCH]);
+#pragma unroll
+          for (int c = 0; c < CPN; ++c) {
+            const double2 q2 = ok ? src[c] : make_double2(0.0, 0.0);  // (unissued slots hold stale bits)
+            v[j][2 * c] = q2.x;
+            v[j][2 * c + 1] = q2.y;
+          }
+#pragma unroll
+          for (int tt = 0; tt < TG; ++tt) cxy[j][tt] = ok ? wx_tab[tt][cx] * wy_tab[tt][cy] : 0.0;
+          if (++cy == nyu) {
+            cy = 0;
+            ++cx;
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < G7_STEP; ++j)
+#pragma unroll
+          for (int tt = 0; tt < TG; ++tt)
+#pragma unroll
+            for (int c = 0; c < NCH; ++c) E[tt][c] = fma(cxy[j][tt], v[j][c], E[tt][c]);
+      }
+    }
+    cp_async_wait<0>();
+    if (amask) {
+      // z factors of this lane's node, reduce over the warp; lane t accumulates target t
+      const int z = W0[2] + lane;
+#pragma unroll
+      for (int tt = 0; tt < TG; ++tt) {
+        const double pz = __shfl_sync(0xffffffffu, pc[2], tt);
+        const int lz = __shfl_sync(0xffffffffu, lo[2], tt);
+        double wz = 0.0;
+        if (((amask >> tt) & 1u) && z >= lz && z < lz + P) {
+          const double d = window_d(pz, g.origin[2], g.h, z);
+          wz = exp(-g.alpha * d * d);
+        }
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) {
+          const double sum = warp_sum(wz * E[tt][c]);
+          if (lane == tt) res[c] = sum;
+        }
+      }
+    }
+    if (act) {
+      const int o = orig[t];
+      const double h3p = g.h * g.h * g.h * g.pref;
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        double v = res[k] * h3p;
+        if (NCH == 6) v -= pt.z * (res[3 + k] * h3p);
+        if (u_four) u_four[3 * (size_t)o + k] = v;
+        if (u_tot) u_tot[3 * (size_t)o + k] = (u_real ? u_real[3 * (size_t)o + k] : 0.0) + v;
+      }
+    }
+  }
+}
+
+bool gather_v5() {
+  static const bool v5 = getenv("HS_GATHER_V5") != nullptr;  // previous default (comparison)
+  return v5;
+}
+
 hs_status launch_gather_fourier(hs_ctx* ctx, const double4* pts, const int* orig, int n, int half, const GridGeom& g,
-                                const double* T, double* u_fourier, double* u_total, const double* u_real) {
+                                const double* T, double* u_fourier, double* u_total, const double* u_real,
+                                const int* bstart) {
   if (n == 0) return HS_OK;
   static const bool v1 = getenv("HS_GATHER_V1") != nullptr;  // debugging aid: warp-per-target gather
   if (v1) {
@@ -1078,6 +1342,34 @@ hs_status launch_gather_fourier(hs_ctx* ctx, const double4* pts, const int* orig
   }
   if (g.P > GA_ZM) return fail(HS_ERR_PARAMETER, "window support P > 32 is not supported by the gather");
   static const bool v3 = getenv("HS_GATHER_V3") != nullptr;  // CTA-staged variant (comparison)
+  if (!v3 && !gather_v5()) {
+    if (!bstart) return fail(HS_ERR_PARAMETER, "gather v7 needs the block order");
+    if (g.P > 32 || g.P > G7_ZC) return fail(HS_ERR_PARAMETER, "window support P > 32 is not supported by the gather");
+    // items (worst case one per target): count per 4x4 block, scan, fill
+    const int nb4 = ((g.dims[0] + 3) / 4) * ((g.dims[1] + 3) / 4);
+    void* scr = nullptr;
+    const size_t bytes = sizeof(int4) * (size_t)n + sizeof(int) * (3 * (size_t)nb4 + 8);
+    HS_TRY(ctx_scratch(ctx, bytes, &scr));
+    int4* items = (int4*)scr;
+    int* cnt = (int*)(items + n);
+    int* istart = cnt + nb4;  // nb4 + 1
+    int* sc = istart + nb4 + 1;
+    const int gsb = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(nb4, 128), ctx->sm_count * 4));
+    k_g7_count<<<gsb, 128, 0, ctx->stream>>>(pts, bstart, nb4, g.dims[2], g, cnt);
+    HS_LAUNCHED(ctx);
+    HS_TRY(exclusive_scan(ctx, cnt, nb4, istart, sc));
+    k_g7_fill<<<gsb, 128, 0, ctx->stream>>>(pts, bstart, nb4, g.dims[2], g, istart, items);
+    HS_LAUNCHED(ctx);
+    const int gs7 = (int)std::min<int64_t>(n, (int64_t)ctx->sm_count * 2);
+    if (half)
+      k_gather7<6, 6><<<gs7, G7_WARPS * 32, 0, ctx->stream>>>(pts, orig, items, istart + nb4, g, T, u_fourier,
+                                                             u_total, u_real, ctx->d_flags);
+    else
+      k_gather7<3, 4><<<gs7, G7_WARPS * 32, 0, ctx->stream>>>(pts, orig, items, istart + nb4, g, T, u_fourier,
+                                                             u_total, u_real, ctx->d_flags);
+    HS_LAUNCHED(ctx);
+    return HS_OK;
+  }
   if (!v3) {
     const int gs5 = (int)std::min<int64_t>(ceil_div(n, 256), (int64_t)ctx->sm_count * 32);
     if (half)

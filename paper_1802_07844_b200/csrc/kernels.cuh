@@ -36,8 +36,12 @@ struct GridGeom {
   int64_t ch_stride;       // element stride between channels
 };
 constexpr int SP_TX = 16, SP_TY = 16, SP_TZ = 8;  // spread tile / bin shape
-// gather target order: (8x8 (x,y) column, z cell) of the window-centre cell
-inline int gather_keys(const GridGeom& g) { return ((g.dims[0] + 7) / 8) * ((g.dims[1] + 7) / 8) * g.dims[2]; }
+// gather target order: (4x4 (x,y) column, z node) of the window-centre node (v5: 8x8 columns)
+bool gather_v5();
+inline int gather_keys(const GridGeom& g) {
+  if (gather_v5()) return ((g.dims[0] + 7) / 8) * ((g.dims[1] + 7) / 8) * g.dims[2];
+  return ((g.dims[0] + 3) / 4) * ((g.dims[1] + 3) / 4) * g.dims[2];
+}
 inline int sp_nbins(const GridGeom& g, int k) {
   const int t[3] = {SP_TX, SP_TY, SP_TZ};
   return (int)ceil_div(g.dims[k], t[k]);
@@ -55,9 +59,10 @@ hs_status launch_spread(hs_ctx* ctx, const double4* pts, const double* w, int n,
 hs_status launch_gather(hs_ctx* ctx, const double4* pts, const int* perm, int n, int nch,
                         const GridGeom& g, const double* grids, double* out, int ldo, double scale);
 // half-space Fourier gather: u[orig] (+)= h^3 (T1 . w - x3 T2 . w) (ewald_fourier.py:626-630)
+// bstart: start of every gather-order key (the (4x4 block, z node) sort of the targets)
 hs_status launch_gather_fourier(hs_ctx* ctx, const double4* pts, const int* orig, int n, int half,
                                 const GridGeom& g, const double* T, double* u_fourier, double* u_total,
-                                const double* u_real);
+                                const double* u_real, const int* bstart);
 
 // ---------------------------------------------------------------------------
 // real space (pair.cu)

@@ -806,7 +806,7 @@ extern "C" hs_status hs_plan_execute(hs_plan* p, const double* positions, const 
       HS_LAUNCHED(ctx);
       HS_CUDA(cudaEventRecord(ev[13], st));
       HS_TRY(launch_gather_fourier(ctx, p->TG, p->tg_orig, nt, p->half ? 1 : 0, p->go, p->grid_out, p->u_four, p->u,
-                                   p->u_real));
+                                   p->u_real, p->bt_start));
       HS_CUDA(cudaEventRecord(ev[14], st));
       gather_timed = true;
     }
