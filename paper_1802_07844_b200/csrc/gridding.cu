@@ -1250,40 +1250,44 @@ __global__ void __launch_bounds__(G7_WARPS * 32, 2) k_gather7(const double4* __r
     for (int tt = 0; tt < TG; ++tt)
 #pragma unroll
       for (int c = 0; c < NCH; ++c) E[tt][c] = 0.0;
-    int cx = 0, cy = 0;
-    const int nstep = (ncol + G7_STEP - 1) / G7_STEP;
-    for (int sidx = 0; sidx < nstep; ++sidx) {
+    int cx = 0, cy = 0, slot = 0;
+    // one column: node values and window factors, then the FMAs
+    auto column = [&](int sl) {
+      const double2* src = reinterpret_cast<const double2*>(&s_ring[sl][zn * PITCH]);
+      double v[PITCH], cxy[TG];
+#pragma unroll
+      for (int c = 0; c < CPN; ++c) {
+        const double2 q2 = src[c];
+        v[2 * c] = q2.x;
+        v[2 * c + 1] = q2.y;
+      }
+#pragma unroll
+      for (int tt = 0; tt < TG; ++tt) cxy[tt] = wx_tab[tt][cx] * wy_tab[tt][cy];
+      if (++cy == nyu) {
+        cy = 0;
+        ++cx;
+      }
+#pragma unroll
+      for (int tt = 0; tt < TG; ++tt)
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) E[tt][c] = fma(cxy[tt], v[c], E[tt][c]);
+    };
+    static_assert(G7_STEP == 2, "the step loop below handles two columns");
+    const int nfull = ncol / G7_STEP;
+    for (int sidx = 0; sidx < nfull; ++sidx) {
       cp_async_wait<1>();
       __syncthreads();
       issue_step(sidx + 2);
       if (amask) {
-        // both columns of the step: node values and window factors first, then the FMAs
-        double v[G7_STEP][PITCH], cxy[G7_STEP][TG];
-#pragma unroll
-        for (int j = 0; j < G7_STEP; ++j) {
-          const int ci = sidx * G7_STEP + j;
-          const bool ok = ci < ncol;
-          const double2* src = reinterpret_cast<const double2*>(&s_ring[ci % G7_R][zn * PITCH]);
-#pragma unroll
-          for (int c = 0; c < CPN; ++c) {
-            const double2 q2 = ok ? src[c] : make_double2(0.0, 0.0);  // (unissued slots hold stale bits)
-            v[j][2 * c] = q2.x;
-            v[j][2 * c + 1] = q2.y;
-          }
-#pragma unroll
-          for (int tt = 0; tt < TG; ++tt) cxy[j][tt] = ok ? wx_tab[tt][cx] * wy_tab[tt][cy] : 0.0;
-          if (++cy == nyu) {
-            cy = 0;
-            ++cx;
-          }
-        }
-#pragma unroll
-        for (int j = 0; j < G7_STEP; ++j)
-#pragma unroll
-          for (int tt = 0; tt < TG; ++tt)
-#pragma unroll
-            for (int c = 0; c < NCH; ++c) E[tt][c] = fma(cxy[j][tt], v[j][c], E[tt][c]);
+        column(slot);
+        column(slot + 1);
       }
+      slot = slot + 2 == G7_R ? 0 : slot + 2;
+    }
+    if (ncol & 1) {  // ragged last step: one column (already issued)
+      cp_async_wait<1>();
+      __syncthreads();
+      if (amask) column(slot);
     }
     cp_async_wait<0>();
     if (amask) {
