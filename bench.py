@@ -45,8 +45,8 @@ def _peaks():
         src = "MEASURED_PEAKS.json"
     if os.path.exists(FP64_PEAK_SOURCE):
         d = json.load(open(FP64_PEAK_SOURCE))
-        fp64 = max(d["dfma_tflops"], d["dmma_tflops"])
-    return hbm, fp64 or 37.0, src
+        fp64 = {"dfma": d["dfma_tflops"], "dmma": d["dmma_tflops"]}
+    return hbm, fp64 or {"dfma": 33.9, "dmma": 37.1}, src
 
 
 # ---------------------------------------------------------------------------
@@ -189,9 +189,10 @@ def roofline(times, work, hbm_peak, fp64_peak):
             ks[name] = {"bound": "hbm", "achieved": ach, "peak": hbm_peak, "unit": "GB/s", "frac": ach / hbm_peak,
                         "ms": t, "algorithmic": amount}
         else:
+            pk = fp64_peak[bound.split(":")[1]]  # "fp64:dfma" (FP64 FMA pipe) or "fp64:dmma" (FP64 tensor pipe)
             ach = amount / (t * 1e-3) / 1e12
-            ks[name] = {"bound": "fp64", "achieved": ach, "peak": fp64_peak, "unit": "TFLOP/s",
-                        "frac": ach / fp64_peak, "ms": t, "algorithmic": amount}
+            ks[name] = {"bound": "fp64", "pipe": bound.split(":")[1], "achieved": ach, "peak": pk,
+                        "unit": "TFLOP/s", "frac": ach / pk, "ms": t, "algorithmic": amount}
     return ks
 
 
@@ -309,10 +310,10 @@ def run_ours(args, rank, world, local_rank):
     n_half = grid.padded_dims[0] * grid.padded_dims[1] * (grid.padded_dims[2] // 2 + 1)
     pairs, img_pairs = avg["pairs"], avg["image_pairs"]
     work = {
-        "k_spread": ("flop", 2.0 * P3 * (2 * s.n * 3 + s.n * 4), "fp64"),
-        "k_gather": ("flop", 2.0 * P3 * 6 * s.n, "fp64"),
+        "k_spread": ("flop", 2.0 * P3 * (2 * s.n * 3 + s.n * 4), "fp64:dmma"),
+        "k_gather": ("flop", 2.0 * P3 * 6 * s.n, "fp64:dfma"),
         "k_scale": ("bytes", n_half * (16 * 7 + 16 * 6 + 8 * 2), "hbm"),
-        "k_pair": ("flop", 2.0 * (64 * pairs + 33 * img_pairs), "fp64"),
+        "k_pair": ("flop", 2.0 * (64 * pairs + 33 * img_pairs), "fp64:dfma"),
     }
     kern = roofline(avg, work, hbm_peak, fp64_peak)
     dom = max(kern, key=lambda k: kern[k]["ms"])
@@ -323,7 +324,7 @@ def run_ours(args, rank, world, local_rank):
     rf = dict(kern[dom])
     rf.update({"kernel": dom, "traffic": traffic, "peak_source": (
         "MEASURED_PEAKS.json hbm_gbs" if rf["bound"] == "hbm" else
-        "measured FP64 DMMA/DFMA microbenchmark, profiles/r01_probe_fp64.json")})
+        f"measured FP64 {rf['pipe'].upper()} microbenchmark, profiles/r01_probe_fp64.json")})
 
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
