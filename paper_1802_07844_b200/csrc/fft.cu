@@ -234,6 +234,13 @@ __device__ __noinline__ void scale_nyquist(double2* col, int cstride, int kx, in
 
 constexpr int XF_THREADS = 256;  // 2 CTAs per SM: one CTA's loads overlap the other's FFTs
 
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+
 template <int KIND, bool HALF, int KB, class FFT>
 __global__ void __launch_bounds__(XF_THREADS, 2) k_xfused(const XArgs a) {
   constexpr int NIN = KChan<KIND, HALF>::NIN, NOUT = KChan<KIND, HALF>::NOUT;
@@ -253,27 +260,24 @@ __global__ void __launch_bounds__(XF_THREADS, 2) k_xfused(const XArgs a) {
     const int kz0 = (item % nkb) * KB;
     const int kbn = min(KB, a.nzh - kz0);
     __syncthreads();
-    // load the nx nonzero x-values of every channel, zero-extend to px
-    for (int i = tid; i < NIN * px; i += blockDim.x) {
-      const int c = i / px, x = i - c * px;
-      double2 v[KB];
+    // load the nx nonzero x-values of every channel (cp.async, all in flight at once),
+    // zero-extend to px
+#pragma unroll 1
+    for (int c = 0; c < NIN; ++c) {
+      const double2* src = a.B + c * a.ch_stride + (int64_t)ky * a.nx * a.nzh + kz0;
+      for (int x = tid; x < px; x += blockDim.x) {
 #pragma unroll
-      for (int kb = 0; kb < KB; ++kb) v[kb] = make_double2(0.0, 0.0);
-      if (x < a.nx) {
-        const double2* src = a.B + c * a.ch_stride + ((int64_t)ky * a.nx + x) * a.nzh + kz0;
-        if (KB == 2 && kbn == 2) {
-          const double4 w = *reinterpret_cast<const double4*>(src);
-          v[0] = make_double2(w.x, w.y);
-          v[KB - 1] = make_double2(w.z, w.w);
-        } else {
-#pragma unroll
-          for (int kb = 0; kb < KB; ++kb)
-            if (kb < kbn) v[kb] = src[kb];
+        for (int kb = 0; kb < KB; ++kb) {
+          double2* dst = &lines[(c * KB + kb) * LS + pd8(x)];
+          if (x < a.nx && kb < kbn)
+            cp_async16(dst, src + (int64_t)x * a.nzh + kb);
+          else
+            *dst = make_double2(0.0, 0.0);
         }
       }
-#pragma unroll
-      for (int kb = 0; kb < KB; ++kb) lines[(c * KB + kb) * LS + pd8(x)] = v[kb];
     }
+    cp_async_commit();
+    cp_async_wait_all();
     __syncthreads();
     for (int l = warp; l < NIN * KB; l += blockDim.x / 32) FFT::run(lines + l * LS, a.plan, tw, lane);
     __syncthreads();
