@@ -293,6 +293,315 @@ __device__ __forceinline__ void dmma_884(double& c0, double& c1, double a, doubl
                : "d"(a), "d"(b));
 }
 
+// ---------------------------------------------------------------------------
+// Spread v3 (default): the DMMA accumulation of k_spread_mma, with the per-tile staging
+// replaced by asynchronous copies.  k_spread_wtab evaluates every source's full window
+// once (exp(-alpha d^2) per node, _gridding.py:21-30; the normalisation folded into the
+// x factor) into zero-padded rows; a tile then copies (cp.async, 16-byte chunks) the
+// slices it needs into a double-buffered shared-memory chunk while the warps accumulate
+// the previous chunk -- one barrier per chunk, no window arithmetic in the tile loop.
+struct WTab {                              // row layout of one source (doubles)
+  int wx, wy, wz, stride;                  // padded row lengths and their sum
+  __host__ __device__ static WTab make(int P) {
+    WTab t;
+    t.wx = (2 * SP_TX + P + 1) & ~1;
+    t.wy = (2 * SP_TY + P + 1) & ~1;
+    t.wz = (2 * SP_TZ + P + 1) & ~1;
+    t.stride = t.wx + t.wy + t.wz;
+    return t;
+  }
+};
+
+__global__ void k_spread_wtab(const double4* __restrict__ pts, int n, GridGeom g, WTab wt, int4* __restrict__ lo,
+                              double* __restrict__ tab) {
+  // one warp per (source, axis) row; lanes write consecutive entries (coalesced)
+  const int P = g.P;
+  const int lane = threadIdx.x & 31;
+  const int64_t nrow = (int64_t)n * 3;
+  for (int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; r < nrow;
+       r += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int s = (int)(r / 3), k = (int)(r - 3 * (int64_t)s);
+    const double4 p = pts[s];
+    const double pc = k == 0 ? p.x : (k == 1 ? p.y : p.z);
+    const int64_t l = window_lo(pc, g.origin[k], g.h, P);
+    const int pad = k == 0 ? SP_TX : (k == 1 ? SP_TY : SP_TZ);
+    const int len = k == 0 ? wt.wx : (k == 1 ? wt.wy : wt.wz);
+    double* row = tab + (int64_t)s * wt.stride + (k == 0 ? 0 : (k == 1 ? wt.wx : wt.wx + wt.wy));
+    const double scale = k == 0 ? g.pref : 1.0;
+    for (int j = lane; j < len; j += 32) {
+      const int a = j - pad;
+      double v = 0.0;
+      if (a >= 0 && a < P) {
+        const double d = window_d(pc, g.origin[k], g.h, l + a);
+        v = scale * exp(-g.alpha * d * d);
+      }
+      row[j] = v;
+    }
+    if (k == 0 && lane == 0)
+      lo[s] = make_int4((int)l, (int)window_lo(p.y, g.origin[1], g.h, P), (int)window_lo(p.z, g.origin[2], g.h, P), 0);
+  }
+}
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "HS_WAIT_%=:\n"
+      " mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra HS_WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// bulk global -> shared copy (16-byte aligned, size a multiple of 16) completing on `bar`
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void cpa16(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cpa8(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem));
+}
+
+// Warp-specialised pipeline: warp 8 produces chunks of SW_CH candidate sources into a
+// ring of SW_K shared-memory buffers (hit masks, slice parities and weights by plain
+// stores; the x / y / z window slices by bulk asynchronous copies from the window table,
+// completing on the buffer's `full` mbarrier), warps 0-7 consume them (DMMA) and release
+// the buffer on its `empty` mbarrier.  Consumers never wait for staging and may run up
+// to SW_K chunks ahead of each other, so per-chunk load imbalance averages out.
+constexpr int SW_CH = 64, SW_K = 4, SW_RX = SP_TX + 2, SW_RY = SP_TY + 2, SW_RZ = SP_TZ + 2;
+template <int NCH>
+struct SwBuf {
+  static constexpr int RQ = NCH | 1;
+  static constexpr int DOUBLES = SW_CH * (SW_RX + SW_RY + SW_RZ + RQ + 1);
+};
+
+template <int NCH>
+__global__ void __launch_bounds__(288, 2) k_spread_mma4(const int4* __restrict__ lo4, const double* __restrict__ tab,
+                                                       WTab wt, const double* __restrict__ w, int ldw,
+                                                       const int* __restrict__ bin_start, GridGeom g, int nbx,
+                                                       int nby, int nbz, double* __restrict__ grids) {
+  constexpr int RX = SW_RX, RY = SW_RY, RZ = SW_RZ, RQ = SwBuf<NCH>::RQ, PER = SwBuf<NCH>::DOUBLES;
+  extern __shared__ __align__(16) double sm_dyn[];
+  __shared__ __align__(8) uint64_t full_bar[SW_K], empty_bar[SW_K];
+  __shared__ int run_beg[9], run_pre[10];
+  __shared__ int s_nrun;
+  auto bx_ = [&](int b) { return reinterpret_cast<double(*)[RX]>(sm_dyn + b * PER); };
+  auto by_ = [&](int b) { return reinterpret_cast<double(*)[RY]>(sm_dyn + b * PER + SW_CH * RX); };
+  auto bz_ = [&](int b) { return reinterpret_cast<double(*)[RZ]>(sm_dyn + b * PER + SW_CH * (RX + RY)); };
+  auto bq_ = [&](int b) { return reinterpret_cast<double(*)[RQ]>(sm_dyn + b * PER + SW_CH * (RX + RY + RZ)); };
+  auto bm_ = [&](int b) { return reinterpret_cast<unsigned*>(sm_dyn + b * PER + SW_CH * (RX + RY + RZ + RQ)); };
+
+  const int tz = blockIdx.x % nbz;
+  const int ty = (blockIdx.x / nbz) % nby;
+  const int tx = blockIdx.x / (nbz * nby);
+  const int x0 = tx * SP_TX, y0 = ty * SP_TY, z0 = tz * SP_TZ;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int P = g.P;
+
+  if (threadIdx.x == 0) {
+    int nr = 0, tot = 0;
+    const int zlo = max(tz - 2, 0), zhi = min(tz + 2, nbz - 1);
+    for (int bx = max(tx - 1, 0); bx <= min(tx + 1, nbx - 1); ++bx)
+      for (int by = max(ty - 1, 0); by <= min(ty + 1, nby - 1); ++by) {
+        const int f = (bx * nby + by) * nbz;
+        const int b = bin_start[f + zlo], e = bin_start[f + zhi + 1];
+        if (e > b) {
+          run_beg[nr] = b;
+          run_pre[nr] = tot;
+          tot += e - b;
+          ++nr;
+        }
+      }
+    run_pre[nr] = tot;
+    s_nrun = nr;
+#pragma unroll
+    for (int k = 0; k < SW_K; ++k) {
+      mbar_init(&full_bar[k], 64);    // producer lanes: stores released + their cp.async completed
+      mbar_init(&empty_bar[k], 256);  // every consumer thread
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  const int nrun = s_nrun, ncand = run_pre[nrun];
+  const int nchunk = (ncand + SW_CH - 1) / SW_CH;
+
+  if (warp == 8) {
+    // ---------------- producer ----------------
+    int4 lo_n[2];
+    double q_n[2][NCH];
+    int row_n[2];
+    auto fetch = [&](int c) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int v = c * SW_CH + lane + 32 * h;
+        row_n[h] = -1;
+        if (c < nchunk && v < ncand) {
+          int r = 0;
+          while (r + 1 < nrun && run_pre[r + 1] <= v) ++r;
+          const int row = run_beg[r] + (v - run_pre[r]);
+          row_n[h] = row;
+          lo_n[h] = lo4[row];
+#pragma unroll
+          for (int ch = 0; ch < NCH; ++ch) q_n[h][ch] = w[(int64_t)row * ldw + ch];
+        }
+      }
+    };
+    fetch(0);
+    for (int c = 0; c < nchunk; ++c) {
+      const int b = c % SW_K;
+      int4 lo_c[2] = {lo_n[0], lo_n[1]};
+      int row_c[2] = {row_n[0], row_n[1]};
+      double q_c[2][NCH];
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int ch = 0; ch < NCH; ++ch) q_c[h][ch] = q_n[h][ch];
+      fetch(c + 1);  // next chunk's rows in flight while this one is staged
+      if (c >= SW_K) mbar_wait(&empty_bar[b], ((c / SW_K) - 1) & 1);
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      unsigned bytes = 0, m[2] = {0u, 0u};
+      int ex[2], ey[2], ez[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int sl = lane + 32 * h;
+        if (row_c[h] >= 0) {
+          const int4 l = lo_c[h];
+          if (l.z < z0 + SP_TZ && l.z + P > z0) {
+#pragma unroll
+            for (int wq = 0; wq < 8; ++wq) {
+              const int px = x0 + (wq & 3) * 4, py = y0 + (wq >> 2) * 8;
+              if (l.x < px + 4 && l.x + P > px && l.y < py + 8 && l.y + P > py) m[h] |= 1u << wq;
+            }
+          }
+          ex[h] = SP_TX + (x0 - l.x);
+          ey[h] = SP_TY + (y0 - l.y);
+          ez[h] = SP_TZ + (z0 - l.z);
+          if (m[h]) {
+            bytes += 8u * (RX + RY + RZ);
+#pragma unroll
+            for (int ch = 0; ch < NCH; ++ch) bq_(b)[sl][ch] = q_c[h][ch];
+          }
+        }
+        bm_(b)[sl] = m[h] | (m[h] ? ((unsigned)(ex[h] & 1) << 8) | ((unsigned)(ey[h] & 1) << 9) |
+                                        ((unsigned)(ez[h] & 1) << 10)
+                                  : 0u);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) bytes += __shfl_xor_sync(0xffffffffu, bytes, o);
+      (void)bytes;
+      mbar_arrive(&full_bar[b]);  // masks / weights (plain stores) released
+      // window slices: 16-byte cp.async chunks, completion tracked by the same barrier
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        if (m[h]) {
+          const int sl = lane + 32 * h;
+          const double* src = tab + (int64_t)row_c[h] * wt.stride;
+          const double* sx = src + (ex[h] & ~1);
+          const double* sy = src + wt.wx + (ey[h] & ~1);
+          const double* sz = src + wt.wx + wt.wy + (ez[h] & ~1);
+#pragma unroll
+          for (int j = 0; j < RX / 2; ++j) cpa16(&bx_(b)[sl][2 * j], sx + 2 * j);
+#pragma unroll
+          for (int j = 0; j < RY / 2; ++j) cpa16(&by_(b)[sl][2 * j], sy + 2 * j);
+#pragma unroll
+          for (int j = 0; j < RZ / 2; ++j) cpa16(&bz_(b)[sl][2 * j], sz + 2 * j);
+        }
+      }
+      asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(&full_bar[b])) : "memory");
+    }
+    return;
+  }
+
+  // ---------------- consumers (warps 0-7) ----------------
+  const int wx0 = (warp & 3) * 4, wy0 = (warp >> 2) * 8;  // warp patch origin inside the tile
+  const int kq = lane & 3;   // k index (source slot) of this lane's A and B fragments
+  const int rq = lane >> 2;  // A row / B column / C row of this lane
+  double acc[4][NCH][2];
+#pragma unroll
+  for (int rb = 0; rb < 4; ++rb)
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) acc[rb][c][0] = acc[rb][c][1] = 0.0;
+  for (int c = 0; c < nchunk; ++c) {
+    const int b = c % SW_K;
+    const int nc = min(SW_CH, ncand - c * SW_CH);
+    mbar_wait(&full_bar[b], (c / SW_K) & 1);
+    double(*s_wx)[RX] = bx_(b);
+    double(*s_wy)[RY] = by_(b);
+    double(*s_wz)[RZ] = bz_(b);
+    double(*s_q)[RQ] = bq_(b);
+    const unsigned* s_mask = bm_(b);
+    for (int base = 0; base < nc; base += 32) {
+      const unsigned mk = base + lane < nc ? s_mask[base + lane] : 0u;
+      unsigned m = __ballot_sync(0xffffffffu, (mk >> warp) & 1u);
+      while (m) {
+        int sk = -1;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int sb = m ? base + __ffs(m) - 1 : -1;
+          if (m) m &= m - 1;
+          if (k == kq) sk = sb;
+        }
+        double bz = 0.0, q[NCH], cxy[4];
+#pragma unroll
+        for (int ch = 0; ch < NCH; ++ch) q[ch] = 0.0;
+#pragma unroll
+        for (int rb = 0; rb < 4; ++rb) cxy[rb] = 0.0;
+        if (sk >= 0) {
+          const unsigned par = s_mask[sk];
+          const int pxo = (par >> 8) & 1, pyo = (par >> 9) & 1, pzo = (par >> 10) & 1;
+          bz = s_wz[sk][pzo + rq];  // B[k][n] = wz_{s_k}(z_n), n = rq
+#pragma unroll
+          for (int ch = 0; ch < NCH; ++ch) q[ch] = s_q[sk][ch];
+#pragma unroll
+          for (int rb = 0; rb < 4; ++rb) {
+            const int p = rb * 8 + rq;  // position of A row rq in row block rb
+            cxy[rb] = s_wx[sk][pxo + wx0 + (p & 3)] * s_wy[sk][pyo + wy0 + (p >> 2)];
+          }
+        }
+#pragma unroll
+        for (int rb = 0; rb < 4; ++rb)
+#pragma unroll
+          for (int ch = 0; ch < NCH; ++ch) dmma_884(acc[rb][ch][0], acc[rb][ch][1], cxy[rb] * q[ch], bz);
+      }
+    }
+    mbar_arrive(&empty_bar[b]);
+  }
+  // C fragment: row rq of row block rb = position p, columns z = 2 kq, 2 kq + 1
+#pragma unroll
+  for (int rb = 0; rb < 4; ++rb) {
+    const int p = rb * 8 + rq;
+    const int x = x0 + wx0 + (p & 3), y = y0 + wy0 + (p >> 2);
+    if (x < g.dims[0] && y < g.dims[1]) {
+#pragma unroll
+      for (int c = 0; c < NCH; ++c) {
+        double* dst = grids + c * g.ch_stride + x * g.stride[0] + y * g.stride[1];
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const int z = z0 + 2 * kq + i;
+          if (z < g.dims[2]) dst[z * g.stride[2]] = acc[rb][c][i];
+        }
+      }
+    }
+  }
+}
+
 template <int NCH, int CH>
 __global__ void __launch_bounds__(256, 2) k_spread_mma(const int4* __restrict__ lo4, const double4* __restrict__ wxy,
                                                       const double2* __restrict__ wzp, const double* __restrict__ w,
@@ -570,6 +879,40 @@ hs_status launch_spread(hs_ctx* ctx, const double4* pts, const double* w, int n,
                         const GridGeom& g, double* grids) {
   if (g.P > SP_MAXP) return fail(HS_ERR_PARAMETER, "spread supports window support P <= 64");
   const int nbx = sp_nbins(g, 0), nby = sp_nbins(g, 1), nbz = sp_nbins(g, 2);
+  // default: v3 (window tables + cp.async staging + DMMA); HS_SPREAD_V0 = DMMA with in-tile window
+  // arithmetic, HS_SPREAD_V1 = scalar DFMA, HS_SPREAD_V2 = warp-independent (comparison only)
+  static const int variant = getenv("HS_SPREAD_V0") ? 0 : getenv("HS_SPREAD_V1") ? 1 : getenv("HS_SPREAD_V2") ? 2 : 3;
+  if (variant == 3) {
+    const WTab wt = WTab::make(g.P);
+    void* scr3 = nullptr;
+    const size_t nn = (size_t)std::max(n, 1);
+    HS_TRY(ctx_scratch(ctx, nn * (sizeof(int4) + sizeof(double) * wt.stride), &scr3));
+    int4* lo = (int4*)scr3;
+    double* tab = (double*)(lo + nn);
+    if (n > 0) {
+      const int gs = (int)std::min<int64_t>(ceil_div((int64_t)n * 3 * 32, 256), ctx->sm_count * 16);
+      k_spread_wtab<<<gs, 256, 0, ctx->stream>>>(pts, n, g, wt, lo, tab);
+      HS_LAUNCHED(ctx);
+    }
+    dim3 grid(nbx * nby * nbz), block(256);
+    for (int c0 = 0; c0 < nch; c0 += SP_MAXCH) {
+      const int cn = std::min(SP_MAXCH, nch - c0);
+      double* gout = grids + (size_t)c0 * g.ch_stride;
+      const double* wc0 = w + c0;
+      switch (cn) {
+#define HS_SP3(N)                                                                                                    \
+  case N: {                                                                                                          \
+    const size_t smm = sizeof(double) * SW_K * SwBuf<N>::DOUBLES;                                                    \
+    HS_CUDA(cudaFuncSetAttribute(k_spread_mma4<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smm));          \
+    k_spread_mma4<N><<<grid, 288, smm, ctx->stream>>>(lo, tab, wt, wc0, nch, bin_start, g, nbx, nby, nbz, gout);    \
+  } break;
+        HS_SP3(1) HS_SP3(2) HS_SP3(3) HS_SP3(4)
+#undef HS_SP3
+      }
+      HS_LAUNCHED(ctx);
+    }
+    return HS_OK;
+  }
   void* scr = nullptr;
   const size_t per = sizeof(int4) + sizeof(double4) + sizeof(double2);
   HS_TRY(ctx_scratch(ctx, per * (size_t)std::max(n, 1), &scr));
@@ -588,8 +931,6 @@ hs_status launch_spread(hs_ctx* ctx, const double4* pts, const double* w, int n,
     const int cn = std::min(SP_MAXCH, nch - c0);
     double* gout = grids + (size_t)c0 * g.ch_stride;
     const double* wc0 = w + c0;
-    // default: DMMA tensor-core accumulation; HS_SPREAD_V1 = scalar DFMA, HS_SPREAD_V2 = warp-independent
-    static const int variant = getenv("HS_SPREAD_V1") ? 1 : (getenv("HS_SPREAD_V2") ? 2 : 0);
     switch (cn) {
 #define HS_SP(N)                                                                                              \
   case N:                                                                                                     \
