@@ -444,45 +444,46 @@ __global__ void __launch_bounds__(288, 2) k_spread_mma4(const int4* __restrict__
 
   if (warp == 8) {
     // ---------------- producer ----------------
-    int4 lo_n[2];
-    double q_n[2][NCH];
-    int row_n[2];
-    auto fetch = [&](int c) {
+    // rows / windows starts / weights of chunk c+1 and c+2 are in flight (registers) while
+    // chunk c is staged, so the producer runs at one chunk per staging pass, not per load latency
+    struct Pre {
+      int4 lo[2];
+      int row[2];
+      double q[2][NCH];
+    };
+    auto fetch = [&](int c, Pre& f) {
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int v = c * SW_CH + lane + 32 * h;
-        row_n[h] = -1;
+        f.row[h] = -1;
         if (c < nchunk && v < ncand) {
           int r = 0;
           while (r + 1 < nrun && run_pre[r + 1] <= v) ++r;
           const int row = run_beg[r] + (v - run_pre[r]);
-          row_n[h] = row;
-          lo_n[h] = lo4[row];
+          f.row[h] = row;
+          f.lo[h] = lo4[row];
 #pragma unroll
-          for (int ch = 0; ch < NCH; ++ch) q_n[h][ch] = w[(int64_t)row * ldw + ch];
+          for (int ch = 0; ch < NCH; ++ch) f.q[h][ch] = w[(int64_t)row * ldw + ch];
         }
       }
     };
-    fetch(0);
+    Pre f1, f2;
+    fetch(0, f1);
+    fetch(1, f2);
     for (int c = 0; c < nchunk; ++c) {
       const int b = c % SW_K;
-      int4 lo_c[2] = {lo_n[0], lo_n[1]};
-      int row_c[2] = {row_n[0], row_n[1]};
-      double q_c[2][NCH];
-#pragma unroll
-      for (int h = 0; h < 2; ++h)
-#pragma unroll
-        for (int ch = 0; ch < NCH; ++ch) q_c[h][ch] = q_n[h][ch];
-      fetch(c + 1);  // next chunk's rows in flight while this one is staged
+      const Pre cur = f1;
+      f1 = f2;
+      fetch(c + 2, f2);
       if (c >= SW_K) mbar_wait(&empty_bar[b], ((c / SW_K) - 1) & 1);
-      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-      unsigned bytes = 0, m[2] = {0u, 0u};
+      unsigned m[2] = {0u, 0u};
       int ex[2], ey[2], ez[2];
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int sl = lane + 32 * h;
-        if (row_c[h] >= 0) {
-          const int4 l = lo_c[h];
+        ex[h] = ey[h] = ez[h] = 0;
+        if (cur.row[h] >= 0) {
+          const int4 l = cur.lo[h];
           if (l.z < z0 + SP_TZ && l.z + P > z0) {
 #pragma unroll
             for (int wq = 0; wq < 8; ++wq) {
@@ -494,25 +495,21 @@ __global__ void __launch_bounds__(288, 2) k_spread_mma4(const int4* __restrict__
           ey[h] = SP_TY + (y0 - l.y);
           ez[h] = SP_TZ + (z0 - l.z);
           if (m[h]) {
-            bytes += 8u * (RX + RY + RZ);
 #pragma unroll
-            for (int ch = 0; ch < NCH; ++ch) bq_(b)[sl][ch] = q_c[h][ch];
+            for (int ch = 0; ch < NCH; ++ch) bq_(b)[sl][ch] = cur.q[h][ch];
           }
         }
         bm_(b)[sl] = m[h] | (m[h] ? ((unsigned)(ex[h] & 1) << 8) | ((unsigned)(ey[h] & 1) << 9) |
                                         ((unsigned)(ez[h] & 1) << 10)
                                   : 0u);
       }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) bytes += __shfl_xor_sync(0xffffffffu, bytes, o);
-      (void)bytes;
       mbar_arrive(&full_bar[b]);  // masks / weights (plain stores) released
       // window slices: 16-byte cp.async chunks, completion tracked by the same barrier
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         if (m[h]) {
           const int sl = lane + 32 * h;
-          const double* src = tab + (int64_t)row_c[h] * wt.stride;
+          const double* src = tab + (int64_t)cur.row[h] * wt.stride;
           const double* sx = src + (ex[h] & ~1);
           const double* sy = src + wt.wx + (ey[h] & ~1);
           const double* sz = src + wt.wx + wt.wy + (ez[h] & ~1);
