@@ -385,7 +385,11 @@ __device__ __forceinline__ void cpa8(void* smem, const void* gmem) {
 // completing on the buffer's `full` mbarrier), warps 0-7 consume them (DMMA) and release
 // the buffer on its `empty` mbarrier.  Consumers never wait for staging and may run up
 // to SW_K chunks ahead of each other, so per-chunk load imbalance averages out.
-constexpr int SW_CH = 64, SW_K = 4, SW_RX = SP_TX + 2, SW_RY = SP_TY + 2, SW_RZ = SP_TZ + 2;
+#ifndef SW_CH_DEF
+#define SW_CH_DEF 32
+#define SW_K_DEF 8
+#endif
+constexpr int SW_CH = SW_CH_DEF, SW_K = SW_K_DEF, SW_H = SW_CH_DEF / 32, SW_RX = SP_TX + 2, SW_RY = SP_TY + 2, SW_RZ = SP_TZ + 2;
 template <int NCH>
 struct SwBuf {
   static constexpr int RQ = NCH | 1;
@@ -447,13 +451,13 @@ __global__ void __launch_bounds__(288, 2) k_spread_mma4(const int4* __restrict__
     // rows / windows starts / weights of chunk c+1 and c+2 are in flight (registers) while
     // chunk c is staged, so the producer runs at one chunk per staging pass, not per load latency
     struct Pre {
-      int4 lo[2];
-      int row[2];
-      double q[2][NCH];
+      int4 lo[SW_H];
+      int row[SW_H];
+      double q[SW_H][NCH];
     };
     auto fetch = [&](int c, Pre& f) {
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
+      for (int h = 0; h < SW_H; ++h) {
         const int v = c * SW_CH + lane + 32 * h;
         f.row[h] = -1;
         if (c < nchunk && v < ncand) {
@@ -476,12 +480,13 @@ __global__ void __launch_bounds__(288, 2) k_spread_mma4(const int4* __restrict__
       f1 = f2;
       fetch(c + 2, f2);
       if (c >= SW_K) mbar_wait(&empty_bar[b], ((c / SW_K) - 1) & 1);
-      unsigned m[2] = {0u, 0u};
-      int ex[2], ey[2], ez[2];
+      unsigned m[SW_H];
+      int ex[SW_H], ey[SW_H], ez[SW_H];
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
+      for (int h = 0; h < SW_H; ++h) {
         const int sl = lane + 32 * h;
         ex[h] = ey[h] = ez[h] = 0;
+        m[h] = 0u;
         if (cur.row[h] >= 0) {
           const int4 l = cur.lo[h];
           if (l.z < z0 + SP_TZ && l.z + P > z0) {
@@ -506,7 +511,7 @@ __global__ void __launch_bounds__(288, 2) k_spread_mma4(const int4* __restrict__
       mbar_arrive(&full_bar[b]);  // masks / weights (plain stores) released
       // window slices: 16-byte cp.async chunks, completion tracked by the same barrier
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
+      for (int h = 0; h < SW_H; ++h) {
         if (m[h]) {
           const int sl = lane + 32 * h;
           const double* src = tab + (int64_t)cur.row[h] * wt.stride;
@@ -891,7 +896,7 @@ hs_status launch_spread(hs_ctx* ctx, const double4* pts, const double* w, int n,
       k_spread_wtab<<<gs, 256, 0, ctx->stream>>>(pts, n, g, wt, lo, tab);
       HS_LAUNCHED(ctx);
     }
-    dim3 grid(nbx * nby * nbz), block(256);
+    dim3 grid(nbx * nby * nbz);
     for (int c0 = 0; c0 < nch; c0 += SP_MAXCH) {
       const int cn = std::min(SP_MAXCH, nch - c0);
       double* gout = grids + (size_t)c0 * g.ch_stride;
