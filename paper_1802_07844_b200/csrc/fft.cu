@@ -330,6 +330,201 @@ __global__ void __launch_bounds__(XF_THREADS, 2) k_xfused(const XArgs a) {
   }
 }
 
+// ---- register-resident x-stage (N = 32 M) -------------------------------------------------
+// One warp transforms one line: lane l holds x[l + 32 j] (j < M) and computes the M-point DFTs
+// over j in registers; twiddles W_N^{l k1}; one transpose through shared memory
+// (S[k1][l], rows padded to 33); the 32-point DFTs over l are split over lane pairs
+// (r = lane/2 < M, h = lane%2: a 16-point DFT of the even/odd half each, then one radix-2
+// combine across the pair by shuffles).  Lane (r,h) ends with X[r + M (k' + 16 h)], k' < 16.
+// Shared-memory traffic per line: one write + one read of the line (the Stockham version
+// makes a round trip per radix pass).
+__constant__ double2 c_w15[15];  // exp(-2 pi i m / 15)
+__constant__ double2 c_w16[16];  // exp(-2 pi i m / 16)
+__constant__ double2 c_w32[16];  // exp(-2 pi i m / 32)
+static bool g_xreg_consts = false;
+
+static hs_status xreg_constants() {
+  if (g_xreg_consts) return HS_OK;
+  double2 w15[15], w16[16], w32[16];
+  const long double tp = 6.283185307179586476925286766559005768L;
+  for (int m = 0; m < 15; ++m) w15[m] = make_double2((double)std::cos(tp * m / 15), (double)-std::sin(tp * m / 15));
+  for (int m = 0; m < 16; ++m) w16[m] = make_double2((double)std::cos(tp * m / 16), (double)-std::sin(tp * m / 16));
+  for (int m = 0; m < 16; ++m) w32[m] = make_double2((double)std::cos(tp * m / 32), (double)-std::sin(tp * m / 32));
+  HS_CUDA(cudaMemcpyToSymbol(c_w15, w15, sizeof(w15)));
+  HS_CUDA(cudaMemcpyToSymbol(c_w16, w16, sizeof(w16)));
+  HS_CUDA(cudaMemcpyToSymbol(c_w32, w32, sizeof(w32)));
+  g_xreg_consts = true;
+  return HS_OK;
+}
+
+// DFT-15 in place: j = j1 + 3 j2, k = 5 k1 + k2 (DFT5 over j2, twiddle W15^{j1 k2}, DFT3 over j1)
+__device__ __forceinline__ void dft15(double2* v) {
+  double2 Y[3][5];
+#pragma unroll
+  for (int j1 = 0; j1 < 3; ++j1) {
+    double2 t[5];
+#pragma unroll
+    for (int j2 = 0; j2 < 5; ++j2) t[j2] = v[j1 + 3 * j2];
+    dft<5>(t);
+#pragma unroll
+    for (int k2 = 0; k2 < 5; ++k2) Y[j1][k2] = (j1 * k2 == 0) ? t[k2] : cm(t[k2], c_w15[j1 * k2]);
+  }
+#pragma unroll
+  for (int k2 = 0; k2 < 5; ++k2) {
+    double2 t[3] = {Y[0][k2], Y[1][k2], Y[2][k2]};
+    dft<3>(t);
+#pragma unroll
+    for (int k1 = 0; k1 < 3; ++k1) v[5 * k1 + k2] = t[k1];
+  }
+}
+
+// DFT-16 in place: m = m1 + 4 m2, k = k2 + 4 k1 (DFT4 over m2, twiddle W16^{m1 k2}, DFT4 over m1)
+__device__ __forceinline__ void dft16(double2* a) {
+  double2 B[4][4];
+#pragma unroll
+  for (int m1 = 0; m1 < 4; ++m1) {
+    double2 t[4] = {a[m1], a[m1 + 4], a[m1 + 8], a[m1 + 12]};
+    dft<4>(t);
+#pragma unroll
+    for (int k2 = 0; k2 < 4; ++k2) B[m1][k2] = (m1 * k2 == 0) ? t[k2] : cm(t[k2], c_w16[m1 * k2]);
+  }
+#pragma unroll
+  for (int k2 = 0; k2 < 4; ++k2) {
+    double2 t[4] = {B[0][k2], B[1][k2], B[2][k2], B[3][k2]};
+    dft<4>(t);
+#pragma unroll
+    for (int k1 = 0; k1 < 4; ++k1) a[k2 + 4 * k1] = t[k1];
+  }
+}
+
+template <int M>
+__device__ __forceinline__ void dftM(double2* v) {
+  static_assert(M == 15, "register x-stage: M = 15 (N = 480)");
+  dft15(v);
+}
+
+// forward DFT of the line whose element l + 32 j is v[j]; S: warp scratch (M x 33);
+// tw: pd8-padded W_N^i table; out: X[r + M (k' + 16 h)], k' < 16 (r = lane/2 < M)
+template <int M>
+__device__ __forceinline__ void warp_fft_reg(double2* v, double2* S, const double2* tw, int lane, double2* out) {
+  dftM<M>(v);
+#pragma unroll
+  for (int k1 = 1; k1 < M; ++k1) v[k1] = cm(v[k1], tw[pd8(lane * k1)]);
+  __syncwarp();
+#pragma unroll
+  for (int k1 = 0; k1 < M; ++k1) S[k1 * 33 + lane] = v[k1];
+  __syncwarp();
+  const int r = lane >> 1, h = lane & 1;
+  const int rr = r < M ? r : M - 1;
+#pragma unroll
+  for (int m = 0; m < 16; ++m) out[m] = S[rr * 33 + 2 * m + h];
+  dft16(out);
+  // radix-2 combine across the lane pair: X[k'] = Y0 + W32^k' Y1, X[k'+16] = Y0 - W32^k' Y1
+#pragma unroll
+  for (int k = 0; k < 16; ++k) {
+    const double2 t = (h && k) ? cm(out[k], c_w32[k]) : out[k];  // h = 1 holds Y1
+    double2 p;
+    p.x = __shfl_xor_sync(0xffffffffu, t.x, 1);
+    p.y = __shfl_xor_sync(0xffffffffu, t.y, 1);
+    out[k] = h ? sb(p, t) : ad(t, p);
+  }
+}
+
+template <int KIND, bool HALF, int M>
+__global__ void __launch_bounds__(XF_THREADS, 2) k_xreg(const XArgs a) {
+  constexpr int N = 32 * M, LSR = M * 33;
+  constexpr int NIN = KChan<KIND, HALF>::NIN, NOUT = KChan<KIND, HALF>::NOUT;
+  static_assert(NIN <= XF_THREADS / 32 && NOUT <= XF_THREADS / 32, "one warp per channel line");
+  extern __shared__ double2 smem[];
+  double2* lines = smem;                         // [8 warps][LSR]: transpose scratch, then channel line
+  double2* tw = smem + (XF_THREADS / 32) * LSR;  // pd8-padded twiddles
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int i = tid; i < N; i += blockDim.x) tw[pd8(i)] = a.tw[i];
+  const int n_items = a.py * a.nzh;
+  const int p[3] = {a.px, a.py, a.pz};
+  const int r = lane >> 1, h = lane & 1;
+  for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+    const int ky = item / a.nzh;
+    const int kz = item - ky * a.nzh;
+    __syncthreads();  // previous item's lines consumed (and twiddles visible)
+    if (warp < NIN) {
+      double2 v[M], out[16];
+      const double2* src = a.B + warp * a.ch_stride + (int64_t)ky * a.nx * a.nzh + kz;
+#pragma unroll
+      for (int j = 0; j < M; ++j) {
+        const int x = lane + 32 * j;
+        v[j] = x < a.nx ? src[(int64_t)x * a.nzh] : make_double2(0.0, 0.0);
+      }
+      double2* S = lines + warp * LSR;
+      warp_fft_reg<M>(v, S, tw, lane, out);
+      __syncwarp();
+      if (r < M) {
+#pragma unroll
+        for (int k = 0; k < 16; ++k) S[r + M * (k + 16 * h)] = out[k];
+      }
+    }
+    __syncthreads();
+    // k-space scaling at every kx of the column (channel c of kx at lines[c * LSR + kx])
+    for (int kx = tid; kx < N; kx += blockDim.x) {
+      const int64_t ti = ((int64_t)ky * a.nzh + kz) * N + kx;
+      const double tB = (KIND == HS_ROTLET) ? 0.0 : a.tabB[ti];
+      const double tH = (KIND == HS_ROTLET || HALF) ? a.tabH[ti] : 0.0;
+      double2* col = lines + kx;
+      if (2 * kx == N || 2 * ky == a.py || 2 * kz == a.pz) {
+        scale_nyquist<KIND, HALF>(col, LSR, kx, ky, kz, p, a.kscale, a.ka, a.kb, a.inv_n, tB, tH);
+        continue;
+      }
+      cplx C[NIN], outc[6];
+#pragma unroll
+      for (int c = 0; c < NIN; ++c) {
+        const double2 vv = col[c * LSR];
+        C[c] = {vv.x, vv.y};
+      }
+      const double s8 = 1.0 / (8.0 * kPi), s4 = 1.0 / (4.0 * kPi);
+      const double kxv = kval(kx, N, a.kscale[0]), kyv = kval(ky, a.py, a.kscale[1]), kzv = kval(kz, a.pz, a.kscale[2]);
+      const double k2 = kxv * kxv + kyv * kyv + kzv * kzv;
+      const double E = exp(-a.ka * k2);
+      const double G = (KIND == HS_ROTLET) ? tH * E * s4 * a.inv_n : tB * E * (1.0 + a.kb * k2) * s8 * a.inv_n;
+      const double Fc = HALF ? tH * E * s4 * a.inv_n : 0.0;
+      apply_multiplier<KIND, HALF>(kxv, kyv, kzv, G, Fc, C, outc);
+      // inverse transform by conjugation: IFFT(y) = conj(FFT(conj(y))) (normalisation already in inv_n)
+#pragma unroll
+      for (int o = 0; o < NOUT; ++o) col[o * LSR] = make_double2(outc[o].re, -outc[o].im);
+    }
+    __syncthreads();
+    if (warp < NOUT) {
+      double2 v[M], out[16];
+      double2* S = lines + warp * LSR;
+#pragma unroll
+      for (int j = 0; j < M; ++j) v[j] = S[lane + 32 * j];
+      warp_fft_reg<M>(v, S, tw, lane, out);
+      if (r < M) {
+        double2* dst = a.B + warp * a.ch_stride + (int64_t)ky * a.nx * a.nzh + kz;
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          const int x = r + M * (k + 16 * h);
+          if (x < a.nx) dst[(int64_t)x * a.nzh] = make_double2(out[k].x, -out[k].y);
+        }
+      }
+    }
+  }
+}
+
+template <int KIND, bool HALF, int M>
+static hs_status launch_xreg_t(hs_ctx* ctx, const XArgs& a) {
+  HS_TRY(xreg_constants());
+  const size_t smem = sizeof(double2) * ((size_t)(XF_THREADS / 32) * M * 33 + padded_line(32 * M));
+  auto kern = k_xreg<KIND, HALF, M>;
+  HS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per_sm = 0;
+  HS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, XF_THREADS, smem));
+  const int items = a.py * a.nzh;
+  const int grid = std::max(1, std::min(items, ctx->sm_count * std::max(per_sm, 1) * 8));
+  kern<<<grid, XF_THREADS, smem, ctx->stream>>>(a);
+  HS_LAUNCHED(ctx);
+  return HS_OK;
+}
+
 template <int KIND, bool HALF, int KB, class FFT>
 static hs_status launch_xfused_t(hs_ctx* ctx, const XArgs& a) {
   constexpr int NL = KChan<KIND, HALF>::NIN > KChan<KIND, HALF>::NOUT ? KChan<KIND, HALF>::NIN
@@ -355,7 +550,12 @@ static hs_status launch_xfused_half(hs_ctx* ctx, const XArgs& a) {
   switch (a.plan.n) {
     case 240: return launch_xfused_t<KIND, true, KB, FixedFFT<8, 2, 3, 5>>(ctx, a);
     case 352: return launch_xfused_t<KIND, true, KB, FixedFFT<8, 4, 11>>(ctx, a);
-    case 480: return launch_xfused_t<KIND, true, KB, FixedFFT<8, 4, 3, 5>>(ctx, a);
+    case 480: {
+      static const bool stockham = getenv("HS_XSTAGE_STOCKHAM") != nullptr;  // previous kernel (comparison)
+      if constexpr (KChan<KIND, true>::NIN <= XF_THREADS / 32)  // one warp per source channel
+        if (!stockham) return launch_xreg_t<KIND, true, 15>(ctx, a);
+      return launch_xfused_t<KIND, true, KB, FixedFFT<8, 4, 3, 5>>(ctx, a);
+    }
     case 750: return launch_xfused_t<KIND, true, KB, FixedFFT<2, 3, 5, 5, 5>>(ctx, a);
     case 864: return launch_xfused_t<KIND, true, KB, FixedFFT<8, 4, 3, 3, 3>>(ctx, a);
     default: return launch_xfused_t<KIND, true, KB, AnyFFT>(ctx, a);
