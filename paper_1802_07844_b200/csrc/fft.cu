@@ -339,18 +339,21 @@ __global__ void __launch_bounds__(XF_THREADS, 2) k_xfused(const XArgs a) {
 // Shared-memory traffic per line: one write + one read of the line (the Stockham version
 // makes a round trip per radix pass).
 __constant__ double2 c_w15[15];  // exp(-2 pi i m / 15)
+__constant__ double2 c_w11[11];  // exp(-2 pi i m / 11)
 __constant__ double2 c_w16[16];  // exp(-2 pi i m / 16)
 __constant__ double2 c_w32[16];  // exp(-2 pi i m / 32)
 static bool g_xreg_consts = false;
 
 static hs_status xreg_constants() {
   if (g_xreg_consts) return HS_OK;
-  double2 w15[15], w16[16], w32[16];
+  double2 w15[15], w16[16], w32[16], w11[11];
   const long double tp = 6.283185307179586476925286766559005768L;
   for (int m = 0; m < 15; ++m) w15[m] = make_double2((double)std::cos(tp * m / 15), (double)-std::sin(tp * m / 15));
+  for (int m = 0; m < 11; ++m) w11[m] = make_double2((double)std::cos(tp * m / 11), (double)-std::sin(tp * m / 11));
   for (int m = 0; m < 16; ++m) w16[m] = make_double2((double)std::cos(tp * m / 16), (double)-std::sin(tp * m / 16));
   for (int m = 0; m < 16; ++m) w32[m] = make_double2((double)std::cos(tp * m / 32), (double)-std::sin(tp * m / 32));
   HS_CUDA(cudaMemcpyToSymbol(c_w15, w15, sizeof(w15)));
+  HS_CUDA(cudaMemcpyToSymbol(c_w11, w11, sizeof(w11)));
   HS_CUDA(cudaMemcpyToSymbol(c_w16, w16, sizeof(w16)));
   HS_CUDA(cudaMemcpyToSymbol(c_w32, w32, sizeof(w32)));
   g_xreg_consts = true;
@@ -397,10 +400,43 @@ __device__ __forceinline__ void dft16(double2* a) {
   }
 }
 
+// DFT-11 in place (direct, symmetric pairs: 5 cos/sin pairs per output)
+__device__ __forceinline__ void dft11(double2* v) {
+  double2 sp[5], sm[5];
+#pragma unroll
+  for (int m = 1; m <= 5; ++m) {
+    sp[m - 1] = ad(v[m], v[11 - m]);
+    sm[m - 1] = sb(v[m], v[11 - m]);
+  }
+  double2 y[11];
+  double2 s0 = v[0];
+#pragma unroll
+  for (int m = 0; m < 5; ++m) s0 = ad(s0, sp[m]);
+  y[0] = s0;
+#pragma unroll
+  for (int k = 1; k <= 5; ++k) {
+    double2 re = v[0], im = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int m = 1; m <= 5; ++m) {
+      const double2 w = c_w11[(m * k) % 11];  // (cos, -sin)
+      re = make_double2(fma(w.x, sp[m - 1].x, re.x), fma(w.x, sp[m - 1].y, re.y));
+      im = make_double2(fma(w.y, sm[m - 1].x, im.x), fma(w.y, sm[m - 1].y, im.y));
+    }
+    // X_k = re + i im, X_{11-k} = re - i im  (im holds -sin * (a_m - a_{11-m}))
+    y[k] = make_double2(re.x - im.y, re.y + im.x);
+    y[11 - k] = make_double2(re.x + im.y, re.y - im.x);
+  }
+#pragma unroll
+  for (int k = 0; k < 11; ++k) v[k] = y[k];
+}
+
 template <int M>
 __device__ __forceinline__ void dftM(double2* v) {
-  static_assert(M == 15, "register x-stage: M = 15 (N = 480)");
-  dft15(v);
+  static_assert(M == 15 || M == 11, "register x-stage: M = 15 (N = 480) or 11 (N = 352)");
+  if constexpr (M == 15)
+    dft15(v);
+  else
+    dft11(v);
 }
 
 // forward DFT of the line whose element l + 32 j is v[j]; S: warp scratch (M x 33);
@@ -434,10 +470,10 @@ template <int KIND, bool HALF, int M>
 __global__ void __launch_bounds__(XF_THREADS, 2) k_xreg(const XArgs a) {
   constexpr int N = 32 * M, LSR = M * 33;
   constexpr int NIN = KChan<KIND, HALF>::NIN, NOUT = KChan<KIND, HALF>::NOUT;
-  static_assert(NIN <= XF_THREADS / 32 && NOUT <= XF_THREADS / 32, "one warp per channel line");
+  constexpr int NL = NIN > NOUT ? NIN : NOUT, NW = XF_THREADS / 32;
   extern __shared__ double2 smem[];
-  double2* lines = smem;                         // [8 warps][LSR]: transpose scratch, then channel line
-  double2* tw = smem + (XF_THREADS / 32) * LSR;  // pd8-padded twiddles
+  double2* lines = smem;            // [NL][LSR]: transpose scratch of the line's warp, then the channel line
+  double2* tw = smem + NL * LSR;    // pd8-padded twiddles
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int i = tid; i < N; i += blockDim.x) tw[pd8(i)] = a.tw[i];
   const int n_items = a.py * a.nzh;
@@ -447,15 +483,15 @@ __global__ void __launch_bounds__(XF_THREADS, 2) k_xreg(const XArgs a) {
     const int ky = item / a.nzh;
     const int kz = item - ky * a.nzh;
     __syncthreads();  // previous item's lines consumed (and twiddles visible)
-    if (warp < NIN) {
+    for (int c = warp; c < NIN; c += NW) {
       double2 v[M], out[16];
-      const double2* src = a.B + warp * a.ch_stride + (int64_t)ky * a.nx * a.nzh + kz;
+      const double2* src = a.B + c * a.ch_stride + (int64_t)ky * a.nx * a.nzh + kz;
 #pragma unroll
       for (int j = 0; j < M; ++j) {
         const int x = lane + 32 * j;
         v[j] = x < a.nx ? src[(int64_t)x * a.nzh] : make_double2(0.0, 0.0);
       }
-      double2* S = lines + warp * LSR;
+      double2* S = lines + c * LSR;
       warp_fft_reg<M>(v, S, tw, lane, out);
       __syncwarp();
       if (r < M) {
@@ -492,14 +528,14 @@ __global__ void __launch_bounds__(XF_THREADS, 2) k_xreg(const XArgs a) {
       for (int o = 0; o < NOUT; ++o) col[o * LSR] = make_double2(outc[o].re, -outc[o].im);
     }
     __syncthreads();
-    if (warp < NOUT) {
+    for (int o = warp; o < NOUT; o += NW) {
       double2 v[M], out[16];
-      double2* S = lines + warp * LSR;
+      double2* S = lines + o * LSR;
 #pragma unroll
       for (int j = 0; j < M; ++j) v[j] = S[lane + 32 * j];
       warp_fft_reg<M>(v, S, tw, lane, out);
       if (r < M) {
-        double2* dst = a.B + warp * a.ch_stride + (int64_t)ky * a.nx * a.nzh + kz;
+        double2* dst = a.B + o * a.ch_stride + (int64_t)ky * a.nx * a.nzh + kz;
 #pragma unroll
         for (int k = 0; k < 16; ++k) {
           const int x = r + M * (k + 16 * h);
@@ -513,7 +549,8 @@ __global__ void __launch_bounds__(XF_THREADS, 2) k_xreg(const XArgs a) {
 template <int KIND, bool HALF, int M>
 static hs_status launch_xreg_t(hs_ctx* ctx, const XArgs& a) {
   HS_TRY(xreg_constants());
-  const size_t smem = sizeof(double2) * ((size_t)(XF_THREADS / 32) * M * 33 + padded_line(32 * M));
+  constexpr int NL = KChan<KIND, HALF>::NIN > KChan<KIND, HALF>::NOUT ? KChan<KIND, HALF>::NIN : KChan<KIND, HALF>::NOUT;
+  const size_t smem = sizeof(double2) * ((size_t)NL * M * 33 + padded_line(32 * M));
   auto kern = k_xreg<KIND, HALF, M>;
   HS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0;
@@ -549,11 +586,14 @@ template <int KIND, int KB>
 static hs_status launch_xfused_half(hs_ctx* ctx, const XArgs& a) {
   switch (a.plan.n) {
     case 240: return launch_xfused_t<KIND, true, KB, FixedFFT<8, 2, 3, 5>>(ctx, a);
-    case 352: return launch_xfused_t<KIND, true, KB, FixedFFT<8, 4, 11>>(ctx, a);
+    case 352: {
+      static const bool stockham = getenv("HS_XSTAGE_STOCKHAM") != nullptr;
+      if (!stockham) return launch_xreg_t<KIND, true, 11>(ctx, a);
+      return launch_xfused_t<KIND, true, KB, FixedFFT<8, 4, 11>>(ctx, a);
+    }
     case 480: {
       static const bool stockham = getenv("HS_XSTAGE_STOCKHAM") != nullptr;  // previous kernel (comparison)
-      if constexpr (KChan<KIND, true>::NIN <= XF_THREADS / 32)  // one warp per source channel
-        if (!stockham) return launch_xreg_t<KIND, true, 15>(ctx, a);
+      if (!stockham) return launch_xreg_t<KIND, true, 15>(ctx, a);
       return launch_xfused_t<KIND, true, KB, FixedFFT<8, 4, 3, 5>>(ctx, a);
     }
     case 750: return launch_xfused_t<KIND, true, KB, FixedFFT<2, 3, 5, 5, 5>>(ctx, a);

@@ -340,18 +340,20 @@ def test_fourier_gather_layouts_vs_oracle(gpu, oracle, kind, nt):
         assert rel_l2(r2.velocities, r.velocities[sub]) < 1e-13
 
 
-@pytest.mark.parametrize("kind", ("stokeslet", "rotlet"))
-def test_xstage_register_fft_matches_stockham(tmp_path, kind):
-    """The register-resident x-stage (N = 480 = 15 x 32) against the shared-memory Stockham
-    x-stage on the same input at the headline grid (each selected in its own process)."""
+@pytest.mark.parametrize("kind", KINDS)
+@pytest.mark.parametrize("M", (192, 128))
+def test_xstage_register_fft_matches_stockham(tmp_path, kind, M):
+    """The register-resident x-stage (N = 480 = 15 x 32 at M=192, 352 = 11 x 32 at M=128)
+    against the shared-memory Stockham x-stage on the same input (each selected in its own
+    process)."""
     import os
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     tool = os.path.join(root, "tools", "xstage_ab.py")
     a, b = tmp_path / "reg.npy", tmp_path / "stockham.npy"
-    subprocess.run([sys.executable, tool, str(a), kind], check=True)
+    subprocess.run([sys.executable, tool, str(a), kind, str(M)], check=True)
     env = dict(os.environ, HS_XSTAGE_STOCKHAM="1")
-    subprocess.run([sys.executable, tool, str(b), kind], check=True, env=env)
+    subprocess.run([sys.executable, tool, str(b), kind, str(M)], check=True, env=env)
     ua, ub = np.load(a), np.load(b)
     assert rel_l2(ua, ub) < 1e-12
