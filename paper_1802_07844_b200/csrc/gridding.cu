@@ -577,10 +577,15 @@ __global__ void __launch_bounds__(288, 2) k_spread_mma4(const int4* __restrict__
             cxy[rb] = s_wx[sk][pxo + wx0 + (p & 3)] * s_wy[sk][pyo + wy0 + (p >> 2)];
           }
         }
+        // the weight goes into the B operand (wz q_c, one product per channel) so A = wx wy is
+        // shared by the channels
+        double bq[NCH];
+#pragma unroll
+        for (int ch = 0; ch < NCH; ++ch) bq[ch] = bz * q[ch];
 #pragma unroll
         for (int rb = 0; rb < 4; ++rb)
 #pragma unroll
-          for (int ch = 0; ch < NCH; ++ch) dmma_884(acc[rb][ch][0], acc[rb][ch][1], cxy[rb] * q[ch], bz);
+          for (int ch = 0; ch < NCH; ++ch) dmma_884(acc[rb][ch][0], acc[rb][ch][1], cxy[rb], bq[ch]);
       }
     }
     mbar_arrive(&empty_bar[b]);
