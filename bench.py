@@ -69,7 +69,7 @@ def cpu_sample(wname: str, threads: int | None = None):
     zz, sa, sb, sign = o.reflect(pos, "stokeslet", f=f)
     # real space: set-up (reflection, cell list of all 2N points, permutations) once; the
     # pair loop on a sample of targets, scaled
-    nts = min(n, 16000)
+    nts = min(n, 48000)
     sub = np.sort(rng.choice(n, nts, replace=False))
     tr = {}
     o.real_space_sum("stokeslet", "half", w.L, pos, w.xi, w.rc, f=f, targets=pos[sub], target_indices=sub,
@@ -77,7 +77,7 @@ def cpu_sample(wname: str, threads: int | None = None):
     parts["real"] = tr["setup"] + tr["pairs"] * n / nts
     # spreading: the scatter loop on a sample of sources (3 kernel + 4 wall channels), scaled;
     # grid zeroing and the channel-first copy at full size
-    frac = min(1.0, 80000 / (2 * n))
+    frac = min(1.0, 240000 / (2 * n))
     ks = rng.choice(2 * n, int(2 * n * frac), replace=False)
     s_, v_, _ = o.phi_channels("stokeslet", pos, f=f)
     cs = rng.choice(n, int(n * frac), replace=False)
@@ -102,7 +102,7 @@ def cpu_sample(wname: str, threads: int | None = None):
     parts["fft"] = 7 * tf * sc
     parts["ifft"] = 6 * ti * sc
     # k-space scaling (kernel + wall channels) on a slab of planes
-    planes = 12
+    planes = 36
     shp = (planes, pd[1], pd[2])
     Ch = (rng.normal(size=(3,) + shp) + 1j * rng.normal(size=(3,) + shp))
     tab = rng.normal(size=shp)
@@ -121,7 +121,7 @@ def cpu_sample(wname: str, threads: int | None = None):
     del Ch, out, phi, Fc, tab
     # gather: 6 channels at a target sample
     grids = np.zeros((3,) + tuple(g.dims))
-    ntg = 6000
+    ntg = 18000
     tg = {}
     o.gather(grids, pos[:ntg], g, timings=tg)
     parts["gather"] = 2 * (tg["copy"] + tg["loop"] * n / ntg)
