@@ -37,9 +37,10 @@ static bool g_erfcx_ready = false;
 // Branch-free: x >= 8 (only reachable when xi r_c >= 8) evaluates the last interval's
 // polynomial outside its interval; there erfc(x) < 1.2e-29, so the pair's contribution is
 // below the double resolution of any sum it enters, and E * p stays finite.
-__device__ __forceinline__ double erfc_from_E(double x, double E, const double2* __restrict__ tab) {
-  const int k = min((int)(x * (1.0 / HS_ERFCX_W)), HS_ERFCX_NINT - 1);
-  const double t = (x - (HS_ERFCX_W * k + 0.5 * HS_ERFCX_W)) * (2.0 / HS_ERFCX_W);
+// xw = x / W (interval units): k = trunc(xw), t = 2 (xw - k) - 1
+__device__ __forceinline__ double erfc_from_E(double xw, double E, const double2* __restrict__ tab) {
+  const int k = min((int)xw, HS_ERFCX_NINT - 1);
+  const double t = fma(2.0, xw, -(double)(2 * k + 1));
   const double2 top = tab[(HS_ERFCX_NPAIR - 1) * HS_ERFCX_NINT + k];
   double p = (HS_ERFCX_DEG & 1) ? fma(top.y, t, top.x) : top.x;
 #pragma unroll
@@ -89,6 +90,7 @@ constexpr int PT_MAXRUN = 25;  // 5 x 5 (x, y) cell columns
 
 struct PairConst {
   double xi, xi2, c2xs;  // xi, xi^2, 2 xi / sqrt(pi)
+  double xiw;            // xi / HS_ERFCX_W (erfc argument in table-interval units)
 };
 
 // Radial coefficients of one pair (the transcendental part; branch-free when SCREENED).
@@ -104,7 +106,7 @@ __device__ __forceinline__ PairCoef pair_coef(const PairConst& pc, double r2, co
     q.ri = rsqrt_pos(r2);
     const double rn = r2 * q.ri;
     const double E = exp_nonpos(-pc.xi2 * r2);
-    C = erfc_from_E(pc.xi * rn, E, etab);
+    C = erfc_from_E(pc.xiw * rn, E, etab);
     q.e = pc.c2xs * E;
   } else {
     q.ri = rsqrt(r2);
@@ -247,6 +249,7 @@ __global__ void __launch_bounds__(PC_TG, PC_MINB) k_pair_q(const PairArgs a) {
   pc.xi = a.xi;
   pc.xi2 = a.xi * a.xi;
   pc.c2xs = 2.0 * a.xi / kSqrtPi;
+  pc.xiw = a.xi * (1.0 / HS_ERFCX_W);
   const double norm_k = (KIND == HS_ROTLET) ? 1.0 / (4.0 * kPi) : 1.0 / (8.0 * kPi);
   const double norm_c = 1.0 / (4.0 * kPi);
   unsigned short(*q)[32] = sq[warp];
@@ -324,7 +327,7 @@ __global__ void __launch_bounds__(PC_TG, PC_MINB) k_pair_q(const PairArgs a) {
       bool img;
       load_cand(jj, S, A, B, img);
       const double e0 = T.x - S.x, e1 = T.y - S.y, e2 = T.z - S.z;
-      const double rr = exact_r2(e0, e1, e2);
+      const double rr = fma(e0, e0, fma(e1, e1, e2 * e2));  // (neighbour test done exactly in the scan)
       if (img) ++n_img;
       eval_pair<KIND, true>(pc, e0, e1, e2, rr, T.z, S, A, B, img, &acc[0], &acc[3], s_erfcx);
     };
@@ -363,7 +366,7 @@ __global__ void __launch_bounds__(PC_TG, PC_MINB) k_pair_q(const PairArgs a) {
       load_cand(j2, S2, A2, B2, i2);
       const double f0 = T.x - S1.x, f1 = T.y - S1.y, f2 = T.z - S1.z;
       const double g0 = T.x - S2.x, g1 = T.y - S2.y, g2 = T.z - S2.z;
-      const double r1 = exact_r2(f0, f1, f2), r2 = exact_r2(g0, g1, g2);
+      const double r1 = fma(f0, f0, fma(f1, f1, f2 * f2)), r2 = fma(g0, g0, fma(g1, g1, g2 * g2));
       const PairCoef q1 = pair_coef<true>(pc, r1, s_erfcx);
       const PairCoef q2 = pair_coef<true>(pc, r2, s_erfcx);
       n_img += (unsigned)i1 + (unsigned)i2;
