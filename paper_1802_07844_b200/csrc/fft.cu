@@ -562,6 +562,90 @@ static hs_status launch_xreg_t(hs_ctx* ctx, const XArgs& a) {
   return HS_OK;
 }
 
+// ---- y stage (N = 32 M) with the register FFT ----------------------------------------------
+// Lines along y of the [y][x][kz] channel layout: a CTA takes one x and 8 consecutive kz
+// (one warp per kz line); rows of 8 kz (128 contiguous bytes) are staged through shared
+// memory with cp.async (coalesced), each warp transforms its column in registers
+// (warp_fft_reg), and the results leave through shared memory as coalesced rows again.
+// Forward: only the ny nonzero input rows are read (input pruning).  Inverse
+// (unnormalised, by conjugation): only the ny output rows that the z stage needs are
+// written (output pruning); in place.
+constexpr int YS_KB = 8, YS_RS = YS_KB + 1;  // kz per CTA, padded row length (bank spread)
+
+template <int M, bool FWD>
+__global__ void __launch_bounds__(256, 2) k_ystage(const double2* __restrict__ in, double2* __restrict__ out,
+                                                  const double2* __restrict__ twg, int nx, int nzh, int ny) {
+  constexpr int N = 32 * M;
+  extern __shared__ double2 smem[];
+  double2* buf = smem;              // [N rows][YS_RS]; later per-warp transpose scratch (8 x M*33)
+  double2* tw = smem + N * YS_RS;   // pd8-padded twiddles
+  static_assert(8 * M * 33 <= N * YS_RS, "scratch fits the row buffer");
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int i = tid; i < N; i += blockDim.x) tw[pd8(i)] = twg[i];
+  const int nkb = (nzh + YS_KB - 1) / YS_KB;
+  const int n_items = nx * nkb;
+  const int rows_in = FWD ? ny : N, rows_out = FWD ? N : ny;
+  const int64_t rstride = (int64_t)nx * nzh;  // elements between rows (y)
+  const int r = lane >> 1, h = lane & 1;
+  for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+    const int x = item / nkb, kz0 = (item - x * nkb) * YS_KB;
+    const int kbn = min(YS_KB, nzh - kz0);
+    const int64_t base = (int64_t)x * nzh + kz0;
+    __syncthreads();  // previous item done with buf
+    for (int i = tid; i < rows_in * YS_KB; i += blockDim.x) {
+      const int row = i / YS_KB, k = i - row * YS_KB;
+      if (k < kbn) cp_async16(&buf[row * YS_RS + k], in + base + row * rstride + k);
+    }
+    cp_async_commit();
+    cp_async_wait_all();
+    __syncthreads();
+    double2 v[M], o16[16];
+#pragma unroll
+    for (int j = 0; j < M; ++j) {
+      const int row = lane + 32 * j;
+      double2 e = row < rows_in ? buf[row * YS_RS + warp] : make_double2(0.0, 0.0);
+      if (!FWD) e.y = -e.y;
+      v[j] = e;
+    }
+    __syncthreads();  // every column read: the buffer becomes transpose scratch
+    warp_fft_reg<M>(v, buf + warp * M * 33, tw, lane, o16);
+    __syncthreads();  // scratch use finished: the buffer collects the output rows
+    if (r < M) {
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        const int row = r + M * (k + 16 * h);
+        double2 e = o16[k];
+        if (!FWD) e.y = -e.y;
+        if (row < rows_out) buf[row * YS_RS + warp] = e;
+      }
+    }
+    __syncthreads();
+    for (int i = tid; i < rows_out * YS_KB; i += blockDim.x) {
+      const int row = i / YS_KB, k = i - row * YS_KB;
+      if (k < kbn) out[base + row * rstride + k] = buf[row * YS_RS + k];
+    }
+  }
+}
+
+// y stage of one channel; false when the length has no register kernel (caller uses cuFFT)
+bool ystage_supported(int py) { return py == 480 || py == 352; }
+hs_status launch_ystage(hs_ctx* ctx, bool fwd, const double2* in, double2* out, const double2* tw, int py, int nx,
+                        int nzh, int ny) {
+  HS_TRY(xreg_constants());
+  auto go = [&](auto kern, int M) -> hs_status {
+    const size_t smem = sizeof(double2) * ((size_t)32 * M * YS_RS + padded_line(32 * M));
+    HS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const int items = nx * ((nzh + YS_KB - 1) / YS_KB);
+    const int grid = std::max(1, std::min(items, ctx->sm_count * 2 * 8));
+    kern<<<grid, 256, smem, ctx->stream>>>(in, out, tw, nx, nzh, ny);
+    HS_LAUNCHED(ctx);
+    return HS_OK;
+  };
+  if (py == 480) return fwd ? go(k_ystage<15, true>, 15) : go(k_ystage<15, false>, 15);
+  if (py == 352) return fwd ? go(k_ystage<11, true>, 11) : go(k_ystage<11, false>, 11);
+  return fail(HS_ERR_PARAMETER, "y stage: unsupported length");
+}
+
 template <int KIND, bool HALF, int KB, class FFT>
 static hs_status launch_xfused_t(hs_ctx* ctx, const XArgs& a) {
   constexpr int NL = KChan<KIND, HALF>::NIN > KChan<KIND, HALF>::NOUT ? KChan<KIND, HALF>::NIN

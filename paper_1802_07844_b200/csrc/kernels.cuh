@@ -146,6 +146,11 @@ struct XArgs {
 hs_status make_fft_plan(int n, FftPlan* pl);
 hs_status make_twiddles(int n, double2* d_tw, cudaStream_t st);
 hs_status launch_xfused(hs_ctx* ctx, int kind, int half, const XArgs& a);
+// y stage with the register FFT (py = 480 or 352): forward reads rows y < ny, writes all py rows;
+// inverse reads all py rows, writes rows y < ny (in place allowed)
+bool ystage_supported(int py);
+hs_status launch_ystage(hs_ctx* ctx, bool fwd, const double2* in, double2* out, const double2* tw, int py, int nx,
+                        int nzh, int ny);
 hs_status launch_table_to_xmajor(hs_ctx* ctx, const double* in, int px, int py, int nzh, double* out);
 
 // plan.cu helpers reused by the stand-alone API

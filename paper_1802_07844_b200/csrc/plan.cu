@@ -250,6 +250,7 @@ struct hs_plan {
   double* tabB = nullptr;       // x-stage layout [ky][kz][kx]
   double* tabH = nullptr;
   double2* tw = nullptr;        // px twiddles
+  double2* ytw = nullptr;       // py twiddles of the register y stage (null: cuFFT y stage)
   FftPlan xplan{};
   bool have_B = false, have_H = false;
   cufftHandle zf = 0, yf = 0, zi = 0;
@@ -415,6 +416,10 @@ extern "C" hs_status hs_plan_create(hs_ctx* ctx, const hs_params* prm, hs_plan**
   if (table_needs(prm->kind, p->half, HS_HARMONIC)) A_(p->n_half, p->tabH);
   A_(px, p->tw);
   if ((st = make_twiddles((int)px, p->tw, ctx->stream)) != HS_OK) return bail(st);
+  if (ystage_supported((int)py) && !getenv("HS_YSTAGE_CUFFT")) {  // env: cuFFT y stage (comparison)
+    A_(py, p->ytw);
+    if ((st = make_twiddles((int)py, p->ytw, ctx->stream)) != HS_OK) return bail(st);
+  }
   A_(3 * (size_t)std::max(nt, 1), p->u);
   A_(3 * (size_t)std::max(nt, 1), p->u_real, true);
   A_(3 * (size_t)std::max(nt, 1), p->u_four, true);
@@ -764,9 +769,13 @@ extern "C" hs_status hs_plan_execute(hs_plan* p, const double* positions, const 
     for (int c = 0; c < p->n_in; ++c) {
       if (cufftExecD2Z(p->zf, p->grid_in + (size_t)c * p->n_grid, (cufftDoubleComplex*)p->Amix) != CUFFT_SUCCESS)
         return fail(HS_ERR_CUDA, "cuFFT z D2Z failed");
-      if (cufftExecZ2Z(p->yf, (cufftDoubleComplex*)p->Amix, (cufftDoubleComplex*)(p->spec + (size_t)c * p->n_mixed),
-                       CUFFT_FORWARD) != CUFFT_SUCCESS)
+      if (p->ytw) {
+        HS_TRY(launch_ystage(ctx, true, p->Amix, p->spec + (size_t)c * p->n_mixed, p->ytw, p->kg.p[1], p->gg.dims[0],
+                             p->kg.nzh, p->gg.dims[1]));
+      } else if (cufftExecZ2Z(p->yf, (cufftDoubleComplex*)p->Amix,
+                              (cufftDoubleComplex*)(p->spec + (size_t)c * p->n_mixed), CUFFT_FORWARD) != CUFFT_SUCCESS) {
         return fail(HS_ERR_CUDA, "cuFFT y Z2Z failed");
+      }
     }
     HS_CUDA(cudaEventRecord(ev[4], st));
     {
@@ -791,7 +800,12 @@ extern "C" hs_status hs_plan_execute(hs_plan* p, const double* positions, const 
     HS_CUDA(cudaEventRecord(ev[5], st));
     for (int o = 0; o < p->n_out; ++o) {
       cufftDoubleComplex* so = (cufftDoubleComplex*)(p->spec + (size_t)o * p->n_mixed);
-      if (cufftExecZ2Z(p->yf, so, so, CUFFT_INVERSE) != CUFFT_SUCCESS) return fail(HS_ERR_CUDA, "cuFFT y^-1 failed");
+      if (p->ytw) {
+        HS_TRY(launch_ystage(ctx, false, (double2*)so, (double2*)so, p->ytw, p->kg.p[1], p->gg.dims[0], p->kg.nzh,
+                             p->gg.dims[1]));
+      } else if (cufftExecZ2Z(p->yf, so, so, CUFFT_INVERSE) != CUFFT_SUCCESS) {
+        return fail(HS_ERR_CUDA, "cuFFT y^-1 failed");
+      }
       if (cufftExecZ2D(p->zi, so, p->grid_tmp + (size_t)o * p->n_grid) != CUFFT_SUCCESS)
         return fail(HS_ERR_CUDA, "cuFFT z Z2D failed");
     }

@@ -342,10 +342,11 @@ def test_fourier_gather_layouts_vs_oracle(gpu, oracle, kind, nt):
 
 @pytest.mark.parametrize("kind", KINDS)
 @pytest.mark.parametrize("M", (192, 128))
-def test_xstage_register_fft_matches_stockham(tmp_path, kind, M):
-    """The register-resident x-stage (N = 480 = 15 x 32 at M=192, 352 = 11 x 32 at M=128)
-    against the shared-memory Stockham x-stage on the same input (each selected in its own
-    process)."""
+@pytest.mark.parametrize("alt", ("HS_XSTAGE_STOCKHAM", "HS_YSTAGE_CUFFT"))
+def test_register_fft_stages_match_alternatives(tmp_path, kind, M, alt):
+    """The register-FFT x stage and y stage (N = 480 = 15 x 32 at M=192, 352 = 11 x 32 at
+    M=128) against the shared-memory Stockham x stage / the cuFFT y stage on the same input
+    (each selected in its own process)."""
     import os
     import subprocess
     import sys
@@ -353,7 +354,7 @@ def test_xstage_register_fft_matches_stockham(tmp_path, kind, M):
     tool = os.path.join(root, "tools", "xstage_ab.py")
     a, b = tmp_path / "reg.npy", tmp_path / "stockham.npy"
     subprocess.run([sys.executable, tool, str(a), kind, str(M)], check=True)
-    env = dict(os.environ, HS_XSTAGE_STOCKHAM="1")
+    env = dict(os.environ, **{alt: "1"})
     subprocess.run([sys.executable, tool, str(b), kind, str(M)], check=True, env=env)
     ua, ub = np.load(a), np.load(b)
     assert rel_l2(ua, ub) < 1e-12
