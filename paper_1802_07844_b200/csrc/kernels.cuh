@@ -118,6 +118,12 @@ hs_status launch_kscale(hs_ctx* ctx, int kind, int half, const KGeom& k, const d
 // Green's table precompute (ewald_fourier.py:154-174,207-244)
 hs_status launch_greens_hat(hs_ctx* ctx, int kind, double R, double h, const int64_t big[3],
                             double2* out);
+// separable table precompute pieces (kspace.cu)
+hs_status launch_hat_lines(hs_ctx* ctx, int kind, double R, double h, const int64_t big[3], int64_t l0, int64_t nl,
+                           int64_t h1, int64_t h2, int64_t ltot, double2* out);
+hs_status launch_sep_scatter(hs_ctx* ctx, const double* src, int64_t l0, int64_t nl, int64_t ltot, int64_t n,
+                             int64_t kp, int64_t na, int64_t nb, double scale, double2* dst, double* dst_real);
+hs_status launch_sep_crop(hs_ctx* ctx, const double* F, const int64_t k[3], double* crop);
 hs_status launch_crop(hs_ctx* ctx, const double* field, const int64_t big[3], const int64_t keep[3], double scale,
                       double* crop);
 hs_status launch_real_part(hs_ctx* ctx, const double2* spec, int64_t n, double* out);

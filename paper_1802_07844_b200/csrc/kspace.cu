@@ -167,6 +167,25 @@ hs_status launch_kscale(hs_ctx* ctx, int kind, int half, const KGeom& k, const d
 
 // ---------------------------------------------------------------------------
 // Green's tables (ewald_fourier.py:154-174 truncated_greens_hat, :207-244 precompute_greens)
+// truncated Green's function at |k| (ewald_fourier.py:154-174)
+__device__ __forceinline__ double greens_hat_value(int kind, double R, double kmag) {
+  const double x = R * kmag;
+  if (kind == HS_HARMONIC) {
+    // 2 pi R^2 sinc(x / 2 pi)^2, np.sinc(t) = sin(pi t)/(pi t)
+    const double t = x / (2.0 * kPi);
+    double sc = 1.0;
+    if (t != 0.0) {
+      const double pt = kPi * t;
+      sc = sin(pt) / pt;
+    }
+    return 2.0 * kPi * R * R * sc * sc;
+  }
+  const double R4 = R * R * R * R;
+  const double x2 = x * x;
+  if (x < 0.3) return kPi * R4 * (1.0 - x2 / 9.0 + x2 * x2 / 240.0 - x2 * x2 * x2 / 12600.0);
+  return 4.0 * kPi * R4 * ((2.0 - x2) * cos(x) + 2.0 * x * sin(x) - 2.0) / (x2 * x2);
+}
+
 __global__ void k_greens_hat(int kind, double R, double ks0, double ks1, double ks2, int64_t n0, int64_t n1,
                              int64_t n2, int64_t nzh, double2* __restrict__ out) {
   const int64_t npt = n0 * n1 * nzh;
@@ -178,30 +197,88 @@ __global__ void k_greens_hat(int kind, double R, double ks0, double ks1, double 
     const double kx = (2.0 * kPi) * ((double)fx * ks0);
     const double ky = (2.0 * kPi) * ((double)fy * ks1);
     const double kz = (2.0 * kPi) * ((double)iz * ks2);  // rfftfreq: 0..n/2
-    const double kmag = sqrt(kx * kx + ky * ky + kz * kz);
-    const double x = R * kmag;
-    double v;
-    if (kind == HS_HARMONIC) {
-      // 2 pi R^2 sinc(x / 2 pi)^2, np.sinc(t) = sin(pi t)/(pi t)
-      const double t = x / (2.0 * kPi);
-      double sc = 1.0;
-      if (t != 0.0) {
-        const double pt = kPi * t;
-        sc = sin(pt) / pt;
-      }
-      v = 2.0 * kPi * R * R * sc * sc;
-    } else {
-      const double R4 = R * R * R * R;
-      if (x < 0.3) {
-        const double x2 = x * x;
-        v = kPi * R4 * (1.0 - x2 / 9.0 + x2 * x2 / 240.0 - x2 * x2 * x2 / 12600.0);
-      } else {
-        const double x2 = x * x;
-        v = 4.0 * kPi * R4 * ((2.0 - x2) * cos(x) + 2.0 * x * sin(x) - 2.0) / (x2 * x2);
-      }
+    out[i] = make_double2(greens_hat_value(kind, R, sqrt(kx * kx + ky * ky + kz * kz)), 0.0);
+  }
+}
+
+// ---- separable, pruned table precompute (no big-grid array) --------------------------------
+// The truncated Green's function is real and even in every frequency index, so the
+// irfftn on the oversampled grid is a product of three cosine transforms, each a 1-D C2R
+// of a real "half spectrum".  Evaluated dimension by dimension (z, then y, then x), keeping
+// after each stage only the real-space nodes the crop needs (0..k_i, with the crop's
+// wrapped half following from evenness), the largest intermediate is
+// h0 x (k2+1) x h1 complex instead of the big grid.
+// stage-1 input: lines l = (kx, ky) in [0,h0) x [0,h1), values at kz in [0, h2)
+__global__ void k_hat_lines(int kind, double R, double ks0, double ks1, double ks2, int64_t l0, int64_t nl, int64_t h1,
+                            int64_t h2, int64_t ltot, double2* __restrict__ out) {
+  const int64_t npt = nl * h2;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < npt; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t line = l0 + i / h2, kz = i % h2;
+    double v = 0.0;
+    if (line < ltot) {
+      const int64_t kx = line / h1, ky = line % h1;
+      const double a = (2.0 * kPi) * ((double)kx * ks0), b = (2.0 * kPi) * ((double)ky * ks1),
+                   c = (2.0 * kPi) * ((double)kz * ks2);
+      v = greens_hat_value(kind, R, sqrt(a * a + b * b + c * c));
     }
     out[i] = make_double2(v, 0.0);
   }
+}
+
+// real C2R outputs of lines [l0, l0+nl) (length n each) -> next stage, keeping nodes 0..kp-1:
+// line l = (a, b), b in [0, nb), a in [0, na): dst[((node * na) + a) * nb + b] = (scale v, 0)
+// (complex rows of the next transform, b contiguous), or, when dst_real != null,
+// dst_real[l * kp + node] = scale v
+__global__ void k_sep_scatter(const double* __restrict__ src, int64_t l0, int64_t nl, int64_t ltot, int64_t n,
+                              int64_t kp, int64_t na, int64_t nb, double scale, double2* __restrict__ dst,
+                              double* __restrict__ dst_real) {
+  const int64_t npt = nl * kp;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < npt; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t li = i / kp, node = i % kp, line = l0 + li;
+    if (line >= ltot) continue;
+    const double v = scale * src[li * n + node];
+    if (dst_real) {
+      dst_real[line * kp + node] = v;
+    } else {
+      const int64_t a = line / nb, b = line % nb;
+      dst[(node * na + a) * nb + b] = make_double2(v, 0.0);
+    }
+  }
+}
+
+// crop[cx][cy][cz] (shape 2k) = F[|y|][|z|][|x|] with |c| = c < k ? c : 2k - c; F: (k1+1, k2+1, k0+1)
+__global__ void k_sep_crop(const double* __restrict__ F, int64_t k0, int64_t k1, int64_t k2,
+                           double* __restrict__ crop) {
+  const int64_t c0 = 2 * k0, c1 = 2 * k1, c2 = 2 * k2;
+  const int64_t npt = c0 * c1 * c2;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < npt; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t z = i % c2, y = (i / c2) % c1, x = i / (c2 * c1);
+    const int64_t ax = x < k0 ? x : c0 - x, ay = y < k1 ? y : c1 - y, az = z < k2 ? z : c2 - z;
+    crop[i] = F[(ay * (k2 + 1) + az) * (k0 + 1) + ax];
+  }
+}
+
+hs_status launch_hat_lines(hs_ctx* ctx, int kind, double R, double h, const int64_t big[3], int64_t l0, int64_t nl,
+                           int64_t h1, int64_t h2, int64_t ltot, double2* out) {
+  const int gs = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(nl * h2, 256), (int64_t)ctx->sm_count * 16));
+  k_hat_lines<<<gs, 256, 0, ctx->stream>>>(kind, R, 1.0 / ((double)big[0] * h), 1.0 / ((double)big[1] * h),
+                                           1.0 / ((double)big[2] * h), l0, nl, h1, h2, ltot, out);
+  HS_LAUNCHED(ctx);
+  return HS_OK;
+}
+hs_status launch_sep_scatter(hs_ctx* ctx, const double* src, int64_t l0, int64_t nl, int64_t ltot, int64_t n,
+                             int64_t kp, int64_t na, int64_t nb, double scale, double2* dst, double* dst_real) {
+  const int gs = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(nl * kp, 256), (int64_t)ctx->sm_count * 16));
+  k_sep_scatter<<<gs, 256, 0, ctx->stream>>>(src, l0, nl, ltot, n, kp, na, nb, scale, dst, dst_real);
+  HS_LAUNCHED(ctx);
+  return HS_OK;
+}
+hs_status launch_sep_crop(hs_ctx* ctx, const double* F, const int64_t k[3], double* crop) {
+  const int64_t npt = 8 * k[0] * k[1] * k[2];
+  const int gs = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(npt, 256), (int64_t)ctx->sm_count * 16));
+  k_sep_crop<<<gs, 256, 0, ctx->stream>>>(F, k[0], k[1], k[2], crop);
+  HS_LAUNCHED(ctx);
+  return HS_OK;
 }
 
 hs_status launch_greens_hat(hs_ctx* ctx, int kind, double R, double h, const int64_t big[3], double2* out) {

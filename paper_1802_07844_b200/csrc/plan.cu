@@ -518,8 +518,179 @@ extern "C" hs_status hs_plan_set_table(hs_plan* p, int table_kind, const double*
 
 namespace hs {
 // precompute_greens into a half-spectrum real table (ewald_fourier.py:207-244)
+static hs_status greens_half_table_full(hs_ctx* ctx, int kind, double R, double h, const int64_t big[3],
+                                        const int64_t dims[3], const int64_t guards[3], const int64_t pd[3],
+                                        double* half_out);
+
+// Separable, pruned precompute (kspace.cu k_hat_lines / k_sep_scatter / k_sep_crop): the
+// oversampled grid never exists; three batched 1-D C2R stages (z, y, x) keep only the
+// real-space nodes 0..k_i of the crop after each stage.  Peak memory at cfg5 (big
+// (1432,1432,2864)): ~12 GB of intermediates + the pd-sized crop and its spectrum, instead
+// of 94 GB.  HS_TABLE_FULL=1 selects the 3-D big-grid transform (comparison).
 hs_status greens_half_table(hs_ctx* ctx, int kind, double R, double h, const int64_t big[3], const int64_t dims[3],
                             const int64_t guards[3], const int64_t pd[3], double* half_out) {
+  if (getenv("HS_TABLE_FULL")) return greens_half_table_full(ctx, kind, R, h, big, dims, guards, pd, half_out);
+  cudaStream_t st = ctx->stream;
+  const int64_t n[3] = {big[0], big[1], big[2]};
+  const int64_t hh[3] = {n[0] / 2 + 1, n[1] / 2 + 1, n[2] / 2 + 1};
+  int64_t k[3], kp[3];
+  for (int d = 0; d < 3; ++d) {
+    k[d] = dims[d] + guards[d];
+    kp[d] = k[d] + 1;
+    if (2 * k[d] != pd[d] || 2 * k[d] > n[d]) return fail(HS_ERR_PARAMETER, "precompute: crop does not match the grids");
+  }
+  const double scale = 1.0 / ((double)n[0] * (double)n[1] * (double)n[2]);
+  const int64_t lt1 = hh[0] * hh[1], lt2 = kp[2] * hh[0], lt3 = kp[1] * kp[2];
+  // lines per chunk: ~512 MB of line buffers per stage
+  auto chunk = [](int64_t len_in_c, int64_t len_out_r, int64_t ltot) {
+    const int64_t per = 16 * len_in_c + 8 * len_out_r;
+    return std::max<int64_t>(1, std::min<int64_t>(ltot, ((int64_t)512 << 20) / per));
+  };
+  const int64_t B1 = chunk(hh[2], n[2], lt1), B2 = chunk(hh[1], n[1], lt2), B3 = chunk(hh[0], n[0], lt3);
+  double2 *lin = nullptr, *A2 = nullptr, *A3 = nullptr, *spec = nullptr;
+  double *lout = nullptr, *F = nullptr, *crop = nullptr;
+  void* ws = nullptr;
+  cufftHandle pl[3] = {0, 0, 0}, pf = 0;
+  hs_status rs = HS_OK;
+  auto cleanup = [&]() {
+    for (auto& q : pl)
+      if (q) cufftDestroy(q);
+    if (pf) cufftDestroy(pf);
+    cudaFree(lin);
+    cudaFree(lout);
+    cudaFree(A2);
+    cudaFree(A3);
+    cudaFree(F);
+    cudaFree(crop);
+    cudaFree(spec);
+    cudaFree(ws);
+  };
+  auto alloc = [&](void** ptr, size_t bytes) {
+    if (cudaMalloc(ptr, std::max<size_t>(bytes, 16)) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    return true;
+  };
+  do {
+    const size_t lin_b = 16 * (size_t)std::max(B1 * hh[2], 1L), lout_b = 8 * (size_t)std::max(B1 * n[2], 1L);
+    const size_t lin2 = 16 * (size_t)std::max(B2 * hh[1], B3 * hh[0]), lout2 = 8 * (size_t)std::max(B2 * n[1], B3 * n[0]);
+    if (!alloc((void**)&lin, std::max(lin_b, lin2)) || !alloc((void**)&lout, std::max(lout_b, lout2)) ||
+        !alloc((void**)&A2, 16 * (size_t)(lt2 + B2) * hh[1])) {
+      rs = fail(HS_ERR_RESOURCE, "precompute: intermediate allocation failed");
+      break;
+    }
+    // batched 1-D C2R plans (contiguous lines), one shared work area
+    size_t wsz[3] = {0, 0, 0};
+    const int64_t Bs[3] = {B1, B2, B3}, len[3] = {n[2], n[1], n[0]}, hin[3] = {hh[2], hh[1], hh[0]};
+    bool ok = true;
+    for (int s = 0; s < 3 && ok; ++s) {
+      long long nn[1] = {len[s]}, ni[1] = {hin[s]}, no[1] = {len[s]};
+      ok = cufftCreate(&pl[s]) == CUFFT_SUCCESS && cufftSetAutoAllocation(pl[s], 0) == CUFFT_SUCCESS &&
+           cufftMakePlanMany64(pl[s], 1, nn, ni, 1, hin[s], no, 1, len[s], CUFFT_Z2D, Bs[s], &wsz[s]) == CUFFT_SUCCESS;
+    }
+    if (!ok) {
+      rs = fail(HS_ERR_RESOURCE, "precompute: cuFFT C2R plan failed");
+      break;
+    }
+    const size_t wmax = std::max(wsz[0], std::max(wsz[1], wsz[2]));
+    if (!alloc(&ws, wmax)) {
+      rs = fail(HS_ERR_RESOURCE, "precompute: cuFFT work area allocation failed");
+      break;
+    }
+    for (auto& q : pl) {
+      cufftSetWorkArea(q, ws);
+      cufftSetStream(q, st);
+    }
+    // stage 1 (z): lines (kx, ky), generated on the fly
+    for (int64_t l0 = 0; l0 < lt1 && rs == HS_OK; l0 += B1) {
+      if ((rs = launch_hat_lines(ctx, kind, R, h, big, l0, B1, hh[1], hh[2], lt1, lin)) != HS_OK) break;
+      if (cufftExecZ2D(pl[0], (cufftDoubleComplex*)lin, lout) != CUFFT_SUCCESS) {
+        rs = fail(HS_ERR_CUDA, "precompute: z C2R failed");
+        break;
+      }
+      rs = launch_sep_scatter(ctx, lout, l0, B1, lt1, n[2], kp[2], hh[0], hh[1], 1.0, A2, nullptr);
+    }
+    if (rs != HS_OK) break;
+    if (!alloc((void**)&A3, 16 * (size_t)(lt3 + B3) * hh[0])) {
+      rs = fail(HS_ERR_RESOURCE, "precompute: intermediate allocation failed");
+      break;
+    }
+    // stage 2 (y): rows (z, kx) of A2
+    for (int64_t l0 = 0; l0 < lt2 && rs == HS_OK; l0 += B2) {
+      if (cufftExecZ2D(pl[1], (cufftDoubleComplex*)(A2 + l0 * hh[1]), lout) != CUFFT_SUCCESS) {
+        rs = fail(HS_ERR_CUDA, "precompute: y C2R failed");
+        break;
+      }
+      rs = launch_sep_scatter(ctx, lout, l0, B2, lt2, n[1], kp[1], kp[2], hh[0], 1.0, A3, nullptr);
+    }
+    if (rs != HS_OK) break;
+    HS_CUDA(cudaStreamSynchronize(st));
+    cudaFree(A2);
+    A2 = nullptr;
+    if (!alloc((void**)&F, 8 * (size_t)lt3 * kp[0])) {
+      rs = fail(HS_ERR_RESOURCE, "precompute: intermediate allocation failed");
+      break;
+    }
+    // stage 3 (x): rows (y, z) of A3
+    for (int64_t l0 = 0; l0 < lt3 && rs == HS_OK; l0 += B3) {
+      if (cufftExecZ2D(pl[2], (cufftDoubleComplex*)(A3 + l0 * hh[0]), lout) != CUFFT_SUCCESS) {
+        rs = fail(HS_ERR_CUDA, "precompute: x C2R failed");
+        break;
+      }
+      rs = launch_sep_scatter(ctx, lout, l0, B3, lt3, n[0], kp[0], 0, 0, scale, nullptr, F);
+    }
+    if (rs != HS_OK) break;
+    HS_CUDA(cudaStreamSynchronize(st));
+    for (auto& q : pl) {
+      cufftDestroy(q);
+      q = 0;
+    }
+    cudaFree(A3);
+    A3 = nullptr;
+    cudaFree(lin);
+    lin = nullptr;
+    cudaFree(lout);
+    lout = nullptr;
+    cudaFree(ws);
+    ws = nullptr;
+    // crop (evenness) and the forward transform on the padded grid
+    const size_t ncrop = (size_t)pd[0] * pd[1] * pd[2], nch = (size_t)pd[0] * pd[1] * (pd[2] / 2 + 1);
+    if (!alloc((void**)&crop, 8 * ncrop) || !alloc((void**)&spec, 16 * nch)) {
+      rs = fail(HS_ERR_RESOURCE, "precompute: padded-grid allocation failed");
+      break;
+    }
+    if ((rs = launch_sep_crop(ctx, F, k, crop)) != HS_OK) break;
+    long long np[3] = {pd[0], pd[1], pd[2]};
+    size_t w2 = 0;
+    if (cufftCreate(&pf) != CUFFT_SUCCESS || cufftSetAutoAllocation(pf, 0) != CUFFT_SUCCESS ||
+        cufftMakePlanMany64(pf, 3, np, nullptr, 1, 0, nullptr, 1, 0, CUFFT_D2Z, 1, &w2) != CUFFT_SUCCESS) {
+      rs = fail(HS_ERR_RESOURCE, "precompute: cuFFT D2Z plan failed");
+      break;
+    }
+    if (!alloc(&ws, w2)) {
+      rs = fail(HS_ERR_RESOURCE, "precompute: cuFFT work area allocation failed");
+      break;
+    }
+    cufftSetWorkArea(pf, ws);
+    cufftSetStream(pf, st);
+    if (cufftExecD2Z(pf, crop, (cufftDoubleComplex*)spec) != CUFFT_SUCCESS) {
+      rs = fail(HS_ERR_CUDA, "precompute: D2Z failed");
+      break;
+    }
+    if ((rs = launch_real_part(ctx, spec, (int64_t)nch, half_out)) != HS_OK) break;
+    if (cudaStreamSynchronize(st) != cudaSuccess) {
+      rs = fail(HS_ERR_CUDA, "precompute: stream sync failed");
+      break;
+    }
+  } while (false);
+  cleanup();
+  return rs;
+}
+
+static hs_status greens_half_table_full(hs_ctx* ctx, int kind, double R, double h, const int64_t big[3],
+                                        const int64_t dims[3], const int64_t guards[3], const int64_t pd[3],
+                                        double* half_out) {
   cudaStream_t st = ctx->stream;
   const int64_t nzb = big[2] / 2 + 1;
   const size_t nbh = (size_t)big[0] * big[1] * nzb, nbr = (size_t)big[0] * big[1] * big[2];

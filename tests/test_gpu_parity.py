@@ -358,3 +358,19 @@ def test_register_fft_stages_match_alternatives(tmp_path, kind, M, alt):
     subprocess.run([sys.executable, tool, str(b), kind, str(M)], check=True, env=env)
     ua, ub = np.load(a), np.load(b)
     assert rel_l2(ua, ub) < 1e-12
+
+
+@pytest.mark.parametrize("kind", ("harmonic", "biharmonic"))
+def test_separable_tables_match_full_grid(tmp_path, kind):
+    """The separable pruned table precompute against the 3-D big-grid transform (each selected
+    in its own process) on a moderate grid."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    tool = os.path.join(root, "tools", "table_ab.py")
+    a, b = tmp_path / "sep.npy", tmp_path / "full.npy"
+    subprocess.run([sys.executable, tool, str(a), kind, "64"], check=True)
+    subprocess.run([sys.executable, tool, str(b), kind, "64"], check=True, env=dict(os.environ, HS_TABLE_FULL="1"))
+    ta, tb = np.load(a), np.load(b)
+    assert rel_l2(ta, tb) < 1e-12
