@@ -10,12 +10,13 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import gc
 import threading
 
 import numpy as np
 
 from . import _lib
-from .errors import ParameterError
+from .errors import ResourceError, ParameterError
 
 TIME_KEYS = ("gridding", "fft", "scale", "ifft", "gather", "real", "fourier", "prep", "total", "io",
              "k_pair", "k_spread", "k_gather", "k_scale", "pairs", "image_pairs")
@@ -164,7 +165,13 @@ def get_evaluator(kind, geometry, L, xi, rc, grid, n, n_targets, targets_are_sou
         if ev is None:
             while len(_cache) >= _CACHE_MAX:
                 _cache.pop(next(iter(_cache)))
-            ev = Evaluator(kind, geometry, L, xi, rc, grid, n, n_targets, targets_are_sources)
+            try:
+                ev = Evaluator(kind, geometry, L, xi, rc, grid, n, n_targets, targets_are_sources)
+            except ResourceError:
+                # device memory held by cached plans of other shapes: release them and retry once
+                _cache.clear()
+                gc.collect()
+                ev = Evaluator(kind, geometry, L, xi, rc, grid, n, n_targets, targets_are_sources)
             _cache[key] = ev
         return ev
 

@@ -374,3 +374,19 @@ def test_separable_tables_match_full_grid(tmp_path, kind):
     subprocess.run([sys.executable, tool, str(b), kind, "64"], check=True, env=dict(os.environ, HS_TABLE_FULL="1"))
     ta, tb = np.load(a), np.load(b)
     assert rel_l2(ta, tb) < 1e-12
+
+
+def test_cfg5_full_size_vs_direct_subset(gpu):
+    """BASELINE configs[4] (4e6 sources, 4e6 separate targets, L=2, M=384: padded grid
+    (864,864,1680), ~100 GB plan, separable table precompute) at full size against the direct
+    half-space sum on a target subset."""
+    from paper_1802_07844_b200.configs import WORKLOADS, make_system
+    from paper_1802_07844_b200 import _plan
+    _plan.clear_cache()
+    w = WORKLOADS["cfg5"]
+    s, tg = make_system(w)
+    try:
+        err = _subset_direct_check(gpu, s, tg, gpu.EwaldParams(xi=w.xi, rc=w.rc, M=w.M, P=w.P), nsub=200)
+    finally:
+        _plan.clear_cache()   # release the ~100 GB plan
+    assert err < 1e-8, err
