@@ -340,20 +340,23 @@ __global__ void __launch_bounds__(XF_THREADS, 2) k_xfused(const XArgs a) {
 // makes a round trip per radix pass).
 __constant__ double2 c_w15[15];  // exp(-2 pi i m / 15)
 __constant__ double2 c_w11[11];  // exp(-2 pi i m / 11)
+__constant__ double2 c_w27[27];  // exp(-2 pi i m / 27)
 __constant__ double2 c_w16[16];  // exp(-2 pi i m / 16)
 __constant__ double2 c_w32[16];  // exp(-2 pi i m / 32)
 static bool g_xreg_consts = false;
 
 static hs_status xreg_constants() {
   if (g_xreg_consts) return HS_OK;
-  double2 w15[15], w16[16], w32[16], w11[11];
+  double2 w15[15], w16[16], w32[16], w11[11], w27[27];
   const long double tp = 6.283185307179586476925286766559005768L;
   for (int m = 0; m < 15; ++m) w15[m] = make_double2((double)std::cos(tp * m / 15), (double)-std::sin(tp * m / 15));
+  for (int m = 0; m < 27; ++m) w27[m] = make_double2((double)std::cos(tp * m / 27), (double)-std::sin(tp * m / 27));
   for (int m = 0; m < 11; ++m) w11[m] = make_double2((double)std::cos(tp * m / 11), (double)-std::sin(tp * m / 11));
   for (int m = 0; m < 16; ++m) w16[m] = make_double2((double)std::cos(tp * m / 16), (double)-std::sin(tp * m / 16));
   for (int m = 0; m < 16; ++m) w32[m] = make_double2((double)std::cos(tp * m / 32), (double)-std::sin(tp * m / 32));
   HS_CUDA(cudaMemcpyToSymbol(c_w15, w15, sizeof(w15)));
   HS_CUDA(cudaMemcpyToSymbol(c_w11, w11, sizeof(w11)));
+  HS_CUDA(cudaMemcpyToSymbol(c_w27, w27, sizeof(w27)));
   HS_CUDA(cudaMemcpyToSymbol(c_w16, w16, sizeof(w16)));
   HS_CUDA(cudaMemcpyToSymbol(c_w32, w32, sizeof(w32)));
   g_xreg_consts = true;
@@ -430,19 +433,67 @@ __device__ __forceinline__ void dft11(double2* v) {
   for (int k = 0; k < 11; ++k) v[k] = y[k];
 }
 
+// DFT-9 in place: j = j1 + 3 j2, k = 3 k1 + k2 (W9^m = W27^{3m})
+__device__ __forceinline__ void dft9(double2* v) {
+  double2 Y[3][3];
+#pragma unroll
+  for (int j1 = 0; j1 < 3; ++j1) {
+    double2 t[3] = {v[j1], v[j1 + 3], v[j1 + 6]};
+    dft<3>(t);
+#pragma unroll
+    for (int k2 = 0; k2 < 3; ++k2) Y[j1][k2] = (j1 * k2 == 0) ? t[k2] : cm(t[k2], c_w27[3 * j1 * k2]);
+  }
+#pragma unroll
+  for (int k2 = 0; k2 < 3; ++k2) {
+    double2 t[3] = {Y[0][k2], Y[1][k2], Y[2][k2]};
+    dft<3>(t);
+#pragma unroll
+    for (int k1 = 0; k1 < 3; ++k1) v[3 * k1 + k2] = t[k1];
+  }
+}
+
+// DFT-27 in place: j = j1 + 3 j2 (j2 < 9), k = 9 k1 + k2 (DFT9 over j2, twiddle W27^{j1 k2}, DFT3)
+__device__ __forceinline__ void dft27(double2* v) {
+  double2 Y[3][9];
+#pragma unroll
+  for (int j1 = 0; j1 < 3; ++j1) {
+    double2 t[9];
+#pragma unroll
+    for (int j2 = 0; j2 < 9; ++j2) t[j2] = v[j1 + 3 * j2];
+    dft9(t);
+#pragma unroll
+    for (int k2 = 0; k2 < 9; ++k2) Y[j1][k2] = (j1 * k2 == 0) ? t[k2] : cm(t[k2], c_w27[j1 * k2]);
+  }
+#pragma unroll
+  for (int k2 = 0; k2 < 9; ++k2) {
+    double2 t[3] = {Y[0][k2], Y[1][k2], Y[2][k2]};
+    dft<3>(t);
+#pragma unroll
+    for (int k1 = 0; k1 < 3; ++k1) v[9 * k1 + k2] = t[k1];
+  }
+}
+
 template <int M>
 __device__ __forceinline__ void dftM(double2* v) {
-  static_assert(M == 15 || M == 11, "register x-stage: M = 15 (N = 480) or 11 (N = 352)");
+  static_assert(M == 15 || M == 11 || M == 27, "register FFT: M = 15 (N = 480), 11 (352), 27 (864)");
   if constexpr (M == 15)
     dft15(v);
-  else
+  else if constexpr (M == 11)
     dft11(v);
+  else
+    dft27(v);
 }
 
 // forward DFT of the line whose element l + 32 j is v[j]; S: warp scratch (M x 33);
-// tw: pd8-padded W_N^i table; out: X[r + M (k' + 16 h)], k' < 16 (r = lane/2 < M)
+// tw: pd8-padded W_N^i table; out[g]: X[r + M (k' + 16 h)], k' < 16, for the row r = 16 g + lane/2
+// (< M) of row group g (M <= 16: one group; M = 27: two, the second half-populated)
 template <int M>
-__device__ __forceinline__ void warp_fft_reg(double2* v, double2* S, const double2* tw, int lane, double2* out) {
+struct RegFFT {
+  static constexpr int NG = (M + 15) / 16;
+};
+template <int M>
+__device__ __forceinline__ void warp_fft_reg(double2* v, double2* S, const double2* tw, int lane,
+                                             double2 (*out)[16]) {
   dftM<M>(v);
 #pragma unroll
   for (int k1 = 1; k1 < M; ++k1) v[k1] = cm(v[k1], tw[pd8(lane * k1)]);
@@ -450,24 +501,31 @@ __device__ __forceinline__ void warp_fft_reg(double2* v, double2* S, const doubl
 #pragma unroll
   for (int k1 = 0; k1 < M; ++k1) S[k1 * 33 + lane] = v[k1];
   __syncwarp();
-  const int r = lane >> 1, h = lane & 1;
-  const int rr = r < M ? r : M - 1;
+  const int h = lane & 1;
 #pragma unroll
-  for (int m = 0; m < 16; ++m) out[m] = S[rr * 33 + 2 * m + h];
-  dft16(out);
-  // radix-2 combine across the lane pair: X[k'] = Y0 + W32^k' Y1, X[k'+16] = Y0 - W32^k' Y1
+  for (int g = 0; g < RegFFT<M>::NG; ++g) {
+    const int r = 16 * g + (lane >> 1);
+    const int rr = r < M ? r : M - 1;
 #pragma unroll
-  for (int k = 0; k < 16; ++k) {
-    const double2 t = (h && k) ? cm(out[k], c_w32[k]) : out[k];  // h = 1 holds Y1
-    double2 p;
-    p.x = __shfl_xor_sync(0xffffffffu, t.x, 1);
-    p.y = __shfl_xor_sync(0xffffffffu, t.y, 1);
-    out[k] = h ? sb(p, t) : ad(t, p);
+    for (int m = 0; m < 16; ++m) out[g][m] = S[rr * 33 + 2 * m + h];
+  }
+#pragma unroll
+  for (int g = 0; g < RegFFT<M>::NG; ++g) {
+    dft16(out[g]);
+    // radix-2 combine across the lane pair: X[k'] = Y0 + W32^k' Y1, X[k'+16] = Y0 - W32^k' Y1
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      const double2 t = (h && k) ? cm(out[g][k], c_w32[k]) : out[g][k];  // h = 1 holds Y1
+      double2 p;
+      p.x = __shfl_xor_sync(0xffffffffu, t.x, 1);
+      p.y = __shfl_xor_sync(0xffffffffu, t.y, 1);
+      out[g][k] = h ? sb(p, t) : ad(t, p);
+    }
   }
 }
 
 template <int KIND, bool HALF, int M>
-__global__ void __launch_bounds__(XF_THREADS, 2) k_xreg(const XArgs a) {
+__global__ void __launch_bounds__(XF_THREADS, M == 27 ? 1 : 2) k_xreg(const XArgs a) {
   constexpr int N = 32 * M, LSR = M * 33;
   constexpr int NIN = KChan<KIND, HALF>::NIN, NOUT = KChan<KIND, HALF>::NOUT;
   constexpr int NL = NIN > NOUT ? NIN : NOUT, NW = XF_THREADS / 32;
@@ -484,7 +542,7 @@ __global__ void __launch_bounds__(XF_THREADS, 2) k_xreg(const XArgs a) {
     const int kz = item - ky * a.nzh;
     __syncthreads();  // previous item's lines consumed (and twiddles visible)
     for (int c = warp; c < NIN; c += NW) {
-      double2 v[M], out[16];
+      double2 v[M], out[RegFFT<M>::NG][16];
       const double2* src = a.B + c * a.ch_stride + (int64_t)ky * a.nx * a.nzh + kz;
 #pragma unroll
       for (int j = 0; j < M; ++j) {
@@ -494,9 +552,13 @@ __global__ void __launch_bounds__(XF_THREADS, 2) k_xreg(const XArgs a) {
       double2* S = lines + c * LSR;
       warp_fft_reg<M>(v, S, tw, lane, out);
       __syncwarp();
-      if (r < M) {
 #pragma unroll
-        for (int k = 0; k < 16; ++k) S[r + M * (k + 16 * h)] = out[k];
+      for (int g = 0; g < RegFFT<M>::NG; ++g) {
+        const int rg = r + 16 * g;
+        if (rg < M) {
+#pragma unroll
+          for (int k = 0; k < 16; ++k) S[rg + M * (k + 16 * h)] = out[g][k];
+        }
       }
     }
     __syncthreads();
@@ -529,17 +591,21 @@ __global__ void __launch_bounds__(XF_THREADS, 2) k_xreg(const XArgs a) {
     }
     __syncthreads();
     for (int o = warp; o < NOUT; o += NW) {
-      double2 v[M], out[16];
+      double2 v[M], out[RegFFT<M>::NG][16];
       double2* S = lines + o * LSR;
 #pragma unroll
       for (int j = 0; j < M; ++j) v[j] = S[lane + 32 * j];
       warp_fft_reg<M>(v, S, tw, lane, out);
-      if (r < M) {
-        double2* dst = a.B + o * a.ch_stride + (int64_t)ky * a.nx * a.nzh + kz;
+      double2* dst = a.B + o * a.ch_stride + (int64_t)ky * a.nx * a.nzh + kz;
 #pragma unroll
-        for (int k = 0; k < 16; ++k) {
-          const int x = r + M * (k + 16 * h);
-          if (x < a.nx) dst[(int64_t)x * a.nzh] = make_double2(out[k].x, -out[k].y);
+      for (int g = 0; g < RegFFT<M>::NG; ++g) {
+        const int rg = r + 16 * g;
+        if (rg < M) {
+#pragma unroll
+          for (int k = 0; k < 16; ++k) {
+            const int x = rg + M * (k + 16 * h);
+            if (x < a.nx) dst[(int64_t)x * a.nzh] = make_double2(out[g][k].x, -out[g][k].y);
+          }
         }
       }
     }
@@ -573,7 +639,7 @@ static hs_status launch_xreg_t(hs_ctx* ctx, const XArgs& a) {
 constexpr int YS_KB = 8, YS_RS = YS_KB + 1;  // kz per CTA, padded row length (bank spread)
 
 template <int M, bool FWD>
-__global__ void __launch_bounds__(256, 2) k_ystage(const double2* __restrict__ in, double2* __restrict__ out,
+__global__ void __launch_bounds__(256, M == 27 ? 1 : 2) k_ystage(const double2* __restrict__ in, double2* __restrict__ out,
                                                   const double2* __restrict__ twg, int nx, int nzh, int ny) {
   constexpr int N = 32 * M;
   extern __shared__ double2 smem[];
@@ -599,7 +665,7 @@ __global__ void __launch_bounds__(256, 2) k_ystage(const double2* __restrict__ i
     cp_async_commit();
     cp_async_wait_all();
     __syncthreads();
-    double2 v[M], o16[16];
+    double2 v[M], o16[RegFFT<M>::NG][16];
 #pragma unroll
     for (int j = 0; j < M; ++j) {
       const int row = lane + 32 * j;
@@ -610,13 +676,17 @@ __global__ void __launch_bounds__(256, 2) k_ystage(const double2* __restrict__ i
     __syncthreads();  // every column read: the buffer becomes transpose scratch
     warp_fft_reg<M>(v, buf + warp * M * 33, tw, lane, o16);
     __syncthreads();  // scratch use finished: the buffer collects the output rows
-    if (r < M) {
 #pragma unroll
-      for (int k = 0; k < 16; ++k) {
-        const int row = r + M * (k + 16 * h);
-        double2 e = o16[k];
-        if (!FWD) e.y = -e.y;
-        if (row < rows_out) buf[row * YS_RS + warp] = e;
+    for (int g = 0; g < RegFFT<M>::NG; ++g) {
+      const int rg = r + 16 * g;
+      if (rg < M) {
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          const int row = rg + M * (k + 16 * h);
+          double2 e = o16[g][k];
+          if (!FWD) e.y = -e.y;
+          if (row < rows_out) buf[row * YS_RS + warp] = e;
+        }
       }
     }
     __syncthreads();
@@ -628,7 +698,7 @@ __global__ void __launch_bounds__(256, 2) k_ystage(const double2* __restrict__ i
 }
 
 // y stage of one channel; false when the length has no register kernel (caller uses cuFFT)
-bool ystage_supported(int py) { return py == 480 || py == 352; }
+bool ystage_supported(int py) { return py == 480 || py == 352 || py == 864; }
 hs_status launch_ystage(hs_ctx* ctx, bool fwd, const double2* in, double2* out, const double2* tw, int py, int nx,
                         int nzh, int ny) {
   HS_TRY(xreg_constants());
@@ -643,6 +713,7 @@ hs_status launch_ystage(hs_ctx* ctx, bool fwd, const double2* in, double2* out, 
   };
   if (py == 480) return fwd ? go(k_ystage<15, true>, 15) : go(k_ystage<15, false>, 15);
   if (py == 352) return fwd ? go(k_ystage<11, true>, 11) : go(k_ystage<11, false>, 11);
+  if (py == 864) return fwd ? go(k_ystage<27, true>, 27) : go(k_ystage<27, false>, 27);
   return fail(HS_ERR_PARAMETER, "y stage: unsupported length");
 }
 
@@ -681,7 +752,11 @@ static hs_status launch_xfused_half(hs_ctx* ctx, const XArgs& a) {
       return launch_xfused_t<KIND, true, KB, FixedFFT<8, 4, 3, 5>>(ctx, a);
     }
     case 750: return launch_xfused_t<KIND, true, KB, FixedFFT<2, 3, 5, 5, 5>>(ctx, a);
-    case 864: return launch_xfused_t<KIND, true, KB, FixedFFT<8, 4, 3, 3, 3>>(ctx, a);
+    case 864: {
+      static const bool stockham = getenv("HS_XSTAGE_STOCKHAM") != nullptr;
+      if (!stockham) return launch_xreg_t<KIND, true, 27>(ctx, a);
+      return launch_xfused_t<KIND, true, KB, FixedFFT<8, 4, 3, 3, 3>>(ctx, a);
+    }
     default: return launch_xfused_t<KIND, true, KB, AnyFFT>(ctx, a);
   }
 }
