@@ -138,6 +138,59 @@ hs_status hs_plan_real_parts(hs_plan* plan, double* kernel_part, double* correct
 /* Number of forward / inverse 3-D transforms one execute performs. */
 hs_status hs_plan_fft_counts(const hs_plan* plan, int* n_fft, int* n_ifft);
 
+/* ---- y-slab decomposition of one evaluation over W ranks (multi-GPU) ----
+ * The reference is single-process (ewald_fourier.py:486-636); this is the
+ * sharded form of the same ewald_sum.  Rank r owns grid planes y in [y0, y1)
+ * (all x, z) and half-spectrum columns kz in [kz0, kz1) (all kx, ky).  Its plan
+ * holds ALL sources (real-space neighbours and images are global) and only
+ * its own targets: those whose gather window starts in [y0, y1) (the caller
+ * partitions them, see sharding.py).  One evaluation is five stages with four
+ * exchanges the caller performs (torch.distributed / NCCL, or copies when all
+ * ranks live in one process):
+ *   hs_slab_begin     real-space sums of the rank's targets; spread of the
+ *                     sources whose y window starts in the slab into planes
+ *                     [y0, y1 + P - 1); ghost_out <- planes [y1, y1+P-1) of
+ *                     every channel, layout [n_in][P-1][nx][nz]
+ *   (send ghost_out to rank r+1)
+ *   hs_slab_forward   ghost_in (from r-1, or NULL) added to planes [y0, y0+P-1);
+ *                     z D2Z on owned planes; send <- per channel c the kz
+ *                     blocks of every destination, layout [n_in][W][y1-y0][nx][kz1_s-kz0_s]
+ *   (per channel: all-to-all send[c] -> recv[c]; recv layout [n_in][py][nx][kz1-kz0],
+ *    block s = rows [y0_s, y1_s); rows >= ny must be zero)
+ *   hs_slab_kspace    y transform, fused x transform + k-space scaling, inverse y;
+ *                     back <- [n_out][ny][nx][kz1-kz0]
+ *   (per channel: all-to-all back[c] rows [y0_s, y1_s) -> recv_back[c] block s,
+ *    recv_back layout [n_out][W][y1-y0][nx][kz1_s-kz0_s])
+ *   hs_slab_backward  inverse z on owned planes; halo_out <- output planes
+ *                     [y0, y0+P-1), layout [P-1][nx][nz][pitch]
+ *   (send halo_out to rank r-1)
+ *   hs_slab_finish    halo_in (from r+1, or NULL) fills planes [y1, y1+P-1);
+ *                     gather at the rank's targets; u = real + Fourier.
+ * All exchange buffers are device memory on the plan's device; sizes come from
+ * hs_slab_sizes.  Pointers passed to hs_slab_begin (inputs) must stay valid
+ * until hs_slab_finish returns. */
+typedef struct {
+  int64_t rank, world;
+  int64_t y0, y1;         /* owned grid planes */
+  int64_t kz0, kz1;       /* owned half-spectrum columns */
+  int64_t kz_split[65];   /* column boundaries of all ranks: rank s owns [kz_split[s], kz_split[s+1]) */
+  int64_t y_split[65];    /* plane boundaries of all ranks */
+} hs_slab;
+
+/* Sizes of the exchange buffers, in doubles (complex values count 2):
+ *   [0] ghost: n_in (P-1) nx nz             [1] send / recv_back, per channel: 2 (y1-y0) nx nzh
+ *   [2] recv, per channel: 2 py nx (kz1-kz0)  [3] back, per channel: 2 ny nx (kz1-kz0)
+ *   [4] halo: (P-1) nx nz pitch             [5] n_in   [6] n_out   [7] pitch */
+hs_status hs_plan_create_slab(hs_ctx* ctx, const hs_params* params, const hs_slab* slab, hs_plan** out);
+hs_status hs_slab_sizes(const hs_plan* plan, int64_t sizes[8]);
+hs_status hs_slab_begin(hs_plan* plan, const double* positions, const double* sa, const double* sb,
+                        const double* targets, const int64_t* tcols, int mem, double* ghost_out);
+hs_status hs_slab_forward(hs_plan* plan, const double* ghost_in, double* send);
+hs_status hs_slab_kspace(hs_plan* plan, const double* recv, double* back);
+hs_status hs_slab_backward(hs_plan* plan, const double* recv_back, double* halo_out);
+hs_status hs_slab_finish(hs_plan* plan, const double* halo_in, double* u, double* u_real, double* u_fourier,
+                         int mem, double* times);
+
 /* ---- direct O(N Nt) half-space/free-space sum on the GPU (kernels_direct.py:211-371).
  * Same argument meaning as hs_plan_execute's strengths; returns physically
  * normalised velocities. */

@@ -37,6 +37,15 @@ class HsParams(C.Structure):
     ]
 
 
+class HsSlab(C.Structure):
+    _fields_ = [
+        ("rank", C.c_int64), ("world", C.c_int64), ("y0", C.c_int64), ("y1", C.c_int64),
+        ("kz0", C.c_int64), ("kz1", C.c_int64), ("kz_split", C.c_int64 * 65), ("y_split", C.c_int64 * 65),
+    ]
+
+
+MAX_SLAB_RANKS = 64
+
 # (name, restype, argtypes)
 _SIGS = [
     ("hs_ctx_create", C.c_int, [C.c_int, C.POINTER(C.c_void_p)]),
@@ -62,6 +71,14 @@ _SIGS = [
                                   C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int, _dp]),
     ("hs_plan_real_parts", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int]),
     ("hs_plan_fft_counts", C.c_int, [C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    ("hs_plan_create_slab", C.c_int, [C.c_void_p, C.POINTER(HsParams), C.POINTER(HsSlab), C.POINTER(C.c_void_p)]),
+    ("hs_slab_sizes", C.c_int, [C.c_void_p, _i64p]),
+    ("hs_slab_begin", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int,
+                                C.c_void_p]),
+    ("hs_slab_forward", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    ("hs_slab_kspace", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    ("hs_slab_backward", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    ("hs_slab_finish", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, _dp]),
     ("hs_direct_sum", C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p,
                                 C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int]),
 ]

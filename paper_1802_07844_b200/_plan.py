@@ -36,7 +36,7 @@ def _host_f64(a, shape_cols=3):
 class Evaluator:
     """Device plan for one configuration (grid from a GridSpec-like object)."""
 
-    def __init__(self, kind, geometry, L, xi, rc, grid, n, n_targets, targets_are_sources, device=None):
+    def __init__(self, kind, geometry, L, xi, rc, grid, n, n_targets, targets_are_sources, device=None, slab=None):
         self.ctx = _lib.Context.get(device)
         self.lib = self.ctx.lib
         self.kind, self.geometry = kind, geometry
@@ -61,7 +61,10 @@ class Evaluator:
         p.targets_are_sources = 1 if self.targets_are_sources else 0
         self.params = p
         h = C.c_void_p()
-        _lib.check(self.lib.hs_plan_create(self.ctx.handle, C.byref(p), C.byref(h)))
+        if slab is None:
+            _lib.check(self.lib.hs_plan_create(self.ctx.handle, C.byref(p), C.byref(h)))
+        else:   # y-slab share of a sharded evaluation (sharding.py)
+            _lib.check(self.lib.hs_plan_create_slab(self.ctx.handle, C.byref(p), C.byref(slab), C.byref(h)))
         self.handle = h
         self._table_ids = {}
         self.tables_ready = False

@@ -285,8 +285,8 @@ __global__ void __launch_bounds__(XF_THREADS, 2) k_xfused(const XArgs a) {
     for (int i = tid; i < KB * px; i += blockDim.x) {
       const int kb = i / px, kx = i - kb * px;
       if (kb >= kbn) continue;
-      const int kz = kz0 + kb;
-      const int64_t ti = ((int64_t)ky * a.nzh + kz) * px + kx;
+      const int kzl = kz0 + kb, kz = a.kz0 + kzl;  // local column, global wavenumber index
+      const int64_t ti = ((int64_t)ky * a.nzh + kzl) * px + kx;
       const double tB = (KIND == HS_ROTLET) ? 0.0 : a.tabB[ti];
       const double tH = (KIND == HS_ROTLET || HALF) ? a.tabH[ti] : 0.0;
       double2* col = lines + kb * LS + pd8(kx);  // channel c at col[c * KB * LS]
@@ -539,11 +539,11 @@ __global__ void __launch_bounds__(XF_THREADS, M == 27 ? 1 : 2) k_xreg(const XArg
   const int r = lane >> 1, h = lane & 1;
   for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
     const int ky = item / a.nzh;
-    const int kz = item - ky * a.nzh;
+    const int kzl = item - ky * a.nzh, kz = a.kz0 + kzl;  // local column, global wavenumber index
     __syncthreads();  // previous item's lines consumed (and twiddles visible)
     for (int c = warp; c < NIN; c += NW) {
       double2 v[M], out[RegFFT<M>::NG][16];
-      const double2* src = a.B + c * a.ch_stride + (int64_t)ky * a.nx * a.nzh + kz;
+      const double2* src = a.B + c * a.ch_stride + (int64_t)ky * a.nx * a.nzh + kzl;
 #pragma unroll
       for (int j = 0; j < M; ++j) {
         const int x = lane + 32 * j;
@@ -564,7 +564,7 @@ __global__ void __launch_bounds__(XF_THREADS, M == 27 ? 1 : 2) k_xreg(const XArg
     __syncthreads();
     // k-space scaling at every kx of the column (channel c of kx at lines[c * LSR + kx])
     for (int kx = tid; kx < N; kx += blockDim.x) {
-      const int64_t ti = ((int64_t)ky * a.nzh + kz) * N + kx;
+      const int64_t ti = ((int64_t)ky * a.nzh + kzl) * N + kx;
       const double tB = (KIND == HS_ROTLET) ? 0.0 : a.tabB[ti];
       const double tH = (KIND == HS_ROTLET || HALF) ? a.tabH[ti] : 0.0;
       double2* col = lines + kx;
@@ -596,7 +596,7 @@ __global__ void __launch_bounds__(XF_THREADS, M == 27 ? 1 : 2) k_xreg(const XArg
 #pragma unroll
       for (int j = 0; j < M; ++j) v[j] = S[lane + 32 * j];
       warp_fft_reg<M>(v, S, tw, lane, out);
-      double2* dst = a.B + o * a.ch_stride + (int64_t)ky * a.nx * a.nzh + kz;
+      double2* dst = a.B + o * a.ch_stride + (int64_t)ky * a.nx * a.nzh + kzl;
 #pragma unroll
       for (int g = 0; g < RegFFT<M>::NG; ++g) {
         const int rg = r + 16 * g;
@@ -784,21 +784,26 @@ hs_status make_twiddles(int n, double2* d_tw, cudaStream_t st) {
   return HS_OK;
 }
 
-// half-spectrum table [kx][ky][kz] -> x-stage layout [ky][kz][kx]
-__global__ void k_table_to_xmajor(const double* __restrict__ in, int px, int py, int nzh, double* __restrict__ out) {
-  const int64_t n = (int64_t)px * py * nzh;
+// half-spectrum table [kx][ky][kz] -> x-stage layout [ky][kz - kz0][kx], kz in [kz0, kz0 + nzl)
+__global__ void k_table_to_xmajor(const double* __restrict__ in, int px, int py, int nzh, int kz0, int nzl,
+                                  double* __restrict__ out) {
+  const int64_t n = (int64_t)px * py * nzl;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const int kx = (int)(i % px);
     const int64_t r = i / px;
-    const int kz = (int)(r % nzh), ky = (int)(r / nzh);
-    out[i] = in[((int64_t)kx * py + ky) * nzh + kz];
+    const int kzl = (int)(r % nzl), ky = (int)(r / nzl);
+    out[i] = in[((int64_t)kx * py + ky) * nzh + kz0 + kzl];
   }
 }
 
-hs_status launch_table_to_xmajor(hs_ctx* ctx, const double* in, int px, int py, int nzh, double* out) {
-  const int64_t n = (int64_t)px * py * nzh;
+hs_status launch_table_to_xmajor(hs_ctx* ctx, const double* in, int px, int py, int nzh, double* out, int kz0,
+                                 int nzl) {
+  if (nzl < 0) nzl = nzh - kz0;
+  if (kz0 < 0 || kz0 + nzl > nzh) return fail(HS_ERR_PARAMETER, "table kz slice out of range");
+  const int64_t n = (int64_t)px * py * nzl;
+  if (n == 0) return HS_OK;
   const int gs = (int)std::min<int64_t>(ceil_div(n, 256), (int64_t)ctx->sm_count * 16);
-  k_table_to_xmajor<<<gs, 256, 0, ctx->stream>>>(in, px, py, nzh, out);
+  k_table_to_xmajor<<<gs, 256, 0, ctx->stream>>>(in, px, py, nzh, kz0, nzl, out);
   HS_LAUNCHED(ctx);
   return HS_OK;
 }

@@ -32,18 +32,24 @@ __global__ void k_grid_keys(const double* __restrict__ pos, int n_src, int n, in
     const bool mir = (mode == 2) || (mode == 1 && i >= n_src);
     const double pc[3] = {pos[3 * s], pos[3 * s + 1], mir ? -pos[3 * s + 2] : pos[3 * s + 2]};
     int b[3], cc[3];
+    bool drop = false;  // y-slab plan: window starts in another rank's slab
     const int tsz[3] = {SP_TX, SP_TY, SP_TZ};
     const int nb[3] = {nbx, nby, nbz};
     bool bad = false;
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-      const int64_t lo = window_lo(pc[k], g.origin[k], g.h, g.P);
+      const int64_t lo = g_lo(g, k, pc[k]);
       bad |= (lo < 0) || (lo + g.P > g.dims[k]);
+      if (k == 1 && g.sel && !fine) drop = lo < g.sel_lo || lo >= g.sel_hi;
       int64_t c = lo + g.P / 2 - 1;  // window-centre cell i0
       c = c < 0 ? 0 : (c >= g.dims[k] ? g.dims[k] - 1 : c);
       int bb = (int)(c / tsz[k]);
       b[k] = bb >= nb[k] ? nb[k] - 1 : bb;
       cc[k] = (int)c;
+    }
+    if (drop) {
+      keys[i] = nbx * nby * nbz;  // one extra bin past the spread bins: never read
+      continue;
     }
     if (bad) atomicOr(flags, FLAG_OUT_OF_GRID);
     if (fine && gather_v5_keys) {
@@ -95,9 +101,9 @@ __global__ void k_spread_windows(const double4* __restrict__ pts, int n, GridGeo
     double e1[3], e2[3];
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-      const int64_t lk = window_lo(pc[k], g.origin[k], g.h, g.P);
+      const int64_t lk = g_lo(g, k, pc[k]);
       l[k] = (int)lk;
-      const double d0 = window_d(pc[k], g.origin[k], g.h, lk);
+      const double d0 = g_d(g, k, pc[k], lk);
       e1[k] = exp(-g.alpha * d0 * d0);
       e2[k] = exp(2.0 * g.alpha * d0 * g.h);
     }
@@ -323,7 +329,7 @@ __global__ void k_spread_wtab(const double4* __restrict__ pts, int n, GridGeom g
     const int s = (int)(r / 3), k = (int)(r - 3 * (int64_t)s);
     const double4 p = pts[s];
     const double pc = k == 0 ? p.x : (k == 1 ? p.y : p.z);
-    const int64_t l = window_lo(pc, g.origin[k], g.h, P);
+    const int64_t l = g_lo(g, k, pc);
     const int pad = k == 0 ? SP_TX : (k == 1 ? SP_TY : SP_TZ);
     const int len = k == 0 ? wt.wx : (k == 1 ? wt.wy : wt.wz);
     double* row = tab + (int64_t)s * wt.stride + (k == 0 ? 0 : (k == 1 ? wt.wx : wt.wx + wt.wy));
@@ -332,13 +338,13 @@ __global__ void k_spread_wtab(const double4* __restrict__ pts, int n, GridGeom g
       const int a = j - pad;
       double v = 0.0;
       if (a >= 0 && a < P) {
-        const double d = window_d(pc, g.origin[k], g.h, l + a);
+        const double d = g_d(g, k, pc, l + a);
         v = scale * exp(-g.alpha * d * d);
       }
       row[j] = v;
     }
     if (k == 0 && lane == 0)
-      lo[s] = make_int4((int)l, (int)window_lo(p.y, g.origin[1], g.h, P), (int)window_lo(p.z, g.origin[2], g.h, P), 0);
+      lo[s] = make_int4((int)l, (int)g_lo(g, 1, p.y), (int)g_lo(g, 2, p.z), 0);
   }
 }
 
@@ -977,9 +983,9 @@ __global__ void __launch_bounds__(256) k_gather(const double4* __restrict__ pts,
   const int P = g.P;
   for (int i = blockIdx.x * 8 + warp; i < n; i += gridDim.x * 8) {
     const double4 p = pts[i];
-    const int64_t lx = window_lo(p.x, g.origin[0], g.h, P);
-    const int64_t ly = window_lo(p.y, g.origin[1], g.h, P);
-    const int64_t lz = window_lo(p.z, g.origin[2], g.h, P);
+    const int64_t lx = g_lo(g, 0, p.x);
+    const int64_t ly = g_lo(g, 1, p.y);
+    const int64_t lz = g_lo(g, 2, p.z);
     const bool bad = lx < 0 || ly < 0 || lz < 0 || lx + P > g.dims[0] || ly + P > g.dims[1] || lz + P > g.dims[2];
     double acc[NCH];
 #pragma unroll
@@ -987,14 +993,14 @@ __global__ void __launch_bounds__(256) k_gather(const double4* __restrict__ pts,
     if (!bad) {
       __syncwarp();
       if (lane < P) {
-        const double dx = window_d(p.x, g.origin[0], g.h, lx + lane);
-        const double dy = window_d(p.y, g.origin[1], g.h, ly + lane);
+        const double dx = g_d(g, 0, p.x, lx + lane);
+        const double dy = g_d(g, 1, p.y, ly + lane);
         s_w[warp][0][lane] = exp(-g.alpha * dx * dx);
         s_w[warp][1][lane] = exp(-g.alpha * dy * dy);
       }
       double wz = 0.0;
       if (lane < P) {
-        const double dz = window_d(p.z, g.origin[2], g.h, lz + lane);
+        const double dz = g_d(g, 2, p.z, lz + lane);
         wz = exp(-g.alpha * dz * dz);
       }
       __syncwarp();
@@ -1087,7 +1093,7 @@ __global__ void __launch_bounds__(GA_T, 2) k_gather3(const double4* __restrict__
     bool bad = false;
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-      const int64_t l = window_lo(pc[k], g.origin[k], g.h, P);
+      const int64_t l = g_lo(g, k, pc[k]);
       bad |= (l < 0) || (l + P > g.dims[k]);
       lo[k] = (int)l;
     }
@@ -1122,7 +1128,7 @@ __global__ void __launch_bounds__(GA_T, 2) k_gather3(const double4* __restrict__
       double w0[3], r0[3];
 #pragma unroll
       for (int k = 0; k < 3; ++k) {
-        const double d = window_d(pc[k], g.origin[k], g.h, lo[k]);
+        const double d = g_d(g, k, pc[k], lo[k]);
         w0[k] = act ? exp(-g.alpha * d * d) : 0.0;
         r0[k] = exp(g.alpha * (2.0 * d * g.h - g.h * g.h));
       }
@@ -1279,7 +1285,7 @@ __global__ void __launch_bounds__(256, 2) k_gather5(const double4* __restrict__ 
     bool bad = false;
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-      const int64_t l = window_lo(pc[k], g.origin[k], g.h, P);
+      const int64_t l = g_lo(g, k, pc[k]);
       bad |= (l < 0) || (l + P > g.dims[k]);
       lo[k] = (int)l;
     }
@@ -1299,7 +1305,7 @@ __global__ void __launch_bounds__(256, 2) k_gather5(const double4* __restrict__ 
       double w0[3], r0[3];
 #pragma unroll
       for (int k = 0; k < 3; ++k) {
-        const double d = window_d(pc[k], g.origin[k], g.h, lo[k]);
+        const double d = g_d(g, k, pc[k], lo[k]);
         w0[k] = act ? exp(-g.alpha * d * d) : 0.0;
         r0[k] = exp(g.alpha * (2.0 * d * g.h - g.h * g.h));
       }
@@ -1384,7 +1390,7 @@ __global__ void __launch_bounds__(256, 2) k_gather5(const double4* __restrict__ 
         double ws[3][GA_ZM];
         for (int k = 0; k < 3; ++k)
           for (int a2 = 0; a2 < P; ++a2) {
-            const double d = window_d(pc[k], g.origin[k], g.h, lo[k] + a2);
+            const double d = g_d(g, k, pc[k], lo[k] + a2);
             ws[k][a2] = exp(-g.alpha * d * d);
           }
         for (int a2 = 0; a2 < P; ++a2)
@@ -1445,14 +1451,14 @@ __device__ int g7_cut(const double4* __restrict__ pts, int b, int e, const GridG
     const int ib = i;
     int nrun = 0;
     int lens = 0;
-    const int64_t zi0 = window_lo(pts[i].z, g.origin[2], g.h, g.P);
+    const int64_t zi0 = g_lo(g, 2, pts[i].z);
     while (i < e && nrun < G7_WARPS) {
-      const int64_t zr0 = window_lo(pts[i].z, g.origin[2], g.h, g.P);
+      const int64_t zr0 = g_lo(g, 2, pts[i].z);
       if (zr0 - zi0 > G7_ZC - g.P) break;
       int len = 1;
       ++i;
       while (i < e && len < G7_TG) {
-        const int64_t z = window_lo(pts[i].z, g.origin[2], g.h, g.P);
+        const int64_t z = g_lo(g, 2, pts[i].z);
         if (z - zr0 > 32 - g.P || z - zi0 > G7_ZC - g.P) break;
         ++len;
         ++i;
@@ -1510,7 +1516,7 @@ __global__ void __launch_bounds__(G7_WARPS * 32, 2) k_gather7(const double4* __r
     bool bad = false;
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-      const int64_t l = window_lo(pc[k], g.origin[k], g.h, P);
+      const int64_t l = g_lo(g, k, pc[k]);
       bad |= (l < 0) || (l + P > g.dims[k]);
       lo[k] = (int)l;
     }
@@ -1540,8 +1546,10 @@ __global__ void __launch_bounds__(G7_WARPS * 32, 2) k_gather7(const double4* __r
         C0[k] = min(C0[k], s_u[w][k]);
         C1[k] = max(C1[k], s_u[w][3 + k]);
       }
+    // no active target in the item (all out of the grid): C0 = INT_MAX and C1 - C0 would wrap
+    if (C0[0] == 0x7fffffff) continue;
     const int nxu = C1[0] - C0[0], nyu = C1[1] - C0[1], nzu = C1[2] - C0[2];
-    // no active target, or (only with out-of-grid targets, an error anyway) limits exceeded
+    // limits exceeded (only with out-of-grid targets, an error anyway)
     if (nxu <= 0 || nxu > GW || nyu > GW || nzu > G7_ZC) continue;
     double res[NCH];
 #pragma unroll
@@ -1555,11 +1563,11 @@ __global__ void __launch_bounds__(G7_WARPS * 32, 2) k_gather7(const double4* __r
       double vx = 0.0, vy = 0.0;
       const int x = C0[0] + lane, y = C0[1] + lane;
       if (tin && lane < nxu && x >= lx && x < lx + P) {
-        const double d = window_d(px, g.origin[0], g.h, x);
+        const double d = g_d(g, 0, px, x);
         vx = exp(-g.alpha * d * d);
       }
       if (tin && lane < nyu && y >= ly && y < ly + P) {
-        const double d = window_d(py, g.origin[1], g.h, y);
+        const double d = g_d(g, 1, py, y);
         vy = exp(-g.alpha * d * d);
       }
       wx_tab[tt][lane] = vx;
@@ -1647,7 +1655,7 @@ __global__ void __launch_bounds__(G7_WARPS * 32, 2) k_gather7(const double4* __r
         const int lz = __shfl_sync(0xffffffffu, lo[2], tt);
         double wz = 0.0;
         if (((amask >> tt) & 1u) && z >= lz && z < lz + P) {
-          const double d = window_d(pz, g.origin[2], g.h, z);
+          const double d = g_d(g, 2, pz, z);
           wz = exp(-g.alpha * d * d);
         }
 #pragma unroll

@@ -5,7 +5,8 @@
 namespace hs {
 
 // sort.cu
-hs_status counting_sort(hs_ctx* ctx, const int* keys, int n, int nb, int* order, int* start, int* work);
+hs_status counting_sort(hs_ctx* ctx, const int* keys, int n, int nb, int* order, int* start, int* work,
+                        int nb_rank = -1);
 inline size_t counting_sort_work_ints(int n, int nb) { return (size_t)2 * nb + 4 + (size_t)n; }
 // exclusive scan of in[0..n) into out[0..n] (out[n] = total); scratch: n + 2 ints
 hs_status exclusive_scan(hs_ctx* ctx, const int* in, int n, int* out, int* scratch);
@@ -34,7 +35,19 @@ struct GridGeom {
   int P;
   int64_t stride[3];       // element strides of the storage layout (x, y, z)
   int64_t ch_stride;       // element stride between channels
+  // y-slab decomposition (sharding.py): stored node (i,j,k) is global node (i, j + off[1], k);
+  // window starts are computed from the GLOBAL geometry (bit-identical on every rank) and
+  // shifted.  sel: spreading keeps only points whose local y window start is in [sel_lo, sel_hi)
+  int off[3];
+  int sel, sel_lo, sel_hi;
 };
+// window start / node distance in the grid's local node numbering (off = 0: _gridding.py:24-29)
+__device__ __forceinline__ int64_t g_lo(const GridGeom& g, int k, double pos) {
+  return window_lo(pos, g.origin[k], g.h, g.P) - g.off[k];
+}
+__device__ __forceinline__ double g_d(const GridGeom& g, int k, double pos, int64_t local_idx) {
+  return window_d(pos, g.origin[k], g.h, local_idx + g.off[k]);
+}
 constexpr int SP_TX = 16, SP_TY = 16, SP_TZ = 8;  // spread tile / bin shape
 // gather target order: (4x4 (x,y) column, z node) of the window-centre node (v5: 8x8 columns)
 bool gather_v5();
@@ -145,6 +158,7 @@ struct XArgs {
   const double2* tw;     // px twiddles exp(-2 pi i j/px)
   FftPlan plan;          // radix plan of px
   int px, py, pz, nzh, nx;
+  int kz0;               // global kz of local column 0 (y-slab plans own kz columns [kz0, kz0 + nzh))
   double kscale[3];      // 1/(p_i h)
   double ka, kb;         // (1-eta)/4xi^2, 1/4xi^2
   double inv_n;          // 1/(px py pz)
@@ -157,7 +171,9 @@ hs_status launch_xfused(hs_ctx* ctx, int kind, int half, const XArgs& a);
 bool ystage_supported(int py);
 hs_status launch_ystage(hs_ctx* ctx, bool fwd, const double2* in, double2* out, const double2* tw, int py, int nx,
                         int nzh, int ny);
-hs_status launch_table_to_xmajor(hs_ctx* ctx, const double* in, int px, int py, int nzh, double* out);
+// kz columns [kz0, kz0 + nzl) only (a y-slab plan's share; full table: kz0 = 0, nzl = nzh)
+hs_status launch_table_to_xmajor(hs_ctx* ctx, const double* in, int px, int py, int nzh, double* out, int kz0 = 0,
+                                 int nzl = -1);
 
 // plan.cu helpers reused by the stand-alone API
 hs_status greens_half_table(hs_ctx* ctx, int kind, double R, double h, const int64_t big[3], const int64_t dims[3],

@@ -157,9 +157,10 @@ __global__ void k_self_term(int nt, const double* __restrict__ tpos, const long 
   }
 }
 
-// grid_out[i * pitch + c] = tmp[c][i]
-__global__ void k_interleave(const double* __restrict__ tmp, int nch, int64_t n, int pitch, double* __restrict__ out) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+// grid_out[i * pitch + c] = tmp[c][i] for i < count (channel stride n)
+__global__ void k_interleave(const double* __restrict__ tmp, int nch, int64_t n, int64_t count, int pitch,
+                             double* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
     double v[8];
 #pragma unroll
     for (int c = 0; c < 8; ++c) v[c] = c < nch ? tmp[(int64_t)c * n + i] : 0.0;
@@ -259,6 +260,17 @@ struct hs_plan {
   double *u = nullptr, *u_real = nullptr, *u_four = nullptr, *uk = nullptr, *uc = nullptr;
   unsigned long long* pair_counts = nullptr;
   cudaEvent_t ev[16] = {};
+  // y-slab decomposition (hs_plan_create_slab; sharding.py).  slab.world == 0: whole grid.
+  hs_slab slab{};
+  int yo = 0;                   // owned y planes y1 - y0 (whole grid: ny)
+  int nzs = 0;                  // kz columns held in the mixed spectra (whole grid: nzh)
+  int64_t n_amix = 0;           // elements of Amix (slab: yo * nx * nzh z-stage outputs)
+  int n_sel_k = 0, n_sel_c = 0; // slab: kernel / correction sources spread by this rank
+  // device inputs of the current evaluation (slab stages keep them between calls)
+  const double *cur_pos = nullptr, *cur_fa = nullptr, *cur_fb = nullptr, *cur_tp = nullptr;
+  const long long* cur_tc = nullptr;
+  int cur_tcol_identity = 0;
+  bool pair_timed = false, spread_timed = false, gather_timed = false;
 };
 
 namespace {
@@ -300,12 +312,14 @@ hs_status plan_channels(int kind, int half, int* nk, int* nc) {
 }
 }  // namespace hs
 
-extern "C" hs_status hs_plan_create(hs_ctx* ctx, const hs_params* prm, hs_plan** out) {
+static hs_status plan_create_impl(hs_ctx* ctx, const hs_params* prm, const hs_slab* slab, hs_plan** out) {
   if (!ctx || !prm || !out) return fail(HS_ERR_PARAMETER, "null argument");
   HS_CUDA(cudaSetDevice(ctx->device));
   hs_plan* p = new hs_plan();
   p->ctx = ctx;
   p->prm = *prm;
+  if (slab) p->slab = *slab;
+  const bool sl = slab != nullptr;
   p->half = prm->geometry == HS_HALF;
   hs_status st = HS_OK;
   auto bail = [&](hs_status s) {
@@ -340,14 +354,36 @@ extern "C" hs_status hs_plan_create(hs_ctx* ctx, const hs_params* prm, hs_plan**
   g.alpha = 2.0 * prm->xi * prm->xi / prm->eta;
   g.pref = std::pow(2.0 * prm->xi * prm->xi / (kPi * prm->eta), 1.5);
   const int64_t px = prm->padded[0], py = prm->padded[1], pz = prm->padded[2];
-  const int64_t nxd = prm->dims[0], nyd = prm->dims[1], nzh = pz / 2 + 1;
+  const int64_t nxd = prm->dims[0], nzh = pz / 2 + 1;
+  int64_t nyd = prm->dims[1];
+  p->yo = (int)nyd;
+  p->nzs = (int)nzh;
+  if (sl) {
+    // owned planes [y0, y1) plus P - 1 ghost planes above (spread contributions for the next
+    // rank, then the gather halo received from it); owned kz columns [kz0, kz1)
+    const hs_slab& s = *slab;
+    if (s.world < 1 || s.rank < 0 || s.rank >= s.world || s.y0 < 0 || s.y1 <= s.y0 || s.y1 > prm->dims[1] ||
+        s.kz0 < 0 || s.kz1 <= s.kz0 || s.kz1 > nzh)
+      return bail(fail(HS_ERR_PARAMETER, "invalid slab (rank, world, y range, kz range)"));
+    if (s.rank + 1 < s.world && s.y1 - s.y0 < prm->P - 1)
+      return bail(fail(HS_ERR_PARAMETER, "y slab thinner than P - 1 planes: use fewer ranks"));
+    p->yo = (int)(s.y1 - s.y0);
+    p->nzs = (int)(s.kz1 - s.kz0);
+    nyd = p->yo + prm->P - 1;
+    g.dims[1] = (int)nyd;
+    g.off[1] = (int)s.y0;
+    g.sel = 1;
+    g.sel_lo = 0;
+    g.sel_hi = p->yo;
+  }
   // grids are stored [y][x][z] with z-pitch pz (see fft.cu)
   g.stride[0] = pz;
   g.stride[1] = nxd * pz;
   g.stride[2] = 1;
   g.ch_stride = nyd * nxd * pz;
   p->n_grid = nyd * nxd * pz;
-  p->n_mixed = py * nxd * nzh;
+  p->n_mixed = py * nxd * p->nzs;
+  p->n_amix = sl ? (int64_t)p->yo * nxd * nzh : p->n_mixed;
   p->n_real_grid = px * py * pz;
   p->n_half = px * py * nzh;
   if (px != py) return bail(fail(HS_ERR_PARAMETER, "padded x and y lengths must agree"));
@@ -366,7 +402,7 @@ extern "C" hs_status hs_plan_create(hs_ctx* ctx, const hs_params* prm, hs_plan**
 
   // ---- buffers
   const int maxn = std::max(p->n_comb, std::max(nt, n));
-  const int maxb = std::max(std::max(ncell * kTargetSub, nb), gather_keys(g));
+  const int maxb = std::max(std::max(ncell * kTargetSub, nb + 1), gather_keys(g));
 #define A_(cnt, ptr, ...) if ((st = palloc(p, (size_t)(cnt), &(ptr), ##__VA_ARGS__)) != HS_OK) return bail(st)
   A_(3 * (size_t)n, p->d_pos);
   A_(3 * (size_t)n, p->d_sa);
@@ -388,9 +424,9 @@ extern "C" hs_status hs_plan_create(hs_ctx* ctx, const hs_params* prm, hs_plan**
   A_(std::max(nt, 1), p->TP);
   A_(std::max(nt, 1), p->torig);
   A_(p->n_comb, p->bk_order);
-  A_(nb + 1, p->bk_start);
+  A_(nb + 2, p->bk_start);  // + the slab plan's drop bin
   A_(n, p->bc_order);
-  A_(nb + 1, p->bc_start);
+  A_(nb + 2, p->bc_start);
   A_(std::max(nt, 1), p->bt_order);
   A_((size_t)gather_keys(g) + 1, p->bt_start);
   A_(p->n_comb, p->SPk);
@@ -402,7 +438,7 @@ extern "C" hs_status hs_plan_create(hs_ctx* ctx, const hs_params* prm, hs_plan**
   A_(std::max(nt, 1), p->TG);
   A_(std::max(nt, 1), p->tg_orig);
   A_((size_t)p->n_in * p->n_grid, p->grid_in, true);
-  A_((size_t)p->n_mixed, p->Amix, true);
+  A_((size_t)p->n_amix, p->Amix, true);
   A_((size_t)std::max(p->n_in, p->n_out) * p->n_mixed, p->spec);
   p->out_pitch = p->half ? 6 : 4;
   A_((size_t)p->out_pitch * p->n_grid, p->grid_out, true);
@@ -412,8 +448,10 @@ extern "C" hs_status hs_plan_create(hs_ctx* ctx, const hs_params* prm, hs_plan**
   p->go.stride[1] = (int64_t)p->out_pitch * nxd * pz;
   p->go.stride[2] = p->out_pitch;
   p->go.ch_stride = 1;
-  if (table_needs(prm->kind, p->half, HS_BIHARMONIC)) A_(p->n_half, p->tabB);
-  if (table_needs(prm->kind, p->half, HS_HARMONIC)) A_(p->n_half, p->tabH);
+  // tables in x-stage layout, only the plan's kz columns
+  const size_t ntab = (size_t)px * py * p->nzs;
+  if (table_needs(prm->kind, p->half, HS_BIHARMONIC)) A_(ntab, p->tabB);
+  if (table_needs(prm->kind, p->half, HS_HARMONIC)) A_(ntab, p->tabH);
   A_(px, p->tw);
   if ((st = make_twiddles((int)px, p->tw, ctx->stream)) != HS_OK) return bail(st);
   if (ystage_supported((int)py) && !getenv("HS_YSTAGE_CUFFT")) {  // env: cuFFT y stage (comparison)
@@ -438,12 +476,12 @@ extern "C" hs_status hs_plan_create(hs_ctx* ctx, const hs_params* prm, hs_plan**
     cufftSetAutoAllocation(p->yf, 0);
     cufftSetAutoAllocation(p->zi, 0);
     long long nz1[1] = {pz}, nzh1[1] = {nzh}, ny1[1] = {py};
-    if (cufftMakePlanMany64(p->zf, 1, nz1, nz1, 1, pz, nzh1, 1, nzh, CUFFT_D2Z, nyd * nxd, &w1) != CUFFT_SUCCESS)
+    const long long zlines = (long long)p->yo * nxd, ylines = nxd * p->nzs;  // z: owned planes only
+    if (cufftMakePlanMany64(p->zf, 1, nz1, nz1, 1, pz, nzh1, 1, nzh, CUFFT_D2Z, zlines, &w1) != CUFFT_SUCCESS)
       return bail(fail(HS_ERR_RESOURCE, "cuFFT z D2Z plan failed"));
-    if (cufftMakePlanMany64(p->yf, 1, ny1, ny1, nxd * nzh, 1, ny1, nxd * nzh, 1, CUFFT_Z2Z, nxd * nzh, &w2) !=
-        CUFFT_SUCCESS)
+    if (cufftMakePlanMany64(p->yf, 1, ny1, ny1, ylines, 1, ny1, ylines, 1, CUFFT_Z2Z, ylines, &w2) != CUFFT_SUCCESS)
       return bail(fail(HS_ERR_RESOURCE, "cuFFT y Z2Z plan failed"));
-    if (cufftMakePlanMany64(p->zi, 1, nz1, nzh1, 1, nzh, nz1, 1, pz, CUFFT_Z2D, nyd * nxd, &w3) != CUFFT_SUCCESS)
+    if (cufftMakePlanMany64(p->zi, 1, nz1, nzh1, 1, nzh, nz1, 1, pz, CUFFT_Z2D, zlines, &w3) != CUFFT_SUCCESS)
       return bail(fail(HS_ERR_RESOURCE, "cuFFT z Z2D plan failed"));
     const size_t ws = std::max(w1, std::max(w2, w3));
     char* wsp = nullptr;
@@ -456,6 +494,15 @@ extern "C" hs_status hs_plan_create(hs_ctx* ctx, const hs_params* prm, hs_plan**
   for (auto& e : p->ev) HS_CUDA(cudaEventCreate(&e));
   *out = p;
   return HS_OK;
+}
+
+extern "C" hs_status hs_plan_create(hs_ctx* ctx, const hs_params* prm, hs_plan** out) {
+  return plan_create_impl(ctx, prm, nullptr, out);
+}
+
+extern "C" hs_status hs_plan_create_slab(hs_ctx* ctx, const hs_params* prm, const hs_slab* slab, hs_plan** out) {
+  if (!slab) return fail(HS_ERR_PARAMETER, "null slab");
+  return plan_create_impl(ctx, prm, slab, out);
 }
 
 extern "C" hs_status hs_plan_destroy(hs_plan* p) {
@@ -489,6 +536,8 @@ extern "C" hs_status hs_plan_real_parts(hs_plan* p, double* kernel_part, double*
   return HS_OK;
 }
 
+static int table_kz0(const hs_plan* p) { return p->slab.world > 0 ? (int)p->slab.kz0 : 0; }
+
 extern "C" hs_status hs_plan_set_table(hs_plan* p, int table_kind, const double* samples, int mem) {
   if (!p || !samples) return fail(HS_ERR_PARAMETER, "null argument");
   double* dst = table_kind == HS_BIHARMONIC ? p->tabB : p->tabH;
@@ -506,7 +555,8 @@ extern "C" hs_status hs_plan_set_table(hs_plan* p, int table_kind, const double*
   double* half = nullptr;
   HS_CUDA(cudaMallocAsync(&half, (size_t)p->n_half * sizeof(double), ctx->stream));
   hs_status st = launch_take_half(ctx, src, pd, half);
-  if (st == HS_OK) st = launch_table_to_xmajor(ctx, half, (int)pd[0], (int)pd[1], (int)(pd[2] / 2 + 1), dst);
+  if (st == HS_OK)
+    st = launch_table_to_xmajor(ctx, half, (int)pd[0], (int)pd[1], (int)(pd[2] / 2 + 1), dst, table_kz0(p), p->nzs);
   cudaFreeAsync(half, ctx->stream);
   if (tmp) cudaFreeAsync(tmp, ctx->stream);
   HS_TRY(st);
@@ -776,7 +826,8 @@ extern "C" hs_status hs_plan_build_tables(hs_plan* p, const int64_t big[3], doub
     double* dst = kind == HS_BIHARMONIC ? p->tabB : p->tabH;
     if (!dst) continue;
     st = greens_half_table(ctx, kind, R, p->prm.h, big, p->prm.dims, guards, pd, half);
-    if (st == HS_OK) st = launch_table_to_xmajor(ctx, half, (int)pd[0], (int)pd[1], (int)(pd[2] / 2 + 1), dst);
+    if (st == HS_OK)
+      st = launch_table_to_xmajor(ctx, half, (int)pd[0], (int)pd[1], (int)(pd[2] / 2 + 1), dst, table_kz0(p), p->nzs);
     if (st == HS_OK && cudaStreamSynchronize(ctx->stream) != cudaSuccess) st = fail(HS_ERR_CUDA, "table build");
     if (st == HS_OK) (kind == HS_BIHARMONIC ? p->have_B : p->have_H) = true;
   }
@@ -797,30 +848,29 @@ hs_status sort_points_by_bin(hs_plan* p, const double* pos, int n_src, int n_tot
                              int* start) {
   hs_ctx* ctx = p->ctx;
   HS_TRY(launch_grid_keys(ctx, pos, n_src, n_total, mode, p->gg, p->keys));
+  // slab plans: spread keys of sources owned by another rank are the extra bin nbins (not
+  // ranked, never read)
+  if (!(mode & 8) && p->slab.world > 0)
+    return counting_sort(ctx, p->keys, n_total, p->nbins + 1, order, start, p->work, p->nbins);
   const int nb = (mode & 8) ? gather_keys(p->gg) : p->nbins;
   return counting_sort(ctx, p->keys, n_total, nb, order, start, p->work);
 }
 
 }  // namespace
 
-extern "C" hs_status hs_plan_execute(hs_plan* p, const double* positions, const double* sa, const double* sb,
-                                     const double* targets, const int64_t* tcols, double* u, double* u_real,
-                                     double* u_fourier, int mem, int what, double* times) {
-  if (!p || !positions || !sa || !u) return fail(HS_ERR_PARAMETER, "null argument");
+namespace {
+
+// device views of the caller's inputs (mem == HOST: staged through the plan's buffers)
+hs_status stage_inputs(hs_plan* p, const double* positions, const double* sa, const double* sb,
+                       const double* targets, const int64_t* tcols, int mem) {
   hs_ctx* ctx = p->ctx;
   cudaStream_t st = ctx->stream;
   const hs_params& prm = p->prm;
   const int n = (int)prm.n, nt = (int)prm.n_targets;
   const int kind = prm.kind;
+  if (!positions || !sa) return fail(HS_ERR_PARAMETER, "null argument");
   if (kind != HS_STOKESLET && !sb) return fail(HS_ERR_PARAMETER, "stresslet/rotlet need q");
   if (!prm.targets_are_sources && nt > 0 && !targets) return fail(HS_ERR_PARAMETER, "targets required");
-  if ((what & 2) && (p->tabB && !p->have_B)) return fail(HS_ERR_CONFIG, "missing biharmonic table");
-  if ((what & 2) && (p->tabH && !p->have_H)) return fail(HS_ERR_CONFIG, "missing harmonic table");
-  HS_CUDA(cudaSetDevice(ctx->device));
-  HS_TRY(ctx_reset_flags(ctx));
-  cudaEvent_t* ev = p->ev;
-  HS_CUDA(cudaEventRecord(ev[0], st));
-  // ---- inputs
   const double *pos = positions, *fa = sa, *fb = sb, *tp = targets;
   const long long* tc = (const long long*)tcols;
   if (mem == HS_MEM_HOST) {
@@ -842,11 +892,25 @@ extern "C" hs_status hs_plan_execute(hs_plan* p, const double* positions, const 
     }
   }
   if (prm.targets_are_sources) tp = pos;
-  const int tcol_identity = prm.targets_are_sources ? 1 : 0;
-  HS_CUDA(cudaEventRecord(ev[1], st));
-  // ---- real space
-  const bool do_real = (what & 1) && prm.rc > 0;
-  bool pair_timed = false, spread_timed = false, gather_timed = false;
+  p->cur_pos = pos;
+  p->cur_fa = fa;
+  p->cur_fb = fb;
+  p->cur_tp = tp;
+  p->cur_tc = tc;
+  p->cur_tcol_identity = prm.targets_are_sources ? 1 : 0;
+  return HS_OK;
+}
+
+// real-space sums (ewald_real.py:381-455) of the plan's targets into u_real / uk / uc
+hs_status stage_real(hs_plan* p, bool want) {
+  hs_ctx* ctx = p->ctx;
+  cudaStream_t st = ctx->stream;
+  const hs_params& prm = p->prm;
+  const int n = (int)prm.n, nt = (int)prm.n_targets, kind = prm.kind;
+  const double *pos = p->cur_pos, *fa = p->cur_fa, *fb = p->cur_fb, *tp = p->cur_tp;
+  const long long* tc = p->cur_tc;
+  const int tcol_identity = p->cur_tcol_identity;
+  const bool do_real = want && prm.rc > 0;
   if (do_real) {
     HS_TRY(sort_points_by_cell(p, pos, n, p->n_comb, p->half ? 1 : 0, 1, p->order, p->start));
     k_pair_records<<<grid_size(ctx, p->n_comb), 256, 0, st>>>(kind, p->half, p->order, p->n_comb, n, pos, fa, fb,
@@ -895,106 +959,231 @@ extern "C" hs_status hs_plan_execute(hs_plan* p, const double* positions, const 
       a.flags = ctx->d_flags;
       a.counts = p->pair_counts;
       HS_CUDA(cudaMemsetAsync(p->pair_counts, 0, 2 * sizeof(unsigned long long), st));
-      HS_CUDA(cudaEventRecord(ev[9], st));
+      HS_CUDA(cudaEventRecord(p->ev[9], st));
       HS_TRY(launch_pair(ctx, a));
-      HS_CUDA(cudaEventRecord(ev[10], st));
-      pair_timed = true;
+      HS_CUDA(cudaEventRecord(p->ev[10], st));
+      p->pair_timed = true;
     }
   } else if (nt > 0) {
     HS_CUDA(cudaMemsetAsync(p->u_real, 0, 24 * (size_t)nt, st));
     HS_CUDA(cudaMemsetAsync(p->uk, 0, 24 * (size_t)nt, st));
     HS_CUDA(cudaMemsetAsync(p->uc, 0, 24 * (size_t)nt, st));
-    if ((what & 1) && kind == HS_STOKESLET) {
+    if (want && kind == HS_STOKESLET) {
       // rc = 0: no pairs, but the self term is still added (ewald_real.py:444-449)
       k_self_term<<<grid_size(ctx, nt), 256, 0, st>>>(nt, tp, tc, tcol_identity, n, prm.xi, fa, p->u_real);
       HS_LAUNCHED(ctx);
     }
   }
-  HS_CUDA(cudaEventRecord(ev[2], st));
-  // ---- Fourier space
-  const bool do_four = (what & 2) != 0;
-  if (do_four) {
-    // kernel sources [y; y^I] (or y) and wall-correction sources y^I
-    HS_TRY(sort_points_by_bin(p, pos, n, p->n_comb, p->half ? 1 : 0, p->bk_order, p->bk_start));
-    k_spread_records<<<grid_size(ctx, p->n_comb), 256, 0, st>>>(kind, p->half, 0, p->bk_order, p->n_comb, n, pos,
-                                                                fa, fb, p->nk, p->SPk, p->SWk);
+  return HS_OK;
+}
+
+// spreading of kernel sources [y; y^I] (or y) and wall-correction sources y^I into grid_in
+// (ewald_fourier.py:319-332,353-382); a slab plan keeps the sources whose y window starts
+// in its slab (k_grid_keys drop bin)
+hs_status stage_spread(hs_plan* p) {
+  hs_ctx* ctx = p->ctx;
+  cudaStream_t st = ctx->stream;
+  const hs_params& prm = p->prm;
+  const int n = (int)prm.n, kind = prm.kind;
+  const double *pos = p->cur_pos, *fa = p->cur_fa, *fb = p->cur_fb;
+  const bool sl = p->slab.world > 0;
+  HS_TRY(sort_points_by_bin(p, pos, n, p->n_comb, p->half ? 1 : 0, p->bk_order, p->bk_start));
+  if (p->nc) HS_TRY(sort_points_by_bin(p, pos, n, n, 2, p->bc_order, p->bc_start));
+  int nk_sel = p->n_comb, nc_sel = n;
+  if (sl) {
+    // selected sources lead the bin order: their count is the start of the drop bin
+    int cnt[2] = {0, 0};
+    HS_CUDA(cudaMemcpyAsync(&cnt[0], p->bk_start + p->nbins, sizeof(int), cudaMemcpyDeviceToHost, st));
+    if (p->nc) HS_CUDA(cudaMemcpyAsync(&cnt[1], p->bc_start + p->nbins, sizeof(int), cudaMemcpyDeviceToHost, st));
+    HS_CUDA(cudaStreamSynchronize(st));
+    nk_sel = cnt[0];
+    nc_sel = cnt[1];
+  }
+  if (nk_sel > 0) {
+    k_spread_records<<<grid_size(ctx, nk_sel), 256, 0, st>>>(kind, p->half, 0, p->bk_order, nk_sel, n, pos, fa, fb,
+                                                             p->nk, p->SPk, p->SWk);
     HS_LAUNCHED(ctx);
-    if (p->nc) {
-      HS_TRY(sort_points_by_bin(p, pos, n, n, 2, p->bc_order, p->bc_start));
-      k_spread_records<<<grid_size(ctx, n), 256, 0, st>>>(kind, p->half, 1, p->bc_order, n, n, pos, fa, fb, p->nc,
-                                                          p->SPc, p->SWc);
-      HS_LAUNCHED(ctx);
-    }
-    HS_CUDA(cudaEventRecord(ev[11], st));
-    HS_TRY(launch_spread(ctx, p->SPk, p->SWk, p->n_comb, p->nk, p->bk_start, p->gg, p->grid_in));
-    if (p->nc)
-      HS_TRY(launch_spread(ctx, p->SPc, p->SWc, n, p->nc, p->bc_start, p->gg,
-                           p->grid_in + (size_t)p->nk * p->n_grid));
-    HS_CUDA(cudaEventRecord(ev[12], st));
-    spread_timed = true;
+  }
+  if (p->nc && nc_sel > 0) {
+    k_spread_records<<<grid_size(ctx, nc_sel), 256, 0, st>>>(kind, p->half, 1, p->bc_order, nc_sel, n, pos, fa, fb,
+                                                             p->nc, p->SPc, p->SWc);
+    HS_LAUNCHED(ctx);
+  }
+  p->n_sel_k = nk_sel;
+  p->n_sel_c = nc_sel;
+  HS_CUDA(cudaEventRecord(p->ev[11], st));
+  HS_TRY(launch_spread(ctx, p->SPk, p->SWk, nk_sel, p->nk, p->bk_start, p->gg, p->grid_in));
+  if (p->nc)
+    HS_TRY(launch_spread(ctx, p->SPc, p->SWc, nc_sel, p->nc, p->bc_start, p->gg, p->grid_in + (size_t)p->nk * p->n_grid));
+  HS_CUDA(cudaEventRecord(p->ev[12], st));
+  p->spread_timed = true;
+  return HS_OK;
+}
+
+void set_fft_streams(hs_plan* p) {
+  cufftSetStream(p->zf, p->ctx->stream);
+  cufftSetStream(p->yf, p->ctx->stream);
+  cufftSetStream(p->zi, p->ctx->stream);
+}
+
+// forward y transform of one channel: rows y < ny of `in` ([py][nx][nzs]) -> spec channel c
+hs_status stage_yfwd(hs_plan* p, double2* in, int c) {
+  double2* out = p->spec + (size_t)c * p->n_mixed;
+  if (p->ytw)
+    return launch_ystage(p->ctx, true, in, out, p->ytw, p->kg.p[1], p->gg.dims[0], p->nzs, (int)p->prm.dims[1]);
+  if (cufftExecZ2Z(p->yf, (cufftDoubleComplex*)in, (cufftDoubleComplex*)out, CUFFT_FORWARD) != CUFFT_SUCCESS)
+    return fail(HS_ERR_CUDA, "cuFFT y Z2Z failed");
+  return HS_OK;
+}
+
+// inverse y transform of output channel o: rows y < ny written to `out` ([ny][nx][nzs] rows)
+hs_status stage_yinv(hs_plan* p, int o, double2* out) {
+  double2* so = p->spec + (size_t)o * p->n_mixed;
+  const int ny = (int)p->prm.dims[1];
+  if (p->ytw) return launch_ystage(p->ctx, false, so, out, p->ytw, p->kg.p[1], p->gg.dims[0], p->nzs, ny);
+  if (cufftExecZ2Z(p->yf, (cufftDoubleComplex*)so, (cufftDoubleComplex*)so, CUFFT_INVERSE) != CUFFT_SUCCESS)
+    return fail(HS_ERR_CUDA, "cuFFT y^-1 failed");
+  if (out != so)
+    HS_CUDA(cudaMemcpyAsync(out, so, sizeof(double2) * (size_t)ny * p->gg.dims[0] * p->nzs, cudaMemcpyDeviceToDevice,
+                            p->ctx->stream));
+  return HS_OK;
+}
+
+hs_status stage_xstage(hs_plan* p) {
+  XArgs xa{};
+  xa.B = p->spec;
+  xa.ch_stride = p->n_mixed;
+  xa.tabB = p->tabB;
+  xa.tabH = p->tabH;
+  xa.tw = p->tw;
+  xa.plan = p->xplan;
+  xa.px = p->kg.p[0];
+  xa.py = p->kg.p[1];
+  xa.pz = p->kg.p[2];
+  xa.nzh = p->nzs;
+  xa.kz0 = p->slab.world > 0 ? (int)p->slab.kz0 : 0;
+  xa.nx = p->gg.dims[0];
+  for (int k = 0; k < 3; ++k) xa.kscale[k] = p->kg.kscale[k];
+  xa.ka = p->kg.a;
+  xa.kb = p->kg.b;
+  xa.inv_n = p->kg.inv_n;
+  return launch_xfused(p->ctx, p->prm.kind, p->half, xa);
+}
+
+// Fourier gather at the plan's targets: u_four, and u = u_real + u_four (ewald_fourier.py:626-630)
+hs_status stage_gather(hs_plan* p) {
+  hs_ctx* ctx = p->ctx;
+  cudaStream_t st = ctx->stream;
+  const int nt = (int)p->prm.n_targets;
+  if (nt == 0) return HS_OK;
+  HS_TRY(sort_points_by_bin(p, p->cur_tp, nt, nt, 8, p->bt_order, p->bt_start));
+  k_gather_records<<<grid_size(ctx, nt), 256, 0, st>>>(p->bt_order, nt, p->cur_tp, p->TG, p->tg_orig);
+  HS_LAUNCHED(ctx);
+  HS_CUDA(cudaEventRecord(p->ev[13], st));
+  HS_TRY(launch_gather_fourier(ctx, p->TG, p->tg_orig, nt, p->half ? 1 : 0, p->go, p->grid_out, p->u_four, p->u,
+                               p->u_real, p->bt_start));
+  HS_CUDA(cudaEventRecord(p->ev[14], st));
+  p->gather_timed = true;
+  return HS_OK;
+}
+
+hs_status stage_outputs(hs_plan* p, double* u, double* u_real, double* u_fourier, int mem) {
+  cudaStream_t st = p->ctx->stream;
+  const int nt = (int)p->prm.n_targets;
+  const cudaMemcpyKind ok = mem == HS_MEM_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+  if (nt > 0) {
+    HS_CUDA(cudaMemcpyAsync(u, p->u, 24 * (size_t)nt, ok, st));
+    if (u_real) HS_CUDA(cudaMemcpyAsync(u_real, p->u_real, 24 * (size_t)nt, ok, st));
+    if (u_fourier) HS_CUDA(cudaMemcpyAsync(u_fourier, p->u_four, 24 * (size_t)nt, ok, st));
+  }
+  return HS_OK;
+}
+
+void fill_times(hs_plan* p, double* times) {
+  cudaEvent_t* ev = p->ev;
+  float ms[9] = {0};
+  for (int k = 0; k < 8; ++k) cudaEventElapsedTime(&ms[k], ev[k], ev[k + 1]);
+  float tot = 0;
+  cudaEventElapsedTime(&tot, ev[0], ev[8]);
+  float fourier = 0;
+  cudaEventElapsedTime(&fourier, ev[2], ev[7]);
+  // [gridding, fft, scale, ifft, gather, real, fourier, prep, total, io]
+  times[0] = ms[2];
+  times[1] = ms[3];
+  times[2] = ms[4];
+  times[3] = ms[5];
+  times[4] = ms[6];
+  times[5] = ms[1];
+  times[6] = fourier;
+  times[7] = ms[0];
+  times[8] = tot;
+  times[9] = ms[7] + ms[0];
+  float kp = 0, ks = 0, kg = 0;
+  if (p->pair_timed) cudaEventElapsedTime(&kp, ev[9], ev[10]);
+  if (p->spread_timed) cudaEventElapsedTime(&ks, ev[11], ev[12]);
+  if (p->gather_timed) cudaEventElapsedTime(&kg, ev[13], ev[14]);
+  // kernel-only times: [10] pair, [11] spread, [12] gather, [13] scale
+  times[10] = kp;
+  times[11] = ks;
+  times[12] = kg;
+  times[13] = ms[4];
+  unsigned long long cnt[2] = {0, 0};
+  if (p->pair_timed) cudaMemcpy(cnt, p->pair_counts, sizeof(cnt), cudaMemcpyDeviceToHost);
+  times[14] = (double)cnt[0];  // accepted pairs
+  times[15] = (double)cnt[1];  // accepted image pairs
+}
+
+hs_status begin_eval(hs_plan* p) {
+  HS_CUDA(cudaSetDevice(p->ctx->device));
+  HS_TRY(ctx_reset_flags(p->ctx));
+  p->pair_timed = p->spread_timed = p->gather_timed = false;
+  return HS_OK;
+}
+
+}  // namespace
+
+extern "C" hs_status hs_plan_execute(hs_plan* p, const double* positions, const double* sa, const double* sb,
+                                     const double* targets, const int64_t* tcols, double* u, double* u_real,
+                                     double* u_fourier, int mem, int what, double* times) {
+  if (!p || !positions || !sa || !u) return fail(HS_ERR_PARAMETER, "null argument");
+  if (p->slab.world > 0) return fail(HS_ERR_PARAMETER, "slab plans evaluate through the hs_slab_* stages");
+  hs_ctx* ctx = p->ctx;
+  cudaStream_t st = ctx->stream;
+  const int nt = (int)p->prm.n_targets;
+  if ((what & 2) && (p->tabB && !p->have_B)) return fail(HS_ERR_CONFIG, "missing biharmonic table");
+  if ((what & 2) && (p->tabH && !p->have_H)) return fail(HS_ERR_CONFIG, "missing harmonic table");
+  HS_TRY(begin_eval(p));
+  cudaEvent_t* ev = p->ev;
+  HS_CUDA(cudaEventRecord(ev[0], st));
+  HS_TRY(stage_inputs(p, positions, sa, sb, targets, tcols, mem));
+  HS_CUDA(cudaEventRecord(ev[1], st));
+  HS_TRY(stage_real(p, (what & 1) != 0));
+  HS_CUDA(cudaEventRecord(ev[2], st));
+  if (what & 2) {
+    HS_TRY(stage_spread(p));
     HS_CUDA(cudaEventRecord(ev[3], st));
-    cufftSetStream(p->zf, st);
-    cufftSetStream(p->yf, st);
-    cufftSetStream(p->zi, st);
+    set_fft_streams(p);
     // forward z (D2Z) and y (Z2Z) stages, one source channel at a time through the shared A buffer
     for (int c = 0; c < p->n_in; ++c) {
       if (cufftExecD2Z(p->zf, p->grid_in + (size_t)c * p->n_grid, (cufftDoubleComplex*)p->Amix) != CUFFT_SUCCESS)
         return fail(HS_ERR_CUDA, "cuFFT z D2Z failed");
-      if (p->ytw) {
-        HS_TRY(launch_ystage(ctx, true, p->Amix, p->spec + (size_t)c * p->n_mixed, p->ytw, p->kg.p[1], p->gg.dims[0],
-                             p->kg.nzh, p->gg.dims[1]));
-      } else if (cufftExecZ2Z(p->yf, (cufftDoubleComplex*)p->Amix,
-                              (cufftDoubleComplex*)(p->spec + (size_t)c * p->n_mixed), CUFFT_FORWARD) != CUFFT_SUCCESS) {
-        return fail(HS_ERR_CUDA, "cuFFT y Z2Z failed");
-      }
+      HS_TRY(stage_yfwd(p, p->Amix, c));
     }
     HS_CUDA(cudaEventRecord(ev[4], st));
-    {
-      XArgs xa{};
-      xa.B = p->spec;
-      xa.ch_stride = p->n_mixed;
-      xa.tabB = p->tabB;
-      xa.tabH = p->tabH;
-      xa.tw = p->tw;
-      xa.plan = p->xplan;
-      xa.px = p->kg.p[0];
-      xa.py = p->kg.p[1];
-      xa.pz = p->kg.p[2];
-      xa.nzh = p->kg.nzh;
-      xa.nx = p->gg.dims[0];
-      for (int k = 0; k < 3; ++k) xa.kscale[k] = p->kg.kscale[k];
-      xa.ka = p->kg.a;
-      xa.kb = p->kg.b;
-      xa.inv_n = p->kg.inv_n;
-      HS_TRY(launch_xfused(ctx, kind, p->half, xa));
-    }
+    HS_TRY(stage_xstage(p));
     HS_CUDA(cudaEventRecord(ev[5], st));
     for (int o = 0; o < p->n_out; ++o) {
-      cufftDoubleComplex* so = (cufftDoubleComplex*)(p->spec + (size_t)o * p->n_mixed);
-      if (p->ytw) {
-        HS_TRY(launch_ystage(ctx, false, (double2*)so, (double2*)so, p->ytw, p->kg.p[1], p->gg.dims[0], p->kg.nzh,
-                             p->gg.dims[1]));
-      } else if (cufftExecZ2Z(p->yf, so, so, CUFFT_INVERSE) != CUFFT_SUCCESS) {
-        return fail(HS_ERR_CUDA, "cuFFT y^-1 failed");
-      }
-      if (cufftExecZ2D(p->zi, so, p->grid_tmp + (size_t)o * p->n_grid) != CUFFT_SUCCESS)
+      double2* so = p->spec + (size_t)o * p->n_mixed;
+      HS_TRY(stage_yinv(p, o, so));
+      if (cufftExecZ2D(p->zi, (cufftDoubleComplex*)so, p->grid_tmp + (size_t)o * p->n_grid) != CUFFT_SUCCESS)
         return fail(HS_ERR_CUDA, "cuFFT z Z2D failed");
     }
     // channel-interleave the (y < ny, x < nx, z < nz) outputs for the broadcast gather
-    k_interleave<<<grid_size(ctx, p->n_grid / 2), 256, 0, st>>>(p->grid_tmp, p->n_out, p->n_grid, p->out_pitch,
-                                                                p->grid_out);
+    k_interleave<<<grid_size(ctx, p->n_grid / 2), 256, 0, st>>>(p->grid_tmp, p->n_out, p->n_grid, p->n_grid,
+                                                                p->out_pitch, p->grid_out);
     HS_LAUNCHED(ctx);
     HS_CUDA(cudaEventRecord(ev[6], st));
-    if (nt > 0) {
-      HS_TRY(sort_points_by_bin(p, tp, nt, nt, 8, p->bt_order, p->bt_start));
-      k_gather_records<<<grid_size(ctx, nt), 256, 0, st>>>(p->bt_order, nt, tp, p->TG, p->tg_orig);
-      HS_LAUNCHED(ctx);
-      HS_CUDA(cudaEventRecord(ev[13], st));
-      HS_TRY(launch_gather_fourier(ctx, p->TG, p->tg_orig, nt, p->half ? 1 : 0, p->go, p->grid_out, p->u_four, p->u,
-                                   p->u_real, p->bt_start));
-      HS_CUDA(cudaEventRecord(ev[14], st));
-      gather_timed = true;
-    }
+    HS_TRY(stage_gather(p));
   } else {
     for (int k = 3; k <= 6; ++k) HS_CUDA(cudaEventRecord(ev[k], st));
     if (nt > 0) {
@@ -1003,47 +1192,199 @@ extern "C" hs_status hs_plan_execute(hs_plan* p, const double* positions, const 
     }
   }
   HS_CUDA(cudaEventRecord(ev[7], st));
-  // ---- outputs
-  const cudaMemcpyKind ok = mem == HS_MEM_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
-  if (nt > 0) {
-    HS_CUDA(cudaMemcpyAsync(u, p->u, 24 * (size_t)nt, ok, st));
-    if (u_real) HS_CUDA(cudaMemcpyAsync(u_real, p->u_real, 24 * (size_t)nt, ok, st));
-    if (u_fourier) HS_CUDA(cudaMemcpyAsync(u_fourier, p->u_four, 24 * (size_t)nt, ok, st));
-  }
+  HS_TRY(stage_outputs(p, u, u_real, u_fourier, mem));
   HS_CUDA(cudaEventRecord(ev[8], st));
   HS_CUDA(cudaStreamSynchronize(st));
   HS_TRY(ctx_check_flags(ctx, "hs_plan_execute"));
-  if (times) {
-    float ms[9] = {0};
-    for (int k = 0; k < 8; ++k) cudaEventElapsedTime(&ms[k], ev[k], ev[k + 1]);
-    float tot = 0;
-    cudaEventElapsedTime(&tot, ev[0], ev[8]);
-    float fourier = 0;
-    cudaEventElapsedTime(&fourier, ev[2], ev[7]);
-    // [gridding, fft, scale, ifft, gather, real, fourier, prep, total, io]
-    times[0] = ms[2];
-    times[1] = ms[3];
-    times[2] = ms[4];
-    times[3] = ms[5];
-    times[4] = ms[6];
-    times[5] = ms[1];
-    times[6] = fourier;
-    times[7] = ms[0];
-    times[8] = tot;
-    times[9] = ms[7] + ms[0];
-    float kp = 0, ks = 0, kg = 0;
-    if (pair_timed) cudaEventElapsedTime(&kp, ev[9], ev[10]);
-    if (spread_timed) cudaEventElapsedTime(&ks, ev[11], ev[12]);
-    if (gather_timed) cudaEventElapsedTime(&kg, ev[13], ev[14]);
-    // kernel-only times: [10] pair, [11] spread, [12] gather, [13] scale
-    times[10] = kp;
-    times[11] = ks;
-    times[12] = kg;
-    times[13] = ms[4];
-    unsigned long long cnt[2] = {0, 0};
-    if (pair_timed) cudaMemcpy(cnt, p->pair_counts, sizeof(cnt), cudaMemcpyDeviceToHost);
-    times[14] = (double)cnt[0];  // accepted pairs
-    times[15] = (double)cnt[1];  // accepted image pairs
+  if (times) fill_times(p, times);
+  return HS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// y-slab stages (see hsewald_b200.h).  Every stage is stream-ordered on the context's
+// stream; the caller's exchanges must be ordered on the same stream (sharding.py binds
+// the context to torch's current stream).
+
+namespace {
+
+// kz split / merge between the z-stage layout [rows][nzh] and per-rank blocks [W][rows][kz_s]
+// (the all-to-all send / receive layout).  dir 0: split (lines -> blocks), 1: merge.
+struct KzSplit {
+  int w;
+  int b[65];
+};
+__global__ void k_kz_exchange(double2* __restrict__ lines, double2* __restrict__ blocks, int64_t rows, int nzh,
+                              KzSplit ks, int dir) {
+  const int64_t n = rows * nzh;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / nzh;
+    const int kz = (int)(i - r * nzh);
+    int s = 0;
+    while (s + 1 < ks.w && kz >= ks.b[s + 1]) ++s;
+    const int w = ks.b[s + 1] - ks.b[s];
+    const int64_t bi = (int64_t)ks.b[s] * rows + r * w + (kz - ks.b[s]);  // block s starts at rows * b[s]
+    if (dir == 0) blocks[bi] = lines[i];
+    else lines[i] = blocks[bi];
   }
+}
+
+// grid[c][y < P-1][x][z < nz] += ghost[c][y][x][z]
+__global__ void k_ghost_add(double* __restrict__ grid, const double* __restrict__ ghost, int nch, int planes, int nx,
+                            int nz, int pz, int64_t ch_stride) {
+  const int64_t per = (int64_t)planes * nx * nz, n = per * nch;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(i / per);
+    const int64_t r = i - c * per;
+    const int64_t line = r / nz;
+    const int z = (int)(r - line * nz);
+    grid[c * ch_stride + line * pz + z] += ghost[i];
+  }
+}
+
+KzSplit kz_split_of(const hs_plan* p) {
+  KzSplit ks{};
+  ks.w = (int)p->slab.world;
+  for (int s = 0; s <= ks.w; ++s) ks.b[s] = (int)p->slab.kz_split[s];
+  return ks;
+}
+
+hs_status check_slab(const hs_plan* p) {
+  if (!p) return fail(HS_ERR_PARAMETER, "null plan");
+  if (p->slab.world <= 0) return fail(HS_ERR_PARAMETER, "not a slab plan");
+  return HS_OK;
+}
+
+}  // namespace
+
+extern "C" hs_status hs_slab_sizes(const hs_plan* p, int64_t sizes[8]) {
+  HS_TRY(check_slab(p));
+  const int64_t nx = p->gg.dims[0], nz = p->prm.dims[2], P1 = p->prm.P - 1;
+  const int64_t nzh = p->kg.nzh;
+  sizes[0] = (int64_t)p->n_in * P1 * nx * nz;
+  sizes[1] = 2 * (int64_t)p->yo * nx * nzh;
+  sizes[2] = 2 * (int64_t)p->kg.p[1] * nx * p->nzs;
+  sizes[3] = 2 * p->prm.dims[1] * nx * p->nzs;
+  sizes[4] = P1 * nx * nz * p->out_pitch;
+  sizes[5] = p->n_in;
+  sizes[6] = p->n_out;
+  sizes[7] = p->out_pitch;
+  return HS_OK;
+}
+
+extern "C" hs_status hs_slab_begin(hs_plan* p, const double* positions, const double* sa, const double* sb,
+                                   const double* targets, const int64_t* tcols, int mem, double* ghost_out) {
+  HS_TRY(check_slab(p));
+  if (!ghost_out) return fail(HS_ERR_PARAMETER, "null ghost buffer");
+  if ((p->tabB && !p->have_B) || (p->tabH && !p->have_H)) return fail(HS_ERR_CONFIG, "missing Green's table");
+  hs_ctx* ctx = p->ctx;
+  cudaStream_t st = ctx->stream;
+  HS_TRY(begin_eval(p));
+  cudaEvent_t* ev = p->ev;
+  HS_CUDA(cudaEventRecord(ev[0], st));
+  HS_TRY(stage_inputs(p, positions, sa, sb, targets, tcols, mem));
+  HS_CUDA(cudaEventRecord(ev[1], st));
+  HS_TRY(stage_real(p, true));
+  HS_CUDA(cudaEventRecord(ev[2], st));
+  HS_TRY(stage_spread(p));
+  // ghost planes [yo, yo + P - 1) of every channel, z compacted to nz
+  const int64_t nx = p->gg.dims[0], nz = p->prm.dims[2], pz = p->kg.p[2], P1 = p->prm.P - 1;
+  for (int c = 0; c < p->n_in; ++c)
+    HS_CUDA(cudaMemcpy2DAsync(ghost_out + (size_t)c * P1 * nx * nz, nz * 8,
+                              p->grid_in + (size_t)c * p->n_grid + (size_t)p->yo * nx * pz, pz * 8, nz * 8, P1 * nx,
+                              cudaMemcpyDeviceToDevice, st));
+  HS_CUDA(cudaEventRecord(ev[3], st));
+  return HS_OK;
+}
+
+extern "C" hs_status hs_slab_forward(hs_plan* p, const double* ghost_in, double* send) {
+  HS_TRY(check_slab(p));
+  if (!send) return fail(HS_ERR_PARAMETER, "null send buffer");
+  hs_ctx* ctx = p->ctx;
+  cudaStream_t st = ctx->stream;
+  const int64_t nx = p->gg.dims[0], nz = p->prm.dims[2], pz = p->kg.p[2], P1 = p->prm.P - 1;
+  if (ghost_in && P1 > 0) {
+    k_ghost_add<<<grid_size(ctx, p->n_in * P1 * nx * nz), 256, 0, st>>>(p->grid_in, ghost_in, p->n_in, (int)P1,
+                                                                        (int)nx, (int)nz, (int)pz, p->gg.ch_stride);
+    HS_LAUNCHED(ctx);
+  }
+  set_fft_streams(p);
+  const KzSplit ks = kz_split_of(p);
+  const int64_t rows = (int64_t)p->yo * nx;
+  for (int c = 0; c < p->n_in; ++c) {
+    if (cufftExecD2Z(p->zf, p->grid_in + (size_t)c * p->n_grid, (cufftDoubleComplex*)p->Amix) != CUFFT_SUCCESS)
+      return fail(HS_ERR_CUDA, "cuFFT z D2Z failed");
+    k_kz_exchange<<<grid_size(ctx, rows * p->kg.nzh), 256, 0, st>>>(
+        p->Amix, (double2*)send + (size_t)c * p->n_amix, rows, p->kg.nzh, ks, 0);
+    HS_LAUNCHED(ctx);
+  }
+  return HS_OK;
+}
+
+extern "C" hs_status hs_slab_kspace(hs_plan* p, const double* recv, double* back) {
+  HS_TRY(check_slab(p));
+  if (!recv || !back) return fail(HS_ERR_PARAMETER, "null exchange buffer");
+  hs_ctx* ctx = p->ctx;
+  cudaStream_t st = ctx->stream;
+  set_fft_streams(p);
+  // phase events: fft = z + exchange + y, scale = x stage, ifft = y^-1 + exchange + z^-1
+  for (int c = 0; c < p->n_in; ++c) HS_TRY(stage_yfwd(p, (double2*)recv + (size_t)c * p->n_mixed, c));
+  HS_CUDA(cudaEventRecord(p->ev[4], st));
+  HS_TRY(stage_xstage(p));
+  HS_CUDA(cudaEventRecord(p->ev[5], st));
+  const size_t back_ch = (size_t)p->prm.dims[1] * p->gg.dims[0] * p->nzs;
+  for (int o = 0; o < p->n_out; ++o) HS_TRY(stage_yinv(p, o, (double2*)back + o * back_ch));
+  return HS_OK;
+}
+
+extern "C" hs_status hs_slab_backward(hs_plan* p, const double* recv_back, double* halo_out) {
+  HS_TRY(check_slab(p));
+  if (!recv_back || !halo_out) return fail(HS_ERR_PARAMETER, "null exchange buffer");
+  hs_ctx* ctx = p->ctx;
+  cudaStream_t st = ctx->stream;
+  set_fft_streams(p);
+  const int64_t nx = p->gg.dims[0], nz = p->prm.dims[2], pz = p->kg.p[2], P1 = p->prm.P - 1;
+  const KzSplit ks = kz_split_of(p);
+  const int64_t rows = (int64_t)p->yo * nx;
+  for (int o = 0; o < p->n_out; ++o) {
+    k_kz_exchange<<<grid_size(ctx, rows * p->kg.nzh), 256, 0, st>>>(
+        p->Amix, (double2*)recv_back + (size_t)o * p->n_amix, rows, p->kg.nzh, ks, 1);
+    HS_LAUNCHED(ctx);
+    if (cufftExecZ2D(p->zi, (cufftDoubleComplex*)p->Amix, p->grid_tmp + (size_t)o * p->n_grid) != CUFFT_SUCCESS)
+      return fail(HS_ERR_CUDA, "cuFFT z Z2D failed");
+  }
+  // interleave the owned planes; the ghost planes are filled by hs_slab_finish
+  const int64_t n_owned = rows * pz;
+  k_interleave<<<grid_size(ctx, n_owned / 2), 256, 0, st>>>(p->grid_tmp, p->n_out, p->n_grid, n_owned,
+                                                            p->out_pitch, p->grid_out);
+  HS_LAUNCHED(ctx);
+  // halo for rank r-1: output planes [0, P-1), z compacted
+  const int pitch = p->out_pitch;
+  HS_CUDA(cudaMemcpy2DAsync(halo_out, nz * pitch * 8, p->grid_out, pz * pitch * 8, nz * pitch * 8, P1 * nx,
+                            cudaMemcpyDeviceToDevice, st));
+  HS_CUDA(cudaEventRecord(p->ev[6], st));
+  return HS_OK;
+}
+
+extern "C" hs_status hs_slab_finish(hs_plan* p, const double* halo_in, double* u, double* u_real, double* u_fourier,
+                                    int mem, double* times) {
+  HS_TRY(check_slab(p));
+  if (!u) return fail(HS_ERR_PARAMETER, "null output");
+  hs_ctx* ctx = p->ctx;
+  cudaStream_t st = ctx->stream;
+  const int64_t nx = p->gg.dims[0], nz = p->prm.dims[2], pz = p->kg.p[2], P1 = p->prm.P - 1;
+  const int pitch = p->out_pitch;
+  double* ghost = p->grid_out + (size_t)p->yo * nx * pz * pitch;
+  if (halo_in)
+    HS_CUDA(cudaMemcpy2DAsync(ghost, pz * pitch * 8, halo_in, nz * pitch * 8, nz * pitch * 8, P1 * nx,
+                              cudaMemcpyDeviceToDevice, st));
+  else
+    HS_CUDA(cudaMemsetAsync(ghost, 0, sizeof(double) * (size_t)P1 * nx * pz * pitch, st));
+  HS_TRY(stage_gather(p));
+  HS_CUDA(cudaEventRecord(p->ev[7], st));
+  HS_TRY(stage_outputs(p, u, u_real, u_fourier, mem));
+  HS_CUDA(cudaEventRecord(p->ev[8], st));
+  HS_CUDA(cudaStreamSynchronize(st));
+  HS_TRY(ctx_check_flags(ctx, "hs_slab_finish"));
+  if (times) fill_times(p, times);
   return HS_OK;
 }

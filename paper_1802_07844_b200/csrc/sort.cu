@@ -128,7 +128,10 @@ __global__ void k_find_big(const int* __restrict__ start, int nb, int limit, int
 
 // keys[n] in [0, nb): writes order[n] (stable argsort) and start[nb+1].
 // Scratch: counts/cursor (2*nb+4 ints) + tmp (n ints).
-hs_status counting_sort(hs_ctx* ctx, const int* keys, int n, int nb, int* order, int* start, int* work) {
+hs_status counting_sort(hs_ctx* ctx, const int* keys, int n, int nb, int* order, int* start, int* work,
+                        int nb_rank) {
+  // nb_rank < nb: segments >= nb_rank are left unranked (their order entries undefined)
+  if (nb_rank < 0 || nb_rank > nb) nb_rank = nb;
   cudaStream_t st = ctx->stream;
   int* counts = work;              // nb
   int* cursor = work + nb;         // nb
@@ -148,12 +151,13 @@ hs_status counting_sort(hs_ctx* ctx, const int* keys, int n, int nb, int* order,
   k_scatter<<<gs, 256, 0, st>>>(keys, n, cursor, tmp);
   HS_LAUNCHED(ctx);
   const int kWarpLimit = 2048;
-  const int wb = (int)std::min<int64_t>(ceil_div(nb, 8), ctx->sm_count * 16);
-  k_segment_rank_warp<<<wb, 256, 0, st>>>(start, nb, tmp, order, kWarpLimit);
+  if (nb_rank == 0) return HS_OK;
+  const int wb = (int)std::min<int64_t>(ceil_div(nb_rank, 8), ctx->sm_count * 16);
+  k_segment_rank_warp<<<wb, 256, 0, st>>>(start, nb_rank, tmp, order, kWarpLimit);
   HS_LAUNCHED(ctx);
   // segments longer than kWarpLimit (clustered or degenerate cell lists): one CTA each
   int* big = cursor;  // cursor is dead after the scatter
-  k_find_big<<<(int)ceil_div(nb, 256), 256, 0, st>>>(start, nb, kWarpLimit, big, nbig);
+  k_find_big<<<(int)ceil_div(nb_rank, 256), 256, 0, st>>>(start, nb_rank, kWarpLimit, big, nbig);
   HS_LAUNCHED(ctx);
   k_segment_rank_block<<<ctx->sm_count, 1024, 0, st>>>(start, big, nbig, tmp, order);
   HS_LAUNCHED(ctx);

@@ -132,6 +132,22 @@ def test_spread_out_of_grid(gpu):
         gpu.spread(np.array([[2.5, 0.5, 0.5]]), np.ones((1, 1)), g)
 
 
+@pytest.mark.parametrize("tg", ([[0.25, np.nextafter(1.0, 0.0), 0.5]],
+                                [[0.5, 0.5, 0.5], [0.25, np.nextafter(1.0, 0.0), 0.5]]))
+def test_gather_target_window_leaving_grid_raises(gpu, tg):
+    """A target whose window leaves the grid (y = 1 - ulp rounds to the top node) raises
+    GeometryError like the reference's gather (_gridding.py:50-52) -- also when it is alone in
+    its work item (regression: an all-inactive item must not touch memory)."""
+    from paper_1802_07844_b200.configs import make_system
+    s, _ = make_system("cfg3", n=3000)
+    p = gpu.EwaldParams(xi=33.28, rc=0.12, M=128, P=24)
+    with pytest.raises(gpu.GeometryError):
+        gpu.ewald_sum(s, p, targets=np.array(tg))
+    # the context stays usable
+    r = gpu.ewald_sum(s, p, targets=np.array([[0.5, 0.5, 0.5]]))
+    assert np.all(np.isfinite(r.velocities))
+
+
 @pytest.mark.parametrize("geom", ("half", "free"))
 @pytest.mark.parametrize("kind", ("harmonic", "biharmonic"))
 def test_tables_golden(gpu, geom, kind):
