@@ -10,9 +10,12 @@ inside the timed region).  `--impl reference` times the CPU restatement of the
 reference (oracle/, OpenMP C + scipy.fft) on a bounded sample of the same
 workload, extrapolated to the full evaluation.
 
-Multi-GPU (torchrun): every rank evaluates its own independent HL system
-(replicas, weak scaling); the sharded single-system path is future work
-(DESIGN.md section 7).
+Multi-GPU (torchrun), two modes:
+  --mode replicas (default): every rank evaluates its own independent HL system
+      (weak scaling, no data-path collective);
+  --mode slab: ONE system y-slab decomposed over the ranks (sharding.py: spread
+      ghost planes, per-channel NCCL all-to-all transposes of the FFT, gather halo;
+      strong scaling, value = N / time of one sharded evaluation).
 """
 
 from __future__ import annotations
@@ -353,6 +356,87 @@ def run_ours(args, rank, world, local_rank):
         dist.destroy_process_group()
 
 
+def run_slab(args, rank, world, local_rank):
+    """One system, y-slab decomposed over `world` ranks (strong scaling)."""
+    import torch
+    import torch.distributed as dist
+    from paper_1802_07844_b200 import EwaldParams, _lib
+    from paper_1802_07844_b200.configs import WORKLOADS, make_system
+    from paper_1802_07844_b200.sharding import DistExchange, _rank_inputs, run_slab_pipeline, slab_rank
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo", device_id=dev,
+                            rank=rank, world_size=world)
+    w = WORKLOADS[args.workload]
+    s, targets = make_system(w)
+    p = EwaldParams(xi=w.xi, rc=w.rc, M=w.M, P=w.P)
+    st, lay, tg, ti, rows = slab_rank(s, p, targets=targets, device=local_rank)
+    t0 = time.perf_counter()
+    st.build_tables()
+    t_tables = time.perf_counter() - t0
+    inputs = {rank: _rank_inputs(s, tg, ti, rows, rank, dev)}
+    xch = DistExchange()
+    for _ in range(args.warmup):
+        run_slab_pipeline([st], xch, inputs)
+    ctx = _lib.Context.get(local_rank)
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    time.sleep(0.25)
+    dist.barrier()
+    torch.cuda.synchronize()
+    l0 = ctx.launches()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    step_times = []
+    for _ in range(args.steps):
+        step_times.append(run_slab_pipeline([st], xch, inputs)[rank])
+    e1.record()
+    torch.cuda.synchronize()
+    dist.barrier()
+    launches = ctx.launches() - l0
+    clk = clocks.stop()
+    tt = torch.tensor([e0.elapsed_time(e1)], device=dev)
+    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    ms = float(tt.item())
+    n_t = tg.shape[0]
+    value = n_t * args.steps / (ms * 1e-3)
+    # e2e: this rank's inputs copied from pinned host memory and its rows read back, every step
+    pin = [None if a is None else a.cpu().pin_memory() for a in inputs[rank]]
+    hu = torch.empty((max(len(rows[rank]), 1), 3), dtype=torch.float64).pin_memory()
+    bi = sum(a.numel() * a.element_size() for a in pin if a is not None)
+    dist.barrier()
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(args.steps):
+        dins = {rank: tuple(None if a is None else a.to(dev, non_blocking=True) for a in pin)}
+        run_slab_pipeline([st], xch, dins)
+        hu.copy_(st.out[0, :hu.shape[0]], non_blocking=True)
+    e1.record()
+    torch.cuda.synchronize()
+    tt = torch.tensor([e0.elapsed_time(e1)], device=dev)
+    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    ms_e2e = float(tt.item())
+    avg = {k: float(np.mean([t[k] for t in step_times])) for k in step_times[0]}
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded PCG64, BASELINE.json shapes)",
+            "config": {"workload": w.name, "kind": w.kind, "n": s.n, "n_targets": n_t, "xi": w.xi, "rc": w.rc,
+                       "M": w.M, "P": w.P, "parallelism": f"yslab{world}", "y_split": lay.y_split,
+                       "kz_split": lay.kz_split,
+                       "l2": "not flushed: each step streams >30 GB of grids/spectra through HBM (126 MB L2)"},
+            "e2e": {"value": n_t * args.steps / (ms_e2e * 1e-3), "unit": UNIT, "h2d_bytes_per_step": int(bi),
+                    "d2h_bytes_per_step": int(hu.numel() * 8), "ms_per_step": ms_e2e / args.steps},
+            "gpu_launches": int(launches), "gpu_launches_note": "hand-written kernels only; cuFFT/NCCL excluded",
+            "phases_ms_rank0": {k: round(avg[k], 4) for k in ("real", "gridding", "fft", "scale", "ifft", "gather",
+                                                              "total")},
+            "targets_per_rank": [len(r) for r in rows], "precompute_tables_s": round(t_tables, 3),
+            "plan_device_bytes_rank0": st.ev.device_bytes, "clocks": clk}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser(description=__doc__)
     ap.add_argument("--gpus", type=int, default=1)
@@ -361,6 +445,8 @@ def main():
     ap.add_argument("--impl", default="b200", choices=("b200", "reference"))
     ap.add_argument("--workload", default="HL")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--mode", default="replicas", choices=("replicas", "slab"),
+                    help="multi-GPU decomposition: independent replicas (weak) or one y-slab sharded system (strong)")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -369,6 +455,10 @@ def main():
         args.warmup = 3
     if args.impl == "reference":
         run_reference(args, rank)
+    elif args.mode == "slab":
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29511")
+        run_slab(args, rank, world, local_rank)
     else:
         run_ours(args, rank, world, local_rank)
 

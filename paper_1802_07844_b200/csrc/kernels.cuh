@@ -35,18 +35,20 @@ struct GridGeom {
   int P;
   int64_t stride[3];       // element strides of the storage layout (x, y, z)
   int64_t ch_stride;       // element stride between channels
-  // y-slab decomposition (sharding.py): stored node (i,j,k) is global node (i, j + off[1], k);
+  // y-slab decomposition (sharding.py): stored node (i,j,k) is global node (i, j + yoff, k);
   // window starts are computed from the GLOBAL geometry (bit-identical on every rank) and
   // shifted.  sel: spreading keeps only points whose local y window start is in [sel_lo, sel_hi)
-  int off[3];
+  int yoff;
   int sel, sel_lo, sel_hi;
 };
-// window start / node distance in the grid's local node numbering (off = 0: _gridding.py:24-29)
+// window start / node distance in the grid's local node numbering (yoff = 0: _gridding.py:24-29);
+// only y is ever offset, so x / z (k a compile-time constant at every call) cost nothing extra
 __device__ __forceinline__ int64_t g_lo(const GridGeom& g, int k, double pos) {
-  return window_lo(pos, g.origin[k], g.h, g.P) - g.off[k];
+  const int64_t l = window_lo(pos, g.origin[k], g.h, g.P);
+  return k == 1 ? l - g.yoff : l;
 }
 __device__ __forceinline__ double g_d(const GridGeom& g, int k, double pos, int64_t local_idx) {
-  return window_d(pos, g.origin[k], g.h, local_idx + g.off[k]);
+  return window_d(pos, g.origin[k], g.h, k == 1 ? local_idx + g.yoff : local_idx);
 }
 constexpr int SP_TX = 16, SP_TY = 16, SP_TZ = 8;  // spread tile / bin shape
 // gather target order: (4x4 (x,y) column, z node) of the window-centre node (v5: 8x8 columns)

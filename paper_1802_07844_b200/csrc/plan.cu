@@ -371,7 +371,7 @@ static hs_status plan_create_impl(hs_ctx* ctx, const hs_params* prm, const hs_sl
     p->nzs = (int)(s.kz1 - s.kz0);
     nyd = p->yo + prm->P - 1;
     g.dims[1] = (int)nyd;
-    g.off[1] = (int)s.y0;
+    g.yoff = (int)s.y0;
     g.sel = 1;
     g.sel_lo = 0;
     g.sel_hi = p->yo;
