@@ -313,7 +313,9 @@ def run_ours(args, rank, world, local_rank):
     n_half = grid.padded_dims[0] * grid.padded_dims[1] * (grid.padded_dims[2] // 2 + 1)
     pairs, img_pairs = avg["pairs"], avg["image_pairs"]
     work = {
-        "k_spread": ("flop", 2.0 * P3 * (2 * s.n * 3 + s.n * 4), "fp64:dmma"),
+        # mirrored spreading (csrc/plan.cu k_mirror_z): 3 kernel + 4 wall channels at the N
+        # sources, images by reflection of the grid (10 N P^3 -> 7 N P^3 FMAs)
+        "k_spread": ("flop", 2.0 * P3 * 7 * s.n, "fp64:dmma"),
         "k_gather": ("flop", 2.0 * P3 * 6 * s.n, "fp64:dfma"),
         "k_scale": ("bytes", n_half * (16 * 7 + 16 * 6 + 8 * 2), "hbm"),
         "k_pair": ("flop", 2.0 * (64 * pairs + 33 * img_pairs), "fp64:dfma"),

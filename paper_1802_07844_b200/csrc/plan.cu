@@ -79,19 +79,24 @@ __global__ void k_target_records(const int* __restrict__ order, int nt, const do
 }
 
 // spread source records in bin order.  set 0: kernel sources [y; y^I]; set 1: images y^I
-// with wall channels.  W has nch doubles per row (see kspace.cu channel layout).
+// with wall channels; set 2 (mirrored spreading, see k_mirror_z): the sources y themselves
+// carrying their kernel channels followed by their images' wall channels.  W has nch
+// doubles per row (see kspace.cu channel layout).
 __global__ void k_spread_records(int kind, int half, int set, const int* __restrict__ order, int n_rows, int n,
                                  const double* __restrict__ pos, const double* __restrict__ sa,
                                  const double* __restrict__ sb, int nch, double4* __restrict__ P,
                                  double* __restrict__ W) {
+  const int nk_m = kind == HS_STRESSLET ? 6 : 3;  // set 2: kernel channels before the wall channels
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n_rows; k += gridDim.x * blockDim.x) {
     const int i = order[k];
-    const bool img = (set == 1) || (half && i >= n);
+    const bool img = (set == 1) || (set == 0 && half && i >= n);
     const int s = (set == 0 && half && i >= n) ? i - n : i;
     const double m = img ? -1.0 : 1.0;
     const double y3 = pos[3 * s + 2];
     P[k] = make_double4(pos[3 * s], pos[3 * s + 1], m * y3, 0.0);
     double* w = W + (size_t)k * nch;
+    for (int part = (set == 2 ? 0 : set); part <= (set == 2 ? 1 : set); ++part) {
+    if (set == 2 && part == 1) w += nk_m;
     const double a0 = sa[3 * s], a1 = sa[3 * s + 1], a2 = sa[3 * s + 2];
     double b0 = 0, b1 = 0, b2 = 0;
     if (kind != HS_STOKESLET) {
@@ -99,7 +104,7 @@ __global__ void k_spread_records(int kind, int half, int set, const int* __restr
       b1 = sb[3 * s + 1];
       b2 = sb[3 * s + 2];
     }
-    if (set == 0) {
+    if (part == 0) {
       if (kind == HS_STOKESLET) {  // _kernel_weights: combined_f (ewald_fourier.py:357-359)
         w[0] = img ? -a0 : a0;
         w[1] = img ? -a1 : a1;
@@ -141,6 +146,46 @@ __global__ void k_spread_records(int kind, int half, int set, const int* __restr
         w[0] = 4.0 * (b2 * g0 - a2 * q0);
         w[1] = 4.0 * (b2 * g1 - a2 * q1);
       }
+    }
+    }
+  }
+}
+
+// Mirrored spreading (half space).  Grid node k of z sits at -Lt + k h, so node 2Mt - k is
+// its mirror image through the wall.  An image source y^I = (y1, y2, -y3) carries the
+// kernel channels of its source up to a per-channel sign sigma_c (exact sign flips of the
+// same products; k_spread_records set 0): stokeslet -f^I = (-f1, -f2, f3), stresslet
+// -(R g)(R q)^T, rotlet -(Rg x Rq) = R (g x q).  Its window is the mirror of the source's
+// window (floor((-y3 - o)/h) = 2Mt - 1 - floor((y3 - o)/h) up to rounding at exact node
+// hits, where the dropped edge weight is exp(-pi P c^2 / 2) ~ 1e-15 relative).  So with S the
+// spread of the N sources only (kernel + wall channels at y),
+//   kernel channels:  G_c(k) = S_c(k) + sigma_c S_c(2Mt - k)
+//   wall channels:    G_c(k) = S_c(2Mt - k)           (spread at the images y^I only)
+// which replaces spreading 2N kernel + N wall sources (10 N P^3 for the stokeslet) by N
+// sources (7 N P^3) and one pass over the grid.  In place, one thread per mirror pair.
+__global__ void k_mirror_z(double* __restrict__ grid, int nch, int nk, unsigned sigma_neg, int64_t ch_stride,
+                           int64_t lines, int pz, int nz) {
+  const int half_n = nz / 2;  // pairs (k, nz - k) for k = 1 .. nz/2 - 1, plus k = nz/2 and k = 0
+  const int64_t per = lines * (half_n + 1);
+  const int64_t n = per * nch;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(i / per);
+    const int64_t r = i - c * per;
+    const int64_t line = r / (half_n + 1);
+    const int k = (int)(r - line * (half_n + 1));
+    double* g = grid + c * ch_stride + line * pz;
+    const bool kern = c < nk;
+    const double sg = ((sigma_neg >> c) & 1u) ? -1.0 : 1.0;
+    if (k == 0) {  // mirror of node 0 is node nz (outside the grid, where S = 0)
+      if (!kern) g[0] = 0.0;
+    } else if (k == half_n) {  // the wall plane is its own mirror
+      const double v = g[k];
+      g[k] = kern ? v + sg * v : v;
+    } else {
+      const int kk = nz - k;
+      const double a = g[k], b = g[kk];
+      g[k] = kern ? a + sg * b : b;
+      g[kk] = kern ? b + sg * a : a;
     }
   }
 }
@@ -271,6 +316,7 @@ struct hs_plan {
   const long long* cur_tc = nullptr;
   int cur_tcol_identity = 0;
   bool pair_timed = false, spread_timed = false, gather_timed = false;
+  bool mirror = false;          // half space: spread the N sources once and mirror (k_mirror_z)
 };
 
 namespace {
@@ -429,8 +475,10 @@ static hs_status plan_create_impl(hs_ctx* ctx, const hs_params* prm, const hs_sl
   A_(nb + 2, p->bc_start);
   A_(std::max(nt, 1), p->bt_order);
   A_((size_t)gather_keys(g) + 1, p->bt_start);
+  // mirrored spreading (half space; HS_SPREAD_IMAGES=1 spreads the images explicitly, comparison)
+  p->mirror = p->half && !getenv("HS_SPREAD_IMAGES");
   A_(p->n_comb, p->SPk);
-  A_((size_t)p->n_comb * p->nk, p->SWk);
+  A_(std::max((size_t)p->n_comb * p->nk, (size_t)n * p->n_in), p->SWk);
   if (p->nc) {
     A_(n, p->SPc);
     A_((size_t)n * p->nc, p->SWc);
@@ -977,6 +1025,44 @@ hs_status stage_real(hs_plan* p, bool want) {
   return HS_OK;
 }
 
+unsigned mirror_sigma_neg(int kind) {
+  // channels whose image value is minus the source value (k_spread_records set 0)
+  if (kind == HS_STOKESLET) return 0x3u;               // (-, -, +)
+  if (kind == HS_STRESSLET) return 0x1u | 0x2u | 0x8u | 0x20u;  // 00 01 11 22 negative, 02 12 positive
+  return 0x4u;                                          // rotlet (+, +, -)
+}
+
+// half space: spread the N sources with kernel + wall channels, then mirror (k_mirror_z)
+hs_status stage_spread_mirrored(hs_plan* p) {
+  hs_ctx* ctx = p->ctx;
+  cudaStream_t st = ctx->stream;
+  const hs_params& prm = p->prm;
+  const int n = (int)prm.n, kind = prm.kind;
+  HS_TRY(sort_points_by_bin(p, p->cur_pos, n, n, 0, p->bk_order, p->bk_start));
+  int n_sel = n;
+  if (p->slab.world > 0) {
+    HS_CUDA(cudaMemcpyAsync(&n_sel, p->bk_start + p->nbins, sizeof(int), cudaMemcpyDeviceToHost, st));
+    HS_CUDA(cudaStreamSynchronize(st));
+  }
+  p->n_sel_k = n_sel;
+  p->n_sel_c = 0;
+  if (n_sel > 0) {
+    k_spread_records<<<grid_size(ctx, n_sel), 256, 0, st>>>(kind, 1, 2, p->bk_order, n_sel, n, p->cur_pos, p->cur_fa,
+                                                            p->cur_fb, p->n_in, p->SPk, p->SWk);
+    HS_LAUNCHED(ctx);
+  }
+  HS_CUDA(cudaEventRecord(p->ev[11], st));
+  HS_TRY(launch_spread(ctx, p->SPk, p->SWk, n_sel, p->n_in, p->bk_start, p->gg, p->grid_in));
+  const int64_t lines = (int64_t)p->gg.dims[1] * p->gg.dims[0];
+  const int nz = p->gg.dims[2];
+  k_mirror_z<<<grid_size(ctx, lines * (nz / 2 + 1) * p->n_in), 256, 0, st>>>(
+      p->grid_in, p->n_in, p->nk, mirror_sigma_neg(kind), p->gg.ch_stride, lines, p->kg.p[2], nz);
+  HS_LAUNCHED(ctx);
+  HS_CUDA(cudaEventRecord(p->ev[12], st));
+  p->spread_timed = true;
+  return HS_OK;
+}
+
 // spreading of kernel sources [y; y^I] (or y) and wall-correction sources y^I into grid_in
 // (ewald_fourier.py:319-332,353-382); a slab plan keeps the sources whose y window starts
 // in its slab (k_grid_keys drop bin)
@@ -987,6 +1073,7 @@ hs_status stage_spread(hs_plan* p) {
   const int n = (int)prm.n, kind = prm.kind;
   const double *pos = p->cur_pos, *fa = p->cur_fa, *fb = p->cur_fb;
   const bool sl = p->slab.world > 0;
+  if (p->mirror) return stage_spread_mirrored(p);
   HS_TRY(sort_points_by_bin(p, pos, n, p->n_comb, p->half ? 1 : 0, p->bk_order, p->bk_start));
   if (p->nc) HS_TRY(sort_points_by_bin(p, pos, n, n, 2, p->bc_order, p->bc_start));
   int nk_sel = p->n_comb, nc_sel = n;
