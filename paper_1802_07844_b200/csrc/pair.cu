@@ -347,6 +347,11 @@ __global__ void __launch_bounds__(PC_TG, PC_MINB) k_pair_q(const PairArgs a) {
           break;
         }
     }
+    // stride permutation, incrementally: thread tid stages v = ((c0 + tid) * pstride) mod ncand,
+    // and c0 advances by PC_H per chunk (PC_H == PC_TG: one candidate per thread per chunk)
+    static_assert(PC_H == PC_TG, "one staged candidate per thread per chunk");
+    const int vstep = (int)(((long long)PC_H * pstride) % max(ncand, 1));
+    int vcur = (int)(((long long)threadIdx.x * pstride) % max(ncand, 1));
     auto pop_eval = [&]() {
       const int jj = q[head & (PC_Q - 1)][lane];
       ++head;
@@ -380,15 +385,23 @@ __global__ void __launch_bounds__(PC_TG, PC_MINB) k_pair_q(const PairArgs a) {
         if (tail > head && (q[head & (PC_Q - 1)][lane] >> 7) == h) pop_eval();
       }
       __syncthreads();
-      for (int j = threadIdx.x; j < PC_H; j += PC_TG) {
+      {
+        const int j = threadIdx.x;
         const int v0 = c0 + j;
+        const int v = vcur;
+        vcur += vstep;
+        if (vcur >= ncand) vcur -= ncand;
         if (v0 < ncand) {
           // stride permutation of the candidate list: every chunk samples the whole
           // neighbourhood, so each lane's acceptance rate per chunk is about its average
-          // and the full-round evaluation below keeps all lanes busy
-          const int v = (int)(((long long)v0 * pstride) % ncand);
-          int r = 0;
-          while (r + 1 < nrun && run_pre[r + 1] <= v) ++r;
+          // and the full-round evaluation below keeps all lanes busy.  Run of v: binary search
+          // for the last run_pre[r] <= v (run_pre[0] = 0)
+          int r = 0, rhi = nrun - 1;
+          while (r < rhi) {
+            const int mid = (r + rhi + 1) >> 1;
+            if (run_pre[mid] <= v) r = mid;
+            else rhi = mid - 1;
+          }
           const int row = run_beg[r] + (v - run_pre[r]);
           const double4 S = a.P[row];
           const double4 A = a.A[row];
@@ -422,32 +435,49 @@ __global__ void __launch_bounds__(PC_TG, PC_MINB) k_pair_q(const PairArgs a) {
           }
           near = __ballot_sync(0xffffffffu, keep);
         }
-        while (near) {
-          const int j = hb + j0 + __ffs(near) - 1;
-          near &= near - 1;
-          const float4 F = sF[j];  // broadcast
+        // FP32 distance inside r_c by a margin far above its rounding error: the exact
+        // reference test would accept too; in the shell around r_c run the exact test
+        // (bit-identical neighbour sets).  The slot at `tail` is free (tail - head < PC_Q),
+        // so every tested candidate is written there and `tail` advances only on accept.
+        auto test_fp32 = [&](const float4& F, bool& sure, bool& shell) {
           const float fx = tfx - F.x, fy = tfy - F.y, fz = tfz - F.z;
           const float r2f = fx * fx + fy * fy + fz * fz;
-          if (r2f <= a.rc2_hi) {
-            // FP32 distance inside r_c by a margin far above its rounding error: the exact
-            // reference test would accept too; otherwise run it (bit-identical neighbour sets)
-            bool ok = r2f > 0.0f && r2f <= a.rc2_lo, sing = false;
-            if (!ok) {
-              const double2 xy = sXY[j];
-              const double sz = sZA[j].x;
-              const double d0 = __dsub_rn(T.x, xy.x), d1 = __dsub_rn(T.y, xy.y), d2 = __dsub_rn(T.z, sz);
-              const double r2 = exact_r2(d0, d1, d2);
-              ok = r2 <= a.rc2;
-              sing = r2 == 0.0;
-            }
-            if (ok && __float_as_int(F.w) != tcol_i && tvalid) {
-              if (sing) {
-                singular = true;
-              } else {
-                q[tail & (PC_Q - 1)][lane] = (unsigned short)j;
-                ++tail;
-              }
-            }
+          sure = r2f > 0.0f && r2f <= a.rc2_lo;
+          shell = !sure && r2f <= a.rc2_hi;
+        };
+        auto push = [&](int j, const float4& F, bool sure, bool shell) {
+          bool ok = sure;
+          if (shell) {
+            const double2 xy = sXY[j];
+            const double sz = sZA[j].x;
+            const double d0 = __dsub_rn(T.x, xy.x), d1 = __dsub_rn(T.y, xy.y), d2 = __dsub_rn(T.z, sz);
+            const double r2 = exact_r2(d0, d1, d2);
+            const bool own = __float_as_int(F.w) != tcol_i && tvalid;
+            singular |= own && r2 == 0.0;
+            ok = r2 <= a.rc2 && r2 != 0.0;
+          }
+          ok = ok && __float_as_int(F.w) != tcol_i && tvalid;
+          q[tail & (PC_Q - 1)][lane] = (unsigned short)j;
+          tail += ok ? 1 : 0;
+        };
+        // two candidates per iteration: independent broadcast loads and tests
+        while (near) {
+          const int ja = hb + j0 + __ffs(near) - 1;
+          near &= near - 1;
+          if (near) {
+            const int jb = hb + j0 + __ffs(near) - 1;
+            near &= near - 1;
+            const float4 Fa = sF[ja], Fb = sF[jb];  // broadcast
+            bool sa, ha, sb, hb2;
+            test_fp32(Fa, sa, ha);
+            test_fp32(Fb, sb, hb2);
+            push(ja, Fa, sa, ha);
+            push(jb, Fb, sb, hb2);
+          } else {
+            const float4 Fa = sF[ja];
+            bool sa, ha;
+            test_fp32(Fa, sa, ha);
+            push(ja, Fa, sa, ha);
           }
         }
         // full rounds while every valid lane has work; partial rounds only against overflow
