@@ -396,6 +396,11 @@ __device__ __forceinline__ void cpa8(void* smem, const void* gmem) {
 #define SW_K_DEF 8
 #endif
 constexpr int SW_CH = SW_CH_DEF, SW_K = SW_K_DEF, SW_H = SW_CH_DEF / 32, SW_RX = SP_TX + 2, SW_RY = SP_TY + 2, SW_RZ = SP_TZ + 2;
+// producer warps (8, 9, ...): producer p stages the chunks c = p mod SW_NP, so the SW_K ring
+// slots of one producer are fixed (SW_K % SW_NP == 0) and one warp's staging rate no longer
+// bounds the eight consumers
+constexpr int SW_NP = 2, SW_THREADS = (8 + SW_NP) * 32;
+static_assert(SW_K % SW_NP == 0, "ring slots must divide among the producers");
 template <int NCH>
 struct SwBuf {
   static constexpr int RQ = NCH | 1;
@@ -403,7 +408,7 @@ struct SwBuf {
 };
 
 template <int NCH>
-__global__ void __launch_bounds__(288, 2) k_spread_mma4(const int4* __restrict__ lo4, const double* __restrict__ tab,
+__global__ void __launch_bounds__(SW_THREADS, 2) k_spread_mma4(const int4* __restrict__ lo4, const double* __restrict__ tab,
                                                        WTab wt, const double* __restrict__ w, int ldw,
                                                        const int* __restrict__ bin_start, GridGeom g, int nbx,
                                                        int nby, int nbz, double* __restrict__ grids) {
@@ -452,8 +457,9 @@ __global__ void __launch_bounds__(288, 2) k_spread_mma4(const int4* __restrict__
   const int nrun = s_nrun, ncand = run_pre[nrun];
   const int nchunk = (ncand + SW_CH - 1) / SW_CH;
 
-  if (warp == 8) {
-    // ---------------- producer ----------------
+  if (warp >= 8) {
+    // ---------------- producers ----------------
+    const int pid = warp - 8;
     // rows / windows starts / weights of chunk c+1 and c+2 are in flight (registers) while
     // chunk c is staged, so the producer runs at one chunk per staging pass, not per load latency
     struct Pre {
@@ -467,8 +473,12 @@ __global__ void __launch_bounds__(288, 2) k_spread_mma4(const int4* __restrict__
         const int v = c * SW_CH + lane + 32 * h;
         f.row[h] = -1;
         if (c < nchunk && v < ncand) {
-          int r = 0;
-          while (r + 1 < nrun && run_pre[r + 1] <= v) ++r;
+          int r = 0, rhi = nrun - 1;  // last run with run_pre[r] <= v
+          while (r < rhi) {
+            const int mid = (r + rhi + 1) >> 1;
+            if (run_pre[mid] <= v) r = mid;
+            else rhi = mid - 1;
+          }
           const int row = run_beg[r] + (v - run_pre[r]);
           f.row[h] = row;
           f.lo[h] = lo4[row];
@@ -478,13 +488,13 @@ __global__ void __launch_bounds__(288, 2) k_spread_mma4(const int4* __restrict__
       }
     };
     Pre f1, f2;
-    fetch(0, f1);
-    fetch(1, f2);
-    for (int c = 0; c < nchunk; ++c) {
+    fetch(pid, f1);
+    fetch(pid + SW_NP, f2);
+    for (int c = pid; c < nchunk; c += SW_NP) {
       const int b = c % SW_K;
       const Pre cur = f1;
       f1 = f2;
-      fetch(c + 2, f2);
+      fetch(c + 2 * SW_NP, f2);
       if (c >= SW_K) mbar_wait(&empty_bar[b], ((c / SW_K) - 1) & 1);
       unsigned m[SW_H];
       int ex[SW_H], ey[SW_H], ez[SW_H];
@@ -917,7 +927,8 @@ hs_status launch_spread(hs_ctx* ctx, const double4* pts, const double* w, int n,
   case N: {                                                                                                          \
     const size_t smm = sizeof(double) * SW_K * SwBuf<N>::DOUBLES;                                                    \
     HS_CUDA(cudaFuncSetAttribute(k_spread_mma4<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smm));          \
-    k_spread_mma4<N><<<grid, 288, smm, ctx->stream>>>(lo, tab, wt, wc0, nch, bin_start, g, nbx, nby, nbz, gout);    \
+    k_spread_mma4<N><<<grid, SW_THREADS, smm, ctx->stream>>>(lo, tab, wt, wc0, nch, bin_start, g, nbx, nby, nbz, \
+                                                             gout);                                                \
   } break;
         HS_SP3(1) HS_SP3(2) HS_SP3(3) HS_SP3(4)
 #undef HS_SP3

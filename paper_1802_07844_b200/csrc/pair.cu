@@ -52,6 +52,32 @@ __device__ __forceinline__ double erfc_from_E(double xw, double E, const double2
   return E * p;
 }
 
+// erfc(x) = exp(-x^2) erfcx(x) without tables (default; HS_ERFC_TABLE=1 at build time selects
+// the piecewise table above): erfcx as one degree-18 polynomial in s = S0 + S1/(x + 3) on
+// [0, 8] (tools/gen_erfcx_poly.py, max rel. error 6.9e-15; the reference's own Hermite table
+// is ~2e-13, ewald_real.py:33-58), coefficients as constant-bank DFMA operands.  Trades the
+// table's six lane-divergent 16-byte shared-memory loads per pair (the pair kernel's
+// shared-memory pipe is its co-bottleneck) for ~12 more DFMAs.  x > 8 (xi r_c > 8 only):
+// evaluated at 8, where erfc < 1.2e-29, below the resolution of any sum it enters.
+#include "erfcx_poly.inc"
+__device__ __forceinline__ double rcp_pos(double v) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(v));
+#pragma unroll
+  for (int it = 0; it < 2; ++it) y = fma(y, fma(-v, y, 1.0), y);
+  return y;
+}
+__device__ __forceinline__ double erfc_poly_from_E(double x, double E) {
+  const double s = fma(HS_EP_S1, rcp_pos(fmin(x, HS_EP_XMAX) + HS_EP_K), HS_EP_S0);
+  double p = c_erfcx_poly[0];
+#pragma unroll
+  for (int j = 1; j <= HS_EP_DEG; ++j) p = fma(p, s, c_erfcx_poly[j]);
+  return E * p;
+}
+#ifndef HS_ERFC_TABLE
+#define HS_ERFC_TABLE 0
+#endif
+
 // exp(x) for x <= 0, branch-free (no special-case slow path, so two pair evaluations
 // interleave freely): x = n ln2 + r, |r| <= ln2/2, Taylor degree 13 (truncation 5e-18),
 // 2^n assembled in the exponent field; below -708 (2^n subnormal) the result flushes to 0.
@@ -106,7 +132,7 @@ __device__ __forceinline__ PairCoef pair_coef(const PairConst& pc, double r2, co
     q.ri = rsqrt_pos(r2);
     const double rn = r2 * q.ri;
     const double E = exp_nonpos(-pc.xi2 * r2);
-    C = erfc_from_E(pc.xiw * rn, E, etab);
+    C = HS_ERFC_TABLE ? erfc_from_E(pc.xiw * rn, E, etab) : erfc_poly_from_E(pc.xi * rn, E);
     q.e = pc.c2xs * E;
   } else {
     q.ri = rsqrt(r2);
@@ -240,8 +266,9 @@ __global__ void __launch_bounds__(PC_TG, PC_MINB) k_pair_q(const PairArgs a) {
   __shared__ int run_beg[PT_MAXRUN];
   __shared__ int run_pre[PT_MAXRUN + 1];
   __shared__ int s_nrun;
-  __shared__ double2 s_erfcx[HS_ERFCX_NPAIR * HS_ERFCX_NINT];
-  for (int i = threadIdx.x; i < HS_ERFCX_NPAIR * HS_ERFCX_NINT; i += blockDim.x) s_erfcx[i] = g_erfcx_coef[i];
+  __shared__ double2 s_erfcx[HS_ERFC_TABLE ? HS_ERFCX_NPAIR * HS_ERFCX_NINT : 1];
+  if (HS_ERFC_TABLE)
+    for (int i = threadIdx.x; i < HS_ERFCX_NPAIR * HS_ERFCX_NINT; i += blockDim.x) s_erfcx[i] = g_erfcx_coef[i];
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nx = a.dims[0], ny = a.dims[1], nz = a.dims[2];
