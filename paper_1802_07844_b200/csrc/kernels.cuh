@@ -7,7 +7,9 @@ namespace hs {
 // sort.cu
 hs_status counting_sort(hs_ctx* ctx, const int* keys, int n, int nb, int* order, int* start, int* work,
                         int nb_rank = -1);
-inline size_t counting_sort_work_ints(int n, int nb) { return (size_t)2 * nb + 4 + (size_t)n; }
+inline size_t counting_sort_work_ints(int n, int nb) {
+  return (size_t)2 * nb + 4 + (size_t)n + 3 * (size_t)ceil_div(nb, 2048) + 8;  // + multi-CTA scan scratch
+}
 // exclusive scan of in[0..n) into out[0..n] (out[n] = total); scratch: n + 2 ints
 hs_status exclusive_scan(hs_ctx* ctx, const int* in, int n, int* out, int* scratch);
 

@@ -66,6 +66,61 @@ __global__ void k_scan(const int* __restrict__ counts, int nb, int* __restrict__
   if (lane == 0) atomicMax(max_count, local_max);
 }
 
+// Multi-CTA exclusive scan for large key ranges (the gather's (4x4 block, z node) keys reach
+// ~1.3 M bins at HL, where the single-CTA scan above took 0.2 ms per sort):
+// tile sums -> single-CTA scan of the tile sums -> per-tile rescan with the tile offset.
+constexpr int SCAN_T = 1024, SCAN_TILE = 2 * SCAN_T;
+__device__ __forceinline__ int block_excl_scan(int v, int* ws, int* total) {
+  // exclusive scan of v over the CTA (SCAN_T threads); *total = CTA sum (smem broadcast)
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) ws[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    int w = ws[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += y;
+    }
+    ws[lane] = w;
+  }
+  __syncthreads();
+  const int r = (warp > 0 ? ws[warp - 1] : 0) + x - v;
+  *total = ws[31];
+  __syncthreads();
+  return r;
+}
+__global__ void __launch_bounds__(SCAN_T) k_scan_tiles(const int* __restrict__ counts, int nb, int* __restrict__ sums,
+                                                       int* __restrict__ max_count) {
+  __shared__ int ws[32];
+  const int i = blockIdx.x * SCAN_TILE + 2 * threadIdx.x;
+  const int a = i < nb ? counts[i] : 0, b = i + 1 < nb ? counts[i + 1] : 0;
+  int tot;
+  block_excl_scan(a + b, ws, &tot);
+  if (threadIdx.x == 0) sums[blockIdx.x] = tot;
+  int m = max(a, b);
+  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(max_count, m);
+}
+__global__ void __launch_bounds__(SCAN_T) k_scan_apply(const int* __restrict__ counts, int nb,
+                                                       const int* __restrict__ off, int ntile, int* __restrict__ start,
+                                                       int* __restrict__ cursor) {
+  __shared__ int ws[32];
+  const int i = blockIdx.x * SCAN_TILE + 2 * threadIdx.x;
+  const int a = i < nb ? counts[i] : 0, b = i + 1 < nb ? counts[i + 1] : 0;
+  int tot;
+  const int e = off[blockIdx.x] + block_excl_scan(a + b, ws, &tot);
+  if (i < nb) start[i] = cursor[i] = e;
+  if (i + 1 < nb) start[i + 1] = cursor[i + 1] = e + a;
+  if (blockIdx.x == 0 && threadIdx.x == 0) start[nb] = off[ntile];
+}
+
 __global__ void k_scatter(const int* __restrict__ keys, int n, int* __restrict__ cursor,
                           int* __restrict__ tmp) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
@@ -145,8 +200,21 @@ hs_status counting_sort(hs_ctx* ctx, const int* keys, int n, int nb, int* order,
     k_histogram<<<gs, 256, 0, st>>>(keys, n, counts);
     HS_LAUNCHED(ctx);
   }
-  k_scan<<<1, 1024, 0, st>>>(counts, nb, start, cursor, maxc);
-  HS_LAUNCHED(ctx);
+  if (nb <= 4 * SCAN_TILE) {
+    k_scan<<<1, 1024, 0, st>>>(counts, nb, start, cursor, maxc);
+    HS_LAUNCHED(ctx);
+  } else {
+    const int ntile = (int)ceil_div(nb, SCAN_TILE);
+    int* sums = work + 2 * nb + 4 + n;   // counting_sort_work_ints: + 2 ntile + 8
+    int* off = sums + ntile;              // ntile + 1
+    int* junk = off + ntile + 1;          // cursor of the tile-sum scan (ntile) and its max
+    k_scan_tiles<<<ntile, SCAN_T, 0, st>>>(counts, nb, sums, maxc);
+    HS_LAUNCHED(ctx);
+    k_scan<<<1, 1024, 0, st>>>(sums, ntile, off, junk, junk + ntile);
+    HS_LAUNCHED(ctx);
+    k_scan_apply<<<ntile, SCAN_T, 0, st>>>(counts, nb, off, ntile, start, cursor);
+    HS_LAUNCHED(ctx);
+  }
   if (n == 0) return HS_OK;
   k_scatter<<<gs, 256, 0, st>>>(keys, n, cursor, tmp);
   HS_LAUNCHED(ctx);
