@@ -467,12 +467,27 @@ __global__ void __launch_bounds__(SW_THREADS, 2) k_spread_mma4(const int4* __res
       int row[SW_H];
       double q[SW_H][NCH];
     };
+    // stride permutation of the candidate list (as in the pair kernel): candidates are in bin
+    // order, so consecutive chunks would come from ONE neighbour bin and hit only the warp
+    // patches on that side of the tile, leaving the other consumers idle while the ring fills;
+    // permuted, every chunk samples all bins and the per-chunk work is even across warps
+    int pstride = 1;
+    {
+      const int primes[4] = {1000003, 999983, 1000033, 1000037};
+      for (int k = 0; k < 4; ++k)
+        if (ncand % primes[k] != 0) {
+          pstride = primes[k] % max(ncand, 1);
+          if (pstride == 0) pstride = 1;
+          break;
+        }
+    }
     auto fetch = [&](int c, Pre& f) {
 #pragma unroll
       for (int h = 0; h < SW_H; ++h) {
-        const int v = c * SW_CH + lane + 32 * h;
+        const int v0 = c * SW_CH + lane + 32 * h;
         f.row[h] = -1;
-        if (c < nchunk && v < ncand) {
+        if (c < nchunk && v0 < ncand) {
+          const int v = (int)(((long long)v0 * pstride) % ncand);
           int r = 0, rhi = nrun - 1;  // last run with run_pre[r] <= v
           while (r < rhi) {
             const int mid = (r + rhi + 1) >> 1;
