@@ -407,9 +407,17 @@ struct SwBuf {
   static constexpr int DOUBLES = SW_CH * (SW_RX + SW_RY + SW_RZ + RQ + 1);
 };
 
-template <int NCH>
+// FLY (HS_SPREAD_FLY=1, comparison): the producers compute each source's window slices for the tile from its
+// position (two exps per axis, then the Gaussian ratio recurrence w_{a+1} = w_a r_a,
+// r_{a+1} = r_a exp(-2 alpha h^2); ~4e-15 relative after <= 18 steps) instead of copying them
+// from the per-source window table: every source's slices were re-read by the ~25 tiles its
+// support touches (11 GB of DRAM reads per channel group at HL), now only its 32-byte record
+// and weights are -- but the producers' dependent recurrence chains then bound the consumers
+// (24.4 vs 18.1 ms at HL), so !FLY (window tables + cp.async) is the default.
+template <int NCH, bool FLY>
 __global__ void __launch_bounds__(SW_THREADS, 2) k_spread_mma4(const int4* __restrict__ lo4, const double* __restrict__ tab,
-                                                       WTab wt, const double* __restrict__ w, int ldw,
+                                                       WTab wt, const double4* __restrict__ pts,
+                                                       const double* __restrict__ w, int ldw,
                                                        const int* __restrict__ bin_start, GridGeom g, int nbx,
                                                        int nby, int nbz, double* __restrict__ grids) {
   constexpr int RX = SW_RX, RY = SW_RY, RZ = SW_RZ, RQ = SwBuf<NCH>::RQ, PER = SwBuf<NCH>::DOUBLES;
@@ -466,6 +474,25 @@ __global__ void __launch_bounds__(SW_THREADS, 2) k_spread_mma4(const int4* __res
       int4 lo[SW_H];
       int row[SW_H];
       double q[SW_H][NCH];
+      double p[SW_H][3];
+    };
+    const double rq2 = exp(-2.0 * g.alpha * g.h * g.h);  // ratio of successive window ratios
+    // dst[j] = window value of node a = a0 + j (relative to the window start lo), 0 outside [0, P)
+    auto fill = [&](double* dst, int n, double pos, int k, int lo_local, int a0, double scale) {
+      const int as = max(a0, 0);
+      const double d = g_d(g, k, pos, lo_local + as);
+      double wv = scale * exp(-g.alpha * d * d);
+      double r = exp(g.alpha * g.h * (2.0 * d - g.h));
+      for (int j = 0; j < n; ++j) {
+        const int a = a0 + j;
+        double v = 0.0;
+        if (a >= as && a < P) {
+          v = wv;
+          wv *= r;
+          r *= rq2;
+        }
+        dst[j] = v;
+      }
     };
     // stride permutation of the candidate list (as in the pair kernel): candidates are in bin
     // order, so consecutive chunks would come from ONE neighbour bin and hit only the warp
@@ -496,7 +523,15 @@ __global__ void __launch_bounds__(SW_THREADS, 2) k_spread_mma4(const int4* __res
           }
           const int row = run_beg[r] + (v - run_pre[r]);
           f.row[h] = row;
-          f.lo[h] = lo4[row];
+          if (FLY) {
+            const double4 pp = pts[row];
+            f.p[h][0] = pp.x;
+            f.p[h][1] = pp.y;
+            f.p[h][2] = pp.z;
+            f.lo[h] = make_int4((int)g_lo(g, 0, pp.x), (int)g_lo(g, 1, pp.y), (int)g_lo(g, 2, pp.z), 0);
+          } else {
+            f.lo[h] = lo4[row];
+          }
 #pragma unroll
           for (int ch = 0; ch < NCH; ++ch) f.q[h][ch] = w[(int64_t)row * ldw + ch];
         }
@@ -540,6 +575,20 @@ __global__ void __launch_bounds__(SW_THREADS, 2) k_spread_mma4(const int4* __res
                                   : 0u);
       }
       mbar_arrive(&full_bar[b]);  // masks / weights (plain stores) released
+      if (FLY) {
+#pragma unroll
+        for (int h = 0; h < SW_H; ++h) {
+          if (m[h]) {
+            const int sl = lane + 32 * h;
+            const int4 l = cur.lo[h];
+            fill(bx_(b)[sl], RX, cur.p[h][0], 0, l.x, (ex[h] & ~1) - SP_TX, g.pref);
+            fill(by_(b)[sl], RY, cur.p[h][1], 1, l.y, (ey[h] & ~1) - SP_TY, 1.0);
+            fill(bz_(b)[sl], RZ, cur.p[h][2], 2, l.z, (ez[h] & ~1) - SP_TZ, 1.0);
+          }
+        }
+        mbar_arrive(&full_bar[b]);  // window slices (plain stores) released
+        continue;
+      }
       // window slices: 16-byte cp.async chunks, completion tracked by the same barrier
 #pragma unroll
       for (int h = 0; h < SW_H; ++h) {
@@ -920,14 +969,22 @@ hs_status launch_spread(hs_ctx* ctx, const double4* pts, const double* w, int n,
   // default: v3 (window tables + cp.async staging + DMMA); HS_SPREAD_V0 = DMMA with in-tile window
   // arithmetic, HS_SPREAD_V1 = scalar DFMA, HS_SPREAD_V2 = warp-independent (comparison only)
   static const int variant = getenv("HS_SPREAD_V0") ? 0 : getenv("HS_SPREAD_V1") ? 1 : getenv("HS_SPREAD_V2") ? 2 : 3;
+  // window tables + cp.async (default); HS_SPREAD_FLY=1: producers compute the slices (comparison:
+  // 24.4 vs 18.1 ms at HL -- the producers' recurrence chains then bound the consumers, while the
+  // table re-reads, 11 GB per channel group, run at ~1.2 TB/s off the critical path)
+  static const bool tables = getenv("HS_SPREAD_FLY") == nullptr;
   if (variant == 3) {
     const WTab wt = WTab::make(g.P);
     void* scr3 = nullptr;
     const size_t nn = (size_t)std::max(n, 1);
-    HS_TRY(ctx_scratch(ctx, nn * (sizeof(int4) + sizeof(double) * wt.stride), &scr3));
-    int4* lo = (int4*)scr3;
-    double* tab = (double*)(lo + nn);
-    if (n > 0) {
+    int4* lo = nullptr;
+    double* tab = nullptr;
+    if (tables) {
+      HS_TRY(ctx_scratch(ctx, nn * (sizeof(int4) + sizeof(double) * wt.stride), &scr3));
+      lo = (int4*)scr3;
+      tab = (double*)(lo + nn);
+    }
+    if (n > 0 && tables) {
       const int gs = (int)std::min<int64_t>(ceil_div((int64_t)n * 3 * 32, 256), ctx->sm_count * 16);
       k_spread_wtab<<<gs, 256, 0, ctx->stream>>>(pts, n, g, wt, lo, tab);
       HS_LAUNCHED(ctx);
@@ -941,9 +998,15 @@ hs_status launch_spread(hs_ctx* ctx, const double4* pts, const double* w, int n,
 #define HS_SP3(N)                                                                                                    \
   case N: {                                                                                                          \
     const size_t smm = sizeof(double) * SW_K * SwBuf<N>::DOUBLES;                                                    \
-    HS_CUDA(cudaFuncSetAttribute(k_spread_mma4<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smm));          \
-    k_spread_mma4<N><<<grid, SW_THREADS, smm, ctx->stream>>>(lo, tab, wt, wc0, nch, bin_start, g, nbx, nby, nbz, \
-                                                             gout);                                                \
+    if (tables) {                                                                                                    \
+      HS_CUDA(cudaFuncSetAttribute(k_spread_mma4<N, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smm)); \
+      k_spread_mma4<N, false><<<grid, SW_THREADS, smm, ctx->stream>>>(lo, tab, wt, pts, wc0, nch, bin_start, g, nbx, \
+                                                                      nby, nbz, gout);                               \
+    } else {                                                                                                         \
+      HS_CUDA(cudaFuncSetAttribute(k_spread_mma4<N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smm));  \
+      k_spread_mma4<N, true><<<grid, SW_THREADS, smm, ctx->stream>>>(lo, tab, wt, pts, wc0, nch, bin_start, g, nbx,  \
+                                                                     nby, nbz, gout);                                \
+    }                                                                                                                \
   } break;
         HS_SP3(1) HS_SP3(2) HS_SP3(3) HS_SP3(4)
 #undef HS_SP3
