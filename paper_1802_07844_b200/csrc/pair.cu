@@ -464,48 +464,40 @@ __global__ void __launch_bounds__(PC_TG, PC_MINB) k_pair_q(const PairArgs a) {
         }
         // FP32 distance inside r_c by a margin far above its rounding error: the exact
         // reference test would accept too; in the shell around r_c run the exact test
-        // (bit-identical neighbour sets).  The slot at `tail` is free (tail - head < PC_Q),
-        // so every tested candidate is written there and `tail` advances only on accept.
-        auto test_fp32 = [&](const float4& F, bool& sure, bool& shell) {
-          const float fx = tfx - F.x, fy = tfy - F.y, fz = tfz - F.z;
-          const float r2f = fx * fx + fy * fy + fz * fz;
-          sure = r2f > 0.0f && r2f <= a.rc2_lo;
-          shell = !sure && r2f <= a.rc2_hi;
+        // (bit-identical neighbour sets) -- warp-uniformly skipped when no lane is in the shell.
+        // The slot at `tail` is free (tail - head < PC_Q), so every tested candidate is written
+        // there and `tail` advances only on accept.  Two candidates per iteration.
+        const float4* sFg = sF + hb + j0;
+        auto exact_ok = [&](int j, const float4& F, bool& ok) {
+          const double2 xy = sXY[j];
+          const double sz = sZA[j].x;
+          const double d0 = __dsub_rn(T.x, xy.x), d1 = __dsub_rn(T.y, xy.y), d2 = __dsub_rn(T.z, sz);
+          const double r2 = exact_r2(d0, d1, d2);
+          singular |= __float_as_int(F.w) != tcol_i && tvalid && r2 == 0.0;
+          ok = r2 <= a.rc2 && r2 != 0.0;
         };
-        auto push = [&](int j, const float4& F, bool sure, bool shell) {
-          bool ok = sure;
-          if (shell) {
-            const double2 xy = sXY[j];
-            const double sz = sZA[j].x;
-            const double d0 = __dsub_rn(T.x, xy.x), d1 = __dsub_rn(T.y, xy.y), d2 = __dsub_rn(T.z, sz);
-            const double r2 = exact_r2(d0, d1, d2);
-            const bool own = __float_as_int(F.w) != tcol_i && tvalid;
-            singular |= own && r2 == 0.0;
-            ok = r2 <= a.rc2 && r2 != 0.0;
-          }
-          ok = ok && __float_as_int(F.w) != tcol_i && tvalid;
-          q[tail & (PC_Q - 1)][lane] = (unsigned short)j;
-          tail += ok ? 1 : 0;
-        };
-        // two candidates per iteration: independent broadcast loads and tests
         while (near) {
-          const int ja = hb + j0 + __ffs(near) - 1;
+          const int ia = __ffs(near) - 1;
           near &= near - 1;
-          if (near) {
-            const int jb = hb + j0 + __ffs(near) - 1;
-            near &= near - 1;
-            const float4 Fa = sF[ja], Fb = sF[jb];  // broadcast
-            bool sa, ha, sb, hb2;
-            test_fp32(Fa, sa, ha);
-            test_fp32(Fb, sb, hb2);
-            push(ja, Fa, sa, ha);
-            push(jb, Fb, sb, hb2);
-          } else {
-            const float4 Fa = sF[ja];
-            bool sa, ha;
-            test_fp32(Fa, sa, ha);
-            push(ja, Fa, sa, ha);
+          const bool two = near != 0;
+          const int ib = two ? __ffs(near) - 1 : ia;
+          near &= near - 1;
+          const float4 Fa = sFg[ia], Fb = sFg[ib];  // broadcast
+          const float ax = tfx - Fa.x, ay = tfy - Fa.y, az = tfz - Fa.z;
+          const float bx = tfx - Fb.x, by = tfy - Fb.y, bz = tfz - Fb.z;
+          const float ra = ax * ax + ay * ay + az * az, rb = bx * bx + by * by + bz * bz;
+          bool oka = ra > 0.0f && ra <= a.rc2_lo, okb = two && rb > 0.0f && rb <= a.rc2_lo;
+          const bool sha = !oka && ra <= a.rc2_hi, shb = two && !okb && rb <= a.rc2_hi;
+          if (__any_sync(0xffffffffu, sha || shb)) {
+            if (sha) exact_ok(hb + j0 + ia, Fa, oka);
+            if (shb) exact_ok(hb + j0 + ib, Fb, okb);
           }
+          oka = oka && __float_as_int(Fa.w) != tcol_i && tvalid;
+          okb = okb && __float_as_int(Fb.w) != tcol_i && tvalid;
+          q[tail & (PC_Q - 1)][lane] = (unsigned short)(hb + j0 + ia);
+          tail += oka ? 1 : 0;
+          q[tail & (PC_Q - 1)][lane] = (unsigned short)(hb + j0 + ib);
+          tail += okb ? 1 : 0;
         }
         // full rounds while every valid lane has work; partial rounds only against overflow
         unsigned mn = __reduce_min_sync(0xffffffffu, (unsigned)(tvalid ? tail - head : 0x7fffffff));
