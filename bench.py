@@ -275,6 +275,13 @@ def run_ours(args, rank, world, local_rank):
     ms = e0.elapsed_time(e1)
     launches = ctx.launches() - l0
     clk = clocks.stop()
+    # per-kernel times for the roofline: the same evaluations with the real-space and Fourier
+    # pipelines serialised (what bit 2), since in the timed steps they overlap on two streams
+    # and a kernel's event interval would include the other pipeline's work
+    step_times = []
+    for _ in range(args.steps):
+        _, _, _, tm = ev.execute(pos, f, out=out, what=7)
+        step_times.append(tm)
     if world > 1:
         tt = torch.tensor([ms], device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -336,6 +343,8 @@ def run_ours(args, rank, world, local_rank):
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded PCG64, BASELINE.json shapes)",
             "config": {"workload": w.name, "kind": w.kind, "n": s.n, "xi": w.xi, "rc": w.rc, "M": w.M, "P": w.P,
                        "padded_dims": list(grid.padded_dims), "parallelism": f"replicas{world}",
+                       "streams": "real space concurrent with the Fourier pipeline up to the gather; "
+                                  "kernels/phases_ms/roofline from the same steps run serialised",
                        "l2": "not flushed: each step streams >30 GB of grids/spectra through HBM (126 MB L2)"},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(hp.numel() * 8 + hf.numel() * 8),
                     "d2h_bytes_per_step": int(hu.numel() * 8), "ms_per_step": ms_e2e / args.steps,

@@ -126,7 +126,10 @@ hs_status hs_plan_build_tables(hs_plan* plan, const int64_t big[3], double R, co
  *   times (optional, 16 doubles, milliseconds, CUDA events):
  *     [gridding, fft, scale, ifft, gather, real, fourier, h2d, total, io,
  *      k_pair, k_spread, k_gather, k_scale (kernel-only), accepted pairs, accepted image pairs]
- *   what: bit 0 = real part, bit 1 = Fourier part (3 = full sum). */
+ *   what: bit 0 = real part, bit 1 = Fourier part (3 = full sum); bit 2 = run the two parts
+ *   one after the other on the context stream (by default the real-space part runs on a second,
+ *   high-priority stream concurrently with the Fourier part up to the gather; serialised runs
+ *   give undisturbed per-kernel times). */
 hs_status hs_plan_execute(hs_plan* plan, const double* positions, const double* sa, const double* sb,
                           const double* targets, const int64_t* tcols, double* u, double* u_real,
                           double* u_fourier, int mem, int what, double* times);

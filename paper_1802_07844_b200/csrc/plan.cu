@@ -317,6 +317,13 @@ struct hs_plan {
   int cur_tcol_identity = 0;
   bool pair_timed = false, spread_timed = false, gather_timed = false;
   bool mirror = false;          // half space: spread the N sources once and mirror (k_mirror_z)
+  // concurrent real-space / Fourier pipelines (hs_plan_execute): the Fourier side runs on its
+  // own high-priority stream with its own sort buffers, joined before the gather
+  cudaStream_t st_four = nullptr;
+  cudaEvent_t ev_in = nullptr, ev_four = nullptr;
+  int *keys_f = nullptr, *work_f = nullptr;
+  int* sort_keys = nullptr;     // buffers the spread / gather sorts use (keys or keys_f)
+  int* sort_work = nullptr;
 };
 
 namespace {
@@ -460,6 +467,10 @@ static hs_status plan_create_impl(hs_ctx* ctx, const hs_params* prm, const hs_sl
   A_(maxn, p->keys);
   A_(maxn, p->order);
   A_(counting_sort_work_ints(maxn, maxb), p->work);
+  A_(maxn, p->keys_f);
+  A_(counting_sort_work_ints(maxn, maxb), p->work_f);
+  p->sort_keys = p->keys;
+  p->sort_work = p->work;
   A_(ncell + 1, p->start);
   A_(nt + 1, p->t_order);
   A_((size_t)ncell * kTargetSub + 1, p->t_start);
@@ -540,6 +551,13 @@ static hs_status plan_create_impl(hs_ctx* ctx, const hs_params* prm, const hs_sl
     cufftSetWorkArea(p->zi, wsp);
   }
   for (auto& e : p->ev) HS_CUDA(cudaEventCreate(&e));
+  {
+    int lo_prio = 0, hi_prio = 0;
+    HS_CUDA(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
+    HS_CUDA(cudaStreamCreateWithPriority(&p->st_four, cudaStreamNonBlocking, hi_prio));
+    HS_CUDA(cudaEventCreateWithFlags(&p->ev_in, cudaEventDisableTiming));
+    HS_CUDA(cudaEventCreateWithFlags(&p->ev_four, cudaEventDisableTiming));
+  }
   *out = p;
   return HS_OK;
 }
@@ -560,6 +578,9 @@ extern "C" hs_status hs_plan_destroy(hs_plan* p) {
   if (p->zi) cufftDestroy(p->zi);
   for (auto& e : p->ev)
     if (e) cudaEventDestroy(e);
+  if (p->ev_in) cudaEventDestroy(p->ev_in);
+  if (p->ev_four) cudaEventDestroy(p->ev_four);
+  if (p->st_four) cudaStreamDestroy(p->st_four);
   for (auto& b : p->bufs) cudaFree(b.p);
   delete p;
   return HS_OK;
@@ -895,13 +916,13 @@ hs_status sort_points_by_cell(hs_plan* p, const double* pos, int n_src, int n_to
 hs_status sort_points_by_bin(hs_plan* p, const double* pos, int n_src, int n_total, int mode, int* order,
                              int* start) {
   hs_ctx* ctx = p->ctx;
-  HS_TRY(launch_grid_keys(ctx, pos, n_src, n_total, mode, p->gg, p->keys));
+  HS_TRY(launch_grid_keys(ctx, pos, n_src, n_total, mode, p->gg, p->sort_keys));
   // slab plans: spread keys of sources owned by another rank are the extra bin nbins (not
   // ranked, never read)
   if (!(mode & 8) && p->slab.world > 0)
-    return counting_sort(ctx, p->keys, n_total, p->nbins + 1, order, start, p->work, p->nbins);
+    return counting_sort(ctx, p->sort_keys, n_total, p->nbins + 1, order, start, p->sort_work, p->nbins);
   const int nb = (mode & 8) ? gather_keys(p->gg) : p->nbins;
-  return counting_sort(ctx, p->keys, n_total, nb, order, start, p->work);
+  return counting_sort(ctx, p->sort_keys, n_total, nb, order, start, p->sort_work);
 }
 
 }  // namespace
@@ -1186,7 +1207,7 @@ hs_status stage_outputs(hs_plan* p, double* u, double* u_real, double* u_fourier
   return HS_OK;
 }
 
-void fill_times(hs_plan* p, double* times) {
+void fill_times(hs_plan* p, double* times, bool overlapped = false) {
   cudaEvent_t* ev = p->ev;
   float ms[9] = {0};
   for (int k = 0; k < 8; ++k) cudaEventElapsedTime(&ms[k], ev[k], ev[k + 1]);
@@ -1194,6 +1215,20 @@ void fill_times(hs_plan* p, double* times) {
   cudaEventElapsedTime(&tot, ev[0], ev[8]);
   float fourier = 0;
   cudaEventElapsedTime(&fourier, ev[2], ev[7]);
+  if (overlapped) {
+    // both pipelines start at ev[1]: real = ev1 -> ev2 (context stream), gridding = ev1 -> ev3
+    // (Fourier stream), gather = join -> ev7; the phases overlap, so they no longer sum to total
+    cudaEventElapsedTime(&ms[2], ev[1], ev[3]);
+    float g0 = 0;
+    cudaEventElapsedTime(&g0, ev[6], ev[7]);
+    float r = 0;
+    cudaEventElapsedTime(&r, ev[1], ev[2]);
+    ms[1] = r;
+    float lastjoin = 0;  // gather proper: from the later of (real end, Fourier end)
+    cudaEventElapsedTime(&lastjoin, ev[2], ev[7]);
+    ms[6] = std::min(g0, lastjoin);
+    cudaEventElapsedTime(&fourier, ev[1], ev[7]);
+  }
   // [gridding, fft, scale, ifft, gather, real, fourier, prep, total, io]
   times[0] = ms[2];
   times[1] = ms[3];
@@ -1244,21 +1279,27 @@ extern "C" hs_status hs_plan_execute(hs_plan* p, const double* positions, const 
   HS_CUDA(cudaEventRecord(ev[0], st));
   HS_TRY(stage_inputs(p, positions, sa, sb, targets, tcols, mem));
   HS_CUDA(cudaEventRecord(ev[1], st));
-  HS_TRY(stage_real(p, (what & 1) != 0));
-  HS_CUDA(cudaEventRecord(ev[2], st));
-  if (what & 2) {
+  // The real-space pipeline (FP64 pair kernel) and the Fourier pipeline up to the gather are
+  // independent: with both requested, the Fourier side is issued on the plan's high-priority
+  // stream (its own sort buffers; the context stream is switched while its launches are
+  // issued) and runs concurrently with the pair kernel, filling the SM slots and pipes the
+  // pair kernel leaves idle; the gather, which adds u_real, waits for both.
+  // HS_NO_OVERLAP=1: one stream (comparison).
+  static const bool overlap_env = getenv("HS_NO_OVERLAP") == nullptr;
+  const bool two = overlap_env && (what & 3) == 3 && !(what & 4);  // what bit 2: serialise (kernel timing)
+  auto fourier_to_gather = [&]() -> hs_status {
     HS_TRY(stage_spread(p));
-    HS_CUDA(cudaEventRecord(ev[3], st));
+    HS_CUDA(cudaEventRecord(ev[3], ctx->stream));
     set_fft_streams(p);
-    // forward z (D2Z) and y (Z2Z) stages, one source channel at a time through the shared A buffer
+    // forward z (D2Z) and y stages, one source channel at a time through the shared A buffer
     for (int c = 0; c < p->n_in; ++c) {
       if (cufftExecD2Z(p->zf, p->grid_in + (size_t)c * p->n_grid, (cufftDoubleComplex*)p->Amix) != CUFFT_SUCCESS)
         return fail(HS_ERR_CUDA, "cuFFT z D2Z failed");
       HS_TRY(stage_yfwd(p, p->Amix, c));
     }
-    HS_CUDA(cudaEventRecord(ev[4], st));
+    HS_CUDA(cudaEventRecord(ev[4], ctx->stream));
     HS_TRY(stage_xstage(p));
-    HS_CUDA(cudaEventRecord(ev[5], st));
+    HS_CUDA(cudaEventRecord(ev[5], ctx->stream));
     for (int o = 0; o < p->n_out; ++o) {
       double2* so = p->spec + (size_t)o * p->n_mixed;
       HS_TRY(stage_yinv(p, o, so));
@@ -1266,10 +1307,49 @@ extern "C" hs_status hs_plan_execute(hs_plan* p, const double* positions, const 
         return fail(HS_ERR_CUDA, "cuFFT z Z2D failed");
     }
     // channel-interleave the (y < ny, x < nx, z < nz) outputs for the broadcast gather
-    k_interleave<<<grid_size(ctx, p->n_grid / 2), 256, 0, st>>>(p->grid_tmp, p->n_out, p->n_grid, p->n_grid,
-                                                                p->out_pitch, p->grid_out);
+    k_interleave<<<grid_size(ctx, p->n_grid / 2), 256, 0, ctx->stream>>>(p->grid_tmp, p->n_out, p->n_grid,
+                                                                         p->n_grid, p->out_pitch, p->grid_out);
     HS_LAUNCHED(ctx);
-    HS_CUDA(cudaEventRecord(ev[6], st));
+    HS_CUDA(cudaEventRecord(ev[6], ctx->stream));
+    return HS_OK;
+  };
+  // HS_OVERLAP_FOURIER_HI=1: the Fourier side on the high-priority stream (default: the
+  // real-space side there, so the pair kernel keeps its slots and the Fourier kernels fill in)
+  static const bool fourier_hi = getenv("HS_OVERLAP_FOURIER_HI") != nullptr;
+  hs_status fst = HS_OK;
+  if (two) {
+    HS_CUDA(cudaStreamWaitEvent(p->st_four, ev[1], 0));
+    ctx->stream = p->st_four;
+    if (fourier_hi) {
+      p->sort_keys = p->keys_f;
+      p->sort_work = p->work_f;
+      fst = fourier_to_gather();
+    } else {
+      fst = stage_real(p, (what & 1) != 0);
+      if (fst == HS_OK && cudaEventRecord(ev[2], p->st_four) != cudaSuccess) fst = fail(HS_ERR_CUDA, "event");
+    }
+    if (fst == HS_OK && cudaEventRecord(p->ev_four, p->st_four) != cudaSuccess) fst = fail(HS_ERR_CUDA, "event");
+    ctx->stream = st;
+    p->sort_keys = p->keys;
+    p->sort_work = p->work;
+    set_fft_streams(p);
+    HS_TRY(fst);
+    if (!fourier_hi) {
+      p->sort_keys = p->keys_f;
+      p->sort_work = p->work_f;
+      fst = fourier_to_gather();
+      p->sort_keys = p->keys;
+      p->sort_work = p->work;
+      HS_TRY(fst);
+    }
+  }
+  if (!two || fourier_hi) {
+    HS_TRY(stage_real(p, (what & 1) != 0));
+    HS_CUDA(cudaEventRecord(ev[2], st));
+  }
+  if (what & 2) {
+    if (two) HS_CUDA(cudaStreamWaitEvent(st, p->ev_four, 0));
+    else HS_TRY(fourier_to_gather());
     HS_TRY(stage_gather(p));
   } else {
     for (int k = 3; k <= 6; ++k) HS_CUDA(cudaEventRecord(ev[k], st));
@@ -1283,7 +1363,7 @@ extern "C" hs_status hs_plan_execute(hs_plan* p, const double* positions, const 
   HS_CUDA(cudaEventRecord(ev[8], st));
   HS_CUDA(cudaStreamSynchronize(st));
   HS_TRY(ctx_check_flags(ctx, "hs_plan_execute"));
-  if (times) fill_times(p, times);
+  if (times) fill_times(p, times, two);
   return HS_OK;
 }
 

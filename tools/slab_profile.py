@@ -56,8 +56,11 @@ def profile(wname, world, reps=3):
         for st in states:
             cur["backward"][st.rank] = timed(st, "backward", lambda: st.backward())
         got = xch.shift(states, "halo_out", "halo_in", -1)
+        phases = {}
         for st in states:
-            cur["finish"][st.rank] = timed(st, "finish", lambda: st.finish(st.rank in got))
+            res = {}
+            cur["finish"][st.rank] = timed(st, "finish", lambda: res.update(st.finish(st.rank in got)))
+            phases[st.rank] = res
         if it:
             for k in stages:
                 ms[k] += cur[k] / reps
@@ -70,7 +73,9 @@ def profile(wname, world, reps=3):
            "critical_path_ms": round(float(sum(ms[k].max() for k in stages)), 3),
            "alltoall_bytes_per_rank": int(a2a_bytes * (world - 1) / world),
            "ghost_halo_bytes_per_rank": int(8 * (st0.ghost_out.numel() + st0.halo_out.numel())),
-           "plan_bytes_rank0": st0.ev.device_bytes}
+           "plan_bytes_rank0": st0.ev.device_bytes,
+           "rank0_phases_ms": {k: round(v, 3) for k, v in phases[0].items()
+                               if k in ("real", "gridding", "k_pair", "k_spread", "k_gather", "total")}}
     del states
     torch.cuda.empty_cache()
     return out
