@@ -201,3 +201,32 @@ def test_slab_local_headline_grid_world8(gpu):
     ref = gpu.ewald_sum(s, p)
     r = ewald_sum_slab_local(s, p, 8)
     assert rel_l2(r.velocities, ref.velocities) < 1e-12
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind", KINDS)
+def test_slab_local_free_space(gpu, kind):
+    """Free-space geometry (no images, no wall channels, the non-mirrored spread) through a
+    3-way slab decomposition == the single plan."""
+    from paper_1802_07844_b200.sharding import ewald_sum_slab_local
+    s = gpu.generate_system(6000, 1.0, kind, "free", seed=21)
+    p = gpu.EwaldParams(xi=18.0, rc=0.2, M=72, P=24)
+    ref = gpu.ewald_sum(s, p)
+    r = ewald_sum_slab_local(s, p, 3)
+    assert rel_l2(r.velocities, ref.velocities) < 1e-12
+
+
+@pytest.mark.gpu
+def test_slab_local_wall_clustered_rotlet(gpu):
+    """cfg4's wall-clustered rotlet (sources within a few grid cells of the wall, so the
+    mirrored spread's source and image windows overlap) through a 2-way slab decomposition:
+    == the single plan, and close to the direct half-space sum."""
+    from paper_1802_07844_b200.configs import make_system
+    from paper_1802_07844_b200.sharding import ewald_sum_slab_local
+    s, _ = make_system("cfg4", n=8000)
+    p = gpu.EwaldParams(xi=20.8, rc=0.17, M=96, P=24)
+    ref = gpu.ewald_sum(s, p)
+    r = ewald_sum_slab_local(s, p, 2)
+    assert rel_l2(r.velocities, ref.velocities) < 1e-12
+    d = gpu.direct_sum_half(s, targets=s.positions[:300], target_indices=np.arange(300)).velocities
+    assert rel_l2(r.velocities[:300], d) < 1e-5

@@ -12,6 +12,6 @@ echo "ref rc=$?" >> $out/status
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $out/launches.csv \
     python bench.py --steps 1 --warmup 3 --no-cpu-baseline > $out/ncu_launch.log 2>&1
 echo "launch rc=$?" >> $out/status
-ncu --set full --clock-control none --import-source on -k regex:"k_pair_q|k_spread_mma|k_gather7|k_xreg|k_ystage|k_mirror_z|k_interleave" -c 10 \
+ncu --set full --clock-control none --import-source on -k regex:"k_pair_q|k_spread_mma|k_mirror_z" -c 4 \
     -o $out/full python tools/profile_step.py --iters 1 > $out/ncu_full.log 2>&1
 echo "full rc=$?" >> $out/status
