@@ -524,7 +524,11 @@ __device__ __forceinline__ void warp_fft_reg(double2* v, double2* S, const doubl
   }
 }
 
-template <int KIND, bool HALF, int M>
+// STAGE: the next column's nx input values of every channel are prefetched with cp.async into a
+// shared-memory staging area while the current column is scaled and inverse-transformed, so the
+// forward FFTs read shared memory instead of waiting on strided global loads (used when the
+// extra NIN * nx * 16 bytes keep the kernel's CTAs per SM).
+template <int KIND, bool HALF, int M, bool STAGE>
 __global__ void __launch_bounds__(XF_THREADS, M == 27 ? 1 : 2) k_xreg(const XArgs a) {
   constexpr int N = 32 * M, LSR = M * 33;
   constexpr int NIN = KChan<KIND, HALF>::NIN, NOUT = KChan<KIND, HALF>::NOUT;
@@ -532,22 +536,39 @@ __global__ void __launch_bounds__(XF_THREADS, M == 27 ? 1 : 2) k_xreg(const XArg
   extern __shared__ double2 smem[];
   double2* lines = smem;            // [NL][LSR]: transpose scratch of the line's warp, then the channel line
   double2* tw = smem + NL * LSR;    // pd8-padded twiddles
+  double2* stage = tw + padded_line(N);  // [NIN][nx] (STAGE)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int i = tid; i < N; i += blockDim.x) tw[pd8(i)] = a.tw[i];
   const int n_items = a.py * a.nzh;
   const int p[3] = {a.px, a.py, a.pz};
   const int r = lane >> 1, h = lane & 1;
+  auto prefetch = [&](int it) {
+    if (it < n_items) {
+      const int ky2 = it / a.nzh, kz2 = it - ky2 * a.nzh;
+      const int tot = NIN * a.nx;
+      for (int i = tid; i < tot; i += blockDim.x) {
+        const int c = i / a.nx, x = i - c * a.nx;
+        cp_async16(&stage[i], a.B + c * a.ch_stride + ((int64_t)ky2 * a.nx + x) * a.nzh + kz2);
+      }
+    }
+    cp_async_commit();
+  };
+  if (STAGE) prefetch(blockIdx.x);
   for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
     const int ky = item / a.nzh;
     const int kzl = item - ky * a.nzh, kz = a.kz0 + kzl;  // local column, global wavenumber index
-    __syncthreads();  // previous item's lines consumed (and twiddles visible)
+    if (STAGE) cp_async_wait_all();
+    __syncthreads();  // previous item's lines consumed (and twiddles / staged inputs visible)
     for (int c = warp; c < NIN; c += NW) {
       double2 v[M], out[RegFFT<M>::NG][16];
       const double2* src = a.B + c * a.ch_stride + (int64_t)ky * a.nx * a.nzh + kzl;
 #pragma unroll
       for (int j = 0; j < M; ++j) {
         const int x = lane + 32 * j;
-        v[j] = x < a.nx ? src[(int64_t)x * a.nzh] : make_double2(0.0, 0.0);
+        if (STAGE)
+          v[j] = x < a.nx ? stage[c * a.nx + x] : make_double2(0.0, 0.0);
+        else
+          v[j] = x < a.nx ? src[(int64_t)x * a.nzh] : make_double2(0.0, 0.0);
       }
       double2* S = lines + c * LSR;
       warp_fft_reg<M>(v, S, tw, lane, out);
@@ -562,6 +583,7 @@ __global__ void __launch_bounds__(XF_THREADS, M == 27 ? 1 : 2) k_xreg(const XArg
       }
     }
     __syncthreads();
+    if (STAGE) prefetch(item + gridDim.x);  // staging area free: the forward FFTs have read it
     // k-space scaling at every kx of the column (channel c of kx at lines[c * LSR + kx])
     for (int kx = tid; kx < N; kx += blockDim.x) {
       const int64_t ti = ((int64_t)ky * a.nzh + kzl) * N + kx;
@@ -616,8 +638,14 @@ template <int KIND, bool HALF, int M>
 static hs_status launch_xreg_t(hs_ctx* ctx, const XArgs& a) {
   HS_TRY(xreg_constants());
   constexpr int NL = KChan<KIND, HALF>::NIN > KChan<KIND, HALF>::NOUT ? KChan<KIND, HALF>::NIN : KChan<KIND, HALF>::NOUT;
-  const size_t smem = sizeof(double2) * ((size_t)NL * M * 33 + padded_line(32 * M));
-  auto kern = k_xreg<KIND, HALF, M>;
+  const size_t smem0 = sizeof(double2) * ((size_t)NL * M * 33 + padded_line(32 * M));
+  const size_t smem1 = smem0 + sizeof(double2) * (size_t)KChan<KIND, HALF>::NIN * a.nx;
+  // staging only if the kernel keeps its CTAs per SM (2, or 1 for M = 27) and HS_XSTAGE_NOSTAGE unset
+  static const bool nostage = getenv("HS_XSTAGE_NOSTAGE") != nullptr;
+  const size_t budget = (M == 27 ? 227 : 113) * 1024;
+  const bool use_stage = !nostage && smem1 <= budget;
+  const size_t smem = use_stage ? smem1 : smem0;
+  auto kern = use_stage ? k_xreg<KIND, HALF, M, true> : k_xreg<KIND, HALF, M, false>;
   HS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0;
   HS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, XF_THREADS, smem));
