@@ -225,7 +225,7 @@ def run_reference(args, rank):
                              "phases_s": {k: round(v, 4) for k, v in parts.items()},
                              "sample_wall_s": round(float(np.mean(walls)), 2)},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 def run_ours(args, rank, world, local_rank):
@@ -362,7 +362,7 @@ def run_ours(args, rank, world, local_rank):
                                 "phases_s": {k: round(v, 4) for k, v in parts.items()},
                                 "sample_wall_s": round(wall, 2)}
     if rank == 0:
-        print(json.dumps(line), flush=True)
+        emit(line)
     if world > 1:
         dist.destroy_process_group()
 
@@ -444,11 +444,26 @@ def run_slab(args, rank, world, local_rank):
             "targets_per_rank": [len(r) for r in rows], "precompute_tables_s": round(t_tables, 3),
             "plan_device_bytes_rank0": st.ev.device_bytes, "clocks": clk}
     if rank == 0:
-        print(json.dumps(line), flush=True)
+        emit(line)
     dist.destroy_process_group()
 
 
+_OUT = None
+
+
+def emit(line):
+    """The one JSON line on the real stdout (fd 1 is redirected to stderr in main(), so NCCL's
+    or any library's own stdout chatter cannot interleave with it)."""
+    out = _OUT if _OUT is not None else sys.stdout
+    out.write(json.dumps(line) + "\n")
+    out.flush()
+
+
 def main():
+    global _OUT
+    sys.stdout.flush()
+    _OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
     ap = argparse.ArgumentParser(description=__doc__)
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)

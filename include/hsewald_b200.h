@@ -193,6 +193,16 @@ hs_status hs_slab_kspace(hs_plan* plan, const double* recv, double* back);
 hs_status hs_slab_backward(hs_plan* plan, const double* recv_back, double* halo_out);
 hs_status hs_slab_finish(hs_plan* plan, const double* halo_in, double* u, double* u_real, double* u_fourier,
                          int mem, double* times);
+/* Channel-range forms of the middle stages, so the all-to-all of channel c can run (on the
+ * collective's own stream) while channel c+1 is transformed:
+ *   hs_slab_forward_range: as hs_slab_forward for input channels [c0, c1) (ghost add with c0 == 0);
+ *   hs_slab_kspace_part:   part 0 = y transforms of input channels [c0, c1) from recv,
+ *                          part 1 = the x stage, part 2 = inverse y of output channels [c0, c1);
+ *   hs_slab_backward_range: inverse z of output channels [c0, c1); the call with c1 == n_out
+ *                          also interleaves and writes halo_out. */
+hs_status hs_slab_forward_range(hs_plan* plan, const double* ghost_in, double* send, int c0, int c1);
+hs_status hs_slab_kspace_part(hs_plan* plan, int part, const double* recv, double* back, int c0, int c1);
+hs_status hs_slab_backward_range(hs_plan* plan, const double* recv_back, double* halo_out, int c0, int c1);
 
 /* ---- direct O(N Nt) half-space/free-space sum on the GPU (kernels_direct.py:211-371).
  * Same argument meaning as hs_plan_execute's strengths; returns physically

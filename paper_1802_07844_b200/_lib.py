@@ -79,6 +79,9 @@ _SIGS = [
     ("hs_slab_kspace", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     ("hs_slab_backward", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     ("hs_slab_finish", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, _dp]),
+    ("hs_slab_forward_range", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int]),
+    ("hs_slab_kspace_part", C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_int, C.c_int]),
+    ("hs_slab_backward_range", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int]),
     ("hs_direct_sum", C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p,
                                 C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int]),
 ]

@@ -1463,13 +1463,16 @@ extern "C" hs_status hs_slab_begin(hs_plan* p, const double* positions, const do
   return HS_OK;
 }
 
-extern "C" hs_status hs_slab_forward(hs_plan* p, const double* ghost_in, double* send) {
+// Channel-range forms of the middle stages, so a caller can overlap the all-to-all of channel
+// c with the transforms of channel c+1 (sharding.py issues the collectives asynchronously).
+extern "C" hs_status hs_slab_forward_range(hs_plan* p, const double* ghost_in, double* send, int c0, int c1) {
   HS_TRY(check_slab(p));
   if (!send) return fail(HS_ERR_PARAMETER, "null send buffer");
+  if (c0 < 0 || c1 > p->n_in || c0 > c1) return fail(HS_ERR_PARAMETER, "channel range");
   hs_ctx* ctx = p->ctx;
   cudaStream_t st = ctx->stream;
   const int64_t nx = p->gg.dims[0], nz = p->prm.dims[2], pz = p->kg.p[2], P1 = p->prm.P - 1;
-  if (ghost_in && P1 > 0) {
+  if (c0 == 0 && ghost_in && P1 > 0) {
     k_ghost_add<<<grid_size(ctx, p->n_in * P1 * nx * nz), 256, 0, st>>>(p->grid_in, ghost_in, p->n_in, (int)P1,
                                                                         (int)nx, (int)nz, (int)pz, p->gg.ch_stride);
     HS_LAUNCHED(ctx);
@@ -1477,7 +1480,7 @@ extern "C" hs_status hs_slab_forward(hs_plan* p, const double* ghost_in, double*
   set_fft_streams(p);
   const KzSplit ks = kz_split_of(p);
   const int64_t rows = (int64_t)p->yo * nx;
-  for (int c = 0; c < p->n_in; ++c) {
+  for (int c = c0; c < c1; ++c) {
     if (cufftExecD2Z(p->zf, p->grid_in + (size_t)c * p->n_grid, (cufftDoubleComplex*)p->Amix) != CUFFT_SUCCESS)
       return fail(HS_ERR_CUDA, "cuFFT z D2Z failed");
     k_kz_exchange<<<grid_size(ctx, rows * p->kg.nzh), 256, 0, st>>>(
@@ -1487,38 +1490,64 @@ extern "C" hs_status hs_slab_forward(hs_plan* p, const double* ghost_in, double*
   return HS_OK;
 }
 
-extern "C" hs_status hs_slab_kspace(hs_plan* p, const double* recv, double* back) {
+extern "C" hs_status hs_slab_forward(hs_plan* p, const double* ghost_in, double* send) {
   HS_TRY(check_slab(p));
-  if (!recv || !back) return fail(HS_ERR_PARAMETER, "null exchange buffer");
+  return hs_slab_forward_range(p, ghost_in, send, 0, p->n_in);
+}
+
+// part 0: y transforms of input channels [c0, c1) from recv; part 1: the x stage (c0, c1
+// ignored); part 2: inverse y transforms of output channels [c0, c1) into back
+extern "C" hs_status hs_slab_kspace_part(hs_plan* p, int part, const double* recv, double* back, int c0, int c1) {
+  HS_TRY(check_slab(p));
   hs_ctx* ctx = p->ctx;
   cudaStream_t st = ctx->stream;
   set_fft_streams(p);
-  // phase events: fft = z + exchange + y, scale = x stage, ifft = y^-1 + exchange + z^-1
-  for (int c = 0; c < p->n_in; ++c) HS_TRY(stage_yfwd(p, (double2*)recv + (size_t)c * p->n_mixed, c));
-  HS_CUDA(cudaEventRecord(p->ev[4], st));
-  HS_TRY(stage_xstage(p));
-  HS_CUDA(cudaEventRecord(p->ev[5], st));
+  if (part == 0) {
+    if (!recv || c0 < 0 || c1 > p->n_in || c0 > c1) return fail(HS_ERR_PARAMETER, "kspace part 0 arguments");
+    for (int c = c0; c < c1; ++c) HS_TRY(stage_yfwd(p, (double2*)recv + (size_t)c * p->n_mixed, c));
+    if (c1 == p->n_in) HS_CUDA(cudaEventRecord(p->ev[4], st));
+    return HS_OK;
+  }
+  if (part == 1) {
+    HS_TRY(stage_xstage(p));
+    HS_CUDA(cudaEventRecord(p->ev[5], st));
+    return HS_OK;
+  }
+  if (part != 2 || !back || c0 < 0 || c1 > p->n_out || c0 > c1) return fail(HS_ERR_PARAMETER, "kspace part arguments");
   const size_t back_ch = (size_t)p->prm.dims[1] * p->gg.dims[0] * p->nzs;
-  for (int o = 0; o < p->n_out; ++o) HS_TRY(stage_yinv(p, o, (double2*)back + o * back_ch));
+  for (int o = c0; o < c1; ++o) HS_TRY(stage_yinv(p, o, (double2*)back + o * back_ch));
   return HS_OK;
 }
 
-extern "C" hs_status hs_slab_backward(hs_plan* p, const double* recv_back, double* halo_out) {
+extern "C" hs_status hs_slab_kspace(hs_plan* p, const double* recv, double* back) {
   HS_TRY(check_slab(p));
-  if (!recv_back || !halo_out) return fail(HS_ERR_PARAMETER, "null exchange buffer");
+  if (!recv || !back) return fail(HS_ERR_PARAMETER, "null exchange buffer");
+  // phase events: fft = z + exchange + y, scale = x stage, ifft = y^-1 + exchange + z^-1
+  HS_TRY(hs_slab_kspace_part(p, 0, recv, back, 0, p->n_in));
+  HS_TRY(hs_slab_kspace_part(p, 1, recv, back, 0, 0));
+  return hs_slab_kspace_part(p, 2, recv, back, 0, p->n_out);
+}
+
+// inverse z transforms of output channels [o0, o1); the call with o1 == n_out also interleaves
+// the owned planes and writes the halo for rank r-1
+extern "C" hs_status hs_slab_backward_range(hs_plan* p, const double* recv_back, double* halo_out, int o0, int o1) {
+  HS_TRY(check_slab(p));
+  if (!recv_back || (o1 == p->n_out && !halo_out)) return fail(HS_ERR_PARAMETER, "null exchange buffer");
+  if (o0 < 0 || o1 > p->n_out || o0 > o1) return fail(HS_ERR_PARAMETER, "channel range");
   hs_ctx* ctx = p->ctx;
   cudaStream_t st = ctx->stream;
   set_fft_streams(p);
   const int64_t nx = p->gg.dims[0], nz = p->prm.dims[2], pz = p->kg.p[2], P1 = p->prm.P - 1;
   const KzSplit ks = kz_split_of(p);
   const int64_t rows = (int64_t)p->yo * nx;
-  for (int o = 0; o < p->n_out; ++o) {
+  for (int o = o0; o < o1; ++o) {
     k_kz_exchange<<<grid_size(ctx, rows * p->kg.nzh), 256, 0, st>>>(
         p->Amix, (double2*)recv_back + (size_t)o * p->n_amix, rows, p->kg.nzh, ks, 1);
     HS_LAUNCHED(ctx);
     if (cufftExecZ2D(p->zi, (cufftDoubleComplex*)p->Amix, p->grid_tmp + (size_t)o * p->n_grid) != CUFFT_SUCCESS)
       return fail(HS_ERR_CUDA, "cuFFT z Z2D failed");
   }
+  if (o1 < p->n_out) return HS_OK;
   // interleave the owned planes; the ghost planes are filled by hs_slab_finish
   const int64_t n_owned = rows * pz;
   k_interleave<<<grid_size(ctx, n_owned / 2), 256, 0, st>>>(p->grid_tmp, p->n_out, p->n_grid, n_owned,
@@ -1530,6 +1559,11 @@ extern "C" hs_status hs_slab_backward(hs_plan* p, const double* recv_back, doubl
                             cudaMemcpyDeviceToDevice, st));
   HS_CUDA(cudaEventRecord(p->ev[6], st));
   return HS_OK;
+}
+
+extern "C" hs_status hs_slab_backward(hs_plan* p, const double* recv_back, double* halo_out) {
+  HS_TRY(check_slab(p));
+  return hs_slab_backward_range(p, recv_back, halo_out, 0, p->n_out);
 }
 
 extern "C" hs_status hs_slab_finish(hs_plan* p, const double* halo_in, double* u, double* u_real, double* u_fourier,

@@ -219,6 +219,29 @@ class SlabRank:
         from . import _lib
         _lib.check(self.lib.hs_slab_backward(self.handle, self._vp(self.recv_back), self._vp(self.halo_out)))
 
+    # channel-range forms (pipelined exchanges: run_slab_pipeline(..., overlap=True))
+    def forward_ch(self, have_ghost: bool, c: int):
+        from . import _lib
+        _lib.check(self.lib.hs_slab_forward_range(self.handle, self._vp(self.ghost_in) if have_ghost else None,
+                                                  self._vp(self.send), c, c + 1))
+
+    def kspace_in(self, c: int):
+        from . import _lib
+        _lib.check(self.lib.hs_slab_kspace_part(self.handle, 0, self._vp(self.recv), self._vp(self.back), c, c + 1))
+
+    def kspace_x(self):
+        from . import _lib
+        _lib.check(self.lib.hs_slab_kspace_part(self.handle, 1, self._vp(self.recv), self._vp(self.back), 0, 0))
+
+    def kspace_out(self, o: int):
+        from . import _lib
+        _lib.check(self.lib.hs_slab_kspace_part(self.handle, 2, self._vp(self.recv), self._vp(self.back), o, o + 1))
+
+    def backward_ch(self, o: int):
+        from . import _lib
+        _lib.check(self.lib.hs_slab_backward_range(self.handle, self._vp(self.recv_back), self._vp(self.halo_out),
+                                                   o, o + 1))
+
     def finish(self, have_halo: bool):
         import ctypes as C
         from . import _lib
@@ -244,15 +267,19 @@ class LocalExchange:
                 got.add(d)
         return got
 
-    def all_to_all(self, states, send_attr, recv_attr, send_splits, recv_splits):
+    def all_to_all(self, states, send_attr, recv_attr, send_splits, recv_splits, channels=None):
         n_ch = getattr(states[0], send_attr).shape[0]
-        for c in range(n_ch):
+        for c in (range(n_ch) if channels is None else channels):
             chunks = [getattr(st, send_attr)[c, :sum(send_splits(st.rank))].split(send_splits(st.rank))
                       for st in states]
             for st in states:
                 dst = getattr(st, recv_attr)[c, :sum(recv_splits(st.rank))].split(recv_splits(st.rank))
                 for s in range(len(states)):
                     dst[s].copy_(chunks[s][st.rank])
+        return None
+
+    def wait(self, handle):
+        pass
 
 
 class DistExchange:
@@ -279,31 +306,67 @@ class DistExchange:
                 w.wait()
         return {st.rank} if 0 <= s < self.world else set()
 
-    def all_to_all(self, states, send_attr, recv_attr, send_splits, recv_splits):
+    def all_to_all(self, states, send_attr, recv_attr, send_splits, recv_splits, channels=None, async_op=False):
         (st,) = states
         ss, rs = send_splits(st.rank), recv_splits(st.rank)
         src, dst = getattr(st, send_attr), getattr(st, recv_attr)
-        for c in range(src.shape[0]):
-            self.dist.all_to_all_single(dst[c, :sum(rs)], src[c, :sum(ss)], rs, ss, group=self.group)
+        works = []
+        for c in (range(src.shape[0]) if channels is None else channels):
+            works.append(self.dist.all_to_all_single(dst[c, :sum(rs)], src[c, :sum(ss)], rs, ss, group=self.group,
+                                                     async_op=async_op))
+        return works if async_op else None
+
+    def wait(self, handle):
+        # NCCL: orders the current stream after the collective (no host block); gloo: blocks
+        for w in handle or ():
+            w.wait()
 
 
-def run_slab_pipeline(states, xch, inputs):
+def run_slab_pipeline(states, xch, inputs, overlap=True):
     """One sharded evaluation over the ranks in `states` (all ranks, or this process's one).
 
     inputs[rank] = (positions, sa, sb, targets, tcols) device tensors of that rank.
-    Returns {rank: times}."""
+    overlap: per-channel pipelining -- the all-to-all of channel c is issued asynchronously
+    (DistExchange: on the collective's stream) right after channel c is transformed, so it
+    overlaps the z / y transforms of the next channels.  Returns {rank: times}."""
     lay = states[0].layout
     for st in states:
         st.begin(*inputs[st.rank])
     got = xch.shift(states, "ghost_out", "ghost_in", +1)
-    for st in states:
-        st.forward(st.rank in got)
-    xch.all_to_all(states, "send", "recv", lay.fwd_send_splits, lay.fwd_recv_splits)
-    for st in states:
-        st.kspace()
-    xch.all_to_all(states, "back", "recv_back", lay.fwd_recv_splits, lay.fwd_send_splits)
-    for st in states:
-        st.backward()
+    if not overlap:
+        for st in states:
+            st.forward(st.rank in got)
+        xch.all_to_all(states, "send", "recv", lay.fwd_send_splits, lay.fwd_recv_splits)
+        for st in states:
+            st.kspace()
+        xch.all_to_all(states, "back", "recv_back", lay.fwd_recv_splits, lay.fwd_send_splits)
+        for st in states:
+            st.backward()
+    else:
+        n_in, n_out = states[0].n_in, states[0].n_out
+        kw = {"async_op": True} if isinstance(xch, DistExchange) else {}
+        pend = []
+        for c in range(n_in):
+            for st in states:
+                st.forward_ch(st.rank in got, c)
+            pend.append(xch.all_to_all(states, "send", "recv", lay.fwd_send_splits, lay.fwd_recv_splits,
+                                       channels=[c], **kw))
+        for c in range(n_in):
+            xch.wait(pend[c])
+            for st in states:
+                st.kspace_in(c)
+        for st in states:
+            st.kspace_x()
+        pend = []
+        for o in range(n_out):
+            for st in states:
+                st.kspace_out(o)
+            pend.append(xch.all_to_all(states, "back", "recv_back", lay.fwd_recv_splits, lay.fwd_send_splits,
+                                       channels=[o], **kw))
+        for o in range(n_out):
+            xch.wait(pend[o])
+            for st in states:
+                st.backward_ch(o)
     got = xch.shift(states, "halo_out", "halo_in", -1)
     return {st.rank: st.finish(st.rank in got) for st in states}
 
