@@ -414,15 +414,22 @@ struct SwBuf {
 // support touches (11 GB of DRAM reads per channel group at HL), now only its 32-byte record
 // and weights are -- but the producers' dependent recurrence chains then bound the consumers
 // (24.4 vs 18.1 ms at HL), so !FLY (window tables + cp.async) is the default.
-template <int NCH, bool FLY>
-__global__ void __launch_bounds__(SW_THREADS, 2) k_spread_mma4(const int4* __restrict__ lo4, const double* __restrict__ tab,
+// NCW consumer warps: 8 (warp patch 4x8 (x,y) x 8 z, 2 CTAs/SM) or 16 (patch 4x4 x 8, 1 CTA/SM,
+// a 16-deep ring): the smaller patch cuts the y padding of the DMMA work (window rows outside a
+// warp's patch) from (24+7)/24 to (24+3)/24, and with all channels in one launch the producers
+// stage every source once instead of once per channel group.
+template <int NCH, bool FLY, int NCW = 8>
+__global__ void __launch_bounds__((NCW + SW_NP) * 32, NCW == 8 ? 2 : 1) k_spread_mma4(const int4* __restrict__ lo4, const double* __restrict__ tab,
                                                        WTab wt, const double4* __restrict__ pts,
                                                        const double* __restrict__ w, int ldw,
                                                        const int* __restrict__ bin_start, GridGeom g, int nbx,
                                                        int nby, int nbz, double* __restrict__ grids) {
   constexpr int RX = SW_RX, RY = SW_RY, RZ = SW_RZ, RQ = SwBuf<NCH>::RQ, PER = SwBuf<NCH>::DOUBLES;
   extern __shared__ __align__(16) double sm_dyn[];
-  __shared__ __align__(8) uint64_t full_bar[SW_K], empty_bar[SW_K];
+  constexpr int K = NCW == 16 ? 16 : SW_K;  // ring depth
+  constexpr int PY = 64 / NCW, RB = PY / 2;  // warp patch rows, row blocks of 8 positions
+  constexpr int PB = NCW;                    // mask bit of the window-slice parities
+  __shared__ __align__(8) uint64_t full_bar[K], empty_bar[K];
   __shared__ int run_beg[9], run_pre[10];
   __shared__ int s_nrun;
   auto bx_ = [&](int b) { return reinterpret_cast<double(*)[RX]>(sm_dyn + b * PER); };
@@ -455,9 +462,9 @@ __global__ void __launch_bounds__(SW_THREADS, 2) k_spread_mma4(const int4* __res
     run_pre[nr] = tot;
     s_nrun = nr;
 #pragma unroll
-    for (int k = 0; k < SW_K; ++k) {
-      mbar_init(&full_bar[k], 64);    // producer lanes: stores released + their cp.async completed
-      mbar_init(&empty_bar[k], 256);  // every consumer thread
+    for (int k = 0; k < K; ++k) {
+      mbar_init(&full_bar[k], 64);          // producer lanes: stores released + their cp.async completed
+      mbar_init(&empty_bar[k], NCW * 32);   // every consumer thread
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
@@ -465,9 +472,9 @@ __global__ void __launch_bounds__(SW_THREADS, 2) k_spread_mma4(const int4* __res
   const int nrun = s_nrun, ncand = run_pre[nrun];
   const int nchunk = (ncand + SW_CH - 1) / SW_CH;
 
-  if (warp >= 8) {
+  if (warp >= NCW) {
     // ---------------- producers ----------------
-    const int pid = warp - 8;
+    const int pid = warp - NCW;
     // rows / windows starts / weights of chunk c+1 and c+2 are in flight (registers) while
     // chunk c is staged, so the producer runs at one chunk per staging pass, not per load latency
     struct Pre {
@@ -541,11 +548,11 @@ __global__ void __launch_bounds__(SW_THREADS, 2) k_spread_mma4(const int4* __res
     fetch(pid, f1);
     fetch(pid + SW_NP, f2);
     for (int c = pid; c < nchunk; c += SW_NP) {
-      const int b = c % SW_K;
+      const int b = c % K;
       const Pre cur = f1;
       f1 = f2;
       fetch(c + 2 * SW_NP, f2);
-      if (c >= SW_K) mbar_wait(&empty_bar[b], ((c / SW_K) - 1) & 1);
+      if (c >= K) mbar_wait(&empty_bar[b], ((c / K) - 1) & 1);
       unsigned m[SW_H];
       int ex[SW_H], ey[SW_H], ez[SW_H];
 #pragma unroll
@@ -557,9 +564,9 @@ __global__ void __launch_bounds__(SW_THREADS, 2) k_spread_mma4(const int4* __res
           const int4 l = cur.lo[h];
           if (l.z < z0 + SP_TZ && l.z + P > z0) {
 #pragma unroll
-            for (int wq = 0; wq < 8; ++wq) {
-              const int px = x0 + (wq & 3) * 4, py = y0 + (wq >> 2) * 8;
-              if (l.x < px + 4 && l.x + P > px && l.y < py + 8 && l.y + P > py) m[h] |= 1u << wq;
+            for (int wq = 0; wq < NCW; ++wq) {
+              const int px = x0 + (wq & 3) * 4, py = y0 + (wq >> 2) * PY;
+              if (l.x < px + 4 && l.x + P > px && l.y < py + PY && l.y + P > py) m[h] |= 1u << wq;
             }
           }
           ex[h] = SP_TX + (x0 - l.x);
@@ -570,8 +577,8 @@ __global__ void __launch_bounds__(SW_THREADS, 2) k_spread_mma4(const int4* __res
             for (int ch = 0; ch < NCH; ++ch) bq_(b)[sl][ch] = cur.q[h][ch];
           }
         }
-        bm_(b)[sl] = m[h] | (m[h] ? ((unsigned)(ex[h] & 1) << 8) | ((unsigned)(ey[h] & 1) << 9) |
-                                        ((unsigned)(ez[h] & 1) << 10)
+        bm_(b)[sl] = m[h] | (m[h] ? ((unsigned)(ex[h] & 1) << PB) | ((unsigned)(ey[h] & 1) << (PB + 1)) |
+                                        ((unsigned)(ez[h] & 1) << (PB + 2))
                                   : 0u);
       }
       mbar_arrive(&full_bar[b]);  // masks / weights (plain stores) released
@@ -611,19 +618,19 @@ __global__ void __launch_bounds__(SW_THREADS, 2) k_spread_mma4(const int4* __res
     return;
   }
 
-  // ---------------- consumers (warps 0-7) ----------------
-  const int wx0 = (warp & 3) * 4, wy0 = (warp >> 2) * 8;  // warp patch origin inside the tile
+  // ---------------- consumers (warps 0 .. NCW-1) ----------------
+  const int wx0 = (warp & 3) * 4, wy0 = (warp >> 2) * PY;  // warp patch origin inside the tile
   const int kq = lane & 3;   // k index (source slot) of this lane's A and B fragments
   const int rq = lane >> 2;  // A row / B column / C row of this lane
-  double acc[4][NCH][2];
+  double acc[RB][NCH][2];
 #pragma unroll
-  for (int rb = 0; rb < 4; ++rb)
+  for (int rb = 0; rb < RB; ++rb)
 #pragma unroll
     for (int c = 0; c < NCH; ++c) acc[rb][c][0] = acc[rb][c][1] = 0.0;
   for (int c = 0; c < nchunk; ++c) {
-    const int b = c % SW_K;
+    const int b = c % K;
     const int nc = min(SW_CH, ncand - c * SW_CH);
-    mbar_wait(&full_bar[b], (c / SW_K) & 1);
+    mbar_wait(&full_bar[b], (c / K) & 1);
     double(*s_wx)[RX] = bx_(b);
     double(*s_wy)[RY] = by_(b);
     double(*s_wz)[RZ] = bz_(b);
@@ -640,19 +647,19 @@ __global__ void __launch_bounds__(SW_THREADS, 2) k_spread_mma4(const int4* __res
           if (m) m &= m - 1;
           if (k == kq) sk = sb;
         }
-        double bz = 0.0, q[NCH], cxy[4];
+        double bz = 0.0, q[NCH], cxy[RB];
 #pragma unroll
         for (int ch = 0; ch < NCH; ++ch) q[ch] = 0.0;
 #pragma unroll
-        for (int rb = 0; rb < 4; ++rb) cxy[rb] = 0.0;
+        for (int rb = 0; rb < RB; ++rb) cxy[rb] = 0.0;
         if (sk >= 0) {
           const unsigned par = s_mask[sk];
-          const int pxo = (par >> 8) & 1, pyo = (par >> 9) & 1, pzo = (par >> 10) & 1;
+          const int pxo = (par >> PB) & 1, pyo = (par >> (PB + 1)) & 1, pzo = (par >> (PB + 2)) & 1;
           bz = s_wz[sk][pzo + rq];  // B[k][n] = wz_{s_k}(z_n), n = rq
 #pragma unroll
           for (int ch = 0; ch < NCH; ++ch) q[ch] = s_q[sk][ch];
 #pragma unroll
-          for (int rb = 0; rb < 4; ++rb) {
+          for (int rb = 0; rb < RB; ++rb) {
             const int p = rb * 8 + rq;  // position of A row rq in row block rb
             cxy[rb] = s_wx[sk][pxo + wx0 + (p & 3)] * s_wy[sk][pyo + wy0 + (p >> 2)];
           }
@@ -663,7 +670,7 @@ __global__ void __launch_bounds__(SW_THREADS, 2) k_spread_mma4(const int4* __res
 #pragma unroll
         for (int ch = 0; ch < NCH; ++ch) bq[ch] = bz * q[ch];
 #pragma unroll
-        for (int rb = 0; rb < 4; ++rb)
+        for (int rb = 0; rb < RB; ++rb)
 #pragma unroll
           for (int ch = 0; ch < NCH; ++ch) dmma_884(acc[rb][ch][0], acc[rb][ch][1], cxy[rb], bq[ch]);
       }
@@ -672,7 +679,7 @@ __global__ void __launch_bounds__(SW_THREADS, 2) k_spread_mma4(const int4* __res
   }
   // C fragment: row rq of row block rb = position p, columns z = 2 kq, 2 kq + 1
 #pragma unroll
-  for (int rb = 0; rb < 4; ++rb) {
+  for (int rb = 0; rb < RB; ++rb) {
     const int p = rb * 8 + rq;
     const int x = x0 + wx0 + (p & 3), y = y0 + wy0 + (p >> 2);
     if (x < g.dims[0] && y < g.dims[1]) {
@@ -990,6 +997,33 @@ hs_status launch_spread(hs_ctx* ctx, const double4* pts, const double* w, int n,
       HS_LAUNCHED(ctx);
     }
     dim3 grid(nbx * nby * nbz);
+    // default: 16 consumer warps (4x4 patches), up to 7 channels per launch, groups balanced
+    // (7 -> 7, 13 -> 7 + 6); HS_SPREAD_W8=1: 8 warps (4x8 patches), 4 channels per launch
+    static const bool w8 = getenv("HS_SPREAD_W8") != nullptr;
+    if (tables && !w8 && nch >= 3) {
+      const int ngroup = (nch + 6) / 7;
+      for (int gi = 0, c0 = 0; gi < ngroup; ++gi) {
+        const int cn = (nch - c0) / (ngroup - gi);
+        double* gout = grids + (size_t)c0 * g.ch_stride;
+        const double* wc0 = w + c0;
+        switch (cn) {
+#define HS_SP16(N)                                                                                                 \
+  case N: {                                                                                                        \
+    const size_t smm = sizeof(double) * 16 * SwBuf<N>::DOUBLES;                                                    \
+    HS_CUDA(cudaFuncSetAttribute(k_spread_mma4<N, false, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize,        \
+                                 (int)smm));                                                                       \
+    k_spread_mma4<N, false, 16><<<grid, (16 + SW_NP) * 32, smm, ctx->stream>>>(lo, tab, wt, pts, wc0, nch,         \
+                                                                             bin_start, g, nbx, nby, nbz, gout);   \
+  } break;
+          HS_SP16(3) HS_SP16(4) HS_SP16(5) HS_SP16(6) HS_SP16(7)
+#undef HS_SP16
+          default: return fail(HS_ERR_PARAMETER, "spread channel group");
+        }
+        HS_LAUNCHED(ctx);
+        c0 += cn;
+      }
+      return HS_OK;
+    }
     for (int c0 = 0; c0 < nch; c0 += SP_MAXCH) {
       const int cn = std::min(SP_MAXCH, nch - c0);
       double* gout = grids + (size_t)c0 * g.ch_stride;
