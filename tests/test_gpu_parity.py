@@ -254,6 +254,23 @@ def test_ewald_deterministic(gpu):
     np.testing.assert_array_equal(a, b)
 
 
+def test_concurrent_pipelines_bitwise_equal_serial(gpu):
+    """The default evaluation runs the real-space pipeline on a second stream concurrently with
+    the Fourier pipeline; serialised (what bit 2) it must give the same bits, parts included."""
+    from paper_1802_07844_b200._plan import get_evaluator
+    from paper_1802_07844_b200.configs import make_system
+    from paper_1802_07844_b200.ewald_fourier import prepare_tables
+    s, _ = make_system("cfg3", n=30_000)
+    p = gpu.EwaldParams(xi=20.8, rc=0.17, M=80, P=24)
+    g = p.grid(1.0, "half")
+    ev = get_evaluator(s.kind, s.geometry, 1.0, p.xi, p.rc, g, s.n, s.n, True)
+    prepare_tables(ev, s, g, None, None)
+    u1, r1, f1, _ = ev.execute(s.positions, s.g, s.q, what=3)
+    u2, r2, f2, _ = ev.execute(s.positions, s.g, s.q, what=7)
+    for x, y in ((u1, u2), (r1, r2), (f1, f2)):
+        np.testing.assert_array_equal(x, y)
+
+
 def test_missing_table_rejected(gpu):
     d = golden("fourier")
     s = _mk(gpu, "rotlet", d, "rotlet_half", 2.0)
