@@ -537,6 +537,7 @@ __global__ void __launch_bounds__(XF_THREADS, M == 27 ? 1 : 2) k_xreg(const XArg
   double2* lines = smem;            // [NL][LSR]: transpose scratch of the line's warp, then the channel line
   double2* tw = smem + NL * LSR;    // pd8-padded twiddles
   double2* stage = tw + padded_line(N);  // [NIN][nx] (STAGE)
+  double* stab = reinterpret_cast<double*>(stage + NIN * a.nx);  // [2][N] table rows (STAGE)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int i = tid; i < N; i += blockDim.x) tw[pd8(i)] = a.tw[i];
   const int n_items = a.py * a.nzh;
@@ -553,7 +554,23 @@ __global__ void __launch_bounds__(XF_THREADS, M == 27 ? 1 : 2) k_xreg(const XArg
     }
     cp_async_commit();
   };
-  if (STAGE) prefetch(blockIdx.x);
+  // table rows of a column (its scaling phase), prefetched while the previous column is
+  // inverse-transformed
+  auto prefetch_tab = [&](int it) {
+    if (it < n_items) {
+      const int ky2 = it / a.nzh, kz2 = it - ky2 * a.nzh;
+      const int64_t t0 = ((int64_t)ky2 * a.nzh + kz2) * N;
+      for (int i = tid; i < N / 2; i += blockDim.x) {
+        if (KIND != HS_ROTLET) cp_async16(&stab[2 * i], a.tabB + t0 + 2 * i);
+        if (KIND == HS_ROTLET || HALF) cp_async16(&stab[N + 2 * i], a.tabH + t0 + 2 * i);
+      }
+    }
+    cp_async_commit();
+  };
+  if (STAGE) {
+    prefetch(blockIdx.x);
+    prefetch_tab(blockIdx.x);
+  }
   for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
     const int ky = item / a.nzh;
     const int kzl = item - ky * a.nzh, kz = a.kz0 + kzl;  // local column, global wavenumber index
@@ -587,8 +604,8 @@ __global__ void __launch_bounds__(XF_THREADS, M == 27 ? 1 : 2) k_xreg(const XArg
     // k-space scaling at every kx of the column (channel c of kx at lines[c * LSR + kx])
     for (int kx = tid; kx < N; kx += blockDim.x) {
       const int64_t ti = ((int64_t)ky * a.nzh + kzl) * N + kx;
-      const double tB = (KIND == HS_ROTLET) ? 0.0 : a.tabB[ti];
-      const double tH = (KIND == HS_ROTLET || HALF) ? a.tabH[ti] : 0.0;
+      const double tB = (KIND == HS_ROTLET) ? 0.0 : (STAGE ? stab[kx] : a.tabB[ti]);
+      const double tH = (KIND == HS_ROTLET || HALF) ? (STAGE ? stab[N + kx] : a.tabH[ti]) : 0.0;
       double2* col = lines + kx;
       if (2 * kx == N || 2 * ky == a.py || 2 * kz == a.pz) {
         scale_nyquist<KIND, HALF>(col, LSR, kx, ky, kz, p, a.kscale, a.ka, a.kb, a.inv_n, tB, tH);
@@ -612,6 +629,7 @@ __global__ void __launch_bounds__(XF_THREADS, M == 27 ? 1 : 2) k_xreg(const XArg
       for (int o = 0; o < NOUT; ++o) col[o * LSR] = make_double2(outc[o].re, -outc[o].im);
     }
     __syncthreads();
+    if (STAGE) prefetch_tab(item + gridDim.x);  // table rows read by this column's scaling
     for (int o = warp; o < NOUT; o += NW) {
       double2 v[M], out[RegFFT<M>::NG][16];
       double2* S = lines + o * LSR;
@@ -639,7 +657,7 @@ static hs_status launch_xreg_t(hs_ctx* ctx, const XArgs& a) {
   HS_TRY(xreg_constants());
   constexpr int NL = KChan<KIND, HALF>::NIN > KChan<KIND, HALF>::NOUT ? KChan<KIND, HALF>::NIN : KChan<KIND, HALF>::NOUT;
   const size_t smem0 = sizeof(double2) * ((size_t)NL * M * 33 + padded_line(32 * M));
-  const size_t smem1 = smem0 + sizeof(double2) * (size_t)KChan<KIND, HALF>::NIN * a.nx;
+  const size_t smem1 = smem0 + sizeof(double2) * (size_t)KChan<KIND, HALF>::NIN * a.nx + sizeof(double) * 2 * 32 * M;
   // staging only if the kernel keeps its CTAs per SM (2, or 1 for M = 27) and HS_XSTAGE_NOSTAGE unset
   static const bool nostage = getenv("HS_XSTAGE_NOSTAGE") != nullptr;
   const size_t budget = (M == 27 ? 227 : 113) * 1024;
