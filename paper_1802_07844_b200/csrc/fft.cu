@@ -699,27 +699,42 @@ __global__ void __launch_bounds__(256, M == 27 ? 1 : 2) k_ystage(const double2* 
   const int rows_in = FWD ? ny : N, rows_out = FWD ? N : ny;
   const int64_t rstride = (int64_t)nx * nzh;  // elements between rows (y)
   const int r = lane >> 1, h = lane & 1;
+  // forward: the next item's ny input rows are prefetched into a separate staging area (pre)
+  // while the current item is transformed and written (the inverse reads all N rows; its
+  // staging would not fit two CTAs per SM)
+  double2* pre = tw + padded_line(N);  // [ny][YS_RS] (FWD)
+  auto load_rows = [&](int it, double2* dst) {
+    if (it < n_items) {
+      const int x2 = it / nkb, k02 = (it - x2 * nkb) * YS_KB;
+      const int kb2 = min(YS_KB, nzh - k02);
+      const int64_t b2 = (int64_t)x2 * nzh + k02;
+      for (int i = tid; i < rows_in * YS_KB; i += blockDim.x) {
+        const int row = i / YS_KB, k = i - row * YS_KB;
+        if (k < kb2) cp_async16(&dst[row * YS_RS + k], in + b2 + row * rstride + k);
+      }
+    }
+    cp_async_commit();
+  };
+  if (FWD) load_rows(blockIdx.x, pre);
   for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
     const int x = item / nkb, kz0 = (item - x * nkb) * YS_KB;
     const int kbn = min(YS_KB, nzh - kz0);
     const int64_t base = (int64_t)x * nzh + kz0;
     __syncthreads();  // previous item done with buf
-    for (int i = tid; i < rows_in * YS_KB; i += blockDim.x) {
-      const int row = i / YS_KB, k = i - row * YS_KB;
-      if (k < kbn) cp_async16(&buf[row * YS_RS + k], in + base + row * rstride + k);
-    }
-    cp_async_commit();
+    if (!FWD) load_rows(item, buf);
     cp_async_wait_all();
     __syncthreads();
+    const double2* src = FWD ? pre : buf;
     double2 v[M], o16[RegFFT<M>::NG][16];
 #pragma unroll
     for (int j = 0; j < M; ++j) {
       const int row = lane + 32 * j;
-      double2 e = row < rows_in ? buf[row * YS_RS + warp] : make_double2(0.0, 0.0);
+      double2 e = row < rows_in ? src[row * YS_RS + warp] : make_double2(0.0, 0.0);
       if (!FWD) e.y = -e.y;
       v[j] = e;
     }
     __syncthreads();  // every column read: the buffer becomes transpose scratch
+    if (FWD) load_rows(item + gridDim.x, pre);
     warp_fft_reg<M>(v, buf + warp * M * 33, tw, lane, o16);
     __syncthreads();  // scratch use finished: the buffer collects the output rows
 #pragma unroll
@@ -749,7 +764,8 @@ hs_status launch_ystage(hs_ctx* ctx, bool fwd, const double2* in, double2* out, 
                         int nzh, int ny) {
   HS_TRY(xreg_constants());
   auto go = [&](auto kern, int M) -> hs_status {
-    const size_t smem = sizeof(double2) * ((size_t)32 * M * YS_RS + padded_line(32 * M));
+    const size_t smem = sizeof(double2) * ((size_t)32 * M * YS_RS + padded_line(32 * M) +
+                                           (fwd ? (size_t)ny * YS_RS : 0));  // + forward prefetch rows
     HS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int items = nx * ((nzh + YS_KB - 1) / YS_KB);
     const int grid = std::max(1, std::min(items, ctx->sm_count * 2 * 8));
