@@ -248,7 +248,13 @@ constexpr int PC_WARPS = 4;
 constexpr int PC_TG = PC_WARPS * 32;  // targets per work item
 constexpr int PC_K = 256;             // staged candidates (two halves of PC_H)
 constexpr int PC_H = PC_K / 2;        // candidates per chunk
-constexpr int PC_Q = 64;              // per-lane queue capacity
+#ifndef PC_Q_DEF
+#define PC_Q_DEF 64
+#endif
+#ifndef PC_ODD_SINGLE
+#define PC_ODD_SINGLE 0
+#endif
+constexpr int PC_Q = PC_Q_DEF;        // per-lane queue capacity (power of two)
 #ifndef PC_MINB
 #define PC_MINB 4                     // resident CTAs per SM (register budget 128)
 #endif
@@ -507,7 +513,8 @@ __global__ void __launch_bounds__(PC_TG, PC_MINB) k_pair_q(const PairArgs a) {
         if (tvalid) {
           unsigned r = 0;
           for (; r + 1 < mn; r += 2) pop_eval2();
-          if (r < mn) pop_eval();
+          // an odd leftover stays queued for the next two-pair round (PC_ODD_SINGLE=1: evaluate it now)
+          if (PC_ODD_SINGLE && r < mn) pop_eval();
         }
         while ((int)__reduce_max_sync(0xffffffffu, (unsigned)(tail - head)) > PC_Q - 32) {
           if (tail > head) pop_eval();
