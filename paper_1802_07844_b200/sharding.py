@@ -283,27 +283,40 @@ class LocalExchange:
 
 
 class DistExchange:
-    """One rank per process; torch.distributed collectives on the process group."""
+    """One rank per process; torch.distributed collectives on the process group.
 
-    def __init__(self, group=None):
+    staged: the group's backend cannot move device tensors (gloo): buffers go through host
+    copies around each collective.  Defaults to True for a gloo group and device tensors --
+    the multi-process check of the whole pipeline on one GPU (tests/test_slab.py); NCCL
+    moves the device buffers directly."""
+
+    def __init__(self, group=None, staged=None):
         import torch.distributed as dist
         self.dist, self.group = dist, group
         self.world = dist.get_world_size(group)
+        self.staged = (dist.get_backend(group) == "gloo") if staged is None else bool(staged)
 
     def _peer(self, r):
         return r if self.group is None else self.dist.get_global_rank(self.group, r)
 
+    def _host(self, t):
+        return t.cpu() if self.staged and t.is_cuda else t
+
     def shift(self, states, src_attr, dst_attr, step):
         (st,) = states
         d, s = st.rank + step, st.rank - step
+        src, dst = getattr(st, src_attr), getattr(st, dst_attr)
+        hsrc, hdst = self._host(src), self._host(dst)
         ops = []
         if 0 <= d < self.world:
-            ops.append(self.dist.P2POp(self.dist.isend, getattr(st, src_attr), self._peer(d), self.group))
+            ops.append(self.dist.P2POp(self.dist.isend, hsrc, self._peer(d), self.group))
         if 0 <= s < self.world:
-            ops.append(self.dist.P2POp(self.dist.irecv, getattr(st, dst_attr), self._peer(s), self.group))
+            ops.append(self.dist.P2POp(self.dist.irecv, hdst, self._peer(s), self.group))
         if ops:
             for w in self.dist.batch_isend_irecv(ops):
                 w.wait()
+        if hdst is not dst and 0 <= s < self.world:
+            dst.copy_(hdst)
         return {st.rank} if 0 <= s < self.world else set()
 
     def all_to_all(self, states, send_attr, recv_attr, send_splits, recv_splits, channels=None, async_op=False):
@@ -312,6 +325,11 @@ class DistExchange:
         src, dst = getattr(st, send_attr), getattr(st, recv_attr)
         works = []
         for c in (range(src.shape[0]) if channels is None else channels):
+            if self.staged and src.is_cuda:   # host round trip, synchronous
+                hd = dst[c, :sum(rs)].cpu()
+                self.dist.all_to_all_single(hd, src[c, :sum(ss)].cpu(), rs, ss, group=self.group)
+                dst[c, :sum(rs)].copy_(hd)
+                continue
             works.append(self.dist.all_to_all_single(dst[c, :sum(rs)], src[c, :sum(ss)], rs, ss, group=self.group,
                                                      async_op=async_op))
         return works if async_op else None
