@@ -246,8 +246,12 @@ __device__ __forceinline__ double exact_r2(double d0, double d1, double d2) {
 // its own target (no cross-lane reductions, no atomics, deterministic order).
 constexpr int PC_WARPS = 4;
 constexpr int PC_TG = PC_WARPS * 32;  // targets per work item
-constexpr int PC_K = 256;             // staged candidates (two halves of PC_H)
-constexpr int PC_H = PC_K / 2;        // candidates per chunk
+constexpr int PC_H = 128;             // candidates per chunk
+// chunks held in the staging ring (stokeslet: 3, so a lane's FIFO entries of the chunk being
+// restaged -- which force partial-round drains -- are rarer; the stresslet / rotlet records
+// leave room for 2 within 48 KB of static shared memory)
+template <int KIND>
+constexpr int pc_nh() { return KIND == HS_STOKESLET ? 3 : 2; }
 #ifndef PC_Q_DEF
 #define PC_Q_DEF 64
 #endif
@@ -263,6 +267,7 @@ template <int KIND, bool HALF>
 __global__ void __launch_bounds__(PC_TG, PC_MINB) k_pair_q(const PairArgs a) {
   // Candidate rows as 16-byte columns: the evaluation reads them at lane-random rows, and a
   // 16-byte array spreads those reads over 8 bank groups (a 32-byte row only over 4).
+  constexpr int PC_K = pc_nh<KIND>() * PC_H;  // staged candidates
   __shared__ double2 sXY[PC_K];  // x, y
   __shared__ double2 sZA[PC_K];  // z (sign bit = image in the half space), a.x
   __shared__ double2 sAA[PC_K];  // a.y, a.z
@@ -414,7 +419,7 @@ __global__ void __launch_bounds__(PC_TG, PC_MINB) k_pair_q(const PairArgs a) {
       apply_pair<KIND>(pc, q2, g0, g1, g2, r2, T.z, S2, A2, B2, i2, &acc[0], &acc[3]);
     };
     for (int c = 0, c0 = 0; c0 < ncand; ++c, c0 += PC_H) {
-      const int h = c & 1, hb = h * PC_H;
+      const int h = c % pc_nh<KIND>(), hb = h * PC_H;
       // drain the (oldest) entries that still reference half h
       while (__any_sync(0xffffffffu, tail > head && (q[head & (PC_Q - 1)][lane] >> 7) == h)) {
         if (tail > head && (q[head & (PC_Q - 1)][lane] >> 7) == h) pop_eval();
