@@ -247,11 +247,22 @@ __device__ __forceinline__ double exact_r2(double d0, double d1, double d2) {
 constexpr int PC_WARPS = 4;
 constexpr int PC_TG = PC_WARPS * 32;  // targets per work item
 constexpr int PC_H = 128;             // candidates per chunk
+#ifndef PC_NH_STOKESLET
+#define PC_NH_STOKESLET 4
+#endif
+#ifndef PC_NH_OTHER
+#define PC_NH_OTHER 3
+#endif
 // chunks held in the staging ring (stokeslet: 3, so a lane's FIFO entries of the chunk being
 // restaged -- which force partial-round drains -- are rarer; the stresslet / rotlet records
 // leave room for 2 within 48 KB of static shared memory)
 template <int KIND>
-constexpr int pc_nh() { return KIND == HS_STOKESLET ? 3 : 2; }
+constexpr int pc_nh() { return KIND == HS_STOKESLET ? PC_NH_STOKESLET : PC_NH_OTHER; }
+// candidate record bytes in shared memory (dynamic): xy, z a.x, a.y a.z, FP32 view, (+ b)
+template <int KIND, bool HALF>
+constexpr int pc_rec_bytes() {
+  return 64 + ((KIND == HS_STRESSLET) || (KIND == HS_ROTLET && HALF) ? 16 : 0) + (KIND == HS_STRESSLET ? 8 : 0);
+}
 #ifndef PC_Q_DEF
 #define PC_Q_DEF 64
 #endif
@@ -267,14 +278,15 @@ template <int KIND, bool HALF>
 __global__ void __launch_bounds__(PC_TG, PC_MINB) k_pair_q(const PairArgs a) {
   // Candidate rows as 16-byte columns: the evaluation reads them at lane-random rows, and a
   // 16-byte array spreads those reads over 8 bank groups (a 32-byte row only over 4).
-  constexpr int PC_K = pc_nh<KIND>() * PC_H;  // staged candidates
-  __shared__ double2 sXY[PC_K];  // x, y
-  __shared__ double2 sZA[PC_K];  // z (sign bit = image in the half space), a.x
-  __shared__ double2 sAA[PC_K];  // a.y, a.z
-  __shared__ float4 sF[PC_K];    // candidate position relative to the item's first target (FP32 prefilter)
+  constexpr int PC_K = pc_nh<KIND>() * PC_H;  // staged candidates (dynamic shared memory)
   constexpr bool kNeedB = (KIND == HS_STRESSLET) || (KIND == HS_ROTLET && HALF);
-  __shared__ double2 sB0[kNeedB ? PC_K : 1];  // b.x, b.y
-  __shared__ double sB1[KIND == HS_STRESSLET ? PC_K : 1];  // b.z
+  extern __shared__ __align__(16) unsigned char pc_dyn[];
+  double2* sXY = reinterpret_cast<double2*>(pc_dyn);  // x, y
+  double2* sZA = sXY + PC_K;                          // z (sign bit = image in the half space), a.x
+  double2* sAA = sZA + PC_K;                          // a.y, a.z
+  float4* sF = reinterpret_cast<float4*>(sAA + PC_K);  // position relative to the item's first target (FP32)
+  double2* sB0 = reinterpret_cast<double2*>(sF + PC_K);  // b.x, b.y (kNeedB)
+  double* sB1 = reinterpret_cast<double*>(sB0 + (kNeedB ? PC_K : 0));  // b.z (stresslet)
   __shared__ unsigned short sq[PC_WARPS][PC_Q][32];
   __shared__ int run_beg[PT_MAXRUN];
   __shared__ int run_pre[PT_MAXRUN + 1];
@@ -606,7 +618,12 @@ hs_status launch_pair(hs_ctx* ctx, const PairArgs& a) {
   const bool is_half = (a.kind & 16) != 0;
   // persistent-style grid: enough CTAs to fill the machine, looping over the device-side item count
   const int grid = std::max(1, std::min(a.max_items, ctx->sm_count * 16));
-#define HS_PAIR_CASE(K, H) k_pair_q<K, H><<<grid, PC_TG, 0, ctx->stream>>>(a)
+#define HS_PAIR_CASE(K, H)                                                                         \
+  do {                                                                                             \
+    const int dyn = pc_nh<K>() * PC_H * pc_rec_bytes<K, H>();                                      \
+    HS_CUDA(cudaFuncSetAttribute(k_pair_q<K, H>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn)); \
+    k_pair_q<K, H><<<grid, PC_TG, dyn, ctx->stream>>>(a);                                           \
+  } while (0)
   if (is_half) {
     if (kind == HS_STOKESLET) HS_PAIR_CASE(HS_STOKESLET, true);
     else if (kind == HS_STRESSLET) HS_PAIR_CASE(HS_STRESSLET, true);
