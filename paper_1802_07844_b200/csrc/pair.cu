@@ -266,6 +266,9 @@ constexpr int pc_rec_bytes() {
 #ifndef PC_Q_DEF
 #define PC_Q_DEF 64
 #endif
+#ifndef PC_ROUND_SLACK
+#define PC_ROUND_SLACK 0
+#endif
 #ifndef PC_ODD_SINGLE
 #define PC_ODD_SINGLE 0
 #endif
@@ -532,6 +535,15 @@ __global__ void __launch_bounds__(PC_TG, PC_MINB) k_pair_q(const PairArgs a) {
           for (; r + 1 < mn; r += 2) pop_eval2();
           // an odd leftover stays queued for the next two-pair round (PC_ODD_SINGLE=1: evaluate it now)
           if (PC_ODD_SINGLE && r < mn) pop_eval();
+        }
+        if (PC_ROUND_SLACK > 0) {
+          // more two-pair rounds while all but PC_ROUND_SLACK of the valid lanes have work (the idle
+          // lanes' slots are cheaper than the partial single rounds a growing backlog forces later)
+          const int nv = __popc(__ballot_sync(0xffffffffu, tvalid));
+          while (__popc(__ballot_sync(0xffffffffu, tvalid && tail - head >= 2)) >= nv - PC_ROUND_SLACK &&
+                 nv > PC_ROUND_SLACK) {
+            if (tvalid && tail - head >= 2) pop_eval2();
+          }
         }
         while ((int)__reduce_max_sync(0xffffffffu, (unsigned)(tail - head)) > PC_Q - 32) {
           if (tail > head) pop_eval();
