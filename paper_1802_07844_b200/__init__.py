@@ -18,5 +18,8 @@ from .ewald_fourier import (BIHARMONIC, HARMONIC, GreensTable, GridSpec, fourier
 from .ewald_real import CellList, RealSpaceParams, build_cell_list, real_space_sum, self_interaction
 from .ewald import EwaldParams, ewald_sum
 from .kernels_direct import direct_sum_free, direct_sum_half
+from .point_kernels import (HarmonicDerivs, correction_phi, harmonic_derivs, kernel_real, rotlet_apply, stokeslet,
+                            stresslet_apply)
+from .ewald_real import f_derivs
 
 __all__ = [n for n in dir() if not n.startswith("_")]

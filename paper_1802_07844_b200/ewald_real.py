@@ -18,6 +18,7 @@ from . import _lib
 from ._plan import get_evaluator
 from .errors import GeometryError, ParameterError
 from .system import HALF_SPACE, ROTLET, STOKESLET, STRESSLET, VelocityResult
+from .point_kernels import kernel_real  # noqa: E402,F401  (ref:ewald_real.py:115-150)
 
 _SQRT_PI = math.sqrt(math.pi)
 

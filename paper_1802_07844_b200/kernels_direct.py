@@ -14,6 +14,8 @@ import numpy as np
 from . import _lib
 from .errors import GeometryError
 from .system import HALF_SPACE, STOKESLET, VelocityResult
+from .point_kernels import (HarmonicDerivs, correction_phi, gfam_coeffs, harmonic_derivs,  # noqa: F401
+                            phi_and_grad, phi_channels, rotlet_apply, stokeslet, stresslet_apply)
 
 
 def _direct(system, geometry, targets, target_indices):
