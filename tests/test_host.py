@@ -162,3 +162,26 @@ def test_product_never_imports_oracle():
                 txt = open(os.path.join(dirpath, f)).read()
                 for bad in ("import oracle", "from oracle", "hsoracle", "liboracle"):
                     assert bad not in txt, (f, bad)
+
+
+def test_install_as_hsewald_aliases_reference_modules():
+    """Callers written for the reference import it by name; the alias maps them here."""
+    import importlib
+    import sys
+    from paper_1802_07844_b200 import compat, experiments, ewald
+    saved = {k: v for k, v in sys.modules.items() if k == "hsewald" or k.startswith("hsewald.")}
+    for k in saved:
+        del sys.modules[k]
+    try:
+        compat.install_as_hsewald()
+        hsewald = importlib.import_module("hsewald")
+        from hsewald.ewald import ewald_sum, EwaldParams  # noqa: F401
+        from hsewald.ewald_fourier import GridSpec, get_tables  # noqa: F401
+        from hsewald.estimates import select_parameters  # noqa: F401
+        assert ewald_sum is ewald.ewald_sum
+        assert hsewald.bench is experiments and callable(hsewald.bench.break_even)
+        assert hsewald.stokeslet is not None and hsewald.kernel_real is not None
+    finally:
+        for k in [k for k in sys.modules if k == "hsewald" or k.startswith("hsewald.")]:
+            del sys.modules[k]
+        sys.modules.update(saved)
