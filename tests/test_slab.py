@@ -297,3 +297,21 @@ def test_slab_multiprocess_one_gpu(gpu, tmp_path, world):
     ref = gpu.ewald_sum(s, gpu.EwaldParams(xi=20.8, rc=0.17, M=96, P=24)).velocities
     for r in range(world):
         assert rel_l2(np.load(tmp_path / f"u{r}.npy"), ref) < 1e-12
+
+
+@pytest.mark.gpu
+def test_headline_full_size_vs_direct_and_slab8(gpu):
+    """The metric's configuration at full size (N = 1e6, M = 192): the single plan against the
+    exact O(N) direct half-space sum at 400 targets (the Ewald truncation error at these
+    parameters is ~2e-11), and the 8-way y-slab decomposition against the single plan."""
+    from paper_1802_07844_b200.configs import WORKLOADS, make_system
+    from paper_1802_07844_b200.sharding import ewald_sum_slab_local
+    w = WORKLOADS["HL"]
+    s, _ = make_system(w)
+    p = gpu.EwaldParams(xi=w.xi, rc=w.rc, M=w.M, P=w.P)
+    u = gpu.ewald_sum(s, p).velocities
+    idx = np.random.default_rng(4).choice(s.n, 400, replace=False)
+    d = gpu.direct_sum_half(s, targets=s.positions[idx], target_indices=idx).velocities
+    assert rel_l2(u[idx], d) < 1e-9
+    r = ewald_sum_slab_local(s, p, 8)
+    assert rel_l2(r.velocities, u) < 1e-12
