@@ -233,6 +233,10 @@ __device__ __noinline__ void scale_nyquist(double2* col, int cstride, int kx, in
 }
 
 constexpr int XF_THREADS = 256;  // 2 CTAs per SM: one CTA's loads overlap the other's FFTs
+#ifndef XR_THREADS_DEF
+#define XR_THREADS_DEF 256
+#endif
+constexpr int XR_THREADS = XR_THREADS_DEF;  // register x-stage CTA size
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
@@ -529,10 +533,10 @@ __device__ __forceinline__ void warp_fft_reg(double2* v, double2* S, const doubl
 // forward FFTs read shared memory instead of waiting on strided global loads (used when the
 // extra NIN * nx * 16 bytes keep the kernel's CTAs per SM).
 template <int KIND, bool HALF, int M, bool STAGE>
-__global__ void __launch_bounds__(XF_THREADS, M == 27 ? 1 : 2) k_xreg(const XArgs a) {
+__global__ void __launch_bounds__(XR_THREADS, M == 27 ? 1 : 2) k_xreg(const XArgs a) {
   constexpr int N = 32 * M, LSR = M * 33;
   constexpr int NIN = KChan<KIND, HALF>::NIN, NOUT = KChan<KIND, HALF>::NOUT;
-  constexpr int NL = NIN > NOUT ? NIN : NOUT, NW = XF_THREADS / 32;
+  constexpr int NL = NIN > NOUT ? NIN : NOUT, NW = XR_THREADS / 32;
   extern __shared__ double2 smem[];
   double2* lines = smem;            // [NL][LSR]: transpose scratch of the line's warp, then the channel line
   double2* tw = smem + NL * LSR;    // pd8-padded twiddles
@@ -666,10 +670,10 @@ static hs_status launch_xreg_t(hs_ctx* ctx, const XArgs& a) {
   auto kern = use_stage ? k_xreg<KIND, HALF, M, true> : k_xreg<KIND, HALF, M, false>;
   HS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0;
-  HS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, XF_THREADS, smem));
+  HS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, XR_THREADS, smem));
   const int items = a.py * a.nzh;
   const int grid = std::max(1, std::min(items, ctx->sm_count * std::max(per_sm, 1) * 8));
-  kern<<<grid, XF_THREADS, smem, ctx->stream>>>(a);
+  kern<<<grid, XR_THREADS, smem, ctx->stream>>>(a);
   HS_LAUNCHED(ctx);
   return HS_OK;
 }
