@@ -347,6 +347,8 @@ __constant__ double2 c_w11[11];  // exp(-2 pi i m / 11)
 __constant__ double2 c_w27[27];  // exp(-2 pi i m / 27)
 __constant__ double2 c_w16[16];  // exp(-2 pi i m / 16)
 __constant__ double2 c_w32[16];  // exp(-2 pi i m / 32)
+__constant__ double2 c_w25[25];  // exp(-2 pi i m / 25)
+__constant__ double2 c_w30[15];  // exp(-2 pi i m / 30)
 static bool g_xreg_consts = false;
 
 static hs_status xreg_constants() {
@@ -363,6 +365,11 @@ static hs_status xreg_constants() {
   HS_CUDA(cudaMemcpyToSymbol(c_w27, w27, sizeof(w27)));
   HS_CUDA(cudaMemcpyToSymbol(c_w16, w16, sizeof(w16)));
   HS_CUDA(cudaMemcpyToSymbol(c_w32, w32, sizeof(w32)));
+  double2 w25[25], w30[15];
+  for (int m = 0; m < 25; ++m) w25[m] = make_double2((double)std::cos(tp * m / 25), (double)-std::sin(tp * m / 25));
+  for (int m = 0; m < 15; ++m) w30[m] = make_double2((double)std::cos(tp * m / 30), (double)-std::sin(tp * m / 30));
+  HS_CUDA(cudaMemcpyToSymbol(c_w25, w25, sizeof(w25)));
+  HS_CUDA(cudaMemcpyToSymbol(c_w30, w30, sizeof(w30)));
   g_xreg_consts = true;
   return HS_OK;
 }
@@ -656,6 +663,149 @@ __global__ void __launch_bounds__(XR_THREADS, M == 27 ? 1 : 2) k_xreg(const XArg
   }
 }
 
+// ---- register x-stage for N = 750 = 30 x 25 (cfg4's padded length) -------------------------
+// Lanes l < 30 hold x[l + 30 j] (j < 25): DFT25 over j in registers, twiddle W750^{l k1}, one
+// transpose through shared memory (S[k1][l], rows of 31), then lanes r < 25 each take row r and
+// finish with a DFT30 (= 2 x DFT15) in registers, ending with X[r + 25 k2], k2 < 30.
+__device__ __forceinline__ void dft25(double2* v) {
+  double2 Y[5][5];
+#pragma unroll
+  for (int j1 = 0; j1 < 5; ++j1) {
+    double2 t[5];
+#pragma unroll
+    for (int j2 = 0; j2 < 5; ++j2) t[j2] = v[j1 + 5 * j2];
+    dft<5>(t);
+#pragma unroll
+    for (int k2 = 0; k2 < 5; ++k2) Y[j1][k2] = (j1 * k2 == 0) ? t[k2] : cm(t[k2], c_w25[j1 * k2]);
+  }
+#pragma unroll
+  for (int k2 = 0; k2 < 5; ++k2) {
+    double2 t[5] = {Y[0][k2], Y[1][k2], Y[2][k2], Y[3][k2], Y[4][k2]};
+    dft<5>(t);
+#pragma unroll
+    for (int k1 = 0; k1 < 5; ++k1) v[5 * k1 + k2] = t[k1];
+  }
+}
+constexpr int X750_L = 30, X750_M = 25, X750_RS = 31, X750_LS = X750_M * X750_RS;  // line slot >= 750
+// forward DFT of the line with x[l + 30 j] in v[j] (lanes < 30); result X[kx] left in S[kx]
+__device__ __forceinline__ void warp_fft750(double2* v, double2* S, const double2* tw, int lane) {
+  if (lane < X750_L) {
+    dft25(v);
+#pragma unroll
+    for (int k1 = 1; k1 < X750_M; ++k1) v[k1] = cm(v[k1], tw[pd8(lane * k1)]);
+  }
+  __syncwarp();
+  if (lane < X750_L) {
+#pragma unroll
+    for (int k1 = 0; k1 < X750_M; ++k1) S[k1 * X750_RS + lane] = v[k1];
+  }
+  __syncwarp();
+  // DFT30 of row r = lane as 2 x DFT15 (even / odd l), read straight into the two halves
+  double2 e[15], o[15];
+  const int rr = lane < X750_M ? lane : X750_M - 1;
+#pragma unroll
+  for (int m = 0; m < 15; ++m) {
+    e[m] = S[rr * X750_RS + 2 * m];
+    o[m] = S[rr * X750_RS + 2 * m + 1];
+  }
+  __syncwarp();
+  dft15(e);
+  dft15(o);
+  if (lane < X750_M) {
+#pragma unroll
+    for (int k = 0; k < 15; ++k) {
+      const double2 t = k == 0 ? o[0] : cm(o[k], c_w30[k]);
+      S[lane + X750_M * k] = ad(e[k], t);
+      S[lane + X750_M * (k + 15)] = sb(e[k], t);
+    }
+  }
+  __syncwarp();
+}
+
+template <int KIND, bool HALF>
+__global__ void __launch_bounds__(XF_THREADS, 2) k_x750(const XArgs a) {
+  constexpr int N = 750, LSR = X750_LS;
+  constexpr int NIN = KChan<KIND, HALF>::NIN, NOUT = KChan<KIND, HALF>::NOUT;
+  constexpr int NL = NIN > NOUT ? NIN : NOUT, NW = XF_THREADS / 32;
+  extern __shared__ double2 smem[];
+  double2* lines = smem;          // [NL][LSR]
+  double2* tw = smem + NL * LSR;  // pd8-padded W750^i
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int i = tid; i < N; i += blockDim.x) tw[pd8(i)] = a.tw[i];
+  const int n_items = a.py * a.nzh;
+  const int p[3] = {a.px, a.py, a.pz};
+  for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+    const int ky = item / a.nzh;
+    const int kzl = item - ky * a.nzh, kz = a.kz0 + kzl;
+    __syncthreads();
+    for (int c = warp; c < NIN; c += NW) {
+      double2 v[X750_M];
+      const double2* src = a.B + c * a.ch_stride + (int64_t)ky * a.nx * a.nzh + kzl;
+#pragma unroll
+      for (int j = 0; j < X750_M; ++j) {
+        const int x = lane + X750_L * j;
+        v[j] = (lane < X750_L && x < a.nx) ? src[(int64_t)x * a.nzh] : make_double2(0.0, 0.0);
+      }
+      warp_fft750(v, lines + c * LSR, tw, lane);
+    }
+    __syncthreads();
+    for (int kx = tid; kx < N; kx += blockDim.x) {
+      const int64_t ti = ((int64_t)ky * a.nzh + kzl) * N + kx;
+      const double tB = (KIND == HS_ROTLET) ? 0.0 : a.tabB[ti];
+      const double tH = (KIND == HS_ROTLET || HALF) ? a.tabH[ti] : 0.0;
+      double2* col = lines + kx;
+      if (2 * kx == N || 2 * ky == a.py || 2 * kz == a.pz) {
+        scale_nyquist<KIND, HALF>(col, LSR, kx, ky, kz, p, a.kscale, a.ka, a.kb, a.inv_n, tB, tH);
+        continue;
+      }
+      cplx C[NIN], outc[6];
+#pragma unroll
+      for (int c = 0; c < NIN; ++c) {
+        const double2 vv = col[c * LSR];
+        C[c] = {vv.x, vv.y};
+      }
+      const double s8 = 1.0 / (8.0 * kPi), s4 = 1.0 / (4.0 * kPi);
+      const double kxv = kval(kx, N, a.kscale[0]), kyv = kval(ky, a.py, a.kscale[1]), kzv = kval(kz, a.pz, a.kscale[2]);
+      const double k2 = kxv * kxv + kyv * kyv + kzv * kzv;
+      const double E = exp(-a.ka * k2);
+      const double G = (KIND == HS_ROTLET) ? tH * E * s4 * a.inv_n : tB * E * (1.0 + a.kb * k2) * s8 * a.inv_n;
+      const double Fc = HALF ? tH * E * s4 * a.inv_n : 0.0;
+      apply_multiplier<KIND, HALF>(kxv, kyv, kzv, G, Fc, C, outc);
+#pragma unroll
+      for (int o = 0; o < NOUT; ++o) col[o * LSR] = make_double2(outc[o].re, -outc[o].im);
+    }
+    __syncthreads();
+    for (int o = warp; o < NOUT; o += NW) {
+      double2 v[X750_M];
+      double2* S = lines + o * LSR;
+#pragma unroll
+      for (int j = 0; j < X750_M; ++j) v[j] = lane < X750_L ? S[lane + X750_L * j] : make_double2(0.0, 0.0);
+      warp_fft750(v, S, tw, lane);
+      double2* dst = a.B + o * a.ch_stride + (int64_t)ky * a.nx * a.nzh + kzl;
+      for (int x = lane; x < a.nx; x += 32) {
+        const double2 w = S[x];
+        dst[(int64_t)x * a.nzh] = make_double2(w.x, -w.y);
+      }
+    }
+  }
+}
+
+template <int KIND, bool HALF>
+static hs_status launch_x750_t(hs_ctx* ctx, const XArgs& a) {
+  HS_TRY(xreg_constants());
+  constexpr int NL = KChan<KIND, HALF>::NIN > KChan<KIND, HALF>::NOUT ? KChan<KIND, HALF>::NIN : KChan<KIND, HALF>::NOUT;
+  const size_t smem = sizeof(double2) * ((size_t)NL * X750_LS + padded_line(750));
+  auto kern = k_x750<KIND, HALF>;
+  HS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per_sm = 0;
+  HS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, XF_THREADS, smem));
+  const int items = a.py * a.nzh;
+  const int grid = std::max(1, std::min(items, ctx->sm_count * std::max(per_sm, 1) * 8));
+  kern<<<grid, XF_THREADS, smem, ctx->stream>>>(a);
+  HS_LAUNCHED(ctx);
+  return HS_OK;
+}
+
 template <int KIND, bool HALF, int M>
 static hs_status launch_xreg_t(hs_ctx* ctx, const XArgs& a) {
   HS_TRY(xreg_constants());
@@ -817,7 +967,11 @@ static hs_status launch_xfused_half(hs_ctx* ctx, const XArgs& a) {
       if (!stockham) return launch_xreg_t<KIND, true, 15>(ctx, a);
       return launch_xfused_t<KIND, true, KB, FixedFFT<8, 4, 3, 5>>(ctx, a);
     }
-    case 750: return launch_xfused_t<KIND, true, KB, FixedFFT<2, 3, 5, 5, 5>>(ctx, a);
+    case 750: {
+      static const bool stockham = getenv("HS_XSTAGE_STOCKHAM") != nullptr;
+      if (!stockham) return launch_x750_t<KIND, true>(ctx, a);
+      return launch_xfused_t<KIND, true, KB, FixedFFT<2, 3, 5, 5, 5>>(ctx, a);
+    }
     case 864: {
       static const bool stockham = getenv("HS_XSTAGE_STOCKHAM") != nullptr;
       if (!stockham) return launch_xreg_t<KIND, true, 27>(ctx, a);

@@ -1,5 +1,5 @@
 """Fourier part of a 1e5-source system on the grid of M (192 -> FFT length 480, 128 -> 352,
-384 with L=2 -> 864) with the current FFT stages; saves the velocities to argv[1] (compares stage
+320 -> 750, 384 with L=2 -> 864) with the current FFT stages; saves the velocities to argv[1] (compares stage
 variants selected by environment variables).  Usage: xstage_ab.py OUT.npy KIND M"""
 import os
 import sys
@@ -20,5 +20,5 @@ if M == 384:
 else:
     s, _ = make_system({"stokeslet": "HL", "rotlet": "cfg4", "stresslet": "cfg3"}[kind], n=100_000)
     g = hs.GridSpec(L=1.0, M=M, P=24, xi=0.26 * M)
-assert g.padded_dims[0] in (480, 352, 864), g.padded_dims
+assert g.padded_dims[0] in (480, 352, 864, 750), g.padded_dims
 np.save(sys.argv[1], hs.fourier_space_sum(s, g).velocities)
