@@ -912,8 +912,82 @@ __global__ void __launch_bounds__(256, M == 27 ? 1 : 2) k_ystage(const double2* 
   }
 }
 
+// y stage for 750-point lines (cfg4): same row staging as k_ystage, the column FFT by
+// warp_fft750 (its natural-order result is read back from the warp's scratch into registers
+// before the buffer collects the output rows)
+template <bool FWD>
+__global__ void __launch_bounds__(256, 1) k_ystage750(const double2* __restrict__ in, double2* __restrict__ out,
+                                                      const double2* __restrict__ twg, int nx, int nzh, int ny) {
+  constexpr int N = 750, NR = (N + 31) / 32;
+  extern __shared__ double2 smem[];
+  double2* buf = smem;             // [N rows][YS_RS]; later per-warp FFT scratch (8 x X750_LS)
+  double2* tw = smem + N * YS_RS;  // pd8-padded twiddles
+  static_assert(8 * X750_LS <= N * YS_RS, "scratch fits the row buffer");
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int i = tid; i < N; i += blockDim.x) tw[pd8(i)] = twg[i];
+  const int nkb = (nzh + YS_KB - 1) / YS_KB;
+  const int n_items = nx * nkb;
+  const int rows_in = FWD ? ny : N, rows_out = FWD ? N : ny;
+  const int64_t rstride = (int64_t)nx * nzh;
+  double2* pre = tw + padded_line(N);  // [ny][YS_RS] (FWD)
+  auto load_rows = [&](int it, double2* dst) {
+    if (it < n_items) {
+      const int x2 = it / nkb, k02 = (it - x2 * nkb) * YS_KB;
+      const int kb2 = min(YS_KB, nzh - k02);
+      const int64_t b2 = (int64_t)x2 * nzh + k02;
+      for (int i = tid; i < rows_in * YS_KB; i += blockDim.x) {
+        const int row = i / YS_KB, k = i - row * YS_KB;
+        if (k < kb2) cp_async16(&dst[row * YS_RS + k], in + b2 + row * rstride + k);
+      }
+    }
+    cp_async_commit();
+  };
+  if (FWD) load_rows(blockIdx.x, pre);
+  for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+    const int x = item / nkb, kz0 = (item - x * nkb) * YS_KB;
+    const int kbn = min(YS_KB, nzh - kz0);
+    const int64_t base = (int64_t)x * nzh + kz0;
+    __syncthreads();
+    if (!FWD) load_rows(item, buf);
+    cp_async_wait_all();
+    __syncthreads();
+    const double2* src = FWD ? pre : buf;
+    double2 v[X750_M];
+#pragma unroll
+    for (int j = 0; j < X750_M; ++j) {
+      const int row = lane + X750_L * j;
+      double2 e = (lane < X750_L && row < rows_in) ? src[row * YS_RS + warp] : make_double2(0.0, 0.0);
+      if (!FWD) e.y = -e.y;
+      v[j] = e;
+    }
+    __syncthreads();  // every column read: the buffer becomes FFT scratch
+    if (FWD) load_rows(item + gridDim.x, pre);
+    double2* S = buf + warp * X750_LS;
+    warp_fft750(v, S, tw, lane);
+    double2 res[NR];
+#pragma unroll
+    for (int i = 0; i < NR; ++i) {
+      const int k = lane + 32 * i;
+      res[i] = k < N ? S[k] : make_double2(0.0, 0.0);
+    }
+    __syncthreads();  // scratch use finished: the buffer collects the output rows
+#pragma unroll
+    for (int i = 0; i < NR; ++i) {
+      const int row = lane + 32 * i;
+      double2 e = res[i];
+      if (!FWD) e.y = -e.y;
+      if (row < rows_out) buf[row * YS_RS + warp] = e;
+    }
+    __syncthreads();
+    for (int i = tid; i < rows_out * YS_KB; i += blockDim.x) {
+      const int row = i / YS_KB, k = i - row * YS_KB;
+      if (k < kbn) out[base + row * rstride + k] = buf[row * YS_RS + k];
+    }
+  }
+}
+
 // y stage of one channel; false when the length has no register kernel (caller uses cuFFT)
-bool ystage_supported(int py) { return py == 480 || py == 352 || py == 864; }
+bool ystage_supported(int py) { return py == 480 || py == 352 || py == 864 || py == 750; }
 hs_status launch_ystage(hs_ctx* ctx, bool fwd, const double2* in, double2* out, const double2* tw, int py, int nx,
                         int nzh, int ny) {
   HS_TRY(xreg_constants());
@@ -930,6 +1004,16 @@ hs_status launch_ystage(hs_ctx* ctx, bool fwd, const double2* in, double2* out, 
   if (py == 480) return fwd ? go(k_ystage<15, true>, 15) : go(k_ystage<15, false>, 15);
   if (py == 352) return fwd ? go(k_ystage<11, true>, 11) : go(k_ystage<11, false>, 11);
   if (py == 864) return fwd ? go(k_ystage<27, true>, 27) : go(k_ystage<27, false>, 27);
+  if (py == 750) {
+    const size_t smem = sizeof(double2) * ((size_t)750 * YS_RS + padded_line(750) + (fwd ? (size_t)ny * YS_RS : 0));
+    auto kern = fwd ? k_ystage750<true> : k_ystage750<false>;
+    HS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const int items = nx * ((nzh + YS_KB - 1) / YS_KB);
+    const int grid = std::max(1, std::min(items, ctx->sm_count * 8));
+    kern<<<grid, 256, smem, ctx->stream>>>(in, out, tw, nx, nzh, ny);
+    HS_LAUNCHED(ctx);
+    return HS_OK;
+  }
   return fail(HS_ERR_PARAMETER, "y stage: unsupported length");
 }
 
