@@ -246,9 +246,16 @@ __device__ __forceinline__ double exact_r2(double d0, double d1, double d2) {
 // its own target (no cross-lane reductions, no atomics, deterministic order).
 constexpr int PC_WARPS = 4;
 constexpr int PC_TG = PC_WARPS * 32;  // targets per work item
-constexpr int PC_H = 128;             // candidates per chunk
+// candidates per chunk (a multiple of PC_TG, a power of two): the stokeslet stages 256 per
+// barrier pair (2 per thread) in a 2-chunk ring; the larger stresslet / rotlet records keep
+// 128-candidate chunks in a 3-chunk ring (4 CTAs per SM either way)
+#ifndef PC_H_STOKESLET
+#define PC_H_STOKESLET 256
+#endif
+template <int KIND>
+constexpr int pc_h() { return KIND == HS_STOKESLET ? PC_H_STOKESLET : 128; }
 #ifndef PC_NH_STOKESLET
-#define PC_NH_STOKESLET 4
+#define PC_NH_STOKESLET 2
 #endif
 #ifndef PC_NH_OTHER
 #define PC_NH_OTHER 3
@@ -281,6 +288,8 @@ template <int KIND, bool HALF>
 __global__ void __launch_bounds__(PC_TG, PC_MINB) k_pair_q(const PairArgs a) {
   // Candidate rows as 16-byte columns: the evaluation reads them at lane-random rows, and a
   // 16-byte array spreads those reads over 8 bank groups (a 32-byte row only over 4).
+  constexpr int PC_H = pc_h<KIND>(), PC_PER = PC_H / PC_TG;
+  constexpr int PC_HSHIFT = PC_H == 128 ? 7 : (PC_H == 256 ? 8 : 9);
   constexpr int PC_K = pc_nh<KIND>() * PC_H;  // staged candidates (dynamic shared memory)
   constexpr bool kNeedB = (KIND == HS_STRESSLET) || (KIND == HS_ROTLET && HALF);
   extern __shared__ __align__(16) unsigned char pc_dyn[];
@@ -403,10 +412,13 @@ __global__ void __launch_bounds__(PC_TG, PC_MINB) k_pair_q(const PairArgs a) {
         }
     }
     // stride permutation, incrementally: thread tid stages v = ((c0 + tid) * pstride) mod ncand,
-    // and c0 advances by PC_H per chunk (PC_H == PC_TG: one candidate per thread per chunk)
-    static_assert(PC_H == PC_TG, "one staged candidate per thread per chunk");
+    // and c0 advances by PC_H per chunk (PC_PER candidates per thread per chunk)
+    static_assert(PC_H % PC_TG == 0 && (1 << PC_HSHIFT) == PC_H, "chunk = whole CTA rounds, power of two");
     const int vstep = (int)(((long long)PC_H * pstride) % max(ncand, 1));
-    int vcur = (int)(((long long)threadIdx.x * pstride) % max(ncand, 1));
+    int vcur[PC_PER];
+#pragma unroll
+    for (int k = 0; k < PC_PER; ++k)
+      vcur[k] = (int)(((long long)(threadIdx.x + k * PC_TG) * pstride) % max(ncand, 1));
     auto pop_eval = [&]() {
       const int jj = q[head & (PC_Q - 1)][lane];
       ++head;
@@ -436,16 +448,17 @@ __global__ void __launch_bounds__(PC_TG, PC_MINB) k_pair_q(const PairArgs a) {
     for (int c = 0, c0 = 0; c0 < ncand; ++c, c0 += PC_H) {
       const int h = c % pc_nh<KIND>(), hb = h * PC_H;
       // drain the (oldest) entries that still reference half h
-      while (__any_sync(0xffffffffu, tail > head && (q[head & (PC_Q - 1)][lane] >> 7) == h)) {
-        if (tail > head && (q[head & (PC_Q - 1)][lane] >> 7) == h) pop_eval();
+      while (__any_sync(0xffffffffu, tail > head && (q[head & (PC_Q - 1)][lane] >> PC_HSHIFT) == h)) {
+        if (tail > head && (q[head & (PC_Q - 1)][lane] >> PC_HSHIFT) == h) pop_eval();
       }
       __syncthreads();
-      {
-        const int j = threadIdx.x;
+#pragma unroll
+      for (int kk = 0; kk < PC_PER; ++kk) {
+        const int j = threadIdx.x + kk * PC_TG;
         const int v0 = c0 + j;
-        const int v = vcur;
-        vcur += vstep;
-        if (vcur >= ncand) vcur -= ncand;
+        const int v = vcur[kk];
+        vcur[kk] += vstep;
+        if (vcur[kk] >= ncand) vcur[kk] -= ncand;
         if (v0 < ncand) {
           // stride permutation of the candidate list: every chunk samples the whole
           // neighbourhood, so each lane's acceptance rate per chunk is about its average
@@ -632,7 +645,7 @@ hs_status launch_pair(hs_ctx* ctx, const PairArgs& a) {
   const int grid = std::max(1, std::min(a.max_items, ctx->sm_count * 16));
 #define HS_PAIR_CASE(K, H)                                                                         \
   do {                                                                                             \
-    const int dyn = pc_nh<K>() * PC_H * pc_rec_bytes<K, H>();                                      \
+    const int dyn = pc_nh<K>() * pc_h<K>() * pc_rec_bytes<K, H>();                                 \
     HS_CUDA(cudaFuncSetAttribute(k_pair_q<K, H>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn)); \
     k_pair_q<K, H><<<grid, PC_TG, dyn, ctx->stream>>>(a);                                           \
   } while (0)
