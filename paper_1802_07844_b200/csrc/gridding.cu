@@ -1555,7 +1555,14 @@ __global__ void __launch_bounds__(256, 2) k_gather5(const double4* __restrict__ 
 // broadcast reads).  The z factor is applied once at the end, u_t,c = sum_l wz_t(z_l)
 // E_l[t][c] (warp reduction).  The x/y factors of a run live in warp-private tables.
 // Windows are evaluated directly, exp(-alpha d^2), as in the reference (_gridding.py:21-30).
-constexpr int G7_TG = 8, G7_GW = 32, G7_WARPS = 4, G7_ZC = 96, G7_STEP = 2, G7_R = 3 * G7_STEP;
+#ifndef G7_STEP_DEF
+#define G7_STEP_DEF 4
+#endif
+#ifndef G7_ZC_DEF
+#define G7_ZC_DEF 48
+#endif
+// columns per barrier step (G7_STEP) and ring slots (3 steps in flight), static shared memory
+constexpr int G7_TG = 8, G7_GW = 32, G7_WARPS = 4, G7_ZC = G7_ZC_DEF, G7_STEP = G7_STEP_DEF, G7_R = 3 * G7_STEP;
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
@@ -1751,22 +1758,22 @@ __global__ void __launch_bounds__(G7_WARPS * 32, 2) k_gather7(const double4* __r
 #pragma unroll
         for (int c = 0; c < NCH; ++c) E[tt][c] = fma(cxy[tt], v[c], E[tt][c]);
     };
-    static_assert(G7_STEP == 2, "the step loop below handles two columns");
-    const int nfull = ncol / G7_STEP;
+    const int nfull = ncol / G7_STEP, nrem = ncol - nfull * G7_STEP;
     for (int sidx = 0; sidx < nfull; ++sidx) {
       cp_async_wait<1>();
       __syncthreads();
       issue_step(sidx + 2);
       if (amask) {
-        column(slot);
-        column(slot + 1);
+#pragma unroll
+        for (int j = 0; j < G7_STEP; ++j) column(slot + j);
       }
-      slot = slot + 2 == G7_R ? 0 : slot + 2;
+      slot = slot + G7_STEP == G7_R ? 0 : slot + G7_STEP;
     }
-    if (ncol & 1) {  // ragged last step: one column (already issued)
+    if (nrem) {  // ragged last step (already issued)
       cp_async_wait<1>();
       __syncthreads();
-      if (amask) column(slot);
+      if (amask)
+        for (int j = 0; j < nrem; ++j) column(slot + j);
     }
     cp_async_wait<0>();
     if (amask) {
