@@ -426,7 +426,7 @@ __global__ void __launch_bounds__((NCW + SW_NP) * 32, NCW == 8 ? 2 : 1) k_spread
                                                        int nby, int nbz, double* __restrict__ grids) {
   constexpr int RX = SW_RX, RY = SW_RY, RZ = SW_RZ, RQ = SwBuf<NCH>::RQ, PER = SwBuf<NCH>::DOUBLES;
   extern __shared__ __align__(16) double sm_dyn[];
-  constexpr int K = NCW == 16 ? 16 : SW_K;  // ring depth
+  constexpr int K = NCW == 16 ? 16 * 32 / SW_CH : SW_K;  // ring depth (16 slots of 32 sources)
   constexpr int PY = 64 / NCW, RB = PY / 2;  // warp patch rows, row blocks of 8 positions
   constexpr int PB = NCW;                    // mask bit of the window-slice parities
   __shared__ __align__(8) uint64_t full_bar[K], empty_bar[K];
@@ -1009,7 +1009,7 @@ hs_status launch_spread(hs_ctx* ctx, const double4* pts, const double* w, int n,
         switch (cn) {
 #define HS_SP16(N)                                                                                                 \
   case N: {                                                                                                        \
-    const size_t smm = sizeof(double) * 16 * SwBuf<N>::DOUBLES;                                                    \
+    const size_t smm = sizeof(double) * (16 * 32 / SW_CH) * SwBuf<N>::DOUBLES;                                     \
     HS_CUDA(cudaFuncSetAttribute(k_spread_mma4<N, false, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize,        \
                                  (int)smm));                                                                       \
     k_spread_mma4<N, false, 16><<<grid, (16 + SW_NP) * 32, smm, ctx->stream>>>(lo, tab, wt, pts, wc0, nch,         \
