@@ -244,7 +244,10 @@ __device__ __forceinline__ double exact_r2(double d0, double d1, double d2) {
 // whenever >= 3/4 of its lanes have work, so the erfc/exp-heavy evaluation
 // runs with nearly full SIMT utilisation while every thread accumulates only
 // its own target (no cross-lane reductions, no atomics, deterministic order).
-constexpr int PC_WARPS = 4;
+#ifndef PC_WARPS_DEF
+#define PC_WARPS_DEF 4
+#endif
+constexpr int PC_WARPS = PC_WARPS_DEF;
 constexpr int PC_TG = PC_WARPS * 32;  // targets per work item
 // candidates per chunk (a multiple of PC_TG, a power of two): the stokeslet stages 256 per
 // barrier pair (2 per thread) in a 2-chunk ring; the larger stresslet / rotlet records keep
@@ -253,7 +256,7 @@ constexpr int PC_TG = PC_WARPS * 32;  // targets per work item
 #define PC_H_STOKESLET 256
 #endif
 template <int KIND>
-constexpr int pc_h() { return KIND == HS_STOKESLET ? PC_H_STOKESLET : 128; }
+constexpr int pc_h() { return KIND == HS_STOKESLET ? PC_H_STOKESLET : (PC_TG > 128 ? PC_TG : 128); }
 #ifndef PC_NH_STOKESLET
 #define PC_NH_STOKESLET 2
 #endif
