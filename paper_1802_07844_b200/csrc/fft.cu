@@ -838,9 +838,17 @@ static hs_status launch_xreg_t(hs_ctx* ctx, const XArgs& a) {
 // written (output pruning); in place.
 constexpr int YS_KB = 8, YS_RS = YS_KB + 1;  // kz per CTA, padded row length (bank spread)
 
+#ifndef YS_INV_PREFETCH
+#define YS_INV_PREFETCH 0
+#endif
+// PRE: the next item's input rows are prefetched into a separate staging area (always for the
+// forward transform, whose ny input rows fit next to the row buffer at two CTAs per SM; for the
+// inverse, all py rows, only with YS_INV_PREFETCH=1 at one CTA per SM)
 template <int M, bool FWD>
-__global__ void __launch_bounds__(256, M == 27 ? 1 : 2) k_ystage(const double2* __restrict__ in, double2* __restrict__ out,
-                                                  const double2* __restrict__ twg, int nx, int nzh, int ny) {
+__global__ void __launch_bounds__(256, (M == 27 || (!FWD && YS_INV_PREFETCH)) ? 1 : 2)
+    k_ystage(const double2* __restrict__ in, double2* __restrict__ out, const double2* __restrict__ twg, int nx,
+             int nzh, int ny) {
+  constexpr bool PRE = FWD || YS_INV_PREFETCH;
   constexpr int N = 32 * M;
   extern __shared__ double2 smem[];
   double2* buf = smem;              // [N rows][YS_RS]; later per-warp transpose scratch (8 x M*33)
@@ -856,7 +864,7 @@ __global__ void __launch_bounds__(256, M == 27 ? 1 : 2) k_ystage(const double2* 
   // forward: the next item's ny input rows are prefetched into a separate staging area (pre)
   // while the current item is transformed and written (the inverse reads all N rows; its
   // staging would not fit two CTAs per SM)
-  double2* pre = tw + padded_line(N);  // [ny][YS_RS] (FWD)
+  double2* pre = tw + padded_line(N);  // [rows_in][YS_RS] (PRE)
   auto load_rows = [&](int it, double2* dst) {
     if (it < n_items) {
       const int x2 = it / nkb, k02 = (it - x2 * nkb) * YS_KB;
@@ -869,16 +877,16 @@ __global__ void __launch_bounds__(256, M == 27 ? 1 : 2) k_ystage(const double2* 
     }
     cp_async_commit();
   };
-  if (FWD) load_rows(blockIdx.x, pre);
+  if (PRE) load_rows(blockIdx.x, pre);
   for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
     const int x = item / nkb, kz0 = (item - x * nkb) * YS_KB;
     const int kbn = min(YS_KB, nzh - kz0);
     const int64_t base = (int64_t)x * nzh + kz0;
     __syncthreads();  // previous item done with buf
-    if (!FWD) load_rows(item, buf);
+    if (!PRE) load_rows(item, buf);
     cp_async_wait_all();
     __syncthreads();
-    const double2* src = FWD ? pre : buf;
+    const double2* src = PRE ? pre : buf;
     double2 v[M], o16[RegFFT<M>::NG][16];
 #pragma unroll
     for (int j = 0; j < M; ++j) {
@@ -888,7 +896,7 @@ __global__ void __launch_bounds__(256, M == 27 ? 1 : 2) k_ystage(const double2* 
       v[j] = e;
     }
     __syncthreads();  // every column read: the buffer becomes transpose scratch
-    if (FWD) load_rows(item + gridDim.x, pre);
+    if (PRE) load_rows(item + gridDim.x, pre);
     warp_fft_reg<M>(v, buf + warp * M * 33, tw, lane, o16);
     __syncthreads();  // scratch use finished: the buffer collects the output rows
 #pragma unroll
@@ -993,7 +1001,8 @@ hs_status launch_ystage(hs_ctx* ctx, bool fwd, const double2* in, double2* out, 
   HS_TRY(xreg_constants());
   auto go = [&](auto kern, int M) -> hs_status {
     const size_t smem = sizeof(double2) * ((size_t)32 * M * YS_RS + padded_line(32 * M) +
-                                           (fwd ? (size_t)ny * YS_RS : 0));  // + forward prefetch rows
+                                           (fwd ? (size_t)ny * YS_RS
+                                                : (YS_INV_PREFETCH ? (size_t)32 * M * YS_RS : 0)));  // prefetch rows
     HS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int items = nx * ((nzh + YS_KB - 1) / YS_KB);
     const int grid = std::max(1, std::min(items, ctx->sm_count * 2 * 8));
