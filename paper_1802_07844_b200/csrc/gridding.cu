@@ -399,7 +399,10 @@ constexpr int SW_CH = SW_CH_DEF, SW_K = SW_K_DEF, SW_H = SW_CH_DEF / 32, SW_RX =
 // producer warps (8, 9, ...): producer p stages the chunks c = p mod SW_NP, so the SW_K ring
 // slots of one producer are fixed (SW_K % SW_NP == 0) and one warp's staging rate no longer
 // bounds the eight consumers
-constexpr int SW_NP = 2, SW_THREADS = (8 + SW_NP) * 32;
+#ifndef SW_NP_DEF
+#define SW_NP_DEF 2
+#endif
+constexpr int SW_NP = SW_NP_DEF, SW_THREADS = (8 + SW_NP) * 32;
 static_assert(SW_K % SW_NP == 0, "ring slots must divide among the producers");
 template <int NCH>
 struct SwBuf {
