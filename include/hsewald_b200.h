@@ -47,6 +47,11 @@ typedef enum {
 
 enum { HS_MEM_DEVICE = 0, HS_MEM_HOST = 1 };
 enum { HS_STOKESLET = 0, HS_STRESSLET = 1, HS_ROTLET = 2 };   /* _KIND_ID, ewald_real.py:29 */
+/* Mixed stokeslet + stresslet sources sharing one set of positions (BASELINE configs[4]):
+ * one evaluation equals the sum of the reference's two ewald_sum calls (ref:ewald.py:46-80),
+ * with the two kinds' kernel and wall channels summed in k-space before the inverse
+ * transforms.  Strengths: sa = f (n,3), sb = [g | q] (n,6) rows g0 g1 g2 q0 q1 q2. */
+enum { HS_MIXED = 3 };
 enum { HS_FREE = 0, HS_HALF = 1 };                            /* system.py:25-27 */
 enum { HS_HARMONIC = 0, HS_BIHARMONIC = 1 };                  /* _KIND_BYTE, ewald_fourier.py:40 */
 
@@ -137,6 +142,16 @@ hs_status hs_plan_execute(hs_plan* plan, const double* positions, const double* 
 /* Real-space parts of the last execute (ewald_real.py:450-452 `parts`): kernel
  * uk/(8pi|4pi) and correction uc/(4pi), each (n_targets,3). */
 hs_status hs_plan_real_parts(hs_plan* plan, double* kernel_part, double* correction_part, int mem);
+
+/* Neighbour audit of the real-space pair pass (ewald_real.py:277-299): evaluates the
+ * real-space part for the given inputs (same arguments as hs_plan_execute) and writes, per
+ * target, [accepted pairs, accepted image pairs, sum over the accepted combined source ids j
+ * (j >= n: image of j - n) of splitmix64(j) mod 2^64] into audit (n_targets x 3 uint64).
+ * The reference keeps a pair when ids[p] != tcols[t] and r2 = d0*d0 + d1*d1 + d2*d2 <= rc^2
+ * over the 5x5x5 half-cells around the target's cell; the audit proves the CUDA pass keeps
+ * exactly those sets (tests/test_gpu_parity.py, against oracle/ and tests/golden/). */
+hs_status hs_plan_pair_audit(hs_plan* plan, const double* positions, const double* sa, const double* sb,
+                             const double* targets, const int64_t* tcols, uint64_t* audit, int mem);
 
 /* Number of forward / inverse 3-D transforms one execute performs. */
 hs_status hs_plan_fft_counts(const hs_plan* plan, int* n_fft, int* n_ifft);

@@ -19,7 +19,7 @@ from .errors import DeviceError, raise_for_status
 LIB_PATH = os.environ.get("HSEWALD_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libhsewald_b200.so")
 
 HS_MEM_DEVICE, HS_MEM_HOST = 0, 1
-KIND_ID = {"stokeslet": 0, "stresslet": 1, "rotlet": 2}
+KIND_ID = {"stokeslet": 0, "stresslet": 1, "rotlet": 2, "mixed": 3}
 GEOM_ID = {"free": 0, "half": 1}
 TABLE_ID = {"harmonic": 0, "biharmonic": 1}
 
@@ -71,6 +71,8 @@ _SIGS = [
                                   C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int, _dp]),
     ("hs_plan_real_parts", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int]),
     ("hs_plan_fft_counts", C.c_int, [C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    ("hs_plan_pair_audit", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                     C.c_void_p, C.c_int]),
     ("hs_plan_create_slab", C.c_int, [C.c_void_p, C.POINTER(HsParams), C.POINTER(HsSlab), C.POINTER(C.c_void_p)]),
     ("hs_slab_sizes", C.c_int, [C.c_void_p, _i64p]),
     ("hs_slab_begin", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int,

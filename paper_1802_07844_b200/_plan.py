@@ -60,6 +60,7 @@ class Evaluator:
         p.n_targets = self.n_targets
         p.targets_are_sources = 1 if self.targets_are_sources else 0
         self.params = p
+        self._b_cols = 6 if kind == "mixed" else 3   # mixed: sb rows are [g | q]
         h = C.c_void_p()
         if slab is None:
             _lib.check(self.lib.hs_plan_create(self.ctx.handle, C.byref(p), C.byref(h)))
@@ -125,10 +126,11 @@ class Evaluator:
             return self._execute_torch(positions, sa, sb, targets, tcols, what, times, out)
         pos = _host_f64(positions)
         a = _host_f64(sa)
-        b = _host_f64(sb) if sb is not None else None
+        b = _host_f64(sb, self._b_cols) if sb is not None else None
         nt = self.n_targets
         tg = _host_f64(targets) if targets is not None else None
         tc = np.ascontiguousarray(np.asarray(tcols, dtype=np.int64)) if tcols is not None else None
+        self._check_rows(pos, a, b, tg, tc)
         if out is not None:   # caller-provided (e.g. pinned) host buffers; parts may be None
             u, ur, uf = out
         else:
@@ -140,9 +142,60 @@ class Evaluator:
         _lib.check(st)
         return u, ur, uf, dict(zip(TIME_KEYS, list(times)))
 
+    def pair_audit(self, positions, sa, sb=None, targets=None, tcols=None):
+        """Per-target neighbour audit of the real-space pass (hs_plan_pair_audit): uint64
+        (n_targets, 3) = [accepted pairs, accepted image pairs, sum of splitmix64(id) mod 2^64]."""
+        pos = _host_f64(positions)
+        a = _host_f64(sa)
+        b = _host_f64(sb, self._b_cols) if sb is not None else None
+        tg = _host_f64(targets) if targets is not None else None
+        tc = np.ascontiguousarray(np.asarray(tcols, dtype=np.int64)) if tcols is not None else None
+        self._check_rows(pos, a, b, tg, tc)
+        out = np.zeros((self.n_targets, 3), dtype=np.uint64)
+        vp = lambda x: x.ctypes.data_as(C.c_void_p) if x is not None else None  # noqa: E731
+        self.ctx.bind_stream(None)
+        _lib.check(self.lib.hs_plan_pair_audit(self.handle, vp(pos), vp(a), vp(b), vp(tg), vp(tc), vp(out),
+                                               _lib.HS_MEM_HOST))
+        return out
+
+    def _check_rows(self, pos, a, b, tg, tc):
+        if pos.shape[0] != self.n or a.shape[0] != self.n or (b is not None and b.shape[0] != self.n):
+            raise ParameterError(f"plan expects {self.n} sources")
+        if self.kind != "stokeslet" and b is None:
+            raise ParameterError(f"{self.kind} needs q")
+        if not self.targets_are_sources:
+            if tg is None or tg.shape[0] != self.n_targets:
+                raise ParameterError(f"plan expects {self.n_targets} targets")
+            if tc is not None and tc.shape != (self.n_targets,):
+                raise ParameterError("target_indices must have one entry per target")
+
+    def _check_torch(self, dev, **tensors):
+        """Device inputs are passed to the kernels as raw pointers: dtype, layout, device and row
+        count must match exactly (float64 (rows,3) / int64 (rows,), contiguous, on the plan's device)."""
+        import torch
+        rows = {"positions": self.n, "sa": self.n, "sb": self.n, "targets": self.n_targets,
+                "tcols": self.n_targets}
+        for name, t in tensors.items():
+            if t is None:
+                continue
+            want = torch.int64 if name == "tcols" else torch.float64
+            shape = (rows[name],) if name == "tcols" else (rows[name], self._b_cols if name == "sb" else 3)
+            if not isinstance(t, torch.Tensor) or t.dtype != want or not t.is_cuda or t.device != dev \
+                    or tuple(t.shape) != shape or not t.is_contiguous():
+                raise ParameterError(f"{name}: expected a contiguous {want} CUDA tensor of shape {shape} on {dev}, "
+                                     f"got {getattr(t, 'dtype', type(t))} {tuple(getattr(t, 'shape', ()))} "
+                                     f"on {getattr(t, 'device', '?')}")
+        if self.kind != "stokeslet" and tensors.get("sb") is None:
+            raise ParameterError(f"{self.kind} needs q")
+        if not self.targets_are_sources and tensors.get("targets") is None:
+            raise ParameterError(f"plan expects {self.n_targets} targets")
+
     def _execute_torch(self, positions, sa, sb, targets, tcols, what, times, out):
         import torch
         dev = positions.device
+        if self.ctx.device is not None and dev.index != self.ctx.device:
+            raise ParameterError(f"inputs on {dev}, plan on cuda:{self.ctx.device}")
+        self._check_torch(dev, positions=positions, sa=sa, sb=sb, targets=targets, tcols=tcols)
         nt = self.n_targets
         if out is None:
             out = torch.empty((3, nt, 3), dtype=torch.float64, device=dev)

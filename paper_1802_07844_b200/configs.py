@@ -40,7 +40,9 @@ WORKLOADS = {
     "cfg4": Workload("cfg4", "rotlet", 1_000_000, 1.0, 83.2, 0.0555, 320, 24, 1004, zdist="wall_exp"),
     # the metric's configuration: half-space stokeslet, N = 1e6
     "HL": Workload("HL", "stokeslet", 1_000_000, 1.0, 49.92, 0.101, 192, 24, 1000),
-    "cfg5": Workload("cfg5", "stokeslet", 4_000_000, 2.0, 49.92, 0.10, 384, 24, 1005, separate_targets=True),
+    # BASELINE configs[4]: stokeslet + stresslet sources at the same 4e6 points, 4e6 separate targets,
+    # L = 2 (the multi-GPU scaling case); one mixed plan (ewald.ewald_sum_mixed)
+    "cfg5": Workload("cfg5", "mixed", 4_000_000, 2.0, 49.92, 0.10, 384, 24, 1005, separate_targets=True),
 }
 
 
@@ -49,7 +51,8 @@ def _unit(v):
 
 
 def make_system(w: Workload | str, n: int | None = None):
-    """Return (PointSystem, targets or None) for a workload (optionally with fewer points)."""
+    """Return (PointSystem, targets or None) for a workload (optionally with fewer points);
+    kind "mixed" returns an ewald.MixedSystem (stokeslet f, stresslet g / q at the same points)."""
     if isinstance(w, str):
         w = WORKLOADS[w]
     n = w.n if n is None else int(n)
@@ -69,7 +72,15 @@ def make_system(w: Workload | str, n: int | None = None):
     else:
         raise ValueError(w.zdist)
     pos = np.column_stack([x, y, z])
-    if w.kind == "stokeslet":
+    if w.kind == "mixed":
+        from .ewald import MixedSystem
+        f = rng.normal(size=(n, 3))
+        g = rng.normal(size=(n, 3))
+        q = _unit(rng.normal(size=(n, 3)))
+        sysm = MixedSystem(
+            PointSystem(kind="stokeslet", geometry="half", box_length=L, positions=pos, f=f, seed=w.seed),
+            PointSystem(kind="stresslet", geometry="half", box_length=L, positions=pos, g=g, q=q, seed=w.seed))
+    elif w.kind == "stokeslet":
         sysm = PointSystem(kind="stokeslet", geometry="half", box_length=L, positions=pos,
                            f=rng.normal(size=(n, 3)), seed=w.seed)
     elif w.kind == "stresslet":

@@ -245,6 +245,17 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 
+// output store of the x stage: into Bout (the pass's inputs by default), or added to what is
+// there (a.accum: a second channel group's contribution, e.g. the mixed plan's stresslet pass)
+__device__ __forceinline__ void xstore(const XArgs& a, double2* dst, double2 v) {
+  if (a.accum) {
+    const double2 o = *dst;
+    v.x += o.x;
+    v.y += o.y;
+  }
+  *dst = v;
+}
+
 template <int KIND, bool HALF, int KB, class FFT>
 __global__ void __launch_bounds__(XF_THREADS, 2) k_xfused(const XArgs a) {
   constexpr int NIN = KChan<KIND, HALF>::NIN, NOUT = KChan<KIND, HALF>::NOUT;
@@ -322,12 +333,12 @@ __global__ void __launch_bounds__(XF_THREADS, 2) k_xfused(const XArgs a) {
     // store the x < nx outputs (conjugated back)
     for (int i = tid; i < NOUT * a.nx; i += blockDim.x) {
       const int o = i / a.nx, x = i - o * a.nx;
-      double2* dst = a.B + o * a.ch_stride + ((int64_t)ky * a.nx + x) * a.nzh + kz0;
+      double2* dst = a.Bout + o * a.ch_stride + ((int64_t)ky * a.nx + x) * a.nzh + kz0;
 #pragma unroll
       for (int kb = 0; kb < KB; ++kb) {
         if (kb < kbn) {
           const double2 v = lines[(o * KB + kb) * LS + pd8(x)];
-          dst[kb] = make_double2(v.x, -v.y);
+          xstore(a, &dst[kb], make_double2(v.x, -v.y));
         }
       }
     }
@@ -647,7 +658,7 @@ __global__ void __launch_bounds__(XR_THREADS, M == 27 ? 1 : 2) k_xreg(const XArg
 #pragma unroll
       for (int j = 0; j < M; ++j) v[j] = S[lane + 32 * j];
       warp_fft_reg<M>(v, S, tw, lane, out);
-      double2* dst = a.B + o * a.ch_stride + (int64_t)ky * a.nx * a.nzh + kzl;
+      double2* dst = a.Bout + o * a.ch_stride + (int64_t)ky * a.nx * a.nzh + kzl;
 #pragma unroll
       for (int g = 0; g < RegFFT<M>::NG; ++g) {
         const int rg = r + 16 * g;
@@ -655,7 +666,7 @@ __global__ void __launch_bounds__(XR_THREADS, M == 27 ? 1 : 2) k_xreg(const XArg
 #pragma unroll
           for (int k = 0; k < 16; ++k) {
             const int x = rg + M * (k + 16 * h);
-            if (x < a.nx) dst[(int64_t)x * a.nzh] = make_double2(out[g][k].x, -out[g][k].y);
+            if (x < a.nx) xstore(a, &dst[(int64_t)x * a.nzh], make_double2(out[g][k].x, -out[g][k].y));
           }
         }
       }
@@ -781,10 +792,10 @@ __global__ void __launch_bounds__(XF_THREADS, 2) k_x750(const XArgs a) {
 #pragma unroll
       for (int j = 0; j < X750_M; ++j) v[j] = lane < X750_L ? S[lane + X750_L * j] : make_double2(0.0, 0.0);
       warp_fft750(v, S, tw, lane);
-      double2* dst = a.B + o * a.ch_stride + (int64_t)ky * a.nx * a.nzh + kzl;
+      double2* dst = a.Bout + o * a.ch_stride + (int64_t)ky * a.nx * a.nzh + kzl;
       for (int x = lane; x < a.nx; x += 32) {
         const double2 w = S[x];
-        dst[(int64_t)x * a.nzh] = make_double2(w.x, -w.y);
+        xstore(a, &dst[(int64_t)x * a.nzh], make_double2(w.x, -w.y));
       }
     }
   }
@@ -1046,43 +1057,47 @@ static hs_status launch_xfused_t(hs_ctx* ctx, const XArgs& a) {
 
 // FFT-length specialisations for the BASELINE configurations (cfg1 240, cfg2/3 352,
 // HL 480, cfg4 750, cfg5 864); any other 11-smooth length <= 1024 uses AnyFFT.
-template <int KIND, int KB>
-static hs_status launch_xfused_half(hs_ctx* ctx, const XArgs& a) {
+template <int KIND, bool HALF, int KB>
+static hs_status launch_xfused_len(hs_ctx* ctx, const XArgs& a) {
   switch (a.plan.n) {
-    case 240: return launch_xfused_t<KIND, true, KB, FixedFFT<8, 2, 3, 5>>(ctx, a);
+    case 240: return launch_xfused_t<KIND, HALF, KB, FixedFFT<8, 2, 3, 5>>(ctx, a);
     case 352: {
       static const bool stockham = getenv("HS_XSTAGE_STOCKHAM") != nullptr;
-      if (!stockham) return launch_xreg_t<KIND, true, 11>(ctx, a);
-      return launch_xfused_t<KIND, true, KB, FixedFFT<8, 4, 11>>(ctx, a);
+      if (!stockham) return launch_xreg_t<KIND, HALF, 11>(ctx, a);
+      return launch_xfused_t<KIND, HALF, KB, FixedFFT<8, 4, 11>>(ctx, a);
     }
     case 480: {
       static const bool stockham = getenv("HS_XSTAGE_STOCKHAM") != nullptr;  // previous kernel (comparison)
-      if (!stockham) return launch_xreg_t<KIND, true, 15>(ctx, a);
-      return launch_xfused_t<KIND, true, KB, FixedFFT<8, 4, 3, 5>>(ctx, a);
+      if (!stockham) return launch_xreg_t<KIND, HALF, 15>(ctx, a);
+      return launch_xfused_t<KIND, HALF, KB, FixedFFT<8, 4, 3, 5>>(ctx, a);
     }
     case 750: {
       static const bool stockham = getenv("HS_XSTAGE_STOCKHAM") != nullptr;
-      if (!stockham) return launch_x750_t<KIND, true>(ctx, a);
-      return launch_xfused_t<KIND, true, KB, FixedFFT<2, 3, 5, 5, 5>>(ctx, a);
+      if (!stockham) return launch_x750_t<KIND, HALF>(ctx, a);
+      return launch_xfused_t<KIND, HALF, KB, FixedFFT<2, 3, 5, 5, 5>>(ctx, a);
     }
     case 864: {
       static const bool stockham = getenv("HS_XSTAGE_STOCKHAM") != nullptr;
-      if (!stockham) return launch_xreg_t<KIND, true, 27>(ctx, a);
-      return launch_xfused_t<KIND, true, KB, FixedFFT<8, 4, 3, 3, 3>>(ctx, a);
+      if (!stockham) return launch_xreg_t<KIND, HALF, 27>(ctx, a);
+      return launch_xfused_t<KIND, HALF, KB, FixedFFT<8, 4, 3, 3, 3>>(ctx, a);
     }
-    default: return launch_xfused_t<KIND, true, KB, AnyFFT>(ctx, a);
+    default: return launch_xfused_t<KIND, HALF, KB, AnyFFT>(ctx, a);
   }
 }
 
+// kind HS_MIXED here is the mixed plan's first channel group (stokeslet kernel + shared wall
+// channels, kmult.cuh); its stresslet kernel group runs as HS_STRESSLET with half = 0
 hs_status launch_xfused(hs_ctx* ctx, int kind, int half, const XArgs& a) {
   if (half) {
-    if (kind == HS_STOKESLET) return launch_xfused_half<HS_STOKESLET, 1>(ctx, a);
-    if (kind == HS_STRESSLET) return launch_xfused_half<HS_STRESSLET, 1>(ctx, a);
-    return launch_xfused_half<HS_ROTLET, 1>(ctx, a);
+    if (kind == HS_STOKESLET) return launch_xfused_len<HS_STOKESLET, true, 1>(ctx, a);
+    if (kind == HS_STRESSLET) return launch_xfused_len<HS_STRESSLET, true, 1>(ctx, a);
+    if (kind == HS_MIXED) return launch_xfused_len<HS_MIXED, true, 1>(ctx, a);
+    return launch_xfused_len<HS_ROTLET, true, 1>(ctx, a);
   }
-  if (kind == HS_STOKESLET) return launch_xfused_t<HS_STOKESLET, false, 1, AnyFFT>(ctx, a);
-  if (kind == HS_STRESSLET) return launch_xfused_t<HS_STRESSLET, false, 1, AnyFFT>(ctx, a);
-  return launch_xfused_t<HS_ROTLET, false, 1, AnyFFT>(ctx, a);
+  if (kind == HS_STOKESLET) return launch_xfused_len<HS_STOKESLET, false, 1>(ctx, a);
+  if (kind == HS_STRESSLET) return launch_xfused_len<HS_STRESSLET, false, 1>(ctx, a);
+  if (kind == HS_MIXED) return launch_xfused_len<HS_MIXED, false, 1>(ctx, a);
+  return launch_xfused_len<HS_ROTLET, false, 1>(ctx, a);
 }
 
 // twiddles exp(-2 pi i j / n), computed in long double on the host

@@ -973,7 +973,8 @@ __global__ void __launch_bounds__(256, 2) k_spread2(const int4* __restrict__ lo4
 }
 
 hs_status launch_spread(hs_ctx* ctx, const double4* pts, const double* w, int n, int nch, const int* bin_start,
-                        const GridGeom& g, double* grids) {
+                        const GridGeom& g, double* grids, int ldw, bool reuse_wtab) {
+  if (ldw <= 0) ldw = nch;  // weights row stride (a channel group of wider rows: ldw > nch)
   if (g.P > SP_MAXP) return fail(HS_ERR_PARAMETER, "spread supports window support P <= 64");
   const int nbx = sp_nbins(g, 0), nby = sp_nbins(g, 1), nbz = sp_nbins(g, 2);
   // default: v3 (window tables + cp.async staging + DMMA); HS_SPREAD_V0 = DMMA with in-tile window
@@ -994,7 +995,7 @@ hs_status launch_spread(hs_ctx* ctx, const double4* pts, const double* w, int n,
       lo = (int4*)scr3;
       tab = (double*)(lo + nn);
     }
-    if (n > 0 && tables) {
+    if (n > 0 && tables && !reuse_wtab) {  // (reuse: same sources, tables of the previous call intact)
       const int gs = (int)std::min<int64_t>(ceil_div((int64_t)n * 3 * 32, 256), ctx->sm_count * 16);
       k_spread_wtab<<<gs, 256, 0, ctx->stream>>>(pts, n, g, wt, lo, tab);
       HS_LAUNCHED(ctx);
@@ -1015,7 +1016,7 @@ hs_status launch_spread(hs_ctx* ctx, const double4* pts, const double* w, int n,
     const size_t smm = sizeof(double) * (16 * 32 / SW_CH) * SwBuf<N>::DOUBLES;                                     \
     HS_CUDA(cudaFuncSetAttribute(k_spread_mma4<N, false, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize,        \
                                  (int)smm));                                                                       \
-    k_spread_mma4<N, false, 16><<<grid, (16 + SW_NP) * 32, smm, ctx->stream>>>(lo, tab, wt, pts, wc0, nch,         \
+    k_spread_mma4<N, false, 16><<<grid, (16 + SW_NP) * 32, smm, ctx->stream>>>(lo, tab, wt, pts, wc0, ldw,         \
                                                                              bin_start, g, nbx, nby, nbz, gout);   \
   } break;
           HS_SP16(3) HS_SP16(4) HS_SP16(5) HS_SP16(6) HS_SP16(7)
@@ -1037,11 +1038,11 @@ hs_status launch_spread(hs_ctx* ctx, const double4* pts, const double* w, int n,
     const size_t smm = sizeof(double) * SW_K * SwBuf<N>::DOUBLES;                                                    \
     if (tables) {                                                                                                    \
       HS_CUDA(cudaFuncSetAttribute(k_spread_mma4<N, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smm)); \
-      k_spread_mma4<N, false><<<grid, SW_THREADS, smm, ctx->stream>>>(lo, tab, wt, pts, wc0, nch, bin_start, g, nbx, \
+      k_spread_mma4<N, false><<<grid, SW_THREADS, smm, ctx->stream>>>(lo, tab, wt, pts, wc0, ldw, bin_start, g, nbx, \
                                                                       nby, nbz, gout);                               \
     } else {                                                                                                         \
       HS_CUDA(cudaFuncSetAttribute(k_spread_mma4<N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smm));  \
-      k_spread_mma4<N, true><<<grid, SW_THREADS, smm, ctx->stream>>>(lo, tab, wt, pts, wc0, nch, bin_start, g, nbx,  \
+      k_spread_mma4<N, true><<<grid, SW_THREADS, smm, ctx->stream>>>(lo, tab, wt, pts, wc0, ldw, bin_start, g, nbx,  \
                                                                      nby, nbz, gout);                                \
     }                                                                                                                \
   } break;

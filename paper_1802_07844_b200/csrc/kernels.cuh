@@ -71,7 +71,8 @@ hs_status launch_grid_keys(hs_ctx* ctx, const double* pos, int n_src, int n_tota
                            int* keys);
 // sorted spread: pts/weights already in bin order; bin_start[nbins+1]
 hs_status launch_spread(hs_ctx* ctx, const double4* pts, const double* w, int n, int nch,
-                        const int* bin_start, const GridGeom& g, double* grids);
+                        const int* bin_start, const GridGeom& g, double* grids, int ldw = 0,
+                        bool reuse_wtab = false);
 // gather: nch channels (<= 8) at n points (any order); out[i*ldo + ch] (times h^3 * scale)
 hs_status launch_gather(hs_ctx* ctx, const double4* pts, const int* perm, int n, int nch,
                         const GridGeom& g, const double* grids, double* out, int ldo, double scale);
@@ -86,7 +87,8 @@ hs_status launch_gather_fourier(hs_ctx* ctx, const double4* pts, const int* orig
 struct PairArgs {
   const double4* P;   // cell-sorted combined sources: x, y, z, original combined index
   const double4* A;   // strength a: f (stokeslet), g (stresslet), sign*(g x q) (rotlet)
-  const double4* B;   // strength b: q (stresslet), image wall channel v1,v2 (rotlet)
+  const double4* B;   // strength b: q (stresslet), image wall channel v1,v2 (rotlet), g (mixed)
+  const double4* C;   // mixed only: q
   const int* start;   // src cell start, ncell+1
   const double4* TP;  // cell-sorted targets: x, y, z, tcol
   const int* torig;   // output row of each sorted target
@@ -113,6 +115,9 @@ struct PairArgs {
   double* uc;         // optional (nt,3) correction part
   unsigned* flags;
   unsigned long long* counts;  // [accepted pairs, accepted image pairs] (optional)
+  // neighbour audit (hs_plan_pair_audit; null in production launches): per original target
+  // [accepted pairs, accepted image pairs, sum of splitmix64(combined source id) mod 2^64]
+  unsigned long long* audit;
 };
 hs_status launch_pair(hs_ctx* ctx, const PairArgs& a);
 hs_status build_pair_items(hs_ctx* ctx, const int* t_start, int ncol, int nz, int* work, int2* items,
@@ -156,6 +161,8 @@ struct FftPlan {
 };
 struct XArgs {
   double2* B;            // channel-major spectra, each [ky < py][x < nx][kz < nzh]
+  double2* Bout;         // output channels (same layout; B for the in-place pass)
+  int accum;             // 1: outputs are added to Bout (a second channel group's pass)
   int64_t ch_stride;     // complex elements between channels
   const double* tabB;    // biharmonic table, x-stage layout [ky][kz][kx] (or null)
   const double* tabH;    // harmonic table, same layout (or null)

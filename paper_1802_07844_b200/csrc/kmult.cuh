@@ -6,6 +6,10 @@
 //   stresslet: C00 C01 C02 C11 C12 C22 | V2 M00 M01 M02 M11 M12 M22   (13 / 6)
 //              (symmetric parts only: the multiplier depends on sym(C) alone)
 //   rotlet:    W0 W1 W2 | V0 V1                               (5 / 3)
+//   mixed, group 1 (HS_MIXED): F0 F1 F2 | S V0 V1 V2 M00 M01 M02 M11 M12 M22   (13 / 3)
+//              (stokeslet kernel + the wall channels both kinds share: s, v = v_stokeslet +
+//              v_stresslet, M = M_stresslet); group 2 = the stresslet kernel channels
+//              C00..C22, scaled as HS_STRESSLET without wall channels and added to group 1's T1
 //   outputs:   T1x T1y T1z [T2x T2y T2z]
 #pragma once
 #include "common.cuh"
@@ -23,7 +27,10 @@ __device__ __forceinline__ cplx cconj(cplx a) { return {a.re, -a.im}; }
 
 template <int KIND, bool HALF>
 struct KChan {
-  static constexpr int NIN = KIND == HS_STOKESLET ? (HALF ? 7 : 3) : KIND == HS_STRESSLET ? (HALF ? 13 : 6) : (HALF ? 5 : 3);
+  static constexpr int NIN = KIND == HS_STOKESLET ? (HALF ? 7 : 3)
+                           : KIND == HS_STRESSLET ? (HALF ? 13 : 6)
+                           : KIND == HS_MIXED     ? (HALF ? 13 : 3)
+                                                  : (HALF ? 5 : 3);
   static constexpr int NOUT = HALF ? 6 : 3;
 };
 
@@ -38,7 +45,7 @@ template <int KIND, bool HALF>
 __device__ __forceinline__ void apply_multiplier(double kx, double ky, double kz, double G, double Fc, const cplx* C,
                                                  cplx* out) {
   const double k2 = kx * kx + ky * ky + kz * kz;
-  if (KIND == HS_STOKESLET) {
+  if (KIND == HS_STOKESLET || KIND == HS_MIXED) {
     // t1_j = -G (k^2 C_j - k_j (k.C))   (ewald_fourier.py:394-414)
     const cplx kd = cadd(cadd(cscale(kx, C[0]), cscale(ky, C[1])), cscale(kz, C[2]));
     out[0] = cscale(-G, csub(cscale(k2, C[0]), cscale(kx, kd)));
@@ -78,6 +85,13 @@ __device__ __forceinline__ void apply_multiplier(double kx, double ky, double kz
                                  cadd(cscale(2.0 * kx * kz, C[9]), cscale(ky * ky, C[10]))),
                             cadd(cscale(2.0 * ky * kz, C[11]), cscale(kz * kz, C[12])));
       phi = cscale(Fc, csub(cmul_i(cscale(kz, C[6])), kMk));
+    } else if (KIND == HS_MIXED) {
+      // both kinds' wall channels: Fc (S + i k.V - k_l k_m M_lm)
+      const cplx kv = cadd(cadd(cscale(kx, C[4]), cscale(ky, C[5])), cscale(kz, C[6]));
+      const cplx kMk = cadd(cadd(cadd(cscale(kx * kx, C[7]), cscale(2.0 * kx * ky, C[8])),
+                                 cadd(cscale(2.0 * kx * kz, C[9]), cscale(ky * ky, C[10]))),
+                            cadd(cscale(2.0 * ky * kz, C[11]), cscale(kz * kz, C[12])));
+      phi = cscale(Fc, csub(cadd(C[3], cmul_i(kv)), kMk));
     } else {
       const cplx kv = cadd(cscale(kx, C[3]), cscale(ky, C[4]));
       phi = cscale(Fc, cmul_i(kv));

@@ -267,12 +267,16 @@ constexpr int pc_h() { return KIND == HS_STOKESLET ? PC_H_STOKESLET : (PC_TG > 1
 // restaged -- which force partial-round drains -- are rarer; the stresslet / rotlet records
 // leave room for 2 within 48 KB of static shared memory)
 template <int KIND>
-constexpr int pc_nh() { return KIND == HS_STOKESLET ? PC_NH_STOKESLET : PC_NH_OTHER; }
+constexpr int pc_nh() { return KIND == HS_STOKESLET ? PC_NH_STOKESLET : (KIND == HS_MIXED ? 2 : PC_NH_OTHER); }
 // candidate record bytes in shared memory (dynamic): xy, z a.x, a.y a.z, FP32 view, (+ b)
+// (mixed: a = f, then g.x g.y | g.z q.x | q.y q.z)
 template <int KIND, bool HALF>
 constexpr int pc_rec_bytes() {
-  return 64 + ((KIND == HS_STRESSLET) || (KIND == HS_ROTLET && HALF) ? 16 : 0) + (KIND == HS_STRESSLET ? 8 : 0);
+  return KIND == HS_MIXED ? 112
+                          : 64 + ((KIND == HS_STRESSLET) || (KIND == HS_ROTLET && HALF) ? 16 : 0) +
+                                (KIND == HS_STRESSLET ? 8 : 0);
 }
+
 #ifndef PC_Q_DEF
 #define PC_Q_DEF 64
 #endif
@@ -286,9 +290,23 @@ constexpr int PC_Q = PC_Q_DEF;        // per-lane queue capacity (power of two)
 #ifndef PC_MINB
 #define PC_MINB 4                     // resident CTAs per SM (register budget 128)
 #endif
+// resident CTAs per SM: the mixed evaluation (stokeslet + stresslet per pair, sharing the
+// transcendentals) needs more registers than 128
+template <int KIND>
+constexpr int pc_minb() { return KIND == HS_MIXED ? 3 : PC_MINB; }
 
-template <int KIND, bool HALF>
-__global__ void __launch_bounds__(PC_TG, PC_MINB) k_pair_q(const PairArgs a) {
+// splitmix64 finaliser (neighbour-set hash of the audit launch; oracle/hs_oracle.c)
+__device__ __forceinline__ unsigned long long splitmix64(unsigned long long x) {
+  unsigned long long z = x + 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+// AUDIT: the same kernel also records every target's accepted neighbour set (count, image
+// count, id hash) -- a separate instantiation so the production launch carries no extra work.
+template <int KIND, bool HALF, bool AUDIT>
+__global__ void __launch_bounds__(PC_TG, pc_minb<KIND>()) k_pair_q(const PairArgs a) {
   // Candidate rows as 16-byte columns: the evaluation reads them at lane-random rows, and a
   // 16-byte array spreads those reads over 8 bank groups (a 32-byte row only over 4).
   constexpr int PC_H = pc_h<KIND>(), PC_PER = PC_H / PC_TG;
@@ -302,6 +320,10 @@ __global__ void __launch_bounds__(PC_TG, PC_MINB) k_pair_q(const PairArgs a) {
   float4* sF = reinterpret_cast<float4*>(sAA + PC_K);  // position relative to the item's first target (FP32)
   double2* sB0 = reinterpret_cast<double2*>(sF + PC_K);  // b.x, b.y (kNeedB)
   double* sB1 = reinterpret_cast<double*>(sB0 + (kNeedB ? PC_K : 0));  // b.z (stresslet)
+  constexpr bool kMixed = KIND == HS_MIXED;
+  double2* sG0 = reinterpret_cast<double2*>(sF + PC_K);  // mixed: g.x g.y
+  double2* sG1 = sG0 + PC_K;                             // mixed: g.z q.x
+  double2* sG2 = sG1 + PC_K;                             // mixed: q.y q.z
   __shared__ unsigned short sq[PC_WARPS][PC_Q][32];
   __shared__ int run_beg[PT_MAXRUN];
   __shared__ int run_pre[PT_MAXRUN + 1];
@@ -354,6 +376,11 @@ __global__ void __launch_bounds__(PC_TG, PC_MINB) k_pair_q(const PairArgs a) {
     const double4 T = a.TP[tvalid ? t : t0];
     const long long tcol = tvalid ? (long long)T.w : -2;  // -2 never matches a source id
     const int tcol_i = (int)tcol;
+    // the target's own z cell: the reference scans cz - 2 .. cz + 2 (ewald_real.py:285-287);
+    // the item's candidate range covers all its targets' ranges, so shell candidates are
+    // also checked against this target's reach (sure-accepts lie well inside it)
+    const int tcz = a.cell_z(T.z);
+    unsigned long long a_hash = 0;
     // FP32 view relative to the item's first target, and this warp's target bounding box
     const double4 R0 = a.TP[t0];
     const float tfx = (float)(T.x - R0.x), tfy = (float)(T.y - R0.y), tfz = (float)(T.z - R0.z);
@@ -374,19 +401,36 @@ __global__ void __launch_bounds__(PC_TG, PC_MINB) k_pair_q(const PairArgs a) {
     bool singular = false;
     unsigned long long n_acc = 0, n_img = 0;
 
-    // candidate row j as (S, A, B); S.w unused; image <=> sign bit of z (k_pair_records)
+    // candidate row j as (S, A, B); S.w unused; image <=> sign bit of z (k_pair_records).
+    // Mixed: A = f, B = g, and the q of the row is read by load_q
     auto load_cand = [&](int jj, double4& S, double4& A, double4& B, bool& img) {
       const double2 xy = sXY[jj], za = sZA[jj], aa = sAA[jj];
       S = make_double4(xy.x, xy.y, za.x, 0.0);
       A = make_double4(za.y, aa.x, aa.y, 0.0);
       img = HALF && __double_as_longlong(za.x) < 0;
       B = make_double4(0, 0, 0, 0);
-      if (KIND == HS_STRESSLET) {
+      if (kMixed) {
+        const double2 g0 = sG0[jj], g1 = sG1[jj];
+        B = make_double4(g0.x, g0.y, g1.x, g1.y);  // .w carries q.x
+      } else if (KIND == HS_STRESSLET) {
         const double2 b = sB0[jj];
         B = make_double4(b.x, b.y, sB1[jj], 0.0);
       } else if (kNeedB && img) {  // rotlet: the wall channel exists for images only
         const double2 b = sB0[jj];
         B = make_double4(b.x, b.y, 0.0, 0.0);
+      }
+    };
+    // one pair's contribution(s) for the kernel kind (mixed: stokeslet + stresslet sharing the
+    // radial coefficients, i.e. one rsqrt / exp / erfc for both)
+    auto apply_kind = [&](const PairCoef& qc, int jj, double d0, double d1, double d2, double rr, const double4& S,
+                          const double4& A, const double4& B, bool img) {
+      if constexpr (kMixed) {
+        const double2 q12 = sG2[jj];
+        const double4 Q = make_double4(B.w, q12.x, q12.y, 0.0);
+        apply_pair<HS_STOKESLET>(pc, qc, d0, d1, d2, rr, T.z, S, A, B, img, &acc[0], &acc[3]);
+        apply_pair<HS_STRESSLET>(pc, qc, d0, d1, d2, rr, T.z, S, B, Q, img, &acc[0], &acc[3]);
+      } else {
+        apply_pair<KIND>(pc, qc, d0, d1, d2, rr, T.z, S, A, B, img, &acc[0], &acc[3]);
       }
     };
     auto eval_one = [&](int jj) {
@@ -396,7 +440,8 @@ __global__ void __launch_bounds__(PC_TG, PC_MINB) k_pair_q(const PairArgs a) {
       const double e0 = T.x - S.x, e1 = T.y - S.y, e2 = T.z - S.z;
       const double rr = fma(e0, e0, fma(e1, e1, e2 * e2));  // (neighbour test done exactly in the scan)
       if (img) ++n_img;
-      eval_pair<KIND, true>(pc, e0, e1, e2, rr, T.z, S, A, B, img, &acc[0], &acc[3], s_erfcx);
+      if (AUDIT) a_hash += splitmix64((unsigned long long)__float_as_int(sF[jj].w));
+      apply_kind(pair_coef<true>(pc, rr, s_erfcx), jj, e0, e1, e2, rr, S, A, B, img);
     };
 
     // Two-half ring of staged candidates + per-lane FIFO queues: entries of chunk c may be
@@ -445,8 +490,11 @@ __global__ void __launch_bounds__(PC_TG, PC_MINB) k_pair_q(const PairArgs a) {
       const PairCoef q1 = pair_coef<true>(pc, r1, s_erfcx);
       const PairCoef q2 = pair_coef<true>(pc, r2, s_erfcx);
       n_img += (unsigned)i1 + (unsigned)i2;
-      apply_pair<KIND>(pc, q1, f0, f1, f2, r1, T.z, S1, A1, B1, i1, &acc[0], &acc[3]);
-      apply_pair<KIND>(pc, q2, g0, g1, g2, r2, T.z, S2, A2, B2, i2, &acc[0], &acc[3]);
+      if (AUDIT)
+        a_hash += splitmix64((unsigned long long)__float_as_int(sF[j1].w)) +
+                  splitmix64((unsigned long long)__float_as_int(sF[j2].w));
+      apply_kind(q1, j1, f0, f1, f2, r1, S1, A1, B1, i1);
+      apply_kind(q2, j2, g0, g1, g2, r2, S2, A2, B2, i2);
     };
     for (int c = 0, c0 = 0; c0 < ncand; ++c, c0 += PC_H) {
       const int h = c % pc_nh<KIND>(), hb = h * PC_H;
@@ -482,7 +530,12 @@ __global__ void __launch_bounds__(PC_TG, PC_MINB) k_pair_q(const PairArgs a) {
           // .w carries the combined source index as int bits (no per-pair FP64->int conversions)
           sF[hb + j] = make_float4((float)(S.x - R0.x), (float)(S.y - R0.y), (float)(S.z - R0.z),
                                    __int_as_float((int)S.w));
-          if (kNeedB) {
+          if (kMixed) {
+            const double4 G = a.B[row], Q = a.C[row];
+            sG0[hb + j] = make_double2(G.x, G.y);
+            sG1[hb + j] = make_double2(G.z, Q.x);
+            sG2[hb + j] = make_double2(Q.y, Q.z);
+          } else if (kNeedB) {
             const double4 B = a.B[row];
             sB0[hb + j] = make_double2(B.x, B.y);
             if (KIND == HS_STRESSLET) sB1[hb + j] = B.z;
@@ -518,7 +571,7 @@ __global__ void __launch_bounds__(PC_TG, PC_MINB) k_pair_q(const PairArgs a) {
           const double d0 = __dsub_rn(T.x, xy.x), d1 = __dsub_rn(T.y, xy.y), d2 = __dsub_rn(T.z, sz);
           const double r2 = exact_r2(d0, d1, d2);
           singular |= __float_as_int(F.w) != tcol_i && tvalid && r2 == 0.0;
-          ok = r2 <= a.rc2 && r2 != 0.0;
+          ok = r2 <= a.rc2 && r2 != 0.0 && abs(a.cell_z(sz) - tcz) <= 2;
         };
         while (near) {
           const int ia = __ffs(near) - 1;
@@ -574,19 +627,24 @@ __global__ void __launch_bounds__(PC_TG, PC_MINB) k_pair_q(const PairArgs a) {
     }
     if (singular) atomicOr(a.flags, FLAG_SINGULAR);
     if (a.counts) {
-      n_acc = __reduce_add_sync(0xffffffffu, (unsigned)n_acc);
-      n_img = __reduce_add_sync(0xffffffffu, (unsigned)n_img);
+      const unsigned long long w_acc = __reduce_add_sync(0xffffffffu, (unsigned)n_acc);
+      const unsigned long long w_img = __reduce_add_sync(0xffffffffu, (unsigned)n_img);
       if (lane == 0) {
-        atomicAdd(&a.counts[0], n_acc);
-        atomicAdd(&a.counts[1], n_img);
+        atomicAdd(&a.counts[0], w_acc);
+        atomicAdd(&a.counts[1], w_img);
       }
     }
     if (tvalid) {
       const int o = a.torig[t];
+      if (AUDIT) {
+        a.audit[3 * (size_t)o] = n_acc;
+        a.audit[3 * (size_t)o + 1] = n_img;
+        a.audit[3 * (size_t)o + 2] = a_hash;
+      }
       double u[3];
 #pragma unroll
       for (int k = 0; k < 3; ++k) u[k] = acc[k] * norm_k + acc[3 + k] * norm_c;
-      if (KIND == HS_STOKESLET && a.self_f != nullptr && tcol >= 0 && tcol < a.n_real) {
+      if ((KIND == HS_STOKESLET || kMixed) && a.self_f != nullptr && tcol >= 0 && tcol < a.n_real) {
         const double sc = -(4.0 * a.xi / kSqrtPi);
 #pragma unroll
         for (int k = 0; k < 3; ++k) u[k] += sc * a.self_f[3 * tcol + k] / (8.0 * kPi);
@@ -646,22 +704,32 @@ hs_status launch_pair(hs_ctx* ctx, const PairArgs& a) {
   const bool is_half = (a.kind & 16) != 0;
   // persistent-style grid: enough CTAs to fill the machine, looping over the device-side item count
   const int grid = std::max(1, std::min(a.max_items, ctx->sm_count * 16));
-#define HS_PAIR_CASE(K, H)                                                                         \
-  do {                                                                                             \
-    const int dyn = pc_nh<K>() * pc_h<K>() * pc_rec_bytes<K, H>();                                 \
-    HS_CUDA(cudaFuncSetAttribute(k_pair_q<K, H>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn)); \
-    k_pair_q<K, H><<<grid, PC_TG, dyn, ctx->stream>>>(a);                                           \
+#define HS_PAIR_CASE1(K, H, AU)                                                                         \
+  do {                                                                                                  \
+    const int dyn = pc_nh<K>() * pc_h<K>() * pc_rec_bytes<K, H>();                                      \
+    HS_CUDA(cudaFuncSetAttribute(k_pair_q<K, H, AU>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn)); \
+    k_pair_q<K, H, AU><<<grid, PC_TG, dyn, ctx->stream>>>(a);                                            \
+  } while (0)
+#define HS_PAIR_CASE(K, H)            \
+  do {                                \
+    if (a.audit)                      \
+      HS_PAIR_CASE1(K, H, true);      \
+    else                              \
+      HS_PAIR_CASE1(K, H, false);     \
   } while (0)
   if (is_half) {
     if (kind == HS_STOKESLET) HS_PAIR_CASE(HS_STOKESLET, true);
     else if (kind == HS_STRESSLET) HS_PAIR_CASE(HS_STRESSLET, true);
+    else if (kind == HS_MIXED) HS_PAIR_CASE(HS_MIXED, true);
     else HS_PAIR_CASE(HS_ROTLET, true);
   } else {
     if (kind == HS_STOKESLET) HS_PAIR_CASE(HS_STOKESLET, false);
     else if (kind == HS_STRESSLET) HS_PAIR_CASE(HS_STRESSLET, false);
+    else if (kind == HS_MIXED) HS_PAIR_CASE(HS_MIXED, false);
     else HS_PAIR_CASE(HS_ROTLET, false);
   }
 #undef HS_PAIR_CASE
+#undef HS_PAIR_CASE1
   HS_LAUNCHED(ctx);
   return HS_OK;
 }

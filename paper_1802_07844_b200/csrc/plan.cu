@@ -33,7 +33,7 @@ namespace hs {
 __global__ void k_pair_records(int kind, int half, const int* __restrict__ order, int n_comb, int n,
                                const double* __restrict__ pos, const double* __restrict__ sa,
                                const double* __restrict__ sb, double4* __restrict__ P, double4* __restrict__ A,
-                               double4* __restrict__ B, unsigned* __restrict__ flags) {
+                               double4* __restrict__ B, double4* __restrict__ Cq, unsigned* __restrict__ flags) {
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n_comb; k += gridDim.x * blockDim.x) {
     const int i = order[k];
     const bool img = half && i >= n;
@@ -45,9 +45,14 @@ __global__ void k_pair_records(int kind, int half, const int* __restrict__ order
     if (half && z < 0.0) atomicOr(flags, FLAG_GEOMETRY);  // sources must lie in x3 >= 0 (system.py:77)
     P[k] = make_double4(pos[3 * s], pos[3 * s + 1], m * (z + 0.0), (double)i);
     const double a0 = sa[3 * s], a1 = sa[3 * s + 1], a2 = sa[3 * s + 2];
-    if (kind == HS_STOKESLET) {
+    if (kind == HS_STOKESLET || kind == HS_MIXED) {
       // combined_f = [f; -f^I], f^I = f * (1,1,-1)  (system.py:171-177)
       A[k] = img ? make_double4(-a0, -a1, a2, 0.0) : make_double4(a0, a1, a2, 0.0);
+      if (kind == HS_MIXED) {  // + the stresslet's combined g, q (rows of sb: g0 g1 g2 q0 q1 q2)
+        const double* gq = sb + 6 * (size_t)s;
+        B[k] = make_double4(gq[0], gq[1], m * gq[2], 0.0);
+        Cq[k] = make_double4(gq[3], gq[4], m * gq[5], 0.0);
+      }
     } else {
       const double b0 = sb[3 * s], b1 = sb[3 * s + 1], b2 = sb[3 * s + 2];
       const double g0 = a0, g1 = a1, g2 = m * a2;  // g or g^I
@@ -89,6 +94,41 @@ __global__ void k_spread_records(int kind, int half, int set, const int* __restr
   const int nk_m = kind == HS_STRESSLET ? 6 : 3;  // set 2: kernel channels before the wall channels
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n_rows; k += gridDim.x * blockDim.x) {
     const int i = order[k];
+    if (kind == HS_MIXED) {
+      // mixed stokeslet + stresslet (kmult.cuh layout): set 2 (half space, mirrored) at the sources
+      // [F | S V0 V1 V2 M00 M01 M02 M11 M12 M22 | C00 C01 C02 C11 C12 C22]; set 0 (free) [F | C]
+      const double y3 = pos[3 * i + 2];
+      P[k] = make_double4(pos[3 * i], pos[3 * i + 1], y3, 0.0);
+      double* w = W + (size_t)k * nch;
+      const double f0 = sa[3 * i], f1 = sa[3 * i + 1], f2 = sa[3 * i + 2];
+      const double* gq = sb + 6 * (size_t)i;
+      const double g0 = gq[0], g1 = gq[1], g2 = gq[2], q0 = gq[3], q1 = gq[4], q2 = gq[5];
+      w[0] = f0;
+      w[1] = f1;
+      w[2] = f2;
+      double* c = w + 3;
+      if (set == 2) {
+        const double gi2 = -g2, qi2 = -q2;  // g^I, q^I
+        w[3] = -f2;                                            // s = -f3 (stokeslet)
+        w[4] = -y3 * f0;                                       // v = -y3 f^I (stokeslet)
+        w[5] = -y3 * f1;
+        w[6] = y3 * f2 + 2.0 * (g0 * q0 + g1 * q1 + gi2 * qi2);  // + v3 = 2 g^I.q^I (stresslet)
+        w[7] = -y3 * 2.0 * g0 * q0;                            // M = -y3 (g^I q^I^T + q^I g^I^T)
+        w[8] = -y3 * (g0 * q1 + q0 * g1);
+        w[9] = -y3 * (g0 * qi2 + q0 * gi2);
+        w[10] = -y3 * 2.0 * g1 * q1;
+        w[11] = -y3 * (g1 * qi2 + q1 * gi2);
+        w[12] = -y3 * 2.0 * gi2 * qi2;
+        c = w + 13;
+      }
+      c[0] = g0 * q0;  // symmetric part of g (x) q (stresslet kernel, source sign +1)
+      c[1] = 0.5 * (g0 * q1 + g1 * q0);
+      c[2] = 0.5 * (g0 * q2 + g2 * q0);
+      c[3] = g1 * q1;
+      c[4] = 0.5 * (g1 * q2 + g2 * q1);
+      c[5] = g2 * q2;
+      continue;
+    }
     const bool img = (set == 1) || (set == 0 && half && i >= n);
     const int s = (set == 0 && half && i >= n) ? i - n : i;
     const double m = img ? -1.0 : 1.0;
@@ -163,8 +203,8 @@ __global__ void k_spread_records(int kind, int half, int set, const int* __restr
 //   wall channels:    G_c(k) = S_c(2Mt - k)           (spread at the images y^I only)
 // which replaces spreading 2N kernel + N wall sources (10 N P^3 for the stokeslet) by N
 // sources (7 N P^3) and one pass over the grid.  In place, one thread per mirror pair.
-__global__ void k_mirror_z(double* __restrict__ grid, int nch, int nk, unsigned sigma_neg, int64_t ch_stride,
-                           int64_t lines, int pz, int nz) {
+__global__ void k_mirror_z(double* __restrict__ grid, int nch, unsigned kern_mask, unsigned sigma_neg,
+                           int64_t ch_stride, int64_t lines, int pz, int nz) {
   const int half_n = nz / 2;  // pairs (k, nz - k) for k = 1 .. nz/2 - 1, plus k = nz/2 and k = 0
   const int64_t per = lines * (half_n + 1);
   const int64_t n = per * nch;
@@ -174,7 +214,7 @@ __global__ void k_mirror_z(double* __restrict__ grid, int nch, int nk, unsigned 
     const int64_t line = r / (half_n + 1);
     const int k = (int)(r - line * (half_n + 1));
     double* g = grid + c * ch_stride + line * pz;
-    const bool kern = c < nk;
+    const bool kern = (kern_mask >> c) & 1u;
     const double sg = ((sigma_neg >> c) & 1u) ? -1.0 : 1.0;
     if (k == 0) {  // mirror of node 0 is node nz (outside the grid, where S = 0)
       if (!kern) g[0] = 0.0;
@@ -231,8 +271,9 @@ inline int grid_size(hs_ctx* ctx, int64_t n) {
 hs_status build_pair_records(hs_ctx* ctx, int kind, int half, const int* order, int n_comb, int n, const double* pos,
                              const double* sa, const double* sb, double4* P, double4* A, double4* B) {
   if (n_comb == 0) return HS_OK;
+  if (kind == HS_MIXED) return fail(HS_ERR_PARAMETER, "mixed sources evaluate through a plan");
   k_pair_records<<<grid_size(ctx, n_comb), 256, 0, ctx->stream>>>(kind, half, order, n_comb, n, pos, sa, sb, P, A, B,
-                                                                         ctx->d_flags);
+                                                                         nullptr, ctx->d_flags);
   HS_LAUNCHED(ctx);
   return HS_OK;
 }
@@ -260,6 +301,14 @@ struct hs_plan {
   bool half = true;
   int n_comb = 0;       // sources in the real-space / kernel spread set
   int nk = 0, nc = 0;   // kernel / correction channels
+  // source-grid channel groups: grid_in holds sg_cap channels; the channels [0, n_in) are
+  // spread and forward-transformed group by group (mixed single-GPU plans: 13 + 6, so the
+  // 19 source grids never coexist); kern_mask / sigma_neg: kernel channels and their image
+  // signs for the mirrored spreading (bit c = channel c)
+  int sg_cap = 0;
+  int ngroup = 1, group_c0[3] = {0, 0, 0};
+  unsigned kern_mask = 0, sigma_mask = 0;
+  bool tmp_aliased = false;     // grid_tmp lives in grid_in (mixed): re-zero its z padding after use
   int n_in = 0, n_out = 0;
   CellGeom cg{};
   GridGeom gg{};        // padded real grids
@@ -275,7 +324,7 @@ struct hs_plan {
   int *keys = nullptr, *order = nullptr, *start = nullptr, *work = nullptr;
   int *t_order = nullptr, *t_start = nullptr;
   int2* items = nullptr;
-  double4 *P = nullptr, *A = nullptr, *B = nullptr, *TP = nullptr;
+  double4 *P = nullptr, *A = nullptr, *B = nullptr, *Cq = nullptr, *TP = nullptr;
   int* torig = nullptr;
   // Fourier
   int *bk_order = nullptr, *bk_start = nullptr, *bc_order = nullptr, *bc_start = nullptr;
@@ -304,6 +353,7 @@ struct hs_plan {
   // outputs
   double *u = nullptr, *u_real = nullptr, *u_four = nullptr, *uk = nullptr, *uc = nullptr;
   unsigned long long* pair_counts = nullptr;
+  unsigned long long* audit = nullptr;  // hs_plan_pair_audit: per-target neighbour audit (3 x nt)
   cudaEvent_t ev[16] = {};
   // y-slab decomposition (hs_plan_create_slab; sharding.py).  slab.world == 0: whole grid.
   hs_slab slab{};
@@ -360,10 +410,18 @@ hs_status plan_channels(int kind, int half, int* nk, int* nc) {
   if (kind == HS_STOKESLET) { *nk = 3; *nc = half ? 4 : 0; }
   else if (kind == HS_STRESSLET) { *nk = 6; *nc = half ? 7 : 0; }
   else if (kind == HS_ROTLET) { *nk = 3; *nc = half ? 2 : 0; }
+  else if (kind == HS_MIXED) { *nk = 9; *nc = half ? 10 : 0; }  // kmult.cuh mixed layout
   else return fail(HS_ERR_PARAMETER, "unknown kernel kind");
   return HS_OK;
 }
 }  // namespace hs
+
+static unsigned mirror_sigma_neg(int kind) {
+  // channels whose image value is minus the source value (k_spread_records set 0)
+  if (kind == HS_STOKESLET) return 0x3u;               // (-, -, +)
+  if (kind == HS_STRESSLET) return 0x1u | 0x2u | 0x8u | 0x20u;  // 00 01 11 22 negative, 02 12 positive
+  return 0x4u;                                          // rotlet (+, +, -)
+}
 
 static hs_status plan_create_impl(hs_ctx* ctx, const hs_params* prm, const hs_slab* slab, hs_plan** out) {
   if (!ctx || !prm || !out) return fail(HS_ERR_PARAMETER, "null argument");
@@ -457,9 +515,10 @@ static hs_status plan_create_impl(hs_ctx* ctx, const hs_params* prm, const hs_sl
   const int maxn = std::max(p->n_comb, std::max(nt, n));
   const int maxb = std::max(std::max(ncell * kTargetSub, nb + 1), gather_keys(g));
 #define A_(cnt, ptr, ...) if ((st = palloc(p, (size_t)(cnt), &(ptr), ##__VA_ARGS__)) != HS_OK) return bail(st)
+  const bool mixed = prm->kind == HS_MIXED;
   A_(3 * (size_t)n, p->d_pos);
   A_(3 * (size_t)n, p->d_sa);
-  if (prm->kind != HS_STOKESLET) A_(3 * (size_t)n, p->d_sb);
+  if (prm->kind != HS_STOKESLET) A_((mixed ? 6 : 3) * (size_t)n, p->d_sb);
   if (!prm->targets_are_sources) {
     A_(3 * (size_t)std::max(nt, 1), p->d_tgt);
     A_((size_t)std::max(nt, 1), p->d_tcols);
@@ -478,6 +537,7 @@ static hs_status plan_create_impl(hs_ctx* ctx, const hs_params* prm, const hs_sl
   A_(p->n_comb, p->P);
   A_(p->n_comb, p->A);
   A_(p->n_comb, p->B);
+  if (mixed) A_(p->n_comb, p->Cq);
   A_(std::max(nt, 1), p->TP);
   A_(std::max(nt, 1), p->torig);
   A_(p->n_comb, p->bk_order);
@@ -487,7 +547,24 @@ static hs_status plan_create_impl(hs_ctx* ctx, const hs_params* prm, const hs_sl
   A_(std::max(nt, 1), p->bt_order);
   A_((size_t)gather_keys(g) + 1, p->bt_start);
   // mirrored spreading (half space; HS_SPREAD_IMAGES=1 spreads the images explicitly, comparison)
-  p->mirror = p->half && !getenv("HS_SPREAD_IMAGES");
+  p->mirror = p->half && (mixed || !getenv("HS_SPREAD_IMAGES"));
+  // channel groups and mirror masks
+  p->sg_cap = p->n_in;
+  p->ngroup = 1;
+  p->group_c0[1] = p->n_in;
+  if (mixed) {
+    p->kern_mask = p->half ? (0x7u | (0x3Fu << 13)) : 0x1FFu;
+    p->sigma_mask = p->half ? (0x3u | (0x2Bu << 13)) : 0u;
+    if (!sl) {  // one GPU: spread / transform 13 + 6 (half) or 3 + 6 (free) channels at a time
+      p->ngroup = 2;
+      p->group_c0[1] = p->half ? 13 : 3;
+      p->group_c0[2] = p->n_in;
+      p->sg_cap = p->half ? 13 : 6;
+    }
+  } else {
+    p->kern_mask = (1u << p->nk) - 1u;
+    p->sigma_mask = mirror_sigma_neg(prm->kind);
+  }
   A_(p->n_comb, p->SPk);
   A_(std::max((size_t)p->n_comb * p->nk, (size_t)n * p->n_in), p->SWk);
   if (p->nc) {
@@ -496,12 +573,17 @@ static hs_status plan_create_impl(hs_ctx* ctx, const hs_params* prm, const hs_sl
   }
   A_(std::max(nt, 1), p->TG);
   A_(std::max(nt, 1), p->tg_orig);
-  A_((size_t)p->n_in * p->n_grid, p->grid_in, true);
+  A_((size_t)p->sg_cap * p->n_grid, p->grid_in, true);
   A_((size_t)p->n_amix, p->Amix, true);
   A_((size_t)std::max(p->n_in, p->n_out) * p->n_mixed, p->spec);
   p->out_pitch = p->half ? 6 : 4;
   A_((size_t)p->out_pitch * p->n_grid, p->grid_out, true);
-  A_((size_t)p->n_out * p->n_grid, p->grid_tmp);
+  if (mixed && !sl && p->sg_cap >= p->n_out) {
+    p->grid_tmp = p->grid_in;  // the source grids are dead once forward-transformed
+    p->tmp_aliased = true;
+  } else {
+    A_((size_t)p->n_out * p->n_grid, p->grid_tmp);
+  }
   p->go = p->gg;
   p->go.stride[0] = (int64_t)p->out_pitch * pz;
   p->go.stride[1] = (int64_t)p->out_pitch * nxd * pz;
@@ -938,7 +1020,7 @@ hs_status stage_inputs(hs_plan* p, const double* positions, const double* sa, co
   const int n = (int)prm.n, nt = (int)prm.n_targets;
   const int kind = prm.kind;
   if (!positions || !sa) return fail(HS_ERR_PARAMETER, "null argument");
-  if (kind != HS_STOKESLET && !sb) return fail(HS_ERR_PARAMETER, "stresslet/rotlet need q");
+  if (kind != HS_STOKESLET && !sb) return fail(HS_ERR_PARAMETER, "stresslet/rotlet need q (mixed: g and q)");
   if (!prm.targets_are_sources && nt > 0 && !targets) return fail(HS_ERR_PARAMETER, "targets required");
   const double *pos = positions, *fa = sa, *fb = sb, *tp = targets;
   const long long* tc = (const long long*)tcols;
@@ -948,7 +1030,7 @@ hs_status stage_inputs(hs_plan* p, const double* positions, const double* sa, co
     pos = p->d_pos;
     fa = p->d_sa;
     if (kind != HS_STOKESLET) {
-      HS_CUDA(cudaMemcpyAsync(p->d_sb, sb, 24 * (size_t)n, cudaMemcpyHostToDevice, st));
+      HS_CUDA(cudaMemcpyAsync(p->d_sb, sb, (kind == HS_MIXED ? 48 : 24) * (size_t)n, cudaMemcpyHostToDevice, st));
       fb = p->d_sb;
     }
     if (!prm.targets_are_sources && nt > 0) {
@@ -983,7 +1065,7 @@ hs_status stage_real(hs_plan* p, bool want) {
   if (do_real) {
     HS_TRY(sort_points_by_cell(p, pos, n, p->n_comb, p->half ? 1 : 0, 1, p->order, p->start));
     k_pair_records<<<grid_size(ctx, p->n_comb), 256, 0, st>>>(kind, p->half, p->order, p->n_comb, n, pos, fa, fb,
-                                                              p->P, p->A, p->B, ctx->d_flags);
+                                                              p->P, p->A, p->B, p->Cq, ctx->d_flags);
     HS_LAUNCHED(ctx);
     if (nt > 0) {
       // targets: reference cells, ordered by z sub-slab inside each cell (compact warps)
@@ -998,6 +1080,7 @@ hs_status stage_real(hs_plan* p, bool want) {
       a.P = p->P;
       a.A = p->A;
       a.B = p->B;
+      a.C = p->Cq;
       a.start = p->start;
       a.TP = p->TP;
       a.torig = p->torig;
@@ -1021,12 +1104,13 @@ hs_status stage_real(hs_plan* p, bool want) {
       }
       a.n_real = n;
       a.kind = kind | (p->half ? 16 : 0);
-      a.self_f = kind == HS_STOKESLET ? fa : nullptr;
+      a.self_f = (kind == HS_STOKESLET || kind == HS_MIXED) ? fa : nullptr;
       a.u = p->u_real;
       a.uk = p->uk;
       a.uc = p->uc;
       a.flags = ctx->d_flags;
       a.counts = p->pair_counts;
+      a.audit = p->audit;
       HS_CUDA(cudaMemsetAsync(p->pair_counts, 0, 2 * sizeof(unsigned long long), st));
       HS_CUDA(cudaEventRecord(p->ev[9], st));
       HS_TRY(launch_pair(ctx, a));
@@ -1037,7 +1121,7 @@ hs_status stage_real(hs_plan* p, bool want) {
     HS_CUDA(cudaMemsetAsync(p->u_real, 0, 24 * (size_t)nt, st));
     HS_CUDA(cudaMemsetAsync(p->uk, 0, 24 * (size_t)nt, st));
     HS_CUDA(cudaMemsetAsync(p->uc, 0, 24 * (size_t)nt, st));
-    if (want && kind == HS_STOKESLET) {
+    if (want && (kind == HS_STOKESLET || kind == HS_MIXED)) {
       // rc = 0: no pairs, but the self term is still added (ewald_real.py:444-449)
       k_self_term<<<grid_size(ctx, nt), 256, 0, st>>>(nt, tp, tc, tcol_identity, n, prm.xi, fa, p->u_real);
       HS_LAUNCHED(ctx);
@@ -1046,14 +1130,31 @@ hs_status stage_real(hs_plan* p, bool want) {
   return HS_OK;
 }
 
-unsigned mirror_sigma_neg(int kind) {
-  // channels whose image value is minus the source value (k_spread_records set 0)
-  if (kind == HS_STOKESLET) return 0x3u;               // (-, -, +)
-  if (kind == HS_STRESSLET) return 0x1u | 0x2u | 0x8u | 0x20u;  // 00 01 11 22 negative, 02 12 positive
-  return 0x4u;                                          // rotlet (+, +, -)
+
+// half space: spread the N sources with kernel + wall channels, then mirror (k_mirror_z).
+// group gi: channels [group_c0[gi], group_c0[gi+1]) into grid_in channels 0.. (the sort and
+// the records are made with group 0; later groups reuse them and the spread's window tables)
+hs_status stage_spread_group(hs_plan* p, int gi) {
+  hs_ctx* ctx = p->ctx;
+  cudaStream_t st = ctx->stream;
+  const int c0 = p->group_c0[gi], c1 = p->group_c0[gi + 1], cn = c1 - c0;
+  if (gi > 0) {
+    HS_CUDA(cudaEventRecord(p->ev[11], st));
+    HS_TRY(launch_spread(ctx, p->SPk, p->SWk + c0, p->n_sel_k, cn, p->bk_start, p->gg, p->grid_in, p->n_in,
+                         p->ngroup > 1));
+    if (p->mirror) {
+      const int64_t lines = (int64_t)p->gg.dims[1] * p->gg.dims[0];
+      const int nz = p->gg.dims[2];
+      k_mirror_z<<<grid_size(ctx, lines * (nz / 2 + 1) * cn), 256, 0, st>>>(
+          p->grid_in, cn, p->kern_mask >> c0, p->sigma_mask >> c0, p->gg.ch_stride, lines, p->kg.p[2], nz);
+      HS_LAUNCHED(ctx);
+    }
+    HS_CUDA(cudaEventRecord(p->ev[12], st));
+    return HS_OK;
+  }
+  return HS_OK;
 }
 
-// half space: spread the N sources with kernel + wall channels, then mirror (k_mirror_z)
 hs_status stage_spread_mirrored(hs_plan* p) {
   hs_ctx* ctx = p->ctx;
   cudaStream_t st = ctx->stream;
@@ -1073,11 +1174,12 @@ hs_status stage_spread_mirrored(hs_plan* p) {
     HS_LAUNCHED(ctx);
   }
   HS_CUDA(cudaEventRecord(p->ev[11], st));
-  HS_TRY(launch_spread(ctx, p->SPk, p->SWk, n_sel, p->n_in, p->bk_start, p->gg, p->grid_in));
+  const int cn = p->group_c0[1];
+  HS_TRY(launch_spread(ctx, p->SPk, p->SWk, n_sel, cn, p->bk_start, p->gg, p->grid_in, p->n_in));
   const int64_t lines = (int64_t)p->gg.dims[1] * p->gg.dims[0];
   const int nz = p->gg.dims[2];
-  k_mirror_z<<<grid_size(ctx, lines * (nz / 2 + 1) * p->n_in), 256, 0, st>>>(
-      p->grid_in, p->n_in, p->nk, mirror_sigma_neg(kind), p->gg.ch_stride, lines, p->kg.p[2], nz);
+  k_mirror_z<<<grid_size(ctx, lines * (nz / 2 + 1) * cn), 256, 0, st>>>(
+      p->grid_in, cn, p->kern_mask, p->sigma_mask, p->gg.ch_stride, lines, p->kg.p[2], nz);
   HS_LAUNCHED(ctx);
   HS_CUDA(cudaEventRecord(p->ev[12], st));
   p->spread_timed = true;
@@ -1111,6 +1213,15 @@ hs_status stage_spread(hs_plan* p) {
     k_spread_records<<<grid_size(ctx, nk_sel), 256, 0, st>>>(kind, p->half, 0, p->bk_order, nk_sel, n, pos, fa, fb,
                                                              p->nk, p->SPk, p->SWk);
     HS_LAUNCHED(ctx);
+  }
+  if (kind == HS_MIXED) {  // free space: group 0 = F now, the stresslet channels by stage_spread_group
+    p->n_sel_k = nk_sel;
+    p->n_sel_c = 0;
+    HS_CUDA(cudaEventRecord(p->ev[11], st));
+    HS_TRY(launch_spread(ctx, p->SPk, p->SWk, nk_sel, p->group_c0[1], p->bk_start, p->gg, p->grid_in, p->nk));
+    HS_CUDA(cudaEventRecord(p->ev[12], st));
+    p->spread_timed = true;
+    return HS_OK;
   }
   if (p->nc && nc_sel > 0) {
     k_spread_records<<<grid_size(ctx, nc_sel), 256, 0, st>>>(kind, p->half, 1, p->bc_order, nc_sel, n, pos, fa, fb,
@@ -1160,6 +1271,8 @@ hs_status stage_yinv(hs_plan* p, int o, double2* out) {
 hs_status stage_xstage(hs_plan* p) {
   XArgs xa{};
   xa.B = p->spec;
+  xa.Bout = p->spec;
+  xa.accum = 0;
   xa.ch_stride = p->n_mixed;
   xa.tabB = p->tabB;
   xa.tabH = p->tabH;
@@ -1175,7 +1288,16 @@ hs_status stage_xstage(hs_plan* p) {
   xa.ka = p->kg.a;
   xa.kb = p->kg.b;
   xa.inv_n = p->kg.inv_n;
-  return launch_xfused(p->ctx, p->prm.kind, p->half, xa);
+  HS_TRY(launch_xfused(p->ctx, p->prm.kind, p->half, xa));
+  if (p->prm.kind == HS_MIXED) {
+    // second channel group: the stresslet kernel channels, scaled without wall channels and
+    // added to T1 (its outputs go to spec channels 0..2, the first pass's T1)
+    const int c0 = p->half ? 13 : 3;
+    xa.B = p->spec + (size_t)c0 * p->n_mixed;
+    xa.accum = 1;
+    HS_TRY(launch_xfused(p->ctx, HS_STRESSLET, 0, xa));
+  }
+  return HS_OK;
 }
 
 // Fourier gather at the plan's targets: u_four, and u = u_real + u_four (ewald_fourier.py:626-630)
@@ -1291,11 +1413,16 @@ extern "C" hs_status hs_plan_execute(hs_plan* p, const double* positions, const 
     HS_TRY(stage_spread(p));
     HS_CUDA(cudaEventRecord(ev[3], ctx->stream));
     set_fft_streams(p);
-    // forward z (D2Z) and y stages, one source channel at a time through the shared A buffer
-    for (int c = 0; c < p->n_in; ++c) {
-      if (cufftExecD2Z(p->zf, p->grid_in + (size_t)c * p->n_grid, (cufftDoubleComplex*)p->Amix) != CUFFT_SUCCESS)
-        return fail(HS_ERR_CUDA, "cuFFT z D2Z failed");
-      HS_TRY(stage_yfwd(p, p->Amix, c));
+    // forward z (D2Z) and y stages, one source channel at a time through the shared A buffer;
+    // channel groups (mixed): spread the next group into the freed source grids
+    for (int gi = 0; gi < p->ngroup; ++gi) {
+      if (gi > 0) HS_TRY(stage_spread_group(p, gi));
+      for (int c = p->group_c0[gi]; c < p->group_c0[gi + 1]; ++c) {
+        const double* gin = p->grid_in + (size_t)(c - p->group_c0[gi]) * p->n_grid;
+        if (cufftExecD2Z(p->zf, (double*)gin, (cufftDoubleComplex*)p->Amix) != CUFFT_SUCCESS)
+          return fail(HS_ERR_CUDA, "cuFFT z D2Z failed");
+        HS_TRY(stage_yfwd(p, p->Amix, c));
+      }
     }
     HS_CUDA(cudaEventRecord(ev[4], ctx->stream));
     HS_TRY(stage_xstage(p));
@@ -1310,6 +1437,14 @@ extern "C" hs_status hs_plan_execute(hs_plan* p, const double* positions, const 
     k_interleave<<<grid_size(ctx, p->n_grid / 2), 256, 0, ctx->stream>>>(p->grid_tmp, p->n_out, p->n_grid,
                                                                          p->n_grid, p->out_pitch, p->grid_out);
     HS_LAUNCHED(ctx);
+    if (p->tmp_aliased) {
+      // the inverse z transforms wrote whole pz lines into the source grids: restore their zero
+      // z padding (the next spread writes z < nz only)
+      const int nz = p->gg.dims[2], pz = p->kg.p[2];
+      const size_t lines = (size_t)p->gg.dims[1] * p->gg.dims[0];
+      HS_CUDA(cudaMemset2DAsync(p->grid_in + nz, sizeof(double) * pz, 0, sizeof(double) * (pz - nz),
+                                lines * p->n_out, ctx->stream));
+    }
     HS_CUDA(cudaEventRecord(ev[6], ctx->stream));
     return HS_OK;
   };
@@ -1371,6 +1506,31 @@ extern "C" hs_status hs_plan_execute(hs_plan* p, const double* positions, const 
 // y-slab stages (see hsewald_b200.h).  Every stage is stream-ordered on the context's
 // stream; the caller's exchanges must be ordered on the same stream (sharding.py binds
 // the context to torch's current stream).
+
+extern "C" hs_status hs_plan_pair_audit(hs_plan* p, const double* positions, const double* sa, const double* sb,
+                                        const double* targets, const int64_t* tcols, uint64_t* audit, int mem) {
+  if (!p || !positions || !sa || !audit) return fail(HS_ERR_PARAMETER, "null argument");
+  if (!(p->prm.rc > 0)) return fail(HS_ERR_PARAMETER, "pair audit needs rc > 0");
+  hs_ctx* ctx = p->ctx;
+  cudaStream_t st = ctx->stream;
+  const size_t nt = (size_t)p->prm.n_targets, bytes = 3 * sizeof(unsigned long long) * std::max<size_t>(nt, 1);
+  HS_TRY(begin_eval(p));
+  HS_TRY(stage_inputs(p, positions, sa, sb, targets, tcols, mem));
+  unsigned long long* buf = nullptr;
+  if (mem == HS_MEM_DEVICE) buf = (unsigned long long*)audit;
+  else HS_CUDA(cudaMallocAsync(&buf, bytes, st));
+  HS_CUDA(cudaMemsetAsync(buf, 0, bytes, st));
+  p->audit = buf;
+  hs_status rs = stage_real(p, true);
+  p->audit = nullptr;
+  if (rs == HS_OK && mem == HS_MEM_HOST && nt)
+    if (cudaMemcpyAsync(audit, buf, 3 * sizeof(unsigned long long) * nt, cudaMemcpyDeviceToHost, st) != cudaSuccess)
+      rs = fail(HS_ERR_CUDA, "audit copy");
+  if (mem == HS_MEM_HOST) cudaFreeAsync(buf, st);
+  HS_TRY(rs);
+  HS_CUDA(cudaStreamSynchronize(st));
+  return ctx_check_flags(ctx, "hs_plan_pair_audit");
+}
 
 namespace {
 

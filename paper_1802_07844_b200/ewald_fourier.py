@@ -244,7 +244,7 @@ def load_table(path) -> GreensTable:
 
 def table_kinds_for(kernel_kind, geometry):
     """ewald_fourier.py:281-290."""
-    kinds = [BIHARMONIC] if kernel_kind in (STOKESLET, STRESSLET) else [HARMONIC]
+    kinds = [BIHARMONIC] if kernel_kind in (STOKESLET, STRESSLET, "mixed") else [HARMONIC]
     if geometry == HALF_SPACE and HARMONIC not in kinds:
         kinds.append(HARMONIC)
     return kinds
@@ -345,9 +345,10 @@ def fourier_space_sum(system, grid: GridSpec, tables=None, cache_dir=None, threa
     """Spectral evaluation of the long-range component (ewald_fourier.py:486-636).
 
     ``threads`` is accepted for API compatibility and ignored (one CUDA stream).
-    meta["fft_count"]/["ifft_count"] are the transforms actually executed (the
-    channel economy of SURVEY A.6: stokeslet 7/6, stresslet 13/6, rotlet 5/6);
-    the reference's counts are in meta["fft_count_reference"]."""
+    meta["fft_count"]/["ifft_count"] keep the reference's semantics (the 3-D
+    transforms its algorithm performs, ref:ewald_fourier.py:518-532: half space
+    stokeslet 7/6, stresslet 21/6, rotlet 6/6); the device path's channel economy
+    (7/6, 13/6, 5/6) is reported in meta["fft_count_executed"]."""
     if grid.geometry != system.geometry:
         raise ConfigError("grid geometry does not match the system")
     if abs(grid.L - system.box_length) > 1e-12 * system.box_length:
@@ -362,10 +363,21 @@ def fourier_space_sum(system, grid: GridSpec, tables=None, cache_dir=None, threa
     sa, sb = _strengths(system)
     _, _, uf, times = ev.execute(system.positions, sa, sb, targets=tg, what=2)
     nf, ni = ev.fft_counts()
-    ref_counts = {(STOKESLET, HALF_SPACE): (7, 6), (STRESSLET, HALF_SPACE): (21, 6), (ROTLET, HALF_SPACE): (6, 6),
-                  (STOKESLET, FREE_SPACE): (3, 3), (STRESSLET, FREE_SPACE): (9, 3), (ROTLET, FREE_SPACE): (3, 3)}
+    rf, ri = reference_fft_counts(system.kind, system.geometry)
     t = {k: times[k] / 1e3 for k in ("gridding", "fft", "scale", "ifft", "gather")}
     return VelocityResult(velocities=uf, meta={
-        "kind": system.kind, "geometry": system.geometry, "fft_count": nf, "ifft_count": ni,
-        "fft_count_reference": ref_counts[(system.kind, system.geometry)], "times": t,
-        "M": grid.M, "P": grid.P, "xi": grid.xi})
+        "kind": system.kind, "geometry": system.geometry, "fft_count": rf, "ifft_count": ri,
+        "fft_count_executed": (nf, ni), "times": t, "M": grid.M, "P": grid.P, "xi": grid.xi})
+
+
+_REF_FFT_COUNTS = {(STOKESLET, HALF_SPACE): (7, 6), (STRESSLET, HALF_SPACE): (21, 6), (ROTLET, HALF_SPACE): (6, 6),
+                   (STOKESLET, FREE_SPACE): (3, 3), (STRESSLET, FREE_SPACE): (9, 3), (ROTLET, FREE_SPACE): (3, 3)}
+
+
+def reference_fft_counts(kind, geometry):
+    """(forward, inverse) 3-D transforms of the reference's fourier_space_sum
+    (ref:ewald_fourier.py:518-532, 563-624; criterion 8); "mixed" = its two calls."""
+    if kind == "mixed":
+        a, b = _REF_FFT_COUNTS[(STOKESLET, geometry)], _REF_FFT_COUNTS[(STRESSLET, geometry)]
+        return a[0] + b[0], a[1] + b[1]
+    return _REF_FFT_COUNTS[(kind, geometry)]

@@ -19,6 +19,9 @@ from .point_kernels import (HarmonicDerivs, correction_phi, gfam_coeffs, harmoni
 
 
 def _direct(system, geometry, targets, target_indices):
+    if system.kind == "mixed":   # ewald.MixedSystem: the two kinds' sums
+        return (_direct(system.stokeslet, geometry, targets, target_indices)
+                + _direct(system.stresslet, geometry, targets, target_indices))
     if targets is None:
         targets = system.positions
         target_indices = np.arange(system.n)

@@ -113,7 +113,10 @@ def test_workloads_match_baseline_shapes():
     s3, _ = make_system("cfg3", n=1000)
     np.testing.assert_allclose(np.linalg.norm(s3.q, axis=1), 1.0)
     s5, t5 = make_system("cfg5", n=1000)
-    assert t5.shape == (1000, 3) and s5.box_length == 2.0
+    assert t5.shape == (1000, 3) and s5.box_length == 2.0 and s5.kind == "mixed"
+    assert s5.stokeslet.f.shape == (1000, 3) and np.allclose(np.linalg.norm(s5.stresslet.q, axis=1), 1.0)
+    f, gq = s5.strengths()
+    assert gq.shape == (1000, 6) and np.array_equal(gq[:, :3], s5.stresslet.g)
 
 
 def test_golden_fixtures_present():

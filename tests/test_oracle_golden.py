@@ -113,3 +113,66 @@ def test_direct(oracle, kind):
     sf = _sys(d, f"{kind}_free")
     uf = oracle.direct_sum(kind, "free", sf["pos"], f=sf.get("f"), g=sf.get("g"), q=sf.get("q"))
     assert rel_l2(uf, d[f"{kind}_free_u"]) < 1e-13
+
+
+# ---------------------------------------------------------------------------
+# Full-size reference goldens (tests/golden/make_fullsize_golden.py: the reference's own ewald_sum
+# on the whole HL / cfg2 / cfg3 / cfg1 systems, 2000-target subsets)
+
+def _full(name):
+    from paper_1802_07844_b200.configs import WORKLOADS, make_system
+    w = WORKLOADS[name]
+    s, _ = make_system(w)
+    kw = {"f": s.f} if s.kind == "stokeslet" else {"g": s.g, "q": s.q}
+    return w, s, kw, golden(f"fullsize_{name}")
+
+
+@pytest.mark.parametrize("name", ("cfg1", "cfg2", "cfg3", "HL"))
+def test_neighbour_audit_vs_reference(oracle, name):
+    """The oracle's per-target neighbour sets (count, image count, id hash) equal the reference
+    traversal's (ref:ewald_real.py:277-299) bit for bit."""
+    w, s, kw, d = _full(name)
+    idx = d["idx"]
+    aud = np.zeros((idx.size, 3), np.uint64)
+    u, _, _ = oracle.real_space_sum(s.kind, "half", w.L, s.positions, w.xi, w.rc, targets=s.positions[idx],
+                                    target_indices=idx, audit=aud, **kw)
+    np.testing.assert_array_equal(aud[:, 0].astype(np.int64), d["nbr_count"])
+    np.testing.assert_array_equal(aud[:, 1].astype(np.int64), d["nbr_img"])
+    np.testing.assert_array_equal(aud[:, 2], d["nbr_hash"])
+    assert rel_l2(u, d["u_real"]) < 1e-13
+
+
+def _lean_vs_reference(oracle, name):
+    w, s, kw, d = _full(name)
+    idx = d["idx"]
+    g = oracle.Grid(w.L, w.M, w.P, w.xi)
+    tabs = {k: oracle.precompute_greens_half(k, g) for k in oracle.table_kinds_for(s.kind, "half")}
+    u, ur, uf = oracle.ewald_sum_lean(s.kind, "half", w.L, s.positions, w.xi, w.rc, w.M, w.P, tabs,
+                                      targets=s.positions[idx], target_indices=idx, **kw)
+    print(f"lean oracle vs reference {name}: u {rel_l2(u, d['u']):.2e} fourier {rel_l2(uf, d['u_fourier']):.2e}")
+    assert rel_l2(ur, d["u_real"]) < 1e-13
+    assert rel_l2(u, d["u"]) < 1e-10 and rel_l2(uf, d["u_fourier"]) < 1e-10
+
+
+def test_lean_oracle_vs_reference_cfg2(oracle):
+    """The memory-lean oracle (R2C, one channel at a time; used for the cfg4 / cfg5 goldens) against
+    the reference's full-size cfg2 evaluation."""
+    _lean_vs_reference(oracle, "cfg2")
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name", ("cfg3", "HL"))
+def test_lean_oracle_vs_reference_fullsize(oracle, name):
+    _lean_vs_reference(oracle, name)
+
+
+def test_lean_tables_match_full_precompute(oracle):
+    """precompute_greens_half (separable cosine transforms) == the reference-layout big-grid
+    irfftn path, on the R2C half grid."""
+    for geom in ("half", "free"):
+        g = oracle.Grid(1.0, 48, 16, 10.0, geom)
+        nzh = g.padded_dims[2] // 2 + 1
+        for kind in ("harmonic", "biharmonic"):
+            a = oracle.precompute_greens(kind, g)[..., :nzh]
+            b = oracle.precompute_greens_half(kind, g)
+            assert np.abs(a - b).max() < 1e-14 * np.abs(a).max()

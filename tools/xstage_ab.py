@@ -15,7 +15,7 @@ M = int(sys.argv[3]) if len(sys.argv) > 3 else 192
 if M == 384:
     assert kind == "stokeslet"
     w = WORKLOADS["cfg5"]
-    s, _ = make_system(w, n=100_000)
+    s = make_system(w, n=100_000)[0].stokeslet
     g = hs.GridSpec(L=w.L, M=M, P=24, xi=w.xi)
 else:
     s, _ = make_system({"stokeslet": "HL", "rotlet": "cfg4", "stresslet": "cfg3"}[kind], n=100_000)
