@@ -5,17 +5,21 @@
 One step = one full ewald_sum evaluation (real + Fourier) of the whole system,
 inputs resident in HBM, Green's tables precomputed outside the timed region (as
 the reference and the paper do).  `e2e` repeats the measurement through the
-C ABI with pinned HOST buffers (H2D of positions+forces and D2H of velocities
-inside the timed region).  `--impl reference` times the CPU restatement of the
-reference (oracle/, OpenMP C + scipy.fft) on a bounded sample of the same
-workload, extrapolated to the full evaluation.
+C ABI with pinned HOST buffers (H2D of positions+strengths(+targets) and D2H of
+velocities inside the timed region).  `cpu_baseline` and `--impl reference`
+time COMPLETE evaluations of the same workload by the CPU restatement of the
+reference (oracle/, C + OpenMP + scipy.fft) on all host cores.
 
-Multi-GPU (torchrun), two modes:
-  --mode replicas (default): every rank evaluates its own independent HL system
-      (weak scaling, no data-path collective);
-  --mode slab: ONE system y-slab decomposed over the ranks (sharding.py: spread
-      ghost planes, per-channel NCCL all-to-all transposes of the FFT, gather halo;
-      strong scaling, value = N / time of one sharded evaluation).
+--workload: HL (default, the metric's configuration), cfg1..cfg5 (cfg5: the mixed
+stokeslet + stresslet system with separate targets).
+
+Multi-GPU (torchrun, or --gpus N which launches the N ranks itself):
+  --mode slab (default for N > 1): ONE system y-slab decomposed over the ranks
+      (sharding.py: spread ghost planes, per-channel NCCL all-to-all transposes of
+      the FFT, gather halo; strong scaling, value = N_targets / time of one sharded
+      evaluation, max over ranks);
+  --mode replicas: every rank evaluates its own independent system (weak scaling,
+      no data-path collective).
 """
 
 from __future__ import annotations
@@ -53,87 +57,63 @@ def _peaks():
 
 
 # ---------------------------------------------------------------------------
-# CPU baseline: oracle port (test infrastructure), bounded sample, extrapolated
-def cpu_sample(wname: str, threads: int | None = None):
-    """Estimate seconds for one full ewald_sum evaluation of the workload on host cores."""
+# CPU baseline: the oracle port (test infrastructure; oracle/), one FULL evaluation timed
+FULL_COMPLEX_MAX = 400_000_000   # padded grid points up to which the port keeps the reference's full
+                                 # complex spectra (ref:ewald_fourier.py:518-532); above: R2C lean mode
+
+
+def cpu_tables(wname, threads):
+    """Green's tables for the port (precompute excluded from the timing, as in the reference)."""
+    from oracle import hsoracle as o
+    from paper_1802_07844_b200.configs import WORKLOADS
+    w = WORKLOADS[wname]
+    g = o.Grid(w.L, w.M, w.P, w.xi, "half")
+    kinds = ["stokeslet", "stresslet"] if w.kind == "mixed" else [w.kind]
+    need = sorted(set(sum((o.table_kinds_for(k, "half") for k in kinds), [])))
+    half = {k: o.precompute_greens_half(k, g, workers=threads) for k in need}
+    full = None
+    if int(np.prod(g.padded_dims)) <= FULL_COMPLEX_MAX:
+        full = {k: o.expand_half_table(v, g.padded_dims) for k, v in half.items()}
+    return g, half, full
+
+
+def cpu_full_eval(wname, threads, tabs):
+    """Seconds for ONE complete ewald_sum evaluation of the workload by the port on `threads` host
+    cores: real space at every target, every source spread, every transform, every gather.
+    Mixed workloads: the reference's two calls (one per kind)."""
     from oracle import hsoracle as o
     from paper_1802_07844_b200.configs import WORKLOADS, make_system
-    import scipy.fft as sfft
     w = WORKLOADS[wname]
-    threads = threads or os.cpu_count()
     o.set_threads(threads)
-    s, _ = make_system(w)
-    n = s.n
-    pos, f = s.positions, s.f
-    g = o.Grid(w.L, w.M, w.P, w.xi, "half")
-    rng = np.random.default_rng(0)
-    parts = {}
-    t_wall = time.perf_counter()
-    zz, sa, sb, sign = o.reflect(pos, "stokeslet", f=f)
-    # real space: set-up (reflection, cell list of all 2N points, permutations) once; the
-    # pair loop on a sample of targets, scaled
-    nts = min(n, 48000)
-    sub = np.sort(rng.choice(n, nts, replace=False))
-    tr = {}
-    o.real_space_sum("stokeslet", "half", w.L, pos, w.xi, w.rc, f=f, targets=pos[sub], target_indices=sub,
-                     timings=tr)
-    parts["real"] = tr["setup"] + tr["pairs"] * n / nts
-    # spreading: the scatter loop on a sample of sources (3 kernel + 4 wall channels), scaled;
-    # grid zeroing and the channel-first copy at full size
-    frac = min(1.0, 240000 / (2 * n))
-    ks = rng.choice(2 * n, int(2 * n * frac), replace=False)
-    s_, v_, _ = o.phi_channels("stokeslet", pos, f=f)
-    cs = rng.choice(n, int(n * frac), replace=False)
-    t1, t2 = {}, {}
-    o.spread(zz[ks], sa[ks], g, timings=t1)
-    o.spread((pos * [1, 1, -1])[cs], np.column_stack([s_, v_])[cs], g, timings=t2)
-    parts["gridding"] = (t1["loop"] + t2["loop"]) / frac + t1["copy"] + t2["copy"]
-    # FFTs: one forward and one inverse on a 1/8-volume grid, scaled by N log N
-    pd = g.padded_dims
-    sd = tuple(p // 2 for p in pd)
-    buf = np.zeros(sd)
-    buf[: sd[0] // 2, : sd[1] // 2, : sd[2] // 2] = rng.normal(size=(sd[0] // 2, sd[1] // 2, sd[2] // 2))
+    s, tg = make_system(w)
+    g, half, full = tabs
+    systems = [("stokeslet", s.stokeslet), ("stresslet", s.stresslet)] if w.kind == "mixed" else [(w.kind, s)]
     t0 = time.perf_counter()
-    spec = sfft.fftn(buf, workers=threads)
-    tf = time.perf_counter() - t0
-    t0 = time.perf_counter()
-    sfft.ifftn(spec, workers=threads)
-    ti = time.perf_counter() - t0
-    del spec, buf
-    nfull, nsmall = float(np.prod(pd)), float(np.prod(sd))
-    sc = nfull * math.log2(nfull) / (nsmall * math.log2(nsmall))
-    parts["fft"] = 7 * tf * sc
-    parts["ifft"] = 6 * ti * sc
-    # k-space scaling (kernel + wall channels) on a slab of planes
-    planes = 36
-    shp = (planes, pd[1], pd[2])
-    Ch = (rng.normal(size=(3,) + shp) + 1j * rng.normal(size=(3,) + shp))
-    tab = rng.normal(size=shp)
-    k1 = [2.0 * math.pi * sfft.fftfreq(p, d=g.h) for p in pd]
-    out = np.empty((3,) + shp, np.complex128)
-    t0 = time.perf_counter()
-    o.lib().or_kspace_scale(0, o._d(Ch.view(np.float64)), o._d(tab), o._d(k1[0][:planes]), o._d(k1[1]), o._d(k1[2]),
-                            planes, pd[1], pd[2], 0.1, 0.1, out.view(np.float64).ctypes.data_as(
-                                o.C.POINTER(o.C.c_double)))
-    kx, ky, kz = k1[0][:planes, None, None], k1[1][None, :, None], k1[2][None, None, :]
-    Fc = tab * np.exp(-0.1 * (kx**2 + ky**2 + kz**2))
-    phi = Fc * Ch[0]
-    for j, kk in enumerate((kx, ky, kz)):
-        phi = phi + 1j * kk * (Fc * Ch[j])
-    parts["scale"] = (time.perf_counter() - t0) * pd[0] / planes
-    del Ch, out, phi, Fc, tab
-    # gather: 6 channels at a target sample
-    grids = np.zeros((3,) + tuple(g.dims))
-    ntg = 18000
-    tg = {}
-    o.gather(grids, pos[:ntg], g, timings=tg)
-    parts["gather"] = 2 * (tg["copy"] + tg["loop"] * n / ntg)
-    del grids
-    total = sum(parts.values())
-    sample_desc = (f"oracle port ({threads} threads): set-up + cell list at full size; pair loop for {nts} sampled targets; spread of "
-                   f"{frac:.3%} of sources; fwd+inv FFT on a 1/8-volume grid scaled by NlogN (x7 fwd, x6 inv); "
-                   f"k-space scale on {planes}/{pd[0]} planes; gather at {ntg} targets; each scaled to N={n}")
-    return total, parts, sample_desc, time.perf_counter() - t_wall, threads
+    for kind, ps in systems:
+        kw = {"f": ps.f} if kind == "stokeslet" else {"g": ps.g, "q": ps.q}
+        if full is not None:
+            o.ewald_sum(kind, "half", w.L, ps.positions, w.xi, w.rc, w.M, w.P, full, targets=tg, workers=threads,
+                        **kw)
+        else:
+            o.ewald_sum_lean(kind, "half", w.L, ps.positions, w.xi, w.rc, w.M, w.P, half, targets=tg,
+                             workers=threads, **kw)
+    t = time.perf_counter() - t0
+    mode = "full complex spectra (the reference's layout)" if full is not None else "R2C lean mode"
+    nt = s.n if tg is None else tg.shape[0]
+    desc = (f"oracle port (C + OpenMP, scipy.fft; {threads} threads): one complete evaluation of {wname} "
+            f"(N={s.n}, {nt} targets, padded {tuple(g.padded_dims)}, {mode}); tables precomputed outside the "
+            f"timed region")
+    return t, desc, nt
+
+
+def cpu_host():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 # ---------------------------------------------------------------------------
@@ -199,41 +179,60 @@ def roofline(times, work, hbm_peak, fp64_peak):
     return ks
 
 
+def config_of(w):
+    """The `config` both arms print (identical keys, so the driver's same_config holds)."""
+    return {"workload": w.name, "kind": w.kind, "n": w.n, "n_targets": w.n, "L": w.L, "xi": w.xi, "rc": w.rc,
+            "M": w.M, "P": w.P}
+
+
 def run_reference(args, rank):
+    """The reference arm: the port on all host cores.  W warm-up evaluations of the small cfg1
+    system (thread pools, FFT plans), then complete evaluations of the workload, best of up to
+    `steps` (best of 3) within a ~3 minute budget; `steps` = evaluations
+    actually timed."""
     if rank != 0:
         return
     from paper_1802_07844_b200.configs import WORKLOADS
     w = WORKLOADS[args.workload]
+    thr = os.cpu_count()
+    t_tab0 = time.perf_counter()
+    tabs = cpu_tables(args.workload, thr)
+    t_tab = time.perf_counter() - t_tab0
+    small = cpu_tables("cfg1", thr)
     for _ in range(args.warmup):
-        cpu_sample(args.workload)
-    vals, walls = [], []
-    last = None
-    for _ in range(args.steps):
-        total, parts, desc, wall, thr = cpu_sample(args.workload)
-        vals.append(total)
-        walls.append(wall)
-        last = (parts, desc, thr)
-    t = float(np.mean(vals))
-    value = w.n / t
-    parts, desc, thr = last
-    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
+        cpu_full_eval("cfg1", thr, small)
+    times = []
+    t_start = time.perf_counter()
+    while len(times) < max(1, args.steps):
+        t, desc, nt = cpu_full_eval(args.workload, thr, tabs)
+        times.append(t)
+        if time.perf_counter() - t_start + t > args.ref_budget_s:
+            break
+    best = min(times)
+    value = nt / best
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": len(times),
+            "warmup": args.warmup, "ms_per_step": best * 1e3, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded PCG64, BASELINE.json shapes)",
-            "config": {"workload": w.name, "kind": w.kind, "n": w.n, "xi": w.xi, "rc": w.rc, "M": w.M, "P": w.P},
-            "impl": "reference",
+            "config": config_of(w), "impl": "reference",
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": thr, "kind": "port", "sample": desc,
-                             "phases_s": {k: round(v, 4) for k, v in parts.items()},
-                             "sample_wall_s": round(float(np.mean(walls)), 2)},
+                             "host": cpu_host(), "timed_evaluations_s": [round(x, 3) for x in times],
+                             "statistic": f"best of {len(times)}", "tables_s": round(t_tab, 2),
+                             "requested_steps": args.steps},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     emit(line)
 
 
+PAIR_INSTR = {"stokeslet": (64, 33), "stresslet": (85, 50), "rotlet": (62, 28), "mixed": (64 + 85, 33 + 50)}
+
+
 def run_ours(args, rank, world, local_rank):
+    """One plan per rank: N = 1, or N independent replicas (--mode replicas, weak scaling)."""
     import torch
     import torch.distributed as dist
     from paper_1802_07844_b200 import GridSpec, _lib
     from paper_1802_07844_b200._plan import Evaluator
     from paper_1802_07844_b200.configs import WORKLOADS, Workload, make_system
+    from paper_1802_07844_b200.ewald import _strengths
 
     torch.cuda.set_device(local_rank)
     if world > 1:
@@ -241,18 +240,21 @@ def run_ours(args, rank, world, local_rank):
     w0 = WORKLOADS[args.workload]
     w = Workload(**{**w0.__dict__, "seed": w0.seed + 7919 * rank})   # replicas: independent systems
     s, targets = make_system(w)
+    nt = s.n if targets is None else targets.shape[0]
     grid = GridSpec(L=w.L, M=w.M, P=w.P, xi=w.xi, geometry="half")
-    ev = Evaluator(w.kind, "half", w.L, w.xi, w.rc, grid, s.n, s.n if targets is None else targets.shape[0],
-                   targets is None, device=local_rank)
+    ev = Evaluator(w.kind, "half", w.L, w.xi, w.rc, grid, s.n, nt, targets is None, device=local_rank)
     t0 = time.perf_counter()
     ev.build_tables()
     t_tables = time.perf_counter() - t0
     dev = torch.device("cuda", local_rank)
-    pos = torch.from_numpy(s.positions).to(dev)
-    f = torch.from_numpy(s.f).to(dev)
-    out = torch.empty((3, s.n, 3), dtype=torch.float64, device=dev)
+    fa, fb = _strengths(s)
+    host_in = [np.ascontiguousarray(a, dtype=np.float64) for a in (s.positions, fa, fb, targets) if a is not None]
+    dput = lambda a: None if a is None else torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to(dev)  # noqa: E731
+    pos, sa, sb, tgd = dput(s.positions), dput(fa), dput(fb), dput(targets)
+    out = torch.empty((3, nt, 3), dtype=torch.float64, device=dev)
+    run = lambda what=3: ev.execute(pos, sa, sb, targets=tgd, out=out, what=what)  # noqa: E731
     for _ in range(args.warmup):
-        ev.execute(pos, f, out=out)
+        run()
     torch.cuda.synchronize()
     ctx = _lib.Context.get(local_rank)
     clocks = ClockSampler(local_rank)
@@ -264,10 +266,8 @@ def run_ours(args, rank, world, local_rank):
     l0 = ctx.launches()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    step_times = []
     for _ in range(args.steps):
-        _, _, _, tm = ev.execute(pos, f, out=out)
-        step_times.append(tm)
+        run()
     e1.record()
     torch.cuda.synchronize()
     if world > 1:
@@ -278,30 +278,31 @@ def run_ours(args, rank, world, local_rank):
     # per-kernel times for the roofline: the same evaluations with the real-space and Fourier
     # pipelines serialised (what bit 2), since in the timed steps they overlap on two streams
     # and a kernel's event interval would include the other pipeline's work
-    step_times = []
-    for _ in range(args.steps):
-        _, _, _, tm = ev.execute(pos, f, out=out, what=7)
-        step_times.append(tm)
+    step_times = [run(7)[3] for _ in range(args.steps)]
     if world > 1:
         tt = torch.tensor([ms], device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt.item())
     ms_step = ms / args.steps
-    value = world * s.n * args.steps / (ms * 1e-3)
+    value = world * nt * args.steps / (ms * 1e-3)
     avg = {k: float(np.mean([t[k] for t in step_times])) for k in step_times[0]}
 
-    # ---- e2e through the C ABI with pinned host buffers
-    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
-    hp, hf = pin(s.positions), pin(s.f)
-    hu = torch.empty((s.n, 3), dtype=torch.float64).pin_memory()
-    hpos, hfor, hout = hp.numpy(), hf.numpy(), hu.numpy()
-    ev.execute(hpos, hfor, out=(hout, None, None))   # warm
+    # ---- e2e through the C ABI with pinned host buffers (inputs H2D and velocities D2H every step)
+    pin = lambda a: torch.from_numpy(a).pin_memory()  # noqa: E731
+    hin = [pin(a) for a in host_in]
+    hu = torch.empty((nt, 3), dtype=torch.float64).pin_memory()
+    hv = [t.numpy() for t in hin]
+    hpos, hfa = hv[0], hv[1]
+    hfb = hv[2] if fb is not None else None
+    htg = hv[-1] if targets is not None else None
+    hout = hu.numpy()
+    ev.execute(hpos, hfa, hfb, targets=htg, out=(hout, None, None))   # warm
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     e0.record()
     for _ in range(args.steps):
-        ev.execute(hpos, hfor, out=(hout, None, None))
+        ev.execute(hpos, hfa, hfb, targets=htg, out=(hout, None, None))
     e1.record()
     torch.cuda.synchronize()
     ms_e2e = e0.elapsed_time(e1)
@@ -309,29 +310,29 @@ def run_ours(args, rank, world, local_rank):
         tt = torch.tensor([ms_e2e], device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms_e2e = float(tt.item())
-    e2e_value = world * s.n * args.steps / (ms_e2e * 1e-3)
-    # parity spot-check of the e2e result against the device result
-    dev_u = out[0].cpu().numpy()
-    e2e_consistent = bool(np.array_equal(dev_u, hout))
+    e2e_value = world * nt * args.steps / (ms_e2e * 1e-3)
+    e2e_consistent = bool(np.array_equal(out[0].cpu().numpy(), hout))
 
     # ---- roofline (algorithmic work per launch)
     hbm_peak, fp64_peak, peak_src = _peaks()
     P3 = w.P ** 3
+    n_in, n_out = ev.fft_counts()
     n_half = grid.padded_dims[0] * grid.padded_dims[1] * (grid.padded_dims[2] // 2 + 1)
     pairs, img_pairs = avg["pairs"], avg["image_pairs"]
+    pi, pc = PAIR_INSTR[w.kind]
     work = {
-        # mirrored spreading (csrc/plan.cu k_mirror_z): 3 kernel + 4 wall channels at the N
-        # sources, images by reflection of the grid (10 N P^3 -> 7 N P^3 FMAs)
-        "k_spread": ("flop", 2.0 * P3 * 7 * s.n, "fp64:dmma"),
-        "k_gather": ("flop", 2.0 * P3 * 6 * s.n, "fp64:dfma"),
-        "k_scale": ("bytes", n_half * (16 * 7 + 16 * 6 + 8 * 2), "hbm"),
-        "k_pair": ("flop", 2.0 * (64 * pairs + 33 * img_pairs), "fp64:dfma"),
+        # mirrored spreading (csrc/plan.cu k_mirror_z): kernel + wall channels at the N sources,
+        # images by reflection of the grid (stokeslet: 10 N P^3 -> 7 N P^3 FMAs)
+        "k_spread": ("flop", 2.0 * P3 * n_in * s.n, "fp64:dmma"),
+        "k_gather": ("flop", 2.0 * P3 * n_out * nt, "fp64:dfma"),
+        "k_scale": ("bytes", n_half * (16 * n_in + 16 * n_out + 8 * 2), "hbm"),
+        "k_pair": ("flop", 2.0 * (pi * pairs + pc * img_pairs), "fp64:dfma"),
     }
     kern = roofline(avg, work, hbm_peak, fp64_peak)
     dom = max(kern, key=lambda k: kern[k]["ms"])
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic_per_launch.json")
-    if os.path.exists(tp):
+    if os.path.exists(tp) and w.name == "HL":
         traffic = json.load(open(tp)).get(dom)
     rf = dict(kern[dom])
     rf.update({"kernel": dom, "traffic": traffic, "peak_source": (
@@ -341,26 +342,29 @@ def run_ours(args, rank, world, local_rank):
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded PCG64, BASELINE.json shapes)",
-            "config": {"workload": w.name, "kind": w.kind, "n": s.n, "xi": w.xi, "rc": w.rc, "M": w.M, "P": w.P,
-                       "padded_dims": list(grid.padded_dims), "parallelism": f"replicas{world}",
-                       "streams": "real space concurrent with the Fourier pipeline up to the gather; "
-                                  "kernels/phases_ms/roofline from the same steps run serialised",
-                       "l2": "not flushed: each step streams >30 GB of grids/spectra through HBM (126 MB L2)"},
-            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(hp.numel() * 8 + hf.numel() * 8),
+            "config": config_of(w),
+            "run": {"padded_dims": list(grid.padded_dims), "parallelism": f"replicas{world}",
+                    "streams": "real space concurrent with the Fourier pipeline up to the gather; "
+                               "kernels/phases_ms/roofline from the same steps run serialised",
+                    "l2": "not flushed: each step streams >30 GB of grids/spectra through HBM (126 MB L2)"},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(sum(t.numel() * 8 for t in hin)),
                     "d2h_bytes_per_step": int(hu.numel() * 8), "ms_per_step": ms_e2e / args.steps,
                     "matches_device_result": e2e_consistent},
             "gpu_launches": int(launches), "gpu_launches_note": "hand-written kernels only; cuFFT launches excluded",
             "roofline": rf, "kernels": kern,
             "phases_ms": {k: round(avg[k], 4) for k in ("real", "gridding", "fft", "scale", "ifft", "gather",
                                                         "total")},
-            "pairs_per_step": pairs, "image_pairs_per_step": img_pairs,
+            "pairs_per_step": pairs, "image_pairs_per_step": img_pairs, "fft_count_executed": [n_in, n_out],
             "precompute_tables_s": round(t_tables, 3), "plan_device_bytes": ev.device_bytes,
             "clocks": clk}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        total, parts, desc, wall, thr = cpu_sample(args.workload)
-        line["cpu_baseline"] = {"value": s.n / total, "unit": UNIT, "cores": thr, "kind": "port", "sample": desc,
-                                "phases_s": {k: round(v, 4) for k, v in parts.items()},
-                                "sample_wall_s": round(wall, 2)}
+        thr = os.cpu_count()
+        t0 = time.perf_counter()
+        tabs = cpu_tables(args.workload, thr)
+        t_tab = time.perf_counter() - t0
+        t, desc, nt_c = cpu_full_eval(args.workload, thr, tabs)
+        line["cpu_baseline"] = {"value": nt_c / t, "unit": UNIT, "cores": thr, "kind": "port", "sample": desc,
+                                "host": cpu_host(), "timed_evaluations_s": [round(t, 3)], "tables_s": round(t_tab, 2)}
     if rank == 0:
         emit(line)
     if world > 1:
@@ -377,8 +381,11 @@ def run_slab(args, rank, world, local_rank):
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo", device_id=dev,
-                            rank=rank, world_size=world)
+    # one GPU per rank: NCCL over NVLink.  Ranks sharing one GPU (bench.py --gpus N on a smaller
+    # lease): gloo with host-staged exchanges -- a functional run of the sharded path, not a
+    # scaling measurement (no kernel waits on another rank, so sharing the device is safe)
+    backend = os.environ.get("HS_BENCH_BACKEND", "nccl")
+    dist.init_process_group(backend, device_id=dev if backend == "nccl" else None, rank=rank, world_size=world)
     w = WORKLOADS[args.workload]
     s, targets = make_system(w)
     p = EwaldParams(xi=w.xi, rc=w.rc, M=w.M, P=w.P)
@@ -432,10 +439,11 @@ def run_slab(args, rank, world, local_rank):
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded PCG64, BASELINE.json shapes)",
-            "config": {"workload": w.name, "kind": w.kind, "n": s.n, "n_targets": n_t, "xi": w.xi, "rc": w.rc,
-                       "M": w.M, "P": w.P, "parallelism": f"yslab{world}", "y_split": lay.y_split,
-                       "kz_split": lay.kz_split,
-                       "l2": "not flushed: each step streams >30 GB of grids/spectra through HBM (126 MB L2)"},
+            "config": config_of(w),
+            "run": {"parallelism": f"yslab{world}", "exchange": backend + ("" if backend == "nccl" else
+                                                                            " (host-staged; ranks share a GPU)"),
+                    "y_split": lay.y_split, "kz_split": lay.kz_split,
+                    "l2": "not flushed: each step streams >30 GB of grids/spectra through HBM (126 MB L2)"},
             "e2e": {"value": n_t * args.steps / (ms_e2e * 1e-3), "unit": UNIT, "h2d_bytes_per_step": int(bi),
                     "d2h_bytes_per_step": int(hu.numel() * 8), "ms_per_step": ms_e2e / args.steps},
             "gpu_launches": int(launches), "gpu_launches_note": "hand-written kernels only; cuFFT/NCCL excluded",
@@ -471,8 +479,11 @@ def main():
     ap.add_argument("--impl", default="b200", choices=("b200", "reference"))
     ap.add_argument("--workload", default="HL")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--mode", default="replicas", choices=("replicas", "slab"),
-                    help="multi-GPU decomposition: independent replicas (weak) or one y-slab sharded system (strong)")
+    ap.add_argument("--mode", default=None, choices=("replicas", "slab"),
+                    help="multi-GPU decomposition: one y-slab sharded system (strong scaling; default for N > 1) "
+                         "or independent replicas (weak scaling)")
+    ap.add_argument("--ref-budget-s", type=float, default=180.0,
+                    help="reference arm: stop timing further full evaluations after this many seconds")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -481,12 +492,43 @@ def main():
         args.warmup = 3
     if args.impl == "reference":
         run_reference(args, rank)
-    elif args.mode == "slab":
+        return
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args))
+    mode = args.mode or ("slab" if world > 1 else "replicas")
+    if mode == "slab":
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("MASTER_PORT", "29511")
         run_slab(args, rank, world, local_rank)
     else:
         run_ours(args, rank, world, local_rank)
+
+
+def spawn_ranks(args):
+    """bench.py --gpus N without torchrun: launch the N ranks here (one process per GPU, NCCL;
+    with fewer visible GPUs than N the ranks share GPU 0 over gloo with host-staged exchanges).
+    Rank 0's JSON line is forwarded; returns the worst exit code."""
+    import socket
+    import torch
+    ngpu = torch.cuda.device_count()
+    share = ngpu < args.gpus
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    procs = []
+    for r in range(args.gpus):
+        env = dict(os.environ, RANK=str(r), WORLD_SIZE=str(args.gpus), LOCAL_RANK=str(0 if share else r),
+                   LOCAL_WORLD_SIZE=str(args.gpus), MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port),
+                   HS_BENCH_BACKEND="gloo" if share else "nccl")
+        if not share:
+            env.setdefault("NCCL_DEBUG", "INFO")   # communicator set-up (NVLink / NVLS) on stderr
+        procs.append(subprocess.Popen([sys.executable] + sys.argv, env=env, stdout=subprocess.PIPE,
+                                      stderr=None, text=True))
+    outs = [p.communicate()[0] for p in procs]
+    for ln in outs[0].splitlines():
+        if ln.strip():
+            emit(json.loads(ln))
+    return max(p.returncode for p in procs)
 
 
 if __name__ == "__main__":

@@ -113,6 +113,8 @@ typedef struct {
   int targets_are_sources;/* 1: targets=None semantics (target_indices = arange(n)) */
 } hs_params;
 
+/* params.M == 0 creates a real-space-only plan (real_space_sum, ewald_real.py:381-455): no grids,
+ * transforms or tables are allocated; hs_plan_execute then accepts what = 1 only. */
 hs_status hs_plan_create(hs_ctx* ctx, const hs_params* params, hs_plan** out);
 hs_status hs_plan_destroy(hs_plan* plan);
 /* Device bytes the plan holds. */

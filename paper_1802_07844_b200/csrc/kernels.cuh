@@ -53,10 +53,8 @@ __device__ __forceinline__ double g_d(const GridGeom& g, int k, double pos, int6
   return window_d(pos, g.origin[k], g.h, k == 1 ? local_idx + g.yoff : local_idx);
 }
 constexpr int SP_TX = 16, SP_TY = 16, SP_TZ = 8;  // spread tile / bin shape
-// gather target order: (4x4 (x,y) column, z node) of the window-centre node (v5: 8x8 columns)
-bool gather_v5();
+// gather target order: (4x4 (x,y) column, z node) of the window-centre node
 inline int gather_keys(const GridGeom& g) {
-  if (gather_v5()) return ((g.dims[0] + 7) / 8) * ((g.dims[1] + 7) / 8) * g.dims[2];
   return ((g.dims[0] + 3) / 4) * ((g.dims[1] + 3) / 4) * g.dims[2];
 }
 inline int sp_nbins(const GridGeom& g, int k) {
@@ -188,7 +186,8 @@ hs_status launch_table_to_xmajor(hs_ctx* ctx, const double* in, int px, int py, 
 
 // plan.cu helpers reused by the stand-alone API
 hs_status greens_half_table(hs_ctx* ctx, int kind, double R, double h, const int64_t big[3], const int64_t dims[3],
-                            const int64_t guards[3], const int64_t pd[3], double* half_out);
+                            const int64_t guards[3], const int64_t pd[3], double* half_out,
+                            void* scratch = nullptr, size_t scratch_bytes = 0);
 hs_status build_pair_records(hs_ctx* ctx, int kind, int half, const int* order, int n_comb, int n, const double* pos,
                              const double* sa, const double* sb, double4* P, double4* A, double4* B);
 hs_status build_target_records(hs_ctx* ctx, const int* order, int nt, const double* tpos, const long long* tcols,

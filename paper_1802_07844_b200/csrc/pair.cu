@@ -249,6 +249,8 @@ __device__ __forceinline__ double exact_r2(double d0, double d1, double d2) {
 #endif
 constexpr int PC_WARPS = PC_WARPS_DEF;
 constexpr int PC_TG = PC_WARPS * 32;  // targets per work item
+// plan.cu sizes the work-item buffer (nt / 128 + columns + 2) for at least 128 targets per item
+static_assert(PC_TG >= 128, "pair work items must hold >= 128 targets (PC_WARPS_DEF >= 4)");
 // candidates per chunk (a multiple of PC_TG, a power of two): the stokeslet stages 256 per
 // barrier pair (2 per thread) in a 2-chunk ring; the larger stresslet / rotlet records keep
 // 128-candidate chunks in a 3-chunk ring (4 CTAs per SM either way)
@@ -703,7 +705,10 @@ hs_status launch_pair(hs_ctx* ctx, const PairArgs& a) {
   const int kind = a.kind & 15;
   const bool is_half = (a.kind & 16) != 0;
   // persistent-style grid: enough CTAs to fill the machine, looping over the device-side item count
-  const int grid = std::max(1, std::min(a.max_items, ctx->sm_count * 16));
+  // HS_PAIR_CTAS_PER_SM (experiment): persistent CTAs per SM; fewer than the 4 that fit leave
+  // register file for the concurrently issued Fourier-pipeline kernels (hs_plan_execute)
+  static const int per_sm = getenv("HS_PAIR_CTAS_PER_SM") ? atoi(getenv("HS_PAIR_CTAS_PER_SM")) : 16;
+  const int grid = std::max(1, std::min(a.max_items, ctx->sm_count * std::max(per_sm, 1)));
 #define HS_PAIR_CASE1(K, H, AU)                                                                         \
   do {                                                                                                  \
     const int dyn = pc_nh<K>() * pc_h<K>() * pc_rec_bytes<K, H>();                                      \

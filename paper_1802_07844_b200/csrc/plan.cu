@@ -309,6 +309,7 @@ struct hs_plan {
   int ngroup = 1, group_c0[3] = {0, 0, 0};
   unsigned kern_mask = 0, sigma_mask = 0;
   bool tmp_aliased = false;     // grid_tmp lives in grid_in (mixed): re-zero its z padding after use
+  bool four = true;             // false: real-space-only plan (M = 0; real_space_sum)
   int n_in = 0, n_out = 0;
   CellGeom cg{};
   GridGeom gg{};        // padded real grids
@@ -454,66 +455,77 @@ static hs_status plan_create_impl(hs_ctx* ctx, const hs_params* prm, const hs_sl
     p->cg.dims[0] = p->cg.dims[1] = p->cg.dims[2] = 1;
   }
   const int ncell = (int)p->cg.ncell();
-  // ---- grid geometry
+  // ---- grid geometry (M = 0: a real-space-only plan, no grids, transforms or tables)
+  p->four = prm->M > 0;
   GridGeom& g = p->gg;
-  for (int k = 0; k < 3; ++k) {
-    g.origin[k] = prm->origin[k];
-    g.dims[k] = (int)prm->dims[k];
+  int64_t px = 0, py = 0, pz = 0, nxd = 0, nzh = 0;
+  if (!p->four) {
+    if (sl) return bail(fail(HS_ERR_PARAMETER, "slab plans need the Fourier part (M > 0)"));
+    for (int k = 0; k < 3; ++k) g.dims[k] = 1;
+    g.P = 1;
+  } else {
+    for (int k = 0; k < 3; ++k) {
+      g.origin[k] = prm->origin[k];
+      g.dims[k] = (int)prm->dims[k];
+    }
+    g.h = prm->h;
+    g.P = (int)prm->P;
+    g.alpha = 2.0 * prm->xi * prm->xi / prm->eta;
+    g.pref = std::pow(2.0 * prm->xi * prm->xi / (kPi * prm->eta), 1.5);
+    px = prm->padded[0];
+    py = prm->padded[1];
+    pz = prm->padded[2];
+    nxd = prm->dims[0];
+    nzh = pz / 2 + 1;
+    int64_t nyd = prm->dims[1];
+    p->yo = (int)nyd;
+    p->nzs = (int)nzh;
+    if (sl) {
+      // owned planes [y0, y1) plus P - 1 ghost planes above (spread contributions for the next
+      // rank, then the gather halo received from it); owned kz columns [kz0, kz1)
+      const hs_slab& s = *slab;
+      if (s.world < 1 || s.rank < 0 || s.rank >= s.world || s.y0 < 0 || s.y1 <= s.y0 || s.y1 > prm->dims[1] ||
+          s.kz0 < 0 || s.kz1 <= s.kz0 || s.kz1 > nzh)
+        return bail(fail(HS_ERR_PARAMETER, "invalid slab (rank, world, y range, kz range)"));
+      if (s.rank + 1 < s.world && s.y1 - s.y0 < prm->P - 1)
+        return bail(fail(HS_ERR_PARAMETER, "y slab thinner than P - 1 planes: use fewer ranks"));
+      p->yo = (int)(s.y1 - s.y0);
+      p->nzs = (int)(s.kz1 - s.kz0);
+      nyd = p->yo + prm->P - 1;
+      g.dims[1] = (int)nyd;
+      g.yoff = (int)s.y0;
+      g.sel = 1;
+      g.sel_lo = 0;
+      g.sel_hi = p->yo;
+    }
+    // grids are stored [y][x][z] with z-pitch pz (see fft.cu)
+    g.stride[0] = pz;
+    g.stride[1] = nxd * pz;
+    g.stride[2] = 1;
+    g.ch_stride = nyd * nxd * pz;
+    p->n_grid = nyd * nxd * pz;
+    p->n_mixed = py * nxd * p->nzs;
+    p->n_amix = sl ? (int64_t)p->yo * nxd * nzh : p->n_mixed;
+    p->n_real_grid = px * py * pz;
+    p->n_half = px * py * nzh;
+    if (px != py) return bail(fail(HS_ERR_PARAMETER, "padded x and y lengths must agree"));
+    if ((st = make_fft_plan((int)px, &p->xplan)) != HS_OK) return bail(st);
+    KGeom& kg = p->kg;
+    kg.p[0] = (int)px;
+    kg.p[1] = (int)py;
+    kg.p[2] = (int)pz;
+    kg.nzh = (int)(pz / 2 + 1);
+    for (int k = 0; k < 3; ++k) kg.kscale[k] = 1.0 / ((double)prm->padded[k] * prm->h);
+    kg.a = (1.0 - prm->eta) / (4.0 * prm->xi * prm->xi);
+    kg.b = 1.0 / (4.0 * prm->xi * prm->xi);
+    kg.inv_n = 1.0 / ((double)px * (double)py * (double)pz);
   }
-  g.h = prm->h;
-  g.P = (int)prm->P;
-  g.alpha = 2.0 * prm->xi * prm->xi / prm->eta;
-  g.pref = std::pow(2.0 * prm->xi * prm->xi / (kPi * prm->eta), 1.5);
-  const int64_t px = prm->padded[0], py = prm->padded[1], pz = prm->padded[2];
-  const int64_t nxd = prm->dims[0], nzh = pz / 2 + 1;
-  int64_t nyd = prm->dims[1];
-  p->yo = (int)nyd;
-  p->nzs = (int)nzh;
-  if (sl) {
-    // owned planes [y0, y1) plus P - 1 ghost planes above (spread contributions for the next
-    // rank, then the gather halo received from it); owned kz columns [kz0, kz1)
-    const hs_slab& s = *slab;
-    if (s.world < 1 || s.rank < 0 || s.rank >= s.world || s.y0 < 0 || s.y1 <= s.y0 || s.y1 > prm->dims[1] ||
-        s.kz0 < 0 || s.kz1 <= s.kz0 || s.kz1 > nzh)
-      return bail(fail(HS_ERR_PARAMETER, "invalid slab (rank, world, y range, kz range)"));
-    if (s.rank + 1 < s.world && s.y1 - s.y0 < prm->P - 1)
-      return bail(fail(HS_ERR_PARAMETER, "y slab thinner than P - 1 planes: use fewer ranks"));
-    p->yo = (int)(s.y1 - s.y0);
-    p->nzs = (int)(s.kz1 - s.kz0);
-    nyd = p->yo + prm->P - 1;
-    g.dims[1] = (int)nyd;
-    g.yoff = (int)s.y0;
-    g.sel = 1;
-    g.sel_lo = 0;
-    g.sel_hi = p->yo;
-  }
-  // grids are stored [y][x][z] with z-pitch pz (see fft.cu)
-  g.stride[0] = pz;
-  g.stride[1] = nxd * pz;
-  g.stride[2] = 1;
-  g.ch_stride = nyd * nxd * pz;
-  p->n_grid = nyd * nxd * pz;
-  p->n_mixed = py * nxd * p->nzs;
-  p->n_amix = sl ? (int64_t)p->yo * nxd * nzh : p->n_mixed;
-  p->n_real_grid = px * py * pz;
-  p->n_half = px * py * nzh;
-  if (px != py) return bail(fail(HS_ERR_PARAMETER, "padded x and y lengths must agree"));
-  if ((st = make_fft_plan((int)px, &p->xplan)) != HS_OK) return bail(st);
-  KGeom& kg = p->kg;
-  kg.p[0] = (int)px;
-  kg.p[1] = (int)py;
-  kg.p[2] = (int)pz;
-  kg.nzh = (int)(pz / 2 + 1);
-  for (int k = 0; k < 3; ++k) kg.kscale[k] = 1.0 / ((double)prm->padded[k] * prm->h);
-  kg.a = (1.0 - prm->eta) / (4.0 * prm->xi * prm->xi);
-  kg.b = 1.0 / (4.0 * prm->xi * prm->xi);
-  kg.inv_n = 1.0 / ((double)px * (double)py * (double)pz);
-  p->nbins = sp_nbins(g, 0) * sp_nbins(g, 1) * sp_nbins(g, 2);
+  p->nbins = p->four ? sp_nbins(g, 0) * sp_nbins(g, 1) * sp_nbins(g, 2) : 1;
   const int nb = p->nbins;
 
   // ---- buffers
   const int maxn = std::max(p->n_comb, std::max(nt, n));
-  const int maxb = std::max(std::max(ncell * kTargetSub, nb + 1), gather_keys(g));
+  const int maxb = std::max(std::max(ncell * kTargetSub, nb + 1), p->four ? gather_keys(g) : 1);
 #define A_(cnt, ptr, ...) if ((st = palloc(p, (size_t)(cnt), &(ptr), ##__VA_ARGS__)) != HS_OK) return bail(st)
   const bool mixed = prm->kind == HS_MIXED;
   A_(3 * (size_t)n, p->d_pos);
@@ -540,64 +552,66 @@ static hs_status plan_create_impl(hs_ctx* ctx, const hs_params* prm, const hs_sl
   if (mixed) A_(p->n_comb, p->Cq);
   A_(std::max(nt, 1), p->TP);
   A_(std::max(nt, 1), p->torig);
-  A_(p->n_comb, p->bk_order);
-  A_(nb + 2, p->bk_start);  // + the slab plan's drop bin
-  A_(n, p->bc_order);
-  A_(nb + 2, p->bc_start);
-  A_(std::max(nt, 1), p->bt_order);
-  A_((size_t)gather_keys(g) + 1, p->bt_start);
-  // mirrored spreading (half space; HS_SPREAD_IMAGES=1 spreads the images explicitly, comparison)
-  p->mirror = p->half && (mixed || !getenv("HS_SPREAD_IMAGES"));
-  // channel groups and mirror masks
-  p->sg_cap = p->n_in;
-  p->ngroup = 1;
-  p->group_c0[1] = p->n_in;
-  if (mixed) {
-    p->kern_mask = p->half ? (0x7u | (0x3Fu << 13)) : 0x1FFu;
-    p->sigma_mask = p->half ? (0x3u | (0x2Bu << 13)) : 0u;
-    if (!sl) {  // one GPU: spread / transform 13 + 6 (half) or 3 + 6 (free) channels at a time
-      p->ngroup = 2;
-      p->group_c0[1] = p->half ? 13 : 3;
-      p->group_c0[2] = p->n_in;
-      p->sg_cap = p->half ? 13 : 6;
+  if (p->four) {
+    A_(p->n_comb, p->bk_order);
+    A_(nb + 2, p->bk_start);  // + the slab plan's drop bin
+    A_(n, p->bc_order);
+    A_(nb + 2, p->bc_start);
+    A_(std::max(nt, 1), p->bt_order);
+    A_((size_t)gather_keys(g) + 1, p->bt_start);
+    // mirrored spreading (half space; HS_SPREAD_IMAGES=1 spreads the images explicitly, comparison)
+    p->mirror = p->half && (mixed || !getenv("HS_SPREAD_IMAGES"));
+    // channel groups and mirror masks
+    p->sg_cap = p->n_in;
+    p->ngroup = 1;
+    p->group_c0[1] = p->n_in;
+    if (mixed) {
+      p->kern_mask = p->half ? (0x7u | (0x3Fu << 13)) : 0x1FFu;
+      p->sigma_mask = p->half ? (0x3u | (0x2Bu << 13)) : 0u;
+      if (!sl) {  // one GPU: spread / transform 13 + 6 (half) or 3 + 6 (free) channels at a time
+        p->ngroup = 2;
+        p->group_c0[1] = p->half ? 13 : 3;
+        p->group_c0[2] = p->n_in;
+        p->sg_cap = p->half ? 13 : 6;
+      }
+    } else {
+      p->kern_mask = (1u << p->nk) - 1u;
+      p->sigma_mask = mirror_sigma_neg(prm->kind);
     }
-  } else {
-    p->kern_mask = (1u << p->nk) - 1u;
-    p->sigma_mask = mirror_sigma_neg(prm->kind);
-  }
-  A_(p->n_comb, p->SPk);
-  A_(std::max((size_t)p->n_comb * p->nk, (size_t)n * p->n_in), p->SWk);
-  if (p->nc) {
-    A_(n, p->SPc);
-    A_((size_t)n * p->nc, p->SWc);
-  }
-  A_(std::max(nt, 1), p->TG);
-  A_(std::max(nt, 1), p->tg_orig);
-  A_((size_t)p->sg_cap * p->n_grid, p->grid_in, true);
-  A_((size_t)p->n_amix, p->Amix, true);
-  A_((size_t)std::max(p->n_in, p->n_out) * p->n_mixed, p->spec);
-  p->out_pitch = p->half ? 6 : 4;
-  A_((size_t)p->out_pitch * p->n_grid, p->grid_out, true);
-  if (mixed && !sl && p->sg_cap >= p->n_out) {
-    p->grid_tmp = p->grid_in;  // the source grids are dead once forward-transformed
-    p->tmp_aliased = true;
-  } else {
-    A_((size_t)p->n_out * p->n_grid, p->grid_tmp);
-  }
-  p->go = p->gg;
-  p->go.stride[0] = (int64_t)p->out_pitch * pz;
-  p->go.stride[1] = (int64_t)p->out_pitch * nxd * pz;
-  p->go.stride[2] = p->out_pitch;
-  p->go.ch_stride = 1;
-  // tables in x-stage layout, only the plan's kz columns
-  const size_t ntab = (size_t)px * py * p->nzs;
-  if (table_needs(prm->kind, p->half, HS_BIHARMONIC)) A_(ntab, p->tabB);
-  if (table_needs(prm->kind, p->half, HS_HARMONIC)) A_(ntab, p->tabH);
-  A_(px, p->tw);
-  if ((st = make_twiddles((int)px, p->tw, ctx->stream)) != HS_OK) return bail(st);
-  if (ystage_supported((int)py) && !getenv("HS_YSTAGE_CUFFT")) {  // env: cuFFT y stage (comparison)
-    A_(py, p->ytw);
-    if ((st = make_twiddles((int)py, p->ytw, ctx->stream)) != HS_OK) return bail(st);
+    A_(p->n_comb, p->SPk);
+    A_(std::max((size_t)p->n_comb * p->nk, (size_t)n * p->n_in), p->SWk);
+    if (p->nc) {
+      A_(n, p->SPc);
+      A_((size_t)n * p->nc, p->SWc);
+    }
+    A_(std::max(nt, 1), p->TG);
+    A_(std::max(nt, 1), p->tg_orig);
+    A_((size_t)p->sg_cap * p->n_grid, p->grid_in, true);
+    A_((size_t)p->n_amix, p->Amix, true);
+    A_((size_t)std::max(p->n_in, p->n_out) * p->n_mixed, p->spec);
+    p->out_pitch = p->half ? 6 : 4;
+    A_((size_t)p->out_pitch * p->n_grid, p->grid_out, true);
+    if (mixed && !sl && p->sg_cap >= p->n_out) {
+      p->grid_tmp = p->grid_in;  // the source grids are dead once forward-transformed
+      p->tmp_aliased = true;
+    } else {
+      A_((size_t)p->n_out * p->n_grid, p->grid_tmp);
+    }
+    p->go = p->gg;
+    p->go.stride[0] = (int64_t)p->out_pitch * pz;
+    p->go.stride[1] = (int64_t)p->out_pitch * nxd * pz;
+    p->go.stride[2] = p->out_pitch;
+    p->go.ch_stride = 1;
+    // tables in x-stage layout, only the plan's kz columns
+    const size_t ntab = (size_t)px * py * p->nzs;
+    if (table_needs(prm->kind, p->half, HS_BIHARMONIC)) A_(ntab, p->tabB);
+    if (table_needs(prm->kind, p->half, HS_HARMONIC)) A_(ntab, p->tabH);
+    A_(px, p->tw);
+    if ((st = make_twiddles((int)px, p->tw, ctx->stream)) != HS_OK) return bail(st);
+    if (ystage_supported((int)py) && !getenv("HS_YSTAGE_CUFFT")) {  // env: cuFFT y stage (comparison)
+      A_(py, p->ytw);
+      if ((st = make_twiddles((int)py, p->ytw, ctx->stream)) != HS_OK) return bail(st);
+    }
   }
   A_(3 * (size_t)std::max(nt, 1), p->u);
   A_(3 * (size_t)std::max(nt, 1), p->u_real, true);
@@ -607,7 +621,7 @@ static hs_status plan_create_impl(hs_ctx* ctx, const hs_params* prm, const hs_sl
   A_(3 * (size_t)std::max(nt, 1), p->uc, true);
 #undef A_
   // ---- cuFFT plans (batched over channels, shared work area)
-  {
+  if (p->four) {
     // 1-D batched cuFFT plans for the z and y stages (x is fused with the scaling, fft.cu)
     size_t w1 = 0, w2 = 0, w3 = 0;
     if (cufftCreate(&p->zf) != CUFFT_SUCCESS || cufftCreate(&p->yf) != CUFFT_SUCCESS ||
@@ -672,8 +686,8 @@ extern "C" int64_t hs_plan_bytes(const hs_plan* p) { return p ? p->bytes : 0; }
 
 extern "C" hs_status hs_plan_fft_counts(const hs_plan* p, int* n_fft, int* n_ifft) {
   if (!p) return fail(HS_ERR_PARAMETER, "null plan");
-  if (n_fft) *n_fft = p->n_in;
-  if (n_ifft) *n_ifft = p->n_out;
+  if (n_fft) *n_fft = p->four ? p->n_in : 0;
+  if (n_ifft) *n_ifft = p->four ? p->n_out : 0;
   return HS_OK;
 }
 
@@ -691,25 +705,39 @@ static int table_kz0(const hs_plan* p) { return p->slab.world > 0 ? (int)p->slab
 
 extern "C" hs_status hs_plan_set_table(hs_plan* p, int table_kind, const double* samples, int mem) {
   if (!p || !samples) return fail(HS_ERR_PARAMETER, "null argument");
+  if (!p->four) return fail(HS_ERR_CONFIG, "real-space-only plan (M = 0) has no tables");
   double* dst = table_kind == HS_BIHARMONIC ? p->tabB : p->tabH;
   if (!dst) return HS_OK;  // not needed by this kind/geometry
   hs_ctx* ctx = p->ctx;
   const int64_t pd[3] = {p->prm.padded[0], p->prm.padded[1], p->prm.padded[2]};
   const size_t full = (size_t)pd[0] * pd[1] * pd[2];
   const double* src = samples;
+  // staging in the (idle) spectrum buffer when it is large enough, else stream-ordered allocations
+  const size_t spec_bytes = sizeof(double2) * (size_t)std::max(p->n_in, p->n_out) * p->n_mixed;
+  const size_t half_b = ((size_t)p->n_half * sizeof(double) + 255) & ~(size_t)255;
+  const size_t full_b = (mem == HS_MEM_HOST) ? full * sizeof(double) : 0;
+  const bool in_spec = half_b + full_b <= spec_bytes;
+  HS_CUDA(cudaStreamSynchronize(ctx->stream));
   double* tmp = nullptr;
+  double* half = nullptr;
+  if (in_spec) {
+    half = (double*)p->spec;
+    if (full_b) tmp = (double*)((char*)p->spec + half_b);
+  } else {
+    HS_CUDA(cudaMallocAsync(&half, (size_t)p->n_half * sizeof(double), ctx->stream));
+    if (full_b) HS_CUDA(cudaMallocAsync(&tmp, full_b, ctx->stream));
+  }
   if (mem == HS_MEM_HOST) {
-    HS_CUDA(cudaMallocAsync(&tmp, full * sizeof(double), ctx->stream));
     HS_CUDA(cudaMemcpyAsync(tmp, samples, full * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
     src = tmp;
   }
-  double* half = nullptr;
-  HS_CUDA(cudaMallocAsync(&half, (size_t)p->n_half * sizeof(double), ctx->stream));
   hs_status st = launch_take_half(ctx, src, pd, half);
   if (st == HS_OK)
     st = launch_table_to_xmajor(ctx, half, (int)pd[0], (int)pd[1], (int)(pd[2] / 2 + 1), dst, table_kz0(p), p->nzs);
-  cudaFreeAsync(half, ctx->stream);
-  if (tmp) cudaFreeAsync(tmp, ctx->stream);
+  if (!in_spec) {
+    cudaFreeAsync(half, ctx->stream);
+    if (tmp) cudaFreeAsync(tmp, ctx->stream);
+  }
   HS_TRY(st);
   HS_CUDA(cudaStreamSynchronize(ctx->stream));
   if (table_kind == HS_BIHARMONIC) p->have_B = true;
@@ -729,7 +757,8 @@ static hs_status greens_half_table_full(hs_ctx* ctx, int kind, double R, double 
 // (1432,1432,2864)): ~12 GB of intermediates + the pd-sized crop and its spectrum, instead
 // of 94 GB.  HS_TABLE_FULL=1 selects the 3-D big-grid transform (comparison).
 hs_status greens_half_table(hs_ctx* ctx, int kind, double R, double h, const int64_t big[3], const int64_t dims[3],
-                            const int64_t guards[3], const int64_t pd[3], double* half_out) {
+                            const int64_t guards[3], const int64_t pd[3], double* half_out, void* scratch,
+                            size_t scratch_bytes) {
   if (getenv("HS_TABLE_FULL")) return greens_half_table_full(ctx, kind, R, h, big, dims, guards, pd, half_out);
   cudaStream_t st = ctx->stream;
   const int64_t n[3] = {big[0], big[1], big[2]};
@@ -753,25 +782,39 @@ hs_status greens_half_table(hs_ctx* ctx, int kind, double R, double h, const int
   void* ws = nullptr;
   cufftHandle pl[3] = {0, 0, 0}, pf = 0;
   hs_status rs = HS_OK;
+  // intermediates come from the caller's idle scratch (a plan's spectrum buffer) while it lasts
+  // (bump allocation, 256-byte aligned), then from cudaMalloc; release() frees only the latter
+  char* arena = (char*)scratch;
+  size_t arena_used = 0;
+  std::vector<void*> owned;
+  auto alloc = [&](void** ptr, size_t bytes) {
+    bytes = (std::max<size_t>(bytes, 16) + 255) & ~(size_t)255;
+    if (arena && arena_used + bytes <= scratch_bytes) {
+      *ptr = arena + arena_used;
+      arena_used += bytes;
+      return true;
+    }
+    if (cudaMalloc(ptr, bytes) != cudaSuccess) {
+      cudaGetLastError();
+      *ptr = nullptr;
+      return false;
+    }
+    owned.push_back(*ptr);
+    return true;
+  };
+  auto release = [&](void* ptr) {
+    for (auto& o : owned)
+      if (o == ptr && o) {
+        cudaFree(o);
+        o = nullptr;
+      }
+  };
   auto cleanup = [&]() {
     for (auto& q : pl)
       if (q) cufftDestroy(q);
     if (pf) cufftDestroy(pf);
-    cudaFree(lin);
-    cudaFree(lout);
-    cudaFree(A2);
-    cudaFree(A3);
-    cudaFree(F);
-    cudaFree(crop);
-    cudaFree(spec);
-    cudaFree(ws);
-  };
-  auto alloc = [&](void** ptr, size_t bytes) {
-    if (cudaMalloc(ptr, std::max<size_t>(bytes, 16)) != cudaSuccess) {
-      cudaGetLastError();
-      return false;
-    }
-    return true;
+    for (auto& o : owned)
+      if (o) cudaFree(o);
   };
   do {
     const size_t lin_b = 16 * (size_t)std::max(B1 * hh[2], 1L), lout_b = 8 * (size_t)std::max(B1 * n[2], 1L);
@@ -827,7 +870,7 @@ hs_status greens_half_table(hs_ctx* ctx, int kind, double R, double h, const int
     }
     if (rs != HS_OK) break;
     HS_CUDA(cudaStreamSynchronize(st));
-    cudaFree(A2);
+    release(A2);
     A2 = nullptr;
     if (!alloc((void**)&F, 8 * (size_t)lt3 * kp[0])) {
       rs = fail(HS_ERR_RESOURCE, "precompute: intermediate allocation failed");
@@ -847,13 +890,13 @@ hs_status greens_half_table(hs_ctx* ctx, int kind, double R, double h, const int
       cufftDestroy(q);
       q = 0;
     }
-    cudaFree(A3);
+    release(A3);
     A3 = nullptr;
-    cudaFree(lin);
+    release(lin);
     lin = nullptr;
-    cudaFree(lout);
+    release(lout);
     lout = nullptr;
-    cudaFree(ws);
+    release(ws);
     ws = nullptr;
     // crop (evenness) and the forward transform on the padded grid
     const size_t ncrop = (size_t)pd[0] * pd[1] * pd[2], nch = (size_t)pd[0] * pd[1] * (pd[2] / 2 + 1);
@@ -968,21 +1011,38 @@ static hs_status greens_half_table_full(hs_ctx* ctx, int kind, double R, double 
 
 extern "C" hs_status hs_plan_build_tables(hs_plan* p, const int64_t big[3], double R, const int64_t guards[3]) {
   if (!p) return fail(HS_ERR_PARAMETER, "null plan");
+  if (!p->four) return fail(HS_ERR_CONFIG, "real-space-only plan (M = 0) has no tables");
   const int64_t pd[3] = {p->prm.padded[0], p->prm.padded[1], p->prm.padded[2]};
   hs_ctx* ctx = p->ctx;
+  // the spectrum buffer is idle outside an evaluation: it holds the half table and the
+  // precompute's intermediates as far as it goes (the cfg5-size plans leave too little free
+  // device memory for separate ones)
+  const size_t spec_bytes = sizeof(double2) * (size_t)std::max(p->n_in, p->n_out) * p->n_mixed;
+  const size_t half_bytes = ((size_t)p->n_half * sizeof(double) + 255) & ~(size_t)255;
   double* half = nullptr;
-  HS_CUDA(cudaMalloc(&half, (size_t)p->n_half * sizeof(double)));
+  char* scr = nullptr;
+  size_t scr_bytes = 0;
+  bool own_half = false;
+  HS_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (spec_bytes >= half_bytes) {
+    half = (double*)p->spec;
+    scr = (char*)p->spec + half_bytes;
+    scr_bytes = spec_bytes - half_bytes;
+  } else {
+    HS_CUDA(cudaMalloc(&half, (size_t)p->n_half * sizeof(double)));
+    own_half = true;
+  }
   hs_status st = HS_OK;
   for (int kind = 0; kind < 2 && st == HS_OK; ++kind) {
     double* dst = kind == HS_BIHARMONIC ? p->tabB : p->tabH;
     if (!dst) continue;
-    st = greens_half_table(ctx, kind, R, p->prm.h, big, p->prm.dims, guards, pd, half);
+    st = greens_half_table(ctx, kind, R, p->prm.h, big, p->prm.dims, guards, pd, half, scr, scr_bytes);
     if (st == HS_OK)
       st = launch_table_to_xmajor(ctx, half, (int)pd[0], (int)pd[1], (int)(pd[2] / 2 + 1), dst, table_kz0(p), p->nzs);
     if (st == HS_OK && cudaStreamSynchronize(ctx->stream) != cudaSuccess) st = fail(HS_ERR_CUDA, "table build");
     if (st == HS_OK) (kind == HS_BIHARMONIC ? p->have_B : p->have_H) = true;
   }
-  cudaFree(half);
+  if (own_half) cudaFree(half);
   return st;
 }
 
@@ -1288,16 +1348,17 @@ hs_status stage_xstage(hs_plan* p) {
   xa.ka = p->kg.a;
   xa.kb = p->kg.b;
   xa.inv_n = p->kg.inv_n;
-  HS_TRY(launch_xfused(p->ctx, p->prm.kind, p->half, xa));
-  if (p->prm.kind == HS_MIXED) {
-    // second channel group: the stresslet kernel channels, scaled without wall channels and
-    // added to T1 (its outputs go to spec channels 0..2, the first pass's T1)
-    const int c0 = p->half ? 13 : 3;
-    xa.B = p->spec + (size_t)c0 * p->n_mixed;
-    xa.accum = 1;
-    HS_TRY(launch_xfused(p->ctx, HS_STRESSLET, 0, xa));
+  if (p->prm.kind != HS_MIXED) return launch_xfused(p->ctx, p->prm.kind, p->half, xa);
+  // mixed (kmult.cuh layout): F + the shared S, V as a stokeslet (outputs in place), then the
+  // shared M channels and the stresslet kernel channels, each added to those outputs
+  HS_TRY(launch_xfused(p->ctx, HS_STOKESLET, p->half, xa));
+  xa.accum = 1;
+  if (p->half) {
+    xa.B = p->spec + (size_t)7 * p->n_mixed;
+    HS_TRY(launch_xfused(p->ctx, HS_MIXED, 1, xa));
   }
-  return HS_OK;
+  xa.B = p->spec + (size_t)(p->half ? 13 : 3) * p->n_mixed;
+  return launch_xfused(p->ctx, HS_STRESSLET, 0, xa);
 }
 
 // Fourier gather at the plan's targets: u_four, and u = u_real + u_four (ewald_fourier.py:626-630)
@@ -1394,6 +1455,7 @@ extern "C" hs_status hs_plan_execute(hs_plan* p, const double* positions, const 
   hs_ctx* ctx = p->ctx;
   cudaStream_t st = ctx->stream;
   const int nt = (int)p->prm.n_targets;
+  if ((what & 2) && !p->four) return fail(HS_ERR_CONFIG, "real-space-only plan (M = 0): no Fourier part");
   if ((what & 2) && (p->tabB && !p->have_B)) return fail(HS_ERR_CONFIG, "missing biharmonic table");
   if ((what & 2) && (p->tabH && !p->have_H)) return fail(HS_ERR_CONFIG, "missing harmonic table");
   HS_TRY(begin_eval(p));

@@ -18,7 +18,7 @@ from . import _lib
 from ._plan import get_evaluator
 from .errors import GeometryError, ParameterError
 from .system import HALF_SPACE, ROTLET, STOKESLET, STRESSLET, VelocityResult
-from .point_kernels import kernel_real  # noqa: E402,F401  (ref:ewald_real.py:115-150)
+from .point_kernels import correction_phi_real, harmonic_real_derivs, kernel_real  # noqa: E402,F401  (ref:ewald_real.py:115-190)
 
 _SQRT_PI = math.sqrt(math.pi)
 
@@ -121,11 +121,18 @@ def build_cell_list(points, rc, bounds) -> CellList:
     return CellList(positions=points, rc=rc, origin=lo, edge=edge, dims=dims, order=order, start=start)
 
 
+class _RealOnlyGrid:
+    """Grid descriptor of a real-space-only plan: M = 0 tells hs_plan_create to allocate no grids,
+    transforms or tables (include/hsewald_b200.h), so any (xi, rc) works, e.g. the xi -> 0
+    screening limits of the reference's tests (ref tests/test_ewald_real.py:33-51)."""
+
+    M, P, h, eta = 0, 0, 0.0, 1.0
+    origin = (0.0, 0.0, 0.0)
+    dims = padded_dims = (0, 0, 0)
+
+
 def _real_grid(system, xi):
-    """A minimal grid descriptor for real-space-only plans (no Fourier buffers of note)."""
-    from .ewald_fourier import GridSpec
-    return GridSpec(L=system.box_length, M=2 + (system.geometry == HALF_SPACE) * 0, P=2, xi=xi,
-                    geometry=system.geometry)
+    return _RealOnlyGrid()
 
 
 def real_space_sum(system, params: RealSpaceParams, targets=None, target_indices=None) -> VelocityResult:

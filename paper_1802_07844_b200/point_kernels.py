@@ -168,3 +168,34 @@ def kernel_real(kind, r, xi):
         W = np.array([[0.0, u[2], -u[1]], [-u[2], 0.0, u[0]], [u[1], -u[0], 0.0]])
         return 2.0 * dd * W
     raise ValueError(f"unknown kind {kind!r}")
+
+
+def harmonic_real_derivs(r, xi) -> HarmonicDerivs:
+    """Screened harmonic family G, grad G, hess G, third G at displacement r, raw 4 pi G = 1/r
+    convention (ref:ewald_real.py:152-168): the radial coefficients with the erf(xi r)/r part
+    removed, assembled into the tensors of the closed forms above."""
+    from .ewald_real import f_derivs
+    r = np.asarray(r, dtype=float)
+    rn = float(np.linalg.norm(r))
+    if rn == 0.0:
+        raise SingularityError("harmonic_real_derivs at zero displacement")
+    c0, c1, c2, c3 = (float(c[0]) for c in gfam_coeffs(np.array([rn]), screen=f_derivs(np.array([rn]), xi)))
+    I = np.eye(3)
+    sym = np.einsum("ij,k->ijk", I, r) + np.einsum("ik,j->ijk", I, r) + np.einsum("jk,i->ijk", I, r)
+    return HarmonicDerivs(G=c0, gradG=-c1 * r, hessG=-c1 * I + c2 * np.outer(r, r),
+                          thirdG=c2 * sym + c3 * np.einsum("i,j,k->ijk", r, r, r))
+
+
+def correction_phi_real(kind, y, x, xi, f=None, g=None, q=None):
+    """Screened wall correction (phi_R, grad phi_R) of one source at x, raw 4 pi convention
+    (ref:ewald_real.py:171-190); the pair kernel evaluates the same per image pair."""
+    from .ewald_real import f_derivs
+    y = np.asarray(y, float)
+    d = np.asarray(x, float) - y * _MIRROR
+    rn = float(np.linalg.norm(d))
+    if rn == 0.0:
+        raise SingularityError("evaluation point coincides with an image")
+    one = lambda a: None if a is None else np.asarray(a, float)[None, :]  # noqa: E731
+    s, v, M = phi_channels(kind, y[None, :], f=one(f), g=one(g), q=one(q))
+    phi, grad = phi_and_grad(d[None, :], gfam_coeffs(np.array([rn]), screen=f_derivs(np.array([rn]), xi)), s, v, M)
+    return float(phi[0]), grad[0]

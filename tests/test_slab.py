@@ -312,6 +312,24 @@ def test_headline_full_size_vs_direct_and_slab8(gpu):
     u = gpu.ewald_sum(s, p).velocities
     idx = np.random.default_rng(4).choice(s.n, 400, replace=False)
     d = gpu.direct_sum_half(s, targets=s.positions[idx], target_indices=idx).velocities
-    assert rel_l2(u[idx], d) < 1e-9
+    assert rel_l2(u[idx], d) < 1e-10   # measured 2.1e-11 (the method's truncation error here)
     r = ewald_sum_slab_local(s, p, 8)
     assert rel_l2(r.velocities, u) < 1e-12
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [1, 2, 3])
+def test_slab_local_mixed(gpu, world):
+    """BASELINE configs[4]'s mixed stokeslet + stresslet system (separate targets) through the
+    y-slab decomposition (all 19 source channels per rank, both x-stage passes on each kz
+    share) == the single mixed plan."""
+    from paper_1802_07844_b200.configs import make_system
+    from paper_1802_07844_b200.ewald import ewald_sum_mixed
+    from paper_1802_07844_b200.sharding import ewald_sum_slab_local
+    s, tg = make_system("cfg5", n=20_000)
+    p = gpu.EwaldParams(xi=20.8, rc=0.17, M=80, P=24)
+    ref = ewald_sum_mixed(s, p, targets=tg[:6000])
+    r = ewald_sum_slab_local(s, p, world, targets=tg[:6000])
+    # round-off: the slab ranks add their ghost planes in a different order (measured 1.6e-12 at
+    # W = 2, 3; the stresslet's near-field dominates the mixed velocities)
+    assert rel_l2(r.velocities, ref.velocities) < 5e-12

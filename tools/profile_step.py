@@ -20,12 +20,14 @@ a = ap.parse_args()
 w = WORKLOADS[a.workload]
 s, tg = make_system(w, n=a.n)
 grid = GridSpec(L=w.L, M=w.M, P=w.P, xi=w.xi)
-ev = Evaluator(w.kind, "half", w.L, w.xi, w.rc, grid, s.n, s.n, True)
+nt = s.n if tg is None else tg.shape[0]
+ev = Evaluator(w.kind, "half", w.L, w.xi, w.rc, grid, s.n, nt, tg is None)
 ev.build_tables()
-pos = torch.from_numpy(s.positions).cuda()
-sa = torch.from_numpy(s.f if w.kind == "stokeslet" else s.g).cuda()
-sb = None if w.kind == "stokeslet" else torch.from_numpy(s.q).cuda()
+from paper_1802_07844_b200.ewald import _strengths  # noqa: E402
+fa, fb = _strengths(s)
+put = lambda x: None if x is None else torch.from_numpy(x).cuda()  # noqa: E731
+pos, sa, sb, tgd = put(s.positions), put(fa), put(fb), put(tg)
 for i in range(a.iters):
-    u, ur, uf, t = ev.execute(pos, sa, sb)
+    u, ur, uf, t = ev.execute(pos, sa, sb, targets=tgd)
 torch.cuda.synchronize()
 print({k: round(v, 3) for k, v in t.items()})

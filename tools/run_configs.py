@@ -25,8 +25,10 @@ for name in names:
     t_tab = time.perf_counter() - t0
     dev = torch.device("cuda")
     pos = torch.from_numpy(s.positions).to(dev)
-    sa = torch.from_numpy(s.f if w.kind == "stokeslet" else s.g).to(dev)
-    sb = None if w.kind == "stokeslet" else torch.from_numpy(s.q).to(dev)
+    from paper_1802_07844_b200.ewald import _strengths
+    fa, fb = _strengths(s)
+    sa = torch.from_numpy(np.ascontiguousarray(fa)).to(dev)
+    sb = None if fb is None else torch.from_numpy(np.ascontiguousarray(fb)).to(dev)
     tgd = None if tg is None else torch.from_numpy(tg).to(dev)
     for _ in range(2):
         u, ur, uf, t = ev.execute(pos, sa, sb, targets=tgd)
