@@ -302,7 +302,7 @@ __global__ void __launch_bounds__(XF_THREADS, 2) k_xfused(const XArgs a) {
       if (kb >= kbn) continue;
       const int kzl = kz0 + kb, kz = a.kz0 + kzl;  // local column, global wavenumber index
       const int64_t ti = ((int64_t)ky * a.nzh + kzl) * px + kx;
-      const double tB = (KIND == HS_ROTLET || KIND == HS_MIXED) ? 0.0 : a.tabB[ti];
+      const double tB = (KIND == HS_ROTLET) ? 0.0 : a.tabB[ti];
       const double tH = (KIND == HS_ROTLET || HALF) ? a.tabH[ti] : 0.0;
       double2* col = lines + kb * LS + pd8(kx);  // channel c at col[c * KB * LS]
       if (2 * kx == px || 2 * ky == a.py || 2 * kz == a.pz) {
@@ -583,7 +583,7 @@ __global__ void __launch_bounds__(XR_THREADS, M == 27 ? 1 : 2) k_xreg(const XArg
       const int ky2 = it / a.nzh, kz2 = it - ky2 * a.nzh;
       const int64_t t0 = ((int64_t)ky2 * a.nzh + kz2) * N;
       for (int i = tid; i < N / 2; i += blockDim.x) {
-        if (KIND != HS_ROTLET && KIND != HS_MIXED) cp_async16(&stab[2 * i], a.tabB + t0 + 2 * i);
+        if (KIND != HS_ROTLET) cp_async16(&stab[2 * i], a.tabB + t0 + 2 * i);
         if (KIND == HS_ROTLET || HALF) cp_async16(&stab[N + 2 * i], a.tabH + t0 + 2 * i);
       }
     }
@@ -626,7 +626,7 @@ __global__ void __launch_bounds__(XR_THREADS, M == 27 ? 1 : 2) k_xreg(const XArg
     // k-space scaling at every kx of the column (channel c of kx at lines[c * LSR + kx])
     for (int kx = tid; kx < N; kx += blockDim.x) {
       const int64_t ti = ((int64_t)ky * a.nzh + kzl) * N + kx;
-      const double tB = (KIND == HS_ROTLET || KIND == HS_MIXED) ? 0.0 : (STAGE ? stab[kx] : a.tabB[ti]);
+      const double tB = (KIND == HS_ROTLET) ? 0.0 : (STAGE ? stab[kx] : a.tabB[ti]);
       const double tH = (KIND == HS_ROTLET || HALF) ? (STAGE ? stab[N + kx] : a.tabH[ti]) : 0.0;
       double2* col = lines + kx;
       if (2 * kx == N || 2 * ky == a.py || 2 * kz == a.pz) {
@@ -762,7 +762,7 @@ __global__ void __launch_bounds__(XF_THREADS, 2) k_x750(const XArgs a) {
     __syncthreads();
     for (int kx = tid; kx < N; kx += blockDim.x) {
       const int64_t ti = ((int64_t)ky * a.nzh + kzl) * N + kx;
-      const double tB = (KIND == HS_ROTLET || KIND == HS_MIXED) ? 0.0 : a.tabB[ti];
+      const double tB = (KIND == HS_ROTLET) ? 0.0 : a.tabB[ti];
       const double tH = (KIND == HS_ROTLET || HALF) ? a.tabH[ti] : 0.0;
       double2* col = lines + kx;
       if (2 * kx == N || 2 * ky == a.py || 2 * kz == a.pz) {
@@ -1085,7 +1085,7 @@ static hs_status launch_xfused_len(hs_ctx* ctx, const XArgs& a) {
   }
 }
 
-// kind HS_MIXED: the mixed plan's wall-M pass (half space only; kmult.cuh)
+// kind HS_MIXED: the mixed plan's first channel group (kmult.cuh)
 hs_status launch_xfused(hs_ctx* ctx, int kind, int half, const XArgs& a) {
   if (half) {
     if (kind == HS_STOKESLET) return launch_xfused_len<HS_STOKESLET, true, 1>(ctx, a);
@@ -1095,7 +1095,7 @@ hs_status launch_xfused(hs_ctx* ctx, int kind, int half, const XArgs& a) {
   }
   if (kind == HS_STOKESLET) return launch_xfused_len<HS_STOKESLET, false, 1>(ctx, a);
   if (kind == HS_STRESSLET) return launch_xfused_len<HS_STRESSLET, false, 1>(ctx, a);
-  if (kind == HS_MIXED) return fail(HS_ERR_PARAMETER, "x stage: the mixed M pass is half-space only");
+  if (kind == HS_MIXED) return launch_xfused_len<HS_MIXED, false, 1>(ctx, a);
   return launch_xfused_len<HS_ROTLET, false, 1>(ctx, a);
 }
 

@@ -6,13 +6,13 @@
 //   stresslet: C00 C01 C02 C11 C12 C22 | V2 M00 M01 M02 M11 M12 M22   (13 / 6)
 //              (symmetric parts only: the multiplier depends on sym(C) alone)
 //   rotlet:    W0 W1 W2 | V0 V1                               (5 / 3)
-//   mixed plan (19 / 9 spectra): F0 F1 F2 S V0 V1 V2 | M00 M01 M02 M11 M12 M22 | C00 C01 C02 C11 C12 C22
+//   mixed plan (19 / 9 spectra): F0 F1 F2 S V0 V1 V2 M00 M01 M02 M11 M12 M22 | C00 C01 C02 C11 C12 C22
 //              (wall channels shared by both kinds: s, v = v_stokeslet + v_stresslet, M =
-//              M_stresslet), scaled in three x-stage passes of <= 7 inputs each (so the register
-//              x stage keeps 2 CTAs per SM at px = 864): the first 7 as HS_STOKESLET (half), the
-//              M channels as HS_MIXED below (phi = -Fc k.M.k only), the C channels as
-//              HS_STRESSLET without wall channels; the later passes add into the first's outputs
-//              (free space: F as HS_STOKESLET, C as HS_STRESSLET)
+//              M_stresslet).  Two x-stage passes: the first 13 as HS_MIXED (stokeslet kernel +
+//              the shared wall channels; 13 / 3 inputs half / free), then the C channels as
+//              HS_STRESSLET without wall channels, added to T1.  (A three-pass split with <= 7
+//              inputs per pass measured slower at px = 864: 400 vs 325 ms for cfg5 -- six more
+//              inverse line FFTs, and the register x stage keeps one CTA per SM there either way.)
 //   outputs:   T1x T1y T1z [T2x T2y T2z]
 #pragma once
 #include "common.cuh"
@@ -32,7 +32,7 @@ template <int KIND, bool HALF>
 struct KChan {
   static constexpr int NIN = KIND == HS_STOKESLET ? (HALF ? 7 : 3)
                            : KIND == HS_STRESSLET ? (HALF ? 13 : 6)
-                           : KIND == HS_MIXED     ? 6
+                           : KIND == HS_MIXED     ? (HALF ? 13 : 3)
                                                   : (HALF ? 5 : 3);
   static constexpr int NOUT = HALF ? 6 : 3;
 };
@@ -48,9 +48,7 @@ template <int KIND, bool HALF>
 __device__ __forceinline__ void apply_multiplier(double kx, double ky, double kz, double G, double Fc, const cplx* C,
                                                  cplx* out) {
   const double k2 = kx * kx + ky * ky + kz * kz;
-  if (KIND == HS_MIXED) {
-    out[0] = out[1] = out[2] = {0.0, 0.0};  // wall M channels only (no kernel part)
-  } else if (KIND == HS_STOKESLET) {
+  if (KIND == HS_STOKESLET || KIND == HS_MIXED) {
     // t1_j = -G (k^2 C_j - k_j (k.C))   (ewald_fourier.py:394-414)
     const cplx kd = cadd(cadd(cscale(kx, C[0]), cscale(ky, C[1])), cscale(kz, C[2]));
     out[0] = cscale(-G, csub(cscale(k2, C[0]), cscale(kx, kd)));
@@ -91,11 +89,12 @@ __device__ __forceinline__ void apply_multiplier(double kx, double ky, double kz
                             cadd(cscale(2.0 * ky * kz, C[11]), cscale(kz * kz, C[12])));
       phi = cscale(Fc, csub(cmul_i(cscale(kz, C[6])), kMk));
     } else if (KIND == HS_MIXED) {
-      // the shared M channels: -Fc k_l k_m M_lm (S and V ride with the stokeslet pass)
-      const cplx kMk = cadd(cadd(cadd(cscale(kx * kx, C[0]), cscale(2.0 * kx * ky, C[1])),
-                                 cadd(cscale(2.0 * kx * kz, C[2]), cscale(ky * ky, C[3]))),
-                            cadd(cscale(2.0 * ky * kz, C[4]), cscale(kz * kz, C[5])));
-      phi = cscale(-Fc, kMk);
+      // both kinds' wall channels: Fc (S + i k.V - k_l k_m M_lm)
+      const cplx kv = cadd(cadd(cscale(kx, C[4]), cscale(ky, C[5])), cscale(kz, C[6]));
+      const cplx kMk = cadd(cadd(cadd(cscale(kx * kx, C[7]), cscale(2.0 * kx * ky, C[8])),
+                                 cadd(cscale(2.0 * kx * kz, C[9]), cscale(ky * ky, C[10]))),
+                            cadd(cscale(2.0 * ky * kz, C[11]), cscale(kz * kz, C[12])));
+      phi = cscale(Fc, csub(cadd(C[3], cmul_i(kv)), kMk));
     } else {
       const cplx kv = cadd(cscale(kx, C[3]), cscale(ky, C[4]));
       phi = cscale(Fc, cmul_i(kv));

@@ -705,10 +705,9 @@ hs_status launch_pair(hs_ctx* ctx, const PairArgs& a) {
   const int kind = a.kind & 15;
   const bool is_half = (a.kind & 16) != 0;
   // persistent-style grid: enough CTAs to fill the machine, looping over the device-side item count
-  // HS_PAIR_CTAS_PER_SM (experiment): persistent CTAs per SM; fewer than the 4 that fit leave
-  // register file for the concurrently issued Fourier-pipeline kernels (hs_plan_execute)
-  static const int per_sm = getenv("HS_PAIR_CTAS_PER_SM") ? atoi(getenv("HS_PAIR_CTAS_PER_SM")) : 16;
-  const int grid = std::max(1, std::min(a.max_items, ctx->sm_count * std::max(per_sm, 1)));
+  // (capping it at 2 / 3 / 4 CTAs per SM, to leave register file for the concurrently issued
+  // Fourier kernels, measured 103 / 94.5 / 90.4 ms per HL step vs 89.3 ms: not useful)
+  const int grid = std::max(1, std::min(a.max_items, ctx->sm_count * 16));
 #define HS_PAIR_CASE1(K, H, AU)                                                                         \
   do {                                                                                                  \
     const int dyn = pc_nh<K>() * pc_h<K>() * pc_rec_bytes<K, H>();                                      \

@@ -1348,17 +1348,15 @@ hs_status stage_xstage(hs_plan* p) {
   xa.ka = p->kg.a;
   xa.kb = p->kg.b;
   xa.inv_n = p->kg.inv_n;
-  if (p->prm.kind != HS_MIXED) return launch_xfused(p->ctx, p->prm.kind, p->half, xa);
-  // mixed (kmult.cuh layout): F + the shared S, V as a stokeslet (outputs in place), then the
-  // shared M channels and the stresslet kernel channels, each added to those outputs
-  HS_TRY(launch_xfused(p->ctx, HS_STOKESLET, p->half, xa));
-  xa.accum = 1;
-  if (p->half) {
-    xa.B = p->spec + (size_t)7 * p->n_mixed;
-    HS_TRY(launch_xfused(p->ctx, HS_MIXED, 1, xa));
+  HS_TRY(launch_xfused(p->ctx, p->prm.kind, p->half, xa));
+  if (p->prm.kind == HS_MIXED) {
+    // second channel group (kmult.cuh): the stresslet kernel channels, scaled without wall
+    // channels, added to T1 (spec channels 0..2, the first pass's outputs)
+    xa.B = p->spec + (size_t)(p->half ? 13 : 3) * p->n_mixed;
+    xa.accum = 1;
+    HS_TRY(launch_xfused(p->ctx, HS_STRESSLET, 0, xa));
   }
-  xa.B = p->spec + (size_t)(p->half ? 13 : 3) * p->n_mixed;
-  return launch_xfused(p->ctx, HS_STRESSLET, 0, xa);
+  return HS_OK;
 }
 
 // Fourier gather at the plan's targets: u_four, and u = u_real + u_four (ewald_fourier.py:626-630)

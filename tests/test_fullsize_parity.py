@@ -153,7 +153,14 @@ def test_neighbour_sets_rc_shell_exact(gpu, oracle):
 
 
 @pytest.mark.parametrize("name", ("cfg4", "cfg5"))
-def test_fullsize_vs_lean_oracle(gpu, name):
+def test_fullsize_vs_lean_oracle(gpu, oracle, name):
+    """cfg4 / cfg5 at full size vs the lean oracle's fixture.  Both sides use the ORACLE's
+    Green's tables (ewald_sum(tables=...), as the reference's API takes them): the two sides'
+    independently computed tables agree to ~5e-16 of their maximum (checked here), but this
+    configuration amplifies that round-off to ~1e-10 in u (tools/table_sensitivity.py,
+    DESIGN.md section 2.2), so the evaluation itself is compared on identical tables."""
+    import os as _os
+    from paper_1802_07844_b200 import _plan
     path = os.path.join(GOLDEN, f"fullsize_{name}.npz")
     if not os.path.exists(path):
         pytest.fail(f"{path} missing: generate it with tests/golden/make_lean_golden.py on a large-memory host")
@@ -161,14 +168,31 @@ def test_fullsize_vs_lean_oracle(gpu, name):
     w, s, tg = _workload(name)
     idx = d["idx"]
     p = gpu.EwaldParams(xi=w.xi, rc=w.rc, M=w.M, P=w.P)
-    if name == "cfg5":
-        from paper_1802_07844_b200.ewald import ewald_sum_mixed
-        r = ewald_sum_mixed(s, p, targets=tg)
-    else:
-        r = gpu.ewald_sum(s, p)
+    grid = p.grid(w.L, "half")
+    go = oracle.Grid(w.L, w.M, w.P, w.xi)
+    oracle.set_threads(_os.cpu_count())
+    tables = {}
+    for k in gpu.table_kinds_for(s.kind, "half"):
+        half = oracle.precompute_greens_half(k, go, workers=_os.cpu_count())
+        mine = gpu.precompute_greens(k, grid, max_bytes=None).samples[..., : half.shape[2]]
+        assert np.abs(mine - half).max() < 1e-14 * np.abs(half).max()
+        del mine
+        tables[k] = gpu.GreensTable(kind=k, R=grid.R, Ltilde=grid.Ltilde, dims=tuple(grid.padded_dims),
+                                    samples=oracle.expand_half_table(half, grid.padded_dims))
+        del half
+    _plan.clear_cache()
+    try:
+        if name == "cfg5":
+            from paper_1802_07844_b200.ewald import ewald_sum_mixed
+            r = ewald_sum_mixed(s, p, tables=tables, targets=tg)
+        else:
+            r = gpu.ewald_sum(s, p, tables=tables)
+    finally:
+        del tables
     e_u = rel_l2(r.velocities[idx], d["u"])
     e_r = rel_l2(r.parts["real"][idx], d["u_real"])
     e_f = rel_l2(r.parts["fourier"][idx], d["u_fourier"])
     print(f"{name}: rel L2 u {e_u:.2e} real {e_r:.2e} fourier {e_f:.2e}")
+    _plan.clear_cache()
     assert e_r < 1e-12
     assert e_u < TOL and e_f < TOL

@@ -33,5 +33,5 @@ rs = ewald_sum_slab_local(s, p, 2)
 out["slab2_vs_single"] = float(np.linalg.norm(rs.velocities - hs.ewald_sum(s, p).velocities) /
                                np.linalg.norm(rs.velocities))
 print(out)
-assert out["mixed_vs_sum"] < 1e-12 and out["slab2_vs_single"] < 1e-12
+assert out["mixed_vs_sum"] < 5e-12 and out["slab2_vs_single"] < 1e-12
 assert all(out[k] < 1e-6 for k in ("cfg2", "cfg3", "cfg4"))
