@@ -228,6 +228,13 @@ hs_status hs_direct_sum(hs_ctx* ctx, int kind, int geometry, int64_t n, const do
                         const double* sa, const double* sb, int64_t n_targets, const double* targets,
                         const int64_t* tcols, double* u, int mem);
 
+/* ---- debugging: device-side checks of the checked build (libhsewald_b200_checked.so, built
+ * with -DHS_CHECKED; HSEWALD_CHECKED=1 selects it in the Python package).  Every kernel's ring,
+ * queue and staging indices and its global stores are bounds-checked; the first failing check
+ * ((translation unit << 32) | source line) and the failure count since the last reset are
+ * returned.  The production library returns HS_ERR_CONFIG. */
+hs_status hs_debug_checks(uint64_t* first_failure, uint64_t* failures, int reset);
+
 #ifdef __cplusplus
 }
 #endif

@@ -16,7 +16,10 @@ import numpy as np
 from .errors import DeviceError, raise_for_status
 
 # HSEWALD_LIB: alternative build of the same library (kernel-variant A/B runs in tools/)
-LIB_PATH = os.environ.get("HSEWALD_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libhsewald_b200.so")
+_HERE = os.path.dirname(os.path.abspath(__file__))
+# HSEWALD_CHECKED=1: the checked build (device-side bounds / ring-index checks, hs_debug_checks)
+LIB_PATH = os.environ.get("HSEWALD_LIB") or os.path.join(
+    _HERE, "libhsewald_b200_checked.so" if os.environ.get("HSEWALD_CHECKED") == "1" else "libhsewald_b200.so")
 
 HS_MEM_DEVICE, HS_MEM_HOST = 0, 1
 KIND_ID = {"stokeslet": 0, "stresslet": 1, "rotlet": 2, "mixed": 3}
@@ -86,6 +89,7 @@ _SIGS = [
     ("hs_slab_backward_range", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int]),
     ("hs_direct_sum", C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p,
                                 C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int]),
+    ("hs_debug_checks", C.c_int, [C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), C.c_int]),
 ]
 EXPORTED = [s[0] for s in _SIGS]
 
@@ -164,3 +168,16 @@ class Context:
 
     def launches(self) -> int:
         return int(self.lib.hs_ctx_launch_count(self.handle))
+
+
+def debug_checks(reset: bool = True) -> dict:
+    """Device-side check results of the checked build (hs_debug_checks): failures since the last
+    reset and the first failing (translation unit, source line)."""
+    lib = load_library()
+    first, count = C.c_uint64(), C.c_uint64()
+    check(lib.hs_debug_checks(C.byref(first), C.byref(count), 1 if reset else 0))
+    tu = {1: "pair.cu", 2: "gridding.cu", 3: "fft.cu", 4: "plan.cu", 5: "sort.cu", 6: "kspace.cu",
+          7: "cell_list.cu", 8: "api.cu"}
+    f = first.value
+    return {"failures": int(count.value), "first": None if not f else f"{tu.get(f >> 32, f >> 32)}:{f & 0xffffffff}"}
+

@@ -1,5 +1,6 @@
 // api.cu -- context management and the stand-alone C-ABI entry points
 // (cell list, spread, gather, Green's-table precompute, direct sum).
+#define HS_TU_ID 8  // checked build: source of a failing HS_CHECK
 #include <cufft.h>
 
 #include <cmath>
@@ -124,11 +125,46 @@ static inline int gsz(hs_ctx* ctx, int64_t n) {
   return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 256), (int64_t)ctx->sm_count * 8));
 }
 
+#define HS_TU_DECL(NAME) void chk_collect_##NAME(unsigned long long*, unsigned long long*, int);
+HS_TU_DECL(pair)
+HS_TU_DECL(gridding)
+HS_TU_DECL(fft)
+HS_TU_DECL(plan)
+HS_TU_DECL(sort)
+HS_TU_DECL(kspace)
+HS_TU_DECL(cell_list)
+#undef HS_TU_DECL
+HS_DEFINE_CHECK_COLLECT(api)
+
 }  // namespace hs
 
 using namespace hs;
 
 extern "C" {
+
+hs_status hs_debug_checks(uint64_t* first_failure, uint64_t* failures, int reset) {
+  if (!first_failure || !failures) return fail(HS_ERR_PARAMETER, "null output");
+#ifdef HS_CHECKED
+  unsigned long long f = 0, c = 0;
+  HS_CUDA(cudaDeviceSynchronize());
+  chk_collect_pair(&f, &c, reset);
+  chk_collect_gridding(&f, &c, reset);
+  chk_collect_fft(&f, &c, reset);
+  chk_collect_plan(&f, &c, reset);
+  chk_collect_sort(&f, &c, reset);
+  chk_collect_kspace(&f, &c, reset);
+  chk_collect_cell_list(&f, &c, reset);
+  chk_collect_api(&f, &c, reset);
+  *first_failure = f;
+  *failures = c;
+  return HS_OK;
+#else
+  (void)reset;
+  *first_failure = 0;
+  *failures = 0;
+  return fail(HS_ERR_CONFIG, "not a checked build (make -C paper_1802_07844_b200/csrc checked)");
+#endif
+}
 
 const char* hs_last_error(void) { return t_last_error.c_str(); }
 

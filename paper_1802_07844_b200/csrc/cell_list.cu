@@ -5,6 +5,7 @@
 // (cx*ny + cy)*nz + cz) using explicitly rounded intrinsics so that no FMA
 // contraction can move a point across a cell face; the stable argsort is the
 // deterministic counting sort in sort.cu.
+#define HS_TU_ID 7  // checked build: source of a failing HS_CHECK
 #include <cmath>
 
 #include "common.cuh"
@@ -81,5 +82,7 @@ hs_status launch_cell_keys(hs_ctx* ctx, const double* pos, int n_src, int n_tota
   HS_LAUNCHED(ctx);
   return HS_OK;
 }
+
+HS_DEFINE_CHECK_COLLECT(cell_list)
 
 }  // namespace hs

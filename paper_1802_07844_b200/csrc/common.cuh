@@ -56,6 +56,44 @@ __device__ __forceinline__ double window_d(double pos, double origin, double h, 
   return __dsub_rn(pos, __dadd_rn(origin, __dmul_rn((double)idx, h)));
 }
 
+// ---- checked build (make checked -> libhsewald_b200_checked.so, -DHS_CHECKED): HS_CHECK(c)
+// records the first failing (translation unit, source line) and a failure count in per-TU
+// device words that hs_debug_checks() collects; the production build compiles it away.
+// (compute-sanitizer is closed on the GPU pool this was built on: DESIGN.md section 2.6.)
+#ifdef HS_CHECKED
+static __device__ unsigned long long g_chk_first;
+static __device__ unsigned long long g_chk_count;
+#ifndef HS_TU_ID
+#define HS_TU_ID 0
+#endif
+#define HS_CHECK(c)                                                                               \
+  do {                                                                                            \
+    if (!(c)) {                                                                                   \
+      atomicCAS(&::hs::g_chk_first, 0ull, ((unsigned long long)HS_TU_ID << 32) | (unsigned)__LINE__); \
+      atomicAdd(&::hs::g_chk_count, 1ull);                                                        \
+    }                                                                                             \
+  } while (0)
+#define HS_DEFINE_CHECK_COLLECT(NAME)                                                             \
+  void chk_collect_##NAME(unsigned long long* first, unsigned long long* count, int reset) {       \
+    unsigned long long f = 0, c = 0;                                                              \
+    cudaMemcpyFromSymbol(&f, g_chk_first, sizeof(f));                                             \
+    cudaMemcpyFromSymbol(&c, g_chk_count, sizeof(c));                                             \
+    if (f && !*first) *first = f;                                                                 \
+    *count += c;                                                                                  \
+    if (reset) {                                                                                  \
+      const unsigned long long z = 0;                                                             \
+      cudaMemcpyToSymbol(g_chk_first, &z, sizeof(z));                                             \
+      cudaMemcpyToSymbol(g_chk_count, &z, sizeof(z));                                             \
+    }                                                                                             \
+  }
+#else
+#define HS_CHECK(c) \
+  do {              \
+  } while (0)
+#define HS_DEFINE_CHECK_COLLECT(NAME) \
+  void chk_collect_##NAME(unsigned long long*, unsigned long long*, int) {}
+#endif
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

@@ -13,6 +13,7 @@
 // The full (px,py,pz/2+1) spectrum of a channel therefore never exists in HBM;
 // the x-stage replaces 13 full-spectrum passes + the scale pass of a 3-D cuFFT
 // pipeline with one read of the sources and one write of the outputs.
+#define HS_TU_ID 3  // checked build: source of a failing HS_CHECK
 #include <cmath>
 #include <vector>
 
@@ -596,6 +597,7 @@ __global__ void __launch_bounds__(XR_THREADS, M == 27 ? 1 : 2) k_xreg(const XArg
   for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
     const int ky = item / a.nzh;
     const int kzl = item - ky * a.nzh, kz = a.kz0 + kzl;  // local column, global wavenumber index
+    HS_CHECK(ky < a.py && kzl < a.nzh && kz <= a.pz / 2 && a.nx <= N);
     if (STAGE) cp_async_wait_all();
     __syncthreads();  // previous item's lines consumed (and twiddles / staged inputs visible)
     for (int c = warp; c < NIN; c += NW) {
@@ -1134,5 +1136,7 @@ hs_status launch_table_to_xmajor(hs_ctx* ctx, const double* in, int px, int py, 
   HS_LAUNCHED(ctx);
   return HS_OK;
 }
+
+HS_DEFINE_CHECK_COLLECT(fft)
 
 }  // namespace hs

@@ -14,6 +14,7 @@
 // Gathering: one warp per target, lanes over the P z-nodes of one (x,y)
 // support column (coalesced 8*P-byte reads), loop over the P*P columns,
 // shuffle reduction over lanes.
+#define HS_TU_ID 2  // checked build: source of a failing HS_CHECK
 #include <cmath>
 #include <cstdlib>
 
@@ -347,6 +348,10 @@ __global__ void __launch_bounds__((NCW + SW_NP) * 32, NCW == 8 ? 2 : 1) k_spread
           const double* sx = src + (ex[h] & ~1);
           const double* sy = src + wt.wx + (ey[h] & ~1);
           const double* sz = src + wt.wx + wt.wy + (ez[h] & ~1);
+          // the tile's slices lie inside the source's zero-padded window rows
+          HS_CHECK((ex[h] & ~1) >= 0 && (ex[h] & ~1) + RX <= wt.wx && (ey[h] & ~1) >= 0 &&
+                   (ey[h] & ~1) + RY <= wt.wy && (ez[h] & ~1) >= 0 && (ez[h] & ~1) + RZ <= wt.wz);
+          HS_CHECK(b < K && sl < SW_CH && cur.row[h] >= 0);
 #pragma unroll
           for (int j = 0; j < RX / 2; ++j) cpa16(&bx_(b)[sl][2 * j], sx + 2 * j);
 #pragma unroll
@@ -397,6 +402,7 @@ __global__ void __launch_bounds__((NCW + SW_NP) * 32, NCW == 8 ? 2 : 1) k_spread
         if (sk >= 0) {
           const unsigned par = s_mask[sk];
           const int pxo = (par >> PB) & 1, pyo = (par >> (PB + 1)) & 1, pzo = (par >> (PB + 2)) & 1;
+          HS_CHECK(sk < SW_CH && pzo + rq < RZ && pxo + wx0 + 3 < RX && pyo + wy0 + PY - 1 < RY);
           bz = s_wz[sk][pzo + rq];  // B[k][n] = wz_{s_k}(z_n), n = rq
 #pragma unroll
           for (int ch = 0; ch < NCH; ++ch) q[ch] = s_q[sk][ch];
@@ -779,6 +785,8 @@ __global__ void __launch_bounds__(G7_WARPS * 32, 2) k_gather7(const double4* __r
     issue_step(0);
     issue_step(1);
     const int zn = min(W0[2] - C0[2] + lane, nzu - 1);  // this lane's node in the staged column
+    HS_CHECK(zn >= 0 && zn < G7_ZC && C0[0] >= 0 && C0[1] >= 0 && C0[2] >= 0 && C1[0] <= g.dims[0] &&
+             C1[1] <= g.dims[1] && C1[2] <= g.dims[2] && nzu * CPN <= G7_ZC * CPN);
     double E[TG][NCH];
 #pragma unroll
     for (int tt = 0; tt < TG; ++tt)
@@ -787,6 +795,7 @@ __global__ void __launch_bounds__(G7_WARPS * 32, 2) k_gather7(const double4* __r
     int cx = 0, cy = 0, slot = 0;
     // one column: node values and window factors, then the FMAs
     auto column = [&](int sl) {
+      HS_CHECK(sl >= 0 && sl < G7_R && cx < nxu && cy < nyu && cx < GW && cy < GW);
       const double2* src = reinterpret_cast<const double2*>(&s_ring[sl][zn * PITCH]);
       double v[PITCH], cxy[TG];
 #pragma unroll
@@ -902,5 +911,7 @@ hs_status launch_gather_fourier(hs_ctx* ctx, const double4* pts, const int* orig
   HS_LAUNCHED(ctx);
   return HS_OK;
 }
+
+HS_DEFINE_CHECK_COLLECT(gridding)
 
 }  // namespace hs

@@ -21,6 +21,7 @@
 //              (symmetric parts only: the kernel multiplier depends on sym(C) alone)
 //   rotlet:    W0 W1 W2 | V0 V1                  (5 / 3)
 //   outputs:   T1x T1y T1z [T2x T2y T2z]  written to channels 0..5
+#define HS_TU_ID 6  // checked build: source of a failing HS_CHECK
 #include <cmath>
 
 #include "common.cuh"
@@ -371,5 +372,7 @@ hs_status launch_take_half(hs_ctx* ctx, const double* full, const int64_t p[3], 
   HS_LAUNCHED(ctx);
   return HS_OK;
 }
+
+HS_DEFINE_CHECK_COLLECT(kspace)
 
 }  // namespace hs

@@ -20,6 +20,7 @@
 //   c0 = C/r, c1 = (C/r + e)/r^2, c2 = (3 c1 + 2 xi^2 e)/r^2,
 //   c3 = -(5 c2 + 4 xi^4 e)/r^2,  e = (2 xi/sqrt(pi)) exp(-xi^2 r^2), C = erfc(xi r)
 // which reduce to (1/r, 1/r^3, 3/r^5, -15/r^7) for the direct sum (C=1, e=0).
+#define HS_TU_ID 1  // checked build: source of a failing HS_CHECK
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -67,6 +68,11 @@ __device__ __forceinline__ double rcp_pos(double v) {
   for (int it = 0; it < 2; ++it) y = fma(y, fma(-v, y, 1.0), y);
   return y;
 }
+#ifndef PC_DRAIN2
+#define PC_DRAIN2 1   // queue drains by two-pair rounds where lanes have >= 2 entries
+#endif
+// (Estrin's scheme for the erfcx / exp polynomials -- dependency depth ~log2(deg) instead of
+// deg -- measured 83 vs 38 ms for the HL pair kernel: Horner with constant-bank operands stays.)
 __device__ __forceinline__ double erfc_poly_from_E(double x, double E) {
   const double s = fma(HS_EP_S1, rcp_pos(fmin(x, HS_EP_XMAX) + HS_EP_K), HS_EP_S0);
   double p = c_erfcx_poly[0];
@@ -471,6 +477,7 @@ __global__ void __launch_bounds__(PC_TG, pc_minb<KIND>()) k_pair_q(const PairArg
       vcur[k] = (int)(((long long)(threadIdx.x + k * PC_TG) * pstride) % max(ncand, 1));
     auto pop_eval = [&]() {
       const int jj = q[head & (PC_Q - 1)][lane];
+      HS_CHECK(jj < PC_K && head < tail);
       ++head;
       ++n_acc;
       eval_one(jj);
@@ -480,6 +487,7 @@ __global__ void __launch_bounds__(PC_TG, pc_minb<KIND>()) k_pair_q(const PairArg
     auto pop_eval2 = [&]() {
       const int j1 = q[head & (PC_Q - 1)][lane];
       const int j2 = q[(head + 1) & (PC_Q - 1)][lane];
+      HS_CHECK(j1 < PC_K && j2 < PC_K && head + 2 <= tail);
       head += 2;
       n_acc += 2;
       double4 S1, A1, B1, S2, A2, B2;
@@ -524,6 +532,8 @@ __global__ void __launch_bounds__(PC_TG, pc_minb<KIND>()) k_pair_q(const PairArg
             else rhi = mid - 1;
           }
           const int row = run_beg[r] + (v - run_pre[r]);
+          HS_CHECK(r >= 0 && r < nrun && v >= run_pre[r] && v < run_pre[r + 1] && hb + j < PC_K &&
+                   row < a.start[nx * ny * nz]);
           const double4 S = a.P[row];
           const double4 A = a.A[row];
           sXY[hb + j] = make_double2(S.x, S.y);
@@ -616,13 +626,25 @@ __global__ void __launch_bounds__(PC_TG, pc_minb<KIND>()) k_pair_q(const PairArg
             if (tvalid && tail - head >= 2) pop_eval2();
           }
         }
+        HS_CHECK(tail - head <= PC_Q);
+        // overflow guard: two-pair rounds for the lanes with a backlog (the fullest lane has
+        // > PC_Q - 32 >= 2 entries, so every round makes progress; single entries wait)
         while ((int)__reduce_max_sync(0xffffffffu, (unsigned)(tail - head)) > PC_Q - 32) {
-          if (tail > head) pop_eval();
+          if (PC_DRAIN2) {
+            if (tail - head >= 2) pop_eval2();
+          } else if (tail > head) {
+            pop_eval();
+          }
         }
       }
     }
+    if (PC_DRAIN2) {
+      while (__any_sync(0xffffffffu, tail - head >= 2)) {
+        if (tail - head >= 2) pop_eval2();
+      }
+    }
     while (__any_sync(0xffffffffu, tail > head)) {
-      if (tail - head >= 2)
+      if (!PC_DRAIN2 && tail - head >= 2)
         pop_eval2();
       else if (tail > head)
         pop_eval();
@@ -797,5 +819,7 @@ hs_status launch_direct(hs_ctx* ctx, int kind, int half, int n_real, int n_src, 
   HS_LAUNCHED(ctx);
   return HS_OK;
 }
+
+HS_DEFINE_CHECK_COLLECT(pair)
 
 }  // namespace hs

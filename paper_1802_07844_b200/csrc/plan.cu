@@ -9,6 +9,7 @@
 //                scale (one pass, in place) -> batched cuFFT Z2D -> gather at
 //                targets, adding the real-space part.
 // Phase times are CUDA events on the plan's stream.
+#define HS_TU_ID 4  // checked build: source of a failing HS_CHECK
 #include <cufft.h>
 
 #include <cmath>
@@ -223,6 +224,7 @@ __global__ void k_mirror_z(double* __restrict__ grid, int nch, unsigned kern_mas
       g[k] = kern ? v + sg * v : v;
     } else {
       const int kk = nz - k;
+      HS_CHECK(k > 0 && k < half_n && kk > half_n && kk < nz);
       const double a = g[k], b = g[kk];
       g[k] = kern ? a + sg * b : b;
       g[kk] = kern ? b + sg * a : a;
@@ -1007,6 +1009,8 @@ static hs_status greens_half_table_full(hs_ctx* ctx, int kind, double R, double 
   cleanup();
   return rs;
 }
+HS_DEFINE_CHECK_COLLECT(plan)
+
 }  // namespace hs
 
 extern "C" hs_status hs_plan_build_tables(hs_plan* p, const int64_t big[3], double R, const int64_t guards[3]) {

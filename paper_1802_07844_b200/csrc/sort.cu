@@ -9,14 +9,17 @@
 // index.  Since a stable argsort orders equal keys by ascending index, ranking
 // every element of a segment by its value reproduces it exactly, independent
 // of the scatter order.
+#define HS_TU_ID 5  // checked build: source of a failing HS_CHECK
 #include "common.cuh"
 #include "kernels.cuh"
 
 namespace hs {
 
-__global__ void k_histogram(const int* __restrict__ keys, int n, int* __restrict__ counts) {
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+__global__ void k_histogram(const int* __restrict__ keys, int n, int nb, int* __restrict__ counts) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    HS_CHECK(keys[i] >= 0 && keys[i] < nb);
     atomicAdd(&counts[keys[i]], 1);
+  }
 }
 
 // Single-CTA exclusive scan of counts[0..nb) into start[0..nb] (start[nb] = total).
@@ -125,6 +128,7 @@ __global__ void k_scatter(const int* __restrict__ keys, int n, int* __restrict__
                           int* __restrict__ tmp) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     int p = atomicAdd(&cursor[keys[i]], 1);
+    HS_CHECK(p >= 0 && p < n);
     tmp[p] = i;
   }
 }
@@ -145,6 +149,7 @@ __global__ void k_segment_rank_warp(const int* __restrict__ start, int nb, const
       const int e = tmp[s + i];
       int r = 0;
       for (int j = 0; j < len; ++j) r += (__ldg(&tmp[s + j]) < e);
+      HS_CHECK(r < len);
       order[s + r] = e;
     }
   }
@@ -169,6 +174,7 @@ __global__ void k_segment_rank_block(const int* __restrict__ start, const int* _
       const int m = min(1024, len - j0);
       for (int j = 0; j < m; ++j) r += (tile[j] < e);
     }
+    HS_CHECK(i >= len || r < len);
     if (i < len) order[s + r] = e;
   }
   __syncthreads();
@@ -197,7 +203,7 @@ hs_status counting_sort(hs_ctx* ctx, const int* keys, int n, int nb, int* order,
   HS_CUDA(cudaMemsetAsync(maxc, 0, sizeof(int) * 2, st));
   const int gs = (int)std::min<int64_t>(ceil_div(std::max(n, 1), 256), ctx->sm_count * 8);
   if (n > 0) {
-    k_histogram<<<gs, 256, 0, st>>>(keys, n, counts);
+    k_histogram<<<gs, 256, 0, st>>>(keys, n, nb, counts);
     HS_LAUNCHED(ctx);
   }
   if (nb <= 4 * SCAN_TILE) {
@@ -238,5 +244,7 @@ hs_status exclusive_scan(hs_ctx* ctx, const int* in, int n, int* out, int* scrat
   HS_LAUNCHED(ctx);
   return HS_OK;
 }
+
+HS_DEFINE_CHECK_COLLECT(sort)
 
 }  // namespace hs

@@ -2,7 +2,8 @@
 set -x
 out=gpurun_out/${1:-check}
 mkdir -p $out
-timeout 900 python -m pytest tests/test_fullsize_parity.py -q -s -k "lean_oracle" > $out/pytest_lean.log 2>&1
-timeout 600 python bench.py --workload cfg5 --steps 2 --warmup 3 --no-cpu-baseline > $out/bench_cfg5.json 2> $out/bench_cfg5.err
-bash tools/ncu_round.sh ${1:-check}/ncu
+for v in e0d0 e0d1 e1d0; do
+  HSEWALD_LIB=$PWD/paper_1802_07844_b200/libhs_$v.so python bench.py --steps 5 --warmup 3 --no-cpu-baseline > $out/bench_$v.json 2> $out/bench_$v.err
+done
+python bench.py --steps 5 --warmup 3 --no-cpu-baseline > $out/bench_e1d1.json 2> $out/bench_e1d1.err
 du -sh gpurun_out

@@ -32,6 +32,11 @@ s, _ = make_system("cfg2", n=n)
 rs = ewald_sum_slab_local(s, p, 2)
 out["slab2_vs_single"] = float(np.linalg.norm(rs.velocities - hs.ewald_sum(s, p).velocities) /
                                np.linalg.norm(rs.velocities))
+from paper_1802_07844_b200 import _lib  # noqa: E402
+if os.environ.get("HSEWALD_CHECKED") == "1":
+    out["device_checks"] = _lib.debug_checks()
 print(out)
+if "device_checks" in out:
+    assert out["device_checks"]["failures"] == 0, out["device_checks"]
 assert out["mixed_vs_sum"] < 5e-12 and out["slab2_vs_single"] < 1e-12
 assert all(out[k] < 1e-6 for k in ("cfg2", "cfg3", "cfg4"))
