@@ -61,11 +61,17 @@ __device__ __forceinline__ double erfc_from_E(double xw, double E, const double2
 // shared-memory pipe is its co-bottleneck) for ~12 more DFMAs.  x > 8 (xi r_c > 8 only):
 // evaluated at 8, where erfc < 1.2e-29, below the resolution of any sum it enters.
 #include "erfcx_poly.inc"
+// Newton steps after the hardware rsqrt / rcp approximations (~2^-23): 1 step leaves ~2^-46
+// relative error (erfc ~1e-14, far below the 2e-13 of the reference's own erfc table), 2 steps
+// round-off level
+#ifndef PC_NEWTON
+#define PC_NEWTON 2
+#endif
 __device__ __forceinline__ double rcp_pos(double v) {
   double y;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(v));
 #pragma unroll
-  for (int it = 0; it < 2; ++it) y = fma(y, fma(-v, y, 1.0), y);
+  for (int it = 0; it < PC_NEWTON; ++it) y = fma(y, fma(-v, y, 1.0), y);
   return y;
 }
 #ifndef PC_DRAIN2
@@ -112,7 +118,7 @@ __device__ __forceinline__ double rsqrt_pos(double r2) {
   double y;
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(r2));
 #pragma unroll
-  for (int it = 0; it < 2; ++it) {  // ~2^-23 -> 2^-46 -> rounding level
+  for (int it = 0; it < PC_NEWTON; ++it) {  // ~2^-23 -> 2^-46 -> rounding level
     const double h = r2 * y;
     const double e = fma(-h, y, 1.0);
     y = fma(0.5 * y, e, y);
