@@ -74,7 +74,6 @@ hs_status launch_grid_keys(hs_ctx* ctx, const double* pos, int n_src, int n, int
 }
 
 // ---------------------------------------------------------------------------
-constexpr int SP_MAXCH = 4;    // channels per launch (register budget)
 constexpr int SP_MAXP = 64;
 
 __device__ __forceinline__ void dmma_884(double& c0, double& c1, double a, double b) {
@@ -866,6 +865,228 @@ __global__ void __launch_bounds__(G7_WARPS * 32, 2) k_gather7(const double4* __r
   }
 }
 
+// Gather on the FP64 tensor pipe (k_gather8, default; G7_MMA=0 selects k_gather7).  Same
+// items, runs, column staging ring and x / y window tables as k_gather7, but the per-column
+// contraction over z is a DMMA: for a run of <= 8 targets t and its 32-node z window,
+//   D[t][n] += A[t][k] B[k][n],   A[t][k] = wz_t(z0 + 4 s + k),   B[k][n] = G_c(col, z0 + 4 s + k)
+// with n = (column of the 4-column step, channel of a channel pair), 8 k-steps of 4 nodes; then
+// u_t,c += wx_t(col) wy_t(col) D[t][n].  One m8n8k4 DMMA does 256 FMAs where k_gather7 issued
+// 8 targets x 6 channels DFMAs per lane per column: ~5x fewer instructions per useful FMA, and
+// ~60 registers instead of 200.  (Fragments of mma.m8n8k4.f64: A[lane/4][lane%4],
+// B[lane%4][lane/4], C/D[lane/4][2 (lane%4) + {0,1}].)
+#ifndef G7_MMA
+#define G7_MMA 1
+#endif
+template <int NCH, int PITCH>
+__global__ void __launch_bounds__(G7_WARPS * 32) k_gather8(const double4* __restrict__ pts,
+                                                          const int* __restrict__ orig, const int4* __restrict__ items,
+                                                          const int* __restrict__ n_items_d, GridGeom g,
+                                                          const double* __restrict__ T,
+                                                          double* __restrict__ u_four, double* __restrict__ u_tot,
+                                                          const double* __restrict__ u_real,
+                                                          unsigned* __restrict__ flags) {
+  constexpr int TG = G7_TG, GW = G7_GW, NT = G7_WARPS * 32, CPN = PITCH / 2;  // 16-byte chunks per node
+  constexpr int NCP = (NCH + 1) / 2;  // channel pairs
+  static_assert(G7_STEP == 4, "one DMMA n-block = 4 columns x a channel pair");
+  __shared__ double s_w[G7_WARPS][2][TG][GW];
+  __shared__ __align__(16) double s_ring[G7_R][G7_ZC * PITCH];
+  __shared__ int s_u[G7_WARPS][6];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int P = g.P;
+  const int ft = lane >> 2, fk = lane & 3;  // fragment row (target) / k index; B: n = ft
+  double(*wx_tab)[GW] = s_w[warp][0];
+  double(*wy_tab)[GW] = s_w[warp][1];
+  const int n_items = *n_items_d;
+  for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+    const int4 item = items[it];
+    int rb = item.x;
+#pragma unroll
+    for (int w = 0; w < G7_WARPS; ++w)
+      if (w < warp) rb += (item.z >> (8 * w)) & 0xff;
+    const int rlen = (item.z >> (8 * warp)) & 0xff;
+    const int t = rb + lane;
+    const bool valid = lane < rlen;
+    const double4 pt = pts[valid ? t : item.x];
+    const double pc[3] = {pt.x, pt.y, pt.z};
+    int lo[3];
+    bool bad = false;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const int64_t l = g_lo(g, k, pc[k]);
+      bad |= (l < 0) || (l + P > g.dims[k]);
+      lo[k] = (int)l;
+    }
+    if (valid && bad) atomicOr(flags, FLAG_OUT_OF_GRID);
+    const bool act = valid && !bad;
+    const unsigned amask = __ballot_sync(0xffffffffu, act);
+    int W0[3], W1[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      W0[k] = (int)__reduce_min_sync(0xffffffffu, (unsigned)(act ? lo[k] : 0x7fffffff));
+      W1[k] = (int)__reduce_max_sync(0xffffffffu, (unsigned)(act ? lo[k] + P : 0));
+    }
+    __syncthreads();  // previous item done with s_u / ring / tables
+    if (lane == 0) {
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        s_u[warp][k] = amask ? W0[k] : 0x7fffffff;
+        s_u[warp][3 + k] = amask ? W1[k] : (int)0x80000000;
+      }
+    }
+    __syncthreads();
+    int C0[3] = {0x7fffffff, 0x7fffffff, 0x7fffffff}, C1[3] = {(int)0x80000000, (int)0x80000000, (int)0x80000000};
+#pragma unroll
+    for (int w = 0; w < G7_WARPS; ++w)
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        C0[k] = min(C0[k], s_u[w][k]);
+        C1[k] = max(C1[k], s_u[w][3 + k]);
+      }
+    if (C0[0] == 0x7fffffff) continue;  // no active target in the item
+    const int nxu = C1[0] - C0[0], nyu = C1[1] - C0[1], nzu = C1[2] - C0[2];
+    if (nxu <= 0 || nxu > GW || nyu > GW || nzu > G7_ZC) continue;  // (out-of-grid targets only)
+    // x / y window tables of this warp's run (0 outside a target's support)
+#pragma unroll
+    for (int tt = 0; tt < TG; ++tt) {
+      const bool tin = (amask >> tt) & 1u;
+      const double px = __shfl_sync(0xffffffffu, pc[0], tt), py = __shfl_sync(0xffffffffu, pc[1], tt);
+      const int lx = __shfl_sync(0xffffffffu, lo[0], tt), ly = __shfl_sync(0xffffffffu, lo[1], tt);
+      double vx = 0.0, vy = 0.0;
+      const int x = C0[0] + lane, y = C0[1] + lane;
+      if (tin && lane < nxu && x >= lx && x < lx + P) {
+        const double d = g_d(g, 0, px, x);
+        vx = exp(-g.alpha * d * d);
+      }
+      if (tin && lane < nyu && y >= ly && y < ly + P) {
+        const double d = g_d(g, 1, py, y);
+        vy = exp(-g.alpha * d * d);
+      }
+      wx_tab[tt][lane] = vx;
+      wy_tab[tt][lane] = vy;
+    }
+    // A fragments: wz of fragment row ft (target ft of the run) at nodes W0z + 4 s + fk
+    double a[8];
+    {
+      const bool tin = (amask >> ft) & 1u;
+      const double pz = __shfl_sync(0xffffffffu, pc[2], ft);
+      const int lz = __shfl_sync(0xffffffffu, lo[2], ft);
+#pragma unroll
+      for (int sk = 0; sk < 8; ++sk) {
+        const int z = W0[2] + 4 * sk + fk;
+        double v = 0.0;
+        if (tin && z >= lz && z < lz + P) {
+          const double d = g_d(g, 2, pz, z);
+          v = exp(-g.alpha * d * d);
+        }
+        a[sk] = v;
+      }
+    }
+    // B rows: staged node of k-step sk for this lane's k (clamped into the staged range, where
+    // every target's A is zero anyway)
+    const int zoff = W0[2] - C0[2];
+    HS_CHECK(!amask || (zoff >= 0 && zoff < G7_ZC && nzu <= G7_ZC));  // (idle warps skip the steps)
+    __syncwarp();
+    const int ncol = nxu * nyu, nchunk = nzu * CPN;
+    const double* colp = T + (int64_t)C0[0] * g.stride[0] + (int64_t)C0[1] * g.stride[1] + (int64_t)C0[2] * PITCH +
+                         2 * threadIdx.x;
+    const int64_t row_wrap = g.stride[0] - (int64_t)nyu * g.stride[1];
+    int iy = 0, nissued = 0;
+    auto issue_step = [&](int step) {
+#pragma unroll
+      for (int j = 0; j < G7_STEP; ++j) {
+        if (nissued < ncol) {
+          double* dst = s_ring[(step * G7_STEP + j) % G7_R] + 2 * threadIdx.x;
+#pragma unroll
+          for (int q = 0; q < (G7_ZC * CPN + NT - 1) / NT; ++q)
+            if ((int)threadIdx.x + q * NT < nchunk) cp_async16(dst + 2 * q * NT, colp + 2 * q * NT);
+          ++nissued;
+          colp += g.stride[1];
+          if (++iy == nyu) {
+            iy = 0;
+            colp += row_wrap;
+          }
+        }
+      }
+      cp_async_commit();
+    };
+    issue_step(0);
+    issue_step(1);
+    double acc[2 * NCP];
+#pragma unroll
+    for (int c = 0; c < 2 * NCP; ++c) acc[c] = 0.0;
+    // column index of this lane's D column (fk) in the current step, and of its B column (ft/2)
+    int colD = fk;
+    // one step of (up to) 4 staged columns from ring slot sl: 8 k-steps x NCP channel pairs
+    auto step = [&](int sl, int ncols) {
+      const int cb = ft >> 1;                 // B: column of the step
+      const bool bval = cb < ncols;
+      const double* bcol = s_ring[sl + (bval ? cb : 0)] + (ft & 1);
+      double d[NCP][2];
+#pragma unroll
+      for (int cp = 0; cp < NCP; ++cp) d[cp][0] = d[cp][1] = 0.0;
+#pragma unroll
+      for (int sk = 0; sk < 8; ++sk) {
+        const int zi = min(zoff + 4 * sk + fk, nzu - 1);
+#pragma unroll
+        for (int cp = 0; cp < NCP; ++cp) {
+          const double b = bval ? bcol[zi * PITCH + 2 * cp] : 0.0;
+          dmma_884(d[cp][0], d[cp][1], a[sk], b);
+        }
+      }
+      // epilogue: D[ft][2 fk + j] belongs to column fk of the step, channels 2 cp + j
+      double w = 0.0;
+      if (fk < ncols && colD < ncol) {
+        const int cx = colD / nyu, cy = colD - cx * nyu;
+        HS_CHECK(cx < GW && cy < GW);
+        w = wx_tab[ft][cx] * wy_tab[ft][cy];
+      }
+#pragma unroll
+      for (int cp = 0; cp < NCP; ++cp) {
+        acc[2 * cp] = fma(w, d[cp][0], acc[2 * cp]);
+        acc[2 * cp + 1] = fma(w, d[cp][1], acc[2 * cp + 1]);
+      }
+      colD += G7_STEP;
+    };
+    int slot = 0;
+    const int nfull = ncol / G7_STEP, nrem = ncol - nfull * G7_STEP;
+    for (int sidx = 0; sidx < nfull; ++sidx) {
+      cp_async_wait<1>();
+      __syncthreads();
+      issue_step(sidx + 2);
+      if (amask) step(slot, G7_STEP);
+      slot = slot + G7_STEP == G7_R ? 0 : slot + G7_STEP;
+    }
+    if (nrem) {  // ragged last step (already issued)
+      cp_async_wait<1>();
+      __syncthreads();
+      if (amask) step(slot, nrem);
+    }
+    cp_async_wait<0>();
+    // the 4 lanes of a target hold its sums over the columns = fk (mod 4): reduce, then lane
+    // tt takes target tt's result from lane 4 tt
+    double res[NCH];
+#pragma unroll
+    for (int c = 0; c < 2 * NCP; ++c) {
+      double v = acc[c];
+      v += __shfl_xor_sync(0xffffffffu, v, 1);
+      v += __shfl_xor_sync(0xffffffffu, v, 2);
+      const double r = __shfl_sync(0xffffffffu, v, (lane & 7) * 4);
+      if (c < NCH) res[c] = r;
+    }
+    if (act) {
+      const int o = orig[t];
+      const double h3p = g.h * g.h * g.h * g.pref;
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        double v = res[k] * h3p;
+        if (NCH == 6) v -= pt.z * (res[3 + k] * h3p);
+        if (u_four) u_four[3 * (size_t)o + k] = v;
+        if (u_tot) u_tot[3 * (size_t)o + k] = (u_real ? u_real[3 * (size_t)o + k] : 0.0) + v;
+      }
+    }
+  }
+}
+
 hs_status launch_gather_fourier(hs_ctx* ctx, const double4* pts, const int* orig, int n, int half, const GridGeom& g,
                                 const double* T, double* u_fourier, double* u_total, const double* u_real,
                                 const int* bstart) {
@@ -901,6 +1122,20 @@ hs_status launch_gather_fourier(hs_ctx* ctx, const double4* pts, const int* orig
   HS_TRY(exclusive_scan(ctx, cnt, nb4, istart, sc));
   k_g7_fill<<<gsb, 128, 0, ctx->stream>>>(pts, bstart, nb4, g.dims[2], g, istart, items);
   HS_LAUNCHED(ctx);
+  if (G7_MMA) {
+    int per_sm = 0;
+    HS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, half ? k_gather8<6, 6> : k_gather8<3, 4>,
+                                                          G7_WARPS * 32, 0));
+    const int gs8 = (int)std::min<int64_t>(n, (int64_t)ctx->sm_count * std::max(per_sm, 1));
+    if (half)
+      k_gather8<6, 6><<<gs8, G7_WARPS * 32, 0, ctx->stream>>>(pts, orig, items, istart + nb4, g, T, u_fourier,
+                                                             u_total, u_real, ctx->d_flags);
+    else
+      k_gather8<3, 4><<<gs8, G7_WARPS * 32, 0, ctx->stream>>>(pts, orig, items, istart + nb4, g, T, u_fourier,
+                                                             u_total, u_real, ctx->d_flags);
+    HS_LAUNCHED(ctx);
+    return HS_OK;
+  }
   const int gs7 = (int)std::min<int64_t>(n, (int64_t)ctx->sm_count * 2);
   if (half)
     k_gather7<6, 6><<<gs7, G7_WARPS * 32, 0, ctx->stream>>>(pts, orig, items, istart + nb4, g, T, u_fourier,
