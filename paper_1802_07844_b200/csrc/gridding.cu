@@ -1,19 +1,17 @@
 // gridding.cu -- Gaussian spreading and gathering on the extended grid
 // (reference: _gridding.py:21-89, ewald_fourier.py:319-346,626-630).
 //
-// Spreading is owner-computes and atomic-free: one CTA owns a 16x16x8 tile of
-// grid nodes, each thread one (x,y) column of 8 z-nodes for every channel in
-// registers.  The CTA streams the sources whose P^3 support can reach the
-// tile (sources are bin-sorted by the tile of their window-centre cell, so
-// the candidates are 3x3 (x,y) runs of 5 z-bins), stages per-source window
-// slices restricted to the tile in shared memory, and every warp (a 4x8
-// (x,y) patch) skips sources whose support misses its patch (warp-uniform
-// branch).  Each grid value is written exactly once, deterministically,
-// without FP64 shared-memory atomics (a CAS loop on sm_100a).
+// Spreading (k_spread_wtab + k_spread_mma4) is owner-computes and atomic-free: one CTA owns a
+// 16x16x8 tile of grid nodes; producer warps stream the sources whose P^3 support can reach
+// the tile (bin-sorted by the tile of their window-centre cell: 3x3 (x,y) runs of 5 z-bins)
+// and stage their window slices (cp.async from per-source window rows) and weights into an
+// mbarrier ring; 16 consumer warps, one 4x4 (x,y) x 8 z patch each, accumulate with FP64
+// DMMA in registers.  Each grid value is written exactly once, deterministically, without
+// FP64 shared-memory atomics (a CAS loop on sm_100a).
 //
-// Gathering: one warp per target, lanes over the P z-nodes of one (x,y)
-// support column (coalesced 8*P-byte reads), loop over the P*P columns,
-// shuffle reduction over lanes.
+// Gathering: k_gather8 in the plan (runs of <= 8 targets of one 4x4 block, columns staged by
+// cp.async, the z contraction on the FP64 tensor pipe); k_gather (warp per target, lanes over
+// the z nodes of one support column) for the stand-alone API and window supports P > 29.
 #define HS_TU_ID 2  // checked build: source of a failing HS_CHECK
 #include <cmath>
 #include <cstdlib>
@@ -53,7 +51,7 @@ __global__ void k_grid_keys(const double* __restrict__ pos, int n_src, int n, in
     }
     if (bad) atomicOr(flags, FLAG_OUT_OF_GRID);
     if (fine) {
-      // gather (k_gather7): (4x4 (x,y) column, z node): 8 consecutive targets span a 4x4 footprint
+      // gather (k_gather8): (4x4 (x,y) column, z node): 8 consecutive targets span a 4x4 footprint
       // and ~5 z nodes (union ~(P+3)^2 columns x (P+5) nodes)
       const int n4y = (g.dims[1] + 3) / 4;
       keys[i] = ((cc[0] >> 2) * n4y + (cc[1] >> 2)) * g.dims[2] + cc[2];
@@ -596,17 +594,14 @@ hs_status launch_gather(hs_ctx* ctx, const double4* pts, const int* perm, int n,
 // ---------------------------------------------------------------------------
 // Fourier gather of the half-space pipeline (ewald_fourier.py:626-630):
 //   u_F(t) = h^3 [ sum_p w_t(p) T1(p) - x3_t sum_p w_t(p) T2(p) ]
-// Gather (k_gather7).  Targets are sorted by (4x4 (x,y) block, z node) of their window
+// Gather (k_gather8).  Targets are sorted by (4x4 (x,y) block, z node) of their window
 // centre and cut into RUNS of <= G7_TG targets of one block whose windows start within
-// 32 - P z nodes of each other, and ITEMS of <= G7_WARPS runs of one block
-// (k_g7_items).  A CTA takes an item, one warp per run; the warp's lanes are 32
-// consecutive z nodes.  The CTA walks the (x,y) columns of the item's union (a (P+3)^2
-// square), staging each column's z-range once through a cp.async ring; every lane takes
-// ITS node of the column (all channels) and accumulates, per target t and channel c,
-//   E_l[t][c] += wx_t(x) wy_t(y) G_c(x, y, z_l)
-// so each shared-memory value feeds G7_TG fused multiply-adds from registers (no
-// broadcast reads).  The z factor is applied once at the end, u_t,c = sum_l wz_t(z_l)
-// E_l[t][c] (warp reduction).  The x/y factors of a run live in warp-private tables.
+// 32 - P z nodes of each other, and ITEMS of <= G7_WARPS runs of one block whose windows start
+// within G7_ZC - P nodes (k_g7_count / k_g7_fill).  A CTA takes an item, one warp per run.
+// The CTA walks the (x,y) columns of the item's union (a (P+3)^2 square), staging each
+// column's z-range (<= G7_ZC nodes, all channels) once through a cp.async ring, G7_STEP columns
+// per barrier; each warp contracts the staged columns with its run's window factors on the
+// FP64 tensor pipe (see k_gather8).  The x/y factors of a run live in warp-private tables.
 // Windows are evaluated directly, exp(-alpha d^2), as in the reference (_gridding.py:21-30).
 #ifndef G7_STEP_DEF
 #define G7_STEP_DEF 4
@@ -667,216 +662,15 @@ __global__ void k_g7_fill(const double4* __restrict__ pts, const int* __restrict
     g7_cut(pts, bstart[c * nz], bstart[(c + 1) * nz], g, items + istart[c]);
 }
 
-template <int NCH, int PITCH>
-__global__ void __launch_bounds__(G7_WARPS * 32, 2) k_gather7(const double4* __restrict__ pts,
-                                                             const int* __restrict__ orig, const int4* __restrict__ items,
-                                                             const int* __restrict__ n_items_d, GridGeom g,
-                                                             const double* __restrict__ T,
-                                                             double* __restrict__ u_four, double* __restrict__ u_tot,
-                                                             const double* __restrict__ u_real,
-                                                             unsigned* __restrict__ flags) {
-  constexpr int TG = G7_TG, GW = G7_GW, NT = G7_WARPS * 32, CPN = PITCH / 2;  // 16-byte chunks per node
-  __shared__ double s_w[G7_WARPS][2][TG][GW];
-  __shared__ __align__(16) double s_ring[G7_R][G7_ZC * PITCH];
-  __shared__ int s_u[G7_WARPS][6];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int P = g.P;
-  double(*wx_tab)[GW] = s_w[warp][0];
-  double(*wy_tab)[GW] = s_w[warp][1];
-  const int n_items = *n_items_d;
-  for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
-    const int4 item = items[it];
-    int rb = item.x;
-#pragma unroll
-    for (int w = 0; w < G7_WARPS; ++w)
-      if (w < warp) rb += (item.z >> (8 * w)) & 0xff;
-    const int rlen = (item.z >> (8 * warp)) & 0xff;
-    const int t = rb + lane;
-    const bool valid = lane < rlen;
-    const double4 pt = pts[valid ? t : item.x];
-    const double pc[3] = {pt.x, pt.y, pt.z};
-    int lo[3];
-    bool bad = false;
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      const int64_t l = g_lo(g, k, pc[k]);
-      bad |= (l < 0) || (l + P > g.dims[k]);
-      lo[k] = (int)l;
-    }
-    if (valid && bad) atomicOr(flags, FLAG_OUT_OF_GRID);
-    const bool act = valid && !bad;
-    const unsigned amask = __ballot_sync(0xffffffffu, act);
-    int W0[3], W1[3];
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      W0[k] = (int)__reduce_min_sync(0xffffffffu, (unsigned)(act ? lo[k] : 0x7fffffff));
-      W1[k] = (int)__reduce_max_sync(0xffffffffu, (unsigned)(act ? lo[k] + P : 0));
-    }
-    __syncthreads();  // previous item done with s_u / ring / tables
-    if (lane == 0) {
-#pragma unroll
-      for (int k = 0; k < 3; ++k) {
-        s_u[warp][k] = amask ? W0[k] : 0x7fffffff;
-        s_u[warp][3 + k] = amask ? W1[k] : (int)0x80000000;
-      }
-    }
-    __syncthreads();
-    int C0[3] = {0x7fffffff, 0x7fffffff, 0x7fffffff}, C1[3] = {(int)0x80000000, (int)0x80000000, (int)0x80000000};
-#pragma unroll
-    for (int w = 0; w < G7_WARPS; ++w)
-#pragma unroll
-      for (int k = 0; k < 3; ++k) {
-        C0[k] = min(C0[k], s_u[w][k]);
-        C1[k] = max(C1[k], s_u[w][3 + k]);
-      }
-    // no active target in the item (all out of the grid): C0 = INT_MAX and C1 - C0 would wrap
-    if (C0[0] == 0x7fffffff) continue;
-    const int nxu = C1[0] - C0[0], nyu = C1[1] - C0[1], nzu = C1[2] - C0[2];
-    // limits exceeded (only with out-of-grid targets, an error anyway)
-    if (nxu <= 0 || nxu > GW || nyu > GW || nzu > G7_ZC) continue;
-    double res[NCH];
-#pragma unroll
-    for (int c = 0; c < NCH; ++c) res[c] = 0.0;
-    // x / y window tables of this warp's run (0 outside a target's support)
-#pragma unroll
-    for (int tt = 0; tt < TG; ++tt) {
-      const bool tin = (amask >> tt) & 1u;
-      const double px = __shfl_sync(0xffffffffu, pc[0], tt), py = __shfl_sync(0xffffffffu, pc[1], tt);
-      const int lx = __shfl_sync(0xffffffffu, lo[0], tt), ly = __shfl_sync(0xffffffffu, lo[1], tt);
-      double vx = 0.0, vy = 0.0;
-      const int x = C0[0] + lane, y = C0[1] + lane;
-      if (tin && lane < nxu && x >= lx && x < lx + P) {
-        const double d = g_d(g, 0, px, x);
-        vx = exp(-g.alpha * d * d);
-      }
-      if (tin && lane < nyu && y >= ly && y < ly + P) {
-        const double d = g_d(g, 1, py, y);
-        vy = exp(-g.alpha * d * d);
-      }
-      wx_tab[tt][lane] = vx;
-      wy_tab[tt][lane] = vy;
-    }
-    __syncwarp();
-    const int ncol = nxu * nyu, nchunk = nzu * CPN;
-    // cp.async issue state: this thread's 16-byte chunks k = tid + NT j of every column
-    const double* colp = T + (int64_t)C0[0] * g.stride[0] + (int64_t)C0[1] * g.stride[1] + (int64_t)C0[2] * PITCH +
-                         2 * threadIdx.x;
-    const int64_t row_wrap = g.stride[0] - (int64_t)nyu * g.stride[1];
-    int iy = 0, nissued = 0;
-    auto issue_step = [&](int step) {
-#pragma unroll
-      for (int j = 0; j < G7_STEP; ++j) {
-        if (nissued < ncol) {
-          double* dst = s_ring[(step * G7_STEP + j) % G7_R] + 2 * threadIdx.x;
-#pragma unroll
-          for (int q = 0; q < (G7_ZC * CPN + NT - 1) / NT; ++q)
-            if ((int)threadIdx.x + q * NT < nchunk) cp_async16(dst + 2 * q * NT, colp + 2 * q * NT);
-          ++nissued;
-          colp += g.stride[1];
-          if (++iy == nyu) {
-            iy = 0;
-            colp += row_wrap;
-          }
-        }
-      }
-      cp_async_commit();
-    };
-    issue_step(0);
-    issue_step(1);
-    const int zn = min(W0[2] - C0[2] + lane, nzu - 1);  // this lane's node in the staged column
-    HS_CHECK(zn >= 0 && zn < G7_ZC && C0[0] >= 0 && C0[1] >= 0 && C0[2] >= 0 && C1[0] <= g.dims[0] &&
-             C1[1] <= g.dims[1] && C1[2] <= g.dims[2] && nzu * CPN <= G7_ZC * CPN);
-    double E[TG][NCH];
-#pragma unroll
-    for (int tt = 0; tt < TG; ++tt)
-#pragma unroll
-      for (int c = 0; c < NCH; ++c) E[tt][c] = 0.0;
-    int cx = 0, cy = 0, slot = 0;
-    // one column: node values and window factors, then the FMAs
-    auto column = [&](int sl) {
-      HS_CHECK(sl >= 0 && sl < G7_R && cx < nxu && cy < nyu && cx < GW && cy < GW);
-      const double2* src = reinterpret_cast<const double2*>(&s_ring[sl][zn * PITCH]);
-      double v[PITCH], cxy[TG];
-#pragma unroll
-      for (int c = 0; c < CPN; ++c) {
-        const double2 q2 = src[c];
-        v[2 * c] = q2.x;
-        v[2 * c + 1] = q2.y;
-      }
-#pragma unroll
-      for (int tt = 0; tt < TG; ++tt) cxy[tt] = wx_tab[tt][cx] * wy_tab[tt][cy];
-      if (++cy == nyu) {
-        cy = 0;
-        ++cx;
-      }
-#pragma unroll
-      for (int tt = 0; tt < TG; ++tt)
-#pragma unroll
-        for (int c = 0; c < NCH; ++c) E[tt][c] = fma(cxy[tt], v[c], E[tt][c]);
-    };
-    const int nfull = ncol / G7_STEP, nrem = ncol - nfull * G7_STEP;
-    for (int sidx = 0; sidx < nfull; ++sidx) {
-      cp_async_wait<1>();
-      __syncthreads();
-      issue_step(sidx + 2);
-      if (amask) {
-#pragma unroll
-        for (int j = 0; j < G7_STEP; ++j) column(slot + j);
-      }
-      slot = slot + G7_STEP == G7_R ? 0 : slot + G7_STEP;
-    }
-    if (nrem) {  // ragged last step (already issued)
-      cp_async_wait<1>();
-      __syncthreads();
-      if (amask)
-        for (int j = 0; j < nrem; ++j) column(slot + j);
-    }
-    cp_async_wait<0>();
-    if (amask) {
-      // z factors of this lane's node, reduce over the warp; lane t accumulates target t
-      const int z = W0[2] + lane;
-#pragma unroll
-      for (int tt = 0; tt < TG; ++tt) {
-        const double pz = __shfl_sync(0xffffffffu, pc[2], tt);
-        const int lz = __shfl_sync(0xffffffffu, lo[2], tt);
-        double wz = 0.0;
-        if (((amask >> tt) & 1u) && z >= lz && z < lz + P) {
-          const double d = g_d(g, 2, pz, z);
-          wz = exp(-g.alpha * d * d);
-        }
-#pragma unroll
-        for (int c = 0; c < NCH; ++c) {
-          const double sum = warp_sum(wz * E[tt][c]);
-          if (lane == tt) res[c] = sum;
-        }
-      }
-    }
-    if (act) {
-      const int o = orig[t];
-      const double h3p = g.h * g.h * g.h * g.pref;
-#pragma unroll
-      for (int k = 0; k < 3; ++k) {
-        double v = res[k] * h3p;
-        if (NCH == 6) v -= pt.z * (res[3 + k] * h3p);
-        if (u_four) u_four[3 * (size_t)o + k] = v;
-        if (u_tot) u_tot[3 * (size_t)o + k] = (u_real ? u_real[3 * (size_t)o + k] : 0.0) + v;
-      }
-    }
-  }
-}
-
-// Gather on the FP64 tensor pipe (k_gather8, default; G7_MMA=0 selects k_gather7).  Same
-// items, runs, column staging ring and x / y window tables as k_gather7, but the per-column
-// contraction over z is a DMMA: for a run of <= 8 targets t and its 32-node z window,
+// Gather on the FP64 tensor pipe (k_gather8).  Items, runs, the column staging ring and the
+// x / y window tables as described above; the per-column contraction over z is a DMMA: for a run of <= 8 targets t and its 32-node z window,
 //   D[t][n] += A[t][k] B[k][n],   A[t][k] = wz_t(z0 + 4 s + k),   B[k][n] = G_c(col, z0 + 4 s + k)
 // with n = (column of the 4-column step, channel of a channel pair), 8 k-steps of 4 nodes; then
-// u_t,c += wx_t(col) wy_t(col) D[t][n].  One m8n8k4 DMMA does 256 FMAs where k_gather7 issued
-// 8 targets x 6 channels DFMAs per lane per column: ~5x fewer instructions per useful FMA, and
-// ~60 registers instead of 200.  (Fragments of mma.m8n8k4.f64: A[lane/4][lane%4],
+// u_t,c += wx_t(col) wy_t(col) D[t][n].  One m8n8k4 DMMA does 256 FMAs where the previous
+// DFMA form (lanes = z nodes, E[t][c] += wx wy G in registers) issued 8 targets x 6 channels
+// DFMAs per lane per column: ~5x fewer instructions per useful FMA, 93 registers instead of
+// 200, 16.5 -> 11.6-11.9 ms at HL (profiles/r02/experiments/bench_gather_*).  (Fragments of mma.m8n8k4.f64: A[lane/4][lane%4],
 // B[lane%4][lane/4], C/D[lane/4][2 (lane%4) + {0,1}].)
-#ifndef G7_MMA
-#define G7_MMA 1
-#endif
 
 template <int NCH, int PITCH>
 __global__ void __launch_bounds__(G7_WARPS * 32) k_gather8(const double4* __restrict__ pts,
@@ -1100,7 +894,7 @@ hs_status launch_gather_fourier(hs_ctx* ctx, const double4* pts, const int* orig
                                 const int* bstart) {
   if (n == 0) return HS_OK;
   if (g.P > 32) return fail(HS_ERR_PARAMETER, "window support P > 32 is not supported by the gather");
-  // k_gather7: an item's x / y window union is at most P + 3 nodes wide (targets of one 4x4
+  // k_gather8: an item's x / y window union is at most P + 3 nodes wide (targets of one 4x4
   // block), which must fit the GW = 32 lanes of its tables; wider supports (P = 30 .. 32) take
   // the warp-per-target gather
   if (g.P + 3 > G7_GW || g.P > G7_ZC) {
@@ -1130,26 +924,15 @@ hs_status launch_gather_fourier(hs_ctx* ctx, const double4* pts, const int* orig
   HS_TRY(exclusive_scan(ctx, cnt, nb4, istart, sc));
   k_g7_fill<<<gsb, 128, 0, ctx->stream>>>(pts, bstart, nb4, g.dims[2], g, istart, items);
   HS_LAUNCHED(ctx);
-  if (G7_MMA) {
-    int per_sm = 0;
-    HS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, half ? k_gather8<6, 6> : k_gather8<3, 4>,
-                                                          G7_WARPS * 32, 0));
-    const int gs8 = (int)std::min<int64_t>(n, (int64_t)ctx->sm_count * std::max(per_sm, 1));
-    if (half)
-      k_gather8<6, 6><<<gs8, G7_WARPS * 32, 0, ctx->stream>>>(pts, orig, items, istart + nb4, g, T, u_fourier,
-                                                             u_total, u_real, ctx->d_flags);
-    else
-      k_gather8<3, 4><<<gs8, G7_WARPS * 32, 0, ctx->stream>>>(pts, orig, items, istart + nb4, g, T, u_fourier,
-                                                             u_total, u_real, ctx->d_flags);
-    HS_LAUNCHED(ctx);
-    return HS_OK;
-  }
-  const int gs7 = (int)std::min<int64_t>(n, (int64_t)ctx->sm_count * 2);
+  int per_sm = 0;
+  HS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, half ? k_gather8<6, 6> : k_gather8<3, 4>,
+                                                        G7_WARPS * 32, 0));
+  const int gs8 = (int)std::min<int64_t>(n, (int64_t)ctx->sm_count * std::max(per_sm, 1));
   if (half)
-    k_gather7<6, 6><<<gs7, G7_WARPS * 32, 0, ctx->stream>>>(pts, orig, items, istart + nb4, g, T, u_fourier,
+    k_gather8<6, 6><<<gs8, G7_WARPS * 32, 0, ctx->stream>>>(pts, orig, items, istart + nb4, g, T, u_fourier,
                                                            u_total, u_real, ctx->d_flags);
   else
-    k_gather7<3, 4><<<gs7, G7_WARPS * 32, 0, ctx->stream>>>(pts, orig, items, istart + nb4, g, T, u_fourier,
+    k_gather8<3, 4><<<gs8, G7_WARPS * 32, 0, ctx->stream>>>(pts, orig, items, istart + nb4, g, T, u_fourier,
                                                            u_total, u_real, ctx->d_flags);
   HS_LAUNCHED(ctx);
   return HS_OK;

@@ -460,3 +460,17 @@ def test_mixed_plan_equals_sum_of_kinds(gpu, oracle, geom, sep):
     ua, _, _ = oracle.ewald_sum("stokeslet", geom, L, pos, p.xi, p.rc, p.M, p.P, tabs, f=f, targets=tg)
     ub, _, _ = oracle.ewald_sum("stresslet", geom, L, pos, p.xi, p.rc, p.M, p.P, tabs, g=g, q=q, targets=tg)
     assert rel_l2(r.velocities, ua + ub) < TOL
+
+
+@pytest.mark.parametrize("P", (28, 30, 32))
+def test_fourier_wide_window_support_vs_oracle(gpu, oracle, P):
+    """Window supports up to P = 32 (GridSpec accepts them): P <= 29 runs the tensor-pipe gather
+    (an item's x / y union, P + 3 nodes, fits its 32-wide tables), P = 30 .. 32 the warp-per-
+    target gather; both against the oracle (no silent skips)."""
+    s = gpu.generate_system(400, 1.0, "stokeslet", "half", seed=3)
+    g = gpu.GridSpec(L=1.0, M=36, P=P, xi=9.0, geometry="half")
+    r = gpu.fourier_space_sum(s, g)
+    go = oracle.Grid(1.0, g.M, P, 9.0)
+    tabs = {k: oracle.precompute_greens(k, go) for k in ("biharmonic", "harmonic")}
+    u, _ = oracle.fourier_space_sum("stokeslet", "half", s.positions, go, tabs, f=s.f)
+    assert rel_l2(r.velocities, u) < TOL
