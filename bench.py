@@ -324,7 +324,8 @@ def run_ours(args, rank, world, local_rank):
         # mirrored spreading (csrc/plan.cu k_mirror_z): kernel + wall channels at the N sources,
         # images by reflection of the grid (stokeslet: 10 N P^3 -> 7 N P^3 FMAs)
         "k_spread": ("flop", 2.0 * P3 * n_in * s.n, "fp64:dmma"),
-        "k_gather": ("flop", 2.0 * P3 * n_out * nt, "fp64:dfma"),
+        # k_gather8: the z contraction on the FP64 tensor pipe (DMMA)
+        "k_gather": ("flop", 2.0 * P3 * n_out * nt, "fp64:dmma"),
         "k_scale": ("bytes", n_half * (16 * n_in + 16 * n_out + 8 * 2), "hbm"),
         "k_pair": ("flop", 2.0 * (pi * pairs + pc * img_pairs), "fp64:dfma"),
     }
