@@ -240,6 +240,29 @@ __device__ __forceinline__ void eval_pair(const PairConst& pc, double d0, double
   apply_pair<KIND>(pc, pair_coef<SCREENED>(pc, r2, etab), d0, d1, d2, r2, x2, S, A, B, image, k, c);
 }
 
+// FP32 prefilter distance^2 with a fixed operation order
+__device__ __forceinline__ float dist2f(float tx, float ty, float tz, const float4& F) {
+  const float dx = tx - F.x, dy = ty - F.y, dz = tz - F.z;
+  return __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, __fmul_rn(dx, dx)));
+}
+
+__device__ __forceinline__ float4 lds_f4(unsigned addr) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
+  return v;
+}
+
+__device__ __forceinline__ void sts_u16(unsigned addr, int v) {
+  asm volatile("st.shared.u16 [%0], %1;" ::"r"(addr), "h"((unsigned short)v) : "memory");
+}
+
+// index of the highest set bit (x != 0)
+__device__ __forceinline__ int bfind_u32(unsigned x) {
+  int r;
+  asm("bfind.u32 %0, %1;" : "=r"(r) : "r"(x));
+  return r;
+}
+
 __device__ __forceinline__ double exact_r2(double d0, double d1, double d2) {
   // numba: r2 = d0 * d0 + d1 * d1 + d2 * d2, each op rounded, left to right
   return __dadd_rn(__dadd_rn(__dmul_rn(d0, d0), __dmul_rn(d1, d1)), __dmul_rn(d2, d2));
@@ -397,7 +420,9 @@ __global__ void __launch_bounds__(PC_TG, pc_minb<KIND>()) k_pair_q(const PairArg
     unsigned long long a_hash = 0;
     // FP32 view relative to the item's first target, and this warp's target bounding box
     const double4 R0 = a.TP[t0];
-    const float tfx = (float)(T.x - R0.x), tfy = (float)(T.y - R0.y), tfz = (float)(T.z - R0.z);
+    // (a lane without a target tests a point 1e30 away: it never accepts nor meets the shell)
+    const float tfx = tvalid ? (float)(T.x - R0.x) : 1.0e30f, tfy = tvalid ? (float)(T.y - R0.y) : 1.0e30f,
+                tfz = tvalid ? (float)(T.z - R0.z) : 1.0e30f;
     float bmin[3] = {tfx, tfy, tfz}, bmax[3] = {tfx, tfy, tfz};
     if (!tvalid) {
       bmin[0] = bmin[1] = bmin[2] = 3.0e38f;
@@ -577,42 +602,51 @@ __global__ void __launch_bounds__(PC_TG, pc_minb<KIND>()) k_pair_q(const PairArg
           }
           near = __ballot_sync(0xffffffffu, keep);
         }
-        // FP32 distance inside r_c by a margin far above its rounding error: the exact
-        // reference test would accept too; in the shell around r_c run the exact test
-        // (bit-identical neighbour sets) -- warp-uniformly skipped when no lane is in the shell.
-        // The slot at `tail` is free (tail - head < PC_Q), so every tested candidate is written
-        // there and `tail` advances only on accept.  Two candidates per iteration.
-        const float4* sFg = sF + hb + j0;
-        auto exact_ok = [&](int j, const float4& F, bool& ok) {
-          const double2 xy = sXY[j];
-          const double sz = sZA[j].x;
-          const double d0 = __dsub_rn(T.x, xy.x), d1 = __dsub_rn(T.y, xy.y), d2 = __dsub_rn(T.z, sz);
-          const double r2 = exact_r2(d0, d1, d2);
-          singular |= __float_as_int(F.w) != tcol_i && tvalid && r2 == 0.0;
-          ok = r2 <= a.rc2 && r2 != 0.0 && abs(a.cell_z(sz) - tcz) <= 2;
-        };
-        while (near) {
-          const int ia = __ffs(near) - 1;
-          near &= near - 1;
-          const bool two = near != 0;
-          const int ib = two ? __ffs(near) - 1 : ia;
-          near &= near - 1;
-          const float4 Fa = sFg[ia], Fb = sFg[ib];  // broadcast
-          const float ax = tfx - Fa.x, ay = tfy - Fa.y, az = tfz - Fa.z;
-          const float bx = tfx - Fb.x, by = tfy - Fb.y, bz = tfz - Fb.z;
-          const float ra = ax * ax + ay * ay + az * az, rb = bx * bx + by * by + bz * bz;
-          bool oka = ra > 0.0f && ra <= a.rc2_lo, okb = two && rb > 0.0f && rb <= a.rc2_lo;
-          const bool sha = !oka && ra <= a.rc2_hi, shb = two && !okb && rb <= a.rc2_hi;
-          if (__any_sync(0xffffffffu, sha || shb)) {
-            if (sha) exact_ok(hb + j0 + ia, Fa, oka);
-            if (shb) exact_ok(hb + j0 + ib, Fb, okb);
-          }
-          oka = oka && __float_as_int(Fa.w) != tcol_i && tvalid;
-          okb = okb && __float_as_int(Fb.w) != tcol_i && tvalid;
-          q[tail & (PC_Q - 1)][lane] = (unsigned short)(hb + j0 + ia);
+        // FP32 distance inside r_c by a margin far above its rounding error (sure accept: the
+        // exact reference test accepts too) -> pushed at once; the shell around r_c and FP32
+        // distance 0 (the target itself, coincident sources) are collected as bits and decided
+        // by the exact test after the group -- bit-identical neighbour sets.  The slot at `tail`
+        // is free (tail - head < PC_Q), so every tested candidate is written there and `tail`
+        // advances only on accept.  Two near candidates per iteration, highest bits first
+        // (bfind gives the index; the bit doubles as the shell-mask bit).
+        const unsigned sFg_s = (unsigned)__cvta_generic_to_shared(sF + hb + j0);
+        const unsigned q_s = (unsigned)__cvta_generic_to_shared(&q[0][lane]);  // this lane's slot 0
+        const int qb = hb + j0;
+        unsigned msh = 0;
+        while (near) {  // warp-uniform (lanes without a target test far-away coordinates)
+          const int ia = bfind_u32(near);
+          const unsigned ba = 1u << ia;
+          const unsigned rest = near ^ ba;
+          const bool two = rest != 0;
+          const int ib = two ? bfind_u32(rest) : ia;
+          const unsigned bb = two ? 1u << ib : 0u;
+          near = rest ^ bb;
+          const float4 Fa = lds_f4(sFg_s + (ia << 4)), Fb = lds_f4(sFg_s + (ib << 4));  // broadcast
+          const float ra = dist2f(tfx, tfy, tfz, Fa), rb = dist2f(tfx, tfy, tfz, Fb);
+          const bool oka = ra > 0.0f && ra <= a.rc2_lo;
+          const bool okb = two && rb > 0.0f && rb <= a.rc2_lo;
+          msh |= (!oka && ra <= a.rc2_hi ? ba : 0u) | (!okb && rb <= a.rc2_hi ? bb : 0u);
+          sts_u16(q_s + (((unsigned)tail & (PC_Q - 1)) << 6), qb + ia);
           tail += oka ? 1 : 0;
-          q[tail & (PC_Q - 1)][lane] = (unsigned short)(hb + j0 + ib);
+          sts_u16(q_s + (((unsigned)tail & (PC_Q - 1)) << 6), qb + ib);
           tail += okb ? 1 : 0;
+        }
+        if (__any_sync(0xffffffffu, msh != 0)) {
+          while (msh) {
+            const int ib = bfind_u32(msh);
+            msh ^= 1u << ib;
+            const int j = qb + ib;
+            const double2 xy = sXY[j];
+            const double sz = sZA[j].x;
+            const double d0 = __dsub_rn(T.x, xy.x), d1 = __dsub_rn(T.y, xy.y), d2 = __dsub_rn(T.z, sz);
+            const double r2 = exact_r2(d0, d1, d2);
+            const bool other = __float_as_int(sF[j].w) != tcol_i;
+            singular |= other && r2 == 0.0;
+            const bool ok = other && r2 <= a.rc2 && r2 != 0.0 && abs(a.cell_z(sz) - tcz) <= 2;
+            q[tail & (PC_Q - 1)][lane] = (unsigned short)j;
+            tail += ok ? 1 : 0;
+            // (a lane's backlog after a group stays < PC_Q: <= PC_Q - 32 before it, <= 32 pushes)
+          }
         }
         // full rounds while every valid lane has work; partial rounds only against overflow
         unsigned mn = __reduce_min_sync(0xffffffffu, (unsigned)(tvalid ? tail - head : 0x7fffffff));
