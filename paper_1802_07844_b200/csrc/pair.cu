@@ -58,15 +58,25 @@ __device__ __forceinline__ double erfc_from_E(double xw, double E, const double2
 // [0, 8] (tools/gen_erfcx_poly.py, max rel. error 6.9e-15; the reference's own Hermite table
 // is ~2e-13, ewald_real.py:33-58), coefficients as constant-bank DFMA operands.  Trades the
 // table's six lane-divergent 16-byte shared-memory loads per pair (the pair kernel's
-// shared-memory pipe is its co-bottleneck) for ~12 more DFMAs.  x > 8 (xi r_c > 8 only):
-// evaluated at 8, where erfc < 1.2e-29, below the resolution of any sum it enters.
+// shared-memory pipe is its co-bottleneck) for ~12 more DFMAs.
 #include "erfcx_poly.inc"
 // Newton steps after the hardware rsqrt / rcp approximations (~2^-23): 1 step leaves ~2^-46
 // relative error (erfc ~1e-14, far below the 2e-13 of the reference's own erfc table), 2 steps
 // round-off level
 #ifndef PC_NEWTON
-#define PC_NEWTON 2
+#define PC_NEWTON 3
 #endif
+// PC_NEWTON = 3 (default): ONE third-order step, y (1 + e + e^2) for 1/v and y (1 + e/2 + 3e^2/8)
+// for 1/sqrt(v) (e the residual of the ~2^-22 hardware value): error ~e^3, i.e. round-off
+// level like two Newton steps, in 3 / 5 instead of 4 / 8 FP64 operations
+#if PC_NEWTON == 3
+__device__ __forceinline__ double rcp_pos(double v) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(v));
+  const double e = fma(-v, y, 1.0);
+  return fma(y, fma(e, e, e), y);
+}
+#else
 __device__ __forceinline__ double rcp_pos(double v) {
   double y;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(v));
@@ -74,13 +84,16 @@ __device__ __forceinline__ double rcp_pos(double v) {
   for (int it = 0; it < PC_NEWTON; ++it) y = fma(y, fma(-v, y, 1.0), y);
   return y;
 }
+#endif
 #ifndef PC_DRAIN2
 #define PC_DRAIN2 1   // queue drains by two-pair rounds where lanes have >= 2 entries
 #endif
 // (Estrin's scheme for the erfcx / exp polynomials -- dependency depth ~log2(deg) instead of
 // deg -- measured 83 vs 38 ms for the HL pair kernel: Horner with constant-bank operands stays.)
+// x > HS_EP_XMAX (xi r_c > 8 only) is not clamped: s stays in (1, HS_EP_S0], where the polynomial
+// is bounded by 0.22, so E p < 4e-29 -- below the resolution of any sum it enters
 __device__ __forceinline__ double erfc_poly_from_E(double x, double E) {
-  const double s = fma(HS_EP_S1, rcp_pos(fmin(x, HS_EP_XMAX) + HS_EP_K), HS_EP_S0);
+  const double s = fma(HS_EP_S1, rcp_pos(x + HS_EP_K), HS_EP_S0);
   double p = c_erfcx_poly[0];
 #pragma unroll
   for (int j = 1; j <= HS_EP_DEG; ++j) p = fma(p, s, c_erfcx_poly[j]);
@@ -113,10 +126,15 @@ __device__ __forceinline__ double exp_nonpos(double x) {
   return p * __hiloint2double(max(ni + 1023, 0) << 20, 0);
 }
 
-// 1/sqrt(r2) for normal r2 > 0, branch-free: hardware approximation + two Newton steps
+// 1/sqrt(r2) for normal r2 > 0, branch-free: hardware approximation + refinement
 __device__ __forceinline__ double rsqrt_pos(double r2) {
   double y;
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(r2));
+#if PC_NEWTON == 3
+  const double h = r2 * y;
+  const double e = fma(-h, y, 1.0);
+  return fma(y * e, fma(e, 0.375, 0.5), y);
+#else
 #pragma unroll
   for (int it = 0; it < PC_NEWTON; ++it) {  // ~2^-23 -> 2^-46 -> rounding level
     const double h = r2 * y;
@@ -124,6 +142,7 @@ __device__ __forceinline__ double rsqrt_pos(double r2) {
     y = fma(0.5 * y, e, y);
   }
   return y;
+#endif
 }
 
 constexpr int PT_MAXRUN = 25;  // 5 x 5 (x, y) cell columns
@@ -446,7 +465,7 @@ __global__ void __launch_bounds__(PC_TG, pc_minb<KIND>()) k_pair_q(const PairArg
       const double2 xy = sXY[jj], za = sZA[jj], aa = sAA[jj];
       S = make_double4(xy.x, xy.y, za.x, 0.0);
       A = make_double4(za.y, aa.x, aa.y, 0.0);
-      img = HALF && __double_as_longlong(za.x) < 0;
+      img = HALF && __double2hiint(za.x) < 0;
       B = make_double4(0, 0, 0, 0);
       if (kMixed) {
         const double2 g0 = sG0[jj], g1 = sG1[jj];
