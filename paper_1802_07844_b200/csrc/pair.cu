@@ -91,8 +91,18 @@ __device__ __forceinline__ double rcp_pos(double v) {
 // (Estrin's scheme for the erfcx / exp polynomials -- dependency depth ~log2(deg) instead of
 // deg -- measured 83 vs 38 ms for the HL pair kernel: Horner with constant-bank operands stays.)
 // x > HS_EP_XMAX (xi r_c > 8 only) is not clamped: s stays in (1, HS_EP_S0], where the polynomial
-// is bounded by 0.22, so E p < 4e-29 -- below the resolution of any sum it enters
+// is bounded by 0.07, so E p < 1e-29 -- below the resolution of any sum it enters.
+// EP6: the degree-15 polynomial on [0, 6] (3 DFMAs fewer; max rel. error 5.8e-15), used when
+// xi r_c <= 6, i.e. every accepted pair has x <= 6
+template <bool EP6 = false>
 __device__ __forceinline__ double erfc_poly_from_E(double x, double E) {
+  if (EP6) {
+    const double s = fma(HS_EP6_S1, rcp_pos(x + HS_EP6_K), HS_EP6_S0);
+    double p = c_erfcx_poly6[0];
+#pragma unroll
+    for (int j = 1; j <= HS_EP6_DEG; ++j) p = fma(p, s, c_erfcx_poly6[j]);
+    return E * p;
+  }
   const double s = fma(HS_EP_S1, rcp_pos(x + HS_EP_K), HS_EP_S0);
   double p = c_erfcx_poly[0];
 #pragma unroll
@@ -156,7 +166,7 @@ struct PairConst {
 struct PairCoef {
   double ri, ri2, c0, c1, e;
 };
-template <bool SCREENED>
+template <bool SCREENED, bool EP6 = false>
 __device__ __forceinline__ PairCoef pair_coef(const PairConst& pc, double r2, const double2* __restrict__ etab) {
   PairCoef q;
   double C = 1.0;
@@ -165,7 +175,7 @@ __device__ __forceinline__ PairCoef pair_coef(const PairConst& pc, double r2, co
     q.ri = rsqrt_pos(r2);
     const double rn = r2 * q.ri;
     const double E = exp_nonpos(-pc.xi2 * r2);
-    C = HS_ERFC_TABLE ? erfc_from_E(pc.xiw * rn, E, etab) : erfc_poly_from_E(pc.xi * rn, E);
+    C = HS_ERFC_TABLE ? erfc_from_E(pc.xiw * rn, E, etab) : erfc_poly_from_E<EP6>(pc.xi * rn, E);
     q.e = pc.c2xs * E;
   } else {
     q.ri = rsqrt(r2);
@@ -361,7 +371,7 @@ __device__ __forceinline__ unsigned long long splitmix64(unsigned long long x) {
 
 // AUDIT: the same kernel also records every target's accepted neighbour set (count, image
 // count, id hash) -- a separate instantiation so the production launch carries no extra work.
-template <int KIND, bool HALF, bool AUDIT>
+template <int KIND, bool HALF, bool AUDIT, bool EP6>
 __global__ void __launch_bounds__(PC_TG, pc_minb<KIND>()) k_pair_q(const PairArgs a) {
   // Candidate rows as 16-byte columns: the evaluation reads them at lane-random rows, and a
   // 16-byte array spreads those reads over 8 bank groups (a 32-byte row only over 4).
@@ -499,7 +509,7 @@ __global__ void __launch_bounds__(PC_TG, pc_minb<KIND>()) k_pair_q(const PairArg
       const double rr = fma(e0, e0, fma(e1, e1, e2 * e2));  // (neighbour test done exactly in the scan)
       if (img) ++n_img;
       if (AUDIT) a_hash += splitmix64((unsigned long long)__float_as_int(sF[jj].w));
-      apply_kind(pair_coef<true>(pc, rr, s_erfcx), jj, e0, e1, e2, rr, S, A, B, img);
+      apply_kind(pair_coef<true, EP6>(pc, rr, s_erfcx), jj, e0, e1, e2, rr, S, A, B, img);
     };
 
     // Two-half ring of staged candidates + per-lane FIFO queues: entries of chunk c may be
@@ -547,8 +557,8 @@ __global__ void __launch_bounds__(PC_TG, pc_minb<KIND>()) k_pair_q(const PairArg
       const double f0 = T.x - S1.x, f1 = T.y - S1.y, f2 = T.z - S1.z;
       const double g0 = T.x - S2.x, g1 = T.y - S2.y, g2 = T.z - S2.z;
       const double r1 = fma(f0, f0, fma(f1, f1, f2 * f2)), r2 = fma(g0, g0, fma(g1, g1, g2 * g2));
-      const PairCoef q1 = pair_coef<true>(pc, r1, s_erfcx);
-      const PairCoef q2 = pair_coef<true>(pc, r2, s_erfcx);
+      const PairCoef q1 = pair_coef<true, EP6>(pc, r1, s_erfcx);
+      const PairCoef q2 = pair_coef<true, EP6>(pc, r2, s_erfcx);
       n_img += (unsigned)i1 + (unsigned)i2;
       if (AUDIT)
         a_hash += splitmix64((unsigned long long)__float_as_int(sF[j1].w)) +
@@ -789,18 +799,22 @@ hs_status launch_pair(hs_ctx* ctx, const PairArgs& a) {
   // (capping it at 2 / 3 / 4 CTAs per SM, to leave register file for the concurrently issued
   // Fourier kernels, measured 103 / 94.5 / 90.4 ms per HL step vs 89.3 ms: not useful)
   const int grid = std::max(1, std::min(a.max_items, ctx->sm_count * 16));
-#define HS_PAIR_CASE1(K, H, AU)                                                                         \
-  do {                                                                                                  \
-    const int dyn = pc_nh<K>() * pc_h<K>() * pc_rec_bytes<K, H>();                                      \
-    HS_CUDA(cudaFuncSetAttribute(k_pair_q<K, H, AU>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn)); \
-    k_pair_q<K, H, AU><<<grid, PC_TG, dyn, ctx->stream>>>(a);                                            \
+  // every accepted pair has x = xi r <= xi r_c: the short erfcx polynomial covers it when <= 6
+  const bool ep6 = !HS_ERFC_TABLE && a.xi * std::sqrt(a.rc2) <= HS_EP6_XMAX * (1.0 - 1e-12);
+#define HS_PAIR_CASE1(K, H, AU, E6)                                                                         \
+  do {                                                                                                      \
+    const int dyn = pc_nh<K>() * pc_h<K>() * pc_rec_bytes<K, H>();                                          \
+    HS_CUDA(cudaFuncSetAttribute(k_pair_q<K, H, AU, E6>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn)); \
+    k_pair_q<K, H, AU, E6><<<grid, PC_TG, dyn, ctx->stream>>>(a);                                            \
   } while (0)
-#define HS_PAIR_CASE(K, H)            \
-  do {                                \
-    if (a.audit)                      \
-      HS_PAIR_CASE1(K, H, true);      \
-    else                              \
-      HS_PAIR_CASE1(K, H, false);     \
+#define HS_PAIR_CASE(K, H)                    \
+  do {                                        \
+    if (a.audit)                              \
+      HS_PAIR_CASE1(K, H, true, false);       \
+    else if (ep6)                             \
+      HS_PAIR_CASE1(K, H, false, true);       \
+    else                                      \
+      HS_PAIR_CASE1(K, H, false, false);      \
   } while (0)
   if (is_half) {
     if (kind == HS_STOKESLET) HS_PAIR_CASE(HS_STOKESLET, true);
