@@ -185,6 +185,7 @@ constexpr int SW_CH = SW_CH_DEF, SW_K = SW_K_DEF, SW_H = SW_CH_DEF / 32, SW_RX =
 #endif
 constexpr int SW_NP = SW_NP_DEF, SW_THREADS = (8 + SW_NP) * 32;
 static_assert(SW_K % SW_NP == 0, "ring slots must divide among the producers");
+constexpr int SW_IDQ = 64;  // consumer id FIFO capacity (>= 3 leftovers + SW_CH hits, power of two)
 template <int NCH>
 struct SwBuf {
   static constexpr int RQ = NCH | 1;
@@ -213,6 +214,7 @@ __global__ void __launch_bounds__((NCW + SW_NP) * 32, NCW == 8 ? 2 : 1) k_spread
   __shared__ __align__(8) uint64_t full_bar[K], empty_bar[K];
   __shared__ int run_beg[9], run_pre[10];
   __shared__ int s_nrun;
+  __shared__ unsigned short s_ids[NCW][SW_IDQ];  // per-warp FIFO of hit ids (consumers)
   auto bx_ = [&](int b) { return reinterpret_cast<double(*)[RX]>(sm_dyn + b * PER); };
   auto by_ = [&](int b) { return reinterpret_cast<double(*)[RY]>(sm_dyn + b * PER + SW_CH * RX); };
   auto bz_ = [&](int b) { return reinterpret_cast<double(*)[RZ]>(sm_dyn + b * PER + SW_CH * (RX + RY)); };
@@ -371,57 +373,75 @@ __global__ void __launch_bounds__((NCW + SW_NP) * 32, NCW == 8 ? 2 : 1) k_spread
   for (int rb = 0; rb < RB; ++rb)
 #pragma unroll
     for (int c = 0; c < NCH; ++c) acc[rb][c][0] = acc[rb][c][1] = 0.0;
+  // K-slot carry: the m8n8k4 contraction takes 4 sources, and the sources a warp patch meets in
+  // one chunk rarely come in multiples of 4.  Every chunk's hits are appended (one ballot, one
+  // store per hit lane) to a per-warp FIFO of ring ids (buffer * SW_CH + slot); groups of 4 are
+  // taken from its head, so the < 4 leftover ids of a chunk head the first group of the next one
+  // (their buffer is released one chunk later) and every group but a tile's last is full --
+  // ~15 % fewer DMMAs than a zero-padded group per chunk end, and no serial bit-extraction
+  // chain per group.
+  unsigned short* ids = s_ids[warp];
+  int head = 0, tail = 0;  // warp-uniform
+  const unsigned lanes_lt = (1u << lane) - 1u;
+  auto fire = [&](int gid) {
+    double bz = 0.0, q[NCH], cxy[RB];
+#pragma unroll
+    for (int ch = 0; ch < NCH; ++ch) q[ch] = 0.0;
+#pragma unroll
+    for (int rb = 0; rb < RB; ++rb) cxy[rb] = 0.0;
+    if (gid >= 0) {
+      const int gb = gid / SW_CH, sk = gid % SW_CH;
+      const unsigned par = bm_(gb)[sk];
+      const int pxo = (par >> PB) & 1, pyo = (par >> (PB + 1)) & 1, pzo = (par >> (PB + 2)) & 1;
+      HS_CHECK(gb < K && pzo + rq < RZ && pxo + wx0 + 3 < RX && pyo + wy0 + PY - 1 < RY);
+      bz = bz_(gb)[sk][pzo + rq];  // B[k][n] = wz_{s_k}(z_n), n = rq
+#pragma unroll
+      for (int ch = 0; ch < NCH; ++ch) q[ch] = bq_(gb)[sk][ch];
+#pragma unroll
+      for (int rb = 0; rb < RB; ++rb) {
+        const int p = rb * 8 + rq;  // position of A row rq in row block rb
+        cxy[rb] = bx_(gb)[sk][pxo + wx0 + (p & 3)] * by_(gb)[sk][pyo + wy0 + (p >> 2)];
+      }
+    }
+    // the weight goes into the B operand (wz q_c, one product per channel) so A = wx wy is
+    // shared by the channels
+    double bq[NCH];
+#pragma unroll
+    for (int ch = 0; ch < NCH; ++ch) bq[ch] = bz * q[ch];
+#pragma unroll
+    for (int rb = 0; rb < RB; ++rb)
+#pragma unroll
+      for (int ch = 0; ch < NCH; ++ch) dmma_884(acc[rb][ch][0], acc[rb][ch][1], cxy[rb], bq[ch]);
+  };
+  static_assert(SW_CH == 32, "one ballot per chunk");
   for (int c = 0; c < nchunk; ++c) {
     const int b = c % K;
     const int nc = min(SW_CH, ncand - c * SW_CH);
     mbar_wait(&full_bar[b], (c / K) & 1);
-    double(*s_wx)[RX] = bx_(b);
-    double(*s_wy)[RY] = by_(b);
-    double(*s_wz)[RZ] = bz_(b);
-    double(*s_q)[RQ] = bq_(b);
-    const unsigned* s_mask = bm_(b);
-    for (int base = 0; base < nc; base += 32) {
-      const unsigned mk = base + lane < nc ? s_mask[base + lane] : 0u;
-      unsigned m = __ballot_sync(0xffffffffu, (mk >> warp) & 1u);
-      while (m) {
-        int sk = -1;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const int sb = m ? base + __ffs(m) - 1 : -1;
-          if (m) m &= m - 1;
-          if (k == kq) sk = sb;
-        }
-        double bz = 0.0, q[NCH], cxy[RB];
-#pragma unroll
-        for (int ch = 0; ch < NCH; ++ch) q[ch] = 0.0;
-#pragma unroll
-        for (int rb = 0; rb < RB; ++rb) cxy[rb] = 0.0;
-        if (sk >= 0) {
-          const unsigned par = s_mask[sk];
-          const int pxo = (par >> PB) & 1, pyo = (par >> (PB + 1)) & 1, pzo = (par >> (PB + 2)) & 1;
-          HS_CHECK(sk < SW_CH && pzo + rq < RZ && pxo + wx0 + 3 < RX && pyo + wy0 + PY - 1 < RY);
-          bz = s_wz[sk][pzo + rq];  // B[k][n] = wz_{s_k}(z_n), n = rq
-#pragma unroll
-          for (int ch = 0; ch < NCH; ++ch) q[ch] = s_q[sk][ch];
-#pragma unroll
-          for (int rb = 0; rb < RB; ++rb) {
-            const int p = rb * 8 + rq;  // position of A row rq in row block rb
-            cxy[rb] = s_wx[sk][pxo + wx0 + (p & 3)] * s_wy[sk][pyo + wy0 + (p >> 2)];
-          }
-        }
-        // the weight goes into the B operand (wz q_c, one product per channel) so A = wx wy is
-        // shared by the channels
-        double bq[NCH];
-#pragma unroll
-        for (int ch = 0; ch < NCH; ++ch) bq[ch] = bz * q[ch];
-#pragma unroll
-        for (int rb = 0; rb < RB; ++rb)
-#pragma unroll
-          for (int ch = 0; ch < NCH; ++ch) dmma_884(acc[rb][ch][0], acc[rb][ch][1], cxy[rb], bq[ch]);
-      }
+    const unsigned mk = lane < nc ? bm_(b)[lane] : 0u;
+    const bool hit = (mk >> warp) & 1u;
+    const unsigned m = __ballot_sync(0xffffffffu, hit);
+    const bool had_left = tail > head;  // ids of chunk c - 1
+    if (hit) ids[(tail + __popc(m & lanes_lt)) & (SW_IDQ - 1)] = (unsigned short)(b * SW_CH + lane);
+    tail += __popc(m);
+    __syncwarp();
+    HS_CHECK(tail - head <= 3 + SW_CH);
+    if (had_left && tail - head < 4) {
+      // too few hits to complete the group: fire it partly filled, so that a leftover never
+      // outlives the chunk after its own
+      const int gid = head + kq < tail ? ids[(head + kq) & (SW_IDQ - 1)] : -1;
+      head = tail;
+      fire(gid);
     }
-    mbar_arrive(&empty_bar[b]);
+    while (tail - head >= 4) {
+      const int gid = ids[(head + kq) & (SW_IDQ - 1)];
+      head += 4;
+      fire(gid);
+    }
+    if (c > 0) mbar_arrive(&empty_bar[(c - 1) % K]);  // the previous chunk's leftovers are consumed
   }
+  if (tail > head) fire(head + kq < tail ? ids[(head + kq) & (SW_IDQ - 1)] : -1);
+  if (nchunk > 0) mbar_arrive(&empty_bar[(nchunk - 1) % K]);
   // C fragment: row rq of row block rb = position p, columns z = 2 kq, 2 kq + 1
 #pragma unroll
   for (int rb = 0; rb < RB; ++rb) {
