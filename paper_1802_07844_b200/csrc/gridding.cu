@@ -185,6 +185,9 @@ constexpr int SW_CH = SW_CH_DEF, SW_K = SW_K_DEF, SW_H = SW_CH_DEF / 32, SW_RX =
 #endif
 constexpr int SW_NP = SW_NP_DEF, SW_THREADS = (8 + SW_NP) * 32;
 static_assert(SW_K % SW_NP == 0, "ring slots must divide among the producers");
+#ifndef SW_PREFETCH
+#define SW_PREFETCH 0  // 1: load group g + 1's operands before group g's DMMAs (spills at the 96-register cap: 18.3 vs 14.4 ms)
+#endif
 constexpr int SW_IDQ = 64;  // consumer id FIFO capacity (>= 3 leftovers + SW_CH hits, power of two)
 template <int NCH>
 struct SwBuf {
@@ -383,16 +386,21 @@ __global__ void __launch_bounds__((NCW + SW_NP) * 32, NCW == 8 ? 2 : 1) k_spread
   unsigned short* ids = s_ids[warp];
   int head = 0, tail = 0;  // warp-uniform
   const unsigned lanes_lt = (1u << lane) - 1u;
-  auto fire = [&](int gid) {
-    double bz = 0.0, q[NCH], cxy[RB];
+  // fragments of one group for this lane: A = wx wy at its row's position (per row block), B = wz q_c
+  struct Ops {
+    double cxy[RB], bq[NCH];
+  };
+  // id = ring id | slice parities << 9 (appended by the hit lane, so no mask re-read here)
+  auto load_ops = [&](int gid) {
+    Ops o;
+    double bz = 0.0, q[NCH];
 #pragma unroll
     for (int ch = 0; ch < NCH; ++ch) q[ch] = 0.0;
 #pragma unroll
-    for (int rb = 0; rb < RB; ++rb) cxy[rb] = 0.0;
+    for (int rb = 0; rb < RB; ++rb) o.cxy[rb] = 0.0;
     if (gid >= 0) {
-      const int gb = gid / SW_CH, sk = gid % SW_CH;
-      const unsigned par = bm_(gb)[sk];
-      const int pxo = (par >> PB) & 1, pyo = (par >> (PB + 1)) & 1, pzo = (par >> (PB + 2)) & 1;
+      const int gb = (gid >> 5) & 15, sk = gid & 31;
+      const int pxo = (gid >> 9) & 1, pyo = (gid >> 10) & 1, pzo = (gid >> 11) & 1;
       HS_CHECK(gb < K && pzo + rq < RZ && pxo + wx0 + 3 < RX && pyo + wy0 + PY - 1 < RY);
       bz = bz_(gb)[sk][pzo + rq];  // B[k][n] = wz_{s_k}(z_n), n = rq
 #pragma unroll
@@ -400,20 +408,22 @@ __global__ void __launch_bounds__((NCW + SW_NP) * 32, NCW == 8 ? 2 : 1) k_spread
 #pragma unroll
       for (int rb = 0; rb < RB; ++rb) {
         const int p = rb * 8 + rq;  // position of A row rq in row block rb
-        cxy[rb] = bx_(gb)[sk][pxo + wx0 + (p & 3)] * by_(gb)[sk][pyo + wy0 + (p >> 2)];
+        o.cxy[rb] = bx_(gb)[sk][pxo + wx0 + (p & 3)] * by_(gb)[sk][pyo + wy0 + (p >> 2)];
       }
     }
     // the weight goes into the B operand (wz q_c, one product per channel) so A = wx wy is
     // shared by the channels
-    double bq[NCH];
 #pragma unroll
-    for (int ch = 0; ch < NCH; ++ch) bq[ch] = bz * q[ch];
+    for (int ch = 0; ch < NCH; ++ch) o.bq[ch] = bz * q[ch];
+    return o;
+  };
+  auto mma = [&](const Ops& o) {
 #pragma unroll
     for (int rb = 0; rb < RB; ++rb)
 #pragma unroll
-      for (int ch = 0; ch < NCH; ++ch) dmma_884(acc[rb][ch][0], acc[rb][ch][1], cxy[rb], bq[ch]);
+      for (int ch = 0; ch < NCH; ++ch) dmma_884(acc[rb][ch][0], acc[rb][ch][1], o.cxy[rb], o.bq[ch]);
   };
-  static_assert(SW_CH == 32, "one ballot per chunk");
+  static_assert(SW_CH == 32 && K <= 16, "one ballot per chunk; id = 4 buffer bits | 5 slot bits | 3 parity bits");
   for (int c = 0; c < nchunk; ++c) {
     const int b = c % K;
     const int nc = min(SW_CH, ncand - c * SW_CH);
@@ -422,7 +432,9 @@ __global__ void __launch_bounds__((NCW + SW_NP) * 32, NCW == 8 ? 2 : 1) k_spread
     const bool hit = (mk >> warp) & 1u;
     const unsigned m = __ballot_sync(0xffffffffu, hit);
     const bool had_left = tail > head;  // ids of chunk c - 1
-    if (hit) ids[(tail + __popc(m & lanes_lt)) & (SW_IDQ - 1)] = (unsigned short)(b * SW_CH + lane);
+    if (hit)
+      ids[(tail + __popc(m & lanes_lt)) & (SW_IDQ - 1)] =
+          (unsigned short)(b * SW_CH + lane + (((mk >> PB) & 7u) << 9));
     tail += __popc(m);
     __syncwarp();
     HS_CHECK(tail - head <= 3 + SW_CH);
@@ -431,16 +443,31 @@ __global__ void __launch_bounds__((NCW + SW_NP) * 32, NCW == 8 ? 2 : 1) k_spread
       // outlives the chunk after its own
       const int gid = head + kq < tail ? ids[(head + kq) & (SW_IDQ - 1)] : -1;
       head = tail;
-      fire(gid);
+      mma(load_ops(gid));
     }
+#if SW_PREFETCH
+    if (tail - head >= 4) {
+      // operands of group g + 1 are loaded while group g's DMMAs issue
+      Ops cur = load_ops(ids[(head + kq) & (SW_IDQ - 1)]);
+      head += 4;
+      while (tail - head >= 4) {
+        const Ops nxt = load_ops(ids[(head + kq) & (SW_IDQ - 1)]);
+        head += 4;
+        mma(cur);
+        cur = nxt;
+      }
+      mma(cur);
+    }
+#else
     while (tail - head >= 4) {
       const int gid = ids[(head + kq) & (SW_IDQ - 1)];
       head += 4;
-      fire(gid);
+      mma(load_ops(gid));
     }
+#endif
     if (c > 0) mbar_arrive(&empty_bar[(c - 1) % K]);  // the previous chunk's leftovers are consumed
   }
-  if (tail > head) fire(head + kq < tail ? ids[(head + kq) & (SW_IDQ - 1)] : -1);
+  if (tail > head) mma(load_ops(head + kq < tail ? ids[(head + kq) & (SW_IDQ - 1)] : -1));
   if (nchunk > 0) mbar_arrive(&empty_bar[(nchunk - 1) % K]);
   // C fragment: row rq of row block rb = position p, columns z = 2 kq, 2 kq + 1
 #pragma unroll
