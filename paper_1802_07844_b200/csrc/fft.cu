@@ -1039,6 +1039,291 @@ hs_status launch_ystage(hs_ctx* ctx, bool fwd, const double2* in, double2* out, 
   return fail(HS_ERR_PARAMETER, "y stage: unsupported length");
 }
 
+// ---- register z stage for pz = 924 (the metric configuration's padded z length) ------------
+// A real line of 924 points is the 462-point complex transform of z[n] = x[2n] + i x[2n+1] plus
+// one pass over (k, 462 - k) pairs.  462 = 22 x 21: lanes l < 22 hold z[l + 22 j] (j < 21), DFT21
+// (= 3 x DFT7) over j in registers, twiddle W462^{l k1}, one transpose through shared memory
+// (S[k1][l], rows of 23), then lanes r < 21 each take row r and finish with a DFT22 (= 2 x DFT11),
+// ending with Z[r + 21 k2] in natural order in the warp's scratch.
+//   forward (k_zfwd924, replaces the cuFFT D2Z): one warp per line; only the nz <= 432 nonzero
+//     inputs are read (the zero padding of the source grids is never touched), 463 outputs written;
+//   inverse (k_zinv924, replaces the cuFFT Z2D + k_interleave): a CTA takes LPC lines, one warp per
+//     (line, output channel); only the z < nz outputs are formed and they leave channel-interleaved
+//     ([z][pitch], one contiguous block per line) for the gather.
+// Unnormalised both ways, like cuFFT; the inverse ignores the imaginary parts of the k = 0 and
+// Nyquist entries (Z2D semantics).
+__constant__ double2 c_w7[7];   // exp(-2 pi i m / 7)
+__constant__ double2 c_w21[21];  // exp(-2 pi i m / 21)
+__constant__ double2 c_w22[11];  // exp(-2 pi i m / 22)
+static bool g_z924_consts = false;
+static hs_status z924_constants() {
+  HS_TRY(xreg_constants());  // c_w11
+  if (g_z924_consts) return HS_OK;
+  const long double tp = 6.283185307179586476925286766559005768L;
+  double2 w7[7], w21[21], w22[11];
+  for (int m = 0; m < 7; ++m) w7[m] = make_double2((double)std::cos(tp * m / 7), (double)-std::sin(tp * m / 7));
+  for (int m = 0; m < 21; ++m) w21[m] = make_double2((double)std::cos(tp * m / 21), (double)-std::sin(tp * m / 21));
+  for (int m = 0; m < 11; ++m) w22[m] = make_double2((double)std::cos(tp * m / 22), (double)-std::sin(tp * m / 22));
+  HS_CUDA(cudaMemcpyToSymbol(c_w7, w7, sizeof(w7)));
+  HS_CUDA(cudaMemcpyToSymbol(c_w21, w21, sizeof(w21)));
+  HS_CUDA(cudaMemcpyToSymbol(c_w22, w22, sizeof(w22)));
+  g_z924_consts = true;
+  return HS_OK;
+}
+
+// DFT-7 in place (direct, symmetric pairs: 3 cos/sin pairs per output)
+__device__ __forceinline__ void dft7(double2* v) {
+  double2 sp[3], sm[3];
+#pragma unroll
+  for (int m = 1; m <= 3; ++m) {
+    sp[m - 1] = ad(v[m], v[7 - m]);
+    sm[m - 1] = sb(v[m], v[7 - m]);
+  }
+  double2 y[7];
+  y[0] = ad(ad(v[0], sp[0]), ad(sp[1], sp[2]));
+#pragma unroll
+  for (int k = 1; k <= 3; ++k) {
+    double2 re = v[0], im = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int m = 1; m <= 3; ++m) {
+      const double2 w = c_w7[(m * k) % 7];  // (cos, -sin)
+      re = make_double2(fma(w.x, sp[m - 1].x, re.x), fma(w.x, sp[m - 1].y, re.y));
+      im = make_double2(fma(w.y, sm[m - 1].x, im.x), fma(w.y, sm[m - 1].y, im.y));
+    }
+    y[k] = make_double2(re.x - im.y, re.y + im.x);
+    y[7 - k] = make_double2(re.x + im.y, re.y - im.x);
+  }
+#pragma unroll
+  for (int k = 0; k < 7; ++k) v[k] = y[k];
+}
+
+// DFT-21 in place: j = j1 + 3 j2 (j2 < 7), k = 7 k1 + k2 (DFT7 over j2, twiddle W21^{j1 k2}, DFT3 over j1)
+__device__ __forceinline__ void dft21(double2* v) {
+  double2 Y[3][7];
+#pragma unroll
+  for (int j1 = 0; j1 < 3; ++j1) {
+    double2 t[7];
+#pragma unroll
+    for (int j2 = 0; j2 < 7; ++j2) t[j2] = v[j1 + 3 * j2];
+    dft7(t);
+#pragma unroll
+    for (int k2 = 0; k2 < 7; ++k2) Y[j1][k2] = (j1 * k2 == 0) ? t[k2] : cm(t[k2], c_w21[j1 * k2]);
+  }
+#pragma unroll
+  for (int k2 = 0; k2 < 7; ++k2) {
+    double2 t[3] = {Y[0][k2], Y[1][k2], Y[2][k2]};
+    dft<3>(t);
+#pragma unroll
+    for (int k1 = 0; k1 < 3; ++k1) v[7 * k1 + k2] = t[k1];
+  }
+}
+
+constexpr int Z9_N2 = 462, Z9_L = 22, Z9_M = 21, Z9_RS = 23, Z9_LS = Z9_M * Z9_RS;  // scratch >= 462
+constexpr int Z9_NZH = 463, Z9_PZ = 924;
+// forward DFT of the 462-point line with z[l + 22 j] in v[j] (lanes < 22); result Z[k] left in S[k].
+// NK2: number of DFT22 outputs per row needed (22: all; 11: only Z[k], k < 231)
+template <int NK2>
+__device__ __forceinline__ void warp_fft462(double2* v, double2* S, const double2* tw, int lane) {
+  if (lane < Z9_L) {
+    dft21(v);
+#pragma unroll
+    for (int k1 = 1; k1 < Z9_M; ++k1) v[k1] = cm(v[k1], tw[pd8(lane * k1)]);
+  }
+  __syncwarp();
+  if (lane < Z9_L) {
+#pragma unroll
+    for (int k1 = 0; k1 < Z9_M; ++k1) S[k1 * Z9_RS + lane] = v[k1];
+  }
+  __syncwarp();
+  double2 e[11], o[11];
+  const int rr = lane < Z9_M ? lane : Z9_M - 1;
+#pragma unroll
+  for (int m = 0; m < 11; ++m) {
+    e[m] = S[rr * Z9_RS + 2 * m];
+    o[m] = S[rr * Z9_RS + 2 * m + 1];
+  }
+  __syncwarp();
+  dft11(e);
+  dft11(o);
+  if (lane < Z9_M) {
+#pragma unroll
+    for (int k = 0; k < 11; ++k) {
+      const double2 t = k == 0 ? o[0] : cm(o[k], c_w22[k]);
+      S[lane + Z9_M * k] = ad(e[k], t);
+      if (NK2 > 11) S[lane + Z9_M * (k + 11)] = sb(e[k], t);
+    }
+  }
+  __syncwarp();
+}
+
+constexpr int ZF_WARPS = 8;
+__global__ void __launch_bounds__(ZF_WARPS * 32, 1)
+    k_zfwd924(const double* __restrict__ in, double2* __restrict__ out, const double2* __restrict__ twg, int64_t nlines,
+              int nz) {
+  extern __shared__ double2 smem[];
+  double2* tw = smem;                               // pd8-padded W462^i
+  double2* twh = tw + padded_line(Z9_N2);           // W924^k, k <= 231
+  double2* S = twh + 232 + (threadIdx.x >> 5) * Z9_LS;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < Z9_N2; i += blockDim.x) tw[pd8(i)] = twg[i];
+  for (int i = threadIdx.x; i < 232; i += blockDim.x) twh[i] = twg[Z9_N2 + i];
+  __syncthreads();
+  const int nc = (nz + 1) >> 1;  // nonzero complex inputs (nz <= 432 -> <= 216 -> j <= 9)
+  for (int64_t line = (int64_t)blockIdx.x * ZF_WARPS + warp; line < nlines; line += (int64_t)gridDim.x * ZF_WARPS) {
+    const double2* src = reinterpret_cast<const double2*>(in + line * Z9_PZ);
+    double2 v[Z9_M];
+#pragma unroll
+    for (int j = 0; j < Z9_M; ++j) {
+      v[j] = make_double2(0.0, 0.0);
+      if (j < 10) {
+        const int n = lane + Z9_L * j;
+        if (lane < Z9_L && n < nc) {
+          v[j] = src[n];
+          if (2 * n + 1 >= nz) v[j].y = 0.0;  // odd nz: the last pair's second entry is padding
+        }
+      }
+    }
+    warp_fft462<22>(v, S, tw, lane);
+    // X[k] = E + W924^k O, X[462 - k] = conj(E - W924^k O); E = (Z[k] + conj Z[462-k]) / 2,
+    // O = (Z[k] - conj Z[462-k]) / (2 i)
+    double2* dst = out + line * Z9_NZH;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int k = lane + 32 * q;
+      if (k <= 231) {
+        const double2 zk = S[k], zm = S[k == 0 ? 0 : Z9_N2 - k];
+        const double2 E = make_double2(0.5 * (zk.x + zm.x), 0.5 * (zk.y - zm.y));
+        const double2 O = make_double2(0.5 * (zk.y + zm.y), -0.5 * (zk.x - zm.x));
+        const double2 t = cm(O, twh[k]);
+        dst[k] = ad(E, t);
+        const double2 m = sb(E, t);
+        dst[Z9_N2 - k] = make_double2(m.x, -m.y);
+      }
+    }
+    __syncwarp();
+  }
+}
+
+// LPC lines per CTA, NOUT channels: warp w -> (line w / NOUT, channel w % NOUT)
+template <int NOUT, int PITCH, int LPC>
+__global__ void __launch_bounds__(NOUT * LPC * 32, 1)
+    k_zinv924(const double2* __restrict__ spec, int64_t ch_stride, double* __restrict__ gout,
+              const double2* __restrict__ twg, int64_t nlines, int nz) {
+  extern __shared__ double2 smem[];
+  constexpr int NW = NOUT * LPC;
+  double2* tw = smem;
+  double2* twh = tw + padded_line(Z9_N2);
+  double2* S = twh + 232 + (threadIdx.x >> 5) * Z9_LS;
+  double* obuf = reinterpret_cast<double*>(twh + 232 + NW * Z9_LS);  // [LPC][nz][PITCH]
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lc = warp / NOUT, c = warp - lc * NOUT;
+  for (int i = threadIdx.x; i < Z9_N2; i += blockDim.x) tw[pd8(i)] = twg[i];
+  for (int i = threadIdx.x; i < 232; i += blockDim.x) twh[i] = twg[Z9_N2 + i];
+  if (PITCH > NOUT)
+    for (int i = threadIdx.x; i < LPC * nz * PITCH; i += blockDim.x) obuf[i] = 0.0;  // padding channels stay 0
+  __syncthreads();
+  const int nc = (nz + 1) >> 1;
+  for (int64_t l0 = (int64_t)blockIdx.x * LPC; l0 < nlines; l0 += (int64_t)gridDim.x * LPC) {
+    const int64_t line = l0 + lc;
+    if (line < nlines) {
+      const double2* X = spec + (int64_t)c * ch_stride + line * Z9_NZH;
+      // conj(Z[k]), Z[k] = E[k] + i O[k], E = X[k] + conj X[462-k], O = (X[k] - conj X[462-k]) conj(W924^k);
+      // Z[462-k] = conj E + i conj O
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int k = lane + 32 * q;
+        if (k <= 231) {
+          double2 xk = X[k], xm = X[Z9_N2 - k];
+          if (k == 0) xk.y = xm.y = 0.0;
+          const double2 E = make_double2(xk.x + xm.x, xk.y - xm.y);
+          const double2 D = make_double2(xk.x - xm.x, xk.y + xm.y);
+          const double2 w = twh[k];
+          const double2 O = make_double2(fma(D.x, w.x, D.y * w.y), fma(D.y, w.x, -D.x * w.y));  // D conj(w)
+          // Z[k] = (E.x - O.y, E.y + O.x): conj -> (E.x - O.y, -E.y - O.x)
+          // Z[462-k] = (E.x + O.y, -E.y + O.x): conj -> (E.x + O.y, E.y - O.x)
+          if (k > 0) S[Z9_N2 - k] = make_double2(E.x + O.y, E.y - O.x);
+          S[k] = make_double2(E.x - O.y, -E.y - O.x);
+        }
+      }
+      __syncwarp();
+      double2 v[Z9_M];
+#pragma unroll
+      for (int j = 0; j < Z9_M; ++j) v[j] = lane < Z9_L ? S[lane + Z9_L * j] : make_double2(0.0, 0.0);
+      __syncwarp();
+      warp_fft462<11>(v, S, tw, lane);  // z[n] = conj(S[n]), n < 231 >= nc
+      double* ob = obuf + (size_t)lc * nz * PITCH + c;
+#pragma unroll
+      for (int q = 0; q < 7; ++q) {
+        const int n = lane + 32 * q;
+        if (n < nc) {
+          const double2 f = S[n];
+          ob[(2 * n) * PITCH] = f.x;
+          if (2 * n + 1 < nz) ob[(2 * n + 1) * PITCH] = -f.y;
+        }
+      }
+    }
+    __syncthreads();
+    // one contiguous [nz][PITCH] block per line
+    const int per = nz * PITCH / 2;  // double2 per line (nz * PITCH even)
+    for (int i = threadIdx.x; i < LPC * per; i += blockDim.x) {
+      const int ll = i / per, r = i - ll * per;
+      if (l0 + ll < nlines)
+        reinterpret_cast<double2*>(gout + (l0 + ll) * (int64_t)PITCH * Z9_PZ)[r] =
+            reinterpret_cast<const double2*>(obuf + (size_t)ll * nz * PITCH)[r];
+    }
+    __syncthreads();
+  }
+}
+
+bool zstage_supported(int pz, int nz) { return pz == Z9_PZ && nz <= 432 && nz % 2 == 0; }
+// twiddle table of the z stage: W462^i (462) then W924^k (k < 232)
+int zstage_twiddle_count() { return Z9_N2 + 232; }
+hs_status make_zstage_twiddles(double2* d_tw, cudaStream_t st) {
+  std::vector<double2> tw(Z9_N2 + 232);
+  const long double tp = 6.283185307179586476925286766559005768L;
+  for (int j = 0; j < Z9_N2; ++j)
+    tw[j] = make_double2((double)std::cos(tp * j / Z9_N2), (double)-std::sin(tp * j / Z9_N2));
+  for (int j = 0; j < 232; ++j)
+    tw[Z9_N2 + j] = make_double2((double)std::cos(tp * j / Z9_PZ), (double)-std::sin(tp * j / Z9_PZ));
+  HS_CUDA(cudaMemcpyAsync(d_tw, tw.data(), sizeof(double2) * tw.size(), cudaMemcpyHostToDevice, st));
+  HS_CUDA(cudaStreamSynchronize(st));
+  return HS_OK;
+}
+// forward z of one channel: lines of pitch pz (nz nonzero values) -> nzh = 463 spectrum entries
+hs_status launch_zfwd(hs_ctx* ctx, const double* in, double2* out, const double2* tw, int64_t nlines, int nz) {
+  HS_TRY(z924_constants());
+  const size_t smem = sizeof(double2) * (padded_line(Z9_N2) + 232 + (size_t)ZF_WARPS * Z9_LS);
+  HS_CUDA(cudaFuncSetAttribute(k_zfwd924, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per_sm = 1;
+  HS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_zfwd924, ZF_WARPS * 32, smem));
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(nlines, ZF_WARPS),
+                                                               (int64_t)ctx->sm_count * std::max(per_sm, 1)));
+  k_zfwd924<<<grid, ZF_WARPS * 32, smem, ctx->stream>>>(in, out, tw, nlines, nz);
+  HS_LAUNCHED(ctx);
+  return HS_OK;
+}
+// inverse z of all n_out channels (channel stride ch_stride in `spec`), outputs z < nz interleaved
+// into gout ([line][pz][pitch] storage, z < nz written)
+hs_status launch_zinv_interleaved(hs_ctx* ctx, const double2* spec, int64_t ch_stride, int n_out, int pitch,
+                                  double* gout, const double2* tw, int64_t nlines, int nz) {
+  HS_TRY(z924_constants());
+  auto go = [&](auto kern, int nw, int lpc) -> hs_status {
+    const size_t smem = sizeof(double2) * (padded_line(Z9_N2) + 232 + (size_t)nw * Z9_LS) +
+                        sizeof(double) * (size_t)lpc * nz * pitch;
+    HS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 1;
+    HS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nw * 32, smem));
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(nlines, lpc),
+                                                                 (int64_t)ctx->sm_count * std::max(per_sm, 1)));
+    kern<<<grid, nw * 32, smem, ctx->stream>>>(spec, ch_stride, gout, tw, nlines, nz);
+    HS_LAUNCHED(ctx);
+    return HS_OK;
+  };
+  if (n_out == 6 && pitch == 6) return go(k_zinv924<6, 6, 2>, 12, 2);
+  if (n_out == 3 && pitch == 4) return go(k_zinv924<3, 4, 4>, 12, 4);
+  return fail(HS_ERR_PARAMETER, "z stage: unsupported channel layout");
+}
+
 template <int KIND, bool HALF, int KB, class FFT>
 static hs_status launch_xfused_t(hs_ctx* ctx, const XArgs& a) {
   constexpr int NL = KChan<KIND, HALF>::NIN > KChan<KIND, HALF>::NOUT ? KChan<KIND, HALF>::NIN

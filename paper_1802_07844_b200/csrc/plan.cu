@@ -349,6 +349,7 @@ struct hs_plan {
   double* tabH = nullptr;
   double2* tw = nullptr;        // px twiddles
   double2* ytw = nullptr;       // py twiddles of the register y stage (null: cuFFT y stage)
+  double2* ztw = nullptr;       // twiddles of the register z stage (null: cuFFT z stage + k_interleave)
   FftPlan xplan{};
   bool have_B = false, have_H = false;
   cufftHandle zf = 0, yf = 0, zi = 0;
@@ -593,7 +594,13 @@ static hs_status plan_create_impl(hs_ctx* ctx, const hs_params* prm, const hs_sl
     A_((size_t)std::max(p->n_in, p->n_out) * p->n_mixed, p->spec);
     p->out_pitch = p->half ? 6 : 4;
     A_((size_t)p->out_pitch * p->n_grid, p->grid_out, true);
-    if (mixed && !sl && p->sg_cap >= p->n_out) {
+    // register z stage (single-GPU plans): the inverse writes the interleaved output grids
+    // directly, so no per-channel inverse buffer exists; env HS_ZSTAGE_CUFFT: cuFFT z stage +
+    // k_interleave (comparison)
+    const bool zreg = zstage_supported((int)pz, (int)prm->dims[2]) && !sl && !getenv("HS_ZSTAGE_CUFFT");
+    if (zreg) {
+      A_(zstage_twiddle_count(), p->ztw);
+    } else if (mixed && !sl && p->sg_cap >= p->n_out) {
       p->grid_tmp = p->grid_in;  // the source grids are dead once forward-transformed
       p->tmp_aliased = true;
     } else {
@@ -614,6 +621,7 @@ static hs_status plan_create_impl(hs_ctx* ctx, const hs_params* prm, const hs_sl
       A_(py, p->ytw);
       if ((st = make_twiddles((int)py, p->ytw, ctx->stream)) != HS_OK) return bail(st);
     }
+    if (p->ztw && (st = make_zstage_twiddles(p->ztw, ctx->stream)) != HS_OK) return bail(st);
   }
   A_(3 * (size_t)std::max(nt, 1), p->u);
   A_(3 * (size_t)std::max(nt, 1), p->u_real, true);
@@ -1483,7 +1491,9 @@ extern "C" hs_status hs_plan_execute(hs_plan* p, const double* positions, const 
       if (gi > 0) HS_TRY(stage_spread_group(p, gi));
       for (int c = p->group_c0[gi]; c < p->group_c0[gi + 1]; ++c) {
         const double* gin = p->grid_in + (size_t)(c - p->group_c0[gi]) * p->n_grid;
-        if (cufftExecD2Z(p->zf, (double*)gin, (cufftDoubleComplex*)p->Amix) != CUFFT_SUCCESS)
+        if (p->ztw)
+          HS_TRY(launch_zfwd(ctx, gin, p->Amix, p->ztw, (int64_t)p->gg.dims[1] * p->gg.dims[0], p->gg.dims[2]));
+        else if (cufftExecD2Z(p->zf, (double*)gin, (cufftDoubleComplex*)p->Amix) != CUFFT_SUCCESS)
           return fail(HS_ERR_CUDA, "cuFFT z D2Z failed");
         HS_TRY(stage_yfwd(p, p->Amix, c));
       }
@@ -1494,13 +1504,20 @@ extern "C" hs_status hs_plan_execute(hs_plan* p, const double* positions, const 
     for (int o = 0; o < p->n_out; ++o) {
       double2* so = p->spec + (size_t)o * p->n_mixed;
       HS_TRY(stage_yinv(p, o, so));
-      if (cufftExecZ2D(p->zi, (cufftDoubleComplex*)so, p->grid_tmp + (size_t)o * p->n_grid) != CUFFT_SUCCESS)
+      if (!p->ztw &&
+          cufftExecZ2D(p->zi, (cufftDoubleComplex*)so, p->grid_tmp + (size_t)o * p->n_grid) != CUFFT_SUCCESS)
         return fail(HS_ERR_CUDA, "cuFFT z Z2D failed");
     }
-    // channel-interleave the (y < ny, x < nx, z < nz) outputs for the broadcast gather
-    k_interleave<<<grid_size(ctx, p->n_grid / 2), 256, 0, ctx->stream>>>(p->grid_tmp, p->n_out, p->n_grid,
-                                                                         p->n_grid, p->out_pitch, p->grid_out);
-    HS_LAUNCHED(ctx);
+    if (p->ztw) {
+      // inverse z of all output channels, written channel-interleaved (z < nz) for the gather
+      HS_TRY(launch_zinv_interleaved(ctx, p->spec, (int64_t)p->n_mixed, p->n_out, p->out_pitch, p->grid_out, p->ztw,
+                                     (int64_t)p->gg.dims[1] * p->gg.dims[0], p->gg.dims[2]));
+    } else {
+      // channel-interleave the (y < ny, x < nx, z < nz) outputs for the broadcast gather
+      k_interleave<<<grid_size(ctx, p->n_grid / 2), 256, 0, ctx->stream>>>(p->grid_tmp, p->n_out, p->n_grid,
+                                                                           p->n_grid, p->out_pitch, p->grid_out);
+      HS_LAUNCHED(ctx);
+    }
     if (p->tmp_aliased) {
       // the inverse z transforms wrote whole pz lines into the source grids: restore their zero
       // z padding (the next spread writes z < nz only)

@@ -380,11 +380,14 @@ def test_fourier_gather_layouts_vs_oracle(gpu, oracle, kind, nt):
 
 @pytest.mark.parametrize("kind,M", [(k, m) for k in KINDS for m in (192, 128)] + [("stokeslet", 384),
                                                                                   ("rotlet", 320), ("stresslet", 320)])
-@pytest.mark.parametrize("alt", ("HS_XSTAGE_STOCKHAM", "HS_YSTAGE_CUFFT"))
+@pytest.mark.parametrize("alt", ("HS_XSTAGE_STOCKHAM", "HS_YSTAGE_CUFFT", "HS_ZSTAGE_CUFFT"))
 def test_register_fft_stages_match_alternatives(tmp_path, kind, M, alt):
     """The register-FFT x stage and y stage (N = 480 = 15 x 32 at M=192, 352 = 11 x 32 at
     M=128, 864 = 27 x 32 at M=384, 750 = 30 x 25 at M=320) against the shared-memory Stockham x stage / the cuFFT y stage on the same input
-    (each selected in its own process)."""
+    (each selected in its own process); the register z stage (924 = 2 x 22 x 21 real points at
+    M=192, with the fused channel interleave) against the cuFFT D2Z / Z2D + interleave pass."""
+    if alt == "HS_ZSTAGE_CUFFT" and M != 192:
+        pytest.skip("the register z stage exists for pz = 924 (M = 192)")
     import os
     import subprocess
     import sys
