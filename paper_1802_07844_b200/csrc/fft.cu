@@ -1156,7 +1156,7 @@ __device__ __forceinline__ void warp_fft462(double2* v, double2* S, const double
   __syncwarp();
 }
 
-constexpr int ZF_WARPS = 8;
+constexpr int ZF_WARPS = 8, ZF_STAGE = 216;  // staged complex inputs per line (nz <= 432)
 __global__ void __launch_bounds__(ZF_WARPS * 32, 1)
     k_zfwd924(const double* __restrict__ in, double2* __restrict__ out, const double2* __restrict__ twg, int64_t nlines,
               int nz) {
@@ -1164,13 +1164,27 @@ __global__ void __launch_bounds__(ZF_WARPS * 32, 1)
   double2* tw = smem;                               // pd8-padded W462^i
   double2* twh = tw + padded_line(Z9_N2);           // W924^k, k <= 231
   double2* S = twh + 232 + (threadIdx.x >> 5) * Z9_LS;
+  // the warp's next line is prefetched (cp.async) into its staging row while the current one
+  // is transformed, so the loads of one line overlap the arithmetic of the previous
+  double2* stage = twh + 232 + ZF_WARPS * Z9_LS + (threadIdx.x >> 5) * ZF_STAGE;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int i = threadIdx.x; i < Z9_N2; i += blockDim.x) tw[pd8(i)] = twg[i];
   for (int i = threadIdx.x; i < 232; i += blockDim.x) twh[i] = twg[Z9_N2 + i];
   __syncthreads();
   const int nc = (nz + 1) >> 1;  // nonzero complex inputs (nz <= 432 -> <= 216 -> j <= 9)
-  for (int64_t line = (int64_t)blockIdx.x * ZF_WARPS + warp; line < nlines; line += (int64_t)gridDim.x * ZF_WARPS) {
-    const double2* src = reinterpret_cast<const double2*>(in + line * Z9_PZ);
+  const int64_t lstep = (int64_t)gridDim.x * ZF_WARPS;
+  auto prefetch = [&](int64_t line) {
+    if (line < nlines) {
+      const double2* src = reinterpret_cast<const double2*>(in + line * Z9_PZ);
+      for (int n = lane; n < nc; n += 32) cp_async16(&stage[n], &src[n]);
+    }
+    cp_async_commit();
+  };
+  int64_t line = (int64_t)blockIdx.x * ZF_WARPS + warp;
+  prefetch(line);
+  for (; line < nlines; line += lstep) {
+    cp_async_wait_all();
+    __syncwarp();
     double2 v[Z9_M];
 #pragma unroll
     for (int j = 0; j < Z9_M; ++j) {
@@ -1178,11 +1192,13 @@ __global__ void __launch_bounds__(ZF_WARPS * 32, 1)
       if (j < 10) {
         const int n = lane + Z9_L * j;
         if (lane < Z9_L && n < nc) {
-          v[j] = src[n];
+          v[j] = stage[n];
           if (2 * n + 1 >= nz) v[j].y = 0.0;  // odd nz: the last pair's second entry is padding
         }
       }
     }
+    __syncwarp();
+    prefetch(line + lstep);
     warp_fft462<22>(v, S, tw, lane);
     // X[k] = E + W924^k O, X[462 - k] = conj(E - W924^k O); E = (Z[k] + conj Z[462-k]) / 2,
     // O = (Z[k] - conj Z[462-k]) / (2 i)
@@ -1202,6 +1218,7 @@ __global__ void __launch_bounds__(ZF_WARPS * 32, 1)
     }
     __syncwarp();
   }
+  cp_async_wait_all();
 }
 
 // LPC lines per CTA, NOUT channels: warp w -> (line w / NOUT, channel w % NOUT)
@@ -1292,7 +1309,7 @@ hs_status make_zstage_twiddles(double2* d_tw, cudaStream_t st) {
 // forward z of one channel: lines of pitch pz (nz nonzero values) -> nzh = 463 spectrum entries
 hs_status launch_zfwd(hs_ctx* ctx, const double* in, double2* out, const double2* tw, int64_t nlines, int nz) {
   HS_TRY(z924_constants());
-  const size_t smem = sizeof(double2) * (padded_line(Z9_N2) + 232 + (size_t)ZF_WARPS * Z9_LS);
+  const size_t smem = sizeof(double2) * (padded_line(Z9_N2) + 232 + (size_t)ZF_WARPS * (Z9_LS + ZF_STAGE));
   HS_CUDA(cudaFuncSetAttribute(k_zfwd924, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 1;
   HS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_zfwd924, ZF_WARPS * 32, smem));

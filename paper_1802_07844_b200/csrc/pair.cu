@@ -85,6 +85,9 @@ __device__ __forceinline__ double rcp_pos(double v) {
   return y;
 }
 #endif
+#ifndef PC_SCAN4
+#define PC_SCAN4 0  // scan loop: 4 candidates per iteration (1) or 2 (0)
+#endif
 #ifndef PC_DRAIN2
 #define PC_DRAIN2 1   // queue drains by two-pair rounds where lanes have >= 2 entries
 #endif
@@ -642,6 +645,33 @@ __global__ void __launch_bounds__(PC_TG, pc_minb<KIND>()) k_pair_q(const PairArg
         const unsigned q_s = (unsigned)__cvta_generic_to_shared(&q[0][lane]);  // this lane's slot 0
         const int qb = hb + j0;
         unsigned msh = 0;
+#if PC_SCAN4
+        // four near candidates per iteration: their four broadcast loads are issued together, so
+        // one shared-memory latency is paid per four tests (same test and push order as the
+        // two-candidate form, hence bit-identical queues)
+        while (near) {  // warp-uniform (lanes without a target test far-away coordinates)
+          int ix[4];
+          unsigned bx[4];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const bool has = near != 0;
+            ix[k] = has ? bfind_u32(near) : ix[k > 0 ? k - 1 : 0];
+            bx[k] = has ? 1u << ix[k] : 0u;
+            near ^= bx[k];
+          }
+          float4 Fx[4];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) Fx[k] = lds_f4(sFg_s + (ix[k] << 4));  // broadcast
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const float rk = dist2f(tfx, tfy, tfz, Fx[k]);
+            const bool ok = bx[k] != 0u && rk > 0.0f && rk <= a.rc2_lo;
+            msh |= (!ok && rk <= a.rc2_hi) ? bx[k] : 0u;
+            sts_u16(q_s + (((unsigned)tail & (PC_Q - 1)) << 6), qb + ix[k]);
+            tail += ok ? 1 : 0;
+          }
+        }
+#else
         while (near) {  // warp-uniform (lanes without a target test far-away coordinates)
           const int ia = bfind_u32(near);
           const unsigned ba = 1u << ia;
@@ -660,6 +690,7 @@ __global__ void __launch_bounds__(PC_TG, pc_minb<KIND>()) k_pair_q(const PairArg
           sts_u16(q_s + (((unsigned)tail & (PC_Q - 1)) << 6), qb + ib);
           tail += okb ? 1 : 0;
         }
+#endif
         if (__any_sync(0xffffffffu, msh != 0)) {
           while (msh) {
             const int ib = bfind_u32(msh);
