@@ -669,29 +669,52 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
-// runs and items of one 4x4 block's targets [b, e) (z-sorted); emit == nullptr: count only
-__device__ int g7_cut(const double4* __restrict__ pts, int b, int e, const GridGeom& g, int4* emit) {
-  int nitem = 0, i = b;
-  while (i < e) {
-    const int ib = i;
-    int nrun = 0;
-    int lens = 0;
-    const int64_t zi0 = g_lo(g, 2, pts[i].z);
-    while (i < e && nrun < G7_WARPS) {
-      const int64_t zr0 = g_lo(g, 2, pts[i].z);
-      if (zr0 - zi0 > G7_ZC - g.P) break;
-      int len = 1;
-      ++i;
-      while (i < e && len < G7_TG) {
-        const int64_t z = g_lo(g, 2, pts[i].z);
-        if (z - zr0 > 32 - g.P || z - zi0 > G7_ZC - g.P) break;
-        ++len;
-        ++i;
+// runs and items of one 4x4 block's targets [b, e) (z-sorted), by one warp; emit == nullptr: count
+// only.  The cut is a sequential scan over the targets' z window starts: a run takes up to G7_TG
+// targets whose starts stay within 32 - P nodes of its first, an item up to G7_WARPS runs within
+// G7_ZC - P nodes of its first target.  Lanes load 32 window starts at a time; every lane then
+// steps the same (warp-uniform) state machine over the shuffled values, lane 0 emits.
+__device__ int g7_cut(const double4* __restrict__ pts, int b, int e, const GridGeom& g, int4* emit, int lane) {
+  int nitem = 0;
+  bool item_open = false, in_run = false;
+  int ib = 0, nrun = 0, lens = 0, len = 0;
+  int64_t zi0 = 0, zr0 = 0;
+  const int run_span = 32 - g.P, item_span = G7_ZC - g.P;
+  for (int base = b; base < e; base += 32) {
+    const int64_t zl = base + lane < e ? g_lo(g, 2, pts[base + lane].z) : 0;
+    const int nk = min(32, e - base);
+    for (int k = 0; k < nk; ++k) {
+      const int64_t z = __shfl_sync(0xffffffffu, zl, k);
+      const int i = base + k;
+      if (in_run) {
+        if (len < G7_TG && z - zr0 <= run_span && z - zi0 <= item_span) {
+          ++len;
+          continue;
+        }
+        lens |= len << (8 * nrun);
+        ++nrun;
+        in_run = false;
       }
-      lens |= len << (8 * nrun);
-      ++nrun;
+      if (item_open && !(nrun < G7_WARPS && z - zi0 <= item_span)) {
+        if (emit && lane == 0) emit[nitem] = make_int4(ib, i - ib, lens, 0);
+        ++nitem;
+        item_open = false;
+      }
+      if (!item_open) {
+        ib = i;
+        nrun = 0;
+        lens = 0;
+        zi0 = z;
+        item_open = true;
+      }
+      zr0 = z;
+      len = 1;
+      in_run = true;
     }
-    if (emit) emit[nitem] = make_int4(ib, i - ib, lens, 0);
+  }
+  if (in_run) lens |= len << (8 * nrun);
+  if (item_open) {
+    if (emit && lane == 0) emit[nitem] = make_int4(ib, e - ib, lens, 0);
     ++nitem;
   }
   return nitem;
@@ -699,14 +722,18 @@ __device__ int g7_cut(const double4* __restrict__ pts, int b, int e, const GridG
 
 __global__ void k_g7_count(const double4* __restrict__ pts, const int* __restrict__ bstart, int nblk, int nz,
                            GridGeom g, int* __restrict__ cnt) {
-  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < nblk; c += gridDim.x * blockDim.x)
-    cnt[c] = g7_cut(pts, bstart[c * nz], bstart[(c + 1) * nz], g, nullptr);
+  const int lane = threadIdx.x & 31;
+  for (int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; c < nblk; c += (gridDim.x * blockDim.x) >> 5) {
+    const int n = g7_cut(pts, bstart[c * nz], bstart[(c + 1) * nz], g, nullptr, lane);
+    if (lane == 0) cnt[c] = n;
+  }
 }
 
 __global__ void k_g7_fill(const double4* __restrict__ pts, const int* __restrict__ bstart, int nblk, int nz,
                           GridGeom g, const int* __restrict__ istart, int4* __restrict__ items) {
-  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < nblk; c += gridDim.x * blockDim.x)
-    g7_cut(pts, bstart[c * nz], bstart[(c + 1) * nz], g, items + istart[c]);
+  const int lane = threadIdx.x & 31;
+  for (int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; c < nblk; c += (gridDim.x * blockDim.x) >> 5)
+    g7_cut(pts, bstart[c * nz], bstart[(c + 1) * nz], g, items + istart[c], lane);
 }
 
 // Gather on the FP64 tensor pipe (k_gather8).  Items, runs, the column staging ring and the
@@ -965,7 +992,7 @@ hs_status launch_gather_fourier(hs_ctx* ctx, const double4* pts, const int* orig
   int* cnt = (int*)(items + n);
   int* istart = cnt + nb4;  // nb4 + 1
   int* sc = istart + nb4 + 1;
-  const int gsb = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(nb4, 128), ctx->sm_count * 4));
+  const int gsb = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(nb4, 4), ctx->sm_count * 16));  // warp per block
   k_g7_count<<<gsb, 128, 0, ctx->stream>>>(pts, bstart, nb4, g.dims[2], g, cnt);
   HS_LAUNCHED(ctx);
   HS_TRY(exclusive_scan(ctx, cnt, nb4, istart, sc));
