@@ -85,6 +85,12 @@ __device__ __forceinline__ double rcp_pos(double v) {
   return y;
 }
 #endif
+#ifndef PC_QPREFETCH
+#define PC_QPREFETCH 0  // full rounds: read the next round's queue entries during the current one
+#endif
+#ifndef PC_LN2_SINGLE
+#define PC_LN2_SINGLE 1  // exp: one ln2 constant in the range reduction (1 DFMA fewer; |n| <= 37 so the error stays <= 2e-15)
+#endif
 #ifndef PC_SCAN4
 #define PC_SCAN4 0  // scan loop: 4 candidates per iteration (1) or 2 (0)
 #endif
@@ -131,8 +137,12 @@ __device__ __forceinline__ double exp_nonpos(double x) {
   const double t = fma(x, 1.4426950408889634, kShift);
   const double n = t - kShift;
   const int ni = __double2loint(t);
+#if PC_LN2_SINGLE
+  const double r = fma(n, -0.6931471805599453094, x);
+#else
   double r = fma(n, -6.93147180369123816490e-01, x);  // ln2 hi (exact product for |n| < 2^11)
   r = fma(n, -1.90821492927058770002e-10, r);         // ln2 lo
+#endif
   double p = c_exp_poly[0];
 #pragma unroll
   for (int j = 1; j < 12; ++j) p = fma(p, r, c_exp_poly[j]);
@@ -547,9 +557,7 @@ __global__ void __launch_bounds__(PC_TG, pc_minb<KIND>()) k_pair_q(const PairArg
     };
     // two queued pairs in straight-line code: their exp / erfc / rsqrt chains are
     // independent and interleave (the evaluation is latency-, not issue-bound)
-    auto pop_eval2 = [&]() {
-      const int j1 = q[head & (PC_Q - 1)][lane];
-      const int j2 = q[(head + 1) & (PC_Q - 1)][lane];
+    auto eval2 = [&](int j1, int j2) {
       HS_CHECK(j1 < PC_K && j2 < PC_K && head + 2 <= tail);
       head += 2;
       n_acc += 2;
@@ -568,6 +576,11 @@ __global__ void __launch_bounds__(PC_TG, pc_minb<KIND>()) k_pair_q(const PairArg
                   splitmix64((unsigned long long)__float_as_int(sF[j2].w));
       apply_kind(q1, j1, f0, f1, f2, r1, S1, A1, B1, i1);
       apply_kind(q2, j2, g0, g1, g2, r2, S2, A2, B2, i2);
+    };
+    auto pop_eval2 = [&]() {
+      const int j1 = q[head & (PC_Q - 1)][lane];
+      const int j2 = q[(head + 1) & (PC_Q - 1)][lane];
+      eval2(j1, j2);
     };
     for (int c = 0, c0 = 0; c0 < ncand; ++c, c0 += PC_H) {
       const int h = c % pc_nh<KIND>(), hb = h * PC_H;
@@ -713,7 +726,21 @@ __global__ void __launch_bounds__(PC_TG, pc_minb<KIND>()) k_pair_q(const PairArg
         if (mn == 0x7fffffffu) mn = 0;
         if (tvalid) {
           unsigned r = 0;
+#if PC_QPREFETCH
+          // the next round's queue entries are read while the current round evaluates (slots past
+          // `tail` hold stale but valid indices; they are re-read once pushed)
+          if (mn >= 2) {
+            int j1 = q[head & (PC_Q - 1)][lane], j2 = q[(head + 1) & (PC_Q - 1)][lane];
+            for (; r + 1 < mn; r += 2) {
+              const int n1 = q[(head + 2) & (PC_Q - 1)][lane], n2 = q[(head + 3) & (PC_Q - 1)][lane];
+              eval2(j1, j2);
+              j1 = n1;
+              j2 = n2;
+            }
+          }
+#else
           for (; r + 1 < mn; r += 2) pop_eval2();
+#endif
           // an odd leftover stays queued for the next two-pair round (PC_ODD_SINGLE=1: evaluate it now)
           if (PC_ODD_SINGLE && r < mn) pop_eval();
         }
