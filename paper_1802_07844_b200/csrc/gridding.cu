@@ -185,6 +185,9 @@ constexpr int SW_CH = SW_CH_DEF, SW_K = SW_K_DEF, SW_H = SW_CH_DEF / 32, SW_RX =
 #endif
 constexpr int SW_NP = SW_NP_DEF, SW_THREADS = (8 + SW_NP) * 32;
 static_assert(SW_K % SW_NP == 0, "ring slots must divide among the producers");
+#ifndef SP_STRIP
+#define SP_STRIP 2  // tile-order strip width in x (0: plain x-major order)
+#endif
 #ifndef SW_PREFETCH
 #define SW_PREFETCH 0  // 1: load group g + 1's operands before group g's DMMAs (spills at the 96-register cap: 18.3 vs 14.4 ms)
 #endif
@@ -224,9 +227,24 @@ __global__ void __launch_bounds__((NCW + SW_NP) * 32, NCW == 8 ? 2 : 1) k_spread
   auto bq_ = [&](int b) { return reinterpret_cast<double(*)[RQ]>(sm_dyn + b * PER + SW_CH * (RX + RY + RZ)); };
   auto bm_ = [&](int b) { return reinterpret_cast<unsigned*>(sm_dyn + b * PER + SW_CH * (RX + RY + RZ + RQ)); };
 
-  const int tz = blockIdx.x % nbz;
-  const int ty = (blockIdx.x / nbz) % nby;
-  const int tx = blockIdx.x / (nbz * nby);
+  // Tile order: strips of SP_STRIP tile columns in x; within a strip y-major, then the strip's x
+  // columns, z fastest.  Consecutively launched tiles then share their candidate bins (a source's
+  // window rows are re-read by the ~25 tiles its support touches): the live set is 3 y-columns x
+  // (SP_STRIP + 2) x-columns of sources, which the L2 holds, instead of whole x-slabs.
+  int tx, ty, tz;
+  if (SP_STRIP > 0) {
+    const int per_strip = SP_STRIP * nby * nbz;
+    const int sidx = blockIdx.x / per_strip, r = blockIdx.x - sidx * per_strip;
+    const int kk = min(SP_STRIP, nbx - sidx * SP_STRIP);  // width of this strip
+    ty = r / (kk * nbz);
+    const int r2 = r - ty * kk * nbz;
+    tx = sidx * SP_STRIP + r2 / nbz;
+    tz = r2 - (r2 / nbz) * nbz;
+  } else {
+    tz = blockIdx.x % nbz;
+    ty = (blockIdx.x / nbz) % nby;
+    tx = blockIdx.x / (nbz * nby);
+  }
   const int x0 = tx * SP_TX, y0 = ty * SP_TY, z0 = tz * SP_TZ;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int P = g.P;

@@ -89,7 +89,7 @@ __device__ __forceinline__ double rcp_pos(double v) {
 #define PC_QPREFETCH 0  // full rounds: read the next round's queue entries during the current one
 #endif
 #ifndef PC_LN2_SINGLE
-#define PC_LN2_SINGLE 1  // exp: one ln2 constant in the range reduction (1 DFMA fewer; |n| <= 37 so the error stays <= 2e-15)
+#define PC_LN2_SINGLE 1  // exp: one ln2 constant in the range reduction (1 DFMA fewer; error <= |n| 5.5e-17, below 3e-15 wherever exp(x) > 1e-16)
 #endif
 #ifndef PC_SCAN4
 #define PC_SCAN4 0  // scan loop: 4 candidates per iteration (1) or 2 (0)
