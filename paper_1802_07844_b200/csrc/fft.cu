@@ -1338,6 +1338,7 @@ hs_status launch_zinv_interleaved(hs_ctx* ctx, const double2* spec, int64_t ch_s
   };
   if (n_out == 6 && pitch == 6) return go(k_zinv924<6, 6, 2>, 12, 2);
   if (n_out == 3 && pitch == 4) return go(k_zinv924<3, 4, 4>, 12, 4);
+  if (n_out == 1 && pitch == 1) return go(k_zinv924<1, 1, 12>, 12, 12);  // one channel, not interleaved
   return fail(HS_ERR_PARAMETER, "z stage: unsupported channel layout");
 }
 

@@ -597,14 +597,16 @@ static hs_status plan_create_impl(hs_ctx* ctx, const hs_params* prm, const hs_sl
     // register z stage (single-GPU plans): the inverse writes the interleaved output grids
     // directly, so no per-channel inverse buffer exists; env HS_ZSTAGE_CUFFT: cuFFT z stage +
     // k_interleave (comparison)
-    const bool zreg = zstage_supported((int)pz, (int)prm->dims[2]) && !sl && !getenv("HS_ZSTAGE_CUFFT");
-    if (zreg) {
-      A_(zstage_twiddle_count(), p->ztw);
+    // (y-slab plans keep the per-channel inverse buffer: their channels arrive one at a time from
+    // the all-to-all, so each is inverse-transformed on its own and interleaved at the end)
+    const bool zreg = zstage_supported((int)pz, (int)prm->dims[2]) && !getenv("HS_ZSTAGE_CUFFT");
+    if (zreg) A_(zstage_twiddle_count(), p->ztw);
+    if (zreg && !sl) {
     } else if (mixed && !sl && p->sg_cap >= p->n_out) {
       p->grid_tmp = p->grid_in;  // the source grids are dead once forward-transformed
       p->tmp_aliased = true;
     } else {
-      A_((size_t)p->n_out * p->n_grid, p->grid_tmp);
+      A_((size_t)p->n_out * p->n_grid, p->grid_tmp, true);
     }
     p->go = p->gg;
     p->go.stride[0] = (int64_t)p->out_pitch * pz;
@@ -1722,7 +1724,9 @@ extern "C" hs_status hs_slab_forward_range(hs_plan* p, const double* ghost_in, d
   const KzSplit ks = kz_split_of(p);
   const int64_t rows = (int64_t)p->yo * nx;
   for (int c = c0; c < c1; ++c) {
-    if (cufftExecD2Z(p->zf, p->grid_in + (size_t)c * p->n_grid, (cufftDoubleComplex*)p->Amix) != CUFFT_SUCCESS)
+    if (p->ztw)
+      HS_TRY(launch_zfwd(ctx, p->grid_in + (size_t)c * p->n_grid, p->Amix, p->ztw, rows, (int)nz));
+    else if (cufftExecD2Z(p->zf, p->grid_in + (size_t)c * p->n_grid, (cufftDoubleComplex*)p->Amix) != CUFFT_SUCCESS)
       return fail(HS_ERR_CUDA, "cuFFT z D2Z failed");
     k_kz_exchange<<<grid_size(ctx, rows * p->kg.nzh), 256, 0, st>>>(
         p->Amix, (double2*)send + (size_t)c * p->n_amix, rows, p->kg.nzh, ks, 0);
@@ -1785,7 +1789,9 @@ extern "C" hs_status hs_slab_backward_range(hs_plan* p, const double* recv_back,
     k_kz_exchange<<<grid_size(ctx, rows * p->kg.nzh), 256, 0, st>>>(
         p->Amix, (double2*)recv_back + (size_t)o * p->n_amix, rows, p->kg.nzh, ks, 1);
     HS_LAUNCHED(ctx);
-    if (cufftExecZ2D(p->zi, (cufftDoubleComplex*)p->Amix, p->grid_tmp + (size_t)o * p->n_grid) != CUFFT_SUCCESS)
+    if (p->ztw)  // one channel, plain lines of pitch pz (z < nz written; the padding stays zero)
+      HS_TRY(launch_zinv_interleaved(ctx, p->Amix, 0, 1, 1, p->grid_tmp + (size_t)o * p->n_grid, p->ztw, rows, (int)nz));
+    else if (cufftExecZ2D(p->zi, (cufftDoubleComplex*)p->Amix, p->grid_tmp + (size_t)o * p->n_grid) != CUFFT_SUCCESS)
       return fail(HS_ERR_CUDA, "cuFFT z Z2D failed");
   }
   if (o1 < p->n_out) return HS_OK;

@@ -11,5 +11,5 @@ echo "pytest rc=$?" >> $out/pytest_gpu.log
 python bench.py --gpus 1 --steps 20 --warmup 5 > $out/bench.json 2> $out/bench.err
 python bench.py --impl reference --gpus 1 --steps 20 --warmup 5 > $out/bench_ref.json 2> $out/bench_ref.err
 bash tools/reference_suite.sh run $out
-bash tools/ncu_round.sh ${1:-final}/ncu "k_pair_q|k_gather8|k_spread_mma4|k_xreg|k_mirror_z"
+bash tools/ncu_round.sh ${1:-final}/ncu
 du -sh gpurun_out
