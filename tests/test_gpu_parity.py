@@ -401,6 +401,21 @@ def test_register_fft_stages_match_alternatives(tmp_path, kind, M, alt):
     assert rel_l2(ua, ub) < 1e-12
 
 
+def test_register_z_stage_free_space_matches_cufft(tmp_path):
+    """The register z stage with 3 output channels (free space: pitch-4 interleave) and nz = 428 < 432
+    (M = 404 -> padded z length 924) against the cuFFT z stage + interleave pass."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    tool = os.path.join(root, "tools", "xstage_ab.py")
+    a, b = tmp_path / "reg.npy", tmp_path / "cufft.npy"
+    subprocess.run([sys.executable, tool, str(a), "free", "404"], check=True)
+    subprocess.run([sys.executable, tool, str(b), "free", "404"], check=True, env=dict(os.environ, HS_ZSTAGE_CUFFT="1"))
+    ua, ub = np.load(a), np.load(b)
+    assert np.isfinite(ua).all() and rel_l2(ua, ub) < 1e-12
+
+
 @pytest.mark.parametrize("kind", ("harmonic", "biharmonic"))
 def test_separable_tables_match_full_grid(tmp_path, kind):
     """The separable pruned table precompute against the 3-D big-grid transform (each selected

@@ -12,6 +12,14 @@ from paper_1802_07844_b200.configs import WORKLOADS, make_system  # noqa: E402
 
 kind = sys.argv[2] if len(sys.argv) > 2 else "stokeslet"
 M = int(sys.argv[3]) if len(sys.argv) > 3 else 192
+if kind == "free":
+    # free space: 3 output channels (the z stage's pitch-4 interleave); M = 404 -> nz = 428, pz = 924
+    s0, _ = make_system("HL", n=20_000)
+    s = hs.PointSystem(kind="stokeslet", geometry="free", box_length=1.0, positions=s0.positions, f=s0.f)
+    g = hs.GridSpec(L=1.0, M=M, P=24, xi=0.26 * M, geometry="free")
+    assert g.padded_dims[2] == 924, g.padded_dims
+    np.save(sys.argv[1], hs.fourier_space_sum(s, g).velocities)
+    sys.exit(0)
 if M == 384:
     assert kind == "stokeslet"
     w = WORKLOADS["cfg5"]
