@@ -569,10 +569,11 @@ __global__ void __launch_bounds__(XR_THREADS, M == 27 ? 1 : 2) k_xreg(const XArg
   auto prefetch = [&](int it) {
     if (it < n_items) {
       const int ky2 = it / a.nzh, kz2 = it - ky2 * a.nzh;
-      const int tot = NIN * a.nx;
-      for (int i = tid; i < tot; i += blockDim.x) {
-        const int c = i / a.nx, x = i - c * a.nx;
-        cp_async16(&stage[i], a.B + c * a.ch_stride + ((int64_t)ky2 * a.nx + x) * a.nzh + kz2);
+      // (channel-major loop: no per-element integer division; nx <= N)
+      const double2* src = a.B + ((int64_t)ky2 * a.nx) * a.nzh + kz2;
+      for (int x = tid; x < a.nx; x += blockDim.x) {
+#pragma unroll
+        for (int c = 0; c < NIN; ++c) cp_async16(&stage[c * a.nx + x], src + c * a.ch_stride + (int64_t)x * a.nzh);
       }
     }
     cp_async_commit();
