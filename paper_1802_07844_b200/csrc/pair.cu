@@ -85,6 +85,9 @@ __device__ __forceinline__ double rcp_pos(double v) {
   return y;
 }
 #endif
+#ifndef PC_SPLIT_BARRIER
+#define PC_SPLIT_BARRIER 0  // restaging barrier as mbarrier arrive + evaluate-while-waiting
+#endif
 #ifndef PC_QPREFETCH
 #define PC_QPREFETCH 0  // full rounds: read the next round's queue entries during the current one
 #endif
@@ -407,6 +410,14 @@ __global__ void __launch_bounds__(PC_TG, pc_minb<KIND>()) k_pair_q(const PairArg
   __shared__ int run_beg[PT_MAXRUN];
   __shared__ int run_pre[PT_MAXRUN + 1];
   __shared__ int s_nrun;
+  __shared__ __align__(8) unsigned long long s_bar;  // PC_SPLIT_BARRIER: the restaging barrier
+  if (PC_SPLIT_BARRIER) {
+    if (threadIdx.x == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(&s_bar)), "r"(PC_TG));
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+  }
   __shared__ double2 s_erfcx[HS_ERFC_TABLE ? HS_ERFCX_NPAIR * HS_ERFCX_NINT : 1];
   if (HS_ERFC_TABLE)
     for (int i = threadIdx.x; i < HS_ERFCX_NPAIR * HS_ERFCX_NINT; i += blockDim.x) s_erfcx[i] = g_erfcx_coef[i];
@@ -588,7 +599,28 @@ __global__ void __launch_bounds__(PC_TG, pc_minb<KIND>()) k_pair_q(const PairArg
       while (__any_sync(0xffffffffu, tail > head && (q[head & (PC_Q - 1)][lane] >> PC_HSHIFT) == h)) {
         if (tail > head && (q[head & (PC_Q - 1)][lane] >> PC_HSHIFT) == h) pop_eval();
       }
+#if PC_SPLIT_BARRIER
+      // arrive, then evaluate queued pairs (two-pair rounds of the lanes that have them; their
+      // entries reference the other halves, which nobody restages now) until every warp has
+      // arrived: the wait for the slowest warp is spent on work that full rounds would do later
+      {
+        unsigned long long tok;
+        const unsigned bar = (unsigned)__cvta_generic_to_shared(&s_bar);
+        asm volatile("mbarrier.arrive.shared::cta.b64 %0, [%1];" : "=l"(tok) : "r"(bar) : "memory");
+        while (true) {
+          unsigned done;
+          asm volatile(
+              "{\n .reg .pred p;\n mbarrier.test_wait.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+              : "=r"(done)
+              : "r"(bar), "l"(tok)
+              : "memory");
+          if (__all_sync(0xffffffffu, done != 0)) break;
+          if (tail - head >= 2) pop_eval2();
+        }
+      }
+#else
       __syncthreads();
+#endif
 #pragma unroll
       for (int kk = 0; kk < PC_PER; ++kk) {
         const int j = threadIdx.x + kk * PC_TG;
