@@ -1160,7 +1160,7 @@ __device__ __forceinline__ void warp_fft462(double2* v, double2* S, const double
 constexpr int ZF_WARPS = 8, ZF_STAGE = 216;  // staged complex inputs per line (nz <= 432)
 __global__ void __launch_bounds__(ZF_WARPS * 32, 1)
     k_zfwd924(const double* __restrict__ in, double2* __restrict__ out, const double2* __restrict__ twg, int64_t nlines,
-              int nz) {
+              int nz, int mirror, double msign) {
   extern __shared__ double2 smem[];
   double2* tw = smem;                               // pd8-padded W462^i
   double2* twh = tw + padded_line(Z9_N2);           // W924^k, k <= 231
@@ -1193,7 +1193,18 @@ __global__ void __launch_bounds__(ZF_WARPS * 32, 1)
       if (j < 10) {
         const int n = lane + Z9_L * j;
         if (lane < Z9_L && n < nc) {
-          v[j] = stage[n];
+          if (mirror == 0) {
+            v[j] = stage[n];
+          } else {
+            // mirrored spreading fused in (plan.cu k_mirror_z): node k of the transformed line is
+            // S[k] + msign S[nz - k] (kernel channels, mirror = 1) or S[nz - k] (wall channels,
+            // mirror = 2); the mirror of node 0 lies outside the grid (0).  nz even here.
+            const double* sd = reinterpret_cast<const double*>(stage);
+            const int k0 = 2 * n, k1 = 2 * n + 1;
+            const double a0 = sd[k0], a1 = sd[k1];
+            const double b0 = k0 == 0 ? 0.0 : sd[nz - k0], b1 = sd[nz - k1];
+            v[j] = mirror == 1 ? make_double2(fma(msign, b0, a0), fma(msign, b1, a1)) : make_double2(b0, b1);
+          }
           if (2 * n + 1 >= nz) v[j].y = 0.0;  // odd nz: the last pair's second entry is padding
         }
       }
@@ -1308,7 +1319,11 @@ hs_status make_zstage_twiddles(double2* d_tw, cudaStream_t st) {
   return HS_OK;
 }
 // forward z of one channel: lines of pitch pz (nz nonzero values) -> nzh = 463 spectrum entries
-hs_status launch_zfwd(hs_ctx* ctx, const double* in, double2* out, const double2* tw, int64_t nlines, int nz) {
+// mirror: 0 plain; 1 / 2: the half-space reflection of a kernel / wall channel applied while
+// loading (nz even), msign = the kernel channel's image sign
+hs_status launch_zfwd(hs_ctx* ctx, const double* in, double2* out, const double2* tw, int64_t nlines, int nz,
+                      int mirror, double msign) {
+  if (mirror && (nz & 1)) return fail(HS_ERR_PARAMETER, "z stage: fused mirror needs an even nz");
   HS_TRY(z924_constants());
   const size_t smem = sizeof(double2) * (padded_line(Z9_N2) + 232 + (size_t)ZF_WARPS * (Z9_LS + ZF_STAGE));
   HS_CUDA(cudaFuncSetAttribute(k_zfwd924, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -1316,7 +1331,7 @@ hs_status launch_zfwd(hs_ctx* ctx, const double* in, double2* out, const double2
   HS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_zfwd924, ZF_WARPS * 32, smem));
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(nlines, ZF_WARPS),
                                                                (int64_t)ctx->sm_count * std::max(per_sm, 1)));
-  k_zfwd924<<<grid, ZF_WARPS * 32, smem, ctx->stream>>>(in, out, tw, nlines, nz);
+  k_zfwd924<<<grid, ZF_WARPS * 32, smem, ctx->stream>>>(in, out, tw, nlines, nz, mirror, msign);
   HS_LAUNCHED(ctx);
   return HS_OK;
 }

@@ -371,6 +371,7 @@ struct hs_plan {
   int cur_tcol_identity = 0;
   bool pair_timed = false, spread_timed = false, gather_timed = false;
   bool mirror = false;          // half space: spread the N sources once and mirror (k_mirror_z)
+  bool mirror_in_z = false;     // the reflection is applied by the register z stage while loading (no k_mirror_z pass)
   // concurrent real-space / Fourier pipelines (hs_plan_execute): the Fourier side runs on its
   // own high-priority stream with its own sort buffers, joined before the gather
   cudaStream_t st_four = nullptr;
@@ -601,6 +602,9 @@ static hs_status plan_create_impl(hs_ctx* ctx, const hs_params* prm, const hs_sl
     // the all-to-all, so each is inverse-transformed on its own and interleaved at the end)
     const bool zreg = zstage_supported((int)pz, (int)prm->dims[2]) && !getenv("HS_ZSTAGE_CUFFT");
     if (zreg) A_(zstage_twiddle_count(), p->ztw);
+    // single-GPU plans: the forward z stage applies the half-space reflection while loading
+    // (slab plans exchange ghost planes of the reflected grids, so they keep the k_mirror_z pass)
+    p->mirror_in_z = p->mirror && zreg && !sl && (prm->dims[2] % 2 == 0);
     if (zreg && !sl) {
     } else if (mixed && !sl && p->sg_cap >= p->n_out) {
       p->grid_tmp = p->grid_in;  // the source grids are dead once forward-transformed
@@ -1216,7 +1220,7 @@ hs_status stage_spread_group(hs_plan* p, int gi) {
     HS_CUDA(cudaEventRecord(p->ev[11], st));
     HS_TRY(launch_spread(ctx, p->SPk, p->SWk + c0, p->n_sel_k, cn, p->bk_start, p->gg, p->grid_in, p->n_in,
                          p->ngroup > 1));
-    if (p->mirror) {
+    if (p->mirror && !p->mirror_in_z) {
       const int64_t lines = (int64_t)p->gg.dims[1] * p->gg.dims[0];
       const int nz = p->gg.dims[2];
       k_mirror_z<<<grid_size(ctx, lines * (nz / 2 + 1) * cn), 256, 0, st>>>(
@@ -1250,11 +1254,13 @@ hs_status stage_spread_mirrored(hs_plan* p) {
   HS_CUDA(cudaEventRecord(p->ev[11], st));
   const int cn = p->group_c0[1];
   HS_TRY(launch_spread(ctx, p->SPk, p->SWk, n_sel, cn, p->bk_start, p->gg, p->grid_in, p->n_in));
-  const int64_t lines = (int64_t)p->gg.dims[1] * p->gg.dims[0];
-  const int nz = p->gg.dims[2];
-  k_mirror_z<<<grid_size(ctx, lines * (nz / 2 + 1) * cn), 256, 0, st>>>(
-      p->grid_in, cn, p->kern_mask, p->sigma_mask, p->gg.ch_stride, lines, p->kg.p[2], nz);
-  HS_LAUNCHED(ctx);
+  if (!p->mirror_in_z) {
+    const int64_t lines = (int64_t)p->gg.dims[1] * p->gg.dims[0];
+    const int nz = p->gg.dims[2];
+    k_mirror_z<<<grid_size(ctx, lines * (nz / 2 + 1) * cn), 256, 0, st>>>(
+        p->grid_in, cn, p->kern_mask, p->sigma_mask, p->gg.ch_stride, lines, p->kg.p[2], nz);
+    HS_LAUNCHED(ctx);
+  }
   HS_CUDA(cudaEventRecord(p->ev[12], st));
   p->spread_timed = true;
   return HS_OK;
@@ -1493,8 +1499,11 @@ extern "C" hs_status hs_plan_execute(hs_plan* p, const double* positions, const 
       if (gi > 0) HS_TRY(stage_spread_group(p, gi));
       for (int c = p->group_c0[gi]; c < p->group_c0[gi + 1]; ++c) {
         const double* gin = p->grid_in + (size_t)(c - p->group_c0[gi]) * p->n_grid;
-        if (p->ztw)
-          HS_TRY(launch_zfwd(ctx, gin, p->Amix, p->ztw, (int64_t)p->gg.dims[1] * p->gg.dims[0], p->gg.dims[2]));
+        if (p->ztw) {
+          const int mir = !p->mirror_in_z ? 0 : (((p->kern_mask >> c) & 1u) ? 1 : 2);
+          HS_TRY(launch_zfwd(ctx, gin, p->Amix, p->ztw, (int64_t)p->gg.dims[1] * p->gg.dims[0], p->gg.dims[2], mir,
+                             ((p->sigma_mask >> c) & 1u) ? -1.0 : 1.0));
+        }
         else if (cufftExecD2Z(p->zf, (double*)gin, (cufftDoubleComplex*)p->Amix) != CUFFT_SUCCESS)
           return fail(HS_ERR_CUDA, "cuFFT z D2Z failed");
         HS_TRY(stage_yfwd(p, p->Amix, c));
