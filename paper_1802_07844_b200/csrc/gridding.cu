@@ -100,7 +100,7 @@ struct WTab {                              // row layout of one source (doubles)
 };
 
 __global__ void k_spread_wtab(const double4* __restrict__ pts, int n, GridGeom g, WTab wt, int4* __restrict__ lo,
-                              double* __restrict__ tab) {
+                              double* __restrict__ tab, int zlo_min, unsigned* __restrict__ flags) {
   // one warp per (source, axis) row; lanes write consecutive entries (coalesced)
   const int P = g.P;
   const int lane = threadIdx.x & 31;
@@ -124,8 +124,13 @@ __global__ void k_spread_wtab(const double4* __restrict__ pts, int n, GridGeom g
       }
       row[j] = v;
     }
-    if (k == 0 && lane == 0)
-      lo[s] = make_int4((int)l, (int)g_lo(g, 1, p.y), (int)g_lo(g, 2, p.z), 0);
+    if (k == 0 && lane == 0) {
+      const int lz = (int)g_lo(g, 2, p.z);
+      lo[s] = make_int4((int)l, (int)g_lo(g, 1, p.y), lz, 0);
+      // a window below the first launched z tile (a source at or below the wall of a mirrored
+      // half-space plan) would be dropped silently: flag it like a window leaving the grid
+      if (lz < zlo_min) atomicOr(flags, FLAG_OUT_OF_GRID);
+    }
   }
 }
 
@@ -211,7 +216,7 @@ __global__ void __launch_bounds__((NCW + SW_NP) * 32, NCW == 8 ? 2 : 1) k_spread
                                                        WTab wt, const double4* __restrict__ pts,
                                                        const double* __restrict__ w, int ldw,
                                                        const int* __restrict__ bin_start, GridGeom g, int nbx,
-                                                       int nby, int nbz, double* __restrict__ grids) {
+                                                       int nby, int nbz, double* __restrict__ grids, int tz0) {
   constexpr int RX = SW_RX, RY = SW_RY, RZ = SW_RZ, RQ = SwBuf<NCH>::RQ, PER = SwBuf<NCH>::DOUBLES;
   extern __shared__ __align__(16) double sm_dyn[];
   constexpr int K = NCW == 16 ? 16 * 32 / SW_CH : SW_K;  // ring depth (16 slots of 32 sources)
@@ -231,19 +236,22 @@ __global__ void __launch_bounds__((NCW + SW_NP) * 32, NCW == 8 ? 2 : 1) k_spread
   // columns, z fastest.  Consecutively launched tiles then share their candidate bins (a source's
   // window rows are re-read by the ~25 tiles its support touches): the live set is 3 y-columns x
   // (SP_STRIP + 2) x-columns of sources, which the L2 holds, instead of whole x-slabs.
+  // (only the z tiles tz0 .. nbz - 1 are launched: a mirrored half-space plan never spreads below
+  // the wall, and its forward z stage reads those nodes as the zeros they were allocated with)
   int tx, ty, tz;
+  const int nzl = nbz - tz0;  // launched z tiles per column
   if (SP_STRIP > 0) {
-    const int per_strip = SP_STRIP * nby * nbz;
+    const int per_strip = SP_STRIP * nby * nzl;
     const int sidx = blockIdx.x / per_strip, r = blockIdx.x - sidx * per_strip;
     const int kk = min(SP_STRIP, nbx - sidx * SP_STRIP);  // width of this strip
-    ty = r / (kk * nbz);
-    const int r2 = r - ty * kk * nbz;
-    tx = sidx * SP_STRIP + r2 / nbz;
-    tz = r2 - (r2 / nbz) * nbz;
+    ty = r / (kk * nzl);
+    const int r2 = r - ty * kk * nzl;
+    tx = sidx * SP_STRIP + r2 / nzl;
+    tz = tz0 + r2 - (r2 / nzl) * nzl;
   } else {
-    tz = blockIdx.x % nbz;
-    ty = (blockIdx.x / nbz) % nby;
-    tx = blockIdx.x / (nbz * nby);
+    tz = tz0 + blockIdx.x % nzl;
+    ty = (blockIdx.x / nzl) % nby;
+    tx = blockIdx.x / (nzl * nby);
   }
   const int x0 = tx * SP_TX, y0 = ty * SP_TY, z0 = tz * SP_TZ;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -507,7 +515,7 @@ __global__ void __launch_bounds__((NCW + SW_NP) * 32, NCW == 8 ? 2 : 1) k_spread
 }
 
 hs_status launch_spread(hs_ctx* ctx, const double4* pts, const double* w, int n, int nch, const int* bin_start,
-                        const GridGeom& g, double* grids, int ldw, bool reuse_wtab) {
+                        const GridGeom& g, double* grids, int ldw, bool reuse_wtab, int tz_begin) {
   if (ldw <= 0) ldw = nch;  // weights row stride (a channel group of wider rows: ldw > nch)
   if (g.P > SP_MAXP) return fail(HS_ERR_PARAMETER, "spread supports window support P <= 64");
   const int nbx = sp_nbins(g, 0), nby = sp_nbins(g, 1), nbz = sp_nbins(g, 2);
@@ -519,10 +527,12 @@ hs_status launch_spread(hs_ctx* ctx, const double4* pts, const double* w, int n,
   double* tab = (double*)(lo + nn);
   if (n > 0 && !reuse_wtab) {  // (reuse: same sources, tables of the previous call intact)
     const int gs = (int)std::min<int64_t>(ceil_div((int64_t)n * 3 * 32, 256), ctx->sm_count * 16);
-    k_spread_wtab<<<gs, 256, 0, ctx->stream>>>(pts, n, g, wt, lo, tab);
+    k_spread_wtab<<<gs, 256, 0, ctx->stream>>>(pts, n, g, wt, lo, tab,
+                                               std::max(0, std::min(tz_begin, nbz - 1)) * SP_TZ, ctx->d_flags);
     HS_LAUNCHED(ctx);
   }
-  dim3 grid(nbx * nby * nbz);
+  const int tz0 = std::max(0, std::min(tz_begin, nbz - 1));
+  dim3 grid(nbx * nby * (nbz - tz0));
   if (nch >= 3) {
     // 16 consumer warps (4x4 patches), up to 7 channels per launch, groups balanced
     // (7 -> 7, 13 -> 7 + 6, 19 -> 7 + 6 + 6)
@@ -537,7 +547,7 @@ hs_status launch_spread(hs_ctx* ctx, const double4* pts, const double* w, int n,
     const size_t smm = sizeof(double) * (16 * 32 / SW_CH) * SwBuf<N>::DOUBLES;                                 \
     HS_CUDA(cudaFuncSetAttribute(k_spread_mma4<N, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smm)); \
     k_spread_mma4<N, 16><<<grid, (16 + SW_NP) * 32, smm, ctx->stream>>>(lo, tab, wt, pts, wc0, ldw, bin_start, g, \
-                                                                        nbx, nby, nbz, gout);                 \
+                                                                        nbx, nby, nbz, gout, tz0);            \
   } break;
         HS_SP16(3) HS_SP16(4) HS_SP16(5) HS_SP16(6) HS_SP16(7)
 #undef HS_SP16
@@ -555,7 +565,7 @@ hs_status launch_spread(hs_ctx* ctx, const double4* pts, const double* w, int n,
     const size_t smm = sizeof(double) * SW_K * SwBuf<N>::DOUBLES;                                            \
     HS_CUDA(cudaFuncSetAttribute(k_spread_mma4<N, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smm)); \
     k_spread_mma4<N, 8><<<grid, SW_THREADS, smm, ctx->stream>>>(lo, tab, wt, pts, w, ldw, bin_start, g, nbx, nby, \
-                                                               nbz, grids);                                  \
+                                                               nbz, grids, tz0);                             \
   } break;
     HS_SP8(1) HS_SP8(2)
 #undef HS_SP8

@@ -70,7 +70,7 @@ hs_status launch_grid_keys(hs_ctx* ctx, const double* pos, int n_src, int n_tota
 // sorted spread: pts/weights already in bin order; bin_start[nbins+1]
 hs_status launch_spread(hs_ctx* ctx, const double4* pts, const double* w, int n, int nch,
                         const int* bin_start, const GridGeom& g, double* grids, int ldw = 0,
-                        bool reuse_wtab = false);
+                        bool reuse_wtab = false, int tz_begin = 0);  // tz_begin: first z tile launched
 // gather: nch channels (<= 8) at n points (any order); out[i*ldo + ch] (times h^3 * scale)
 hs_status launch_gather(hs_ctx* ctx, const double4* pts, const int* perm, int n, int nch,
                         const GridGeom& g, const double* grids, double* out, int ldo, double scale);

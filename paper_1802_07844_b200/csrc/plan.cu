@@ -372,6 +372,7 @@ struct hs_plan {
   bool pair_timed = false, spread_timed = false, gather_timed = false;
   bool mirror = false;          // half space: spread the N sources once and mirror (k_mirror_z)
   bool mirror_in_z = false;     // the reflection is applied by the register z stage while loading (no k_mirror_z pass)
+  int spread_tz0 = 0;           // mirror_in_z: first z tile the spread launches (nodes below stay zero)
   // concurrent real-space / Fourier pipelines (hs_plan_execute): the Fourier side runs on its
   // own high-priority stream with its own sort buffers, joined before the gather
   cudaStream_t st_four = nullptr;
@@ -605,6 +606,10 @@ static hs_status plan_create_impl(hs_ctx* ctx, const hs_params* prm, const hs_sl
     // single-GPU plans: the forward z stage applies the half-space reflection while loading
     // (slab plans exchange ghost planes of the reflected grids, so they keep the k_mirror_z pass)
     p->mirror_in_z = p->mirror && zreg && !sl && (prm->dims[2] % 2 == 0);
+    // sources lie above the wall (node nz / 2), so no window starts below nz/2 - P/2 (one node of
+    // margin): those tiles are not launched; their nodes keep the zeros the grids were allocated
+    // with (nothing else writes them once the mirror pass is gone)
+    if (p->mirror_in_z) p->spread_tz0 = (int)std::max<int64_t>(0, (prm->dims[2] / 2 - prm->P / 2 - 1) / SP_TZ);
     if (zreg && !sl) {
     } else if (mixed && !sl && p->sg_cap >= p->n_out) {
       p->grid_tmp = p->grid_in;  // the source grids are dead once forward-transformed
@@ -1219,7 +1224,7 @@ hs_status stage_spread_group(hs_plan* p, int gi) {
   if (gi > 0) {
     HS_CUDA(cudaEventRecord(p->ev[11], st));
     HS_TRY(launch_spread(ctx, p->SPk, p->SWk + c0, p->n_sel_k, cn, p->bk_start, p->gg, p->grid_in, p->n_in,
-                         p->ngroup > 1));
+                         p->ngroup > 1, p->spread_tz0));
     if (p->mirror && !p->mirror_in_z) {
       const int64_t lines = (int64_t)p->gg.dims[1] * p->gg.dims[0];
       const int nz = p->gg.dims[2];
@@ -1253,7 +1258,8 @@ hs_status stage_spread_mirrored(hs_plan* p) {
   }
   HS_CUDA(cudaEventRecord(p->ev[11], st));
   const int cn = p->group_c0[1];
-  HS_TRY(launch_spread(ctx, p->SPk, p->SWk, n_sel, cn, p->bk_start, p->gg, p->grid_in, p->n_in));
+  HS_TRY(launch_spread(ctx, p->SPk, p->SWk, n_sel, cn, p->bk_start, p->gg, p->grid_in, p->n_in, false,
+                       p->spread_tz0));
   if (!p->mirror_in_z) {
     const int64_t lines = (int64_t)p->gg.dims[1] * p->gg.dims[0];
     const int nz = p->gg.dims[2];
