@@ -1160,7 +1160,7 @@ __device__ __forceinline__ void warp_fft462(double2* v, double2* S, const double
 constexpr int ZF_WARPS = 8, ZF_STAGE = 216;  // staged complex inputs per line (nz <= 432)
 __global__ void __launch_bounds__(ZF_WARPS * 32, 1)
     k_zfwd924(const double* __restrict__ in, double2* __restrict__ out, const double2* __restrict__ twg, int64_t nlines,
-              int nz, int mirror, double msign) {
+              int nz, int mirror, double msign, int n0) {
   extern __shared__ double2 smem[];
   double2* tw = smem;                               // pd8-padded W462^i
   double2* twh = tw + padded_line(Z9_N2);           // W924^k, k <= 231
@@ -1177,10 +1177,12 @@ __global__ void __launch_bounds__(ZF_WARPS * 32, 1)
   auto prefetch = [&](int64_t line) {
     if (line < nlines) {
       const double2* src = reinterpret_cast<const double2*>(in + line * Z9_PZ);
-      for (int n = lane; n < nc; n += 32) cp_async16(&stage[n], &src[n]);
+      for (int n = n0 + lane; n < nc; n += 32) cp_async16(&stage[n], &src[n]);
     }
     cp_async_commit();
   };
+  // complex inputs below n0 are known zeros (never written by the spread): not loaded
+  for (int n = lane; n < n0; n += 32) stage[n] = make_double2(0.0, 0.0);
   int64_t line = (int64_t)blockIdx.x * ZF_WARPS + warp;
   prefetch(line);
   for (; line < nlines; line += lstep) {
@@ -1321,8 +1323,9 @@ hs_status make_zstage_twiddles(double2* d_tw, cudaStream_t st) {
 // forward z of one channel: lines of pitch pz (nz nonzero values) -> nzh = 463 spectrum entries
 // mirror: 0 plain; 1 / 2: the half-space reflection of a kernel / wall channel applied while
 // loading (nz even), msign = the kernel channel's image sign
+// zero_below: nodes k < zero_below of every line are known to be zero and are not read
 hs_status launch_zfwd(hs_ctx* ctx, const double* in, double2* out, const double2* tw, int64_t nlines, int nz,
-                      int mirror, double msign) {
+                      int mirror, double msign, int zero_below) {
   if (mirror && (nz & 1)) return fail(HS_ERR_PARAMETER, "z stage: fused mirror needs an even nz");
   HS_TRY(z924_constants());
   const size_t smem = sizeof(double2) * (padded_line(Z9_N2) + 232 + (size_t)ZF_WARPS * (Z9_LS + ZF_STAGE));
@@ -1331,7 +1334,8 @@ hs_status launch_zfwd(hs_ctx* ctx, const double* in, double2* out, const double2
   HS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_zfwd924, ZF_WARPS * 32, smem));
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(nlines, ZF_WARPS),
                                                                (int64_t)ctx->sm_count * std::max(per_sm, 1)));
-  k_zfwd924<<<grid, ZF_WARPS * 32, smem, ctx->stream>>>(in, out, tw, nlines, nz, mirror, msign);
+  k_zfwd924<<<grid, ZF_WARPS * 32, smem, ctx->stream>>>(in, out, tw, nlines, nz, mirror, msign,
+                                                        std::max(0, std::min(zero_below, nz)) / 2);
   HS_LAUNCHED(ctx);
   return HS_OK;
 }

@@ -185,7 +185,7 @@ bool zstage_supported(int pz, int nz);
 int zstage_twiddle_count();
 hs_status make_zstage_twiddles(double2* d_tw, cudaStream_t st);
 hs_status launch_zfwd(hs_ctx* ctx, const double* in, double2* out, const double2* tw, int64_t nlines, int nz,
-                      int mirror = 0, double msign = 1.0);
+                      int mirror = 0, double msign = 1.0, int zero_below = 0);
 hs_status launch_zinv_interleaved(hs_ctx* ctx, const double2* spec, int64_t ch_stride, int n_out, int pitch,
                                   double* gout, const double2* tw, int64_t nlines, int nz);
 // kz columns [kz0, kz0 + nzl) only (a y-slab plan's share; full table: kz0 = 0, nzl = nzh)

@@ -1508,7 +1508,7 @@ extern "C" hs_status hs_plan_execute(hs_plan* p, const double* positions, const 
         if (p->ztw) {
           const int mir = !p->mirror_in_z ? 0 : (((p->kern_mask >> c) & 1u) ? 1 : 2);
           HS_TRY(launch_zfwd(ctx, gin, p->Amix, p->ztw, (int64_t)p->gg.dims[1] * p->gg.dims[0], p->gg.dims[2], mir,
-                             ((p->sigma_mask >> c) & 1u) ? -1.0 : 1.0));
+                             ((p->sigma_mask >> c) & 1u) ? -1.0 : 1.0, p->spread_tz0 * SP_TZ));
         }
         else if (cufftExecD2Z(p->zf, (double*)gin, (cufftDoubleComplex*)p->Amix) != CUFFT_SUCCESS)
           return fail(HS_ERR_CUDA, "cuFFT z D2Z failed");
