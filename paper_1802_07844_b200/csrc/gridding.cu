@@ -678,6 +678,9 @@ hs_status launch_gather(hs_ctx* ctx, const double4* pts, const int* perm, int n,
 // per barrier; each warp contracts the staged columns with its run's window factors on the
 // FP64 tensor pipe (see k_gather8).  The x/y factors of a run live in warp-private tables.
 // Windows are evaluated directly, exp(-alpha d^2), as in the reference (_gridding.py:21-30).
+#ifndef G8_BPIPE
+#define G8_BPIPE 0  // gather: load k-step sk + 1's B fragments before k-step sk's DMMAs
+#endif
 #ifndef G7_STEP_DEF
 #define G7_STEP_DEF 4
 #endif
@@ -926,6 +929,26 @@ __global__ void __launch_bounds__(G7_WARPS * 32) k_gather8(const double4* __rest
       double d[NCP][2];
 #pragma unroll
       for (int cp = 0; cp < NCP; ++cp) d[cp][0] = d[cp][1] = 0.0;
+#if G8_BPIPE
+      // B fragments of k-step sk + 1 are loaded (unconditionally: the node index is clamped into
+      // the staged range) before k-step sk's DMMAs issue, so the shared-memory latency of one
+      // k-step hides behind the previous one's tensor work
+      double bq[2][NCP];
+      auto load_b = [&](int sk, double* dst) {
+        const int zi = min(zoff + 4 * sk + fk, nzu - 1);
+#pragma unroll
+        for (int cp = 0; cp < NCP; ++cp) dst[cp] = bval ? bcol[zi * PITCH + 2 * cp] : 0.0;
+      };
+      load_b(0, bq[0]);
+#pragma unroll
+      for (int sk = 0; sk < 8; ++sk) {
+        if (sk + 1 < 8) load_b(sk + 1, bq[(sk + 1) & 1]);
+        if (sk < nks) {  // warp-uniform
+#pragma unroll
+          for (int cp = 0; cp < NCP; ++cp) dmma_884(d[cp][0], d[cp][1], a[sk], bq[sk & 1][cp]);
+        }
+      }
+#else
 #pragma unroll
       for (int sk = 0; sk < 8; ++sk) {
         if (sk < nks) {  // warp-uniform
@@ -937,6 +960,7 @@ __global__ void __launch_bounds__(G7_WARPS * 32) k_gather8(const double4* __rest
           }
         }
       }
+#endif
       // epilogue: D[ft][2 fk + j] belongs to column fk of the step, channels 2 cp + j
       double w = 0.0;
       if (fk < ncols && colD < ncol) {
