@@ -1040,15 +1040,16 @@ hs_status launch_ystage(hs_ctx* ctx, bool fwd, const double2* in, double2* out, 
   return fail(HS_ERR_PARAMETER, "y stage: unsupported length");
 }
 
-// ---- register z stage for pz = 924 (the metric configuration's padded z length) ------------
-// A real line of 924 points is the 462-point complex transform of z[n] = x[2n] + i x[2n+1] plus
-// one pass over (k, 462 - k) pairs.  462 = 22 x 21: lanes l < 22 hold z[l + 22 j] (j < 21), DFT21
-// (= 3 x DFT7) over j in registers, twiddle W462^{l k1}, one transpose through shared memory
-// (S[k1][l], rows of 23), then lanes r < 21 each take row r and finish with a DFT22 (= 2 x DFT11),
-// ending with Z[r + 21 k2] in natural order in the warp's scratch.
-//   forward (k_zfwd924, replaces the cuFFT D2Z): one warp per line; only the nz <= 432 nonzero
-//     inputs are read (the zero padding of the source grids is never touched), 463 outputs written;
-//   inverse (k_zinv924, replaces the cuFFT Z2D + k_interleave): a CTA takes LPC lines, one warp per
+// ---- register z stage for pz = 924 (the metric configuration) and 660 (cfg2 / cfg3) ---------
+// A real line of pz = 2 N2 points is the N2-point complex transform of z[n] = x[2n] + i x[2n+1] plus
+// one pass over (k, N2 - k) pairs.  N2 = 22 M (M = 21: 462; M = 15: 330): lanes l < 22 hold
+// z[l + 22 j] (j < M), DFT-M (21 = 3 x 7; 15 = 3 x 5) over j in registers, twiddle W_N2^{l k1}, one
+// transpose through shared memory (S[k1][l], rows of 23), then lanes r < M each take row r and
+// finish with a DFT22 (= 2 x DFT11), ending with Z[r + M k2] in natural order in the warp's scratch.
+//   forward (k_zfwd, replaces the cuFFT D2Z): one warp per line; only the nonzero inputs are read
+//     (the zero padding of the source grids is never touched), N2 + 1 outputs written; optionally
+//     applies the half-space reflection while loading (plan.cu k_mirror_z);
+//   inverse (k_zinv, replaces the cuFFT Z2D + k_interleave): a CTA takes LPC lines, one warp per
 //     (line, output channel); only the z < nz outputs are formed and they leave channel-interleaved
 //     ([z][pitch], one contiguous block per line) for the gather.
 // Unnormalised both ways, like cuFFT; the inverse ignores the imaginary parts of the k = 0 and
@@ -1119,58 +1120,72 @@ __device__ __forceinline__ void dft21(double2* v) {
   }
 }
 
-constexpr int Z9_N2 = 462, Z9_L = 22, Z9_M = 21, Z9_RS = 23, Z9_LS = Z9_M * Z9_RS;  // scratch >= 462
-constexpr int Z9_NZH = 463, Z9_PZ = 924;
-// forward DFT of the 462-point line with z[l + 22 j] in v[j] (lanes < 22); result Z[k] left in S[k].
-// NK2: number of DFT22 outputs per row needed (22: all; 11: only Z[k], k < 231)
-template <int NK2>
-__device__ __forceinline__ void warp_fft462(double2* v, double2* S, const double2* tw, int lane) {
-  if (lane < Z9_L) {
-    dft21(v);
+// geometry of the 22 x M scheme (M = 21: pz = 924; M = 15: pz = 660, DFT15 in registers)
+template <int M>
+struct ZR {
+  static constexpr int L = 22, RS = 23, N2 = L * M, LS = M * RS;  // scratch LS >= N2
+  static constexpr int NZH = N2 + 1, PZ = 2 * N2, KH = N2 / 2;    // KH: pairs (k, N2 - k), k <= KH
+  static constexpr int NQ = (KH + 32) / 32;                        // lane rounds over k <= KH
+};
+template <int M>
+__device__ __forceinline__ void dftZ(double2* v) {
+  static_assert(M == 21 || M == 15, "register z stage: pz = 924 (M = 21) or 660 (M = 15)");
+  if constexpr (M == 21) dft21(v);
+  else dft15(v);
+}
+// forward DFT of the 22 M-point line with z[l + 22 j] in v[j] (lanes < 22); result Z[k] left in S[k].
+// NK2: number of DFT22 outputs per row needed (22: all; 11: only Z[k], k < 11 M)
+template <int M, int NK2>
+__device__ __forceinline__ void warp_fft22(double2* v, double2* S, const double2* tw, int lane) {
+  if (lane < ZR<M>::L) {
+    dftZ<M>(v);
 #pragma unroll
-    for (int k1 = 1; k1 < Z9_M; ++k1) v[k1] = cm(v[k1], tw[pd8(lane * k1)]);
+    for (int k1 = 1; k1 < M; ++k1) v[k1] = cm(v[k1], tw[pd8(lane * k1)]);
   }
   __syncwarp();
-  if (lane < Z9_L) {
+  if (lane < ZR<M>::L) {
 #pragma unroll
-    for (int k1 = 0; k1 < Z9_M; ++k1) S[k1 * Z9_RS + lane] = v[k1];
+    for (int k1 = 0; k1 < M; ++k1) S[k1 * ZR<M>::RS + lane] = v[k1];
   }
   __syncwarp();
   double2 e[11], o[11];
-  const int rr = lane < Z9_M ? lane : Z9_M - 1;
+  const int rr = lane < M ? lane : M - 1;
 #pragma unroll
   for (int m = 0; m < 11; ++m) {
-    e[m] = S[rr * Z9_RS + 2 * m];
-    o[m] = S[rr * Z9_RS + 2 * m + 1];
+    e[m] = S[rr * ZR<M>::RS + 2 * m];
+    o[m] = S[rr * ZR<M>::RS + 2 * m + 1];
   }
   __syncwarp();
   dft11(e);
   dft11(o);
-  if (lane < Z9_M) {
+  if (lane < M) {
 #pragma unroll
     for (int k = 0; k < 11; ++k) {
       const double2 t = k == 0 ? o[0] : cm(o[k], c_w22[k]);
-      S[lane + Z9_M * k] = ad(e[k], t);
-      if (NK2 > 11) S[lane + Z9_M * (k + 11)] = sb(e[k], t);
+      S[lane + M * k] = ad(e[k], t);
+      if (NK2 > 11) S[lane + M * (k + 11)] = sb(e[k], t);
     }
   }
   __syncwarp();
 }
 
-constexpr int ZF_WARPS = 8, ZF_STAGE = 216;  // staged complex inputs per line (nz <= 432)
+constexpr int ZF_WARPS = 8;
+template <int M>
 __global__ void __launch_bounds__(ZF_WARPS * 32, 1)
-    k_zfwd924(const double* __restrict__ in, double2* __restrict__ out, const double2* __restrict__ twg, int64_t nlines,
+    k_zfwd(const double* __restrict__ in, double2* __restrict__ out, const double2* __restrict__ twg, int64_t nlines,
               int nz, int mirror, double msign, int n0) {
+  constexpr int Z9_N2 = ZR<M>::N2, Z9_L = ZR<M>::L, Z9_M = M, Z9_LS = ZR<M>::LS, Z9_NZH = ZR<M>::NZH, Z9_PZ = ZR<M>::PZ,
+                ZF_STAGE = ZR<M>::KH, KH = ZR<M>::KH;
   extern __shared__ double2 smem[];
-  double2* tw = smem;                               // pd8-padded W462^i
-  double2* twh = tw + padded_line(Z9_N2);           // W924^k, k <= 231
-  double2* S = twh + 232 + (threadIdx.x >> 5) * Z9_LS;
+  double2* tw = smem;                               // pd8-padded W_N2^i
+  double2* twh = tw + padded_line(Z9_N2);           // W_pz^k, k <= KH
+  double2* S = twh + KH + 1 + (threadIdx.x >> 5) * Z9_LS;
   // the warp's next line is prefetched (cp.async) into its staging row while the current one
   // is transformed, so the loads of one line overlap the arithmetic of the previous
-  double2* stage = twh + 232 + ZF_WARPS * Z9_LS + (threadIdx.x >> 5) * ZF_STAGE;
+  double2* stage = twh + KH + 1 + ZF_WARPS * Z9_LS + (threadIdx.x >> 5) * ZF_STAGE;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int i = threadIdx.x; i < Z9_N2; i += blockDim.x) tw[pd8(i)] = twg[i];
-  for (int i = threadIdx.x; i < 232; i += blockDim.x) twh[i] = twg[Z9_N2 + i];
+  for (int i = threadIdx.x; i <= KH; i += blockDim.x) twh[i] = twg[Z9_N2 + i];
   __syncthreads();
   const int nc = (nz + 1) >> 1;  // nonzero complex inputs (nz <= 432 -> <= 216 -> j <= 9)
   const int64_t lstep = (int64_t)gridDim.x * ZF_WARPS;
@@ -1192,7 +1207,7 @@ __global__ void __launch_bounds__(ZF_WARPS * 32, 1)
 #pragma unroll
     for (int j = 0; j < Z9_M; ++j) {
       v[j] = make_double2(0.0, 0.0);
-      if (j < 10) {
+      if (Z9_L * j < KH) {
         const int n = lane + Z9_L * j;
         if (lane < Z9_L && n < nc) {
           if (mirror == 0) {
@@ -1213,14 +1228,14 @@ __global__ void __launch_bounds__(ZF_WARPS * 32, 1)
     }
     __syncwarp();
     prefetch(line + lstep);
-    warp_fft462<22>(v, S, tw, lane);
-    // X[k] = E + W924^k O, X[462 - k] = conj(E - W924^k O); E = (Z[k] + conj Z[462-k]) / 2,
-    // O = (Z[k] - conj Z[462-k]) / (2 i)
+    warp_fft22<M, 22>(v, S, tw, lane);
+    // X[k] = E + W_pz^k O, X[N2 - k] = conj(E - W_pz^k O); E = (Z[k] + conj Z[N2-k]) / 2,
+    // O = (Z[k] - conj Z[N2-k]) / (2 i)
     double2* dst = out + line * Z9_NZH;
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
+    for (int q = 0; q < ZR<M>::NQ; ++q) {
       const int k = lane + 32 * q;
-      if (k <= 231) {
+      if (k <= KH) {
         const double2 zk = S[k], zm = S[k == 0 ? 0 : Z9_N2 - k];
         const double2 E = make_double2(0.5 * (zk.x + zm.x), 0.5 * (zk.y - zm.y));
         const double2 O = make_double2(0.5 * (zk.y + zm.y), -0.5 * (zk.x - zm.x));
@@ -1236,20 +1251,22 @@ __global__ void __launch_bounds__(ZF_WARPS * 32, 1)
 }
 
 // LPC lines per CTA, NOUT channels: warp w -> (line w / NOUT, channel w % NOUT)
-template <int NOUT, int PITCH, int LPC>
+template <int M, int NOUT, int PITCH, int LPC>
 __global__ void __launch_bounds__(NOUT * LPC * 32, 1)
-    k_zinv924(const double2* __restrict__ spec, int64_t ch_stride, double* __restrict__ gout,
+    k_zinv(const double2* __restrict__ spec, int64_t ch_stride, double* __restrict__ gout,
               const double2* __restrict__ twg, int64_t nlines, int nz) {
+  constexpr int Z9_N2 = ZR<M>::N2, Z9_L = ZR<M>::L, Z9_M = M, Z9_LS = ZR<M>::LS, Z9_NZH = ZR<M>::NZH, Z9_PZ = ZR<M>::PZ,
+                KH = ZR<M>::KH;
   extern __shared__ double2 smem[];
   constexpr int NW = NOUT * LPC;
   double2* tw = smem;
   double2* twh = tw + padded_line(Z9_N2);
-  double2* S = twh + 232 + (threadIdx.x >> 5) * Z9_LS;
-  double* obuf = reinterpret_cast<double*>(twh + 232 + NW * Z9_LS);  // [LPC][nz][PITCH]
+  double2* S = twh + KH + 1 + (threadIdx.x >> 5) * Z9_LS;
+  double* obuf = reinterpret_cast<double*>(twh + KH + 1 + NW * Z9_LS);  // [LPC][nz][PITCH]
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int lc = warp / NOUT, c = warp - lc * NOUT;
   for (int i = threadIdx.x; i < Z9_N2; i += blockDim.x) tw[pd8(i)] = twg[i];
-  for (int i = threadIdx.x; i < 232; i += blockDim.x) twh[i] = twg[Z9_N2 + i];
+  for (int i = threadIdx.x; i <= KH; i += blockDim.x) twh[i] = twg[Z9_N2 + i];
   if (PITCH > NOUT)
     for (int i = threadIdx.x; i < LPC * nz * PITCH; i += blockDim.x) obuf[i] = 0.0;  // padding channels stay 0
   __syncthreads();
@@ -1258,12 +1275,12 @@ __global__ void __launch_bounds__(NOUT * LPC * 32, 1)
     const int64_t line = l0 + lc;
     if (line < nlines) {
       const double2* X = spec + (int64_t)c * ch_stride + line * Z9_NZH;
-      // conj(Z[k]), Z[k] = E[k] + i O[k], E = X[k] + conj X[462-k], O = (X[k] - conj X[462-k]) conj(W924^k);
-      // Z[462-k] = conj E + i conj O
+      // conj(Z[k]), Z[k] = E[k] + i O[k], E = X[k] + conj X[N2-k], O = (X[k] - conj X[N2-k]) conj(W_pz^k);
+      // Z[N2-k] = conj E + i conj O
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
+      for (int q = 0; q < ZR<M>::NQ; ++q) {
         const int k = lane + 32 * q;
-        if (k <= 231) {
+        if (k <= KH) {
           double2 xk = X[k], xm = X[Z9_N2 - k];
           if (k == 0) xk.y = xm.y = 0.0;
           const double2 E = make_double2(xk.x + xm.x, xk.y - xm.y);
@@ -1271,7 +1288,7 @@ __global__ void __launch_bounds__(NOUT * LPC * 32, 1)
           const double2 w = twh[k];
           const double2 O = make_double2(fma(D.x, w.x, D.y * w.y), fma(D.y, w.x, -D.x * w.y));  // D conj(w)
           // Z[k] = (E.x - O.y, E.y + O.x): conj -> (E.x - O.y, -E.y - O.x)
-          // Z[462-k] = (E.x + O.y, -E.y + O.x): conj -> (E.x + O.y, E.y - O.x)
+          // Z[N2-k] = (E.x + O.y, -E.y + O.x): conj -> (E.x + O.y, E.y - O.x)
           if (k > 0) S[Z9_N2 - k] = make_double2(E.x + O.y, E.y - O.x);
           S[k] = make_double2(E.x - O.y, -E.y - O.x);
         }
@@ -1281,10 +1298,10 @@ __global__ void __launch_bounds__(NOUT * LPC * 32, 1)
 #pragma unroll
       for (int j = 0; j < Z9_M; ++j) v[j] = lane < Z9_L ? S[lane + Z9_L * j] : make_double2(0.0, 0.0);
       __syncwarp();
-      warp_fft462<11>(v, S, tw, lane);  // z[n] = conj(S[n]), n < 231 >= nc
+      warp_fft22<M, 11>(v, S, tw, lane);  // z[n] = conj(S[n]), n < 11 M >= nc
       double* ob = obuf + (size_t)lc * nz * PITCH + c;
 #pragma unroll
-      for (int q = 0; q < 7; ++q) {
+      for (int q = 0; q < ZR<M>::NQ; ++q) {
         const int n = lane + 32 * q;
         if (n < nc) {
           const double2 f = S[n];
@@ -1306,46 +1323,54 @@ __global__ void __launch_bounds__(NOUT * LPC * 32, 1)
   }
 }
 
-bool zstage_supported(int pz, int nz) { return pz == Z9_PZ && nz <= 432 && nz % 2 == 0; }
-// twiddle table of the z stage: W462^i (462) then W924^k (k < 232)
-int zstage_twiddle_count() { return Z9_N2 + 232; }
-hs_status make_zstage_twiddles(double2* d_tw, cudaStream_t st) {
-  std::vector<double2> tw(Z9_N2 + 232);
+// (pz, nz) the register z stage handles: nz even, at most half the padded length
+static int zstage_m(int pz) { return pz == ZR<21>::PZ ? 21 : (pz == ZR<15>::PZ ? 15 : 0); }
+bool zstage_supported(int pz, int nz) { return zstage_m(pz) != 0 && nz <= pz / 2 && nz % 2 == 0; }
+// twiddle table of the z stage: W_{N2}^i (N2 = pz / 2 entries) then W_{pz}^k (k <= N2 / 2)
+int zstage_twiddle_count(int pz) { return pz / 2 + pz / 4 + 1; }
+hs_status make_zstage_twiddles(int pz, double2* d_tw, cudaStream_t st) {
+  const int n2 = pz / 2, kh = n2 / 2;
+  std::vector<double2> tw(n2 + kh + 1);
   const long double tp = 6.283185307179586476925286766559005768L;
-  for (int j = 0; j < Z9_N2; ++j)
-    tw[j] = make_double2((double)std::cos(tp * j / Z9_N2), (double)-std::sin(tp * j / Z9_N2));
-  for (int j = 0; j < 232; ++j)
-    tw[Z9_N2 + j] = make_double2((double)std::cos(tp * j / Z9_PZ), (double)-std::sin(tp * j / Z9_PZ));
+  for (int j = 0; j < n2; ++j) tw[j] = make_double2((double)std::cos(tp * j / n2), (double)-std::sin(tp * j / n2));
+  for (int j = 0; j <= kh; ++j) tw[n2 + j] = make_double2((double)std::cos(tp * j / pz), (double)-std::sin(tp * j / pz));
   HS_CUDA(cudaMemcpyAsync(d_tw, tw.data(), sizeof(double2) * tw.size(), cudaMemcpyHostToDevice, st));
   HS_CUDA(cudaStreamSynchronize(st));
   return HS_OK;
 }
-// forward z of one channel: lines of pitch pz (nz nonzero values) -> nzh = 463 spectrum entries
+// forward z of one channel: lines of pitch pz (nz nonzero values) -> nzh = pz / 2 + 1 spectrum entries
 // mirror: 0 plain; 1 / 2: the half-space reflection of a kernel / wall channel applied while
 // loading (nz even), msign = the kernel channel's image sign
 // zero_below: nodes k < zero_below of every line are known to be zero and are not read
-hs_status launch_zfwd(hs_ctx* ctx, const double* in, double2* out, const double2* tw, int64_t nlines, int nz,
-                      int mirror, double msign, int zero_below) {
-  if (mirror && (nz & 1)) return fail(HS_ERR_PARAMETER, "z stage: fused mirror needs an even nz");
-  HS_TRY(z924_constants());
-  const size_t smem = sizeof(double2) * (padded_line(Z9_N2) + 232 + (size_t)ZF_WARPS * (Z9_LS + ZF_STAGE));
-  HS_CUDA(cudaFuncSetAttribute(k_zfwd924, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+template <int M>
+static hs_status launch_zfwd_t(hs_ctx* ctx, const double* in, double2* out, const double2* tw, int64_t nlines, int nz,
+                               int mirror, double msign, int zero_below) {
+  const size_t smem = sizeof(double2) * (padded_line(ZR<M>::N2) + ZR<M>::KH + 1 + (size_t)ZF_WARPS * (ZR<M>::LS + ZR<M>::KH));
+  HS_CUDA(cudaFuncSetAttribute(k_zfwd<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 1;
-  HS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_zfwd924, ZF_WARPS * 32, smem));
+  HS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_zfwd<M>, ZF_WARPS * 32, smem));
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(nlines, ZF_WARPS),
                                                                (int64_t)ctx->sm_count * std::max(per_sm, 1)));
-  k_zfwd924<<<grid, ZF_WARPS * 32, smem, ctx->stream>>>(in, out, tw, nlines, nz, mirror, msign,
-                                                        std::max(0, std::min(zero_below, nz)) / 2);
+  k_zfwd<M><<<grid, ZF_WARPS * 32, smem, ctx->stream>>>(in, out, tw, nlines, nz, mirror, msign,
+                                                         std::max(0, std::min(zero_below, nz)) / 2);
   HS_LAUNCHED(ctx);
   return HS_OK;
 }
+hs_status launch_zfwd(hs_ctx* ctx, int pz, const double* in, double2* out, const double2* tw, int64_t nlines, int nz,
+                      int mirror, double msign, int zero_below) {
+  if (!zstage_supported(pz, nz)) return fail(HS_ERR_PARAMETER, "z stage: unsupported length");
+  if (mirror && (nz & 1)) return fail(HS_ERR_PARAMETER, "z stage: fused mirror needs an even nz");
+  HS_TRY(z924_constants());
+  return zstage_m(pz) == 21 ? launch_zfwd_t<21>(ctx, in, out, tw, nlines, nz, mirror, msign, zero_below)
+                            : launch_zfwd_t<15>(ctx, in, out, tw, nlines, nz, mirror, msign, zero_below);
+}
 // inverse z of all n_out channels (channel stride ch_stride in `spec`), outputs z < nz interleaved
 // into gout ([line][pz][pitch] storage, z < nz written)
-hs_status launch_zinv_interleaved(hs_ctx* ctx, const double2* spec, int64_t ch_stride, int n_out, int pitch,
-                                  double* gout, const double2* tw, int64_t nlines, int nz) {
-  HS_TRY(z924_constants());
+template <int M>
+static hs_status launch_zinv_t(hs_ctx* ctx, const double2* spec, int64_t ch_stride, int n_out, int pitch, double* gout,
+                               const double2* tw, int64_t nlines, int nz) {
   auto go = [&](auto kern, int nw, int lpc) -> hs_status {
-    const size_t smem = sizeof(double2) * (padded_line(Z9_N2) + 232 + (size_t)nw * Z9_LS) +
+    const size_t smem = sizeof(double2) * (padded_line(ZR<M>::N2) + ZR<M>::KH + 1 + (size_t)nw * ZR<M>::LS) +
                         sizeof(double) * (size_t)lpc * nz * pitch;
     HS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 1;
@@ -1356,10 +1381,17 @@ hs_status launch_zinv_interleaved(hs_ctx* ctx, const double2* spec, int64_t ch_s
     HS_LAUNCHED(ctx);
     return HS_OK;
   };
-  if (n_out == 6 && pitch == 6) return go(k_zinv924<6, 6, 2>, 12, 2);
-  if (n_out == 3 && pitch == 4) return go(k_zinv924<3, 4, 4>, 12, 4);
-  if (n_out == 1 && pitch == 1) return go(k_zinv924<1, 1, 12>, 12, 12);  // one channel, not interleaved
+  if (n_out == 6 && pitch == 6) return go(k_zinv<M, 6, 6, 2>, 12, 2);
+  if (n_out == 3 && pitch == 4) return go(k_zinv<M, 3, 4, 4>, 12, 4);
+  if (n_out == 1 && pitch == 1) return go(k_zinv<M, 1, 1, 12>, 12, 12);  // one channel, not interleaved
   return fail(HS_ERR_PARAMETER, "z stage: unsupported channel layout");
+}
+hs_status launch_zinv_interleaved(hs_ctx* ctx, int pz, const double2* spec, int64_t ch_stride, int n_out, int pitch,
+                                  double* gout, const double2* tw, int64_t nlines, int nz) {
+  if (!zstage_supported(pz, nz)) return fail(HS_ERR_PARAMETER, "z stage: unsupported length");
+  HS_TRY(z924_constants());
+  return zstage_m(pz) == 21 ? launch_zinv_t<21>(ctx, spec, ch_stride, n_out, pitch, gout, tw, nlines, nz)
+                            : launch_zinv_t<15>(ctx, spec, ch_stride, n_out, pitch, gout, tw, nlines, nz);
 }
 
 template <int KIND, bool HALF, int KB, class FFT>

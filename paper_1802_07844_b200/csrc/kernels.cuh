@@ -180,13 +180,13 @@ hs_status launch_xfused(hs_ctx* ctx, int kind, int half, const XArgs& a);
 bool ystage_supported(int py);
 hs_status launch_ystage(hs_ctx* ctx, bool fwd, const double2* in, double2* out, const double2* tw, int py, int nx,
                         int nzh, int ny);
-// register z stage (pz = 924): forward replaces the cuFFT D2Z, inverse the cuFFT Z2D + channel interleave
+// register z stage (pz = 924 or 660): forward replaces the cuFFT D2Z, inverse the cuFFT Z2D + channel interleave
 bool zstage_supported(int pz, int nz);
-int zstage_twiddle_count();
-hs_status make_zstage_twiddles(double2* d_tw, cudaStream_t st);
-hs_status launch_zfwd(hs_ctx* ctx, const double* in, double2* out, const double2* tw, int64_t nlines, int nz,
+int zstage_twiddle_count(int pz);
+hs_status make_zstage_twiddles(int pz, double2* d_tw, cudaStream_t st);
+hs_status launch_zfwd(hs_ctx* ctx, int pz, const double* in, double2* out, const double2* tw, int64_t nlines, int nz,
                       int mirror = 0, double msign = 1.0, int zero_below = 0);
-hs_status launch_zinv_interleaved(hs_ctx* ctx, const double2* spec, int64_t ch_stride, int n_out, int pitch,
+hs_status launch_zinv_interleaved(hs_ctx* ctx, int pz, const double2* spec, int64_t ch_stride, int n_out, int pitch,
                                   double* gout, const double2* tw, int64_t nlines, int nz);
 // kz columns [kz0, kz0 + nzl) only (a y-slab plan's share; full table: kz0 = 0, nzl = nzh)
 hs_status launch_table_to_xmajor(hs_ctx* ctx, const double* in, int px, int py, int nzh, double* out, int kz0 = 0,

@@ -602,7 +602,7 @@ static hs_status plan_create_impl(hs_ctx* ctx, const hs_params* prm, const hs_sl
     // (y-slab plans keep the per-channel inverse buffer: their channels arrive one at a time from
     // the all-to-all, so each is inverse-transformed on its own and interleaved at the end)
     const bool zreg = zstage_supported((int)pz, (int)prm->dims[2]) && !getenv("HS_ZSTAGE_CUFFT");
-    if (zreg) A_(zstage_twiddle_count(), p->ztw);
+    if (zreg) A_(zstage_twiddle_count((int)pz), p->ztw);
     // single-GPU plans: the forward z stage applies the half-space reflection while loading
     // (slab plans exchange ghost planes of the reflected grids, so they keep the k_mirror_z pass)
     p->mirror_in_z = p->mirror && zreg && !sl && (prm->dims[2] % 2 == 0);
@@ -632,7 +632,7 @@ static hs_status plan_create_impl(hs_ctx* ctx, const hs_params* prm, const hs_sl
       A_(py, p->ytw);
       if ((st = make_twiddles((int)py, p->ytw, ctx->stream)) != HS_OK) return bail(st);
     }
-    if (p->ztw && (st = make_zstage_twiddles(p->ztw, ctx->stream)) != HS_OK) return bail(st);
+    if (p->ztw && (st = make_zstage_twiddles((int)pz, p->ztw, ctx->stream)) != HS_OK) return bail(st);
   }
   A_(3 * (size_t)std::max(nt, 1), p->u);
   A_(3 * (size_t)std::max(nt, 1), p->u_real, true);
@@ -1507,7 +1507,7 @@ extern "C" hs_status hs_plan_execute(hs_plan* p, const double* positions, const 
         const double* gin = p->grid_in + (size_t)(c - p->group_c0[gi]) * p->n_grid;
         if (p->ztw) {
           const int mir = !p->mirror_in_z ? 0 : (((p->kern_mask >> c) & 1u) ? 1 : 2);
-          HS_TRY(launch_zfwd(ctx, gin, p->Amix, p->ztw, (int64_t)p->gg.dims[1] * p->gg.dims[0], p->gg.dims[2], mir,
+          HS_TRY(launch_zfwd(ctx, p->kg.p[2], gin, p->Amix, p->ztw, (int64_t)p->gg.dims[1] * p->gg.dims[0], p->gg.dims[2], mir,
                              ((p->sigma_mask >> c) & 1u) ? -1.0 : 1.0, p->spread_tz0 * SP_TZ));
         }
         else if (cufftExecD2Z(p->zf, (double*)gin, (cufftDoubleComplex*)p->Amix) != CUFFT_SUCCESS)
@@ -1527,7 +1527,7 @@ extern "C" hs_status hs_plan_execute(hs_plan* p, const double* positions, const 
     }
     if (p->ztw) {
       // inverse z of all output channels, written channel-interleaved (z < nz) for the gather
-      HS_TRY(launch_zinv_interleaved(ctx, p->spec, (int64_t)p->n_mixed, p->n_out, p->out_pitch, p->grid_out, p->ztw,
+      HS_TRY(launch_zinv_interleaved(ctx, p->kg.p[2], p->spec, (int64_t)p->n_mixed, p->n_out, p->out_pitch, p->grid_out, p->ztw,
                                      (int64_t)p->gg.dims[1] * p->gg.dims[0], p->gg.dims[2]));
     } else {
       // channel-interleave the (y < ny, x < nx, z < nz) outputs for the broadcast gather
@@ -1740,7 +1740,7 @@ extern "C" hs_status hs_slab_forward_range(hs_plan* p, const double* ghost_in, d
   const int64_t rows = (int64_t)p->yo * nx;
   for (int c = c0; c < c1; ++c) {
     if (p->ztw)
-      HS_TRY(launch_zfwd(ctx, p->grid_in + (size_t)c * p->n_grid, p->Amix, p->ztw, rows, (int)nz));
+      HS_TRY(launch_zfwd(ctx, (int)pz, p->grid_in + (size_t)c * p->n_grid, p->Amix, p->ztw, rows, (int)nz));
     else if (cufftExecD2Z(p->zf, p->grid_in + (size_t)c * p->n_grid, (cufftDoubleComplex*)p->Amix) != CUFFT_SUCCESS)
       return fail(HS_ERR_CUDA, "cuFFT z D2Z failed");
     k_kz_exchange<<<grid_size(ctx, rows * p->kg.nzh), 256, 0, st>>>(
@@ -1805,7 +1805,7 @@ extern "C" hs_status hs_slab_backward_range(hs_plan* p, const double* recv_back,
         p->Amix, (double2*)recv_back + (size_t)o * p->n_amix, rows, p->kg.nzh, ks, 1);
     HS_LAUNCHED(ctx);
     if (p->ztw)  // one channel, plain lines of pitch pz (z < nz written; the padding stays zero)
-      HS_TRY(launch_zinv_interleaved(ctx, p->Amix, 0, 1, 1, p->grid_tmp + (size_t)o * p->n_grid, p->ztw, rows, (int)nz));
+      HS_TRY(launch_zinv_interleaved(ctx, (int)pz, p->Amix, 0, 1, 1, p->grid_tmp + (size_t)o * p->n_grid, p->ztw, rows, (int)nz));
     else if (cufftExecZ2D(p->zi, (cufftDoubleComplex*)p->Amix, p->grid_tmp + (size_t)o * p->n_grid) != CUFFT_SUCCESS)
       return fail(HS_ERR_CUDA, "cuFFT z Z2D failed");
   }
