@@ -193,9 +193,6 @@ static_assert(SW_K % SW_NP == 0, "ring slots must divide among the producers");
 #ifndef SP_STRIP
 #define SP_STRIP 2  // tile-order strip width in x (0: plain x-major order)
 #endif
-#ifndef SW_PREFETCH
-#define SW_PREFETCH 0  // 1: load group g + 1's operands before group g's DMMAs (spills at the 96-register cap: 18.3 vs 14.4 ms)
-#endif
 constexpr int SW_IDQ = 64;  // consumer id FIFO capacity (>= 3 leftovers + SW_CH hits, power of two)
 template <int NCH>
 struct SwBuf {
@@ -471,26 +468,11 @@ __global__ void __launch_bounds__((NCW + SW_NP) * 32, NCW == 8 ? 2 : 1) k_spread
       head = tail;
       mma(load_ops(gid));
     }
-#if SW_PREFETCH
-    if (tail - head >= 4) {
-      // operands of group g + 1 are loaded while group g's DMMAs issue
-      Ops cur = load_ops(ids[(head + kq) & (SW_IDQ - 1)]);
-      head += 4;
-      while (tail - head >= 4) {
-        const Ops nxt = load_ops(ids[(head + kq) & (SW_IDQ - 1)]);
-        head += 4;
-        mma(cur);
-        cur = nxt;
-      }
-      mma(cur);
-    }
-#else
     while (tail - head >= 4) {
       const int gid = ids[(head + kq) & (SW_IDQ - 1)];
       head += 4;
       mma(load_ops(gid));
     }
-#endif
     if (c > 0) mbar_arrive(&empty_bar[(c - 1) % K]);  // the previous chunk's leftovers are consumed
   }
   if (tail > head) mma(load_ops(head + kq < tail ? ids[(head + kq) & (SW_IDQ - 1)] : -1));
@@ -678,9 +660,6 @@ hs_status launch_gather(hs_ctx* ctx, const double4* pts, const int* perm, int n,
 // per barrier; each warp contracts the staged columns with its run's window factors on the
 // FP64 tensor pipe (see k_gather8).  The x/y factors of a run live in warp-private tables.
 // Windows are evaluated directly, exp(-alpha d^2), as in the reference (_gridding.py:21-30).
-#ifndef G8_BPIPE
-#define G8_BPIPE 0  // gather: load k-step sk + 1's B fragments before k-step sk's DMMAs
-#endif
 #ifndef G7_STEP_DEF
 #define G7_STEP_DEF 4
 #endif
@@ -929,26 +908,6 @@ __global__ void __launch_bounds__(G7_WARPS * 32) k_gather8(const double4* __rest
       double d[NCP][2];
 #pragma unroll
       for (int cp = 0; cp < NCP; ++cp) d[cp][0] = d[cp][1] = 0.0;
-#if G8_BPIPE
-      // B fragments of k-step sk + 1 are loaded (unconditionally: the node index is clamped into
-      // the staged range) before k-step sk's DMMAs issue, so the shared-memory latency of one
-      // k-step hides behind the previous one's tensor work
-      double bq[2][NCP];
-      auto load_b = [&](int sk, double* dst) {
-        const int zi = min(zoff + 4 * sk + fk, nzu - 1);
-#pragma unroll
-        for (int cp = 0; cp < NCP; ++cp) dst[cp] = bval ? bcol[zi * PITCH + 2 * cp] : 0.0;
-      };
-      load_b(0, bq[0]);
-#pragma unroll
-      for (int sk = 0; sk < 8; ++sk) {
-        if (sk + 1 < 8) load_b(sk + 1, bq[(sk + 1) & 1]);
-        if (sk < nks) {  // warp-uniform
-#pragma unroll
-          for (int cp = 0; cp < NCP; ++cp) dmma_884(d[cp][0], d[cp][1], a[sk], bq[sk & 1][cp]);
-        }
-      }
-#else
 #pragma unroll
       for (int sk = 0; sk < 8; ++sk) {
         if (sk < nks) {  // warp-uniform
@@ -960,7 +919,6 @@ __global__ void __launch_bounds__(G7_WARPS * 32) k_gather8(const double4* __rest
           }
         }
       }
-#endif
       // epilogue: D[ft][2 fk + j] belongs to column fk of the step, channels 2 cp + j
       double w = 0.0;
       if (fk < ncols && colD < ncol) {

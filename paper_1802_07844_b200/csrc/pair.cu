@@ -85,18 +85,6 @@ __device__ __forceinline__ double rcp_pos(double v) {
   return y;
 }
 #endif
-#ifndef PC_SPLIT_BARRIER
-#define PC_SPLIT_BARRIER 0  // restaging barrier as mbarrier arrive + evaluate-while-waiting
-#endif
-#ifndef PC_QPREFETCH
-#define PC_QPREFETCH 0  // full rounds: read the next round's queue entries during the current one
-#endif
-#ifndef PC_LN2_SINGLE
-#define PC_LN2_SINGLE 1  // exp: one ln2 constant in the range reduction (1 DFMA fewer; error <= |n| 5.5e-17, below 3e-15 wherever exp(x) > 1e-16)
-#endif
-#ifndef PC_SCAN4
-#define PC_SCAN4 0  // scan loop: 4 candidates per iteration (1) or 2 (0)
-#endif
 #ifndef PC_DRAIN2
 #define PC_DRAIN2 1   // queue drains by two-pair rounds where lanes have >= 2 entries
 #endif
@@ -140,12 +128,9 @@ __device__ __forceinline__ double exp_nonpos(double x) {
   const double t = fma(x, 1.4426950408889634, kShift);
   const double n = t - kShift;
   const int ni = __double2loint(t);
-#if PC_LN2_SINGLE
+  // one ln 2 constant: error <= |n| 5.5e-17, below 3e-15 wherever exp(x) > 1e-16 (one DFMA fewer
+  // than a hi / lo split)
   const double r = fma(n, -0.6931471805599453094, x);
-#else
-  double r = fma(n, -6.93147180369123816490e-01, x);  // ln2 hi (exact product for |n| < 2^11)
-  r = fma(n, -1.90821492927058770002e-10, r);         // ln2 lo
-#endif
   double p = c_exp_poly[0];
 #pragma unroll
   for (int j = 1; j < 12; ++j) p = fma(p, r, c_exp_poly[j]);
@@ -410,14 +395,6 @@ __global__ void __launch_bounds__(PC_TG, pc_minb<KIND>()) k_pair_q(const PairArg
   __shared__ int run_beg[PT_MAXRUN];
   __shared__ int run_pre[PT_MAXRUN + 1];
   __shared__ int s_nrun;
-  __shared__ __align__(8) unsigned long long s_bar;  // PC_SPLIT_BARRIER: the restaging barrier
-  if (PC_SPLIT_BARRIER) {
-    if (threadIdx.x == 0) {
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(&s_bar)), "r"(PC_TG));
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-  }
   __shared__ double2 s_erfcx[HS_ERFC_TABLE ? HS_ERFCX_NPAIR * HS_ERFCX_NINT : 1];
   if (HS_ERFC_TABLE)
     for (int i = threadIdx.x; i < HS_ERFCX_NPAIR * HS_ERFCX_NINT; i += blockDim.x) s_erfcx[i] = g_erfcx_coef[i];
@@ -599,28 +576,7 @@ __global__ void __launch_bounds__(PC_TG, pc_minb<KIND>()) k_pair_q(const PairArg
       while (__any_sync(0xffffffffu, tail > head && (q[head & (PC_Q - 1)][lane] >> PC_HSHIFT) == h)) {
         if (tail > head && (q[head & (PC_Q - 1)][lane] >> PC_HSHIFT) == h) pop_eval();
       }
-#if PC_SPLIT_BARRIER
-      // arrive, then evaluate queued pairs (two-pair rounds of the lanes that have them; their
-      // entries reference the other halves, which nobody restages now) until every warp has
-      // arrived: the wait for the slowest warp is spent on work that full rounds would do later
-      {
-        unsigned long long tok;
-        const unsigned bar = (unsigned)__cvta_generic_to_shared(&s_bar);
-        asm volatile("mbarrier.arrive.shared::cta.b64 %0, [%1];" : "=l"(tok) : "r"(bar) : "memory");
-        while (true) {
-          unsigned done;
-          asm volatile(
-              "{\n .reg .pred p;\n mbarrier.test_wait.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
-              : "=r"(done)
-              : "r"(bar), "l"(tok)
-              : "memory");
-          if (__all_sync(0xffffffffu, done != 0)) break;
-          if (tail - head >= 2) pop_eval2();
-        }
-      }
-#else
       __syncthreads();
-#endif
 #pragma unroll
       for (int kk = 0; kk < PC_PER; ++kk) {
         const int j = threadIdx.x + kk * PC_TG;
@@ -690,33 +646,6 @@ __global__ void __launch_bounds__(PC_TG, pc_minb<KIND>()) k_pair_q(const PairArg
         const unsigned q_s = (unsigned)__cvta_generic_to_shared(&q[0][lane]);  // this lane's slot 0
         const int qb = hb + j0;
         unsigned msh = 0;
-#if PC_SCAN4
-        // four near candidates per iteration: their four broadcast loads are issued together, so
-        // one shared-memory latency is paid per four tests (same test and push order as the
-        // two-candidate form, hence bit-identical queues)
-        while (near) {  // warp-uniform (lanes without a target test far-away coordinates)
-          int ix[4];
-          unsigned bx[4];
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const bool has = near != 0;
-            ix[k] = has ? bfind_u32(near) : ix[k > 0 ? k - 1 : 0];
-            bx[k] = has ? 1u << ix[k] : 0u;
-            near ^= bx[k];
-          }
-          float4 Fx[4];
-#pragma unroll
-          for (int k = 0; k < 4; ++k) Fx[k] = lds_f4(sFg_s + (ix[k] << 4));  // broadcast
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const float rk = dist2f(tfx, tfy, tfz, Fx[k]);
-            const bool ok = bx[k] != 0u && rk > 0.0f && rk <= a.rc2_lo;
-            msh |= (!ok && rk <= a.rc2_hi) ? bx[k] : 0u;
-            sts_u16(q_s + (((unsigned)tail & (PC_Q - 1)) << 6), qb + ix[k]);
-            tail += ok ? 1 : 0;
-          }
-        }
-#else
         while (near) {  // warp-uniform (lanes without a target test far-away coordinates)
           const int ia = bfind_u32(near);
           const unsigned ba = 1u << ia;
@@ -735,7 +664,6 @@ __global__ void __launch_bounds__(PC_TG, pc_minb<KIND>()) k_pair_q(const PairArg
           sts_u16(q_s + (((unsigned)tail & (PC_Q - 1)) << 6), qb + ib);
           tail += okb ? 1 : 0;
         }
-#endif
         if (__any_sync(0xffffffffu, msh != 0)) {
           while (msh) {
             const int ib = bfind_u32(msh);
@@ -758,21 +686,7 @@ __global__ void __launch_bounds__(PC_TG, pc_minb<KIND>()) k_pair_q(const PairArg
         if (mn == 0x7fffffffu) mn = 0;
         if (tvalid) {
           unsigned r = 0;
-#if PC_QPREFETCH
-          // the next round's queue entries are read while the current round evaluates (slots past
-          // `tail` hold stale but valid indices; they are re-read once pushed)
-          if (mn >= 2) {
-            int j1 = q[head & (PC_Q - 1)][lane], j2 = q[(head + 1) & (PC_Q - 1)][lane];
-            for (; r + 1 < mn; r += 2) {
-              const int n1 = q[(head + 2) & (PC_Q - 1)][lane], n2 = q[(head + 3) & (PC_Q - 1)][lane];
-              eval2(j1, j2);
-              j1 = n1;
-              j2 = n2;
-            }
-          }
-#else
           for (; r + 1 < mn; r += 2) pop_eval2();
-#endif
           // an odd leftover stays queued for the next two-pair round (PC_ODD_SINGLE=1: evaluate it now)
           if (PC_ODD_SINGLE && r < mn) pop_eval();
         }
