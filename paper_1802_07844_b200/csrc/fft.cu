@@ -1057,18 +1057,24 @@ hs_status launch_ystage(hs_ctx* ctx, bool fwd, const double2* in, double2* out, 
 __constant__ double2 c_w7[7];   // exp(-2 pi i m / 7)
 __constant__ double2 c_w21[21];  // exp(-2 pi i m / 21)
 __constant__ double2 c_w22[11];  // exp(-2 pi i m / 22)
+__constant__ double2 c_w24[24];  // exp(-2 pi i m / 24)
+__constant__ double2 c_w28[28];  // exp(-2 pi i m / 28)
 static bool g_z924_consts = false;
 static hs_status z924_constants() {
   HS_TRY(xreg_constants());  // c_w11
   if (g_z924_consts) return HS_OK;
   const long double tp = 6.283185307179586476925286766559005768L;
-  double2 w7[7], w21[21], w22[11];
+  double2 w7[7], w21[21], w22[11], w24[24], w28[28];
+  for (int m = 0; m < 24; ++m) w24[m] = make_double2((double)std::cos(tp * m / 24), (double)-std::sin(tp * m / 24));
+  for (int m = 0; m < 28; ++m) w28[m] = make_double2((double)std::cos(tp * m / 28), (double)-std::sin(tp * m / 28));
   for (int m = 0; m < 7; ++m) w7[m] = make_double2((double)std::cos(tp * m / 7), (double)-std::sin(tp * m / 7));
   for (int m = 0; m < 21; ++m) w21[m] = make_double2((double)std::cos(tp * m / 21), (double)-std::sin(tp * m / 21));
   for (int m = 0; m < 11; ++m) w22[m] = make_double2((double)std::cos(tp * m / 22), (double)-std::sin(tp * m / 22));
   HS_CUDA(cudaMemcpyToSymbol(c_w7, w7, sizeof(w7)));
   HS_CUDA(cudaMemcpyToSymbol(c_w21, w21, sizeof(w21)));
   HS_CUDA(cudaMemcpyToSymbol(c_w22, w22, sizeof(w22)));
+  HS_CUDA(cudaMemcpyToSymbol(c_w24, w24, sizeof(w24)));
+  HS_CUDA(cudaMemcpyToSymbol(c_w28, w28, sizeof(w28)));
   g_z924_consts = true;
   return HS_OK;
 }
@@ -1120,50 +1126,105 @@ __device__ __forceinline__ void dft21(double2* v) {
   }
 }
 
-// geometry of the 22 x M scheme (M = 21: pz = 924; M = 15: pz = 660, DFT15 in registers)
+// DFT-24 in place: j = j1 + 3 j2 (j2 < 8), k = 8 k1 + k2 (DFT8 over j2, twiddle W24^{j1 k2}, DFT3 over j1)
+__device__ __forceinline__ void dft24(double2* v) {
+  double2 Y[3][8];
+#pragma unroll
+  for (int j1 = 0; j1 < 3; ++j1) {
+    double2 t[8];
+#pragma unroll
+    for (int j2 = 0; j2 < 8; ++j2) t[j2] = v[j1 + 3 * j2];
+    dft<8>(t);
+#pragma unroll
+    for (int k2 = 0; k2 < 8; ++k2) Y[j1][k2] = (j1 * k2 == 0) ? t[k2] : cm(t[k2], c_w24[j1 * k2]);
+  }
+#pragma unroll
+  for (int k2 = 0; k2 < 8; ++k2) {
+    double2 t[3] = {Y[0][k2], Y[1][k2], Y[2][k2]};
+    dft<3>(t);
+#pragma unroll
+    for (int k1 = 0; k1 < 3; ++k1) v[8 * k1 + k2] = t[k1];
+  }
+}
+// DFT-28 in place: j = j1 + 4 j2 (j2 < 7), k = 7 k1 + k2 (DFT7 over j2, twiddle W28^{j1 k2}, DFT4 over j1)
+__device__ __forceinline__ void dft28(double2* v) {
+  double2 Y[4][7];
+#pragma unroll
+  for (int j1 = 0; j1 < 4; ++j1) {
+    double2 t[7];
+#pragma unroll
+    for (int j2 = 0; j2 < 7; ++j2) t[j2] = v[j1 + 4 * j2];
+    dft7(t);
+#pragma unroll
+    for (int k2 = 0; k2 < 7; ++k2) Y[j1][k2] = (j1 * k2 == 0) ? t[k2] : cm(t[k2], c_w28[j1 * k2]);
+  }
+#pragma unroll
+  for (int k2 = 0; k2 < 7; ++k2) {
+    double2 t[4] = {Y[0][k2], Y[1][k2], Y[2][k2], Y[3][k2]};
+    dft<4>(t);
+#pragma unroll
+    for (int k1 = 0; k1 < 4; ++k1) v[7 * k1 + k2] = t[k1];
+  }
+}
+
+// geometry of the L x M scheme: N2 = L M complex points per line (pz = 2 N2 real points);
+// L = 22 lanes for M = 21 (pz = 924, the metric configuration) and 15 (660: cfg2 / cfg3),
+// L = 30 lanes for M = 7 (420: cfg1), 24 (1440: cfg4) and 28 (1680: cfg5)
 template <int M>
 struct ZR {
-  static constexpr int L = 22, RS = 23, N2 = L * M, LS = M * RS;  // scratch LS >= N2
+  static constexpr int L = (M == 21 || M == 15) ? 22 : 30, H = L / 2, RS = L + 1;
+  static constexpr int N2 = L * M, LS = M * RS;                    // scratch LS >= N2
   static constexpr int NZH = N2 + 1, PZ = 2 * N2, KH = N2 / 2;    // KH: pairs (k, N2 - k), k <= KH
   static constexpr int NQ = (KH + 32) / 32;                        // lane rounds over k <= KH
 };
 template <int M>
 __device__ __forceinline__ void dftZ(double2* v) {
-  static_assert(M == 21 || M == 15, "register z stage: pz = 924 (M = 21) or 660 (M = 15)");
+  static_assert(M == 21 || M == 15 || M == 7 || M == 24 || M == 28, "register z stage: M in {21, 15, 7, 24, 28}");
   if constexpr (M == 21) dft21(v);
-  else dft15(v);
+  else if constexpr (M == 15) dft15(v);
+  else if constexpr (M == 7) dft7(v);
+  else if constexpr (M == 24) dft24(v);
+  else dft28(v);
 }
-// forward DFT of the 22 M-point line with z[l + 22 j] in v[j] (lanes < 22); result Z[k] left in S[k].
-// NK2: number of DFT22 outputs per row needed (22: all; 11: only Z[k], k < 11 M)
-template <int M, int NK2>
-__device__ __forceinline__ void warp_fft22(double2* v, double2* S, const double2* tw, int lane) {
-  if (lane < ZR<M>::L) {
+// forward DFT of the L M-point line with z[l + L j] in v[j] (lanes < L); result Z[k] left in S[k].
+// ALL: every output (false: only Z[k], k < N2 / 2, i.e. the first half of each row's DFT-L)
+template <int M, bool ALL>
+__device__ __forceinline__ void warp_fftz(double2* v, double2* S, const double2* tw, int lane) {
+  constexpr int L = ZR<M>::L, H = ZR<M>::H, RS = ZR<M>::RS;
+  if (lane < L) {
     dftZ<M>(v);
 #pragma unroll
     for (int k1 = 1; k1 < M; ++k1) v[k1] = cm(v[k1], tw[pd8(lane * k1)]);
   }
   __syncwarp();
-  if (lane < ZR<M>::L) {
+  if (lane < L) {
 #pragma unroll
-    for (int k1 = 0; k1 < M; ++k1) S[k1 * ZR<M>::RS + lane] = v[k1];
+    for (int k1 = 0; k1 < M; ++k1) S[k1 * RS + lane] = v[k1];
   }
   __syncwarp();
-  double2 e[11], o[11];
+  // DFT-L of row r = lane as 2 x DFT-(L/2) (even / odd l)
+  double2 e[H], o[H];
   const int rr = lane < M ? lane : M - 1;
 #pragma unroll
-  for (int m = 0; m < 11; ++m) {
-    e[m] = S[rr * ZR<M>::RS + 2 * m];
-    o[m] = S[rr * ZR<M>::RS + 2 * m + 1];
+  for (int m = 0; m < H; ++m) {
+    e[m] = S[rr * RS + 2 * m];
+    o[m] = S[rr * RS + 2 * m + 1];
   }
   __syncwarp();
-  dft11(e);
-  dft11(o);
+  if constexpr (H == 11) {
+    dft11(e);
+    dft11(o);
+  } else {
+    dft15(e);
+    dft15(o);
+  }
   if (lane < M) {
 #pragma unroll
-    for (int k = 0; k < 11; ++k) {
-      const double2 t = k == 0 ? o[0] : cm(o[k], c_w22[k]);
+    for (int k = 0; k < H; ++k) {
+      const double2 w = H == 11 ? c_w22[k] : c_w30[k];
+      const double2 t = k == 0 ? o[0] : cm(o[k], w);
       S[lane + M * k] = ad(e[k], t);
-      if (NK2 > 11) S[lane + M * (k + 11)] = sb(e[k], t);
+      if (ALL) S[lane + M * (k + H)] = sb(e[k], t);
     }
   }
   __syncwarp();
@@ -1228,7 +1289,7 @@ __global__ void __launch_bounds__(ZF_WARPS * 32, 1)
     }
     __syncwarp();
     prefetch(line + lstep);
-    warp_fft22<M, 22>(v, S, tw, lane);
+    warp_fftz<M, true>(v, S, tw, lane);
     // X[k] = E + W_pz^k O, X[N2 - k] = conj(E - W_pz^k O); E = (Z[k] + conj Z[N2-k]) / 2,
     // O = (Z[k] - conj Z[N2-k]) / (2 i)
     double2* dst = out + line * Z9_NZH;
@@ -1298,7 +1359,7 @@ __global__ void __launch_bounds__(NOUT * LPC * 32, 1)
 #pragma unroll
       for (int j = 0; j < Z9_M; ++j) v[j] = lane < Z9_L ? S[lane + Z9_L * j] : make_double2(0.0, 0.0);
       __syncwarp();
-      warp_fft22<M, 11>(v, S, tw, lane);  // z[n] = conj(S[n]), n < 11 M >= nc
+      warp_fftz<M, false>(v, S, tw, lane);  // z[n] = conj(S[n]), n < N2 / 2 >= nc
       double* ob = obuf + (size_t)lc * nz * PITCH + c;
 #pragma unroll
       for (int q = 0; q < ZR<M>::NQ; ++q) {
@@ -1324,7 +1385,16 @@ __global__ void __launch_bounds__(NOUT * LPC * 32, 1)
 }
 
 // (pz, nz) the register z stage handles: nz even, at most half the padded length
-static int zstage_m(int pz) { return pz == ZR<21>::PZ ? 21 : (pz == ZR<15>::PZ ? 15 : 0); }
+static int zstage_m(int pz) {
+  switch (pz) {
+    case ZR<21>::PZ: return 21;
+    case ZR<15>::PZ: return 15;
+    case ZR<7>::PZ: return 7;
+    case ZR<24>::PZ: return 24;
+    case ZR<28>::PZ: return 28;
+    default: return 0;
+  }
+}
 bool zstage_supported(int pz, int nz) { return zstage_m(pz) != 0 && nz <= pz / 2 && nz % 2 == 0; }
 // twiddle table of the z stage: W_{N2}^i (N2 = pz / 2 entries) then W_{pz}^k (k <= N2 / 2)
 int zstage_twiddle_count(int pz) { return pz / 2 + pz / 4 + 1; }
@@ -1361,8 +1431,13 @@ hs_status launch_zfwd(hs_ctx* ctx, int pz, const double* in, double2* out, const
   if (!zstage_supported(pz, nz)) return fail(HS_ERR_PARAMETER, "z stage: unsupported length");
   if (mirror && (nz & 1)) return fail(HS_ERR_PARAMETER, "z stage: fused mirror needs an even nz");
   HS_TRY(z924_constants());
-  return zstage_m(pz) == 21 ? launch_zfwd_t<21>(ctx, in, out, tw, nlines, nz, mirror, msign, zero_below)
-                            : launch_zfwd_t<15>(ctx, in, out, tw, nlines, nz, mirror, msign, zero_below);
+  switch (zstage_m(pz)) {
+    case 21: return launch_zfwd_t<21>(ctx, in, out, tw, nlines, nz, mirror, msign, zero_below);
+    case 15: return launch_zfwd_t<15>(ctx, in, out, tw, nlines, nz, mirror, msign, zero_below);
+    case 7: return launch_zfwd_t<7>(ctx, in, out, tw, nlines, nz, mirror, msign, zero_below);
+    case 24: return launch_zfwd_t<24>(ctx, in, out, tw, nlines, nz, mirror, msign, zero_below);
+    default: return launch_zfwd_t<28>(ctx, in, out, tw, nlines, nz, mirror, msign, zero_below);
+  }
 }
 // inverse z of all n_out channels (channel stride ch_stride in `spec`), outputs z < nz interleaved
 // into gout ([line][pz][pitch] storage, z < nz written)
@@ -1381,17 +1456,25 @@ static hs_status launch_zinv_t(hs_ctx* ctx, const double2* spec, int64_t ch_stri
     HS_LAUNCHED(ctx);
     return HS_OK;
   };
-  if (n_out == 6 && pitch == 6) return go(k_zinv<M, 6, 6, 2>, 12, 2);
-  if (n_out == 3 && pitch == 4) return go(k_zinv<M, 3, 4, 4>, 12, 4);
-  if (n_out == 1 && pitch == 1) return go(k_zinv<M, 1, 1, 12>, 12, 12);  // one channel, not interleaved
+  // 12 warps per CTA; 6 for the long lines (M >= 24: 28 complex registers per lane need the
+  // 255-register budget of a 192-thread CTA)
+  constexpr int NW = M >= 24 ? 6 : 12;
+  if (n_out == 6 && pitch == 6) return go(k_zinv<M, 6, 6, NW / 6>, NW, NW / 6);
+  if (n_out == 3 && pitch == 4) return go(k_zinv<M, 3, 4, NW / 3>, NW, NW / 3);
+  if (n_out == 1 && pitch == 1) return go(k_zinv<M, 1, 1, NW>, NW, NW);  // one channel, not interleaved
   return fail(HS_ERR_PARAMETER, "z stage: unsupported channel layout");
 }
 hs_status launch_zinv_interleaved(hs_ctx* ctx, int pz, const double2* spec, int64_t ch_stride, int n_out, int pitch,
                                   double* gout, const double2* tw, int64_t nlines, int nz) {
   if (!zstage_supported(pz, nz)) return fail(HS_ERR_PARAMETER, "z stage: unsupported length");
   HS_TRY(z924_constants());
-  return zstage_m(pz) == 21 ? launch_zinv_t<21>(ctx, spec, ch_stride, n_out, pitch, gout, tw, nlines, nz)
-                            : launch_zinv_t<15>(ctx, spec, ch_stride, n_out, pitch, gout, tw, nlines, nz);
+  switch (zstage_m(pz)) {
+    case 21: return launch_zinv_t<21>(ctx, spec, ch_stride, n_out, pitch, gout, tw, nlines, nz);
+    case 15: return launch_zinv_t<15>(ctx, spec, ch_stride, n_out, pitch, gout, tw, nlines, nz);
+    case 7: return launch_zinv_t<7>(ctx, spec, ch_stride, n_out, pitch, gout, tw, nlines, nz);
+    case 24: return launch_zinv_t<24>(ctx, spec, ch_stride, n_out, pitch, gout, tw, nlines, nz);
+    default: return launch_zinv_t<28>(ctx, spec, ch_stride, n_out, pitch, gout, tw, nlines, nz);
+  }
 }
 
 template <int KIND, bool HALF, int KB, class FFT>

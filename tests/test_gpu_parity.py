@@ -385,10 +385,9 @@ def test_register_fft_stages_match_alternatives(tmp_path, kind, M, alt):
     """The register-FFT x stage and y stage (N = 480 = 15 x 32 at M=192, 352 = 11 x 32 at
     M=128, 864 = 27 x 32 at M=384, 750 = 30 x 25 at M=320) against the shared-memory Stockham x stage / the cuFFT y stage on the same input
     (each selected in its own process); the register z stage (924 = 2 x 22 x 21 real points at
-    M=192, 660 = 2 x 22 x 15 at M=128, with the fused reflection and channel interleave) against
-    the cuFFT D2Z / Z2D with the mirror and interleave passes."""
-    if alt == "HS_ZSTAGE_CUFFT" and M not in (192, 128):
-        pytest.skip("the register z stage exists for pz = 924 (M = 192) and 660 (M = 128)")
+    M=192, 660 = 2 x 22 x 15 at M=128, 1440 = 2 x 30 x 24 at M=320, 1680 = 2 x 30 x 28 at M=384, with
+    the fused reflection and channel interleave) against the cuFFT D2Z / Z2D with the mirror and
+    interleave passes."""
     import os
     import subprocess
     import sys
