@@ -34,9 +34,6 @@ struct KeyGeom {
   int64_t dims[3];
 };
 
-#ifndef HS_SUB_OCTANT
-#define HS_SUB_OCTANT 0
-#endif
 __global__ void k_cell_keys(const double* __restrict__ pos, int n_src, int n_total, int mirror, KeyGeom g,
                             int check_bounds, int* __restrict__ keys, unsigned* __restrict__ flags, int sub) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_total; i += gridDim.x * blockDim.x) {
@@ -44,7 +41,7 @@ __global__ void k_cell_keys(const double* __restrict__ pos, int n_src, int n_tot
     double p[3] = {pos[3 * s], pos[3 * s + 1], pos[3 * s + 2]};
     if (mirror && i >= n_src) p[2] = -p[2];  // y * MIRROR (system.py:168-169)
     int64_t c[3];
-    double vz = 0.0, vx = 0.0, vy = 0.0;
+    double vz = 0.0;
     bool bad = false;
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
@@ -55,21 +52,11 @@ __global__ void k_cell_keys(const double* __restrict__ pos, int n_src, int n_tot
       ci = ci > g.dims[k] - 1 ? g.dims[k] - 1 : ci;
       c[k] = ci;
       if (k == 2) vz = v;
-      if (k == 0) vx = v;
-      if (k == 1) vy = v;
     }
     if (check_bounds && bad) atomicOr(flags, FLAG_GEOMETRY);
     const int flat = (int)((c[0] * g.dims[1] + c[1]) * g.dims[2] + c[2]);
     if (sub > 1) {
-#if HS_SUB_OCTANT
-      // sub == 8: the cell's octants (x half, y half, z half), so that consecutive targets form
-      // compact blobs (a warp's bounding box then admits fewer candidates than a z sub-slab)
-      int sl = (((vx - (double)c[0]) >= 0.5 ? 4 : 0) | ((vy - (double)c[1]) >= 0.5 ? 2 : 0) |
-                ((vz - (double)c[2]) >= 0.5 ? 1 : 0));
-      if (sub != 8) sl = (int)((vz - (double)c[2]) * sub);
-#else
       int sl = (int)((vz - (double)c[2]) * sub);
-#endif
       sl = sl < 0 ? 0 : (sl > sub - 1 ? sub - 1 : sl);
       keys[i] = flat * sub + sl;
     } else {
