@@ -113,6 +113,7 @@ struct PairArgs {
   double* uc;         // optional (nt,3) correction part
   unsigned* flags;
   unsigned long long* counts;  // [accepted pairs, accepted image pairs] (optional)
+  int* work;          // zeroed work-item counter: CTAs take items dynamically (null: static round robin)
   // neighbour audit (hs_plan_pair_audit; null in production launches): per original target
   // [accepted pairs, accepted image pairs, sum of splitmix64(combined source id) mod 2^64]
   unsigned long long* audit;

@@ -411,7 +411,19 @@ __global__ void __launch_bounds__(PC_TG, pc_minb<KIND>()) k_pair_q(const PairArg
   unsigned short(*q)[32] = sq[warp];
 
   const int n_items = *a.n_items_d;
-  for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+  // work items are taken from a global counter (a.work), so a CTA that drew cheap items (cells
+  // near the wall or the box faces) simply takes more: no tail of idle SMs behind the slowest
+  // static share.  Which CTA evaluates an item does not affect any result.
+  __shared__ int s_item;
+  for (int it0 = blockIdx.x;; it0 += gridDim.x) {
+    int it = it0;
+    if (a.work) {
+      __syncthreads();
+      if (threadIdx.x == 0) s_item = atomicAdd(a.work, 1);
+      __syncthreads();
+      it = s_item;
+    }
+    if (it >= n_items) break;
     const int2 item = a.items[it];
     const int col = item.x, t0 = item.y;
     const int t1 = min(t0 + PC_TG, a.t_start[(col + 1) * nz * a.t_sub]);

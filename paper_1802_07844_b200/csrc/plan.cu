@@ -638,7 +638,7 @@ static hs_status plan_create_impl(hs_ctx* ctx, const hs_params* prm, const hs_sl
   A_(3 * (size_t)std::max(nt, 1), p->u_real, true);
   A_(3 * (size_t)std::max(nt, 1), p->u_four, true);
   A_(3 * (size_t)std::max(nt, 1), p->uk, true);
-  A_(2, p->pair_counts, true);
+  A_(3, p->pair_counts, true);  // [pairs, image pairs, work-item counter]
   A_(3 * (size_t)std::max(nt, 1), p->uc, true);
 #undef A_
   // ---- cuFFT plans (batched over channels, shared work area)
@@ -1193,8 +1193,9 @@ hs_status stage_real(hs_plan* p, bool want) {
       a.uc = p->uc;
       a.flags = ctx->d_flags;
       a.counts = p->pair_counts;
+      a.work = reinterpret_cast<int*>(p->pair_counts + 2);
       a.audit = p->audit;
-      HS_CUDA(cudaMemsetAsync(p->pair_counts, 0, 2 * sizeof(unsigned long long), st));
+      HS_CUDA(cudaMemsetAsync(p->pair_counts, 0, 3 * sizeof(unsigned long long), st));
       HS_CUDA(cudaEventRecord(p->ev[9], st));
       HS_TRY(launch_pair(ctx, a));
       HS_CUDA(cudaEventRecord(p->ev[10], st));
