@@ -759,7 +759,8 @@ __global__ void k_g7_fill(const double4* __restrict__ pts, const int* __restrict
 template <int NCH, int PITCH>
 __global__ void __launch_bounds__(G7_WARPS * 32) k_gather8(const double4* __restrict__ pts,
                                                           const int* __restrict__ orig, const int4* __restrict__ items,
-                                                          const int* __restrict__ n_items_d, GridGeom g,
+                                                          const int* __restrict__ n_items_d, int* __restrict__ work,
+                                                          GridGeom g,
                                                           const double* __restrict__ T,
                                                           double* __restrict__ u_four, double* __restrict__ u_tot,
                                                           const double* __restrict__ u_real,
@@ -777,7 +778,14 @@ __global__ void __launch_bounds__(G7_WARPS * 32) k_gather8(const double4* __rest
   double(*wx_tab)[GW] = s_w[warp][0];
   double(*wy_tab)[GW] = s_w[warp][1];
   const int n_items = *n_items_d;
-  for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+  // items are drawn from a global counter (no static share per CTA: no tail behind the slowest one)
+  __shared__ int s_item;
+  for (;;) {
+    __syncthreads();
+    if (threadIdx.x == 0) s_item = atomicAdd(work, 1);
+    __syncthreads();
+    const int it = s_item;
+    if (it >= n_items) break;
     const int4 item = items[it];
     int rb = item.x;
 #pragma unroll
@@ -996,12 +1004,14 @@ hs_status launch_gather_fourier(hs_ctx* ctx, const double4* pts, const int* orig
   // items (worst case one per target): count per 4x4 block, scan, fill
   const int nb4 = ((g.dims[0] + 3) / 4) * ((g.dims[1] + 3) / 4);
   void* scr = nullptr;
-  const size_t bytes = sizeof(int4) * (size_t)n + sizeof(int) * (3 * (size_t)nb4 + 8);
+  const size_t bytes = sizeof(int4) * (size_t)n + sizeof(int) * (3 * (size_t)nb4 + 8 + 4);
   HS_TRY(ctx_scratch(ctx, bytes, &scr));
   int4* items = (int4*)scr;
   int* cnt = (int*)(items + n);
   int* istart = cnt + nb4;  // nb4 + 1
   int* sc = istart + nb4 + 1;
+  int* work = cnt + 3 * (size_t)nb4 + 8;  // work-item counter of the gather kernel
+  HS_CUDA(cudaMemsetAsync(work, 0, sizeof(int), ctx->stream));
   const int gsb = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(nb4, 4), ctx->sm_count * 16));  // warp per block
   k_g7_count<<<gsb, 128, 0, ctx->stream>>>(pts, bstart, nb4, g.dims[2], g, cnt);
   HS_LAUNCHED(ctx);
@@ -1013,10 +1023,10 @@ hs_status launch_gather_fourier(hs_ctx* ctx, const double4* pts, const int* orig
                                                         G7_WARPS * 32, 0));
   const int gs8 = (int)std::min<int64_t>(n, (int64_t)ctx->sm_count * std::max(per_sm, 1));
   if (half)
-    k_gather8<6, 6><<<gs8, G7_WARPS * 32, 0, ctx->stream>>>(pts, orig, items, istart + nb4, g, T, u_fourier,
+    k_gather8<6, 6><<<gs8, G7_WARPS * 32, 0, ctx->stream>>>(pts, orig, items, istart + nb4, work, g, T, u_fourier,
                                                            u_total, u_real, ctx->d_flags);
   else
-    k_gather8<3, 4><<<gs8, G7_WARPS * 32, 0, ctx->stream>>>(pts, orig, items, istart + nb4, g, T, u_fourier,
+    k_gather8<3, 4><<<gs8, G7_WARPS * 32, 0, ctx->stream>>>(pts, orig, items, istart + nb4, work, g, T, u_fourier,
                                                            u_total, u_real, ctx->d_flags);
   HS_LAUNCHED(ctx);
   return HS_OK;
