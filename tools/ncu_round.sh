@@ -3,7 +3,7 @@
 # Usage: bash tools/ncu_round.sh TAG [kernel names...]
 set -x
 out=gpurun_out/${1:-ncu}; shift
-ks=${@:-"k_pair_q k_spread_mma4 k_gather8 k_xreg k_zfwd924 k_zinv924 k_ystage"}
+ks=${@:-"k_pair_q k_spread_mma4 k_gather8 k_xreg k_zfwd k_zinv k_ystage"}
 mkdir -p $out
 python bench.py --steps 5 --warmup 3 --no-cpu-baseline > $out/bench.json 2> $out/bench.err
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $out/launches.csv \
