@@ -384,7 +384,10 @@ struct hs_plan {
 
 namespace {
 
-constexpr int kTargetSub = 8;  // z sub-slabs per cell in the pair-kernel target order
+#ifndef HS_TARGET_SUB
+#define HS_TARGET_SUB 32
+#endif
+constexpr int kTargetSub = HS_TARGET_SUB;  // z sub-slabs per cell in the pair-kernel target order
 
 template <typename T>
 hs_status palloc(hs_plan* p, size_t count, T** out, bool zero = false) {
