@@ -354,6 +354,8 @@ constexpr int pc_rec_bytes() {
 #define PC_ODD_SINGLE 0
 #endif
 constexpr int PC_Q = PC_Q_DEF;        // per-lane queue capacity (power of two)
+static_assert(PC_Q >= 64 && (PC_Q & (PC_Q - 1)) == 0,
+              "a group of 32 candidates must fit behind a backlog: the overflow guard drains to PC_Q - 32");
 #ifndef PC_MINB
 #define PC_MINB 4                     // resident CTAs per SM (register budget 128)
 #endif
